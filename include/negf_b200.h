@@ -1,0 +1,71 @@
+/* negf_b200 -- C ABI of the B200-native NEGF+GW hot path (sm_100a).
+ *
+ * Plain pointers and sizes only. Every matrix argument is a DEVICE pointer to
+ * complex128 data stored interleaved (re, im), row-major, energy-major packed:
+ *   diagonal blocks   [n_e][n_b][bs][bs]
+ *   off-diagonal      [n_e][n_b-1][bs][bs]
+ * which is the memory layout of a contiguous torch.complex128 tensor of that
+ * shape. `stream` is a cudaStream_t (NULL = legacy default stream). All calls
+ * are stream-ordered and asynchronous; they return 0 on success, a CUDA error
+ * code (>0) on launch failure, or a negative code on invalid arguments.
+ * Caller owns all buffers, including the workspace (query its size first).
+ * No global mutable state beyond per-kernel attribute setup: calls are
+ * reentrant across threads and streams.
+ */
+#ifndef NEGF_B200_H
+#define NEGF_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ABI version (major*100 + minor). */
+int negf_abi_version(void);
+
+/* ---- (1) selected solve -------------------------------------------------
+ * Replaces negfgw.rgf.selected_solve (pkg/src/negfgw/rgf.py:232-243) and, with
+ * symmetrize=1, the SelectedSolution.symmetrize() that scba_run applies
+ * after it (scba.py:987,1087; rgf.py:82-88), for a batch of n_e energies:
+ *   M X^R = I,  M X^lg M^dag = B^lg  (selected blocks).
+ * b_lesser / b_greater are lg-compressed (diag + upper; lower implied by
+ * B[i+1][i] = -B[i][i+1]^dag, blocks.py:110-118); pass NULL for an absent
+ * kind (its outputs are then not touched).
+ * status[n_e] (device int): 0, or 1 + forward step of the first singular
+ * Schur complement (rgf.py:121-126 SingularBlockError). u_spread[n_e][n_b]
+ * (device double, may be NULL): LU pivot spread per step (rgf.py:44-49).  */
+size_t negf_rgf_workspace_bytes(int n_e, int n_b, int bs);
+int negf_rgf_selected_solve_batched(
+    int n_e, int n_b, int bs,
+    const void* m_diag, const void* m_upper, const void* m_lower,
+    const void* bl_diag, const void* bl_upper,
+    const void* bg_diag, const void* bg_upper,
+    void* xr_diag, void* xr_upper, void* xr_lower,
+    void* xl_diag, void* xl_upper,
+    void* xg_diag, void* xg_upper,
+    int symmetrize, int* status, double* u_spread,
+    void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- dense block primitives (negfgw/_linalg.py:19-64) --------------------
+ * D[b] = alpha*op(A[b])op(B[b]) + beta*C[b]; op: 0=N 1=T 2=conj 3=conj-trans.
+ * Replaces _linalg.gemm (_linalg.py:19-22), batched. C may be NULL. */
+int negf_zgemm_batched(int m, int n, int k, int batch,
+                       double alpha_re, double alpha_im,
+                       const void* a, long long stride_a, int lda, int op_a,
+                       const void* b, long long stride_b, int ldb, int op_b,
+                       double beta_re, double beta_im,
+                       const void* c, long long stride_c, int ldc,
+                       void* d, long long stride_d, int ldd, void* stream);
+
+/* Batched pivoted inverse, replaces _linalg.invert (_linalg.py:30-52).
+ * s (n x n packed, stride n*n) is destroyed for n > 64. status[b] = 1 on an
+ * exactly-zero or non-finite pivot. */
+size_t negf_zinv_workspace_bytes(int n, int batch);
+int negf_zinv_batched(int n, int batch, void* s, void* x, int* status, double* u_spread,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NEGF_B200_H */

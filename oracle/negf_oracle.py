@@ -1,0 +1,219 @@
+"""CPU ORACLE -- test infrastructure only. NOT the product path.
+
+A numpy restatement of the reference algorithms on the NEGF+GW hot path
+(arxiv 2508.19138 restatement package ``negfgw``, mounted read-only at
+/root/reference/pkg/src/negfgw). Each function cites the reference lines it
+restates. Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+CPU-baseline leg may import this module, and only as the checker / the timed
+CPU baseline -- the GPU product path never routes through it.
+
+Parity pin: every function here is checked against golden vectors produced
+by running the reference itself (tests/golden/make_golden.py, committed
+fixtures tests/golden/*.npz) in tests/test_oracle_golden.py.
+
+Layout: batched over energies. Diagonal blocks (n_e, n_b, bs, bs), off-diagonal
+blocks (n_e, n_b-1, bs, bs), complex128. lg-compressed sources keep the
+diagonal and upper blocks; B[i+1, i] = -B[i, i+1]^dag (blocks.py:110-118).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import scipy.linalg as sla
+from scipy.fft import fft, ifft, next_fast_len
+from scipy.special import expit
+
+
+def _h(x: np.ndarray) -> np.ndarray:
+    """Conjugate transpose of the trailing two axes."""
+    return np.conj(np.swapaxes(x, -1, -2))
+
+
+class OracleSingular(Exception):
+    pass
+
+
+def lu_inverse(a: np.ndarray) -> tuple[np.ndarray, float]:
+    """_linalg.invert (_linalg.py:30-52): scipy LU + solve against I; raise on
+    an exact-zero / non-finite pivot; return the pivot spread."""
+    lu, piv = sla.lu_factor(a, check_finite=False)
+    d = np.abs(np.diag(lu))
+    if d.min() == 0.0 or not np.isfinite(d).all():
+        raise OracleSingular("singular pivot")
+    inv = sla.lu_solve((lu, piv), np.eye(a.shape[0], dtype=complex), check_finite=False)
+    return inv, float(d.max() / d.min())
+
+
+def _inv_batch(s: np.ndarray, step: int) -> np.ndarray:
+    out = np.empty_like(s)
+    for e in range(s.shape[0]):
+        try:
+            out[e], _ = lu_inverse(s[e])
+        except (OracleSingular, ValueError, np.linalg.LinAlgError) as exc:
+            raise OracleSingular(f"singular Schur complement at forward step {step}") from exc
+    return out
+
+
+# -- RGF selected solve ------------------------------------------------------
+
+
+def rgf_selected(m_diag, m_up, m_lo, b_lg: dict | None = None, symmetrize: bool = False) -> dict:
+    """Selected blocks of X^R = M^-1 and X^lg = M^-1 B^lg M^-dag.
+
+    Restates rgf.py:113-129 (forward_retarded), rgf.py:132-149 (forward_lg),
+    rgf.py:152-183 (rgf_retarded backward), rgf.py:186-229
+    (rgf_lesser_greater backward) and rgf.py:82-88 (symmetrize), vectorised
+    over the energy axis. ``b_lg`` maps kind ('<', '>') to (diag, upper).
+    """
+    b_lg = b_lg or {}
+    n = m_diag.shape[1]
+    # forward retarded: x_i = (M_ii - M_{i,i-1} x_{i-1} M_{i-1,i})^-1
+    xf = [None] * n
+    for i in range(n):
+        s = m_diag[:, i]
+        if i > 0:
+            s = s - (m_lo[:, i - 1] @ xf[i - 1]) @ m_up[:, i - 1]
+        xf[i] = _inv_batch(s, i)
+    out = {}
+    # backward retarded
+    xr_d = [None] * n
+    xr_u = [None] * (n - 1)
+    xr_l = [None] * (n - 1)
+    xr_d[n - 1] = xf[n - 1]
+    for i in range(n - 2, -1, -1):
+        t = xf[i] @ m_up[:, i]
+        u = t @ xr_d[i + 1]
+        mx = m_lo[:, i] @ xf[i]
+        xr_d[i] = xf[i] + u @ mx
+        xr_u[i] = -u
+        xr_l[i] = -(xr_d[i + 1] @ mx)
+    out["xr_diag"] = np.stack(xr_d, 1)
+    out["xr_upper"] = np.stack(xr_u, 1) if n > 1 else np.zeros_like(m_up)
+    out["xr_lower"] = np.stack(xr_l, 1) if n > 1 else np.zeros_like(m_up)
+    for kind, (bd, bu) in b_lg.items():
+        # forward lesser/greater
+        xl = [None] * n
+        for i in range(n):
+            b = bd[:, i]
+            if i > 0:
+                a = m_lo[:, i - 1]
+                y = (a @ xf[i - 1]) @ bu[:, i - 1]
+                b = b + (a @ xl[i - 1]) @ _h(a) - (y - _h(y))
+            xl[i] = (xf[i] @ b) @ _h(xf[i])
+        d = [None] * n
+        up = [None] * (n - 1)
+        d[n - 1] = xl[n - 1]
+        for i in range(n - 2, -1, -1):
+            x = xf[i]
+            t = x @ m_up[:, i]
+            u = t @ xr_d[i + 1]
+            y = (x @ bu[:, i]) @ _h(u)
+            mxl = m_lo[:, i] @ xl[i]
+            z = u @ mxl
+            d[i] = xl[i] + (t @ d[i + 1]) @ _h(t) - (y - _h(y)) + (z - _h(z))
+            b_dn = -_h(bu[:, i])  # B[i+1, i] of the lg-compressed source
+            lower = (xr_d[i + 1] @ b_dn) @ _h(x) - xr_d[i + 1] @ mxl - d[i + 1] @ _h(t)
+            up[i] = -_h(lower)
+        dd = np.stack(d, 1)
+        if symmetrize:
+            dd = 0.5 * (dd - _h(dd))
+        out[f"x{kind}_diag"] = dd
+        out[f"x{kind}_upper"] = np.stack(up, 1) if n > 1 else np.zeros_like(bu)
+    return out
+
+
+def to_dense(diag, up, lo) -> np.ndarray:
+    """Block-tridiagonal (single energy) to a dense matrix."""
+    n, bs = diag.shape[0], diag.shape[1]
+    a = np.zeros((n * bs, n * bs), dtype=complex)
+    for i in range(n):
+        a[i * bs:(i + 1) * bs, i * bs:(i + 1) * bs] = diag[i]
+        if i + 1 < n:
+            a[i * bs:(i + 1) * bs, (i + 1) * bs:(i + 2) * bs] = up[i]
+            a[(i + 1) * bs:(i + 2) * bs, i * bs:(i + 1) * bs] = lo[i]
+    return a
+
+
+def dense_selected(m_diag, m_up, m_lo, b_lg: dict | None = None) -> dict:
+    """rgf.py:246-267 dense_selected_oracle: full inverse + triple product."""
+    b_lg = b_lg or {}
+    ne, n, bs = m_diag.shape[:3]
+    out = {k: [] for k in ("xr_diag", "xr_upper", "xr_lower")}
+    for kind in b_lg:
+        out[f"x{kind}_diag"] = []
+        out[f"x{kind}_upper"] = []
+    cut = lambda d, i, j: d[i * bs:(i + 1) * bs, j * bs:(j + 1) * bs]
+    for e in range(ne):
+        g = np.linalg.inv(to_dense(m_diag[e], m_up[e], m_lo[e]))
+        out["xr_diag"].append([cut(g, i, i) for i in range(n)])
+        out["xr_upper"].append([cut(g, i, i + 1) for i in range(n - 1)])
+        out["xr_lower"].append([cut(g, i + 1, i) for i in range(n - 1)])
+        for kind, (bd, bu) in b_lg.items():
+            bf = to_dense(bd[e], bu[e], -_h(bu[e]))
+            f = g @ bf @ g.conj().T
+            out[f"x{kind}_diag"].append([cut(f, i, i) for i in range(n)])
+            out[f"x{kind}_upper"].append([cut(f, i, i + 1) for i in range(n - 1)])
+    return {k: np.asarray(v).reshape((ne, -1, bs, bs)) for k, v in out.items()}
+
+
+# -- seeded inputs (toys.py) -------------------------------------------------
+
+
+def random_bt_system(seed: int, n_blocks: int | None = None, block_size: int | None = None,
+                     max_blocks: int = 10, max_block_size: int = 8):
+    """toys.py:33-65: same RNG draw order, returned as stacked arrays
+    (m_diag, m_up, m_lo, {'<': (d, u), '>': (d, u)}) with a leading n_e=1 axis."""
+    rng = np.random.default_rng(seed)
+    n = int(n_blocks or rng.integers(2, max_blocks + 1))
+    bs = int(block_size or rng.integers(1, max_block_size + 1))
+    rb = lambda: rng.standard_normal((bs, bs)) + 1j * rng.standard_normal((bs, bs))
+    md = np.zeros((n, bs, bs), complex)
+    mu = np.zeros((n - 1, bs, bs), complex)
+    ml = np.zeros((n - 1, bs, bs), complex)
+    for i in range(n):
+        md[i] = rb() + (4.0 + 1.0j) * np.eye(bs)
+        if i + 1 < n:
+            mu[i] = 0.5 * rb()
+            ml[i] = 0.5 * rb()
+    src = []
+    for _ in range(2):
+        bd = np.zeros((n, bs, bs), complex)
+        bu = np.zeros((n - 1, bs, bs), complex)
+        for i in range(n):
+            d = rb()
+            bd[i] = 0.5 * (d - d.conj().T)
+            if i + 1 < n:
+                bu[i] = rb()
+        src.append((bd[None], bu[None]))
+    return md[None], mu[None], ml[None], {"<": src[0], ">": src[1]}
+
+
+def chain_device(n_blocks: int, block_size: int, t: float = 0.4, onsite_seed: int = 7,
+                 onsite_scale: float = 0.15):
+    """toys.py:89-108: (h_diag, h_upper, h_lower) of the homogeneous chain."""
+    rng = np.random.default_rng(onsite_seed)
+    a = rng.standard_normal((block_size,) * 2) + 1j * rng.standard_normal((block_size,) * 2)
+    onsite = onsite_scale * 0.5 * (a + a.conj().T)
+    c = t * np.eye(block_size, dtype=complex) + 0.05 * (
+        rng.standard_normal((block_size,) * 2) + 1j * rng.standard_normal((block_size,) * 2))
+    hd = np.broadcast_to(onsite, (n_blocks, block_size, block_size)).copy()
+    hu = np.broadcast_to(c, (n_blocks - 1, block_size, block_size)).copy()
+    hl = np.broadcast_to(c.conj().T, (n_blocks - 1, block_size, block_size)).copy()
+    return hd, hu, hl
+
+
+def coulomb_matrix(n_blocks: int, block_size: int, v0: float = 1e-3, seed: int = 11):
+    """toys.py:111-132: real symmetric replicated interaction (diag, up, lo)."""
+    rng = np.random.default_rng(seed)
+    d = rng.standard_normal((block_size, block_size))
+    diag = v0 * (np.eye(block_size) + 0.1 * (d + d.T))
+    off = v0 * 0.3 * rng.standard_normal((block_size, block_size))
+    vd = np.broadcast_to(diag.astype(complex), (n_blocks, block_size, block_size)).copy()
+    vu = np.broadcast_to(off.astype(complex), (n_blocks - 1, block_size, block_size)).copy()
+    vl = np.broadcast_to(off.T.astype(complex), (n_blocks - 1, block_size, block_size)).copy()
+    return vd, vu, vl
+
+
+def fermi(e, mu, kT):
+    """device.py:32-36."""
+    return expit(-(np.asarray(e, dtype=float) - mu) / kT)

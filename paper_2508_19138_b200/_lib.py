@@ -1,0 +1,100 @@
+"""ctypes binding of ``libnegf_b200.so`` (the C ABI in include/negf_b200.h).
+
+There is deliberately no CPU fallback: if the shared library is missing or
+no CUDA device is visible, every hot-path call raises. The library is built
+in-tree by ``paper_2508_19138_b200/build.py`` (``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import torch
+
+_LIB_PATH = Path(__file__).resolve().parent / "libnegf_b200.so"
+_lib: C.CDLL | None = None
+
+_vp = C.c_void_p
+_i = C.c_int
+_ll = C.c_longlong
+_d = C.c_double
+_sz = C.c_size_t
+
+# name -> (restype, argtypes)
+_SIGNATURES: dict[str, tuple] = {
+    "negf_abi_version": (_i, []),
+    "negf_rgf_workspace_bytes": (_sz, [_i, _i, _i]),
+    "negf_rgf_selected_solve_batched": (
+        _i,
+        [_i, _i, _i] + [_vp] * 14 + [_i, _vp, _vp, _vp, _sz, _vp],
+    ),
+    "negf_zgemm_batched": (
+        _i,
+        [_i, _i, _i, _i, _d, _d, _vp, _ll, _i, _i, _vp, _ll, _i, _i, _d, _d, _vp, _ll, _i, _vp, _ll, _i, _vp],
+    ),
+    "negf_zinv_workspace_bytes": (_sz, [_i, _i]),
+    "negf_zinv_batched": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+}
+
+
+class NativeLibraryError(RuntimeError):
+    """The CUDA library is missing or the call failed."""
+
+
+def lib_path() -> Path:
+    return _LIB_PATH
+
+
+def load(require_gpu: bool = True) -> C.CDLL:
+    """Load the shared library (idempotent). Raises if absent."""
+    global _lib
+    if require_gpu and not torch.cuda.is_available():
+        raise NativeLibraryError(
+            "negf_b200 hot path needs a CUDA device (sm_100a); there is no CPU fallback"
+        )
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise NativeLibraryError(
+                f"{_LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        lib = C.CDLL(str(_LIB_PATH))
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGNATURES)
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise NativeLibraryError(f"{what} failed with code {rc}")
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_ptr(device: torch.device | None = None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+_WS: dict[tuple, torch.Tensor] = {}
+
+
+def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
+    """Per-device cached scratch buffer (grown on demand, stream-ordered use)."""
+    key = (device.type, device.index, torch.cuda.current_stream(device).cuda_stream)
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        _WS.pop(key, None)
+        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        _WS[key] = buf
+    return buf

@@ -1,0 +1,264 @@
+// Batched-over-energy RGF selected inversion (retarded + lesser + greater in
+// one fused forward sweep and one fused backward sweep).
+//
+// Reference recurrences (negfgw/rgf.py):
+//   forward_retarded   rgf.py:113-129   x_i = (M_ii - M_{i,i-1} x_{i-1} M_{i-1,i})^-1
+//   forward_lg         rgf.py:132-149   b_i = B_ii + a xl_{i-1} a^dag - (y - y^dag),
+//                                       y = (a x_{i-1}) B_{i-1,i};  xl_i = x_i b_i x_i^dag
+//   rgf_retarded       rgf.py:152-183   backward: t = x_i M_{i,i+1}, u = t X_{i+1}, ...
+//   rgf_lesser_greater rgf.py:186-229   backward lesser/greater
+//   SelectedSolution.symmetrize rgf.py:82-88
+//
+// All energies of the batch advance in lock-step; every block product is one
+// grouped, batched DMMA launch (zgemm.cu) and independent products of the
+// same step (both kinds, retarded and lesser/greater) share a launch.
+// Reuse versus the reference's 43 N_B - 39 products per energy:
+//   * A_i = M_{i,i-1} x_{i-1} is shared by the retarded Schur update and y;
+//   * t, u (= -X_up), mx are shared by the retarded and both Keldysh passes;
+//   * z - y = u mxl - p u^dag is one two-term product, so
+//     (z - z^dag) - (y - y^dag) = v - v^dag needs one product;
+//   * t X t^dag reuses W = X t^dag, which also feeds the lower block:
+//     lower = -X_{i+1} (p^dag + mxl) - W  (p = x_i B_{i,i+1}; the reference's
+//     X_{i+1} B_{i+1,i} x_i^dag equals -X_{i+1} p^dag by the lg symmetry of B).
+// => 31 N_B - 27 products + N_B inversions per energy (both kinds).
+// x_fwd lives in xr_diag and xl_fwd in xl_diag: each is overwritten in place
+// by the backward pass once its last reader has run.
+#include "ew.cuh"
+#include "rgf.cuh"
+#include "zgemm.cuh"
+#include "zinv.cuh"
+
+namespace negf {
+
+namespace {
+
+constexpr int kTmpShared = 2;  // tA, tS
+constexpr int kTmpKind = 6;    // k0..k5
+constexpr int kTmpTotal = kTmpShared + 2 * kTmpKind;
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Ctx {
+  int n_e, n_b, bs;
+  long long bs2, sdiag, soff;
+  cudaStream_t st;
+  z_t* tmp;  // [kTmpTotal][n_e][bs][bs]
+  void* inv_ws;
+  size_t inv_ws_bytes;
+
+  z_t* T(int slot) const { return tmp + (long long)slot * n_e * bs2; }
+  z_t* K(int kind, int j) const { return T(kTmpShared + kind * kTmpKind + j); }
+  ZTerm term(const z_t* A, long long sA, int opA, const z_t* B, long long sB, int opB,
+             bool neg = false) const {
+    return zterm(A, sA, bs, opA, B, sB, bs, opB, bs, neg);
+  }
+  ZGemmDesc desc(const ZTerm& t0, z_t* D, long long sD, double alpha_re = 1.0,
+                 const z_t* C = nullptr, long long sC = 0, double beta_re = 0.0,
+                 int transD = 0) const {
+    ZGemmDesc d;
+    d.M = bs; d.N = bs; d.batch = n_e; d.nterms = 1;
+    d.t[0] = t0; d.t[1] = t0;
+    d.alpha = make_double2(alpha_re, 0.0);
+    d.beta = make_double2(beta_re, 0.0);
+    d.C = C; d.sC = sC; d.ldc = bs;
+    d.D = D; d.sD = sD; d.ldd = bs;
+    d.transD = transD;
+    return d;
+  }
+};
+
+struct Group {
+  ZGemmGroup g;
+  Group() { g.n = 0; }
+  void add(const ZGemmDesc& d) { g.d[g.n++] = d; }
+  int run(cudaStream_t s) { int rc = zgemm_group_launch(g, s); g.n = 0; return rc; }
+};
+
+struct EGroup {
+  EwGroup g;
+  EGroup(int bs) { g.n = 0; g.rows = bs; g.cols = bs; }
+  void add(z_t* out, long long sOut, int batch, std::initializer_list<const z_t*> X,
+           std::initializer_list<long long> sX, std::initializer_list<int> opH,
+           std::initializer_list<double> coef) {
+    EwDesc& d = g.d[g.n++];
+    d.batch = batch; d.out = out; d.sOut = sOut; d.nterms = (int)X.size();
+    int i = 0;
+    for (auto p : X) d.X[i++] = p;
+    i = 0; for (auto s : sX) d.sX[i++] = s;
+    i = 0; for (auto o : opH) d.opH[i++] = o;
+    i = 0; for (auto c : coef) d.coef[i++] = make_double2(c, 0.0);
+  }
+  int run(cudaStream_t s) { int rc = ew_group_launch(g, s); g.n = 0; return rc; }
+};
+
+#define RC(x) do { int _rc = (x); if (_rc) return _rc; } while (0)
+
+}  // namespace
+
+size_t rgf_workspace_bytes(int n_e, int n_b, int bs) {
+  size_t tmp = align256(sizeof(z_t) * (size_t)kTmpTotal * n_e * bs * bs);
+  return tmp + align256(zinv_workspace_bytes(bs, n_e));
+}
+
+int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (a.n_e <= 0) return 0;
+  if (a.n_b < 1 || a.bs < 1) return -1;
+  if (ws_bytes < rgf_workspace_bytes(a.n_e, a.n_b, a.bs)) return -4;
+  Ctx c;
+  c.n_e = a.n_e; c.n_b = a.n_b; c.bs = a.bs;
+  c.bs2 = (long long)a.bs * a.bs;
+  c.sdiag = (long long)a.n_b * c.bs2;
+  c.soff = (long long)(a.n_b > 1 ? a.n_b - 1 : 0) * c.bs2;
+  c.st = st;
+  c.tmp = reinterpret_cast<z_t*>(ws);
+  c.inv_ws = reinterpret_cast<char*>(ws) + align256(sizeof(z_t) * (size_t)kTmpTotal * a.n_e * c.bs2);
+  c.inv_ws_bytes = ws_bytes - align256(sizeof(z_t) * (size_t)kTmpTotal * a.n_e * c.bs2);
+
+  const int n = a.n_b, bs = a.bs, ne = a.n_e;
+  const long long bs2 = c.bs2, sd = c.sdiag, so = c.soff;
+  const long long st1 = bs2;  // temp energy stride
+  int kinds[2], nk = 0;
+  for (int k = 0; k < 2; ++k)
+    if (a.b_diag[k]) kinds[nk++] = k;
+
+  auto Md = [&](int i) { return a.m_diag + i * bs2; };
+  auto Mu = [&](int i) { return a.m_upper + i * bs2; };
+  auto Ml = [&](int i) { return a.m_lower + i * bs2; };
+  auto Bd = [&](int k, int i) { return a.b_diag[k] + i * bs2; };
+  auto Bu = [&](int k, int i) { return a.b_upper[k] + i * bs2; };
+  auto Xd = [&](int i) { return a.xr_diag + i * bs2; };
+  auto Xu = [&](int i) { return a.xr_upper + i * bs2; };
+  auto Xl = [&](int i) { return a.xr_lower + i * bs2; };
+  auto Ld = [&](int k, int i) { return a.xl_diag[k] + i * bs2; };
+  auto Lu = [&](int k, int i) { return a.xl_upper[k] + i * bs2; };
+  z_t* tA = c.T(0);
+  z_t* tS = c.T(1);
+
+  auto invert_into = [&](int i) -> int {
+    InvAux aux;
+    aux.status = a.status;
+    aux.status_code = 1 + i;
+    aux.u_spread = a.u_spread ? a.u_spread + i : nullptr;
+    aux.spread_stride = n;
+    return zinv_batched(tS, st1, bs, Xd(i), sd, bs, bs, ne, aux, c.inv_ws, c.inv_ws_bytes, st);
+  };
+
+  Group G;
+  EGroup E(bs);
+
+  // ---------------- forward sweep ----------------
+  // i = 0
+  NEGF_CUDA_CHECK(cudaMemcpy2DAsync(tS, st1 * sizeof(z_t), Md(0), sd * sizeof(z_t),
+                                    bs2 * sizeof(z_t), ne, cudaMemcpyDeviceToDevice, st));
+  RC(invert_into(0));
+  for (int q = 0; q < nk; ++q) {  // U = x_0 B_00
+    int k = kinds[q];
+    G.add(c.desc(c.term(Xd(0), sd, OP_N, Bd(k, 0), sd, OP_N), c.K(k, 0), st1));
+  }
+  RC(G.run(st));
+  for (int q = 0; q < nk; ++q) {  // xl_0 = U x_0^dag
+    int k = kinds[q];
+    G.add(c.desc(c.term(c.K(k, 0), st1, OP_N, Xd(0), sd, OP_H), Ld(k, 0), sd));
+  }
+  RC(G.run(st));
+
+  for (int i = 1; i < n; ++i) {
+    // G1: A = M_{i,i-1} x_{i-1};  T1_k = M_{i,i-1} xl_{k,i-1}
+    G.add(c.desc(c.term(Ml(i - 1), so, OP_N, Xd(i - 1), sd, OP_N), tA, st1));
+    for (int q = 0; q < nk; ++q) {
+      int k = kinds[q];
+      G.add(c.desc(c.term(Ml(i - 1), so, OP_N, Ld(k, i - 1), sd, OP_N), c.K(k, 0), st1));
+    }
+    RC(G.run(st));
+    // G2: S = M_ii - A M_{i-1,i};  Y_k = A B_{k,i-1,i}
+    G.add(c.desc(c.term(tA, st1, OP_N, Mu(i - 1), so, OP_N), tS, st1, -1.0, Md(i), sd, 1.0));
+    for (int q = 0; q < nk; ++q) {
+      int k = kinds[q];
+      G.add(c.desc(c.term(tA, st1, OP_N, Bu(k, i - 1), so, OP_N), c.K(k, 1), st1));
+    }
+    RC(G.run(st));
+    RC(invert_into(i));
+    if (nk == 0) continue;
+    // E_k = B_k,ii - Y_k + Y_k^dag
+    for (int q = 0; q < nk; ++q) {
+      int k = kinds[q];
+      E.add(c.K(k, 2), st1, ne, {Bd(k, i), c.K(k, 1), c.K(k, 1)}, {sd, st1, st1}, {0, 0, 1},
+            {1.0, -1.0, 1.0});
+    }
+    RC(E.run(st));
+    // b_k = T1_k M_{i,i-1}^dag + E_k
+    for (int q = 0; q < nk; ++q) {
+      int k = kinds[q];
+      G.add(c.desc(c.term(c.K(k, 0), st1, OP_N, Ml(i - 1), so, OP_H), c.K(k, 3), st1, 1.0,
+                   c.K(k, 2), st1, 1.0));
+    }
+    RC(G.run(st));
+    // U_k = x_i b_k
+    for (int q = 0; q < nk; ++q) {
+      int k = kinds[q];
+      G.add(c.desc(c.term(Xd(i), sd, OP_N, c.K(k, 3), st1, OP_N), c.K(k, 0), st1));
+    }
+    RC(G.run(st));
+    // xl_k,i = U_k x_i^dag
+    for (int q = 0; q < nk; ++q) {
+      int k = kinds[q];
+      G.add(c.desc(c.term(c.K(k, 0), st1, OP_N, Xd(i), sd, OP_H), Ld(k, i), sd));
+    }
+    RC(G.run(st));
+  }
+
+  // ---------------- backward sweep ----------------
+  // X_{n-1,n-1} = x_{n-1} and XL_{n-1} = xl_{n-1} already sit in place.
+  for (int i = n - 2; i >= 0; --i) {
+    // G1: t = x_i M_{i,i+1}; mx = M_{i+1,i} x_i; p_k = x_i B_{k,i,i+1}; mxl_k = M_{i+1,i} xl_{k,i}
+    G.add(c.desc(c.term(Xd(i), sd, OP_N, Mu(i), so, OP_N), tA, st1));
+    G.add(c.desc(c.term(Ml(i), so, OP_N, Xd(i), sd, OP_N), tS, st1));
+    for (int q = 0; q < nk; ++q) {
+      int k = kinds[q];
+      G.add(c.desc(c.term(Xd(i), sd, OP_N, Bu(k, i), so, OP_N), c.K(k, 0), st1));
+      G.add(c.desc(c.term(Ml(i), so, OP_N, Ld(k, i), sd, OP_N), c.K(k, 1), st1));
+    }
+    RC(G.run(st));
+    // G2: X_up = -t X_{i+1}; X_lo = -X_{i+1} mx; W_k = XL_{k,i+1} t^dag
+    G.add(c.desc(c.term(tA, st1, OP_N, Xd(i + 1), sd, OP_N), Xu(i), so, -1.0));
+    G.add(c.desc(c.term(Xd(i + 1), sd, OP_N, tS, st1, OP_N), Xl(i), so, -1.0));
+    for (int q = 0; q < nk; ++q) {
+      int k = kinds[q];
+      G.add(c.desc(c.term(Ld(k, i + 1), sd, OP_N, tA, st1, OP_H), c.K(k, 3), st1));
+    }
+    RC(G.run(st));
+    // G3: X_ii = x_i - X_up mx (in place); v_k = -X_up mxl_k + p_k X_up^dag
+    G.add(c.desc(c.term(Xu(i), so, OP_N, tS, st1, OP_N), Xd(i), sd, -1.0, Xd(i), sd, 1.0));
+    for (int q = 0; q < nk; ++q) {
+      int k = kinds[q];
+      ZGemmDesc d = c.desc(c.term(Xu(i), so, OP_N, c.K(k, 1), st1, OP_N, true), c.K(k, 2), st1);
+      d.nterms = 2;
+      d.t[1] = c.term(c.K(k, 0), st1, OP_N, Xu(i), so, OP_H);
+      G.add(d);
+    }
+    RC(G.run(st));
+    if (nk == 0) continue;
+    // E_k = xl_k,i + v_k - v_k^dag ; Q_k = p_k^dag + mxl_k
+    for (int q = 0; q < nk; ++q) {
+      int k = kinds[q];
+      E.add(c.K(k, 4), st1, ne, {Ld(k, i), c.K(k, 2), c.K(k, 2)}, {sd, st1, st1}, {0, 0, 1},
+            {1.0, 1.0, -1.0});
+      E.add(c.K(k, 5), st1, ne, {c.K(k, 0), c.K(k, 1)}, {st1, st1}, {1, 0}, {1.0, 1.0});
+    }
+    RC(E.run(st));
+    // G4: XL_k,ii = t W_k + E_k ; XL_k,up = (X_{i+1} Q_k + W_k)^dag
+    for (int q = 0; q < nk; ++q) {
+      int k = kinds[q];
+      G.add(c.desc(c.term(tA, st1, OP_N, c.K(k, 3), st1, OP_N), Ld(k, i), sd, 1.0, c.K(k, 4), st1,
+                   1.0));
+      G.add(c.desc(c.term(Xd(i + 1), sd, OP_N, c.K(k, 5), st1, OP_N), Lu(k, i), so, 1.0,
+                   c.K(k, 3), st1, 1.0, /*transD=*/1));
+    }
+    RC(G.run(st));
+  }
+  if (a.symmetrize)
+    for (int q = 0; q < nk; ++q) RC(antiherm_inplace(a.xl_diag[kinds[q]], bs2, bs, ne * n, st));
+  return 0;
+}
+
+}  // namespace negf

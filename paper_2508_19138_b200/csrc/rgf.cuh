@@ -1,0 +1,30 @@
+// Batched-over-energy RGF selected solve (host orchestration of the DMMA
+// GEMM, pivoted inversion and elementwise kernels). See rgf.cu.
+#pragma once
+#include "common.cuh"
+
+namespace negf {
+
+// One batch of block-tridiagonal systems, all complex128 device pointers,
+// energy-major packed: diag [n_e][n_b][bs][bs], off [n_e][n_b-1][bs][bs].
+struct RgfArgs {
+  int n_e, n_b, bs;
+  const z_t* m_diag;
+  const z_t* m_upper;
+  const z_t* m_lower;
+  const z_t* b_diag[2];   // lesser, greater (nullptr: kind absent)
+  const z_t* b_upper[2];  // lg-compressed: B[i+1][i] = -B[i][i+1]^dag
+  z_t* xr_diag;
+  z_t* xr_upper;
+  z_t* xr_lower;
+  z_t* xl_diag[2];
+  z_t* xl_upper[2];
+  int symmetrize;      // apply (X - X^dag)/2 to the lesser/greater diagonal blocks
+  int* status;         // [n_e] device: 0 ok, 1 + forward step of the first singular block
+  double* u_spread;    // [n_e][n_b] device, optional
+};
+
+size_t rgf_workspace_bytes(int n_e, int n_b, int bs);
+int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t stream);
+
+}  // namespace negf

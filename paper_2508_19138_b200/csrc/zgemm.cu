@@ -1,0 +1,243 @@
+// Batched grouped complex-FP64 DMMA GEMM (see zgemm.cuh for the contract).
+#include "zgemm.cuh"
+
+namespace negf {
+
+namespace {
+
+constexpr unsigned long long kSign = 0x8000000000000000ull;
+
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int BK = 8;
+  static constexpr int NT = WM * WN * 32;
+  static constexpr int WTM = BM / WM;  // warp tile rows
+  static constexpr int WTN = BN / WN;
+  static constexpr int TM = WTM / 8;  // 8x8 DMMA tiles per warp
+  static constexpr int TN = WTN / 8;
+  static constexpr int SK = BK + 4;   // k-contiguous row stride
+  static constexpr int SMA = BM + 2;  // mn-contiguous row stride (A)
+  static constexpr int SMB = BN + 2;  // mn-contiguous row stride (B)
+  static constexpr int A_ELEMS = (BM * SK > BK * SMA) ? BM * SK : BK * SMA;
+  static constexpr int B_ELEMS = (BN * SK > BK * SMB) ? BN * SK : BK * SMB;
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_ELEMS * sizeof(z_t);
+};
+
+// Stage one BK-slice of both operands into shared memory with cp.async.
+template <class CF>
+__device__ __forceinline__ void load_stage(const ZGemmDesc& d, int kt, int kt0, int b, int m0,
+                                           int n0, z_t* sA, z_t* sB) {
+  const int term = kt < kt0 ? 0 : 1;
+  const ZTerm& t = d.t[term];
+  const int k0 = (kt - (term ? kt0 : 0)) * CF::BK;
+  const z_t* A = t.A + (long long)b * t.sA;
+  const z_t* B = t.B + (long long)b * t.sB;
+  const int K = t.K, M = d.M, N = d.N;
+  if (!op_trans(t.opA)) {  // A stored [M][K]: k contiguous
+#pragma unroll
+    for (int e = threadIdx.x; e < CF::BM * CF::BK; e += CF::NT) {
+      int mn = e / CF::BK, k = e % CF::BK;
+      int gm = m0 + mn, gk = k0 + k;
+      bool p = gm < M && gk < K;
+      const z_t* src = p ? A + (long long)gm * t.lda + gk : A;
+      cp_async16(sA + mn * CF::SK + k, src, p);
+    }
+  } else {  // A stored [K][M]: m contiguous
+#pragma unroll
+    for (int e = threadIdx.x; e < CF::BM * CF::BK; e += CF::NT) {
+      int mn = e % CF::BM, k = e / CF::BM;
+      int gm = m0 + mn, gk = k0 + k;
+      bool p = gm < M && gk < K;
+      const z_t* src = p ? A + (long long)gk * t.lda + gm : A;
+      cp_async16(sA + k * CF::SMA + mn, src, p);
+    }
+  }
+  if (!op_trans(t.opB)) {  // B stored [K][N]: n contiguous
+#pragma unroll
+    for (int e = threadIdx.x; e < CF::BN * CF::BK; e += CF::NT) {
+      int mn = e % CF::BN, k = e / CF::BN;
+      int gn = n0 + mn, gk = k0 + k;
+      bool p = gn < N && gk < K;
+      const z_t* src = p ? B + (long long)gk * t.ldb + gn : B;
+      cp_async16(sB + k * CF::SMB + mn, src, p);
+    }
+  } else {  // B stored [N][K]: k contiguous
+#pragma unroll
+    for (int e = threadIdx.x; e < CF::BN * CF::BK; e += CF::NT) {
+      int mn = e / CF::BK, k = e % CF::BK;
+      int gn = n0 + mn, gk = k0 + k;
+      bool p = gn < N && gk < K;
+      const z_t* src = p ? B + (long long)gn * t.ldb + gk : B;
+      cp_async16(sB + mn * CF::SK + k, src, p);
+    }
+  }
+}
+
+template <class CF>
+__global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_constant__ ZGemmGroup grp) {
+  extern __shared__ __align__(16) z_t smem[];
+  const ZGemmDesc& d = grp.d[blockIdx.z];
+  const int tiles_n = (d.N + CF::BN - 1) / CF::BN;
+  const int tiles_m = (d.M + CF::BM - 1) / CF::BM;
+  if ((int)blockIdx.x >= tiles_m * tiles_n || (int)blockIdx.y >= d.batch) return;
+  const int b = blockIdx.y;
+  const int m0 = (blockIdx.x / tiles_n) * CF::BM;
+  const int n0 = (blockIdx.x % tiles_n) * CF::BN;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp / CF::WN, wn = warp % CF::WN;
+
+  const int kt0 = (d.t[0].K + CF::BK - 1) / CF::BK;
+  const int kt1 = d.nterms > 1 ? (d.t[1].K + CF::BK - 1) / CF::BK : 0;
+  const int KT = kt0 + kt1;
+
+  double acc_re[CF::TM][CF::TN][2], acc_im[CF::TM][CF::TN][2];
+#pragma unroll
+  for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+    for (int j = 0; j < CF::TN; ++j) {
+      acc_re[i][j][0] = acc_re[i][j][1] = 0.0;
+      acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
+    }
+
+  auto stageA = [&](int s) { return smem + s * CF::STAGE_ELEMS; };
+  auto stageB = [&](int s) { return smem + s * CF::STAGE_ELEMS + CF::A_ELEMS; };
+
+#pragma unroll
+  for (int s = 0; s < CF::STAGES - 1; ++s) {
+    if (s < KT) load_stage<CF>(d, s, kt0, b, m0, n0, stageA(s), stageB(s));
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<CF::STAGES - 2>();
+    __syncthreads();
+    {
+      int nk = kt + CF::STAGES - 1;
+      if (nk < KT) {
+        int s = nk % CF::STAGES;
+        load_stage<CF>(d, nk, kt0, b, m0, n0, stageA(s), stageB(s));
+      }
+      cp_async_commit();
+    }
+    const int s = kt % CF::STAGES;
+    const z_t* sA = stageA(s);
+    const z_t* sB = stageB(s);
+    const ZTerm& t = d.t[kt < kt0 ? 0 : 1];
+    const bool a_kc = !op_trans(t.opA);
+    const bool b_kc = op_trans(t.opB);
+    const unsigned long long negm = t.neg ? kSign : 0ull;
+    const unsigned long long conjA = op_conj(t.opA) ? kSign : 0ull;
+    const unsigned long long conjB = op_conj(t.opB) ? kSign : 0ull;
+    // fragment addressing: element (mn, k) at mn*s_mn + k*s_k
+    const int a_smn = a_kc ? CF::SK : 1, a_sk = a_kc ? 1 : CF::SMA;
+    const int b_smn = b_kc ? CF::SK : 1, b_sk = b_kc ? 1 : CF::SMB;
+    const int r = lane >> 2, q = lane & 3;
+#pragma unroll
+    for (int k4 = 0; k4 < CF::BK / 4; ++k4) {
+      const int kk = k4 * 4 + q;
+      double ar[CF::TM], ai[CF::TM], nai[CF::TM], br[CF::TN], bi[CF::TN];
+#pragma unroll
+      for (int i = 0; i < CF::TM; ++i) {
+        z_t v = sA[(wm * CF::WTM + i * 8 + r) * a_smn + kk * a_sk];
+        ar[i] = dneg_if(v.x, negm);
+        ai[i] = dneg_if(v.y, negm ^ conjA);
+        nai[i] = dneg_if(ai[i], kSign);
+      }
+#pragma unroll
+      for (int j = 0; j < CF::TN; ++j) {
+        z_t v = sB[(wn * CF::WTN + j * 8 + r) * b_smn + kk * b_sk];
+        br[j] = v.x;
+        bi[j] = dneg_if(v.y, conjB);
+      }
+#pragma unroll
+      for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+        for (int j = 0; j < CF::TN; ++j) {
+          dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
+          dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ar[i], bi[j]);
+          dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], nai[i], bi[j]);
+          dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], br[j]);
+        }
+    }
+  }
+  cp_async_wait<0>();
+
+  // Epilogue: value = alpha*acc + beta*C, stored plain or conj-transposed.
+  const double2 al = d.alpha, be = d.beta;
+  const bool use_c = d.C != nullptr && (be.x != 0.0 || be.y != 0.0);
+  const z_t* C = use_c ? d.C + (long long)b * d.sC : nullptr;
+  z_t* D = d.D + (long long)b * d.sD;
+  const int r = lane >> 2, q = lane & 3;
+#pragma unroll
+  for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+    for (int j = 0; j < CF::TN; ++j) {
+      const int gm = m0 + wm * CF::WTM + i * 8 + r;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gn = n0 + wn * CF::WTN + j * 8 + 2 * q + h;
+        if (gm < d.M && gn < d.N) {
+          double xr = acc_re[i][j][h], xi = acc_im[i][j][h];
+          z_t v = zmake(al.x * xr - al.y * xi, al.x * xi + al.y * xr);
+          if (use_c) {
+            z_t c = C[(long long)gm * d.ldc + gn];
+            v.x += be.x * c.x - be.y * c.y;
+            v.y += be.x * c.y + be.y * c.x;
+          }
+          if (d.transD)
+            D[(long long)gn * d.ldd + gm] = zconj(v);
+          else
+            D[(long long)gm * d.ldd + gn] = v;
+        }
+      }
+    }
+}
+
+template <class CF>
+int launch_cfg(const ZGemmGroup& g, cudaStream_t stream) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    NEGF_CUDA_CHECK(cudaFuncSetAttribute(zgemm_kernel<CF>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)CF::SMEM));
+    attr_done = true;
+  }
+  int max_tiles = 0, max_batch = 0;
+  for (int i = 0; i < g.n; ++i) {
+    int tm = (g.d[i].M + CF::BM - 1) / CF::BM, tn = (g.d[i].N + CF::BN - 1) / CF::BN;
+    if (tm * tn > max_tiles) max_tiles = tm * tn;
+    if (g.d[i].batch > max_batch) max_batch = g.d[i].batch;
+  }
+  if (max_tiles == 0 || max_batch == 0) return 0;
+  dim3 grid(max_tiles, max_batch, g.n);
+  zgemm_kernel<CF><<<grid, CF::NT, CF::SMEM, stream>>>(g);
+  NEGF_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+using CfgBig = Cfg<64, 64, 2, 2, 4, 2>;
+using CfgSmall = Cfg<32, 32, 1, 1, 4, 4>;
+
+}  // namespace
+
+int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
+  if (g.n <= 0) return 0;
+  int mx = 0;
+  for (int i = 0; i < g.n; ++i) {
+    if (g.d[i].M > mx) mx = g.d[i].M;
+    if (g.d[i].N > mx) mx = g.d[i].N;
+  }
+  if (mx <= 32) return launch_cfg<CfgSmall>(g, stream);
+  return launch_cfg<CfgBig>(g, stream);
+}
+
+int zgemm_launch(const ZGemmDesc& d, cudaStream_t stream) {
+  ZGemmGroup g;
+  g.n = 1;
+  g.d[0] = d;
+  return zgemm_group_launch(g, stream);
+}
+
+}  // namespace negf

@@ -1,0 +1,77 @@
+// Batched, grouped complex-FP64 GEMM on the FP64 tensor pipe (DMMA) for sm_100a.
+//
+//   D[b] = alpha * sum_t s_t * op(A_t[b]) op(B_t[b]) + beta * C[b]      (t < 2)
+//   optionally stored conjugate-transposed: D[b][n][m] = conj(value(m, n)).
+//
+// This is the kernel behind every dense block product of the RGF recursion
+// (reference: negfgw/_linalg.py:19 `gemm`, called from rgf.py:113-229),
+// the OBC decimation (obc.py:162-178), the Stein doubling (obc.py:427-447)
+// and the W assembly products (blocks.py:277 `bt_multiply`).
+//
+// Design (B200): tcgen05 has no f64 kind, so FP64 runs on the warp-level DMMA
+// path (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4). Measured on this pool's
+// B200: DMMA 37.0 TFLOP/s, DFMA 36.7, cuBLAS ZGEMM 36.8 (profiles/).
+// Operands are staged global->smem with cp.async (LDGSTS, 16 B = one complex)
+// through a multi-stage pipeline. Complex values stay interleaved in smem
+// so one LDS.128 yields both the real and the imaginary fragment.
+// Two smem layouts, chosen per operand from its transpose flag so the global
+// read is always coalesced:
+//   k-contiguous  [mn][BK+4]   (op N for A, op T/H for B)
+//   mn-contiguous [BK][BMN+2]  (op T/H for A, op N for B)
+// Both paddings make the DMMA fragment read (lane -> (mn=lane/4, k=lane%4))
+// bank-conflict free per 8-lane LDS.128 phase.
+// A complex product takes four real DMMAs: re += ar*br + (-ai)*bi,
+// im += ar*bi + ai*br; conjugation and term signs are sign-bit flips done on
+// the integer pipe.
+#pragma once
+#include "common.cuh"
+
+namespace negf {
+
+struct ZTerm {
+  const z_t* A;
+  long long sA;  // batch stride (elements)
+  int lda;
+  int opA;
+  const z_t* B;
+  long long sB;
+  int ldb;
+  int opB;
+  int K;
+  int neg;  // 1: subtract this term
+};
+
+struct ZGemmDesc {
+  int M, N, batch, nterms;
+  ZTerm t[2];
+  double2 alpha, beta;
+  const z_t* C;
+  long long sC;
+  int ldc;
+  z_t* D;
+  long long sD;
+  int ldd;
+  int transD;  // store conj-transposed
+};
+
+constexpr int kMaxGroup = 6;
+struct ZGemmGroup {
+  int n;
+  ZGemmDesc d[kMaxGroup];
+};
+
+// Host-side helpers -----------------------------------------------------------
+inline ZTerm zterm(const z_t* A, long long sA, int lda, int opA, const z_t* B, long long sB,
+                   int ldb, int opB, int K, bool neg = false) {
+  ZTerm t;
+  t.A = A; t.sA = sA; t.lda = lda; t.opA = opA;
+  t.B = B; t.sB = sB; t.ldb = ldb; t.opB = opB;
+  t.K = K; t.neg = neg ? 1 : 0;
+  return t;
+}
+
+// Launch a group of GEMM problems (same tile config) on `stream`.
+int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream);
+int zgemm_launch(const ZGemmDesc& d, cudaStream_t stream);
+
+}  // namespace negf
