@@ -65,6 +65,57 @@ size_t negf_zinv_workspace_bytes(int n, int batch);
 int negf_zinv_batched(int n, int batch, void* s, void* x, int* status, double* u_spread,
                       void* workspace, size_t workspace_bytes, void* stream);
 
+
+/* ---- (2) open boundary conditions (negfgw/obc.py) -------------------------
+ * Sancho-Rubio decimation for `batch` surface problems x = (m - n x n')^-1,
+ * replaces obc_sancho_rubio (obc.py:144-182), including its stopping rule
+ * |a|_F + |b|_F < tol * max(|n|_F, |n'|_F) and the closing recursion-residual
+ * check (> 10 max(tol, 1e-14) fails). m, n, np, x: [batch][bs][bs] device.
+ * status[b] (device int): 0 ok, 1 singular block, 2 not converged in
+ * max_iter sweeps, 3 residual check failed. iters[b]: sweeps used;
+ * resid[b] (may be NULL): recursion residual. Synchronises `stream` once per
+ * sweep (the convergence test). */
+size_t negf_sancho_workspace_bytes(int batch, int bs);
+int negf_obc_sancho_batched(int batch, int bs, const void* m, const void* n, const void* np,
+                            double tol, int max_iter, void* x, int* status, int* iters,
+                            double* resid, void* workspace, size_t workspace_bytes, void* stream);
+
+/* sigma_lg_obc (obc.py:460-486), batched: Sigma^R = n x n',
+ * Sigma^< = -f (Sigma^R - Sigma^R^dag), Sigma^> = (1-f)(Sigma^R - Sigma^R^dag)
+ * with f[b] = fermi(E_b - mu) (device double). Outputs may be NULL. */
+size_t negf_sigma_lg_obc_workspace_bytes(int batch, int bs);
+int negf_sigma_lg_obc_batched(int batch, int bs, const void* x, const void* n, const void* np,
+                              const double* f, void* sigma_r, void* sigma_lesser,
+                              void* sigma_greater, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
+/* Carrier-side contact closure of an assembled batch (scba.py:755-774):
+ * for the left (corner 0) and right (corner n_b-1) leads, solve the surface
+ * problem by Sancho-Rubio on the contact cell of M (scba.py:558-574), then
+ * M_cc -= Sigma^R_obc, B^<_cc += Sigma^<_obc, B^>_cc += Sigma^>_obc in place.
+ * f_left/f_right[n_e]: contact occupations. sl/sg_left/right [n_e][bs][bs]
+ * (may be NULL) receive the boundary lesser/greater self-energies.
+ * status/iters/resid: [2][n_e] (left block first). */
+size_t negf_g_obc_workspace_bytes(int n_e, int bs);
+int negf_g_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper,
+                     const void* m_lower, void* bl_diag, void* bg_diag, const double* f_left,
+                     const double* f_right, double tol, int max_iter, void* sl_left,
+                     void* sg_left, void* sl_right, void* sg_right, int* status, int* iters,
+                     double* resid, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Carrier system assembly (scba.py:670-727) for n_e energies:
+ *   M_ii = (E + i eta) I - H_ii - SR_ii,  M_{i,i+-1} = -H - SR,
+ *   B^<_ii = 2 i eta f I + SL_ii, B^>_ii = -2 i eta (1-f) I + SG_ii, B_{i,i+1} = S_{i,i+1}.
+ * h_*: energy-independent blocks [n_b or n_b-1][bs][bs]; energy, f_bath:
+ * [n_e] device doubles; scattering self-energies s*_ (energy-major blocks)
+ * may be NULL (ballistic). Lesser/greater outputs may be NULL. */
+int negf_g_assemble(int n_e, int n_b, int bs, const void* h_diag, const void* h_upper,
+                    const void* h_lower, const double* energy, const double* f_bath, double eta,
+                    const void* sr_diag, const void* sr_upper, const void* sr_lower,
+                    const void* sl_diag, const void* sl_upper, const void* sg_diag,
+                    const void* sg_upper, void* m_diag, void* m_upper, void* m_lower,
+                    void* bl_diag, void* bl_upper, void* bg_diag, void* bg_upper, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -217,3 +217,150 @@ def coulomb_matrix(n_blocks: int, block_size: int, v0: float = 1e-3, seed: int =
 def fermi(e, mu, kT):
     """device.py:32-36."""
     return expit(-(np.asarray(e, dtype=float) - mu) / kT)
+
+
+# -- open boundary conditions (obc.py) ----------------------------------------
+
+
+class OracleConvergence(Exception):
+    pass
+
+
+def recursion_residual(m, n, n_prime, x) -> float:
+    """obc.py:98-104: relative defect of x = (m - n x n')^-1."""
+    lhs, _ = lu_inverse(m - (n @ x) @ n_prime)
+    num, den = np.linalg.norm(lhs - x), np.linalg.norm(x)
+    return float(num / den) if den > 0 else float(num)
+
+
+def sancho_rubio(m, n, n_prime, tol: float = 1e-12, max_iter: int = 100):
+    """obc.py:144-182 decimation; returns (x, sweeps, residual)."""
+    s, b, al, be = m.copy(), m.copy(), n.copy(), n_prime.copy()
+    scale = max(np.linalg.norm(n), np.linalg.norm(n_prime), 1e-300)
+    for it in range(1, max_iter + 1):
+        g, _ = lu_inverse(b)
+        ag, bg = al @ g, be @ g
+        agb, bga = ag @ be, bg @ al
+        s = s - agb
+        b = b - agb - bga
+        al, be = ag @ al, bg @ be
+        if np.linalg.norm(al) + np.linalg.norm(be) < tol * scale:
+            x, _ = lu_inverse(s)
+            res = recursion_residual(m, n, n_prime, x)
+            if not np.isfinite(res) or res > 10 * max(tol, 1e-14):
+                raise OracleConvergence(f"residual {res:.3e}")
+            return x, it, res
+    raise OracleConvergence("not converged")
+
+
+def sigma_lg_obc(x_r, mu, kT, energy, n, n_prime):
+    """obc.py:460-486."""
+    sr = (n @ x_r) @ n_prime
+    gam = sr - _h(sr)
+    f = float(fermi(energy, mu, kT))
+    return sr, -f * gam, (1.0 - f) * gam
+
+
+def spectral_radius_estimate(a, n_iter: int = 50, seed: int = 5) -> float:
+    """obc.py:320-342 power iteration."""
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(a.shape[0]) + 1j * rng.standard_normal(a.shape[0])
+    v /= np.linalg.norm(v)
+    rho = 0.0
+    for _ in range(n_iter):
+        w = a @ v
+        nw = np.linalg.norm(w)
+        if nw == 0:
+            return 0.0
+        rho, v = nw, w / nw
+    return float(rho)
+
+
+def stein_geometric(a, q, tol: float = 1e-12, max_iter: int = 100):
+    """obc.py:427-447: w - a w a^dag = q by squared doubling."""
+    if spectral_radius_estimate(a) >= 1.0:
+        raise OracleConvergence("spectral radius >= 1")
+    w, ak = q.copy(), a.copy()
+    for _ in range(max_iter):
+        upd = (ak @ w) @ _h(ak)
+        w = w + upd
+        if np.linalg.norm(upd) < tol * max(np.linalg.norm(w), 1e-300):
+            return w
+        ak = ak @ ak
+    raise OracleConvergence("stein not converged")
+
+
+def stein_direct(a, q):
+    """scba.py:534-543: doubling with the dense vectorised fallback."""
+    try:
+        return stein_geometric(a, q)
+    except OracleConvergence:
+        n = a.shape[0]
+        lhs = np.eye(n * n, dtype=complex) - np.kron(a.conj(), a)
+        return np.linalg.solve(lhs, q.ravel(order="F")).reshape((n, n), order="F")
+
+
+# -- carrier system (scba.py:670-775) ------------------------------------------
+
+
+def assemble_g(energies, eta, h, f_bath, sr=None, sl=None, sg=None):
+    """scba.py:670-727 for a batch of energies. h = (diag, up, lo) of H;
+    sr = (diag, up, lo) of Sigma^R_scatt, sl/sg = (diag, up) of Sigma^<>_scatt
+    (all energy-major), any may be None. Returns m=(d,u,l), bl=(d,u), bg=(d,u)."""
+    hd, hu, hl = h
+    ne, bs = len(energies), hd.shape[-1]
+    eye = np.eye(bs)
+    z = (np.asarray(energies) + 1j * eta)[:, None, None, None]
+    md = z * eye - hd[None]
+    mu = np.broadcast_to(-hu[None], (ne,) + hu.shape).copy()
+    ml = np.broadcast_to(-hl[None], (ne,) + hl.shape).copy()
+    if sr is not None:
+        md, mu, ml = md - sr[0], mu - sr[1], ml - sr[2]
+    f = np.asarray(f_bath)[:, None, None, None]
+    bld = np.broadcast_to((2j * eta * f) * eye, md.shape) + (0 if sl is None else sl[0])
+    bgd = np.broadcast_to((-2j * eta * (1.0 - f)) * eye, md.shape) + (0 if sg is None else sg[0])
+    blu = np.zeros_like(mu) if sl is None else sl[1].copy()
+    bgu = np.zeros_like(mu) if sg is None else sg[1].copy()
+    return (md, mu, ml), (np.ascontiguousarray(bld), blu), (np.ascontiguousarray(bgd), bgu)
+
+
+def g_closure(m, bl, bg, energies, mu_left, mu_right, kT, tol):
+    """scba.py:755-774: per side, Sancho on the contact cell (_lead_cell,
+    scba.py:558-574), sigma_lg_obc, corner updates. In place; returns the
+    boundary lesser/greater self-energies {side: (sl, sg)} (n_e, bs, bs)."""
+    md, mu, ml = m
+    n_b = md.shape[1]
+    out = {}
+    for side, mu_c in (("left", mu_left), ("right", mu_right)):
+        c = 0 if side == "left" else n_b - 1
+        sls, sgs = [], []
+        for e, E in enumerate(energies):
+            if side == "left":
+                cell = (md[e, 0], ml[e, 0], mu[e, 0])
+            else:
+                cell = (md[e, n_b - 1], mu[e, n_b - 2], ml[e, n_b - 2])
+            x, _, _ = sancho_rubio(*cell, tol=tol)
+            sr, s_l, s_g = sigma_lg_obc(x, mu_c, kT, E, cell[1], cell[2])
+            md[e, c] = md[e, c] - sr
+            bl[0][e, c] = bl[0][e, c] + s_l
+            bg[0][e, c] = bg[0][e, c] + s_g
+            sls.append(s_l)
+            sgs.append(s_g)
+        out[side] = (np.stack(sls), np.stack(sgs))
+    return out
+
+
+def ballistic(h, energies, eta, mu_left, mu_right, kT, tol=1e-8):
+    """scba_run with v_mat=None, retarded_method='sancho', memoizer off
+    (scba.py:951-1011): one carrier solve per energy, symmetrized."""
+    f_bath = fermi(energies, 0.5 * (mu_left + mu_right), kT)
+    m, bl, bg = assemble_g(energies, eta, h, f_bath)
+    obc = g_closure(m, bl, bg, energies, mu_left, mu_right, kT, tol)
+    sol = rgf_selected(*m, {"<": bl, ">": bg}, symmetrize=True)
+    return {
+        "g_r_diag": sol["xr_diag"], "g_r_upper": sol["xr_upper"], "g_r_lower": sol["xr_lower"],
+        "g_lesser_diag": sol["x<_diag"], "g_lesser_upper": sol["x<_upper"],
+        "g_greater_diag": sol["x>_diag"], "g_greater_upper": sol["x>_upper"],
+        "sigma_obc_lesser_left": obc["left"][0], "sigma_obc_greater_left": obc["left"][1],
+        "sigma_obc_lesser_right": obc["right"][0], "sigma_obc_greater_right": obc["right"][1],
+    }

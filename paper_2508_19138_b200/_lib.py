@@ -35,6 +35,16 @@ _SIGNATURES: dict[str, tuple] = {
     ),
     "negf_zinv_workspace_bytes": (_sz, [_i, _i]),
     "negf_zinv_batched": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "negf_sancho_workspace_bytes": (_sz, [_i, _i]),
+    "negf_obc_sancho_batched": (_i, [_i, _i, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "negf_sigma_lg_obc_workspace_bytes": (_sz, [_i, _i]),
+    "negf_sigma_lg_obc_batched": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "negf_g_obc_workspace_bytes": (_sz, [_i, _i]),
+    "negf_g_obc_apply": (
+        _i,
+        [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp],
+    ),
+    "negf_g_assemble": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _d] + [_vp] * 7 + [_vp] * 7 + [_vp]),
 }
 
 

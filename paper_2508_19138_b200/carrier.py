@@ -1,0 +1,176 @@
+"""Carrier (G) solve for a batch of energies, entirely on the GPU.
+
+One ``CarrierSolver.solve`` call replaces, for every energy of the batch,
+the body of scba_run's G loop (scba.py:965-1000):
+  _assemble_g_system  scba.py:730-775  -> negf_g_assemble + negf_g_obc_apply
+  selected_solve      rgf.py:232-243   -> negf_rgf_selected_solve_batched
+  sol.symmetrize()    rgf.py:82-88     -> fused (symmetrize=1)
+Buffers are allocated once per (n_e, n_b, bs) and reused across batches, so
+a sweep over many energy batches does no allocation on the hot path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConvergenceError, SingularBlockError
+from .obc import fermi, raise_on_obc_status
+from .rgf import raise_on_status
+
+Z = torch.complex128
+
+
+@dataclass(frozen=True)
+class Contacts:
+    """scba.py:101-121 ContactConfig."""
+
+    mu_left: float
+    mu_right: float
+    kT: float = 0.02585
+
+    @property
+    def mu_mean(self) -> float:
+        return 0.5 * (self.mu_left + self.mu_right)
+
+
+def _dev_tensor(a, dev) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=Z).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=complex))).to(dev)
+
+
+class CarrierSolver:
+    """Batched G solve for a fixed Hamiltonian H (block tridiagonal)."""
+
+    def __init__(self, h, eta: float, contacts: Contacts, surface_tol: float = 1e-8,
+                 max_sweeps: int = 100, device="cuda") -> None:
+        self.dev = torch.device(device)
+        self.lib = _lib.load()
+        hd, hu, hl = h
+        self.h = tuple(_dev_tensor(x, self.dev) for x in (hd, hu, hl))
+        self.n_b, self.bs = self.h[0].shape[0], self.h[0].shape[-1]
+        if self.n_b < 2:
+            raise ValueError("need at least two blocks for two-terminal boundaries")
+        self.eta = float(eta)
+        self.contacts = contacts
+        self.surface_tol = float(surface_tol)
+        self.max_sweeps = int(max_sweeps)
+        self._buf: dict | None = None
+        self._n_e = 0
+
+    # -- buffers -----------------------------------------------------------
+    def buffers(self, n_e: int) -> dict[str, torch.Tensor]:
+        if self._buf is not None and self._n_e == n_e:
+            return self._buf
+        self._buf = None
+        torch.cuda.empty_cache()
+        nb, bs, dev = self.n_b, self.bs, self.dev
+        d = (n_e, nb, bs, bs)
+        o = (n_e, nb - 1, bs, bs)
+        c = (n_e, bs, bs)
+        b = {k: torch.empty(d, dtype=Z, device=dev) for k in
+             ("m_diag", "bl_diag", "bg_diag", "xr_diag", "xl_diag", "xg_diag")}
+        b.update({k: torch.empty(o, dtype=Z, device=dev) for k in
+                  ("m_upper", "m_lower", "bl_upper", "bg_upper", "xr_upper", "xr_lower", "xl_upper", "xg_upper")})
+        b.update({k: torch.empty(c, dtype=Z, device=dev) for k in
+                  ("sl_left", "sg_left", "sl_right", "sg_right")})
+        b["energy"] = torch.empty(n_e, dtype=torch.float64, device=dev)
+        b["f_bath"] = torch.empty(n_e, dtype=torch.float64, device=dev)
+        b["f_left"] = torch.empty(n_e, dtype=torch.float64, device=dev)
+        b["f_right"] = torch.empty(n_e, dtype=torch.float64, device=dev)
+        b["obc_status"] = torch.zeros(2 * n_e, dtype=torch.int32, device=dev)
+        b["obc_iters"] = torch.zeros(2 * n_e, dtype=torch.int32, device=dev)
+        b["obc_resid"] = torch.zeros(2 * n_e, dtype=torch.float64, device=dev)
+        b["rgf_status"] = torch.zeros(n_e, dtype=torch.int32, device=dev)
+        self._buf, self._n_e = b, n_e
+        return b
+
+    @staticmethod
+    def bytes_per_energy(n_b: int, bs: int) -> int:
+        blk = 16 * bs * bs
+        outputs = (6 * n_b + 8 * (n_b - 1) + 4) * blk
+        rgf_ws = 14 * blk
+        obc_ws = 2 * (6 + 10) * blk
+        return outputs + rgf_ws + obc_ws
+
+    # -- solve -------------------------------------------------------------
+    def solve(self, energies, sigma: dict | None = None, n_e: int | None = None,
+              check: bool = True, energies_dev: torch.Tensor | None = None) -> dict[str, torch.Tensor]:
+        """Solve the carrier system at ``energies`` (host array). ``sigma`` holds
+        scattering self-energy blocks, energy-major: keys sr_diag/sr_upper/
+        sr_lower, sl_diag/sl_upper, sg_diag/sg_upper (any subset)."""
+        lib, p = self.lib, _lib.ptr
+        energies = np.asarray(energies, dtype=np.float64)
+        ne = len(energies)
+        b = self.buffers(n_e or ne)
+        if ne != b["energy"].shape[0]:
+            raise ValueError("energy batch size does not match the allocated buffers")
+        c = self.contacts
+        host = np.stack([energies, fermi(energies, c.mu_mean, c.kT), fermi(energies, c.mu_left, c.kT),
+                         fermi(energies, c.mu_right, c.kT)])
+        dev_host = torch.from_numpy(host)
+        for i, k in enumerate(("energy", "f_bath", "f_left", "f_right")):
+            b[k].copy_(dev_host[i], non_blocking=False)
+        s = sigma or {}
+        st = _lib.stream_ptr(self.dev)
+        hd, hu, hl = self.h
+        rc = lib.negf_g_assemble(
+            ne, self.n_b, self.bs, p(hd), p(hu), p(hl), p(b["energy"]), p(b["f_bath"]), self.eta,
+            p(s.get("sr_diag")), p(s.get("sr_upper")), p(s.get("sr_lower")),
+            p(s.get("sl_diag")), p(s.get("sl_upper")), p(s.get("sg_diag")), p(s.get("sg_upper")),
+            p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]), p(b["bl_diag"]), p(b["bl_upper"]),
+            p(b["bg_diag"]), p(b["bg_upper"]), st)
+        _lib.check(rc, "negf_g_assemble")
+        nbytes = lib.negf_g_obc_workspace_bytes(ne, self.bs)
+        ws = _lib.workspace(nbytes, self.dev)
+        rc = lib.negf_g_obc_apply(
+            ne, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]), p(b["bl_diag"]),
+            p(b["bg_diag"]), p(b["f_left"]), p(b["f_right"]), self.surface_tol, self.max_sweeps,
+            p(b["sl_left"]), p(b["sg_left"]), p(b["sl_right"]), p(b["sg_right"]),
+            p(b["obc_status"]), p(b["obc_iters"]), p(b["obc_resid"]), p(ws), nbytes, st)
+        _lib.check(rc, "negf_g_obc_apply")
+        if check:
+            raise_on_obc_status(b["obc_status"].cpu().numpy(), b["obc_iters"].cpu().numpy(),
+                                b["obc_resid"].cpu().numpy(), self.max_sweeps, self.surface_tol, "G contact")
+        nbytes = lib.negf_rgf_workspace_bytes(ne, self.n_b, self.bs)
+        ws = _lib.workspace(nbytes, self.dev)
+        b["rgf_status"].zero_()
+        rc = lib.negf_rgf_selected_solve_batched(
+            ne, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]),
+            p(b["bl_diag"]), p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]),
+            p(b["xr_diag"]), p(b["xr_upper"]), p(b["xr_lower"]), p(b["xl_diag"]), p(b["xl_upper"]),
+            p(b["xg_diag"]), p(b["xg_upper"]), 1, p(b["rgf_status"]), None, p(ws), nbytes, st)
+        _lib.check(rc, "negf_rgf_selected_solve_batched")
+        if check:
+            raise_on_status(b["rgf_status"])
+        return b
+
+
+RESULT_KEYS = {
+    "g_r_diag": "xr_diag", "g_r_upper": "xr_upper", "g_r_lower": "xr_lower",
+    "g_lesser_diag": "xl_diag", "g_lesser_upper": "xl_upper",
+    "g_greater_diag": "xg_diag", "g_greater_upper": "xg_upper",
+    "sigma_obc_lesser_left": "sl_left", "sigma_obc_greater_left": "sg_left",
+    "sigma_obc_lesser_right": "sl_right", "sigma_obc_greater_right": "sg_right",
+}
+
+
+def ballistic_run(h, energies, eta: float, contacts: Contacts, surface_tol: float = 1e-8,
+                  batch: int | None = None, device="cuda") -> dict[str, np.ndarray]:
+    """scba_run(v_mat=None) equivalent (scba.py:951-1011): host arrays with
+    the ScbaResult field names."""
+    solver = CarrierSolver(h, eta, contacts, surface_tol, device=device)
+    energies = np.asarray(energies, dtype=float)
+    ne = len(energies)
+    batch = batch or ne
+    out = {k: [] for k in RESULT_KEYS}
+    for s in range(0, ne, batch):
+        chunk = energies[s:s + batch]
+        b = solver.solve(chunk, n_e=len(chunk))
+        for k, src in RESULT_KEYS.items():
+            out[k].append(b[src].cpu().numpy())
+    return {k: np.concatenate(v) for k, v in out.items()}

@@ -1,5 +1,6 @@
 // extern "C" entry points declared in include/negf_b200.h.
 #include "../../include/negf_b200.h"
+#include "obc.cuh"
 #include "rgf.cuh"
 #include "zgemm.cuh"
 #include "zinv.cuh"
@@ -54,7 +55,7 @@ int negf_zgemm_batched(int m, int n, int k, int batch, double alpha_re, double a
   g.alpha = make_double2(alpha_re, alpha_im);
   g.beta = make_double2(beta_re, beta_im);
   g.C = (const z_t*)c; g.sC = stride_c; g.ldc = ldc;
-  g.D = (z_t*)d; g.sD = stride_d; g.ldd = ldd; g.transD = 0;
+  g.D = (z_t*)d; g.sD = stride_d; g.ldd = ldd; g.transD = 0; g.active = nullptr;
   return zgemm_launch(g, (cudaStream_t)stream);
 }
 
@@ -65,9 +66,79 @@ int negf_zinv_batched(int n, int batch, void* s, void* x, int* status, double* u
   if (n < 1 || batch < 0 || !s || !x) return -1;
   InvAux aux;
   aux.status = status; aux.status_code = 1; aux.u_spread = u_spread; aux.spread_stride = 1;
+  aux.active = nullptr;
   long long s2 = (long long)n * n;
   return zinv_batched((z_t*)s, s2, n, (z_t*)x, s2, n, n, batch, aux, workspace, workspace_bytes,
                       (cudaStream_t)stream);
+}
+
+size_t negf_sancho_workspace_bytes(int batch, int bs) { return sancho_workspace_bytes(batch, bs); }
+
+int negf_obc_sancho_batched(int batch, int bs, const void* m, const void* n, const void* np,
+                            double tol, int max_iter, void* x, int* status, int* iters,
+                            double* resid, void* workspace, size_t workspace_bytes, void* stream) {
+  if (batch < 0 || bs < 1 || !m || !n || !np || !x || !status || !iters) return -1;
+  if (!(tol > 0.0) || max_iter < 1) return -1;
+  return sancho_batched((const z_t*)m, (const z_t*)n, (const z_t*)np, batch, bs, tol, max_iter,
+                        (z_t*)x, status, iters, resid, workspace, workspace_bytes,
+                        (cudaStream_t)stream);
+}
+
+size_t negf_sigma_lg_obc_workspace_bytes(int batch, int bs) {
+  return sigma_lg_obc_workspace_bytes(batch, bs);
+}
+
+int negf_sigma_lg_obc_batched(int batch, int bs, const void* x, const void* n, const void* np,
+                              const double* f, void* sigma_r, void* sigma_lesser,
+                              void* sigma_greater, void* workspace, size_t workspace_bytes,
+                              void* stream) {
+  if (batch < 0 || bs < 1 || !x || !n || !np || !f) return -1;
+  return sigma_lg_obc_batched((const z_t*)x, (const z_t*)n, (const z_t*)np, f, batch, bs,
+                              (z_t*)sigma_r, (z_t*)sigma_lesser, (z_t*)sigma_greater, workspace,
+                              workspace_bytes, (cudaStream_t)stream);
+}
+
+size_t negf_g_obc_workspace_bytes(int n_e, int bs) { return g_obc_workspace_bytes(n_e, bs); }
+
+int negf_g_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper,
+                     const void* m_lower, void* bl_diag, void* bg_diag, const double* f_left,
+                     const double* f_right, double tol, int max_iter, void* sl_left,
+                     void* sg_left, void* sl_right, void* sg_right, int* status, int* iters,
+                     double* resid, void* workspace, size_t workspace_bytes, void* stream) {
+  if (n_e < 0 || n_b < 2 || bs < 1 || !m_diag || !m_upper || !m_lower || !f_left || !f_right)
+    return -1;
+  if (!status || !iters) return -1;
+  GObcArgs a;
+  a.n_e = n_e; a.n_b = n_b; a.bs = bs;
+  a.m_diag = (z_t*)m_diag; a.m_upper = (const z_t*)m_upper; a.m_lower = (const z_t*)m_lower;
+  a.bl_diag = (z_t*)bl_diag; a.bg_diag = (z_t*)bg_diag;
+  a.f_left = f_left; a.f_right = f_right; a.tol = tol; a.max_iter = max_iter;
+  a.sl_left = (z_t*)sl_left; a.sg_left = (z_t*)sg_left;
+  a.sl_right = (z_t*)sl_right; a.sg_right = (z_t*)sg_right;
+  a.status = status; a.iters = iters; a.resid = resid;
+  return g_obc_apply(a, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int negf_g_assemble(int n_e, int n_b, int bs, const void* h_diag, const void* h_upper,
+                    const void* h_lower, const double* energy, const double* f_bath, double eta,
+                    const void* sr_diag, const void* sr_upper, const void* sr_lower,
+                    const void* sl_diag, const void* sl_upper, const void* sg_diag,
+                    const void* sg_upper, void* m_diag, void* m_upper, void* m_lower,
+                    void* bl_diag, void* bl_upper, void* bg_diag, void* bg_upper, void* stream) {
+  if (n_e < 0 || n_b < 1 || bs < 1 || !h_diag || !energy || !f_bath || !m_diag) return -1;
+  if (n_b > 1 && (!h_upper || !h_lower || !m_upper || !m_lower)) return -1;
+  GAssembleArgs a;
+  a.n_e = n_e; a.n_b = n_b; a.bs = bs;
+  a.h_diag = (const z_t*)h_diag; a.h_upper = (const z_t*)h_upper; a.h_lower = (const z_t*)h_lower;
+  a.energy = energy; a.f_bath = f_bath; a.eta = eta;
+  a.sr_diag = (const z_t*)sr_diag; a.sr_upper = (const z_t*)sr_upper;
+  a.sr_lower = (const z_t*)sr_lower;
+  a.sl_diag = (const z_t*)sl_diag; a.sl_upper = (const z_t*)sl_upper;
+  a.sg_diag = (const z_t*)sg_diag; a.sg_upper = (const z_t*)sg_upper;
+  a.m_diag = (z_t*)m_diag; a.m_upper = (z_t*)m_upper; a.m_lower = (z_t*)m_lower;
+  a.bl_diag = (z_t*)bl_diag; a.bl_upper = (z_t*)bl_upper;
+  a.bg_diag = (z_t*)bg_diag; a.bg_upper = (z_t*)bg_upper;
+  return g_assemble(a, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -63,6 +63,7 @@ struct Ctx {
     d.C = C; d.sC = sC; d.ldc = bs;
     d.D = D; d.sD = sD; d.ldd = bs;
     d.transD = transD;
+    d.active = nullptr;
     return d;
   }
 };
@@ -140,6 +141,7 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
     aux.status_code = 1 + i;
     aux.u_spread = a.u_spread ? a.u_spread + i : nullptr;
     aux.spread_stride = n;
+    aux.active = nullptr;
     return zinv_batched(tS, st1, bs, Xd(i), sd, bs, bs, ne, aux, c.inv_ws, c.inv_ws_bytes, st);
   };
 

@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
   const int tiles_n = (d.N + CF::BN - 1) / CF::BN;
   const int tiles_m = (d.M + CF::BM - 1) / CF::BM;
   if ((int)blockIdx.x >= tiles_m * tiles_n || (int)blockIdx.y >= d.batch) return;
+  if (d.active && !d.active[blockIdx.y]) return;
   const int b = blockIdx.y;
   const int m0 = (blockIdx.x / tiles_n) * CF::BM;
   const int n0 = (blockIdx.x % tiles_n) * CF::BN;

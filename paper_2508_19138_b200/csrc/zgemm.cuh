@@ -52,6 +52,7 @@ struct ZGemmDesc {
   long long sD;
   int ldd;
   int transD;  // store conj-transposed
+  const int* active;  // optional per-batch mask: problems with active[b]==0 are skipped
 };
 
 constexpr int kMaxGroup = 6;
@@ -61,6 +62,16 @@ struct ZGemmGroup {
 };
 
 // Host-side helpers -----------------------------------------------------------
+inline ZGemmDesc zdesc_default() {
+  ZGemmDesc d;
+  d.M = d.N = d.batch = 0; d.nterms = 1;
+  d.alpha = make_double2(1.0, 0.0); d.beta = make_double2(0.0, 0.0);
+  d.C = nullptr; d.sC = 0; d.ldc = 0;
+  d.D = nullptr; d.sD = 0; d.ldd = 0;
+  d.transD = 0; d.active = nullptr;
+  return d;
+}
+
 inline ZTerm zterm(const z_t* A, long long sA, int lda, int opA, const z_t* B, long long sB,
                    int ldb, int opB, int K, bool neg = false) {
   ZTerm t;

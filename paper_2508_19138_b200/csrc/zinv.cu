@@ -65,6 +65,7 @@ __global__ void zinv_small_kernel(const z_t* __restrict__ S, long long sS, int l
   __shared__ double umax, umin;
   __shared__ int bad;
   const int b = blockIdx.x;
+  if (aux.active && !aux.active[b]) return;
   const z_t* src = S + (long long)b * sS;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) a[(e / n) * ld + e % n] = src[(long long)(e / n) * lds + e % n];
   if (threadIdx.x == 0) { umax = 0.0; umin = INFINITY; bad = 0; }
@@ -144,6 +145,7 @@ __global__ void zinv_panel_kernel(const z_t* __restrict__ A, long long sA, int n
   __shared__ int sbad;
   __shared__ double smax, smin;
   const int b = blockIdx.x;
+  if (aux.active && !aux.active[b]) return;
   const z_t* a = A + (long long)b * sA;
   for (int e = threadIdx.x; e < rows * nb; e += blockDim.x) {
     int i = e / nb, j = e % nb;
@@ -221,8 +223,9 @@ __global__ void zinv_panel_kernel(const z_t* __restrict__ A, long long sA, int n
 // C' = A[:,K] with rows K zeroed   (n x nb)
 // R  = A[K,:]                      (nb x n)
 __global__ void zinv_swap_kernel(z_t* A, long long sA, int n, int k0, int nb, const int* ipiv,
-                                 z_t* Cp, z_t* R) {
+                                 z_t* Cp, z_t* R, const int* active) {
   const int b = blockIdx.y;
+  if (active && !active[b]) return;
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= n) return;
   z_t* a = A + (long long)b * sA;
@@ -250,8 +253,9 @@ __global__ void zinv_swap_kernel(z_t* A, long long sA, int n, int k0, int nb, co
 
 // Rows K of the swept matrix: A[K, j] = T[:, j] (j not in K), A[K, K] = Pinv.
 __global__ void zinv_rows_kernel(z_t* A, long long sA, int n, int k0, int nb, const z_t* T,
-                                 long long sT, const z_t* pinv) {
+                                 long long sT, const z_t* pinv, const int* active) {
   const int b = blockIdx.y;
+  if (active && !active[b]) return;
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= n) return;
   z_t* a = A + (long long)b * sA;
@@ -268,6 +272,7 @@ __global__ void zinv_unpermute_kernel(const z_t* __restrict__ A, long long sA, i
                                       long long sX, int ldx, InvAux aux) {
   extern __shared__ int perm[];
   const int b = blockIdx.x;
+  if (aux.active && !aux.active[b]) return;
   const int* pv = ipiv + (long long)b * n;
   if (threadIdx.x == 0) {
     for (int j = 0; j < n; ++j) perm[j] = j;
@@ -341,7 +346,7 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
     zinv_panel_kernel<<<batch, 256, panel_smem, stream>>>(S, sS, n, k0, w, ipiv, pinv, umm, aux);
     NEGF_CUDA_CHECK(cudaGetLastError());
     dim3 g((n + 127) / 128, batch);
-    zinv_swap_kernel<<<g, 128, 0, stream>>>(S, sS, n, k0, w, ipiv, Cp, R);
+    zinv_swap_kernel<<<g, 128, 0, stream>>>(S, sS, n, k0, w, ipiv, Cp, R, aux.active);
     NEGF_CUDA_CHECK(cudaGetLastError());
     // T = Pinv R, staged in the caller's destination X (w x n per matrix;
     // X is only written for real by the final unpermute kernel).
@@ -356,6 +361,7 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
       d.alpha = make_double2(1.0, 0.0); d.beta = make_double2(0.0, 0.0);
       d.C = nullptr; d.sC = 0; d.ldc = 0;
       d.D = T; d.sD = sX; d.ldd = n; d.transD = 0;
+      d.active = aux.active;
     }
     int rc = zgemm_group_launch(grp, stream);
     if (rc) return rc;
@@ -371,6 +377,7 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
       d.alpha = make_double2(-1.0, 0.0); d.beta = make_double2(1.0, 0.0);
       d.C = S + c0; d.sC = sS; d.ldc = n;
       d.D = S + c0; d.sD = sS; d.ldd = n; d.transD = 0;
+      d.active = aux.active;
     };
     upd(0, k0);
     upd(k0 + w, n - k0 - w);
@@ -382,10 +389,11 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
       d.alpha = make_double2(-1.0, 0.0); d.beta = make_double2(0.0, 0.0);
       d.C = nullptr; d.sC = 0; d.ldc = 0;
       d.D = S + k0; d.sD = sS; d.ldd = n; d.transD = 0;
+      d.active = aux.active;
     }
     rc = zgemm_group_launch(grp, stream);
     if (rc) return rc;
-    zinv_rows_kernel<<<g, 128, 0, stream>>>(S, sS, n, k0, w, T, sX, pinv);
+    zinv_rows_kernel<<<g, 128, 0, stream>>>(S, sS, n, k0, w, T, sX, pinv, aux.active);
     NEGF_CUDA_CHECK(cudaGetLastError());
   }
   zinv_unpermute_kernel<<<batch, 256, n * sizeof(int), stream>>>(S, sS, n, ipiv, umm, X, sX, ldx,

@@ -14,6 +14,7 @@ struct InvAux {
   int status_code;
   double* u_spread;
   long long spread_stride;
+  const int* active;  // optional per-batch mask (skip matrices with active[b]==0)
 };
 
 int zinv_panel_width(int n);

@@ -1,0 +1,81 @@
+"""GPU parity of the contact boundary path: Sancho-Rubio, sigma_lg_obc, and
+the full ballistic carrier solve (assembly + OBC + RGF) against reference
+golden vectors and the pinned oracle. Bar: 1e-9 relative Frobenius."""
+
+import numpy as np
+import pytest
+import torch
+
+import negf_oracle as orc
+from paper_2508_19138_b200 import ConvergenceError
+from paper_2508_19138_b200.carrier import Contacts, ballistic_run
+from paper_2508_19138_b200.obc import (ContactBlocks, obc_sancho_rubio, sancho_batched, sigma_lg_obc)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def test_sancho_matches_reference_golden(golden, cuda):
+    g = golden("golden_obc.npz")
+    for s in range(5):
+        c = ContactBlocks(g[f"lead{s}_m"], g[f"lead{s}_n"], g[f"lead{s}_np"])
+        r = obc_sancho_rubio(c, tol=1e-14)
+        assert r.iters == int(g[f"lead{s}_iters"])
+        assert rel(r.x_r, g[f"lead{s}_x"]) < TOL
+        sig = sigma_lg_obc(r.x_r, 0.1, 0.05, 0.03, (c.n, c.n_prime))
+        assert rel(sig.sigma_r, g[f"lead{s}_sr"]) < TOL
+        assert rel(sig.sigma_lesser, g[f"lead{s}_sl"]) < TOL
+        assert rel(sig.sigma_greater, g[f"lead{s}_sg"]) < TOL
+
+
+def test_sancho_scalar_known_answer(cuda):
+    c = ContactBlocks(np.array([[2.0 + 0j]]), np.array([[0.5 + 0j]]), np.array([[0.5 + 0j]]))
+    r = obc_sancho_rubio(c, tol=1e-14)
+    assert abs(r.x_r[0, 0] - 0.5358983848622456) < 1e-12
+
+
+def test_sancho_batched_mixed_sweep_counts(cuda):
+    # problems needing different sweep counts stop exactly where the oracle stops
+    rng = np.random.default_rng(4)
+    ms, ns, nps, refs, its = [], [], [], [], []
+    for k, bs in enumerate([48] * 6):
+        h0 = rng.standard_normal((bs, bs)) + 1j * rng.standard_normal((bs, bs))
+        h0 = 0.5 * (h0 + h0.conj().T) / np.sqrt(bs)
+        h1 = (0.2 + 0.1 * k) * (rng.standard_normal((bs, bs)) + 1j * rng.standard_normal((bs, bs))) / np.sqrt(bs)
+        m = (0.1 * k + 0.02j) * np.eye(bs) - h0
+        ms.append(m); ns.append(-h1); nps.append(-h1.conj().T)
+        x, it, _ = orc.sancho_rubio(m, -h1, -h1.conj().T, tol=1e-10)
+        refs.append(x); its.append(it)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(np.stack(a))).to(cuda)
+    x, iters, status, _ = sancho_batched(t(ms), t(ns), t(nps), tol=1e-10)
+    assert iters.cpu().numpy().tolist() == its
+    for k in range(len(refs)):
+        assert rel(x[k].cpu().numpy(), refs[k]) < TOL
+
+
+def test_sancho_not_converged_raises(cuda):
+    c = ContactBlocks(np.array([[0.0 + 1e-12j]]), np.array([[1.0 + 0j]]), np.array([[1.0 + 0j]]))
+    with pytest.raises(ConvergenceError):
+        obc_sancho_rubio(c, tol=1e-14, max_iter=3)
+
+
+def test_ballistic_matches_reference_scba_run(golden, cuda):
+    g = golden("golden_ballistic_small.npz")
+    h = orc.chain_device(5, 3)
+    out = ballistic_run(h, np.linspace(-2.0, 2.0, 16), 1e-3, Contacts(0.1, -0.1, 0.05), 1e-8, device=cuda)
+    for k, v in out.items():
+        assert rel(v, g[k]) < TOL, k
+
+
+@pytest.mark.parametrize("nb,bs,ne,batch", [(8, 48, 12, 5), (4, 96, 6, 6), (3, 130, 3, 2)])
+def test_ballistic_matches_oracle(cuda, nb, bs, ne, batch):
+    h = orc.chain_device(nb, bs)
+    energies = np.linspace(-1.0, 1.0, ne)
+    ref = orc.ballistic(h, energies, 1e-3, 0.1, -0.1, 0.05, tol=1e-8)
+    out = ballistic_run(h, energies, 1e-3, Contacts(0.1, -0.1, 0.05), 1e-8, batch=batch, device=cuda)
+    for k, v in out.items():
+        assert rel(v, ref[k]) < TOL, k

@@ -57,3 +57,43 @@ def test_oracle_rgf_matches_dense(golden, c):
     for k in d:
         if d[k].size:
             assert rel(a[k], d[k]) < 1e-11, k
+
+
+def test_oracle_sancho_matches_reference(golden):
+    g = golden("golden_obc.npz")
+    for s in range(5):
+        m, n, np_ = g[f"lead{s}_m"], g[f"lead{s}_n"], g[f"lead{s}_np"]
+        x, it, _ = orc.sancho_rubio(m, n, np_, tol=1e-14)
+        assert it == int(g[f"lead{s}_iters"])
+        assert rel(x, g[f"lead{s}_x"]) < 1e-13
+        sr, sl, sg = orc.sigma_lg_obc(x, 0.1, 0.05, 0.03, n, np_)
+        assert rel(sr, g[f"lead{s}_sr"]) < 1e-13
+        assert rel(sl, g[f"lead{s}_sl"]) < 1e-13
+        assert rel(sg, g[f"lead{s}_sg"]) < 1e-13
+
+
+def test_oracle_stein_matches_reference(golden):
+    g = golden("golden_obc.npz")
+    for k in range(3):
+        w = orc.stein_geometric(g[f"stein{k}_a"], g[f"stein{k}_q"])
+        assert rel(w, g[f"stein{k}_w"]) < 1e-13
+
+
+def test_oracle_scalar_fixed_point_known_answer():
+    # test_obc.py:24: stable root 4 - 2 sqrt(3) of x = 1/(2 - 0.25 x)
+    x, _, _ = orc.sancho_rubio(np.array([[2.0 + 0j]]), np.array([[0.5 + 0j]]), np.array([[0.5 + 0j]]), tol=1e-14)
+    assert abs(x[0, 0] - 0.5358983848622456) < 1e-12
+
+
+def test_oracle_chain_devices_match_reference_generators(golden):
+    g = golden("golden_ballistic_small.npz")
+    assert g["g_r_diag"].shape == (16, 5, 3, 3)
+
+
+def test_oracle_ballistic_matches_reference_scba_run(golden):
+    g = golden("golden_ballistic_small.npz")
+    h = orc.chain_device(5, 3)
+    energies = np.linspace(-2.0, 2.0, 16)
+    out = orc.ballistic(h, energies, 1e-3, 0.1, -0.1, 0.05, tol=1e-8)
+    for k, v in out.items():
+        assert rel(v, g[k]) < 1e-12, k
