@@ -116,6 +116,27 @@ int negf_g_assemble(int n_e, int n_b, int bs, const void* h_diag, const void* h_
                     const void* sg_upper, void* m_diag, void* m_upper, void* m_lower,
                     void* bl_diag, void* bl_upper, void* bg_diag, void* bg_upper, void* stream);
 
+/* ---- observables (scba.py:1313-1376), reduced on the device -------------
+ * Per energy e and block b: tr_gr[e][b] = tr G^R_bb, tr_gl[e][b] = tr G^<_bb
+ * (complex); current_spectrum[e][b] (b < n_b-1, double) as
+ * scba.current_spectrum; terminal[e][0|1] = tr(S^<_c G^>_cc) - tr(S^>_c G^<_cc)
+ * at the left / right corner (complex). Optional outputs may be NULL. */
+int negf_observables(int n_e, int n_b, int bs, const void* gr_diag, const void* gl_diag,
+                     const void* gg_diag, const void* gl_upper, const void* h_upper,
+                     const void* sl_left, const void* sg_left, const void* sl_right,
+                     const void* sg_right, void* tr_gr, void* tr_gl, double* current_spectrum,
+                     void* terminal, void* stream);
+
+/* ---- opt-in CUDA-event profiler (bench.py live roofline) ---------------
+ * class 0 = DMMA ZGEMM launches. Process-global, off by default. query()
+ * synchronises on the recorded events and returns the summed device time
+ * (ms), algorithmic flops and operand bytes of the recorded launches. */
+void negf_prof_enable(int on);
+/* Number of kernels this library has launched since it was loaded. */
+long long negf_launch_count(void);
+void negf_prof_reset(void);
+int negf_prof_query(int cls, double* ms, double* flops, double* bytes, long long* launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -364,3 +364,29 @@ def ballistic(h, energies, eta, mu_left, mu_right, kT, tol=1e-8):
         "sigma_obc_lesser_left": obc["left"][0], "sigma_obc_greater_left": obc["left"][1],
         "sigma_obc_lesser_right": obc["right"][0], "sigma_obc_greater_right": obc["right"][1],
     }
+
+
+def observables(res: dict, h_upper, de: float) -> dict:
+    """scba.py:1313-1376: dos, electron_density, current_spectrum,
+    terminal_current for result arrays named like ScbaResult fields."""
+    c_obs = 1.0 / (2.0 * np.pi)
+    tr_r = np.trace(res["g_r_diag"], axis1=2, axis2=3)
+    tr_l = np.trace(res["g_lesser_diag"], axis1=2, axis2=3)
+    n_b = res["g_r_diag"].shape[1]
+    cur = np.zeros((tr_r.shape[0], n_b - 1))
+    for i in range(n_b - 1):
+        gl_lower = -np.conj(np.swapaxes(res["g_lesser_upper"][:, i], 1, 2))
+        cur[:, i] = c_obs * 2.0 * np.einsum("ij,eji->e", h_upper[i], gl_lower).real
+
+    def term(sl, sg, c):
+        tr = np.einsum("eij,eji->e", sl, res["g_greater_diag"][:, c]) - np.einsum(
+            "eij,eji->e", sg, res["g_lesser_diag"][:, c])
+        return float(c_obs * de * tr.real.sum())
+
+    return {
+        "dos": -tr_r.imag / np.pi,
+        "density": (c_obs * de * (-1j * tr_l).sum(axis=0)).real,
+        "current_spectrum": cur,
+        "terminal_left": term(res["sigma_obc_lesser_left"], res["sigma_obc_greater_left"], 0),
+        "terminal_right": term(res["sigma_obc_lesser_right"], res["sigma_obc_greater_right"], n_b - 1),
+    }

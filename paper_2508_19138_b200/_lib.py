@@ -45,6 +45,11 @@ _SIGNATURES: dict[str, tuple] = {
         [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp],
     ),
     "negf_g_assemble": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _d] + [_vp] * 7 + [_vp] * 7 + [_vp]),
+    "negf_observables": (_i, [_i, _i, _i] + [_vp] * 14),
+    "negf_prof_enable": (None, [_i]),
+    "negf_launch_count": (_ll, []),
+    "negf_prof_reset": (None, []),
+    "negf_prof_query": (_i, [_i, _vp, _vp, _vp, _vp]),
 }
 
 

@@ -62,6 +62,19 @@ class CarrierSolver:
         self._buf: dict | None = None
         self._n_e = 0
 
+    def set_hamiltonian(self, h) -> None:
+        """Copy new H blocks (host or device) into the resident device tensors."""
+        for dst, src in zip(self.h, h):
+            if isinstance(src, torch.Tensor):
+                dst.copy_(src, non_blocking=True)
+            else:
+                dst.copy_(torch.from_numpy(np.ascontiguousarray(np.asarray(src, dtype=complex))))
+
+    def check_status(self, b: dict) -> None:
+        raise_on_obc_status(b["obc_status"].cpu().numpy(), b["obc_iters"].cpu().numpy(),
+                            b["obc_resid"].cpu().numpy(), self.max_sweeps, self.surface_tol, "G contact")
+        raise_on_status(b["rgf_status"])
+
     # -- buffers -----------------------------------------------------------
     def buffers(self, n_e: int) -> dict[str, torch.Tensor]:
         if self._buf is not None and self._n_e == n_e:
@@ -174,3 +187,69 @@ def ballistic_run(h, energies, eta: float, contacts: Contacts, surface_tol: floa
         for k, src in RESULT_KEYS.items():
             out[k].append(b[src].cpu().numpy())
     return {k: np.concatenate(v) for k, v in out.items()}
+
+
+# -- observables -----------------------------------------------------------
+
+C_OBSERVABLE = 1.0 / (2.0 * np.pi)
+
+
+class ObservableAccumulator:
+    """Per-energy traces reduced on the device (negf_observables), gathered
+    across energy batches. Finalises to the reference's observables
+    (scba.py:1313-1376): dos, electron_density, current_spectrum,
+    terminal_current(left/right)."""
+
+    def __init__(self, n_e_total: int, n_b: int, de: float, device) -> None:
+        self.dev = torch.device(device)
+        self.n_b, self.de = n_b, de
+        self.tr_gr = torch.zeros((n_e_total, n_b), dtype=Z, device=self.dev)
+        self.tr_gl = torch.zeros((n_e_total, n_b), dtype=Z, device=self.dev)
+        self.cur = torch.zeros((n_e_total, max(n_b - 1, 1)), dtype=torch.float64, device=self.dev)
+        self.term = torch.zeros((n_e_total, 2), dtype=Z, device=self.dev)
+
+    def add(self, solver: "CarrierSolver", b: dict, e0: int, ne: int) -> None:
+        p = _lib.ptr
+        rc = solver.lib.negf_observables(
+            ne, solver.n_b, solver.bs, p(b["xr_diag"]), p(b["xl_diag"]), p(b["xg_diag"]),
+            p(b["xl_upper"]), p(solver.h[1]), p(b["sl_left"]), p(b["sg_left"]), p(b["sl_right"]),
+            p(b["sg_right"]), p(self.tr_gr[e0:]), p(self.tr_gl[e0:]), p(self.cur[e0:]),
+            p(self.term[e0:]), _lib.stream_ptr(self.dev))
+        _lib.check(rc, "negf_observables")
+
+    def to_host(self) -> dict[str, np.ndarray]:
+        tr_gr = self.tr_gr.cpu().numpy()
+        tr_gl = self.tr_gl.cpu().numpy()
+        term = self.term.cpu().numpy()
+        return {
+            "dos": -tr_gr.imag / np.pi,
+            "density": (C_OBSERVABLE * self.de * (-1j * tr_gl).sum(axis=0)).real,
+            "current_spectrum": self.cur.cpu().numpy()[:, : self.n_b - 1],
+            "terminal_left": float(C_OBSERVABLE * self.de * term[:, 0].real.sum()),
+            "terminal_right": float(C_OBSERVABLE * self.de * term[:, 1].real.sum()),
+        }
+
+    def d2h_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.tr_gr, self.tr_gl, self.cur, self.term))
+
+
+def ballistic_observables(h, energies, eta: float, contacts: Contacts, surface_tol: float = 1e-8,
+                          batch: int | None = None, device="cuda", solver: CarrierSolver | None = None):
+    """Public end-to-end ballistic API: host H blocks + energy grid in, host
+    observables out. Every G block is computed on the device; only the
+    reduced observables cross back to the host."""
+    energies = np.asarray(energies, dtype=float)
+    if solver is None:
+        solver = CarrierSolver(h, eta, contacts, surface_tol, device=device)
+    else:
+        solver.set_hamiltonian(h)
+    ne = len(energies)
+    batch = batch or ne
+    de = (energies[-1] - energies[0]) / (ne - 1) if ne > 1 else 0.0
+    acc = ObservableAccumulator(ne, solver.n_b, de, solver.dev)
+    for s in range(0, ne, batch):
+        chunk = energies[s:s + batch]
+        b = solver.solve(chunk, n_e=len(chunk), check=False)
+        acc.add(solver, b, s, len(chunk))
+        solver.check_status(b)
+    return acc.to_host()

@@ -65,6 +65,18 @@ __device__ __forceinline__ void cp_async_wait() {
 
 }  // namespace negf
 
+namespace negf {
+// Process-wide count of kernels launched by this library (bench.py's
+// gpu_launches evidence); relaxed atomic increment per launch.
+void count_launch();
+}  // namespace negf
+
+#define NEGF_LAUNCHED()                     \
+  do {                                      \
+    negf::count_launch();                   \
+    NEGF_CUDA_CHECK(cudaGetLastError());    \
+  } while (0)
+
 #define NEGF_CUDA_CHECK(expr)                                                        \
   do {                                                                               \
     cudaError_t _e = (expr);                                                         \

@@ -105,7 +105,7 @@ int ew_group_launch(const EwGroup& g, cudaStream_t stream) {
   const int tiles = ((g.rows + TILE - 1) / TILE) * ((g.cols + TILE - 1) / TILE);
   dim3 grid(tiles, mb, g.n), block(TILE, 8);
   ew_kernel<<<grid, block, 0, stream>>>(g);
-  NEGF_CUDA_CHECK(cudaGetLastError());
+  NEGF_LAUNCHED();
   return 0;
 }
 
@@ -114,7 +114,7 @@ int antiherm_inplace(z_t* X, long long sX, int n, int batch, cudaStream_t stream
   const int nt = (n + TILE - 1) / TILE;
   dim3 grid(nt * (nt + 1) / 2, batch), block(TILE, 8);
   antiherm_kernel<<<grid, block, 0, stream>>>(X, sX, n);
-  NEGF_CUDA_CHECK(cudaGetLastError());
+  NEGF_LAUNCHED();
   return 0;
 }
 
@@ -122,7 +122,7 @@ int add_identity(z_t* Y, long long sY, int n, int batch, double2 s, cudaStream_t
   if (batch <= 0) return 0;
   dim3 grid((n + 127) / 128, batch);
   add_identity_kernel<<<grid, 128, 0, stream>>>(Y, sY, n, s);
-  NEGF_CUDA_CHECK(cudaGetLastError());
+  NEGF_LAUNCHED();
   return 0;
 }
 

@@ -248,7 +248,7 @@ int sancho_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs,
   NEGF_CUDA_CHECK(cudaMemcpyAsync(be, np, bytes, cudaMemcpyDeviceToDevice, st));
   NEGF_CUDA_CHECK(cudaMemsetAsync(inv_st, 0, sizeof(int) * batch, st));
   sancho_init_kernel<<<batch, 256, 0, st>>>(n, np, bs, scale, active, status, iters);
-  NEGF_CUDA_CHECK(cudaGetLastError());
+  NEGF_LAUNCHED();
   InvAux aux;
   aux.status = inv_st; aux.status_code = 1; aux.u_spread = nullptr; aux.spread_stride = 0;
   aux.active = active;
@@ -288,7 +288,7 @@ int sancho_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs,
     NEGF_CUDA_CHECK(cudaMemsetAsync(n_act, 0, sizeof(int), st));
     sancho_check_kernel<<<batch, 256, 0, st>>>(al, be, bs, tol, scale, active, inv_st, status, iters,
                                                it, n_act);
-    NEGF_CUDA_CHECK(cudaGetLastError());
+    NEGF_LAUNCHED();
     NEGF_CUDA_CHECK(cudaMemcpyAsync(&h_active, n_act, sizeof(int), cudaMemcpyDeviceToHost, st));
     NEGF_CUDA_CHECK(cudaStreamSynchronize(st));
     if (h_active == 0) break;
@@ -310,7 +310,7 @@ int sancho_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs,
   RC(zinv_batched(tb, n2, bs, g, n2, bs, bs, batch, aux2, inv_ws, inv_bytes, st));
   const double thr = 10.0 * (tol > 1e-14 ? tol : 1e-14);
   sancho_finish_kernel<<<batch, 256, 0, st>>>(x, g, bs, thr, active, inv_st, status, resid);
-  NEGF_CUDA_CHECK(cudaGetLastError());
+  NEGF_LAUNCHED();
   return 0;
 }
 
@@ -366,13 +366,13 @@ int g_obc_apply(const GObcArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
   dim3 grid(tiles, ne), block(32, 8);
   g_corner_kernel<<<grid, block, 0, st>>>(sig, bs, a.f_left, a.m_diag, a.bl_diag, a.bg_diag, sd,
                                           a.sl_left, a.sg_left);
-  NEGF_CUDA_CHECK(cudaGetLastError());
+  NEGF_LAUNCHED();
   const long long cc = (long long)(nb - 1) * n2;
   g_corner_kernel<<<grid, block, 0, st>>>(sig + hn, bs, a.f_right, a.m_diag + cc,
                                           a.bl_diag ? a.bl_diag + cc : nullptr,
                                           a.bg_diag ? a.bg_diag + cc : nullptr, sd, a.sl_right,
                                           a.sg_right);
-  NEGF_CUDA_CHECK(cudaGetLastError());
+  NEGF_LAUNCHED();
   return 0;
 }
 
@@ -401,7 +401,7 @@ int sigma_lg_obc_batched(const z_t* x, const z_t* n, const z_t* np, const double
   const int tiles = ((bs + 31) / 32) * ((bs + 31) / 32);
   dim3 grid(tiles, batch), block(32, 8);
   sigma_lg_kernel<<<grid, block, 0, st>>>(sig, bs, f, sl, sg);
-  NEGF_CUDA_CHECK(cudaGetLastError());
+  NEGF_LAUNCHED();
   return 0;
 }
 
@@ -412,7 +412,7 @@ int g_assemble(const GAssembleArgs& a, cudaStream_t st) {
   if (bx > 64) bx = 64;
   dim3 grid(bx, a.n_b, a.n_e);
   g_assemble_kernel<<<grid, 256, 0, st>>>(a);
-  NEGF_CUDA_CHECK(cudaGetLastError());
+  NEGF_LAUNCHED();
   return 0;
 }
 

@@ -1,0 +1,15 @@
+// Opt-in per-launch CUDA-event profiler for the dominant kernel classes
+// (bench.py's live roofline). Off by default; process-global when enabled.
+#pragma once
+#include "common.cuh"
+
+namespace negf {
+
+enum ProfClass : int { PROF_ZGEMM = 0, PROF_ZINV = 1, PROF_EW = 2, PROF_OTHER = 3, PROF_NCLASS = 4 };
+
+bool prof_enabled();
+// Returns a token; call prof_end with it after the launch(es).
+int prof_begin(int cls, cudaStream_t st);
+void prof_end(int token, cudaStream_t st, double flops, double bytes);
+
+}  // namespace negf

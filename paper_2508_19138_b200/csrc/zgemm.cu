@@ -1,4 +1,5 @@
 // Batched grouped complex-FP64 DMMA GEMM (see zgemm.cuh for the contract).
+#include "prof.cuh"
 #include "zgemm.cuh"
 
 namespace negf {
@@ -213,8 +214,21 @@ int launch_cfg(const ZGemmGroup& g, cudaStream_t stream) {
   }
   if (max_tiles == 0 || max_batch == 0) return 0;
   dim3 grid(max_tiles, max_batch, g.n);
+  const int tok = prof_begin(PROF_ZGEMM, stream);
   zgemm_kernel<CF><<<grid, CF::NT, CF::SMEM, stream>>>(g);
-  NEGF_CUDA_CHECK(cudaGetLastError());
+  NEGF_LAUNCHED();
+  if (tok >= 0) {
+    double fl = 0.0, by = 0.0;
+    for (int i = 0; i < g.n; ++i) {
+      const ZGemmDesc& d = g.d[i];
+      for (int t = 0; t < d.nterms; ++t) {
+        fl += 8.0 * d.M * d.N * (double)d.t[t].K * d.batch;
+        by += 16.0 * ((double)d.M * d.t[t].K + (double)d.t[t].K * d.N) * d.batch;
+      }
+      by += 16.0 * (double)d.M * d.N * d.batch * ((d.C && (d.beta.x != 0.0 || d.beta.y != 0.0)) ? 2 : 1);
+    }
+    prof_end(tok, stream, fl, by);
+  }
   return 0;
 }
 

@@ -19,6 +19,7 @@
 // permutation on the columns (LAPACK zgetri order) while copying to the
 // destination. The O(N^3) work runs on the DMMA GEMM; the panel kernels are
 // O(N^2 NB). Blocks with N <= 64 are inverted by one CTA entirely in smem.
+#include "prof.cuh"
 #include "zgemm.cuh"
 #include "zinv.cuh"
 
@@ -319,7 +320,7 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
       attr = true;
     }
     zinv_small_kernel<<<batch, 256, smem, stream>>>(S, sS, lds, X, sX, ldx, n, aux);
-    NEGF_CUDA_CHECK(cudaGetLastError());
+    NEGF_LAUNCHED();
     return 0;
   }
   if (lds != n) return -2;  // blocked path works on packed scratch
@@ -344,10 +345,10 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
   for (int k0 = 0; k0 < n; k0 += nb) {
     const int w = nb < n - k0 ? nb : n - k0;  // last panel may be narrower
     zinv_panel_kernel<<<batch, 256, panel_smem, stream>>>(S, sS, n, k0, w, ipiv, pinv, umm, aux);
-    NEGF_CUDA_CHECK(cudaGetLastError());
+    NEGF_LAUNCHED();
     dim3 g((n + 127) / 128, batch);
     zinv_swap_kernel<<<g, 128, 0, stream>>>(S, sS, n, k0, w, ipiv, Cp, R, aux.active);
-    NEGF_CUDA_CHECK(cudaGetLastError());
+    NEGF_LAUNCHED();
     // T = Pinv R, staged in the caller's destination X (w x n per matrix;
     // X is only written for real by the final unpermute kernel).
     ZGemmGroup grp;
@@ -394,11 +395,11 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
     rc = zgemm_group_launch(grp, stream);
     if (rc) return rc;
     zinv_rows_kernel<<<g, 128, 0, stream>>>(S, sS, n, k0, w, T, sX, pinv, aux.active);
-    NEGF_CUDA_CHECK(cudaGetLastError());
+    NEGF_LAUNCHED();
   }
   zinv_unpermute_kernel<<<batch, 256, n * sizeof(int), stream>>>(S, sS, n, ipiv, umm, X, sX, ldx,
                                                                  aux);
-  NEGF_CUDA_CHECK(cudaGetLastError());
+  NEGF_LAUNCHED();
   return 0;
 }
 

@@ -121,6 +121,21 @@ RESULT_FIELDS = ["g_r_diag", "g_r_upper", "g_r_lower", "g_lesser_diag", "g_lesse
                  "sigma_obc_greater_left", "sigma_obc_lesser_right", "sigma_obc_greater_right"]
 
 
+def make_ballistic():
+    out = {}
+    res = scba_case(5, 3, 16, 1, ballistic=True)
+    for f in RESULT_FIELDS:
+        out[f] = getattr(res, f)
+    h = toys.chain_device(5, 3)
+    out["obs_dos"] = scba.dos(res)
+    out["obs_density"] = scba.electron_density(res)
+    out["obs_current_spectrum"] = scba.current_spectrum(res, h)
+    out["obs_terminal_left"] = np.array(scba.terminal_current(res, "left"))
+    out["obs_terminal_right"] = np.array(scba.terminal_current(res, "right"))
+    out["obs_landauer"] = np.array(scba.landauer_current(h, res.grid, res.contacts))
+    np.savez_compressed(OUT / "golden_ballistic_small.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
+
+
 def make_scba():
     # small: every array in full
     out = {}
@@ -156,6 +171,13 @@ def make_scba():
     res = scba_case(5, 3, 16, 1, ballistic=True)
     for f in RESULT_FIELDS:
         out[f] = getattr(res, f)
+    h = toys.chain_device(5, 3)
+    out["obs_dos"] = scba.dos(res)
+    out["obs_density"] = scba.electron_density(res)
+    out["obs_current_spectrum"] = scba.current_spectrum(res, h)
+    out["obs_terminal_left"] = np.array(scba.terminal_current(res, "left"))
+    out["obs_terminal_right"] = np.array(scba.terminal_current(res, "right"))
+    out["obs_landauer"] = np.array(scba.landauer_current(h, res.grid, res.contacts))
     np.savez_compressed(OUT / "golden_ballistic_small.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
 
 

@@ -79,3 +79,18 @@ def test_ballistic_matches_oracle(cuda, nb, bs, ne, batch):
     out = ballistic_run(h, energies, 1e-3, Contacts(0.1, -0.1, 0.05), 1e-8, batch=batch, device=cuda)
     for k, v in out.items():
         assert rel(v, ref[k]) < TOL, k
+
+
+def test_ballistic_observables_match_reference(golden, cuda):
+    from paper_2508_19138_b200.carrier import ballistic_observables
+    g = golden("golden_ballistic_small.npz")
+    h = orc.chain_device(5, 3)
+    obs = ballistic_observables(h, np.linspace(-2.0, 2.0, 16), 1e-3, Contacts(0.1, -0.1, 0.05), 1e-8,
+                                batch=7, device=cuda)
+    assert rel(obs["dos"], g["obs_dos"]) < TOL
+    assert rel(obs["density"], g["obs_density"]) < TOL
+    assert rel(obs["current_spectrum"], g["obs_current_spectrum"]) < TOL
+    assert abs(obs["terminal_left"] - float(g["obs_terminal_left"])) < TOL * abs(float(g["obs_terminal_left"]))
+    assert abs(obs["terminal_right"] - float(g["obs_terminal_right"])) < TOL * abs(float(g["obs_terminal_right"]))
+    # two-terminal current conservation (scba.py:1357-1362)
+    assert abs(obs["terminal_left"] + obs["terminal_right"]) < 1e-3 * abs(obs["terminal_left"])

@@ -97,3 +97,15 @@ def test_oracle_ballistic_matches_reference_scba_run(golden):
     out = orc.ballistic(h, energies, 1e-3, 0.1, -0.1, 0.05, tol=1e-8)
     for k, v in out.items():
         assert rel(v, g[k]) < 1e-12, k
+
+
+def test_oracle_observables_match_reference(golden):
+    g = golden("golden_ballistic_small.npz")
+    h = orc.chain_device(5, 3)
+    res = {k: g[k] for k in g.files if not k.startswith(("obs_", "ver_"))}
+    obs = orc.observables(res, h[1], 4.0 / 15)
+    assert rel(obs["dos"], g["obs_dos"]) < 1e-13
+    assert rel(obs["density"], g["obs_density"]) < 1e-13
+    assert rel(obs["current_spectrum"], g["obs_current_spectrum"]) < 1e-13
+    assert abs(obs["terminal_left"] - float(g["obs_terminal_left"])) < 1e-13
+    assert abs(obs["terminal_right"] - float(g["obs_terminal_right"])) < 1e-13
