@@ -127,6 +127,85 @@ int negf_observables(int n_e, int n_b, int bs, const void* gr_diag, const void* 
                      const void* sg_right, void* tr_gr, void* tr_gl, double* current_spectrum,
                      void* terminal, void* stream);
 
+/* ---- (3) energy convolutions (negfgw/convolve.py) -----------------------
+ * Entry-major series: row r of an array is the energy series of one matrix
+ * entry, x[r][0..n_e) complex128, rows contiguous (stride n_e).
+ * L: power-of-two circular length >= 2 n_e - 1. tw[L/2] = exp(-2 pi i k/L).
+ * kf/kcf[L]: spectrum (bit-reversed order) of the causal kernel
+ * K = ifft_m(theta), m = scipy next_fast_len(2 n_e) made even, and of conj(K),
+ * laid out circularly on L (see paper_2508_19138_b200/conv.py ConvPlan).
+ * diag[r] (uint8, may be NULL): 1 for row == col entries, which are projected
+ * to their imaginary part (scba.py:406-409).
+ *
+ * Polarization, fused (scba.py:1035-1048):
+ *   P^<[k] = scale sum_m G^<[m] (-conj G^>[m-k]),  P^>[k] = scale sum_m G^>[m] (-conj G^<[m-k])
+ *   (scale = C_POLARIZATION * dE), projection, P^R_up = retarded(P^<, P^>),
+ *   P^R_lo = retarded(-conj P^<, -conj P^>). */
+int negf_conv_polarization(long long n_rows, int n_e, int L, const void* gl, const void* gg,
+                           const void* tw, const void* kf, const void* kcf,
+                           const unsigned char* diag, double scale_re, double scale_im, void* pl,
+                           void* pg, void* pr_up, void* pr_lo, void* stream);
+/* Self-energy, fused (scba.py:1118-1132): Sigma^<>[k] = scale sum_m G^<>[k-m] W^<>[m]
+ * with W rows gathered through w_rows[r] (int64, may be NULL = identity;
+ * the w_to_g map of scba.py:933-937), projection, retarded upper/lower. */
+int negf_conv_sigma(long long n_rows, int n_e, int L, const void* gl, const void* gg,
+                    const void* wl, const void* wg, const long long* w_rows, const void* tw,
+                    const void* kf, const void* kcf, const unsigned char* diag, double scale_re,
+                    double scale_im, void* sl, void* sg, void* sr_up, void* sr_lo, void* stream);
+/* convolve_energy (convolve.py:39-71): mode 0 convolution, 1 correlation. */
+int negf_convolve_energy(long long n_rows, int n_e, int L, const void* x1, const void* x2,
+                         int mode, double scale_re, double scale_im, const void* tw, void* out,
+                         void* stream);
+/* retarded_from_lg (convolve.py:101-129). */
+int negf_retarded_from_lg(long long n_rows, int n_e, int L, const void* x_lesser,
+                          const void* x_greater, const void* tw, const void* kf, void* out,
+                          void* stream);
+
+/* ---- (4) energy <-> entry layout switch (K11/K12) -------------------------
+ * Compressed bandwidth-3 EntryPattern (convolve.py:135-187): per block row bi,
+ * the upper triangle (row-major, r <= c) of block (bi,bi), then block
+ * (bi,bi+1) row-major; n_entries = n_b bs(bs+1)/2 + (n_b-1) bs^2.
+ * tri_q[bs(bs+1)/2] (device int32) = r*bs + c of the triangle entries in order.
+ * Entry-major arrays are (n_entries, ld) row-major; columns e0..e0+n_e-1 are
+ * read/written. Blocks are energy-major [n_e][n_b(-1)][bs][bs]. */
+long long negf_pattern_entries(int n_b, int bs);
+/* _gather_entries (scba.py:252-271) for n_e energies at once. */
+int negf_pack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* x_diag,
+                 const void* x_upper, void* out, long long ld, int e0, void* stream);
+/* _scatter_lg (scba.py:295-308): diagonal blocks get X[c][r] = -conj X[r][c]. */
+int negf_unpack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* in, long long ld,
+                   int e0, void* x_diag, void* x_upper, void* stream);
+/* _scatter_retarded (scba.py:311-325): upper values at (r,c), lower values at
+ * (c,r) (x_lower gets the (bi+1,bi) blocks; diagonal elements take the lower value). */
+int negf_unpack_retarded(int n_e, int n_b, int bs, const int* tri_q, const void* in_upper,
+                         const void* in_lower, long long ld, int e0, void* x_diag, void* x_upper,
+                         void* x_lower, void* stream);
+
+/* ---- (5) screened interaction W (scba.py:784-858) ------------------------
+ * Assembly for n_e energies: M_W = I - trunc3(V P^R), B^<> = trunc3((V P^<>) V).
+ * V blocks are energy independent (v_diag [n_b], v_upper/v_lower [n_b-1]);
+ * P^R full (diag/upper/lower), P^<> lg-compressed (diag/upper, lower implied).
+ * Only tridiagonal output blocks are formed. Workspace: 4 n_b blocks/energy. */
+size_t negf_w_assemble_workspace_bytes(int n_e, int n_b, int bs);
+int negf_w_assemble(int n_e, int n_b, int bs, const void* v_diag, const void* v_upper,
+                    const void* v_lower, const void* pr_diag, const void* pr_upper,
+                    const void* pr_lower, const void* pl_diag, const void* pl_upper,
+                    const void* pg_diag, const void* pg_upper, void* m_diag, void* m_upper,
+                    void* m_lower, void* bl_diag, void* bl_upper, void* bg_diag, void* bg_upper,
+                    void* workspace, size_t workspace_bytes, void* stream);
+/* W contact closure in place (scba.py:839-858, _lead_lg_boundary :617-664):
+ * Sancho surface block per side (status/iters [2][n_e], codes as
+ * negf_obc_sancho_batched), geometric Stein per side and kind (stein_status/
+ * stein_iters [2 kinds][2 sides][n_e]; 4 = spectral radius not certified
+ * < 1 via |a|_F, 2 = not converged), corner source corrections, and
+ * M_cc -= n x n'. */
+size_t negf_w_obc_workspace_bytes(int n_e, int bs);
+int negf_w_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper,
+                     const void* m_lower, void* bl_diag, const void* bl_upper, void* bg_diag,
+                     const void* bg_upper, double surface_tol, int max_sweeps, double stein_tol,
+                     int stein_max_iter, int* status, int* iters, int* stein_status,
+                     int* stein_iters, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- opt-in CUDA-event profiler (bench.py live roofline) ---------------
  * class 0 = DMMA ZGEMM launches. Process-global, off by default. query()
  * synchronises on the recorded events and returns the summed device time

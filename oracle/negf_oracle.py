@@ -90,7 +90,11 @@ def rgf_selected(m_diag, m_up, m_lo, b_lg: dict | None = None, symmetrize: bool 
     out["xr_diag"] = np.stack(xr_d, 1)
     out["xr_upper"] = np.stack(xr_u, 1) if n > 1 else np.zeros_like(m_up)
     out["xr_lower"] = np.stack(xr_l, 1) if n > 1 else np.zeros_like(m_up)
-    for kind, (bd, bu) in b_lg.items():
+    for kind, src in b_lg.items():
+        bd, bu = src[0], src[1]
+        # explicit lower source blocks (FULL-storage sources, e.g. the W
+        # system of scba.py:793-796); default: implied -B_{i,i+1}^dag
+        bl = src[2] if len(src) > 2 else -_h(bu)
         # forward lesser/greater
         xl = [None] * n
         for i in range(n):
@@ -111,7 +115,7 @@ def rgf_selected(m_diag, m_up, m_lo, b_lg: dict | None = None, symmetrize: bool 
             mxl = m_lo[:, i] @ xl[i]
             z = u @ mxl
             d[i] = xl[i] + (t @ d[i + 1]) @ _h(t) - (y - _h(y)) + (z - _h(z))
-            b_dn = -_h(bu[:, i])  # B[i+1, i] of the lg-compressed source
+            b_dn = bl[:, i]  # B[i+1, i]
             lower = (xr_d[i + 1] @ b_dn) @ _h(x) - xr_d[i + 1] @ mxl - d[i + 1] @ _h(t)
             up[i] = -_h(lower)
         dd = np.stack(d, 1)
@@ -390,3 +394,295 @@ def observables(res: dict, h_upper, de: float) -> dict:
         "terminal_left": term(res["sigma_obc_lesser_left"], res["sigma_obc_greater_left"], 0),
         "terminal_right": term(res["sigma_obc_lesser_right"], res["sigma_obc_greater_right"], n_b - 1),
     }
+
+
+# -- energy convolutions (convolve.py) ------------------------------------------
+
+
+def convolve_energy(x1, x2, mode, prefactor, de):
+    """convolve.py:39-71: FFT linear convolution / correlation, window, scale."""
+    x1 = np.asarray(x1, dtype=complex)
+    x2 = np.asarray(x2, dtype=complex)
+    n = x1.shape[-1]
+    if mode == "correlation":
+        x2 = x2[..., ::-1]
+    m = next_fast_len(2 * n - 1)
+    full = ifft(fft(x1, n=m) * fft(x2, n=m), n=m)
+    out = full[..., n - 1:2 * n - 1] if mode == "correlation" else full[..., :n]
+    return prefactor * de * out
+
+
+def convolve_energy_direct(x1, x2, mode, prefactor, de):
+    """convolve.py:74-98: O(N^2) sum (vectorised over the lag)."""
+    n = x1.shape[-1]
+    out = np.zeros(np.broadcast(x1, x2).shape, dtype=complex)
+    for k in range(n):
+        if mode == "convolution":
+            out[..., k] = np.sum(x1[..., k::-1] * x2[..., :k + 1], axis=-1)
+        else:
+            out[..., k] = np.sum(x1[..., k:] * x2[..., :n - k], axis=-1)
+    return prefactor * de * out
+
+
+def retarded_from_lg(xl, xg):
+    """convolve.py:101-129: r = ifft(theta * fft(xg - xl, m))[:N]."""
+    n = xl.shape[-1]
+    m = next_fast_len(2 * n)
+    if m % 2 == 1:
+        m = next_fast_len(m + 1)
+    theta = np.zeros(m)
+    theta[0] = theta[m // 2] = 0.5
+    theta[1:m // 2] = 1.0
+    return ifft(theta * fft(xg - xl, n=m), n=m)[..., :n]
+
+
+def project_diag_rows(arr, diag_mask):
+    """scba.py:406-409."""
+    arr = arr.copy()
+    arr[diag_mask] = 0.5 * (arr[diag_mask] - np.conj(arr[diag_mask]))
+    return arr
+
+
+def polarization(gl, gg, diag_mask, de, c=-1j / (2.0 * np.pi)):
+    """scba.py:1035-1048."""
+    pl = project_diag_rows(convolve_energy(gl, -np.conj(gg), "correlation", c, de), diag_mask)
+    pg = project_diag_rows(convolve_energy(gg, -np.conj(gl), "correlation", c, de), diag_mask)
+    return pl, pg, retarded_from_lg(pl, pg), retarded_from_lg(-np.conj(pl), -np.conj(pg))
+
+
+def self_energy(gl, gg, wl, wg, diag_mask, de, c=1j / (2.0 * np.pi)):
+    """scba.py:1118-1132 (W rows already gathered onto the G pattern)."""
+    sl = project_diag_rows(convolve_energy(gl, wl, "convolution", c, de), diag_mask)
+    sg = project_diag_rows(convolve_energy(gg, wg, "convolution", c, de), diag_mask)
+    return sl, sg, retarded_from_lg(sl, sg), retarded_from_lg(-np.conj(sl), -np.conj(sg))
+
+
+# -- entry-major layout (convolve.py:135-187, scba.py:252-325) ------------------
+
+
+def entry_pattern(n_b: int, bs: int):
+    """Compressed bandwidth-3 EntryPattern: (rows, cols) global indices."""
+    r, c = np.triu_indices(bs)
+    rows, cols = [], []
+    for bi in range(n_b):
+        rows.append(bi * bs + r)
+        cols.append(bi * bs + c)
+        if bi + 1 < n_b:
+            rr, cc = np.divmod(np.arange(bs * bs), bs)
+            rows.append(bi * bs + rr)
+            cols.append((bi + 1) * bs + cc)
+    return np.concatenate(rows), np.concatenate(cols)
+
+
+def gather_entries(diag, upper):
+    """_gather_entries for a batch: (ne, n_b, bs, bs) + (ne, n_b-1, bs, bs) -> (n_entries, ne)."""
+    ne, n_b, bs = diag.shape[:3]
+    r, c = np.triu_indices(bs)
+    parts = []
+    for bi in range(n_b):
+        parts.append(diag[:, bi][:, r, c])
+        if bi + 1 < n_b:
+            parts.append(upper[:, bi].reshape(ne, bs * bs))
+    return np.concatenate(parts, axis=1).T.copy()
+
+
+def scatter_lg(values, n_b, bs):
+    """_scatter_lg: (n_entries, ne) -> diag (mirror rule), upper."""
+    ne = values.shape[1]
+    r, c = np.triu_indices(bs)
+    t = len(r)
+    d = np.zeros((ne, n_b, bs, bs), complex)
+    u = np.zeros((ne, max(n_b - 1, 0), bs, bs), complex)
+    k = 0
+    off = r != c
+    for bi in range(n_b):
+        v = values[k:k + t].T
+        d[:, bi][:, r, c] = v
+        d[:, bi][:, c[off], r[off]] = -np.conj(v[:, off])
+        k += t
+        if bi + 1 < n_b:
+            u[:, bi] = values[k:k + bs * bs].T.reshape(ne, bs, bs)
+            k += bs * bs
+    return d, u
+
+
+def scatter_retarded(up, lo, n_b, bs):
+    """_scatter_retarded: upper values at (r,c), lower values at (c,r)."""
+    ne = up.shape[1]
+    r, c = np.triu_indices(bs)
+    t = len(r)
+    d = np.zeros((ne, n_b, bs, bs), complex)
+    u = np.zeros((ne, max(n_b - 1, 0), bs, bs), complex)
+    l = np.zeros_like(u)
+    k = 0
+    for bi in range(n_b):
+        d[:, bi][:, r, c] = up[k:k + t].T
+        d[:, bi][:, c, r] = lo[k:k + t].T  # diagonal elements end with the lower value
+        k += t
+        if bi + 1 < n_b:
+            u[:, bi] = up[k:k + bs * bs].T.reshape(ne, bs, bs)
+            l[:, bi] = np.swapaxes(lo[k:k + bs * bs].T.reshape(ne, bs, bs), 1, 2)
+            k += bs * bs
+    return d, u, l
+
+
+# -- screened interaction (scba.py:784-858) -------------------------------------
+
+
+def _band_product(a, b):
+    """Banded block product of two (d, u, l) tridiagonal batches, returned as a
+    dict {(i, j): block batch} over the full product band (bt_multiply)."""
+    ad, au, al = a
+    bd, bu, bl = b
+    n = ad.shape[1]
+
+    def get(x, i, j):
+        d, u, l = x
+        if i == j:
+            return d[:, i]
+        if j == i + 1:
+            return u[:, i]
+        if i == j + 1:
+            return l[:, j]
+        return None
+
+    out = {}
+    for i in range(n):
+        for j in range(max(0, i - 2), min(n, i + 3)):
+            acc = None
+            for k in range(max(0, i - 1, j - 1), min(n, i + 2, j + 2)):
+                x, y = get(a, i, k), get(b, k, j)
+                if x is None or y is None:
+                    continue
+                acc = x @ y if acc is None else acc + x @ y
+            if acc is not None:
+                out[(i, j)] = acc
+    return out
+
+
+def w_system(v, pr, pl, pg):
+    """_w_lhs / _w_rhs (scba.py:784-796) for a batch. v = (d, u, l) energy
+    independent; pr = (d, u, l); pl, pg = (d, u) lg-compressed. Returns
+    m = (d, u, l) and full-storage sources {'<': (d, u, l), '>': (d, u, l)}."""
+    ne = pr[0].shape[0]
+    n = v[0].shape[0]
+    vb = tuple(np.broadcast_to(x[None], (ne,) + x.shape) for x in v)
+    vp = _band_product(vb, pr)
+    eye = np.eye(v[0].shape[-1])
+    md = np.stack([eye - vp[(i, i)] for i in range(n)], 1)
+    mu = np.stack([-vp[(i, i + 1)] for i in range(n - 1)], 1)
+    ml = np.stack([-vp[(i + 1, i)] for i in range(n - 1)], 1)
+    srcs = {}
+    for kind, (d, u) in (("<", pl), (">", pg)):
+        p = (d, u, -_h(u))
+        q = _band_product(vb, p)  # V P, bandwidth 5
+        b = {}
+        for i in range(n):
+            for j in range(max(0, i - 1), min(n, i + 2)):
+                acc = None
+                for k in range(max(0, i - 2, j - 1), min(n, i + 3, j + 2)):
+                    x = q.get((i, k))
+                    if x is None:
+                        continue
+                    y = vb[0][:, k] if k == j else (vb[1][:, k] if j == k + 1 else vb[2][:, j])
+                    acc = x @ y if acc is None else acc + x @ y
+                b[(i, j)] = acc
+        srcs[kind] = (np.stack([b[(i, i)] for i in range(n)], 1),
+                      np.stack([b[(i, i + 1)] for i in range(n - 1)], 1),
+                      np.stack([b[(i + 1, i)] for i in range(n - 1)], 1))
+    return (md, mu, ml), srcs
+
+
+def w_closure(m, srcs, surface_tol):
+    """scba.py:839-858 + _lead_lg_boundary (:617-664), W surface by Sancho."""
+    md, mu, ml = m
+    ne, n = md.shape[:2]
+    cells = {}
+    for side in ("left", "right"):
+        xs = []
+        for e in range(ne):
+            if side == "left":
+                cell = (md[e, 0], ml[e, 0], mu[e, 0])
+            else:
+                cell = (md[e, n - 1], mu[e, n - 2], ml[e, n - 2])
+            x, _, _ = sancho_rubio(*cell, tol=surface_tol)
+            xs.append((cell, x))
+        cells[side] = xs
+    for side in ("left", "right"):
+        j, o = (0, 1) if side == "left" else (n - 1, n - 2)
+        for kind in ("<", ">"):
+            bd, bu, bl = srcs[kind]
+            for e in range(ne):
+                (m_c, n_dn, n_up), x = cells[side][e]
+                b_in = bl[e, 0] if side == "left" else bu[e, n - 2]      # B[o, j]
+                b_out = bu[e, 0] if side == "left" else bl[e, n - 2]     # B[j, o]
+                y = (n_dn @ x) @ b_in
+                q0 = bd[e, j] - (y - _h(y))
+                a = x @ n_dn
+                q = (x @ q0) @ _h(x)
+                wl = stein_direct(a, q)
+                t = n_dn @ x
+                bd[e, j] = bd[e, j] + (-(t @ b_in) - (b_out @ _h(x)) @ _h(n_dn) + (n_dn @ wl) @ _h(n_dn))
+    for side in ("left", "right"):
+        j = 0 if side == "left" else n - 1
+        for e in range(ne):
+            (m_c, n_dn, n_up), x = cells[side][e]
+            md[e, j] = md[e, j] - (n_dn @ x) @ n_up
+
+
+# -- full SCBA iteration (scba.py:865-1216, sequential, memoizer off) ---------
+
+
+def scba(h, v, energies, eta, mu_left, mu_right, kT, max_iter=1, tol=1e-12, mixing=0.3,
+         surface_tol=1e-8):
+    """scba_run(retarded_method='sancho', memoizer off, W surface by Sancho).
+    Returns the ScbaResult arrays (G at the start of the last iteration, mixed
+    Sigma after it) plus 'residuals'."""
+    energies = np.asarray(energies, dtype=float)
+    ne = len(energies)
+    de = (energies[-1] - energies[0]) / (ne - 1)
+    n_b, bs = h[0].shape[0], h[0].shape[-1]
+    rows, cols = entry_pattern(n_b, bs)
+    diag_mask = rows == cols
+    trace_idx = [np.flatnonzero(diag_mask & (rows // bs == b)) for b in range(n_b)]
+    n_ent = len(rows)
+    sig = {k: np.zeros((n_ent, ne), complex) for k in ("lesser", "greater", "ret_upper", "ret_lower")}
+    f_bath = fermi(energies, 0.5 * (mu_left + mu_right), kT)
+    residuals = []
+    for it in range(max_iter):
+        sr = scatter_retarded(sig["ret_upper"], sig["ret_lower"], n_b, bs)
+        sl = scatter_lg(sig["lesser"], n_b, bs)
+        sg = scatter_lg(sig["greater"], n_b, bs)
+        m, bl, bg = assemble_g(energies, eta, h, f_bath, sr=sr, sl=sl, sg=sg)
+        obc = g_closure(m, bl, bg, energies, mu_left, mu_right, kT, surface_tol)
+        sol = rgf_selected(*m, {"<": bl, ">": bg}, symmetrize=True)
+        result = {
+            "g_r_diag": sol["xr_diag"], "g_r_upper": sol["xr_upper"], "g_r_lower": sol["xr_lower"],
+            "g_lesser_diag": sol["x<_diag"], "g_lesser_upper": sol["x<_upper"],
+            "g_greater_diag": sol["x>_diag"], "g_greater_upper": sol["x>_upper"],
+            "sigma_obc_lesser_left": obc["left"][0], "sigma_obc_greater_left": obc["left"][1],
+            "sigma_obc_lesser_right": obc["right"][0], "sigma_obc_greater_right": obc["right"][1],
+        }
+        gl = gather_entries(sol["x<_diag"], sol["x<_upper"])
+        gg = gather_entries(sol["x>_diag"], sol["x>_upper"])
+        pl, pg, pru, prl = polarization(gl, gg, diag_mask, de)
+        pr = scatter_retarded(pru, prl, n_b, bs)
+        mw, srcs = w_system(v, pr, scatter_lg(pl, n_b, bs), scatter_lg(pg, n_b, bs))
+        w_closure(mw, srcs, surface_tol)
+        wsol = rgf_selected(*mw, srcs, symmetrize=True)
+        wl = gather_entries(wsol["x<_diag"], wsol["x<_upper"])
+        wg = gather_entries(wsol["x>_diag"], wsol["x>_upper"])
+        raw = dict(zip(("lesser", "greater", "ret_upper", "ret_lower"), self_energy(gl, gg, wl, wg, diag_mask, de)))
+        tr_old = {k: np.stack([sig[k][idx].sum(0) for idx in trace_idx]) for k in ("lesser", "greater")}
+        for k in sig:
+            sig[k] = (1.0 - mixing) * sig[k] + mixing * raw[k]
+        tr_new = {k: np.stack([sig[k][idx].sum(0) for idx in trace_idx]) for k in ("lesser", "greater")}
+        delta = max(float(np.max(np.abs(tr_new[k] - tr_old[k]))) for k in tr_new)
+        scale = max(max(float(np.max(np.abs(tr_old[k]))) for k in tr_old),
+                    max(float(np.max(np.abs(tr_new[k]))) for k in tr_new))
+        residuals.append(delta / (scale + 1e-300))
+        if residuals[-1] < tol:
+            break
+    result.update({"sigma_" + k: v_ for k, v_ in sig.items()})
+    result["residuals"] = np.asarray(residuals)
+    return result

@@ -46,6 +46,18 @@ _SIGNATURES: dict[str, tuple] = {
     ),
     "negf_g_assemble": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _d] + [_vp] * 7 + [_vp] * 7 + [_vp]),
     "negf_observables": (_i, [_i, _i, _i] + [_vp] * 14),
+    "negf_conv_polarization": (_i, [_ll, _i, _i] + [_vp] * 6 + [_d, _d] + [_vp] * 5),
+    "negf_conv_sigma": (_i, [_ll, _i, _i] + [_vp] * 9 + [_d, _d] + [_vp] * 5),
+    "negf_convolve_energy": (_i, [_ll, _i, _i, _vp, _vp, _i, _d, _d, _vp, _vp, _vp]),
+    "negf_retarded_from_lg": (_i, [_ll, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "negf_pattern_entries": (_ll, [_i, _i]),
+    "negf_pack_lg": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _ll, _i, _vp]),
+    "negf_unpack_lg": (_i, [_i, _i, _i, _vp, _vp, _ll, _i, _vp, _vp, _vp]),
+    "negf_unpack_retarded": (_i, [_i, _i, _i, _vp, _vp, _vp, _ll, _i, _vp, _vp, _vp, _vp]),
+    "negf_w_assemble_workspace_bytes": (_sz, [_i, _i, _i]),
+    "negf_w_assemble": (_i, [_i, _i, _i] + [_vp] * 17 + [_sz, _vp]),
+    "negf_w_obc_workspace_bytes": (_sz, [_i, _i]),
+    "negf_w_obc_apply": (_i, [_i, _i, _i] + [_vp] * 7 + [_d, _i, _d, _i] + [_vp] * 5 + [_sz, _vp]),
     "negf_prof_enable": (None, [_i]),
     "negf_launch_count": (_ll, []),
     "negf_prof_reset": (None, []),

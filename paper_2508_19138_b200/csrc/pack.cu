@@ -1,0 +1,185 @@
+// Energy-major blocks <-> entry-major series (the E <-> nnz layout switch).
+//
+// Reference: EntryPattern (convolve.py:135-187, compressed, bandwidth 3):
+// for every block row bi, first the upper triangle (row-major, r <= c) of
+// the diagonal block (bi, bi), then every entry of the upper block
+// (bi, bi+1) row-major. _gather_entries (scba.py:252-271) packs one energy,
+// _scatter_lg (scba.py:295-308) unpacks with the mirror rule
+// X[c][r] = -conj X[r][c] on diagonal blocks, _scatter_retarded
+// (scba.py:311-325) places the (row, col) value and the (col, row) value.
+//
+// Layout: entry-major arrays are row-major (n_entries, ld) with the energy
+// window [e0, e0 + n_e) of the columns touched; blocks are
+// [n_e][n_b][bs][bs] (diag) / [n_e][n_b-1][bs][bs] (upper, lower).
+// Each CTA moves a 32-entry x 32-energy tile through shared memory so both
+// the block side (entries contiguous) and the series side (energies
+// contiguous) are read and written coalesced.
+#include "../../include/negf_b200.h"
+#include "common.cuh"
+
+namespace negf {
+namespace {
+
+constexpr int T = 32;
+
+struct Pat {
+  int n_b, bs;
+  long long tri, per_row, n_entries;  // tri = bs(bs+1)/2, per_row = tri + bs^2
+};
+
+__device__ __forceinline__ void locate(const Pat& p, const int* __restrict__ tri_q, long long t,
+                                       int& bi, int& kind, int& q) {
+  bi = (int)(t / p.per_row);
+  const long long rem = t - (long long)bi * p.per_row;
+  if (rem < p.tri) {
+    kind = 0;
+    q = tri_q[rem];
+  } else {
+    kind = 1;
+    q = (int)(rem - p.tri);
+  }
+}
+
+// blocks -> series
+__global__ void pack_lg_kernel(Pat p, const int* __restrict__ tri_q, int n_e,
+                               const z_t* __restrict__ xd, const z_t* __restrict__ xu, z_t* out,
+                               long long ld, int e0) {
+  __shared__ z_t tile[T][T + 1];
+  const long long t0 = (long long)blockIdx.x * T;
+  const int eb = blockIdx.y * T;
+  const long long n2 = (long long)p.bs * p.bs;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const long long t = t0 + tx;
+  int bi = 0, kind = 0, q = 0;
+  const bool ok = t < p.n_entries;
+  if (ok) locate(p, tri_q, t, bi, kind, q);
+  for (int k = ty; k < T; k += 8) {
+    const int e = eb + k;
+    if (ok && e < n_e) {
+      const z_t* src = kind == 0 ? xd + ((long long)e * p.n_b + bi) * n2
+                                 : xu + ((long long)e * (p.n_b - 1) + bi) * n2;
+      tile[k][tx] = src[q];
+    }
+  }
+  __syncthreads();
+  for (int k = ty; k < T; k += 8) {
+    const long long tt = t0 + k;
+    const int e = eb + tx;
+    if (tt < p.n_entries && e < n_e) out[tt * ld + e0 + e] = tile[tx][k];
+  }
+}
+
+// series -> blocks. mode 0: lg (mirror rule on diagonal blocks);
+// mode 1: retarded (upper values at (r,c), lower values at (c,r)).
+__global__ void unpack_kernel(Pat p, const int* __restrict__ tri_q, int n_e,
+                              const z_t* __restrict__ in_up, const z_t* __restrict__ in_lo,
+                              long long ld, int e0, int mode, z_t* xd, z_t* xu, z_t* xl) {
+  __shared__ z_t tu[T][T + 1];
+  __shared__ z_t tl[T][T + 1];
+  const long long t0 = (long long)blockIdx.x * T;
+  const int eb = blockIdx.y * T;
+  const long long n2 = (long long)p.bs * p.bs;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int k = ty; k < T; k += 8) {
+    const long long tt = t0 + k;
+    const int e = eb + tx;
+    if (tt < p.n_entries && e < n_e) {
+      tu[k][tx] = in_up[tt * ld + e0 + e];
+      if (mode == 1) tl[k][tx] = in_lo[tt * ld + e0 + e];
+    }
+  }
+  __syncthreads();
+  const long long t = t0 + tx;
+  if (t >= p.n_entries) return;
+  int bi, kind, q;
+  locate(p, tri_q, t, bi, kind, q);
+  const int r = q / p.bs, c = q % p.bs;
+  const int qt = c * p.bs + r;
+  for (int k = ty; k < T; k += 8) {
+    const int e = eb + k;
+    if (e >= n_e) continue;
+    const z_t v = tu[tx][k];
+    if (kind == 0) {
+      z_t* d = xd + ((long long)e * p.n_b + bi) * n2;
+      if (mode == 0) {
+        d[q] = v;
+        if (r != c) d[qt] = make_double2(-v.x, v.y);
+      } else {
+        const z_t w = tl[tx][k];
+        if (r != c) d[q] = v;
+        d[qt] = w;  // diagonal elements take the lower value (scba.py:319-321 write order)
+      }
+    } else {
+      z_t* u = xu + ((long long)e * (p.n_b - 1) + bi) * n2;
+      u[q] = v;
+      if (mode == 1) {
+        z_t* l = xl + ((long long)e * (p.n_b - 1) + bi) * n2;
+        l[qt] = tl[tx][k];
+      }
+    }
+  }
+}
+
+Pat make_pat(int n_b, int bs) {
+  Pat p;
+  p.n_b = n_b;
+  p.bs = bs;
+  p.tri = (long long)bs * (bs + 1) / 2;
+  p.per_row = p.tri + (long long)bs * bs;
+  p.n_entries = (long long)n_b * p.tri + (long long)(n_b - 1) * bs * bs;
+  return p;
+}
+
+}  // namespace
+}  // namespace negf
+
+using namespace negf;
+
+extern "C" {
+
+long long negf_pattern_entries(int n_b, int bs) { return make_pat(n_b, bs).n_entries; }
+
+int negf_pack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* x_diag,
+                 const void* x_upper, void* out, long long ld, int e0, void* stream) {
+  if (n_e < 0 || n_b < 1 || bs < 1 || !tri_q || !x_diag || !out || e0 < 0 || ld < e0 + n_e) return -1;
+  if (n_b > 1 && !x_upper) return -1;
+  if (n_e == 0) return 0;
+  Pat p = make_pat(n_b, bs);
+  dim3 grid((unsigned)((p.n_entries + T - 1) / T), (n_e + T - 1) / T), block(T, 8);
+  pack_lg_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(p, tri_q, n_e, (const z_t*)x_diag,
+                                                           (const z_t*)x_upper, (z_t*)out, ld, e0);
+  NEGF_LAUNCHED();
+  return 0;
+}
+
+int negf_unpack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* in, long long ld,
+                   int e0, void* x_diag, void* x_upper, void* stream) {
+  if (n_e < 0 || n_b < 1 || bs < 1 || !tri_q || !in || !x_diag || e0 < 0 || ld < e0 + n_e) return -1;
+  if (n_b > 1 && !x_upper) return -1;
+  if (n_e == 0) return 0;
+  Pat p = make_pat(n_b, bs);
+  dim3 grid((unsigned)((p.n_entries + T - 1) / T), (n_e + T - 1) / T), block(T, 8);
+  unpack_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(p, tri_q, n_e, (const z_t*)in, nullptr, ld,
+                                                          e0, 0, (z_t*)x_diag, (z_t*)x_upper, nullptr);
+  NEGF_LAUNCHED();
+  return 0;
+}
+
+int negf_unpack_retarded(int n_e, int n_b, int bs, const int* tri_q, const void* in_upper,
+                         const void* in_lower, long long ld, int e0, void* x_diag, void* x_upper,
+                         void* x_lower, void* stream) {
+  if (n_e < 0 || n_b < 1 || bs < 1 || !tri_q || !in_upper || !in_lower || !x_diag || e0 < 0 ||
+      ld < e0 + n_e)
+    return -1;
+  if (n_b > 1 && (!x_upper || !x_lower)) return -1;
+  if (n_e == 0) return 0;
+  Pat p = make_pat(n_b, bs);
+  dim3 grid((unsigned)((p.n_entries + T - 1) / T), (n_e + T - 1) / T), block(T, 8);
+  unpack_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(
+      p, tri_q, n_e, (const z_t*)in_upper, (const z_t*)in_lower, ld, e0, 1, (z_t*)x_diag,
+      (z_t*)x_upper, (z_t*)x_lower);
+  NEGF_LAUNCHED();
+  return 0;
+}
+
+}  // extern "C"

@@ -27,12 +27,22 @@ struct Cfg {
 };
 
 // Stage one BK-slice of both operands into shared memory with cp.async.
+struct KtBounds {
+  int b1, b2, b3;  // cumulative k-tile counts after terms 0, 1, 2 (clamped to the total)
+  __device__ __forceinline__ int term(int kt) const {
+    return (kt >= b1) + (kt >= b2) + (kt >= b3);
+  }
+  __device__ __forceinline__ int base(int term) const {
+    return term == 0 ? 0 : term == 1 ? b1 : term == 2 ? b2 : b3;
+  }
+};
+
 template <class CF>
-__device__ __forceinline__ void load_stage(const ZGemmDesc& d, int kt, int kt0, int b, int m0,
-                                           int n0, z_t* sA, z_t* sB) {
-  const int term = kt < kt0 ? 0 : 1;
+__device__ __forceinline__ void load_stage(const ZGemmDesc& d, int kt, const KtBounds& kb, int b,
+                                           int m0, int n0, z_t* sA, z_t* sB) {
+  const int term = kb.term(kt);
   const ZTerm& t = d.t[term];
-  const int k0 = (kt - (term ? kt0 : 0)) * CF::BK;
+  const int k0 = (kt - kb.base(term)) * CF::BK;
   const z_t* A = t.A + (long long)b * t.sA;
   const z_t* B = t.B + (long long)b * t.sB;
   const int K = t.K, M = d.M, N = d.N;
@@ -90,9 +100,15 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp / CF::WN, wn = warp % CF::WN;
 
-  const int kt0 = (d.t[0].K + CF::BK - 1) / CF::BK;
-  const int kt1 = d.nterms > 1 ? (d.t[1].K + CF::BK - 1) / CF::BK : 0;
-  const int KT = kt0 + kt1;
+  KtBounds kb;
+  {
+    auto nk = [&](int i) { return i < d.nterms ? (d.t[i].K + CF::BK - 1) / CF::BK : 0; };
+    kb.b1 = nk(0);
+    kb.b2 = kb.b1 + nk(1);
+    kb.b3 = kb.b2 + nk(2);
+  }
+  const int KT = kb.b3 + (d.nterms > 3 ? (d.t[3].K + CF::BK - 1) / CF::BK : 0);
+  // terms past nterms have zero tiles, so their bounds equal KT and are never reached
 
   double acc_re[CF::TM][CF::TN][2], acc_im[CF::TM][CF::TN][2];
 #pragma unroll
@@ -108,7 +124,7 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
 
 #pragma unroll
   for (int s = 0; s < CF::STAGES - 1; ++s) {
-    if (s < KT) load_stage<CF>(d, s, kt0, b, m0, n0, stageA(s), stageB(s));
+    if (s < KT) load_stage<CF>(d, s, kb, b, m0, n0, stageA(s), stageB(s));
     cp_async_commit();
   }
 
@@ -119,14 +135,14 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
       int nk = kt + CF::STAGES - 1;
       if (nk < KT) {
         int s = nk % CF::STAGES;
-        load_stage<CF>(d, nk, kt0, b, m0, n0, stageA(s), stageB(s));
+        load_stage<CF>(d, nk, kb, b, m0, n0, stageA(s), stageB(s));
       }
       cp_async_commit();
     }
     const int s = kt % CF::STAGES;
     const z_t* sA = stageA(s);
     const z_t* sB = stageB(s);
-    const ZTerm& t = d.t[kt < kt0 ? 0 : 1];
+    const ZTerm& t = d.t[kb.term(kt)];
     const bool a_kc = !op_trans(t.opA);
     const bool b_kc = op_trans(t.opB);
     const unsigned long long negm = t.neg ? kSign : 0ull;

@@ -1,6 +1,6 @@
 // Batched, grouped complex-FP64 GEMM on the FP64 tensor pipe (DMMA) for sm_100a.
 //
-//   D[b] = alpha * sum_t s_t * op(A_t[b]) op(B_t[b]) + beta * C[b]      (t < 2)
+//   D[b] = alpha * sum_t s_t * op(A_t[b]) op(B_t[b]) + beta * C[b]      (t < 4)
 //   optionally stored conjugate-transposed: D[b][n][m] = conj(value(m, n)).
 //
 // This is the kernel behind every dense block product of the RGF recursion
@@ -41,9 +41,11 @@ struct ZTerm {
   int neg;  // 1: subtract this term
 };
 
+constexpr int kMaxTerms = 4;
+
 struct ZGemmDesc {
-  int M, N, batch, nterms;
-  ZTerm t[2];
+  int M, N, batch, nterms;  // nterms <= kMaxTerms
+  ZTerm t[kMaxTerms];
   double2 alpha, beta;
   const z_t* C;
   long long sC;

@@ -228,27 +228,33 @@ __global__ void zinv_swap_kernel(z_t* A, long long sA, int n, int k0, int nb, co
   const int b = blockIdx.y;
   if (active && !active[b]) return;
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= n) return;
   z_t* a = A + (long long)b * sA;
   const int* pv = ipiv + (long long)b * n;
-  for (int j = 0; j < nb; ++j) {
-    int r = pv[k0 + j];
-    if (r != k0 + j) {
-      z_t t = a[(long long)(k0 + j) * n + col];
-      a[(long long)(k0 + j) * n + col] = a[(long long)r * n + col];
-      a[(long long)r * n + col] = t;
+  if (col < n) {
+    for (int j = 0; j < nb; ++j) {
+      int r = pv[k0 + j];
+      if (r != k0 + j) {
+        z_t t = a[(long long)(k0 + j) * n + col];
+        a[(long long)(k0 + j) * n + col] = a[(long long)r * n + col];
+        a[(long long)r * n + col] = t;
+      }
     }
+    z_t* rr = R + (long long)b * nb * n;
+    for (int j = 0; j < nb; ++j) rr[(long long)j * n + col] = a[(long long)(k0 + j) * n + col];
   }
-  z_t* rr = R + (long long)b * nb * n;
-  for (int j = 0; j < nb; ++j) {
-    rr[(long long)j * n + col] = a[(long long)(k0 + j) * n + col];
-  }
-  if (col >= k0 && col < k0 + nb) {
-    const int c = col - k0;
-    z_t* cp = Cp + (long long)b * n * nb;
-    for (int i = 0; i < n; ++i) {
-      cp[(long long)i * nb + c] = (i >= k0 && i < k0 + nb) ? make_double2(0.0, 0.0) : a[(long long)i * n + col];
-    }
+  // The CTA owning columns K (k0 is a multiple of the 128-column tile when
+  // nb divides 128; otherwise two CTAs share the range) copies the swapped
+  // panel columns cooperatively, rows K zeroed.
+  const int c0 = blockIdx.x * blockDim.x, c1 = c0 + blockDim.x;
+  const int lo = k0 > c0 ? k0 : c0, hi = (k0 + nb) < c1 ? (k0 + nb) : c1;
+  if (lo >= hi) return;
+  __syncthreads();
+  const int w = hi - lo;
+  z_t* cp = Cp + (long long)b * n * nb;
+  for (long long e = threadIdx.x; e < (long long)n * w; e += blockDim.x) {
+    const int i = (int)(e / w), c = lo + (int)(e % w);
+    cp[(long long)i * nb + (c - k0)] =
+        (i >= k0 && i < k0 + nb) ? make_double2(0.0, 0.0) : a[(long long)i * n + c];
   }
 }
 

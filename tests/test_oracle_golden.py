@@ -109,3 +109,67 @@ def test_oracle_observables_match_reference(golden):
     assert rel(obs["current_spectrum"], g["obs_current_spectrum"]) < 1e-13
     assert abs(obs["terminal_left"] - float(g["obs_terminal_left"])) < 1e-13
     assert abs(obs["terminal_right"] - float(g["obs_terminal_right"])) < 1e-13
+
+
+@pytest.mark.parametrize("ne", [24, 128, 129, 1000])
+def test_oracle_convolutions_match_reference(golden, ne):
+    g = golden("golden_conv.npz")
+    x1, x2 = g[f"n{ne}_x1"], g[f"n{ne}_x2"]
+    assert rel(orc.convolve_energy(x1, x2, "convolution", 0.7 - 0.2j, 0.01), g[f"n{ne}_conv"]) < 1e-14
+    assert rel(orc.convolve_energy(x1, x2, "correlation", -0.3 + 1.1j, 0.02), g[f"n{ne}_corr"]) < 1e-14
+    assert rel(orc.retarded_from_lg(x1, x2), g[f"n{ne}_ret"]) < 1e-14
+    assert rel(orc.convolve_energy_direct(x1, x2, "convolution", 0.7 - 0.2j, 0.01), g[f"n{ne}_direct_conv"]) < 1e-12
+    assert rel(orc.convolve_energy_direct(x1, x2, "correlation", -0.3 + 1.1j, 0.02), g[f"n{ne}_direct_corr"]) < 1e-12
+
+
+def test_oracle_scba_small_matches_reference(golden):
+    """Full SCBA (3 iterations, 6x4 chain + Coulomb, 32 energies) vs scba_run."""
+    g = golden("golden_scba_small.npz")
+    h = orc.chain_device(6, 4)
+    v = orc.coulomb_matrix(6, 4)
+    res = orc.scba(h, v, np.linspace(-2.0, 2.0, 32), 1e-3, 0.1, -0.1, 0.05, max_iter=3, tol=1e-12)
+    for k in g.files:
+        if k.startswith(("ver_", "config")):
+            continue
+        assert rel(res[k], g[k]) < 1e-11, k
+
+
+def test_oracle_entry_layout_roundtrip():
+    rng = np.random.default_rng(0)
+    n_b, bs, ne = 4, 3, 5
+    d = rng.standard_normal((ne, n_b, bs, bs)) + 1j * rng.standard_normal((ne, n_b, bs, bs))
+    d = 0.5 * (d - np.conj(np.swapaxes(d, -1, -2)))
+    u = rng.standard_normal((ne, n_b - 1, bs, bs)) + 0j
+    vals = orc.gather_entries(d, u)
+    rows, cols = orc.entry_pattern(n_b, bs)
+    assert vals.shape == (len(rows), ne) and np.all(rows <= cols)
+    d2, u2 = orc.scatter_lg(vals, n_b, bs)
+    np.testing.assert_allclose(d2, d, atol=0)
+    np.testing.assert_allclose(u2, u, atol=0)
+
+
+def test_oracle_scba_c1_matches_reference(golden):
+    """C1 (16 blocks x 32 orbitals, 128 energies, 1 SCBA iteration) vs the
+    reference scba_run: energy slices + weighted checksums of every array."""
+    g = golden("golden_scba_c1.npz")
+    res = orc.scba(orc.chain_device(16, 32), orc.coulomb_matrix(16, 32), np.linspace(-2.0, 2.0, 128),
+                   1e-3, 0.1, -0.1, 0.05, max_iter=1)
+    check_c1(res, g)
+
+
+def check_c1(res, g, tol=1e-10):
+    sel = g["sel"]
+    rng = np.random.default_rng(99)
+    for f in ["g_r_diag", "g_r_upper", "g_r_lower", "g_lesser_diag", "g_lesser_upper", "g_greater_diag",
+              "g_greater_upper", "sigma_obc_lesser_left", "sigma_obc_greater_left", "sigma_obc_lesser_right",
+              "sigma_obc_greater_right"]:
+        a = res[f]
+        assert rel(a[sel], g[f + "_sel"]) < tol, f
+        w = rng.standard_normal(a.shape[1:])
+        assert rel(np.tensordot(a, w, axes=a.ndim - 1), g[f + "_chk"]) < tol, f
+    for f in ("lesser", "greater", "ret_upper", "ret_lower"):
+        a = res["sigma_" + f]
+        assert rel(a[:, sel], g["sigma_" + f + "_sel"]) < tol, f
+        assert rel(a.T @ rng.standard_normal(a.shape[0]), g["sigma_" + f + "_chk"]) < tol, f
+        assert abs(np.linalg.norm(a) - float(g["sigma_" + f + "_fro"])) < tol * float(g["sigma_" + f + "_fro"])
+    assert rel(res["residuals"], g["residuals"]) < tol
