@@ -206,6 +206,16 @@ int negf_w_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
                      int stein_max_iter, int* status, int* iters, int* stein_status,
                      int* stein_iters, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- (6) mixing and residual (scba.py:478-481, 1155-1167) ----------------
+ * s_k <- (1 - alpha) s_k + alpha r_k elementwise over n complex values, for
+ * each non-NULL pair. diag_traces: tr[b][e] = sum_r x[diag_rows[b*bs + r]][e]
+ * (the per-block traces _diag_traces, scba.py:1251-1255). */
+int negf_mix(long long n, double alpha, void* s_lesser, void* s_greater, void* s_ret_up,
+             void* s_ret_lo, const void* r_lesser, const void* r_greater, const void* r_ret_up,
+             const void* r_ret_lo, void* stream);
+int negf_diag_traces(const void* x, long long ld, int n_e, const long long* diag_rows, int n_b,
+                     int bs, void* tr, void* stream);
+
 /* ---- opt-in CUDA-event profiler (bench.py live roofline) ---------------
  * class 0 = DMMA ZGEMM launches. Process-global, off by default. query()
  * synchronises on the recorded events and returns the summed device time

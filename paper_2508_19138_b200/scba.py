@@ -1,0 +1,289 @@
+"""Self-consistent Born (GW) iteration on the GPU (drop-in for the hot path
+of negfgw.scba.scba_run, scba.py:865-1216).
+
+One iteration, every stage a call into libnegf_b200.so:
+  1. carrier solve per energy batch (carrier.CarrierSolver): Sigma entries ->
+     blocks (negf_unpack_*), assembly, contact closure, RGF, symmetrize;
+     G^<> blocks -> entry-major series (negf_pack_lg)           scba.py:965-1029
+  2. polarization, fused FFT kernel (negf_conv_polarization)   scba.py:1035-1048
+  3. screened interaction per batch: P entries -> blocks, W assembly
+     (negf_w_assemble), W contact closure (negf_w_obc_apply), RGF, pack W^<>
+                                                                scba.py:1059-1116
+  4. self-energy, fused FFT kernel (negf_conv_sigma)           scba.py:1118-1132
+  5. mixing + residual on per-block traces (negf_mix, negf_diag_traces)
+                                                                scba.py:1155-1177
+Entry-major state stays resident in HBM across iterations; only the
+per-block traces (n_b x N_E) come back to the host for the residual.
+
+Single-GPU driver; the multi-GPU energy-sharded version (E <-> nnz
+transposes over NCCL all-to-all) is in ``dist.py``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .carrier import RESULT_KEYS, CarrierSolver, Contacts
+from .conv import polarization, self_energy
+from .errors import ConvergenceError, SpectralRadiusError
+from .obc import raise_on_obc_status
+from .rgf import raise_on_status
+
+Z = torch.complex128
+
+
+@dataclass(frozen=True)
+class ScbaOptions:
+    """scba.py:157-190 (retarded_method fixed to Sancho-Rubio, memoizer off)."""
+
+    max_iter: int = 50
+    tol: float = 1e-5
+    mixing: float = 0.3
+    surface_tol: float = 1e-8
+    stein_tol: float = 1e-12
+    stein_max_iter: int = 100
+    batch: int | None = None  # energies per device batch (None: all)
+
+    def __post_init__(self) -> None:
+        if self.max_iter < 1:
+            raise ValueError(f"max_iter must be at least 1, got {self.max_iter}")
+        if self.tol <= 0:
+            raise ValueError(f"tol must be positive, got {self.tol}")
+        if not 0 < self.mixing <= 1:
+            raise ValueError(f"mixing must lie in (0, 1], got {self.mixing}")
+
+
+class EntryLayout:
+    """Device tables of the compressed bandwidth-3 EntryPattern."""
+
+    def __init__(self, n_b: int, bs: int, device) -> None:
+        self.n_b, self.bs = n_b, bs
+        self.dev = torch.device(device)
+        lib = _lib.load()
+        self.n_entries = int(lib.negf_pattern_entries(n_b, bs))
+        r, c = np.triu_indices(bs)
+        self.tri_q = torch.from_numpy((r * bs + c).astype(np.int32)).to(self.dev)
+        t = len(r)
+        per_row = t + bs * bs
+        diag = np.zeros(self.n_entries, dtype=np.uint8)
+        rows = []
+        for b in range(n_b):
+            base = b * per_row
+            on = np.flatnonzero(r == c)
+            diag[base + on] = 1
+            rows.append(base + on)
+        self.diag = torch.from_numpy(diag).to(self.dev)
+        self.diag_rows = torch.from_numpy(np.stack(rows).astype(np.int64)).to(self.dev)  # (n_b, bs)
+
+    def pack(self, x_diag, x_upper, out, e0):
+        rc = _lib.load().negf_pack_lg(x_diag.shape[0], self.n_b, self.bs, self.tri_q.data_ptr(), x_diag.data_ptr(),
+                                      x_upper.data_ptr(), out.data_ptr(), out.shape[-1], e0,
+                                      _lib.stream_ptr(self.dev))
+        _lib.check(rc, "negf_pack_lg")
+
+    def unpack_lg(self, src, e0, n_e, x_diag, x_upper):
+        rc = _lib.load().negf_unpack_lg(n_e, self.n_b, self.bs, self.tri_q.data_ptr(), src.data_ptr(), src.shape[-1],
+                                        e0, x_diag.data_ptr(), x_upper.data_ptr(), _lib.stream_ptr(self.dev))
+        _lib.check(rc, "negf_unpack_lg")
+
+    def unpack_retarded(self, up, lo, e0, n_e, x_diag, x_upper, x_lower):
+        rc = _lib.load().negf_unpack_retarded(n_e, self.n_b, self.bs, self.tri_q.data_ptr(), up.data_ptr(),
+                                              lo.data_ptr(), up.shape[-1], e0, x_diag.data_ptr(),
+                                              x_upper.data_ptr(), x_lower.data_ptr(), _lib.stream_ptr(self.dev))
+        _lib.check(rc, "negf_unpack_retarded")
+
+    def traces(self, x) -> torch.Tensor:
+        tr = torch.empty((self.n_b, x.shape[-1]), dtype=Z, device=self.dev)
+        rc = _lib.load().negf_diag_traces(x.data_ptr(), x.shape[-1], x.shape[-1], self.diag_rows.data_ptr(),
+                                          self.n_b, self.bs, tr.data_ptr(), _lib.stream_ptr(self.dev))
+        _lib.check(rc, "negf_diag_traces")
+        return tr
+
+
+class ScreenedSolver:
+    """Batched W solve: assembly + contact closure + RGF (scba.py:1059-1103)."""
+
+    def __init__(self, v, options: ScbaOptions, device) -> None:
+        self.dev = torch.device(device)
+        self.lib = _lib.load()
+        self.v = tuple(torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=complex))).to(self.dev) for x in v)
+        self.n_b, self.bs = self.v[0].shape[0], self.v[0].shape[-1]
+        self.opt = options
+        self._buf, self._n_e = None, 0
+
+    def buffers(self, n_e: int) -> dict:
+        if self._buf is not None and self._n_e == n_e:
+            return self._buf
+        self._buf = None
+        nb, bs, dev = self.n_b, self.bs, self.dev
+        d, o = (n_e, nb, bs, bs), (n_e, nb - 1, bs, bs)
+        b = {k: torch.empty(d, dtype=Z, device=dev) for k in
+             ("pr_diag", "pl_diag", "pg_diag", "m_diag", "bl_diag", "bg_diag", "wr_diag", "wl_diag", "wg_diag")}
+        b.update({k: torch.empty(o, dtype=Z, device=dev) for k in
+                  ("pr_upper", "pr_lower", "pl_upper", "pg_upper", "m_upper", "m_lower", "bl_upper", "bg_upper",
+                   "wr_upper", "wr_lower", "wl_upper", "wg_upper")})
+        b["obc_status"] = torch.zeros(2 * n_e, dtype=torch.int32, device=dev)
+        b["obc_iters"] = torch.zeros(2 * n_e, dtype=torch.int32, device=dev)
+        b["stein_status"] = torch.zeros(4 * n_e, dtype=torch.int32, device=dev)
+        b["stein_iters"] = torch.zeros(4 * n_e, dtype=torch.int32, device=dev)
+        b["rgf_status"] = torch.zeros(n_e, dtype=torch.int32, device=dev)
+        self._buf, self._n_e = b, n_e
+        return b
+
+    def solve(self, n_e: int, check: bool = True) -> dict:
+        """Inputs in buffers pr_*/pl_*/pg_* (filled by the caller)."""
+        lib, p, b, o = self.lib, _lib.ptr, self.buffers(n_e), self.opt
+        st = _lib.stream_ptr(self.dev)
+        vd, vu, vl = self.v
+        nbytes = lib.negf_w_assemble_workspace_bytes(n_e, self.n_b, self.bs)
+        ws = _lib.workspace(nbytes, self.dev)
+        rc = lib.negf_w_assemble(n_e, self.n_b, self.bs, p(vd), p(vu), p(vl), p(b["pr_diag"]), p(b["pr_upper"]),
+                                 p(b["pr_lower"]), p(b["pl_diag"]), p(b["pl_upper"]), p(b["pg_diag"]),
+                                 p(b["pg_upper"]), p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]),
+                                 p(b["bl_diag"]), p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]), p(ws), nbytes, st)
+        _lib.check(rc, "negf_w_assemble")
+        nbytes = lib.negf_w_obc_workspace_bytes(n_e, self.bs)
+        ws = _lib.workspace(nbytes, self.dev)
+        rc = lib.negf_w_obc_apply(n_e, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]),
+                                  p(b["bl_diag"]), p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]),
+                                  o.surface_tol, 100, o.stein_tol, o.stein_max_iter, p(b["obc_status"]),
+                                  p(b["obc_iters"]), p(b["stein_status"]), p(b["stein_iters"]), p(ws), nbytes, st)
+        _lib.check(rc, "negf_w_obc_apply")
+        if check:
+            raise_on_obc_status(b["obc_status"].cpu().numpy(), b["obc_iters"].cpu().numpy(), None, 100,
+                                o.surface_tol, "W contact")
+            ss = b["stein_status"].cpu().numpy()
+            if np.any(ss == 4):
+                raise SpectralRadiusError("W boundary Stein operator not certified contractive (|a|_F >= 1)")
+            if np.any(ss):
+                raise ConvergenceError(f"geometric Stein did not reach tol {o.stein_tol} in {o.stein_max_iter} squarings")
+        nbytes = lib.negf_rgf_workspace_bytes(n_e, self.n_b, self.bs)
+        ws = _lib.workspace(nbytes, self.dev)
+        b["rgf_status"].zero_()
+        rc = lib.negf_rgf_selected_solve_batched(
+            n_e, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]), p(b["bl_diag"]),
+            p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]), p(b["wr_diag"]), p(b["wr_upper"]),
+            p(b["wr_lower"]), p(b["wl_diag"]), p(b["wl_upper"]), p(b["wg_diag"]), p(b["wg_upper"]), 1,
+            p(b["rgf_status"]), None, p(ws), nbytes, st)
+        _lib.check(rc, "negf_rgf_selected_solve_batched")
+        if check:
+            raise_on_status(b["rgf_status"])
+        return b
+
+
+@dataclass
+class ScbaState:
+    """Entry-major scattering self-energy (scba.py:459-489 SigmaState)."""
+
+    lesser: torch.Tensor
+    greater: torch.Tensor
+    ret_upper: torch.Tensor
+    ret_lower: torch.Tensor
+
+    @classmethod
+    def zeros(cls, n_entries: int, n_e: int, device) -> "ScbaState":
+        z = lambda: torch.zeros((n_entries, n_e), dtype=Z, device=device)
+        return cls(z(), z(), z(), z())
+
+    def as_tuple(self):
+        return self.lesser, self.greater, self.ret_upper, self.ret_lower
+
+
+def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOptions | None = None,
+             device="cuda", keep_g: bool = True, initial_sigma: ScbaState | None = None) -> dict:
+    """Single-GPU SCBA. ``h``/``v`` are (diag, upper, lower) block stacks;
+    ``v=None`` runs the ballistic single pass. Returns host arrays named like
+    ScbaResult fields (G of the last iteration's carrier solve when keep_g),
+    the mixed Sigma ('sigma_lesser', ...) and 'residuals'."""
+    options = options or ScbaOptions()
+    dev = torch.device(device)
+    energies = np.asarray(energies, dtype=float)
+    ne = len(energies)
+    de = (energies[-1] - energies[0]) / (ne - 1)
+    carrier = CarrierSolver(h, eta, contacts, options.surface_tol, device=dev)
+    n_b, bs = carrier.n_b, carrier.bs
+    lay = EntryLayout(n_b, bs, dev)
+    batch = options.batch or ne
+    sig = initial_sigma or ScbaState.zeros(lay.n_entries, ne, dev)
+    if v is None:
+        max_iter = 1
+    else:
+        max_iter = options.max_iter
+        screened = ScreenedSolver(v, options, dev)
+        if screened.n_b != n_b or screened.bs != bs:
+            raise ValueError("W blocking must match the carrier blocking (n_w == n_b, bs_w == bs)")
+    em = lambda: torch.empty((lay.n_entries, ne), dtype=Z, device=dev)
+    gl, gg = em(), em()
+    result: dict = {}
+    residuals = []
+    blocks = None
+    for it in range(max_iter):
+        g_host = {k: [] for k in RESULT_KEYS} if keep_g else None
+        # 1. carrier solve per energy batch
+        for e0 in range(0, ne, batch):
+            e1 = min(ne, e0 + batch)
+            nb_ = e1 - e0
+            if blocks is None or blocks["sr_diag"].shape[0] != nb_:
+                d, o = (nb_, n_b, bs, bs), (nb_, n_b - 1, bs, bs)
+                blocks = {k: torch.empty(d, dtype=Z, device=dev) for k in ("sr_diag", "sl_diag", "sg_diag")}
+                blocks.update({k: torch.empty(o, dtype=Z, device=dev) for k in
+                               ("sr_upper", "sr_lower", "sl_upper", "sg_upper")})
+            lay.unpack_retarded(sig.ret_upper, sig.ret_lower, e0, nb_, blocks["sr_diag"], blocks["sr_upper"],
+                                blocks["sr_lower"])
+            lay.unpack_lg(sig.lesser, e0, nb_, blocks["sl_diag"], blocks["sl_upper"])
+            lay.unpack_lg(sig.greater, e0, nb_, blocks["sg_diag"], blocks["sg_upper"])
+            b = carrier.solve(energies[e0:e1], sigma=blocks, n_e=nb_)
+            lay.pack(b["xl_diag"], b["xl_upper"], gl, e0)
+            lay.pack(b["xg_diag"], b["xg_upper"], gg, e0)
+            if keep_g:
+                for k, src in RESULT_KEYS.items():
+                    g_host[k].append(b[src].cpu().numpy())
+        if keep_g:
+            result = {k: np.concatenate(vv) for k, vv in g_host.items()}
+        if v is None:
+            residuals.append(0.0)
+            break
+        # 2. polarization
+        pl, pg, pru, prl = polarization(gl, gg, lay.diag, de)
+        # 3. screened interaction per batch
+        wl, wg = em(), em()
+        for e0 in range(0, ne, batch):
+            e1 = min(ne, e0 + batch)
+            nb_ = e1 - e0
+            wb = screened.buffers(nb_)
+            lay.unpack_retarded(pru, prl, e0, nb_, wb["pr_diag"], wb["pr_upper"], wb["pr_lower"])
+            lay.unpack_lg(pl, e0, nb_, wb["pl_diag"], wb["pl_upper"])
+            lay.unpack_lg(pg, e0, nb_, wb["pg_diag"], wb["pg_upper"])
+            wb = screened.solve(nb_)
+            lay.pack(wb["wl_diag"], wb["wl_upper"], wl, e0)
+            lay.pack(wb["wg_diag"], wb["wg_upper"], wg, e0)
+        del pl, pg, pru, prl
+        # 4. self-energy
+        raw = self_energy(gl, gg, wl, wg, None, lay.diag, de)
+        del wl, wg
+        # 5. mixing + residual (scba.py:1155-1177)
+        tr_old = [lay.traces(sig.lesser), lay.traces(sig.greater)]
+        rc = _lib.load().negf_mix(sig.lesser.numel(), options.mixing, *(x.data_ptr() for x in sig.as_tuple()),
+                                  *(x.data_ptr() for x in raw), _lib.stream_ptr(dev))
+        _lib.check(rc, "negf_mix")
+        tr_new = [lay.traces(sig.lesser), lay.traces(sig.greater)]
+        to = [t.cpu().numpy() for t in tr_old]
+        tn = [t.cpu().numpy() for t in tr_new]
+        delta = max(float(np.max(np.abs(a - b_))) for a, b_ in zip(tn, to))
+        scale = max(max(float(np.max(np.abs(a))) for a in to), max(float(np.max(np.abs(a))) for a in tn))
+        residuals.append(delta / (scale + 1e-300))
+        del raw
+        if residuals[-1] < options.tol:
+            break
+        if len(residuals) >= 11 and residuals[-1] > 5.0 * residuals[-11]:
+            raise ConvergenceError(f"residual grew from {residuals[-11]:.3e} to {residuals[-1]:.3e} over 10 iterations")
+    if v is not None:
+        for k, t in zip(("lesser", "greater", "ret_upper", "ret_lower"), sig.as_tuple()):
+            result["sigma_" + k] = t.cpu().numpy()
+    result["residuals"] = np.asarray(residuals)
+    result["state"] = sig
+    return result

@@ -1,0 +1,103 @@
+"""GPU parity of the full SCBA (GW) iteration and its layout/W stages
+against reference golden vectors and the pinned oracle. Bar: 1e-9 relative
+Frobenius per quantity (north_star)."""
+
+import numpy as np
+import pytest
+import torch
+
+import negf_oracle as orc
+from paper_2508_19138_b200.carrier import Contacts
+from paper_2508_19138_b200.scba import EntryLayout, ScbaOptions, ScreenedSolver, scba_run
+from test_oracle_golden import check_c1
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def t(a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def test_pack_unpack_match_oracle(cuda):
+    rng = np.random.default_rng(1)
+    n_b, bs, ne, tot = 5, 7, 9, 40
+    lay = EntryLayout(n_b, bs, cuda)
+    d = rng.standard_normal((ne, n_b, bs, bs)) + 1j * rng.standard_normal((ne, n_b, bs, bs))
+    u = rng.standard_normal((ne, n_b - 1, bs, bs)) + 1j * rng.standard_normal((ne, n_b - 1, bs, bs))
+    out = torch.zeros((lay.n_entries, tot), dtype=torch.complex128, device=cuda)
+    lay.pack(t(d, cuda), t(u, cuda), out, 13)
+    ref = orc.gather_entries(d, u)
+    np.testing.assert_array_equal(out[:, 13:13 + ne].cpu().numpy(), ref)
+    assert torch.count_nonzero(out[:, :13]).item() == 0
+    vals = rng.standard_normal((lay.n_entries, tot)) + 1j * rng.standard_normal((lay.n_entries, tot))
+    dd = torch.empty((ne, n_b, bs, bs), dtype=torch.complex128, device=cuda)
+    uu = torch.empty((ne, n_b - 1, bs, bs), dtype=torch.complex128, device=cuda)
+    ll = torch.empty_like(uu)
+    lay.unpack_lg(t(vals, cuda), 5, ne, dd, uu)
+    rd, ru = orc.scatter_lg(vals[:, 5:5 + ne], n_b, bs)
+    np.testing.assert_array_equal(dd.cpu().numpy(), rd)
+    np.testing.assert_array_equal(uu.cpu().numpy(), ru)
+    lo = rng.standard_normal((lay.n_entries, tot)) + 1j * rng.standard_normal((lay.n_entries, tot))
+    lay.unpack_retarded(t(vals, cuda), t(lo, cuda), 2, ne, dd, uu, ll)
+    rd, ru, rl = orc.scatter_retarded(vals[:, 2:2 + ne], lo[:, 2:2 + ne], n_b, bs)
+    np.testing.assert_array_equal(dd.cpu().numpy(), rd)
+    np.testing.assert_array_equal(uu.cpu().numpy(), ru)
+    np.testing.assert_array_equal(ll.cpu().numpy(), rl)
+
+
+@pytest.mark.parametrize("n_b,bs,ne", [(4, 6, 5), (6, 40, 3), (3, 80, 2)])
+def test_screened_solve_matches_oracle(cuda, n_b, bs, ne):
+    rng = np.random.default_rng(n_b * bs)
+    v = orc.coulomb_matrix(n_b, bs)
+    mk = lambda *s: 0.3 * (rng.standard_normal(s) + 1j * rng.standard_normal(s))
+    pr = (mk(ne, n_b, bs, bs) - 1j * np.eye(bs), mk(ne, n_b - 1, bs, bs), mk(ne, n_b - 1, bs, bs))
+    def lg():
+        d = mk(ne, n_b, bs, bs)
+        return 0.5 * (d - np.conj(np.swapaxes(d, -1, -2))), mk(ne, n_b - 1, bs, bs)
+    pl, pg = lg(), lg()
+    mw, srcs = orc.w_system(v, pr, pl, pg)
+    orc.w_closure(mw, srcs, 1e-8)
+    ref = orc.rgf_selected(*mw, srcs, symmetrize=True)
+    solver = ScreenedSolver(v, ScbaOptions(), cuda)
+    b = solver.buffers(ne)
+    for k, a in (("pr_diag", pr[0]), ("pr_upper", pr[1]), ("pr_lower", pr[2]), ("pl_diag", pl[0]),
+                 ("pl_upper", pl[1]), ("pg_diag", pg[0]), ("pg_upper", pg[1])):
+        b[k].copy_(t(a, cuda))
+    b = solver.solve(ne)
+    for k, rk in (("wr_diag", "xr_diag"), ("wr_upper", "xr_upper"), ("wl_diag", "x<_diag"),
+                  ("wl_upper", "x<_upper"), ("wg_diag", "x>_diag"), ("wg_upper", "x>_upper")):
+        assert rel(b[k].cpu().numpy(), ref[rk]) < TOL, k
+
+
+def test_scba_small_matches_reference_scba_run(golden, cuda):
+    """3 GW iterations, 6x4 chain + Coulomb, 32 energies (batches of 10)."""
+    g = golden("golden_scba_small.npz")
+    res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=3, tol=1e-12, batch=10), device=cuda)
+    for k in g.files:
+        if k.startswith(("ver_", "config")):
+            continue
+        assert rel(res[k], g[k]) < TOL, k
+
+
+def test_scba_c1_matches_reference_scba_run(golden, cuda):
+    """C1: 16 blocks x 32 orbitals, 128 energies, one GW iteration."""
+    g = golden("golden_scba_c1.npz")
+    res = scba_run(orc.chain_device(16, 32), orc.coulomb_matrix(16, 32), np.linspace(-2.0, 2.0, 128), 1e-3,
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=1, tol=1e-12, batch=64), device=cuda)
+    check_c1(res, g, tol=TOL)
+
+
+def test_scba_c1_matches_oracle_two_iterations(cuda):
+    """Second iteration (nonzero Sigma feeding the carrier assembly) vs the oracle."""
+    h, v = orc.chain_device(16, 32), orc.coulomb_matrix(16, 32)
+    e = np.linspace(-2.0, 2.0, 128)
+    ref = orc.scba(h, v, e, 1e-3, 0.1, -0.1, 0.05, max_iter=2)
+    res = scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=2, tol=1e-12), device=cuda)
+    for k in ref:
+        assert rel(res[k], ref[k]) < TOL, k

@@ -35,3 +35,23 @@ def test_python_binding_covers_header():
     from paper_2508_19138_b200 import _lib
 
     assert set(declared_symbols()) == set(_lib.exported_symbols())
+
+
+def _header_arity():
+    text = (ROOT / "include" / "negf_b200.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    out = {}
+    for m in re.finditer(r"\b(negf_[a-z0-9_]+)\s*\(([^)]*)\)\s*;", text):
+        args = m.group(2).strip()
+        out[m.group(1)] = 0 if args in ("", "void") else args.count(",") + 1
+    return out
+
+
+def test_python_binding_arity_matches_header():
+    """ctypes silently accepts extra arguments, so check every binding's
+    argument count against the C prototype."""
+    from paper_2508_19138_b200 import _lib
+
+    arity = _header_arity()
+    for name, (_, args) in _lib._SIGNATURES.items():
+        assert len(args) == arity[name], (name, len(args), arity[name])
