@@ -169,12 +169,20 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
         br[j] = v.x;
         bi[j] = dneg_if(v.y, conjB);
       }
+      // Phase-major issue order: the two DMMAs feeding the same accumulator
+      // are TM*TN*2 instructions apart, so the FP64 tensor pipe never waits
+      // on its own accumulation dependency.
 #pragma unroll
       for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
         for (int j = 0; j < CF::TN; ++j) {
           dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
           dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ar[i], bi[j]);
+        }
+#pragma unroll
+      for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+        for (int j = 0; j < CF::TN; ++j) {
           dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], nai[i], bi[j]);
           dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], br[j]);
         }

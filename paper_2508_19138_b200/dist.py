@@ -1,0 +1,102 @@
+"""Energy sharding and the energy <-> entry redistribution (the paper's E<->nnz
+transposition) over torch.distributed.
+
+Reference: ``energy_chunks`` (scba.py:243-249), ``transpose_distribution``
+(scba.py:342-368) and its 12 calls per iteration (scba.py:1028-1141). The
+reference moves every slab to every rank (gather + bcast, fully replicated);
+here each rank sends each peer exactly the slab that peer owns, in one
+``all_to_all_single`` per quantity (NCCL over NVLink on the GPU box, gloo in
+the CPU tests):
+
+* to_entry_major: local (n_entries, n_own_e) columns -> (n_own_entries, N_E)
+* to_energy_major: local (n_own_entries, N_E) rows -> (n_entries, n_own_e)
+
+Complex tensors travel as their float64 view.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+def energy_chunks(n: int, size: int) -> list[slice]:
+    """scba.py:243-249: contiguous near-even split."""
+    base, rem = divmod(n, size)
+    bounds = [0]
+    for r in range(size):
+        bounds.append(bounds[-1] + base + (1 if r < rem else 0))
+    return [slice(bounds[r], bounds[r + 1]) for r in range(size)]
+
+
+@dataclass
+class Comm:
+    """Rank/size + process group; size 1 makes every transpose an identity."""
+
+    rank: int = 0
+    size: int = 1
+    group: object = None
+
+    @classmethod
+    def from_env(cls, group=None) -> "Comm":
+        if dist.is_available() and dist.is_initialized():
+            return cls(dist.get_rank(group), dist.get_world_size(group), group)
+        return cls()
+
+    def allreduce_max(self, values: list[float], device) -> list[float]:
+        if self.size == 1:
+            return list(values)
+        t = torch.tensor(values, dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return t.tolist()
+
+
+class Transposer:
+    """E <-> nnz redistribution for one (n_entries, N_E) pattern."""
+
+    def __init__(self, comm: Comm, n_entries: int, n_e: int) -> None:
+        self.comm = comm
+        self.n_entries, self.n_e = n_entries, n_e
+        self.e_sl = energy_chunks(n_e, comm.size)
+        self.r_sl = energy_chunks(n_entries, comm.size)
+        self.own_e = self.e_sl[comm.rank]
+        self.own_r = self.r_sl[comm.rank]
+        self.n_own_e = self.own_e.stop - self.own_e.start
+        self.n_own_r = self.own_r.stop - self.own_r.start
+        self.bytes_moved = 0
+
+    def _a2a(self, send: torch.Tensor, in_splits: list[int], out_splits: list[int]) -> torch.Tensor:
+        sr = torch.view_as_real(send).reshape(-1)
+        recv = torch.empty(2 * sum(out_splits), dtype=torch.float64, device=send.device)
+        dist.all_to_all_single(recv, sr, [2 * s for s in out_splits], [2 * s for s in in_splits],
+                               group=self.comm.group)
+        self.bytes_moved += 16 * (sum(in_splits) - in_splits[self.comm.rank])
+        return torch.view_as_complex(recv.view(-1, 2))
+
+    def to_entry_major(self, cols: torch.Tensor) -> torch.Tensor:
+        """(n_entries, n_own_e) -> (n_own_entries, N_E)."""
+        if self.comm.size == 1:
+            return cols
+        P = self.comm.size
+        send = cols.contiguous()  # entry-chunk row blocks are contiguous
+        in_splits = [(s.stop - s.start) * self.n_own_e for s in self.r_sl]
+        out_splits = [self.n_own_r * (s.stop - s.start) for s in self.e_sl]
+        recv = self._a2a(send, in_splits, out_splits)
+        parts, off = [], 0
+        for s in range(P):
+            ne_s = self.e_sl[s].stop - self.e_sl[s].start
+            parts.append(recv[off:off + self.n_own_r * ne_s].view(self.n_own_r, ne_s))
+            off += self.n_own_r * ne_s
+        return torch.cat(parts, dim=1)
+
+    def to_energy_major(self, rows: torch.Tensor) -> torch.Tensor:
+        """(n_own_entries, N_E) -> (n_entries, n_own_e)."""
+        if self.comm.size == 1:
+            return rows
+        send = torch.cat([rows[:, s].contiguous().view(-1) for s in self.e_sl])
+        in_splits = [self.n_own_r * (s.stop - s.start) for s in self.e_sl]
+        out_splits = [(s.stop - s.start) * self.n_own_e for s in self.r_sl]
+        recv = self._a2a(send, in_splits, out_splits)
+        return recv.view(self.n_entries, self.n_own_e)

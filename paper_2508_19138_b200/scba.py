@@ -29,6 +29,7 @@ import torch
 from . import _lib
 from .carrier import RESULT_KEYS, CarrierSolver, Contacts
 from .conv import polarization, self_energy
+from .dist import Comm, Transposer
 from .errors import ConvergenceError, SpectralRadiusError
 from .obc import raise_on_obc_status
 from .rgf import raise_on_status
@@ -194,12 +195,20 @@ class ScbaState:
 
 
 def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOptions | None = None,
-             device="cuda", keep_g: bool = True, initial_sigma: ScbaState | None = None) -> dict:
-    """Single-GPU SCBA. ``h``/``v`` are (diag, upper, lower) block stacks;
-    ``v=None`` runs the ballistic single pass. Returns host arrays named like
-    ScbaResult fields (G of the last iteration's carrier solve when keep_g),
-    the mixed Sigma ('sigma_lesser', ...) and 'residuals'."""
+             device="cuda", keep_g: bool = True, initial_sigma: ScbaState | None = None,
+             comm: Comm | None = None) -> dict:
+    """SCBA on one GPU or energy-sharded over ``comm`` (one rank per GPU).
+
+    ``h``/``v`` are (diag, upper, lower) block stacks; ``v=None`` runs the
+    ballistic single pass. Each rank solves its energy chunk
+    (energy_chunks, scba.py:243-249) and owns an entry chunk for the
+    convolutions; the E<->nnz switches are NCCL all-to-alls (dist.py).
+    Returns host arrays named like ScbaResult fields for this rank's
+    energies (G of the last iteration's carrier solve when keep_g), the
+    mixed Sigma columns of this rank's energies ('sigma_lesser', ...),
+    'residuals' (global) and 'energy_slice'."""
     options = options or ScbaOptions()
+    comm = comm or Comm()
     dev = torch.device(device)
     energies = np.asarray(energies, dtype=float)
     ne = len(energies)
@@ -207,8 +216,13 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     carrier = CarrierSolver(h, eta, contacts, options.surface_tol, device=dev)
     n_b, bs = carrier.n_b, carrier.bs
     lay = EntryLayout(n_b, bs, dev)
-    batch = options.batch or ne
-    sig = initial_sigma or ScbaState.zeros(lay.n_entries, ne, dev)
+    tr = Transposer(comm, lay.n_entries, ne)
+    own = tr.own_e
+    n_own = tr.n_own_e
+    my_e = energies[own]
+    diag_rows = lay.diag[tr.own_r].contiguous()
+    batch = options.batch or max(n_own, 1)
+    sig = initial_sigma or ScbaState.zeros(lay.n_entries, n_own, dev)
     if v is None:
         max_iter = 1
     else:
@@ -216,16 +230,16 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         screened = ScreenedSolver(v, options, dev)
         if screened.n_b != n_b or screened.bs != bs:
             raise ValueError("W blocking must match the carrier blocking (n_w == n_b, bs_w == bs)")
-    em = lambda: torch.empty((lay.n_entries, ne), dtype=Z, device=dev)
-    gl, gg = em(), em()
+    cols = lambda: torch.empty((lay.n_entries, n_own), dtype=Z, device=dev)
     result: dict = {}
     residuals = []
     blocks = None
     for it in range(max_iter):
         g_host = {k: [] for k in RESULT_KEYS} if keep_g else None
-        # 1. carrier solve per energy batch
-        for e0 in range(0, ne, batch):
-            e1 = min(ne, e0 + batch)
+        gl_c, gg_c = cols(), cols()
+        # 1. carrier solve per energy batch of this rank
+        for e0 in range(0, n_own, batch):
+            e1 = min(n_own, e0 + batch)
             nb_ = e1 - e0
             if blocks is None or blocks["sr_diag"].shape[0] != nb_:
                 d, o = (nb_, n_b, bs, bs), (nb_, n_b - 1, bs, bs)
@@ -236,36 +250,42 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
                                 blocks["sr_lower"])
             lay.unpack_lg(sig.lesser, e0, nb_, blocks["sl_diag"], blocks["sl_upper"])
             lay.unpack_lg(sig.greater, e0, nb_, blocks["sg_diag"], blocks["sg_upper"])
-            b = carrier.solve(energies[e0:e1], sigma=blocks, n_e=nb_)
-            lay.pack(b["xl_diag"], b["xl_upper"], gl, e0)
-            lay.pack(b["xg_diag"], b["xg_upper"], gg, e0)
+            b = carrier.solve(my_e[e0:e1], sigma=blocks, n_e=nb_)
+            lay.pack(b["xl_diag"], b["xl_upper"], gl_c, e0)
+            lay.pack(b["xg_diag"], b["xg_upper"], gg_c, e0)
             if keep_g:
                 for k, src in RESULT_KEYS.items():
                     g_host[k].append(b[src].cpu().numpy())
-        if keep_g:
+        if keep_g and n_own:
             result = {k: np.concatenate(vv) for k, vv in g_host.items()}
         if v is None:
             residuals.append(0.0)
             break
-        # 2. polarization
-        pl, pg, pru, prl = polarization(gl, gg, lay.diag, de)
-        # 3. screened interaction per batch
-        wl, wg = em(), em()
-        for e0 in range(0, ne, batch):
-            e1 = min(ne, e0 + batch)
+        # 2. G^<> to entry-major (all-to-all), polarization on own entry rows
+        gl, gg = tr.to_entry_major(gl_c), tr.to_entry_major(gg_c)
+        del gl_c, gg_c
+        p_rows = polarization(gl, gg, diag_rows, de)
+        pl, pg, pru, prl = (tr.to_energy_major(x) for x in p_rows)
+        del p_rows
+        # 3. screened interaction per batch of own energies
+        wl_c, wg_c = cols(), cols()
+        for e0 in range(0, n_own, batch):
+            e1 = min(n_own, e0 + batch)
             nb_ = e1 - e0
             wb = screened.buffers(nb_)
             lay.unpack_retarded(pru, prl, e0, nb_, wb["pr_diag"], wb["pr_upper"], wb["pr_lower"])
             lay.unpack_lg(pl, e0, nb_, wb["pl_diag"], wb["pl_upper"])
             lay.unpack_lg(pg, e0, nb_, wb["pg_diag"], wb["pg_upper"])
             wb = screened.solve(nb_)
-            lay.pack(wb["wl_diag"], wb["wl_upper"], wl, e0)
-            lay.pack(wb["wg_diag"], wb["wg_upper"], wg, e0)
+            lay.pack(wb["wl_diag"], wb["wl_upper"], wl_c, e0)
+            lay.pack(wb["wg_diag"], wb["wg_upper"], wg_c, e0)
         del pl, pg, pru, prl
-        # 4. self-energy
-        raw = self_energy(gl, gg, wl, wg, None, lay.diag, de)
-        del wl, wg
-        # 5. mixing + residual (scba.py:1155-1177)
+        wl, wg = tr.to_entry_major(wl_c), tr.to_entry_major(wg_c)
+        del wl_c, wg_c
+        # 4. self-energy on own entry rows, back to energy-major columns
+        raw = tuple(tr.to_energy_major(x) for x in self_energy(gl, gg, wl, wg, None, diag_rows, de))
+        del wl, wg, gl, gg
+        # 5. mixing + residual (scba.py:1155-1177), max over ranks
         tr_old = [lay.traces(sig.lesser), lay.traces(sig.greater)]
         rc = _lib.load().negf_mix(sig.lesser.numel(), options.mixing, *(x.data_ptr() for x in sig.as_tuple()),
                                   *(x.data_ptr() for x in raw), _lib.stream_ptr(dev))
@@ -273,8 +293,10 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         tr_new = [lay.traces(sig.lesser), lay.traces(sig.greater)]
         to = [t.cpu().numpy() for t in tr_old]
         tn = [t.cpu().numpy() for t in tr_new]
-        delta = max(float(np.max(np.abs(a - b_))) for a, b_ in zip(tn, to))
-        scale = max(max(float(np.max(np.abs(a))) for a in to), max(float(np.max(np.abs(a))) for a in tn))
+        mx = lambda arrs: max((float(np.max(np.abs(a))) if a.size else 0.0) for a in arrs)
+        delta = mx([a - b_ for a, b_ in zip(tn, to)])
+        scale = max(mx(to), mx(tn))
+        delta, scale = comm.allreduce_max([delta, scale], dev)
         residuals.append(delta / (scale + 1e-300))
         del raw
         if residuals[-1] < options.tol:
@@ -286,4 +308,6 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             result["sigma_" + k] = t.cpu().numpy()
     result["residuals"] = np.asarray(residuals)
     result["state"] = sig
+    result["energy_slice"] = own
+    result["transpose_bytes"] = tr.bytes_moved
     return result
