@@ -251,6 +251,11 @@ def run_native(args):
     g_ms, g_fl, g_by, g_n = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
     _lib.check(lib.negf_prof_query(0, ctypes.byref(g_ms), ctypes.byref(g_fl), ctypes.byref(g_by), ctypes.byref(g_n)),
                "negf_prof_query")
+    breakdown = {}
+    for cls, name in ((0, "zgemm_dmma"), (1, "zinv_panel_swap_rows_unpermute"), (2, "elementwise"), (3, "other")):
+        c_ms, c_fl, c_by, c_n = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
+        lib.negf_prof_query(cls, ctypes.byref(c_ms), ctypes.byref(c_fl), ctypes.byref(c_by), ctypes.byref(c_n))
+        breakdown[name] = {"ms": c_ms.value, "launches": c_n.value}
     lib.negf_prof_reset()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -312,12 +317,17 @@ def run_native(args):
                          "achieved_basis": f"algorithmic 8*M*N*K*batch flops of {g_n.value} ZGEMM launches / "
                                            f"their CUDA-event time ({gemm_avg_ms:.3f} ms avg) in the timed region",
                          "peak_basis": "cuBLAS ZGEMM 4096^3 measured live in this run (FP64 not in MEASURED_PEAKS.json)",
-                         "zgemm_share_of_step": g_ms.value / ms if ms > 0 else None},
+                         "zgemm_share_of_step": g_ms.value / ms if ms > 0 else None,
+                         "complex_product": "3M (Gauss): 3 real DMMA products per complex product; achieved counts "
+                                            "the standard 8*M*N*K complex flops, the DMMA pipe executes 6*M*N*K",
+                         "executed_dmma_tflops": achieved * 0.75,
+                         "executed_frac_of_dmma_peak": achieved * 0.75 / peak if peak else None},
             "e2e": {"value": n_e * world * args.e2e_steps / e2e_s if args.e2e_steps else None, "unit": UNIT,
                     "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "api": "paper_2508_19138_b200.carrier.ballistic_observables (host H in, host observables out)"},
             "gpu_launches": int(launches),
+            "device_time_breakdown": breakdown,
             "clocks": clk,
             "cpu_baseline": cpu,
             "observables_check": {"terminal_left": obs["terminal_left"], "terminal_right": obs["terminal_right"]},

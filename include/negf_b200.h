@@ -24,6 +24,14 @@ extern "C" {
 /* ABI version (major*100 + minor). */
 int negf_abi_version(void);
 
+/* Complex block-product algorithm of the DMMA GEMM (process-wide):
+ * 0 = 4 real products per complex product,
+ * 1 = 3M/Gauss (3 real products, 64x64 tiles), 2 = 3M with 64x32 tiles (default),
+ * 3 = 4M with 64x32 tiles, 4 = 3M with 32x64 tiles.
+ * 3M trades ~25% of the FP64 tensor work for a normwise error bound that is
+ * still O(eps |A||B|). */
+int negf_set_gemm_algo(int algo);
+
 /* ---- (1) selected solve -------------------------------------------------
  * Replaces negfgw.rgf.selected_solve (pkg/src/negfgw/rgf.py:232-243) and, with
  * symmetrize=1, the SelectedSolution.symmetrize() that scba_run applies

@@ -47,7 +47,7 @@ class CarrierSolver:
     """Batched G solve for a fixed Hamiltonian H (block tridiagonal)."""
 
     def __init__(self, h, eta: float, contacts: Contacts, surface_tol: float = 1e-8,
-                 max_sweeps: int = 100, device="cuda") -> None:
+                 max_sweeps: int = 100, device="cuda", streams: int = 1) -> None:
         self.dev = torch.device(device)
         self.lib = _lib.load()
         hd, hu, hl = h
@@ -61,6 +61,8 @@ class CarrierSolver:
         self.max_sweeps = int(max_sweeps)
         self._buf: dict | None = None
         self._n_e = 0
+        self.streams = streams
+        self._side_streams = [torch.cuda.Stream(self.dev) for _ in range(streams)] if streams > 1 else []
 
     def set_hamiltonian(self, h) -> None:
         """Copy new H blocks (host or device) into the resident device tensors."""
@@ -149,18 +151,43 @@ class CarrierSolver:
         if check:
             raise_on_obc_status(b["obc_status"].cpu().numpy(), b["obc_iters"].cpu().numpy(),
                                 b["obc_resid"].cpu().numpy(), self.max_sweeps, self.surface_tol, "G contact")
-        nbytes = lib.negf_rgf_workspace_bytes(ne, self.n_b, self.bs)
-        ws = _lib.workspace(nbytes, self.dev)
         b["rgf_status"].zero_()
-        rc = lib.negf_rgf_selected_solve_batched(
-            ne, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]),
-            p(b["bl_diag"]), p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]),
-            p(b["xr_diag"]), p(b["xr_upper"]), p(b["xr_lower"]), p(b["xl_diag"]), p(b["xl_upper"]),
-            p(b["xg_diag"]), p(b["xg_upper"]), 1, p(b["rgf_status"]), None, p(ws), nbytes, st)
-        _lib.check(rc, "negf_rgf_selected_solve_batched")
+        rgf_selected_solve_split(lib, b, ne, self.n_b, self.bs, self.dev, self.streams, self._side_streams)
         if check:
             raise_on_status(b["rgf_status"])
         return b
+
+
+def rgf_selected_solve_split(lib, b: dict, ne: int, n_b: int, bs: int, dev, streams: int, side_streams,
+                             prefix: tuple = ("m", "bl", "bg", "xr", "xl", "xg"), symmetrize: int = 1) -> None:
+    """RGF over the batch in ``b``, split into ``streams`` energy slices on
+    side streams so the latency-bound inversion panels of one slice overlap
+    the DMMA GEMMs of another (energies are independent)."""
+    m, bl, bg, xr, xl, xg = prefix
+    p = _lib.ptr
+    main = torch.cuda.current_stream(dev)
+    parts = streams if streams > 1 and ne >= 2 * streams else 1
+    bounds = [ne * k // parts for k in range(parts + 1)]
+    ev = main.record_event() if parts > 1 else None
+    for k in range(parts):
+        a, z = bounds[k], bounds[k + 1]
+        st_obj = side_streams[k] if parts > 1 else main
+        if ev is not None:
+            st_obj.wait_event(ev)
+        with torch.cuda.stream(st_obj):
+            nbytes = lib.negf_rgf_workspace_bytes(z - a, n_b, bs)
+            ws = _lib.workspace(nbytes, dev)
+            sl = lambda key: p(b[key][a:z])
+            rc = lib.negf_rgf_selected_solve_batched(
+                z - a, n_b, bs, sl(f"{m}_diag"), sl(f"{m}_upper"), sl(f"{m}_lower"),
+                sl(f"{bl}_diag"), sl(f"{bl}_upper"), sl(f"{bg}_diag"), sl(f"{bg}_upper"),
+                sl(f"{xr}_diag"), sl(f"{xr}_upper"), sl(f"{xr}_lower"), sl(f"{xl}_diag"), sl(f"{xl}_upper"),
+                sl(f"{xg}_diag"), sl(f"{xg}_upper"), symmetrize, p(b["rgf_status"][a:z]), None, p(ws), nbytes,
+                st_obj.cuda_stream)
+            _lib.check(rc, "negf_rgf_selected_solve_batched")
+    if parts > 1:
+        for k in range(parts):
+            main.wait_stream(side_streams[k])
 
 
 RESULT_KEYS = {

@@ -11,6 +11,12 @@ extern "C" {
 
 int negf_abi_version(void) { return 100; }
 
+int negf_set_gemm_algo(int algo) {
+  if (algo < 0 || algo > 4) return -1;
+  set_gemm_algo(algo);
+  return 0;
+}
+
 size_t negf_rgf_workspace_bytes(int n_e, int n_b, int bs) {
   return rgf_workspace_bytes(n_e, n_b, bs);
 }

@@ -23,6 +23,7 @@
 // i.e. one inverse transform yields both P^< and P^>.
 #include "../../include/negf_b200.h"
 #include "common.cuh"
+#include "prof.cuh"
 
 namespace negf {
 namespace {
@@ -243,10 +244,13 @@ int negf_conv_polarization(long long n_rows, int n_e, int L, const void* gl, con
   if (n_rows == 0) return 0;
   int rc = smem_setup((const void*)pol_kernel, L);
   if (rc) return rc;
-  pol_kernel<<<(unsigned)n_rows, threads_for(L), 2 * (size_t)L * sizeof(z_t), (cudaStream_t)stream>>>(
-      (const z_t*)gl, (const z_t*)gg, n_e, L, (const z_t*)tw, (const z_t*)kf, (const z_t*)kcf, diag,
-      make_double2(scale_re, scale_im), (z_t*)pl, (z_t*)pg, (z_t*)pr_up, (z_t*)pr_lo);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_pol_kernel(PROF_OTHER, (cudaStream_t)(stream));
+    pol_kernel<<<(unsigned)n_rows, threads_for(L), 2 * (size_t)L * sizeof(z_t), (cudaStream_t)stream>>>(
+        (const z_t*)gl, (const z_t*)gg, n_e, L, (const z_t*)tw, (const z_t*)kf, (const z_t*)kcf, diag,
+        make_double2(scale_re, scale_im), (z_t*)pl, (z_t*)pg, (z_t*)pr_up, (z_t*)pr_lo);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }
 
@@ -260,11 +264,14 @@ int negf_conv_sigma(long long n_rows, int n_e, int L, const void* gl, const void
   if (n_rows == 0) return 0;
   int rc = smem_setup((const void*)sigma_kernel, L);
   if (rc) return rc;
-  sigma_kernel<<<(unsigned)n_rows, threads_for(L), 2 * (size_t)L * sizeof(z_t), (cudaStream_t)stream>>>(
-      (const z_t*)gl, (const z_t*)gg, (const z_t*)wl, (const z_t*)wg, w_rows, n_e, L, (const z_t*)tw,
-      (const z_t*)kf, (const z_t*)kcf, diag, make_double2(scale_re, scale_im), (z_t*)sl, (z_t*)sg,
-      (z_t*)sr_up, (z_t*)sr_lo);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_sigma_kernel(PROF_OTHER, (cudaStream_t)(stream));
+    sigma_kernel<<<(unsigned)n_rows, threads_for(L), 2 * (size_t)L * sizeof(z_t), (cudaStream_t)stream>>>(
+        (const z_t*)gl, (const z_t*)gg, (const z_t*)wl, (const z_t*)wg, w_rows, n_e, L, (const z_t*)tw,
+        (const z_t*)kf, (const z_t*)kcf, diag, make_double2(scale_re, scale_im), (z_t*)sl, (z_t*)sg,
+        (z_t*)sr_up, (z_t*)sr_lo);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }
 
@@ -277,10 +284,13 @@ int negf_convolve_energy(long long n_rows, int n_e, int L, const void* x1, const
   if (n_rows == 0) return 0;
   int rc = smem_setup((const void*)conv_kernel, L);
   if (rc) return rc;
-  conv_kernel<<<(unsigned)n_rows, threads_for(L), 2 * (size_t)L * sizeof(z_t), (cudaStream_t)stream>>>(
-      (const z_t*)x1, (const z_t*)x2, n_e, L, mode, (const z_t*)tw, make_double2(scale_re, scale_im),
-      (z_t*)out);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_conv_kernel(PROF_OTHER, (cudaStream_t)(stream));
+    conv_kernel<<<(unsigned)n_rows, threads_for(L), 2 * (size_t)L * sizeof(z_t), (cudaStream_t)stream>>>(
+        (const z_t*)x1, (const z_t*)x2, n_e, L, mode, (const z_t*)tw, make_double2(scale_re, scale_im),
+        (z_t*)out);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }
 
@@ -293,9 +303,12 @@ int negf_retarded_from_lg(long long n_rows, int n_e, int L, const void* x_lesser
   if (n_rows == 0) return 0;
   int rc = smem_setup((const void*)ret_kernel, L);
   if (rc) return rc;
-  ret_kernel<<<(unsigned)n_rows, threads_for(L), 2 * (size_t)L * sizeof(z_t), (cudaStream_t)stream>>>(
-      (const z_t*)x_lesser, (const z_t*)x_greater, n_e, L, (const z_t*)tw, (const z_t*)kf, (z_t*)out);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_ret_kernel(PROF_OTHER, (cudaStream_t)(stream));
+    ret_kernel<<<(unsigned)n_rows, threads_for(L), 2 * (size_t)L * sizeof(z_t), (cudaStream_t)stream>>>(
+        (const z_t*)x_lesser, (const z_t*)x_greater, n_e, L, (const z_t*)tw, (const z_t*)kf, (z_t*)out);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }
 

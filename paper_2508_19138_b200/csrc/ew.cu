@@ -1,6 +1,7 @@
 // Elementwise block kernels (HBM-bound; 32x32 tiles staged through smem so
 // the conjugate-transposed reads stay coalesced).
 #include "ew.cuh"
+#include "prof.cuh"
 
 namespace negf {
 
@@ -104,6 +105,7 @@ int ew_group_launch(const EwGroup& g, cudaStream_t stream) {
   if (mb == 0) return 0;
   const int tiles = ((g.rows + TILE - 1) / TILE) * ((g.cols + TILE - 1) / TILE);
   dim3 grid(tiles, mb, g.n), block(TILE, 8);
+  ProfScope ps_(PROF_EW, stream);
   ew_kernel<<<grid, block, 0, stream>>>(g);
   NEGF_LAUNCHED();
   return 0;
@@ -113,6 +115,7 @@ int antiherm_inplace(z_t* X, long long sX, int n, int batch, cudaStream_t stream
   if (batch <= 0) return 0;
   const int nt = (n + TILE - 1) / TILE;
   dim3 grid(nt * (nt + 1) / 2, batch), block(TILE, 8);
+  ProfScope ps_(PROF_EW, stream);
   antiherm_kernel<<<grid, block, 0, stream>>>(X, sX, n);
   NEGF_LAUNCHED();
   return 0;
@@ -121,6 +124,7 @@ int antiherm_inplace(z_t* X, long long sX, int n, int batch, cudaStream_t stream
 int add_identity(z_t* Y, long long sY, int n, int batch, double2 s, cudaStream_t stream) {
   if (batch <= 0) return 0;
   dim3 grid((n + 127) / 128, batch);
+  ProfScope ps_(PROF_EW, stream);
   add_identity_kernel<<<grid, 128, 0, stream>>>(Y, sY, n, s);
   NEGF_LAUNCHED();
   return 0;

@@ -2,6 +2,7 @@
 // 1155-1167, _diag_traces :1251-1255), on the entry-major state.
 #include "../../include/negf_b200.h"
 #include "common.cuh"
+#include "prof.cuh"
 
 namespace negf {
 namespace {
@@ -47,10 +48,13 @@ int negf_mix(long long n, double alpha, void* s_lesser, void* s_greater, void* s
   if (n == 0) return 0;
   int grid = (int)((n + 255) / 256);
   if (grid > 148 * 16) grid = 148 * 16;
-  mix_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
-      (z_t*)s_lesser, (z_t*)s_greater, (z_t*)s_ret_up, (z_t*)s_ret_lo, (const z_t*)r_lesser,
-      (const z_t*)r_greater, (const z_t*)r_ret_up, (const z_t*)r_ret_lo, n, alpha);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_mix_kernel(PROF_OTHER, (cudaStream_t)(stream));
+    mix_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (z_t*)s_lesser, (z_t*)s_greater, (z_t*)s_ret_up, (z_t*)s_ret_lo, (const z_t*)r_lesser,
+        (const z_t*)r_greater, (const z_t*)r_ret_up, (const z_t*)r_ret_lo, n, alpha);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }
 
@@ -59,8 +63,11 @@ int negf_diag_traces(const void* x, long long ld, int n_e, const long long* diag
   if (!x || !diag_rows || !tr || n_e < 0 || n_b < 1 || bs < 1) return -1;
   if (n_e == 0) return 0;
   dim3 grid((n_e + 127) / 128, n_b);
-  trace_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>((const z_t*)x, ld, n_e, diag_rows, bs, (z_t*)tr);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_trace_kernel(PROF_OTHER, (cudaStream_t)(stream));
+    trace_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>((const z_t*)x, ld, n_e, diag_rows, bs, (z_t*)tr);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }
 

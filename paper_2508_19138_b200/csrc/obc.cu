@@ -16,6 +16,7 @@
 // mask freezes problems the moment they meet the reference's stopping test,
 // so every problem stops at exactly the sweep the reference would.
 #include "ew.cuh"
+#include "prof.cuh"
 #include "obc.cuh"
 #include "zgemm.cuh"
 #include "zinv.cuh"
@@ -247,8 +248,11 @@ int sancho_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs,
   NEGF_CUDA_CHECK(cudaMemcpyAsync(al, n, bytes, cudaMemcpyDeviceToDevice, st));
   NEGF_CUDA_CHECK(cudaMemcpyAsync(be, np, bytes, cudaMemcpyDeviceToDevice, st));
   NEGF_CUDA_CHECK(cudaMemsetAsync(inv_st, 0, sizeof(int) * batch, st));
-  sancho_init_kernel<<<batch, 256, 0, st>>>(n, np, bs, scale, active, status, iters);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_sancho_init_kernel(PROF_OTHER, (cudaStream_t)(st));
+    sancho_init_kernel<<<batch, 256, 0, st>>>(n, np, bs, scale, active, status, iters);
+    NEGF_LAUNCHED();
+  }
   InvAux aux;
   aux.status = inv_st; aux.status_code = 1; aux.u_spread = nullptr; aux.spread_stride = 0;
   aux.active = active;
@@ -286,9 +290,12 @@ int sancho_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs,
     std::swap(al, al2);
     std::swap(be, be2);
     NEGF_CUDA_CHECK(cudaMemsetAsync(n_act, 0, sizeof(int), st));
-    sancho_check_kernel<<<batch, 256, 0, st>>>(al, be, bs, tol, scale, active, inv_st, status, iters,
-                                               it, n_act);
-    NEGF_LAUNCHED();
+    {
+      ProfScope ps_sancho_check_kernel(PROF_OTHER, (cudaStream_t)(st));
+      sancho_check_kernel<<<batch, 256, 0, st>>>(al, be, bs, tol, scale, active, inv_st, status, iters,
+                                                 it, n_act);
+      NEGF_LAUNCHED();
+    }
     NEGF_CUDA_CHECK(cudaMemcpyAsync(&h_active, n_act, sizeof(int), cudaMemcpyDeviceToHost, st));
     NEGF_CUDA_CHECK(cudaStreamSynchronize(st));
     if (h_active == 0) break;
@@ -309,8 +316,11 @@ int sancho_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs,
   RC(zgemm_group_launch(G3, st));
   RC(zinv_batched(tb, n2, bs, g, n2, bs, bs, batch, aux2, inv_ws, inv_bytes, st));
   const double thr = 10.0 * (tol > 1e-14 ? tol : 1e-14);
-  sancho_finish_kernel<<<batch, 256, 0, st>>>(x, g, bs, thr, active, inv_st, status, resid);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_sancho_finish_kernel(PROF_OTHER, (cudaStream_t)(st));
+    sancho_finish_kernel<<<batch, 256, 0, st>>>(x, g, bs, thr, active, inv_st, status, resid);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }
 
@@ -364,15 +374,21 @@ int g_obc_apply(const GObcArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
   RC(zgemm_launch(d, st));
   const int tiles = ((bs + 31) / 32) * ((bs + 31) / 32);
   dim3 grid(tiles, ne), block(32, 8);
-  g_corner_kernel<<<grid, block, 0, st>>>(sig, bs, a.f_left, a.m_diag, a.bl_diag, a.bg_diag, sd,
-                                          a.sl_left, a.sg_left);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_g_corner_kernel(PROF_OTHER, (cudaStream_t)(st));
+    g_corner_kernel<<<grid, block, 0, st>>>(sig, bs, a.f_left, a.m_diag, a.bl_diag, a.bg_diag, sd,
+                                            a.sl_left, a.sg_left);
+    NEGF_LAUNCHED();
+  }
   const long long cc = (long long)(nb - 1) * n2;
-  g_corner_kernel<<<grid, block, 0, st>>>(sig + hn, bs, a.f_right, a.m_diag + cc,
-                                          a.bl_diag ? a.bl_diag + cc : nullptr,
-                                          a.bg_diag ? a.bg_diag + cc : nullptr, sd, a.sl_right,
-                                          a.sg_right);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_g_corner_kernel(PROF_OTHER, (cudaStream_t)(st));
+    g_corner_kernel<<<grid, block, 0, st>>>(sig + hn, bs, a.f_right, a.m_diag + cc,
+                                            a.bl_diag ? a.bl_diag + cc : nullptr,
+                                            a.bg_diag ? a.bg_diag + cc : nullptr, sd, a.sl_right,
+                                            a.sg_right);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }
 
@@ -400,8 +416,11 @@ int sigma_lg_obc_batched(const z_t* x, const z_t* n, const z_t* np, const double
   RC(zgemm_launch(d, st));
   const int tiles = ((bs + 31) / 32) * ((bs + 31) / 32);
   dim3 grid(tiles, batch), block(32, 8);
-  sigma_lg_kernel<<<grid, block, 0, st>>>(sig, bs, f, sl, sg);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_sigma_lg_kernel(PROF_OTHER, (cudaStream_t)(st));
+    sigma_lg_kernel<<<grid, block, 0, st>>>(sig, bs, f, sl, sg);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }
 
@@ -411,8 +430,11 @@ int g_assemble(const GAssembleArgs& a, cudaStream_t st) {
   int bx = (int)((n2 + 255) / 256);
   if (bx > 64) bx = 64;
   dim3 grid(bx, a.n_b, a.n_e);
-  g_assemble_kernel<<<grid, 256, 0, st>>>(a);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_g_assemble_kernel(PROF_OTHER, (cudaStream_t)(st));
+    g_assemble_kernel<<<grid, 256, 0, st>>>(a);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }
 

@@ -8,6 +8,7 @@
 // replicates every G block of every energy to every rank (scba.py:1258-1308).
 #include "../../include/negf_b200.h"
 #include "common.cuh"
+#include "prof.cuh"
 
 namespace negf {
 namespace {
@@ -91,10 +92,13 @@ extern "C" int negf_observables(int n_e, int n_b, int bs, const void* gr_diag,
   if (current_spectrum && (!gl_upper || !h_upper)) return -1;
   if (n_e == 0) return 0;
   dim3 grid(n_b, n_e);
-  observables_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
-      n_b, bs, (const z_t*)gr_diag, (const z_t*)gl_diag, (const z_t*)gg_diag, (const z_t*)gl_upper,
-      (const z_t*)h_upper, (const z_t*)sl_left, (const z_t*)sg_left, (const z_t*)sl_right,
-      (const z_t*)sg_right, (z_t*)tr_gr, (z_t*)tr_gl, current_spectrum, (z_t*)terminal);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_observables_kernel(PROF_OTHER, (cudaStream_t)(stream));
+    observables_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+        n_b, bs, (const z_t*)gr_diag, (const z_t*)gl_diag, (const z_t*)gg_diag, (const z_t*)gl_upper,
+        (const z_t*)h_upper, (const z_t*)sl_left, (const z_t*)sg_left, (const z_t*)sl_right,
+        (const z_t*)sg_right, (z_t*)tr_gr, (z_t*)tr_gl, current_spectrum, (z_t*)terminal);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }

@@ -16,6 +16,7 @@
 // contiguous) are read and written coalesced.
 #include "../../include/negf_b200.h"
 #include "common.cuh"
+#include "prof.cuh"
 
 namespace negf {
 namespace {
@@ -146,9 +147,12 @@ int negf_pack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* x_diag,
   if (n_e == 0) return 0;
   Pat p = make_pat(n_b, bs);
   dim3 grid((unsigned)((p.n_entries + T - 1) / T), (n_e + T - 1) / T), block(T, 8);
-  pack_lg_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(p, tri_q, n_e, (const z_t*)x_diag,
-                                                           (const z_t*)x_upper, (z_t*)out, ld, e0);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_pack_lg_kernel(PROF_OTHER, (cudaStream_t)(stream));
+    pack_lg_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(p, tri_q, n_e, (const z_t*)x_diag,
+                                                             (const z_t*)x_upper, (z_t*)out, ld, e0);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }
 
@@ -159,9 +163,12 @@ int negf_unpack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* in, l
   if (n_e == 0) return 0;
   Pat p = make_pat(n_b, bs);
   dim3 grid((unsigned)((p.n_entries + T - 1) / T), (n_e + T - 1) / T), block(T, 8);
-  unpack_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(p, tri_q, n_e, (const z_t*)in, nullptr, ld,
-                                                          e0, 0, (z_t*)x_diag, (z_t*)x_upper, nullptr);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_unpack_kernel(PROF_OTHER, (cudaStream_t)(stream));
+    unpack_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(p, tri_q, n_e, (const z_t*)in, nullptr, ld,
+                                                            e0, 0, (z_t*)x_diag, (z_t*)x_upper, nullptr);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }
 
@@ -175,10 +182,13 @@ int negf_unpack_retarded(int n_e, int n_b, int bs, const int* tri_q, const void*
   if (n_e == 0) return 0;
   Pat p = make_pat(n_b, bs);
   dim3 grid((unsigned)((p.n_entries + T - 1) / T), (n_e + T - 1) / T), block(T, 8);
-  unpack_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(
-      p, tri_q, n_e, (const z_t*)in_upper, (const z_t*)in_lower, ld, e0, 1, (z_t*)x_diag,
-      (z_t*)x_upper, (z_t*)x_lower);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_unpack_kernel(PROF_OTHER, (cudaStream_t)(stream));
+    unpack_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(
+        p, tri_q, n_e, (const z_t*)in_upper, (const z_t*)in_lower, ld, e0, 1, (z_t*)x_diag,
+        (z_t*)x_upper, (z_t*)x_lower);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }
 

@@ -13,3 +13,13 @@ int prof_begin(int cls, cudaStream_t st);
 void prof_end(int token, cudaStream_t st, double flops, double bytes);
 
 }  // namespace negf
+
+namespace negf {
+// RAII span: CUDA events around the launches made while it is alive.
+struct ProfScope {
+  int tok;
+  cudaStream_t st;
+  ProfScope(int cls, cudaStream_t s) : tok(prof_begin(cls, s)), st(s) {}
+  ~ProfScope() { prof_end(tok, st, 0.0, 0.0); }
+};
+}  // namespace negf

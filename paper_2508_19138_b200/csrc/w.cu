@@ -18,6 +18,7 @@
 // weak-V inputs both agree to ~1e-16).
 #include "../../include/negf_b200.h"
 #include "ew.cuh"
+#include "prof.cuh"
 #include "obc.cuh"
 #include "zgemm.cuh"
 
@@ -315,8 +316,11 @@ int stein_batched(const z_t* a, const z_t* q, z_t* w, int n_side, int n_kind, in
   int* n_act = (int*)p;
   NEGF_CUDA_CHECK(cudaMemcpyAsync(ak, a, n_side * blk, cudaMemcpyDeviceToDevice, st));
   NEGF_CUDA_CHECK(cudaMemcpyAsync(w, q, (size_t)n_kind * n_side * blk, cudaMemcpyDeviceToDevice, st));
-  stein_init_kernel<<<n_side, 256, 0, st>>>(a, n2, n_side, n_kind, active, iters, status);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_stein_init_kernel(PROF_OTHER, (cudaStream_t)(st));
+    stein_init_kernel<<<n_side, 256, 0, st>>>(a, n2, n_side, n_kind, active, iters, status);
+    NEGF_LAUNCHED();
+  }
   for (int it = 1; it <= max_iter; ++it) {
     ZGemmGroup g;
     g.n = n_kind;
@@ -338,14 +342,20 @@ int stein_batched(const z_t* a, const z_t* q, z_t* w, int n_side, int n_kind, in
     }
     RC(zgemm_group_launch(g, st));
     NEGF_CUDA_CHECK(cudaMemsetAsync(n_act, 0, sizeof(int), st));
-    stein_step_kernel<<<n_kind * n_side, 256, 0, st>>>(w, U, n2, tol, active, iters, it, n_act);
-    NEGF_LAUNCHED();
+    {
+      ProfScope ps_stein_step_kernel(PROF_OTHER, (cudaStream_t)(st));
+      stein_step_kernel<<<n_kind * n_side, 256, 0, st>>>(w, U, n2, tol, active, iters, it, n_act);
+      NEGF_LAUNCHED();
+    }
     int h = 0;
     NEGF_CUDA_CHECK(cudaMemcpyAsync(&h, n_act, sizeof(int), cudaMemcpyDeviceToHost, st));
     NEGF_CUDA_CHECK(cudaStreamSynchronize(st));
     if (h == 0) break;
-    or_mask_kernel<<<(n_side + 127) / 128, 128, 0, st>>>(active, n_side, n_kind, side_active);
-    NEGF_LAUNCHED();
+    {
+      ProfScope ps_or_mask_kernel(PROF_OTHER, (cudaStream_t)(st));
+      or_mask_kernel<<<(n_side + 127) / 128, 128, 0, st>>>(active, n_side, n_kind, side_active);
+      NEGF_LAUNCHED();
+    }
     ZGemmDesc d = zdesc_default();  // a_k <- a_k^2 where any kind is still active
     d.M = bs; d.N = bs; d.batch = n_side;
     d.t[0] = zterm(ak, n2, bs, OP_N, ak, n2, bs, OP_N, bs);
@@ -355,8 +365,11 @@ int stein_batched(const z_t* a, const z_t* q, z_t* w, int n_side, int n_kind, in
     RC(zgemm_launch(d, st));
     NEGF_CUDA_CHECK(cudaMemcpyAsync(ak, ak2, n_side * blk, cudaMemcpyDeviceToDevice, st));
   }
-  stein_finish_kernel<<<(n_kind * n_side + 127) / 128, 128, 0, st>>>(active, status, n_kind * n_side);
-  NEGF_LAUNCHED();
+  {
+    ProfScope ps_stein_finish_kernel(PROF_OTHER, (cudaStream_t)(st));
+    stein_finish_kernel<<<(n_kind * n_side + 127) / 128, 128, 0, st>>>(active, status, n_kind * n_side);
+    NEGF_LAUNCHED();
+  }
   return 0;
 }
 

@@ -85,6 +85,8 @@ inline ZTerm zterm(const z_t* A, long long sA, int lda, int opA, const z_t* B, l
 
 // Launch a group of GEMM problems (same tile config) on `stream`.
 int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream);
+int gemm_algo();
+void set_gemm_algo(int a);
 int zgemm_launch(const ZGemmDesc& d, cudaStream_t stream);
 
 }  // namespace negf

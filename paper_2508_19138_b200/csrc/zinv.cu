@@ -325,6 +325,7 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr = true;
     }
+    ProfScope ps_(PROF_ZINV, stream);
     zinv_small_kernel<<<batch, 256, smem, stream>>>(S, sS, lds, X, sX, ldx, n, aux);
     NEGF_LAUNCHED();
     return 0;
@@ -350,11 +351,14 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
   if (panel_smem > 220 * 1024) return -5;
   for (int k0 = 0; k0 < n; k0 += nb) {
     const int w = nb < n - k0 ? nb : n - k0;  // last panel may be narrower
+    dim3 g((n + 127) / 128, batch);
+    {
+    ProfScope ps_(PROF_ZINV, stream);
     zinv_panel_kernel<<<batch, 256, panel_smem, stream>>>(S, sS, n, k0, w, ipiv, pinv, umm, aux);
     NEGF_LAUNCHED();
-    dim3 g((n + 127) / 128, batch);
     zinv_swap_kernel<<<g, 128, 0, stream>>>(S, sS, n, k0, w, ipiv, Cp, R, aux.active);
     NEGF_LAUNCHED();
+    }
     // T = Pinv R, staged in the caller's destination X (w x n per matrix;
     // X is only written for real by the final unpermute kernel).
     ZGemmGroup grp;
@@ -400,9 +404,11 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
     }
     rc = zgemm_group_launch(grp, stream);
     if (rc) return rc;
+    ProfScope ps2_(PROF_ZINV, stream);
     zinv_rows_kernel<<<g, 128, 0, stream>>>(S, sS, n, k0, w, T, sX, pinv, aux.active);
     NEGF_LAUNCHED();
   }
+  ProfScope ps3_(PROF_ZINV, stream);
   zinv_unpermute_kernel<<<batch, 256, n * sizeof(int), stream>>>(S, sS, n, ipiv, umm, X, sX, ldx,
                                                                  aux);
   NEGF_LAUNCHED();

@@ -23,7 +23,8 @@ def crand(shape, gen, dev):
 @pytest.mark.parametrize("m,n,k", [(8, 8, 4), (5, 7, 3), (32, 32, 32), (64, 64, 64), (100, 37, 70),
                                    (256, 256, 256), (33, 65, 129), (1, 1, 1)])
 @pytest.mark.parametrize("op_a,op_b", [(0, 0), (0, 3), (3, 0), (1, 2), (2, 1), (3, 3)])
-def test_zgemm_matches_torch(cuda, m, n, k, op_a, op_b):
+@pytest.mark.parametrize("algo", [0, 1, 2, 3, 4])
+def test_zgemm_matches_torch(cuda, m, n, k, op_a, op_b, algo):
     g = torch.Generator().manual_seed(m * 1000 + n * 10 + k + op_a * 7 + op_b)
     batch = 3
     a_shape = (batch, m, k) if op_a in (0, 2) else (batch, k, m)
@@ -32,11 +33,13 @@ def test_zgemm_matches_torch(cuda, m, n, k, op_a, op_b):
     d = torch.empty((batch, m, n), dtype=torch.complex128, device=cuda)
     alpha, beta = complex(0.7, -0.3), complex(-1.1, 0.4)
     lib = _lib.load()
+    assert lib.negf_set_gemm_algo(algo) == 0
     rc = lib.negf_zgemm_batched(m, n, k, batch, alpha.real, alpha.imag,
                                 a.data_ptr(), a[0].numel(), a.shape[-1], op_a,
                                 b.data_ptr(), b[0].numel(), b.shape[-1], op_b,
                                 beta.real, beta.imag, c.data_ptr(), m * n, n,
                                 d.data_ptr(), m * n, n, _lib.stream_ptr())
+    lib.negf_set_gemm_algo(2)
     assert rc == 0
     ref = alpha * (OPS[op_a](a) @ OPS[op_b](b)) + beta * c
     err = (d - ref).abs().max().item() / max(ref.abs().max().item(), 1e-300)
