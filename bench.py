@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-procs", type=int, default=0, help="0 = all host cores")
+    ap.add_argument("--scgw", default="32x128x512", help="n_blocks x block_size x energies-per-rank of the "
+                    "SCGW-iteration measurement ('' to skip)")
     return ap.parse_args()
 
 
@@ -248,14 +250,21 @@ def run_native(args):
     solver.check_status(b)
     import ctypes
 
-    g_ms, g_fl, g_by, g_n = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
-    _lib.check(lib.negf_prof_query(0, ctypes.byref(g_ms), ctypes.byref(g_fl), ctypes.byref(g_by), ctypes.byref(g_n)),
-               "negf_prof_query")
     breakdown = {}
-    for cls, name in ((0, "zgemm_dmma"), (1, "zinv_panel_swap_rows_unpermute"), (2, "elementwise"), (3, "other")):
+    tot = [0.0, 0.0, 0]
+    for cls, name in ((0, "zgemm_dmma_k_gt_32"), (4, "zgemm_dmma_k_le_32 (inversion sweeps)"),
+                      (1, "zinv_panel_swap_rows_unpermute"), (2, "elementwise"), (3, "other")):
         c_ms, c_fl, c_by, c_n = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
-        lib.negf_prof_query(cls, ctypes.byref(c_ms), ctypes.byref(c_fl), ctypes.byref(c_by), ctypes.byref(c_n))
+        _lib.check(lib.negf_prof_query(cls, ctypes.byref(c_ms), ctypes.byref(c_fl), ctypes.byref(c_by),
+                                       ctypes.byref(c_n)), "negf_prof_query")
         breakdown[name] = {"ms": c_ms.value, "launches": c_n.value}
+        if c_fl.value > 0:
+            breakdown[name]["tflops_algorithmic"] = c_fl.value / (c_ms.value * 1e-3) / 1e12
+        if cls in (0, 4):
+            tot[0] += c_ms.value
+            tot[1] += c_fl.value
+            tot[2] += c_n.value
+    g_ms, g_fl, g_n = ctypes.c_double(tot[0]), ctypes.c_double(tot[1]), ctypes.c_longlong(tot[2])
     lib.negf_prof_reset()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -281,6 +290,11 @@ def run_native(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_s = float(t.item())
     d2h = ObservableAccumulator(n_e, n_b, de, dev).d2h_bytes()
+
+    del solver, acc, b
+    _lib._WS.clear()
+    torch.cuda.empty_cache()
+    scgw = run_scgw(args, dev, world, rank, barrier) if args.scgw else None
 
     # CPU baseline: oracle port on this host's cores (rank 0, N=1 only)
     cpu = None
@@ -326,6 +340,7 @@ def run_native(args):
                     "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "api": "paper_2508_19138_b200.carrier.ballistic_observables (host H in, host observables out)"},
+            "scgw_iteration": scgw,
             "gpu_launches": int(launches),
             "device_time_breakdown": breakdown,
             "clocks": clk,
@@ -335,6 +350,46 @@ def run_native(args):
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_scgw(args, dev, world, rank, barrier) -> dict:
+    """One full SCGW (GW) iteration -- carrier solve + OBC, polarization, W
+    (assembly, closure, RGF), self-energy, mixing -- energy-sharded over the
+    ranks with NCCL all-to-all E<->nnz transposes; weak scaling (energies per
+    rank fixed). Time = max over ranks of one iteration after one warm-up."""
+    import numpy as np
+    import torch
+
+    from paper_2508_19138_b200 import toys
+    from paper_2508_19138_b200.carrier import Contacts
+    from paper_2508_19138_b200.dist import Comm
+    from paper_2508_19138_b200.scba import ScbaOptions, scba_run
+
+    n_b, bs, ne_rank = (int(x) for x in args.scgw.split("x"))
+    w = WORKLOAD
+    e = np.linspace(w["e_min"], w["e_max"], ne_rank * world)
+    h, v = toys.chain_device(n_b, bs), toys.coulomb_matrix(n_b, bs)
+    comm = Comm.from_env()
+    opts = ScbaOptions(max_iter=2, tol=1e-300, batch=min(128, ne_rank))
+    contacts = Contacts(w["mu_left"], w["mu_right"], w["kT"])
+    barrier()
+    # two iterations; the second (warm buffers, nonzero Sigma) is the timed one
+    res = scba_run(h, v, e, w["eta"], contacts, opts, device=dev, keep_g=False, comm=comm, sigma_to_host=False)
+    dt = res["iteration_s"][-1]
+    t = torch.tensor([dt], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    flops = 2 * model_flops_per_energy(n_b, bs) * ne_rank * world  # G and W selected solves
+    return {"config": f"chain_device({n_b},{bs}) + coulomb_matrix, {ne_rank * world} energies "
+                      f"({ne_rank}/rank), 1 GW iteration, energy-sharded x{world}",
+            "iteration_s": dt, "energies_per_s": ne_rank * world / dt,
+            "timing": "host wall clock of the 2nd iteration (device-synchronised at both ends), max over ranks",
+            "rgf_tflops_model_GW": flops / dt / 1e12,
+            "transpose_bytes_rank0": int(res["transpose_bytes"]),
+            "residual": float(res["residuals"][-1])}
 
 
 # -- reference arm -----------------------------------------------------------------

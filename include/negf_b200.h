@@ -32,6 +32,12 @@ int negf_abi_version(void);
  * still O(eps |A||B|). */
 int negf_set_gemm_algo(int algo);
 
+/* Forward-sweep pipelining of negf_rgf_selected_solve_batched (process-wide,
+ * default 1): the Keldysh (lesser/greater) forward products run on an
+ * internal second stream so they overlap the retarded chain's pivoted
+ * inversions. 0 serialises everything on the caller's stream. */
+int negf_set_rgf_overlap(int on);
+
 /* ---- (1) selected solve -------------------------------------------------
  * Replaces negfgw.rgf.selected_solve (pkg/src/negfgw/rgf.py:232-243) and, with
  * symmetrize=1, the SelectedSolution.symmetrize() that scba_run applies

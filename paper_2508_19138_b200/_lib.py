@@ -25,6 +25,7 @@ _sz = C.c_size_t
 _SIGNATURES: dict[str, tuple] = {
     "negf_abi_version": (_i, []),
     "negf_set_gemm_algo": (_i, [_i]),
+    "negf_set_rgf_overlap": (_i, [_i]),
     "negf_rgf_workspace_bytes": (_sz, [_i, _i, _i]),
     "negf_rgf_selected_solve_batched": (
         _i,

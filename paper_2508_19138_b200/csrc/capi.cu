@@ -11,6 +11,11 @@ extern "C" {
 
 int negf_abi_version(void) { return 100; }
 
+int negf_set_rgf_overlap(int on) {
+  set_rgf_overlap_default(on ? 1 : 0);
+  return 0;
+}
+
 int negf_set_gemm_algo(int algo) {
   if (algo < 0 || algo > 4) return -1;
   set_gemm_algo(algo);
@@ -44,6 +49,7 @@ int negf_rgf_selected_solve_batched(int n_e, int n_b, int bs, const void* m_diag
   a.symmetrize = symmetrize;
   a.status = status;
   a.u_spread = u_spread;
+  a.overlap = rgf_overlap_default();
   return rgf_selected_solve(a, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 

@@ -5,7 +5,14 @@
 
 namespace negf {
 
-enum ProfClass : int { PROF_ZGEMM = 0, PROF_ZINV = 1, PROF_EW = 2, PROF_OTHER = 3, PROF_NCLASS = 4 };
+enum ProfClass : int {
+  PROF_ZGEMM = 0,        // DMMA GEMM launches with K > 32
+  PROF_ZINV = 1,         // inversion panel / swap / rows / unpermute kernels
+  PROF_EW = 2,
+  PROF_OTHER = 3,
+  PROF_ZGEMM_SMALLK = 4, // DMMA GEMM launches with K <= 32 (inversion sweeps)
+  PROF_NCLASS = 5
+};
 
 bool prof_enabled();
 // Returns a token; call prof_end with it after the launch(es).

@@ -32,7 +32,7 @@ namespace negf {
 
 namespace {
 
-constexpr int kTmpShared = 2;  // tA, tS
+constexpr int kTmpShared = 3;  // tA, tS, second tA buffer (forward pipeline)
 constexpr int kTmpKind = 6;    // k0..k5
 constexpr int kTmpTotal = kTmpShared + 2 * kTmpKind;
 
@@ -96,6 +96,10 @@ struct EGroup {
 
 }  // namespace
 
+static int g_overlap = 1;
+int rgf_overlap_default() { return g_overlap; }
+void set_rgf_overlap_default(int on) { g_overlap = on; }
+
 size_t rgf_workspace_bytes(int n_e, int n_b, int bs) {
   size_t tmp = align256(sizeof(z_t) * (size_t)kTmpTotal * n_e * bs * bs);
   return tmp + align256(zinv_workspace_bytes(bs, n_e));
@@ -149,64 +153,136 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
   EGroup E(bs);
 
   // ---------------- forward sweep ----------------
+  // Two-stream pipeline. The retarded chain (A_i, S_i, pivoted inverse) runs on
+  // the caller's stream `st`; the Keldysh forward products of step i run on an
+  // auxiliary stream `sk`, so the latency-bound inversion panels of step i+1
+  // overlap the lesser/greater GEMMs of step i. A_i is double-buffered
+  // (tA[i & 1]); events order the hand-offs:
+  //   evA[p]: A_i ready (R -> K)   evX[p]: x_i ready (R -> K)
+  //   evK[p]: step i's K work done, before R overwrites tA[p] at step i + 2.
+  cudaStream_t sk = st;
+  cudaEvent_t evA[2] = {nullptr, nullptr}, evX[2] = {nullptr, nullptr}, evK[2] = {nullptr, nullptr};
+  cudaEvent_t ev0 = nullptr;
+  const bool pipe = a.overlap && nk > 0 && n > 1;
+  struct Cleanup {
+    cudaStream_t* s;
+    cudaEvent_t* evs[4];
+    int counts[4];
+    ~Cleanup() {
+      for (int j = 0; j < 4; ++j)
+        for (int q = 0; q < counts[j]; ++q)
+          if (evs[j][q]) cudaEventDestroy(evs[j][q]);
+    }
+  } cleanup{nullptr, {evA, evX, evK, &ev0}, {2, 2, 2, 1}};
+  if (pipe) {
+    NEGF_CUDA_CHECK(cudaStreamCreateWithFlags(&sk, cudaStreamNonBlocking));
+    for (int j = 0; j < 2; ++j) {
+      NEGF_CUDA_CHECK(cudaEventCreateWithFlags(&evA[j], cudaEventDisableTiming));
+      NEGF_CUDA_CHECK(cudaEventCreateWithFlags(&evX[j], cudaEventDisableTiming));
+      NEGF_CUDA_CHECK(cudaEventCreateWithFlags(&evK[j], cudaEventDisableTiming));
+    }
+    NEGF_CUDA_CHECK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+    NEGF_CUDA_CHECK(cudaEventRecord(ev0, st));
+    NEGF_CUDA_CHECK(cudaStreamWaitEvent(sk, ev0, 0));
+  }
+  struct StreamGuard {
+    cudaStream_t s, main;
+    bool own;
+    ~StreamGuard() {
+      if (own) cudaStreamDestroy(s);
+    }
+  } sguard{sk, st, pipe};
+  z_t* tAb[2] = {tA, c.T(2)};
+
   // i = 0
   NEGF_CUDA_CHECK(cudaMemcpy2DAsync(tS, st1 * sizeof(z_t), Md(0), sd * sizeof(z_t),
                                     bs2 * sizeof(z_t), ne, cudaMemcpyDeviceToDevice, st));
   RC(invert_into(0));
+  if (pipe) {
+    NEGF_CUDA_CHECK(cudaEventRecord(evX[0], st));
+    NEGF_CUDA_CHECK(cudaStreamWaitEvent(sk, evX[0], 0));
+  }
   for (int q = 0; q < nk; ++q) {  // U = x_0 B_00
     int k = kinds[q];
     G.add(c.desc(c.term(Xd(0), sd, OP_N, Bd(k, 0), sd, OP_N), c.K(k, 0), st1));
   }
-  RC(G.run(st));
+  RC(G.run(sk));
   for (int q = 0; q < nk; ++q) {  // xl_0 = U x_0^dag
     int k = kinds[q];
     G.add(c.desc(c.term(c.K(k, 0), st1, OP_N, Xd(0), sd, OP_H), Ld(k, 0), sd));
   }
-  RC(G.run(st));
+  RC(G.run(sk));
+  if (pipe) NEGF_CUDA_CHECK(cudaEventRecord(evK[0], sk));
 
   for (int i = 1; i < n; ++i) {
-    // G1: A = M_{i,i-1} x_{i-1};  T1_k = M_{i,i-1} xl_{k,i-1}
-    G.add(c.desc(c.term(Ml(i - 1), so, OP_N, Xd(i - 1), sd, OP_N), tA, st1));
-    for (int q = 0; q < nk; ++q) {
-      int k = kinds[q];
-      G.add(c.desc(c.term(Ml(i - 1), so, OP_N, Ld(k, i - 1), sd, OP_N), c.K(k, 0), st1));
-    }
+    const int p = i & 1;
+    z_t* Ai = pipe ? tAb[p] : tA;
+    // --- retarded chain (stream st)
+    if (pipe && i >= 2) NEGF_CUDA_CHECK(cudaStreamWaitEvent(st, evK[p], 0));  // K done with tA[p]
+    G.add(c.desc(c.term(Ml(i - 1), so, OP_N, Xd(i - 1), sd, OP_N), Ai, st1));  // A = M_{i,i-1} x_{i-1}
+    if (!pipe)
+      for (int q = 0; q < nk; ++q) {  // T1_k = M_{i,i-1} xl_{k,i-1} (same launch when serial)
+        int k = kinds[q];
+        G.add(c.desc(c.term(Ml(i - 1), so, OP_N, Ld(k, i - 1), sd, OP_N), c.K(k, 0), st1));
+      }
     RC(G.run(st));
-    // G2: S = M_ii - A M_{i-1,i};  Y_k = A B_{k,i-1,i}
-    G.add(c.desc(c.term(tA, st1, OP_N, Mu(i - 1), so, OP_N), tS, st1, -1.0, Md(i), sd, 1.0));
-    for (int q = 0; q < nk; ++q) {
-      int k = kinds[q];
-      G.add(c.desc(c.term(tA, st1, OP_N, Bu(k, i - 1), so, OP_N), c.K(k, 1), st1));
-    }
-    RC(G.run(st));
+    if (pipe) NEGF_CUDA_CHECK(cudaEventRecord(evA[p], st));
+    G.add(c.desc(c.term(Ai, st1, OP_N, Mu(i - 1), so, OP_N), tS, st1, -1.0, Md(i), sd, 1.0));
+    if (!pipe)
+      for (int q = 0; q < nk; ++q) {  // Y_k = A B_{k,i-1,i}
+        int k = kinds[q];
+        G.add(c.desc(c.term(Ai, st1, OP_N, Bu(k, i - 1), so, OP_N), c.K(k, 1), st1));
+      }
+    RC(G.run(st));  // S = M_ii - A M_{i-1,i}
     RC(invert_into(i));
+    if (pipe) NEGF_CUDA_CHECK(cudaEventRecord(evX[p], st));
     if (nk == 0) continue;
+    // --- Keldysh forward products (stream sk)
+    if (pipe) {
+      for (int q = 0; q < nk; ++q) {  // T1_k: needs only K-stream data
+        int k = kinds[q];
+        G.add(c.desc(c.term(Ml(i - 1), so, OP_N, Ld(k, i - 1), sd, OP_N), c.K(k, 0), st1));
+      }
+      RC(G.run(sk));
+      NEGF_CUDA_CHECK(cudaStreamWaitEvent(sk, evA[p], 0));
+      for (int q = 0; q < nk; ++q) {  // Y_k = A B_{k,i-1,i}
+        int k = kinds[q];
+        G.add(c.desc(c.term(Ai, st1, OP_N, Bu(k, i - 1), so, OP_N), c.K(k, 1), st1));
+      }
+      RC(G.run(sk));
+    }
     // E_k = B_k,ii - Y_k + Y_k^dag
     for (int q = 0; q < nk; ++q) {
       int k = kinds[q];
       E.add(c.K(k, 2), st1, ne, {Bd(k, i), c.K(k, 1), c.K(k, 1)}, {sd, st1, st1}, {0, 0, 1},
             {1.0, -1.0, 1.0});
     }
-    RC(E.run(st));
+    RC(E.run(sk));
     // b_k = T1_k M_{i,i-1}^dag + E_k
     for (int q = 0; q < nk; ++q) {
       int k = kinds[q];
       G.add(c.desc(c.term(c.K(k, 0), st1, OP_N, Ml(i - 1), so, OP_H), c.K(k, 3), st1, 1.0,
                    c.K(k, 2), st1, 1.0));
     }
-    RC(G.run(st));
+    RC(G.run(sk));
+    if (pipe) NEGF_CUDA_CHECK(cudaStreamWaitEvent(sk, evX[p], 0));
     // U_k = x_i b_k
     for (int q = 0; q < nk; ++q) {
       int k = kinds[q];
       G.add(c.desc(c.term(Xd(i), sd, OP_N, c.K(k, 3), st1, OP_N), c.K(k, 0), st1));
     }
-    RC(G.run(st));
+    RC(G.run(sk));
     // xl_k,i = U_k x_i^dag
     for (int q = 0; q < nk; ++q) {
       int k = kinds[q];
       G.add(c.desc(c.term(c.K(k, 0), st1, OP_N, Xd(i), sd, OP_H), Ld(k, i), sd));
     }
-    RC(G.run(st));
+    RC(G.run(sk));
+    if (pipe) NEGF_CUDA_CHECK(cudaEventRecord(evK[p], sk));
+  }
+  if (pipe) {  // join: the backward sweep reads everything the K stream wrote
+    NEGF_CUDA_CHECK(cudaEventRecord(ev0, sk));
+    NEGF_CUDA_CHECK(cudaStreamWaitEvent(st, ev0, 0));
   }
 
   // ---------------- backward sweep ----------------

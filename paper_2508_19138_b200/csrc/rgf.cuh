@@ -22,7 +22,12 @@ struct RgfArgs {
   int symmetrize;      // apply (X - X^dag)/2 to the lesser/greater diagonal blocks
   int* status;         // [n_e] device: 0 ok, 1 + forward step of the first singular block
   double* u_spread;    // [n_e][n_b] device, optional
+  int overlap;         // forward sweep: Keldysh products on a second stream (default 1)
 };
+
+// Process-wide default for RgfArgs::overlap used by the C ABI.
+int rgf_overlap_default();
+void set_rgf_overlap_default(int on);
 
 size_t rgf_workspace_bytes(int n_e, int n_b, int bs);
 int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t stream);

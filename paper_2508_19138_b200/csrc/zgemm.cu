@@ -8,13 +8,13 @@ namespace {
 
 constexpr unsigned long long kSign = 0x8000000000000000ull;
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_, bool GAUSS_ = false>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_, bool GAUSS_ = false, int BK_ = 8>
 struct Cfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
   // GAUSS: 3 real products per complex product (3M / Gauss):
   //   P1 = ar br, P2 = ai bi, P3 = (ar + ai)(br + bi);  re = P1 - P2, im = P3 - P1 - P2
   static constexpr bool GAUSS = GAUSS_;
-  static constexpr int BK = 8;
+  static constexpr int BK = BK_;
   static constexpr int NT = WM * WN * 32;
   static constexpr int WTM = BM / WM;  // warp tile rows
   static constexpr int WTN = BN / WN;
@@ -269,7 +269,10 @@ int launch_cfg(const ZGemmGroup& g, cudaStream_t stream) {
   }
   if (max_tiles == 0 || max_batch == 0) return 0;
   dim3 grid(max_tiles, max_batch, g.n);
-  const int tok = prof_begin(PROF_ZGEMM, stream);
+  int maxk = 0;
+  for (int i = 0; i < g.n; ++i)
+    for (int t = 0; t < g.d[i].nterms; ++t) maxk = g.d[i].t[t].K > maxk ? g.d[i].t[t].K : maxk;
+  const int tok = prof_begin(maxk <= 32 ? PROF_ZGEMM_SMALLK : PROF_ZGEMM, stream);
   zgemm_kernel<CF><<<grid, CF::NT, CF::SMEM, stream>>>(g);
   NEGF_LAUNCHED();
   if (tok >= 0) {
@@ -294,6 +297,10 @@ using CfgGauss = Cfg<64, 64, 2, 4, 4, 1, true>;
 using CfgGauss2 = Cfg<64, 32, 2, 2, 4, 3, true>;
 using Cfg4M32 = Cfg<64, 32, 2, 2, 4, 3, false>;
 using CfgGauss3 = Cfg<32, 64, 2, 2, 4, 3, true>;
+// Measured alternatives (C2 carrier batch, energies/s; algo 2 = 90.5):
+//   64x32 6-stage 2 CTA/SM 78.9 | 128x32 8 warps 68.1 | 32x32 2 warps 78.2 |
+//   64x32 BK=16 80.8 | 32x32 4 warps (16x16) 87.4 | 64x64 16 warps 69.3 |
+//   64x32 8 warps (16x16) 84.5  -> occupancy of 12 warps with 32x16 warp tiles wins.
 
 }  // namespace
 

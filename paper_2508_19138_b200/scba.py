@@ -135,11 +135,16 @@ class ScreenedSolver:
         self._buf, self._n_e = b, n_e
         return b
 
-    def solve(self, n_e: int, check: bool = True) -> dict:
+    def solve(self, n_e: int, check: bool = True, timer=None) -> dict:
         """Inputs in buffers pr_*/pl_*/pg_* (filled by the caller)."""
+        import contextlib
+
+        T = timer or (lambda name: contextlib.nullcontext())
         lib, p, b, o = self.lib, _lib.ptr, self.buffers(n_e), self.opt
         st = _lib.stream_ptr(self.dev)
         vd, vu, vl = self.v
+        _t = T("W: assembly")
+        _t.__enter__()
         nbytes = lib.negf_w_assemble_workspace_bytes(n_e, self.n_b, self.bs)
         ws = _lib.workspace(nbytes, self.dev)
         rc = lib.negf_w_assemble(n_e, self.n_b, self.bs, p(vd), p(vu), p(vl), p(b["pr_diag"]), p(b["pr_upper"]),
@@ -147,6 +152,9 @@ class ScreenedSolver:
                                  p(b["pg_upper"]), p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]),
                                  p(b["bl_diag"]), p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]), p(ws), nbytes, st)
         _lib.check(rc, "negf_w_assemble")
+        _t.__exit__()
+        _t = T("W: OBC (Sancho+Stein)")
+        _t.__enter__()
         nbytes = lib.negf_w_obc_workspace_bytes(n_e, self.bs)
         ws = _lib.workspace(nbytes, self.dev)
         rc = lib.negf_w_obc_apply(n_e, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]),
@@ -162,6 +170,9 @@ class ScreenedSolver:
                 raise SpectralRadiusError("W boundary Stein operator not certified contractive (|a|_F >= 1)")
             if np.any(ss):
                 raise ConvergenceError(f"geometric Stein did not reach tol {o.stein_tol} in {o.stein_max_iter} squarings")
+        _t.__exit__()
+        _t = T("W: RGF")
+        _t.__enter__()
         nbytes = lib.negf_rgf_workspace_bytes(n_e, self.n_b, self.bs)
         ws = _lib.workspace(nbytes, self.dev)
         b["rgf_status"].zero_()
@@ -171,6 +182,7 @@ class ScreenedSolver:
             p(b["wr_lower"]), p(b["wl_diag"]), p(b["wl_upper"]), p(b["wg_diag"]), p(b["wg_upper"]), 1,
             p(b["rgf_status"]), None, p(ws), nbytes, st)
         _lib.check(rc, "negf_rgf_selected_solve_batched")
+        _t.__exit__()
         if check:
             raise_on_status(b["rgf_status"])
         return b
@@ -196,7 +208,7 @@ class ScbaState:
 
 def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOptions | None = None,
              device="cuda", keep_g: bool = True, initial_sigma: ScbaState | None = None,
-             comm: Comm | None = None) -> dict:
+             comm: Comm | None = None, profile: bool = False, sigma_to_host: bool = True) -> dict:
     """SCBA on one GPU or energy-sharded over ``comm`` (one rank per GPU).
 
     ``h``/``v`` are (diag, upper, lower) block stacks; ``v=None`` runs the
@@ -234,7 +246,27 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     result: dict = {}
     residuals = []
     blocks = None
+    timings: dict[str, float] = {}
+    import time as _time
+
+    class _T:  # stage timer (scba.py:85-94 KernelTimers categories); syncs only when profiling
+        def __init__(self, name):
+            self.name = name
+
+        def __enter__(self):
+            if profile:
+                torch.cuda.synchronize(dev)
+                self.t0 = _time.perf_counter()
+
+        def __exit__(self, *a):
+            if profile:
+                torch.cuda.synchronize(dev)
+                timings[self.name] = timings.get(self.name, 0.0) + _time.perf_counter() - self.t0
+
+    iter_times = []
     for it in range(max_iter):
+        torch.cuda.synchronize(dev)
+        t_iter = _time.perf_counter()
         g_host = {k: [] for k in RESULT_KEYS} if keep_g else None
         gl_c, gg_c = cols(), cols()
         # 1. carrier solve per energy batch of this rank
@@ -246,13 +278,16 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
                 blocks = {k: torch.empty(d, dtype=Z, device=dev) for k in ("sr_diag", "sl_diag", "sg_diag")}
                 blocks.update({k: torch.empty(o, dtype=Z, device=dev) for k in
                                ("sr_upper", "sr_lower", "sl_upper", "sg_upper")})
-            lay.unpack_retarded(sig.ret_upper, sig.ret_lower, e0, nb_, blocks["sr_diag"], blocks["sr_upper"],
-                                blocks["sr_lower"])
-            lay.unpack_lg(sig.lesser, e0, nb_, blocks["sl_diag"], blocks["sl_upper"])
-            lay.unpack_lg(sig.greater, e0, nb_, blocks["sg_diag"], blocks["sg_upper"])
-            b = carrier.solve(my_e[e0:e1], sigma=blocks, n_e=nb_)
-            lay.pack(b["xl_diag"], b["xl_upper"], gl_c, e0)
-            lay.pack(b["xg_diag"], b["xg_upper"], gg_c, e0)
+            with _T("layout"):
+                lay.unpack_retarded(sig.ret_upper, sig.ret_lower, e0, nb_, blocks["sr_diag"], blocks["sr_upper"],
+                                    blocks["sr_lower"])
+                lay.unpack_lg(sig.lesser, e0, nb_, blocks["sl_diag"], blocks["sl_upper"])
+                lay.unpack_lg(sig.greater, e0, nb_, blocks["sg_diag"], blocks["sg_upper"])
+            with _T("G: OBC+RGF"):
+                b = carrier.solve(my_e[e0:e1], sigma=blocks, n_e=nb_)
+            with _T("layout"):
+                lay.pack(b["xl_diag"], b["xl_upper"], gl_c, e0)
+                lay.pack(b["xg_diag"], b["xg_upper"], gg_c, e0)
             if keep_g:
                 for k, src in RESULT_KEYS.items():
                     g_host[k].append(b[src].cpu().numpy())
@@ -262,10 +297,13 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             residuals.append(0.0)
             break
         # 2. G^<> to entry-major (all-to-all), polarization on own entry rows
-        gl, gg = tr.to_entry_major(gl_c), tr.to_entry_major(gg_c)
+        with _T("transpose"):
+            gl, gg = tr.to_entry_major(gl_c), tr.to_entry_major(gg_c)
         del gl_c, gg_c
-        p_rows = polarization(gl, gg, diag_rows, de)
-        pl, pg, pru, prl = (tr.to_energy_major(x) for x in p_rows)
+        with _T("convolution"):
+            p_rows = polarization(gl, gg, diag_rows, de)
+        with _T("transpose"):
+            pl, pg, pru, prl = (tr.to_energy_major(x) for x in p_rows)
         del p_rows
         # 3. screened interaction per batch of own energies
         wl_c, wg_c = cols(), cols()
@@ -273,17 +311,24 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             e1 = min(n_own, e0 + batch)
             nb_ = e1 - e0
             wb = screened.buffers(nb_)
-            lay.unpack_retarded(pru, prl, e0, nb_, wb["pr_diag"], wb["pr_upper"], wb["pr_lower"])
-            lay.unpack_lg(pl, e0, nb_, wb["pl_diag"], wb["pl_upper"])
-            lay.unpack_lg(pg, e0, nb_, wb["pg_diag"], wb["pg_upper"])
-            wb = screened.solve(nb_)
-            lay.pack(wb["wl_diag"], wb["wl_upper"], wl_c, e0)
-            lay.pack(wb["wg_diag"], wb["wg_upper"], wg_c, e0)
+            with _T("layout"):
+                lay.unpack_retarded(pru, prl, e0, nb_, wb["pr_diag"], wb["pr_upper"], wb["pr_lower"])
+                lay.unpack_lg(pl, e0, nb_, wb["pl_diag"], wb["pl_upper"])
+                lay.unpack_lg(pg, e0, nb_, wb["pg_diag"], wb["pg_upper"])
+            wb = screened.solve(nb_, timer=_T)
+            with _T("layout"):
+                lay.pack(wb["wl_diag"], wb["wl_upper"], wl_c, e0)
+                lay.pack(wb["wg_diag"], wb["wg_upper"], wg_c, e0)
         del pl, pg, pru, prl
-        wl, wg = tr.to_entry_major(wl_c), tr.to_entry_major(wg_c)
+        with _T("transpose"):
+            wl, wg = tr.to_entry_major(wl_c), tr.to_entry_major(wg_c)
         del wl_c, wg_c
         # 4. self-energy on own entry rows, back to energy-major columns
-        raw = tuple(tr.to_energy_major(x) for x in self_energy(gl, gg, wl, wg, None, diag_rows, de))
+        with _T("convolution"):
+            s_rows = self_energy(gl, gg, wl, wg, None, diag_rows, de)
+        with _T("transpose"):
+            raw = tuple(tr.to_energy_major(x) for x in s_rows)
+        del s_rows
         del wl, wg, gl, gg
         # 5. mixing + residual (scba.py:1155-1177), max over ranks
         tr_old = [lay.traces(sig.lesser), lay.traces(sig.greater)]
@@ -299,15 +344,18 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         delta, scale = comm.allreduce_max([delta, scale], dev)
         residuals.append(delta / (scale + 1e-300))
         del raw
+        iter_times.append(_time.perf_counter() - t_iter)
         if residuals[-1] < options.tol:
             break
         if len(residuals) >= 11 and residuals[-1] > 5.0 * residuals[-11]:
             raise ConvergenceError(f"residual grew from {residuals[-11]:.3e} to {residuals[-1]:.3e} over 10 iterations")
-    if v is not None:
+    if v is not None and sigma_to_host:
         for k, t in zip(("lesser", "greater", "ret_upper", "ret_lower"), sig.as_tuple()):
             result["sigma_" + k] = t.cpu().numpy()
+    result["iteration_s"] = iter_times
     result["residuals"] = np.asarray(residuals)
     result["state"] = sig
     result["energy_slice"] = own
     result["transpose_bytes"] = tr.bytes_moved
+    result["timings"] = timings
     return result

@@ -8,8 +8,9 @@ dev = torch.device('cuda')
 h = toys.chain_device(nb_, bs)
 from paper_2508_19138_b200 import _lib
 for spec in sys.argv[3:]:
-    batch, streams, algo = (int(x) for x in spec.split('x'))
+    batch, streams, algo, ov = (int(x) for x in spec.split('x'))
     _lib.load().negf_set_gemm_algo(algo)
+    _lib.load().negf_set_rgf_overlap(ov)
     solver = CarrierSolver(h, 1e-3, Contacts(0.1, -0.1, 0.05), 1e-8, device=dev, streams=streams)
     e = np.linspace(-2, 2, batch)
     solver.solve(e, n_e=batch)
@@ -21,7 +22,7 @@ for spec in sys.argv[3:]:
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / reps
     solver.check_status(b)
-    print(f"{nb_}x{bs} batch={batch} streams={streams} algo={algo}: {dt*1e3:.1f} ms/batch  {batch/dt:.1f} energies/s  "
+    print(f"{nb_}x{bs} batch={batch} streams={streams} algo={algo} overlap={ov}: {dt*1e3:.1f} ms/batch  {batch/dt:.1f} energies/s  "
           f"model {8.0*bs**3*(38*nb_-33)*batch/dt/1e12:.2f} TF", flush=True)
     del solver, b
     torch.cuda.empty_cache()
