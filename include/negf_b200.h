@@ -61,6 +61,26 @@ int negf_rgf_selected_solve_batched(
     int symmetrize, int* status, double* u_spread,
     void* workspace, size_t workspace_bytes, void* stream);
 
+/* The two sweeps separately (spatial-decomposition building blocks,
+ * dist.py:529-533, 647-681):
+ *   mode 1: forward only. x_fwd (rgf.py:113-129) is written to xr_diag and
+ *           xl_fwd / xg_fwd (rgf.py:132-149) to xl_diag / xg_diag. With
+ *           fwd_given = 1, xr_diag already holds x_fwd on entry and only the
+ *           lesser/greater recursion runs (forward_lg with a given RetardedPass).
+ *   mode 2: backward only (rgf.py:152-229). On entry xr_diag / xl_diag / xg_diag
+ *           hold x_fwd / xl_fwd / xg_fwd; a caller-written last block acts as
+ *           the x_last seed of rgf_retarded / rgf_lesser_greater.
+ *   mode 0: both (= negf_rgf_selected_solve_batched).
+ * Same workspace as negf_rgf_selected_solve_batched. */
+int negf_rgf_sweeps_batched(int mode, int fwd_given, int n_e, int n_b, int bs,
+                            const void* m_diag, const void* m_upper, const void* m_lower,
+                            const void* bl_diag, const void* bl_upper,
+                            const void* bg_diag, const void* bg_upper,
+                            void* xr_diag, void* xr_upper, void* xr_lower,
+                            void* xl_diag, void* xl_upper, void* xg_diag, void* xg_upper,
+                            int symmetrize, int* status, double* u_spread,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- dense block primitives (negfgw/_linalg.py:19-64) --------------------
  * D[b] = alpha*op(A[b])op(B[b]) + beta*C[b]; op: 0=N 1=T 2=conj 3=conj-trans.
  * Replaces _linalg.gemm (_linalg.py:19-22), batched. C may be NULL. */
@@ -102,6 +122,18 @@ int negf_sigma_lg_obc_batched(int batch, int bs, const void* x, const void* n, c
                               const double* f, void* sigma_r, void* sigma_lesser,
                               void* sigma_greater, void* workspace, size_t workspace_bytes,
                               void* stream);
+
+/* stein_geometric (obc.py:427-447) for `batch` problems w - a w a^dag = q by
+ * squared doubling, stopping at |a_k w a_k^dag|_F < tol max(|w|_F, 1e-300).
+ * v0[bs] (device complex128): start vector of the spectral-radius power
+ * iteration (obc.py:320-342: numpy default_rng(5), normal re + i normal im,
+ * normalised). status[b]: 0 ok, 2 not converged, 4 spectral radius estimate
+ * >= 1 (SpectralRadiusError; the Kronecker fallback of scba.py:534-543 is not
+ * ported). bs <= 6000. */
+size_t negf_stein_workspace_bytes(int batch, int bs);
+int negf_stein_batched(int batch, int bs, const void* a, const void* q, void* w, double tol,
+                       int max_iter, const void* v0, int* status, int* iters, void* workspace,
+                       size_t workspace_bytes, void* stream);
 
 /* Carrier-side contact closure of an assembled batch (scba.py:755-774):
  * for the left (corner 0) and right (corner n_b-1) leads, solve the surface
@@ -210,15 +242,16 @@ int negf_w_assemble(int n_e, int n_b, int bs, const void* v_diag, const void* v_
 /* W contact closure in place (scba.py:839-858, _lead_lg_boundary :617-664):
  * Sancho surface block per side (status/iters [2][n_e], codes as
  * negf_obc_sancho_batched), geometric Stein per side and kind (stein_status/
- * stein_iters [2 kinds][2 sides][n_e]; 4 = spectral radius not certified
- * < 1 via |a|_F, 2 = not converged), corner source corrections, and
+ * stein_iters [2 kinds][2 sides][n_e]; 4 = spectral radius estimate >= 1,
+ * 2 = not converged; v0 as in negf_stein_batched), corner source corrections, and
  * M_cc -= n x n'. */
 size_t negf_w_obc_workspace_bytes(int n_e, int bs);
 int negf_w_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper,
                      const void* m_lower, void* bl_diag, const void* bl_upper, void* bg_diag,
                      const void* bg_upper, double surface_tol, int max_sweeps, double stein_tol,
-                     int stein_max_iter, int* status, int* iters, int* stein_status,
-                     int* stein_iters, void* workspace, size_t workspace_bytes, void* stream);
+                     int stein_max_iter, const void* v0, int* status, int* iters,
+                     int* stein_status, int* stein_iters, void* workspace,
+                     size_t workspace_bytes, void* stream);
 
 /* ---- (6) mixing and residual (scba.py:478-481, 1155-1167) ----------------
  * s_k <- (1 - alpha) s_k + alpha r_k elementwise over n complex values, for

@@ -15,11 +15,24 @@ from .errors import (
     SingularBlockError,
     SpectralRadiusError,
 )
-from .rgf import KIND_GREATER, KIND_LESSER, SelectedSolution, selected_solve, selected_solve_batched
+from .rgf import (
+    KIND_GREATER,
+    KIND_LESSER,
+    LgPass,
+    RetardedPass,
+    SelectedSolution,
+    forward_lg,
+    forward_retarded,
+    rgf_lesser_greater,
+    rgf_retarded,
+    selected_solve,
+    selected_solve_batched,
+)
 
 __all__ = [
     "FULL", "LG_COMPRESSED", "BlockMatrix",
     "C_OBSERVABLE", "C_POLARIZATION", "C_SIGMA", "KT_DEFAULT",
     "BlockStructureError", "ConvergenceError", "NegfError", "SingularBlockError", "SpectralRadiusError",
-    "KIND_GREATER", "KIND_LESSER", "SelectedSolution", "selected_solve", "selected_solve_batched",
+    "KIND_GREATER", "KIND_LESSER", "LgPass", "RetardedPass", "SelectedSolution", "forward_lg",
+    "forward_retarded", "rgf_lesser_greater", "rgf_retarded", "selected_solve", "selected_solve_batched",
 ]

@@ -31,6 +31,10 @@ _SIGNATURES: dict[str, tuple] = {
         _i,
         [_i, _i, _i] + [_vp] * 14 + [_i, _vp, _vp, _vp, _sz, _vp],
     ),
+    "negf_rgf_sweeps_batched": (
+        _i,
+        [_i, _i, _i, _i, _i] + [_vp] * 14 + [_i, _vp, _vp, _vp, _sz, _vp],
+    ),
     "negf_zgemm_batched": (
         _i,
         [_i, _i, _i, _i, _d, _d, _vp, _ll, _i, _i, _vp, _ll, _i, _i, _d, _d, _vp, _ll, _i, _vp, _ll, _i, _vp],
@@ -41,6 +45,8 @@ _SIGNATURES: dict[str, tuple] = {
     "negf_obc_sancho_batched": (_i, [_i, _i, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "negf_sigma_lg_obc_workspace_bytes": (_sz, [_i, _i]),
     "negf_sigma_lg_obc_batched": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "negf_stein_workspace_bytes": (_sz, [_i, _i]),
+    "negf_stein_batched": (_i, [_i, _i, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp, _sz, _vp]),
     "negf_g_obc_workspace_bytes": (_sz, [_i, _i]),
     "negf_g_obc_apply": (
         _i,
@@ -59,7 +65,7 @@ _SIGNATURES: dict[str, tuple] = {
     "negf_w_assemble_workspace_bytes": (_sz, [_i, _i, _i]),
     "negf_w_assemble": (_i, [_i, _i, _i] + [_vp] * 18 + [_sz, _vp]),
     "negf_w_obc_workspace_bytes": (_sz, [_i, _i]),
-    "negf_w_obc_apply": (_i, [_i, _i, _i] + [_vp] * 7 + [_d, _i, _d, _i] + [_vp] * 5 + [_sz, _vp]),
+    "negf_w_obc_apply": (_i, [_i, _i, _i] + [_vp] * 7 + [_d, _i, _d, _i] + [_vp] * 6 + [_sz, _vp]),
     "negf_mix": (_i, [_ll, _d] + [_vp] * 9),
     "negf_diag_traces": (_i, [_vp, _ll, _i, _vp, _i, _i, _vp, _vp]),
     "negf_prof_enable": (None, [_i]),
@@ -111,6 +117,23 @@ def ptr(t: torch.Tensor | None) -> int | None:
     if t is None:
         return None
     return t.data_ptr()
+
+
+_V0: dict = {}
+
+
+def power_start_vector(n: int, device) -> torch.Tensor:
+    """obc.py:329-331: the seeded start vector of spectral_radius_estimate."""
+    import numpy as np
+
+    dev = torch.device(device)
+    key = (n, dev.type, dev.index)
+    if key not in _V0:
+        rng = np.random.default_rng(5)
+        v = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        v /= np.linalg.norm(v)
+        _V0[key] = torch.from_numpy(v).to(dev)
+    return _V0[key]
 
 
 def stream_ptr(device: torch.device | None = None) -> int:

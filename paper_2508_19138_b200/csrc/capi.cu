@@ -50,6 +50,39 @@ int negf_rgf_selected_solve_batched(int n_e, int n_b, int bs, const void* m_diag
   a.status = status;
   a.u_spread = u_spread;
   a.overlap = rgf_overlap_default();
+  a.mode = 0;
+  a.fwd_given = 0;
+  return rgf_selected_solve(a, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int negf_rgf_sweeps_batched(int mode, int fwd_given, int n_e, int n_b, int bs, const void* m_diag,
+                            const void* m_upper, const void* m_lower, const void* bl_diag,
+                            const void* bl_upper, const void* bg_diag, const void* bg_upper,
+                            void* xr_diag, void* xr_upper, void* xr_lower, void* xl_diag,
+                            void* xl_upper, void* xg_diag, void* xg_upper, int symmetrize,
+                            int* status, double* u_spread, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  if (mode < 0 || mode > 2) return -1;
+  if (n_e < 0 || n_b < 1 || bs < 1 || !m_diag || !xr_diag) return -1;
+  if (n_b > 1 && (!m_upper || !m_lower)) return -1;
+  if (mode != 1 && n_b > 1 && (!xr_upper || !xr_lower)) return -1;
+  if ((bl_diag && !xl_diag) || (bg_diag && !xg_diag)) return -1;
+  if (n_b > 1 && ((bl_diag && !bl_upper) || (bg_diag && !bg_upper))) return -1;
+  if (mode != 1 && n_b > 1 && ((bl_diag && !xl_upper) || (bg_diag && !xg_upper))) return -1;
+  RgfArgs a;
+  a.n_e = n_e; a.n_b = n_b; a.bs = bs;
+  a.m_diag = (const z_t*)m_diag; a.m_upper = (const z_t*)m_upper; a.m_lower = (const z_t*)m_lower;
+  a.b_diag[0] = (const z_t*)bl_diag; a.b_upper[0] = (const z_t*)bl_upper;
+  a.b_diag[1] = (const z_t*)bg_diag; a.b_upper[1] = (const z_t*)bg_upper;
+  a.xr_diag = (z_t*)xr_diag; a.xr_upper = (z_t*)xr_upper; a.xr_lower = (z_t*)xr_lower;
+  a.xl_diag[0] = (z_t*)xl_diag; a.xl_upper[0] = (z_t*)xl_upper;
+  a.xl_diag[1] = (z_t*)xg_diag; a.xl_upper[1] = (z_t*)xg_upper;
+  a.symmetrize = mode == 1 ? 0 : symmetrize;
+  a.status = status;
+  a.u_spread = u_spread;
+  a.overlap = rgf_overlap_default();
+  a.mode = mode;
+  a.fwd_given = fwd_given;
   return rgf_selected_solve(a, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 

@@ -194,10 +194,15 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
   } sguard{sk, st, pipe};
   z_t* tAb[2] = {tA, c.T(2)};
 
+  const bool do_fwd = a.mode != 2;
+  const bool do_inv = !(a.mode == 1 && a.fwd_given);
+  if (do_fwd) {
   // i = 0
-  NEGF_CUDA_CHECK(cudaMemcpy2DAsync(tS, st1 * sizeof(z_t), Md(0), sd * sizeof(z_t),
-                                    bs2 * sizeof(z_t), ne, cudaMemcpyDeviceToDevice, st));
-  RC(invert_into(0));
+  if (do_inv) {
+    NEGF_CUDA_CHECK(cudaMemcpy2DAsync(tS, st1 * sizeof(z_t), Md(0), sd * sizeof(z_t),
+                                      bs2 * sizeof(z_t), ne, cudaMemcpyDeviceToDevice, st));
+    RC(invert_into(0));
+  }
   if (pipe) {
     NEGF_CUDA_CHECK(cudaEventRecord(evX[0], st));
     NEGF_CUDA_CHECK(cudaStreamWaitEvent(sk, evX[0], 0));
@@ -227,14 +232,14 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
       }
     RC(G.run(st));
     if (pipe) NEGF_CUDA_CHECK(cudaEventRecord(evA[p], st));
-    G.add(c.desc(c.term(Ai, st1, OP_N, Mu(i - 1), so, OP_N), tS, st1, -1.0, Md(i), sd, 1.0));
+    if (do_inv) G.add(c.desc(c.term(Ai, st1, OP_N, Mu(i - 1), so, OP_N), tS, st1, -1.0, Md(i), sd, 1.0));
     if (!pipe)
       for (int q = 0; q < nk; ++q) {  // Y_k = A B_{k,i-1,i}
         int k = kinds[q];
         G.add(c.desc(c.term(Ai, st1, OP_N, Bu(k, i - 1), so, OP_N), c.K(k, 1), st1));
       }
     RC(G.run(st));  // S = M_ii - A M_{i-1,i}
-    RC(invert_into(i));
+    if (do_inv) RC(invert_into(i));
     if (pipe) NEGF_CUDA_CHECK(cudaEventRecord(evX[p], st));
     if (nk == 0) continue;
     // --- Keldysh forward products (stream sk)
@@ -284,6 +289,8 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
     NEGF_CUDA_CHECK(cudaEventRecord(ev0, sk));
     NEGF_CUDA_CHECK(cudaStreamWaitEvent(st, ev0, 0));
   }
+  }  // do_fwd
+  if (a.mode == 1) return 0;
 
   // ---------------- backward sweep ----------------
   // X_{n-1,n-1} = x_{n-1} and XL_{n-1} = xl_{n-1} already sit in place.

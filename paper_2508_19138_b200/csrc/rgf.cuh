@@ -23,6 +23,12 @@ struct RgfArgs {
   int* status;         // [n_e] device: 0 ok, 1 + forward step of the first singular block
   double* u_spread;    // [n_e][n_b] device, optional
   int overlap;         // forward sweep: Keldysh products on a second stream (default 1)
+  // 0: forward + backward (selected_solve). 1: forward only -- x_fwd lands in
+  // xr_diag, xl_fwd in xl_diag (forward_retarded / forward_lg, rgf.py:113-149).
+  // 2: backward only -- xr_diag / xl_diag hold x_fwd / xl_fwd on entry, with the
+  // last block optionally pre-seeded (rgf_retarded / rgf_lesser_greater x_last).
+  int mode;
+  int fwd_given;       // mode 1: xr_diag already holds x_fwd; run only the Keldysh recursion
 };
 
 // Process-wide default for RgfArgs::overlap used by the C ABI.

@@ -251,23 +251,56 @@ __global__ void stein_step_kernel(z_t* w, const z_t* upd, long long n2, double t
   }
 }
 
-// Frobenius norm test ||a||_F < 1 (certifies spectral radius < 1); init masks.
-__global__ void stein_init_kernel(const z_t* a, long long n2, int n_side, int n_kind, int* active,
-                                  int* iters, int* status) {
+// Spectral-radius gate of stein_geometric (obc.py:320-342, 434-437): 50 power
+// iterations from the reference's seeded start vector v0 (numpy
+// default_rng(5), generated by the caller); rho >= 1 -> OBC_SPECTRAL.
+// One CTA per problem, one warp per row of a (coalesced), v in smem.
+__global__ void stein_init_kernel(const z_t* a, long long n2, int bs, const z_t* v0, int n_side,
+                                  int n_kind, int* active, int* iters, int* status) {
+  extern __shared__ __align__(16) z_t vsh[];  // v (bs) then w (bs)
   __shared__ double red[32];
+  __shared__ double s_rho;
+  __shared__ int s_zero;
   const int s = blockIdx.x;  // (side, e) problem
-  double sa = 0.0;
-  for (long long e = threadIdx.x; e < n2; e += blockDim.x) {
-    z_t v = a[s * n2 + e];
-    sa += v.x * v.x + v.y * v.y;
-  }
-  for (int o = 16; o > 0; o >>= 1) sa += __shfl_down_sync(0xffffffffu, sa, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sa;
+  const z_t* A = a + s * n2;
+  z_t* v = vsh;
+  z_t* w = vsh + bs;
+  for (int i = threadIdx.x; i < bs; i += blockDim.x) v[i] = v0[i];
+  if (threadIdx.x == 0) { s_rho = 0.0; s_zero = 0; }
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int it = 0; it < 50; ++it) {
+    for (int r = warp; r < bs; r += nw) {
+      z_t acc = make_double2(0.0, 0.0);
+      for (int c = lane; c < bs; c += 32) acc = zadd(acc, zmul(A[(long long)r * bs + c], v[c]));
+      for (int o = 16; o > 0; o >>= 1) {
+        acc.x += __shfl_down_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_down_sync(0xffffffffu, acc.y, o);
+      }
+      if (lane == 0) w[r] = acc;
+    }
+    __syncthreads();
+    double sq = 0.0;
+    for (int i = threadIdx.x; i < bs; i += blockDim.x) sq += w[i].x * w[i].x + w[i].y * w[i].y;
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, o);
+    if (lane == 0) red[warp] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int i = 0; i < nw; ++i) t += red[i];
+      const double nrm = sqrt(t);
+      if (nrm == 0.0) s_zero = 1;
+      s_rho = nrm;
+    }
+    __syncthreads();
+    if (s_zero) break;
+    const double inv = 1.0 / s_rho;
+    for (int i = threadIdx.x; i < bs; i += blockDim.x) v[i] = zscale(inv, w[i]);
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) t += red[i];
-    const bool ok = sqrt(t) < 1.0;
+    const double rho = s_zero ? 0.0 : s_rho;
+    const bool ok = rho < 1.0;
     for (int k = 0; k < n_kind; ++k) {
       const int p = k * n_side + s;
       active[p] = ok ? 1 : 0;
@@ -301,7 +334,7 @@ size_t stein_workspace_bytes(int n_side, int n_kind, int bs) {
 }
 
 int stein_batched(const z_t* a, const z_t* q, z_t* w, int n_side, int n_kind, int bs, double tol,
-                  int max_iter, int* status, int* iters, void* ws, size_t ws_bytes,
+                  int max_iter, int* status, int* iters, const z_t* v0, void* ws, size_t ws_bytes,
                   cudaStream_t st) {
   if (ws_bytes < stein_workspace_bytes(n_side, n_kind, bs)) return -4;
   const long long n2 = (long long)bs * bs;
@@ -318,7 +351,8 @@ int stein_batched(const z_t* a, const z_t* q, z_t* w, int n_side, int n_kind, in
   NEGF_CUDA_CHECK(cudaMemcpyAsync(w, q, (size_t)n_kind * n_side * blk, cudaMemcpyDeviceToDevice, st));
   {
     ProfScope ps_stein_init_kernel(PROF_OTHER, (cudaStream_t)(st));
-    stein_init_kernel<<<n_side, 256, 0, st>>>(a, n2, n_side, n_kind, active, iters, status);
+    stein_init_kernel<<<n_side, 256, 2 * (size_t)bs * sizeof(z_t), st>>>(a, n2, bs, v0, n_side, n_kind,
+                                                                          active, iters, status);
     NEGF_LAUNCHED();
   }
   for (int it = 1; it <= max_iter; ++it) {
@@ -384,15 +418,29 @@ size_t negf_w_obc_workspace_bytes(int n_e, int bs) {
          stein_workspace_bytes(ns, 2, bs) + 4 * a256(sizeof(int) * np + 64);
 }
 
+size_t negf_stein_workspace_bytes(int batch, int bs) { return stein_workspace_bytes(batch, 1, bs); }
+
+// stein_geometric (obc.py:427-447) for `batch` independent problems.
+int negf_stein_batched(int batch, int bs, const void* a, const void* q, void* w, double tol,
+                       int max_iter, const void* v0, int* status, int* iters, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  if (batch < 0 || bs < 1 || !a || !q || !w || !v0 || !status || !iters || max_iter < 1) return -1;
+  if (bs > 6000) return -1;  // v0 / w staging in shared memory
+  if (batch == 0) return 0;
+  return stein_batched((const z_t*)a, (const z_t*)q, (z_t*)w, batch, 1, bs, tol, max_iter, status,
+                       iters, (const z_t*)v0, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
 // W-side contact closure (scba.py:839-858), in place on the assembled batch.
 // status: [2 sides][n_e] Sancho; stein_status: [2 kinds][2 sides][n_e].
 int negf_w_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper,
                      const void* m_lower, void* bl_diag, const void* bl_upper, void* bg_diag,
                      const void* bg_upper, double surface_tol, int max_sweeps, double stein_tol,
-                     int stein_max_iter, int* status, int* iters, int* stein_status,
-                     int* stein_iters, void* workspace, size_t workspace_bytes, void* stream) {
+                     int stein_max_iter, const void* v0, int* status, int* iters,
+                     int* stein_status, int* stein_iters, void* workspace,
+                     size_t workspace_bytes, void* stream) {
   if (n_e < 0 || n_b < 2 || bs < 1 || !m_diag || !m_upper || !m_lower || !status || !iters ||
-      !stein_status || !stein_iters)
+      !stein_status || !stein_iters || !v0 || bs > 6000)
     return -1;
   if (!bl_diag || !bl_upper || !bg_diag || !bg_upper) return -1;
   if (n_e == 0) return 0;
@@ -482,7 +530,8 @@ int negf_w_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
       g.d[k] = D1(TMP + (long long)k * ns * n2, n2, OP_N, xr, n2, OP_H, Qm + (long long)k * ns * n2, n2, ns);
     RC(zgemm_group_launch(g, st));
   }
-  RC(stein_batched(a, Qm, Wl, ns, 2, bs, stein_tol, stein_max_iter, stein_status, stein_iters, tws,
+  RC(stein_batched(a, Qm, Wl, ns, 2, bs, stein_tol, stein_max_iter, stein_status, stein_iters,
+                   (const z_t*)v0, tws,
                    stein_workspace_bytes(ns, 2, bs), st));
   // u1 = B_out x^dag (left B_out = B_01, right B_out = -B_{N-2,N-1}^dag); u2 = n wl
   {

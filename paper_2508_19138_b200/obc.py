@@ -14,7 +14,7 @@ import torch
 from scipy.special import expit
 
 from . import _lib
-from .errors import ConvergenceError, SingularBlockError
+from .errors import ConvergenceError, SingularBlockError, SpectralRadiusError
 
 SIDE_LEFT = "left"
 SIDE_RIGHT = "right"
@@ -135,3 +135,59 @@ def sigma_lg_obc(x_r, contact_mu: float, kT: float, energy: float, couplings, de
     f = torch.tensor([float(fermi(energy, contact_mu, kT))], dtype=torch.float64)
     sr, sl, sg = sigma_lg_obc_batched(_t(x_r, dev)[None], _t(n, dev)[None], _t(n_prime, dev)[None], f)
     return ObcSigma(sr[0].cpu().numpy(), sl[0].cpu().numpy(), sg[0].cpu().numpy())
+
+
+def stein_batched(a: torch.Tensor, q: torch.Tensor, tol: float = 1e-12, max_iter: int = 100, check: bool = True):
+    """Geometric Stein w - a w a^dag = q for a batch (batch, bs, bs)."""
+    lib = _lib.load()
+    batch, bs = a.shape[0], a.shape[-1]
+    dev = a.device
+    w = torch.empty_like(q)
+    status = torch.zeros(batch, dtype=torch.int32, device=dev)
+    iters = torch.zeros(batch, dtype=torch.int32, device=dev)
+    nbytes = lib.negf_stein_workspace_bytes(batch, bs)
+    ws = _lib.workspace(nbytes, dev)
+    v0 = _lib.power_start_vector(bs, dev)
+    rc = lib.negf_stein_batched(batch, bs, a.data_ptr(), q.data_ptr(), w.data_ptr(), tol, max_iter, v0.data_ptr(),
+                                status.data_ptr(), iters.data_ptr(), ws.data_ptr(), nbytes, _lib.stream_ptr(dev))
+    _lib.check(rc, "negf_stein_batched")
+    if check:
+        st = status.cpu().numpy()
+        if np.any(st == 4):
+            raise SpectralRadiusError("spectral radius estimate >= 1; geometric series diverges")
+        if np.any(st):
+            raise ConvergenceError(f"geometric Stein did not reach tol {tol} in {max_iter} squarings")
+    return w, iters
+
+
+def stein_geometric(a, q, tol: float = 1e-12, max_iter: int = 100, device="cuda"):
+    """obc.py:427-447 signature (single problem)."""
+    dev = torch.device(device)
+    w, _ = stein_batched(_t(a, dev)[None], _t(q, dev)[None], tol, max_iter)
+    return w[0].cpu().numpy()
+
+
+def fixed_point_step(c, x, device="cuda"):
+    """obc.py:138-141: one surface update (m - n x n')^-1 on the device."""
+    lib = _lib.load()
+    dev = torch.device(device)
+    m, n, npr, xx = (_t(v, dev) for v in (c.m, c.n, c.n_prime, x))
+    bs = m.shape[-1]
+    t = torch.empty_like(m)
+    s_ = t.clone()
+    st = _lib.stream_ptr(dev)
+    rc = lib.negf_zgemm_batched(bs, bs, bs, 1, 1.0, 0.0, n.data_ptr(), 0, bs, 0, xx.data_ptr(), 0, bs, 0, 0.0, 0.0,
+                                None, 0, bs, t.data_ptr(), 0, bs, st)
+    _lib.check(rc, "negf_zgemm_batched")
+    rc = lib.negf_zgemm_batched(bs, bs, bs, 1, -1.0, 0.0, t.data_ptr(), 0, bs, 0, npr.data_ptr(), 0, bs, 0, 1.0, 0.0,
+                                m.data_ptr(), 0, bs, s_.data_ptr(), 0, bs, st)
+    _lib.check(rc, "negf_zgemm_batched")
+    out = torch.empty_like(m)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    nbytes = lib.negf_zinv_workspace_bytes(bs, 1)
+    ws = _lib.workspace(nbytes, dev)
+    rc = lib.negf_zinv_batched(bs, 1, s_.data_ptr(), out.data_ptr(), status.data_ptr(), None, ws.data_ptr(), nbytes, st)
+    _lib.check(rc, "negf_zinv_batched")
+    if int(status.item()):
+        raise SingularBlockError("singular surface update")
+    return out.cpu().numpy()

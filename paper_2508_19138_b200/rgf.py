@@ -193,3 +193,107 @@ def selected_solve(m_tilde, b_lesser=None, b_greater=None, device="cuda") -> Sel
     out = selected_solve_batched(md, mu, ml, srcs[0], srcs[1])
     kinds = [k for k, b in ((KIND_LESSER, b_lesser), (KIND_GREATER, b_greater)) if b is not None]
     return _solution_from(out, 0, n, bs, kinds)
+
+
+# -- the sweeps separately (rgf.py:113-229 signatures) ----------------------
+
+
+@dataclass
+class RetardedPass:
+    """rgf.py:37-49: forward intermediates x_fwd[i] and the pivot spread."""
+
+    x_fwd: list = field(default_factory=list)
+    u_spread: list = field(default_factory=list)
+
+
+@dataclass
+class LgPass:
+    """rgf.py:52-58. ``b_fwd`` (effective sources) is not materialised by the
+    device recursion; no caller on the hot path reads it (dist.py uses
+    x_fwd_lg only)."""
+
+    x_fwd_lg: list = field(default_factory=list)
+    b_fwd: list = field(default_factory=list)
+
+
+def _sweeps(mode: int, m_tilde, b_lg: dict, xr_diag: np.ndarray | None = None, xl: dict | None = None,
+            fwd_given: bool = False, symmetrize: bool = False, device="cuda"):
+    """One call of negf_rgf_sweeps_batched for a single energy. ``xr_diag`` /
+    ``xl`` pre-fill the in/out diagonal arrays (modes 1 with fwd_given, and 2)."""
+    lib = _lib.load()
+    dev = torch.device(device)
+    n, bs = m_tilde.n_blocks, m_tilde.block_size
+    d, u, lo = tridiag_arrays(m_tilde)
+    md, mu, ml = (to_device(x[None], dev) for x in (d, u, lo))
+    z = dict(dtype=torch.complex128, device=dev)
+    out = {"xr_diag": torch.zeros((1, n, bs, bs), **z) if xr_diag is None else to_device(xr_diag[None], dev),
+           "xr_upper": torch.zeros((1, max(n - 1, 0), bs, bs), **z),
+           "xr_lower": torch.zeros((1, max(n - 1, 0), bs, bs), **z)}
+    srcs = {}
+    for kind, b in b_lg.items():
+        bd, bu = lg_arrays(b)
+        srcs[kind] = (to_device(bd[None], dev), to_device(bu[None], dev))
+        pre = None if xl is None else xl.get(kind)
+        out[_KEYS[kind] + "_diag"] = torch.zeros((1, n, bs, bs), **z) if pre is None else to_device(pre[None], dev)
+        out[_KEYS[kind] + "_upper"] = torch.zeros((1, max(n - 1, 0), bs, bs), **z)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    spread = torch.zeros((1, n), dtype=torch.float64, device=dev)
+    nbytes = lib.negf_rgf_workspace_bytes(1, n, bs)
+    ws = _lib.workspace(nbytes, dev)
+    p = _lib.ptr
+    bl = srcs.get(KIND_LESSER, (None, None))
+    bg = srcs.get(KIND_GREATER, (None, None))
+    rc = lib.negf_rgf_sweeps_batched(
+        mode, 1 if fwd_given else 0, 1, n, bs, p(md), p(mu), p(ml), p(bl[0]), p(bl[1]), p(bg[0]), p(bg[1]),
+        p(out["xr_diag"]), p(out["xr_upper"]), p(out["xr_lower"]), p(out.get("xl_diag")), p(out.get("xl_upper")),
+        p(out.get("xg_diag")), p(out.get("xg_upper")), 1 if symmetrize else 0, p(status), p(spread), p(ws), nbytes,
+        _lib.stream_ptr(dev))
+    _lib.check(rc, "negf_rgf_sweeps_batched")
+    raise_on_status(status)
+    host = {k: v[0].cpu().numpy() for k, v in out.items()}
+    return host, spread[0].cpu().numpy()
+
+
+def forward_retarded(m_tilde, device="cuda") -> RetardedPass:
+    """rgf.py:113-129."""
+    host, spread = _sweeps(1, m_tilde, {}, device=device)
+    return RetardedPass(list(host["xr_diag"]), [float(x) for x in spread])
+
+
+def forward_lg(m_tilde, b_lg, fwd: RetardedPass, device="cuda") -> LgPass:
+    """rgf.py:132-149, riding on the given retarded intermediates."""
+    host, _ = _sweeps(1, m_tilde, {KIND_LESSER: b_lg}, xr_diag=np.stack(fwd.x_fwd), fwd_given=True, device=device)
+    return LgPass(list(host["xl_diag"]), [])
+
+
+def rgf_retarded(m_tilde, fwd: RetardedPass | None = None, x_last=None, device="cuda"):
+    """rgf.py:152-183: backward sweep (forward pass computed unless given);
+    ``x_last`` seeds the exact last diagonal block."""
+    if fwd is None:
+        fwd = forward_retarded(m_tilde, device=device)
+    xr = np.stack(fwd.x_fwd).copy()
+    if x_last is not None:
+        xr[-1] = x_last
+    host, _ = _sweeps(2, m_tilde, {}, xr_diag=xr, device=device)
+    n, bs = m_tilde.n_blocks, m_tilde.block_size
+    sol = SelectedSolution(n, bs, list(host["xr_diag"]), list(host["xr_upper"]), list(host["xr_lower"]))
+    return sol, fwd
+
+
+def rgf_lesser_greater(m_tilde, b_lg, fwd: RetardedPass, sol: SelectedSolution, kind: str,
+                       lg: LgPass | None = None, x_last=None, device="cuda") -> LgPass:
+    """rgf.py:186-229: stores X^lg blocks of ``kind`` into ``sol`` (not
+    symmetrized) and returns the forward intermediates. The retarded chain is
+    re-run on the device from ``fwd`` with sol's last retarded block as seed,
+    which reproduces sol's X^R."""
+    if lg is None:
+        lg = forward_lg(m_tilde, b_lg, fwd, device=device)
+    xr = np.stack(fwd.x_fwd).copy()
+    xr[-1] = sol.x_r_diag[-1]
+    xl = np.stack(lg.x_fwd_lg).copy()
+    if x_last is not None:
+        xl[-1] = x_last
+    host, _ = _sweeps(2, m_tilde, {KIND_LESSER: b_lg}, xr_diag=xr, xl={KIND_LESSER: xl}, device=device)
+    sol.x_lg_diag[kind] = list(host["xl_diag"])
+    sol.x_lg_upper[kind] = list(host["xl_upper"])
+    return lg

@@ -159,7 +159,8 @@ class ScreenedSolver:
         ws = _lib.workspace(nbytes, self.dev)
         rc = lib.negf_w_obc_apply(n_e, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]),
                                   p(b["bl_diag"]), p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]),
-                                  o.surface_tol, 100, o.stein_tol, o.stein_max_iter, p(b["obc_status"]),
+                                  o.surface_tol, 100, o.stein_tol, o.stein_max_iter,
+                                  p(_lib.power_start_vector(self.bs, self.dev)), p(b["obc_status"]),
                                   p(b["obc_iters"]), p(b["stein_status"]), p(b["stein_iters"]), p(ws), nbytes, st)
         _lib.check(rc, "negf_w_obc_apply")
         if check:
@@ -167,7 +168,7 @@ class ScreenedSolver:
                                 o.surface_tol, "W contact")
             ss = b["stein_status"].cpu().numpy()
             if np.any(ss == 4):
-                raise SpectralRadiusError("W boundary Stein operator not certified contractive (|a|_F >= 1)")
+                raise SpectralRadiusError("W boundary Stein: spectral radius estimate >= 1 (Kronecker fallback not ported)")
             if np.any(ss):
                 raise ConvergenceError(f"geometric Stein did not reach tol {o.stein_tol} in {o.stein_max_iter} squarings")
         _t.__exit__()

@@ -94,3 +94,18 @@ def test_ballistic_observables_match_reference(golden, cuda):
     assert abs(obs["terminal_right"] - float(g["obs_terminal_right"])) < TOL * abs(float(g["obs_terminal_right"]))
     # two-terminal current conservation (scba.py:1357-1362)
     assert abs(obs["terminal_left"] + obs["terminal_right"]) < 1e-3 * abs(obs["terminal_left"])
+
+
+def test_stein_and_fixed_point_step_dropins(golden, cuda):
+    from paper_2508_19138_b200.obc import fixed_point_step, stein_geometric
+    g = golden("golden_obc.npz")
+    for k in range(3):
+        w = stein_geometric(g[f"stein{k}_a"], g[f"stein{k}_q"])
+        assert rel(w, g[f"stein{k}_w"]) < TOL
+    c = ContactBlocks(g["lead0_m"], g["lead0_n"], g["lead0_np"])
+    x = g["lead0_x"]
+    # the converged surface block is a fixed point of the recursion
+    assert rel(fixed_point_step(c, x), x) < 1e-10
+    x0 = np.zeros_like(x)
+    ref = np.linalg.inv(c.m - c.n @ x0 @ c.n_prime)
+    assert rel(fixed_point_step(c, x0), ref) < TOL

@@ -137,3 +137,56 @@ def test_singular_block_raises_with_step(cuda):
     md2[0, 0] = np.eye(5)
     with pytest.raises(SingularBlockError, match="forward step 2"):
         selected_solve_batched(*(dev(x, cuda) for x in (md2, mu, ml)))
+
+
+def _bm(md, mu, ml):
+    n = md.shape[0]
+    m = BlockMatrix(n, md.shape[-1])
+    for i in range(n):
+        m.set_block(i, i, md[i])
+        if i + 1 < n:
+            m.set_block(i, i + 1, mu[i])
+            m.set_block(i + 1, i, ml[i])
+    return m
+
+
+def _lgbm(bd, bu):
+    n = bd.shape[0]
+    b = BlockMatrix(n, bd.shape[-1], 3, LG_COMPRESSED)
+    for i in range(n):
+        b.set_block(i, i, bd[i])
+        if i + 1 < n:
+            b.set_block(i, i + 1, bu[i])
+    return b
+
+
+def test_split_sweeps_and_seeds_match_reference_semantics(cuda):
+    """forward_retarded / forward_lg / rgf_retarded(fwd, x_last) /
+    rgf_lesser_greater(..., x_last) (rgf.py:113-229) vs the oracle recursion."""
+    from paper_2508_19138_b200 import forward_lg, forward_retarded, rgf_lesser_greater, rgf_retarded
+    md, mu, ml, src = orc.random_bt_system(21, 6, 9)
+    m = _bm(md[0], mu[0], ml[0])
+    bl = _lgbm(src["<"][0][0], src["<"][1][0])
+    ref = orc.rgf_selected(md, mu, ml, {"<": src["<"]})
+    fwd = forward_retarded(m)
+    assert len(fwd.x_fwd) == 6 and len(fwd.u_spread) == 6
+    sol, _ = rgf_retarded(m, fwd=fwd)
+    assert rel(np.stack(sol.x_r_diag), ref["xr_diag"][0]) < TOL
+    assert rel(np.stack(sol.x_r_lower), ref["xr_lower"][0]) < TOL
+    lg = forward_lg(m, bl, fwd)
+    rgf_lesser_greater(m, bl, fwd, sol, "<", lg=lg)
+    assert rel(np.stack(sol.x_lg_diag["<"]), ref["x<_diag"][0]) < TOL
+    assert rel(np.stack(sol.x_lg_upper["<"]), ref["x<_upper"][0]) < TOL
+    # seeds: embedding the chain's last block exactly (dist.py:678-681 usage)
+    x_last = ref["xr_diag"][0][-1] * 0 + np.eye(9) * 0.3
+    sol2, _ = rgf_retarded(m, fwd=fwd, x_last=x_last)
+    # oracle with the same seed
+    xf = [np.linalg.inv(md[0][0])]
+    for i in range(1, 6):
+        xf.append(np.linalg.inv(md[0][i] - ml[0][i - 1] @ xf[-1] @ mu[0][i - 1]))
+    X = [None] * 6
+    X[5] = x_last
+    for i in range(4, -1, -1):
+        t = xf[i] @ mu[0][i]
+        X[i] = xf[i] + t @ X[i + 1] @ ml[0][i] @ xf[i]
+    assert rel(np.stack(sol2.x_r_diag), np.stack(X)) < TOL
