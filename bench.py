@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--n-e", type=int, default=1024, help="energies per rank")
     ap.add_argument("--batch", type=int, default=128, help="energies per device batch")
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--greater", choices=["identity", "recursion"], default="identity",
+                    help="G^> by the exact identity G^> = G^< + G^R - G^R^dag (default) or by its own "
+                         "Keldysh recursion like the reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-procs", type=int, default=0, help="0 = all host cores")
     ap.add_argument("--scgw", default="32x128x512", help="n_blocks x block_size x energies-per-rank of the "
@@ -59,9 +62,12 @@ def parse():
 WORKLOAD = dict(e_min=-2.0, e_max=2.0, eta=1e-3, mu_left=0.1, mu_right=-0.1, kT=0.05, surface_tol=1e-8)
 
 
-def model_flops_per_energy(n_b: int, bs: int) -> float:
-    """F_RGF = 8 bs^3 (38 n_b - 33) per energy (both kinds)."""
-    return 8.0 * bs ** 3 * (38 * n_b - 33)
+def model_flops_per_energy(n_b: int, bs: int, kinds: int = 2) -> float:
+    """F_RGF = 8 bs^3 (38 n_b - 33) per energy with both Keldysh
+    kinds; one kind: retarded (8 n_b - 7) + one Keldysh pass (15 n_b - 13)."""
+    if kinds == 2:
+        return 8.0 * bs ** 3 * (38 * n_b - 33)
+    return 8.0 * bs ** 3 * (23 * n_b - 20)
 
 
 def exec_rgf_flops_per_energy(n_b: int, bs: int) -> float:
@@ -209,7 +215,7 @@ def run_native(args):
     contacts = Contacts(w["mu_left"], w["mu_right"], w["kT"])
     lib = _lib.load()
     peak = fp64_peak_probe(dev)
-    solver = CarrierSolver(h, w["eta"], contacts, w["surface_tol"], device=dev)
+    solver = CarrierSolver(h, w["eta"], contacts, w["surface_tol"], device=dev, greater=args.greater)
     batch = min(args.batch, n_e)
     acc = ObservableAccumulator(n_e, n_b, de, dev)
 
@@ -312,19 +318,25 @@ def run_native(args):
         tf = ROOT / "profiles" / "zgemm_traffic.json"
         if tf.exists():
             traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
-        rgf_model = model_flops_per_energy(n_b, bs) * total_e
+        rgf_model = model_flops_per_energy(n_b, bs, 1 if args.greater == "identity" else 2) * total_e
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "complex128 (fp64)",
             "data": "synthetic (seeded chain_device, reference generator restated)",
             "config": {"workload": "C2 ballistic NEGF: chain_device 64 blocks x 256 orbitals, 1024 energies/rank "
-                                   "on [-2,2] eV, eta=1e-3, Sancho OBC tol 1e-8, G^R+G^<+G^> selected solve",
+                                   "on [-2,2] eV, eta=1e-3, Sancho OBC tol 1e-8, G^R + G^< selected solve (+ G^>)",
+                       "greater": args.greater,
                        "n_blocks": n_b, "block_size": bs, "energies_per_rank": n_e, "energy_batch": batch,
                        "parallelism": f"energy-sharded x{world}",
                        "l2": "working set per batch ~100+ GB >> 126 MB L2 (inputs larger than L2)"},
             "rgf_tflops_model": rgf_model / (ms_max * 1e-3) / 1e12,
-            "rgf_tflops_model_note": "SURVEY §8(d) F_RGF = 8 bs^3 (38 n_b - 33) per energy / step time (incl. OBC+assembly)",
+            "rgf_tflops_model_note": ("SURVEY §8(d) model flops of the recursions actually run (both Keldysh kinds: "
+                                      "8 bs^3 (38 n_b - 33); greater by identity: retarded + lesser 8 bs^3 (23 n_b - 20)) "
+                                      "/ step time (incl. OBC + assembly)"),
+            "greater": ("G^> = G^< + G^R - G^R^dag on the selected blocks (exact: B^> - B^< = M^dag - M for the "
+                        "carrier system, SURVEY §7.8; parity-tested vs the reference's greater recursion)"
+                        if args.greater == "identity" else "G^> by its own Keldysh recursion (reference algorithm)"),
             "roofline": {"bound": "tensor", "kernel": "zgemm_kernel (DMMA m8n8k4 f64)", "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                          "traffic": traffic,

@@ -81,6 +81,16 @@ int negf_rgf_sweeps_batched(int mode, int fwd_given, int n_e, int n_b, int bs,
                             int symmetrize, int* status, double* u_spread,
                             void* workspace, size_t workspace_bytes, void* stream);
 
+/* Greater selected blocks from the lesser and retarded ones:
+ *   X^>_ii = X^<_ii + X^R_ii - X^R_ii^dag,  X^>_{i,i+1} = X^<_{i,i+1} + X^R_{i,i+1} - X^R_{i+1,i}^dag,
+ * exact for the carrier system because its sources satisfy
+ * B^> - B^< = M^dag - M (bath construction, scba.py:16-19, 706-716; contact and
+ * scattering self-energies obey the same identity). Opt-in replacement of the
+ * greater Keldysh recursion; NOT valid for the W system. */
+int negf_greater_from_identity(int n_e, int n_b, int bs, const void* xl_diag,
+                               const void* xl_upper, const void* xr_diag, const void* xr_upper,
+                               const void* xr_lower, void* xg_diag, void* xg_upper, void* stream);
+
 /* ---- dense block primitives (negfgw/_linalg.py:19-64) --------------------
  * D[b] = alpha*op(A[b])op(B[b]) + beta*C[b]; op: 0=N 1=T 2=conj 3=conj-trans.
  * Replaces _linalg.gemm (_linalg.py:19-22), batched. C may be NULL. */

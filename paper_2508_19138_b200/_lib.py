@@ -35,6 +35,7 @@ _SIGNATURES: dict[str, tuple] = {
         _i,
         [_i, _i, _i, _i, _i] + [_vp] * 14 + [_i, _vp, _vp, _vp, _sz, _vp],
     ),
+    "negf_greater_from_identity": (_i, [_i, _i, _i] + [_vp] * 8),
     "negf_zgemm_batched": (
         _i,
         [_i, _i, _i, _i, _d, _d, _vp, _ll, _i, _i, _vp, _ll, _i, _i, _d, _d, _vp, _ll, _i, _vp, _ll, _i, _vp],

@@ -47,7 +47,15 @@ class CarrierSolver:
     """Batched G solve for a fixed Hamiltonian H (block tridiagonal)."""
 
     def __init__(self, h, eta: float, contacts: Contacts, surface_tol: float = 1e-8,
-                 max_sweeps: int = 100, device="cuda", streams: int = 1) -> None:
+                 max_sweeps: int = 100, device="cuda", streams: int = 1,
+                 greater: str = "recursion") -> None:
+        """``greater``: "recursion" runs the greater Keldysh pass like the
+        reference; "identity" derives G^> = G^< + G^R - G^R^dag on the
+        selected blocks (exact for the carrier system), saving
+        ~40% of the RGF work."""
+        if greater not in ("recursion", "identity"):
+            raise ValueError(f"unknown greater mode {greater!r}")
+        self.greater = greater
         self.dev = torch.device(device)
         self.lib = _lib.load()
         hd, hu, hl = h
@@ -152,14 +160,22 @@ class CarrierSolver:
             raise_on_obc_status(b["obc_status"].cpu().numpy(), b["obc_iters"].cpu().numpy(),
                                 b["obc_resid"].cpu().numpy(), self.max_sweeps, self.surface_tol, "G contact")
         b["rgf_status"].zero_()
-        rgf_selected_solve_split(lib, b, ne, self.n_b, self.bs, self.dev, self.streams, self._side_streams)
+        if self.greater == "identity":
+            rgf_selected_solve_split(lib, b, ne, self.n_b, self.bs, self.dev, 1, [], kinds=("bl",))
+            rc = lib.negf_greater_from_identity(ne, self.n_b, self.bs, p(b["xl_diag"]), p(b["xl_upper"]),
+                                                p(b["xr_diag"]), p(b["xr_upper"]), p(b["xr_lower"]),
+                                                p(b["xg_diag"]), p(b["xg_upper"]), st)
+            _lib.check(rc, "negf_greater_from_identity")
+        else:
+            rgf_selected_solve_split(lib, b, ne, self.n_b, self.bs, self.dev, self.streams, self._side_streams)
         if check:
             raise_on_status(b["rgf_status"])
         return b
 
 
 def rgf_selected_solve_split(lib, b: dict, ne: int, n_b: int, bs: int, dev, streams: int, side_streams,
-                             prefix: tuple = ("m", "bl", "bg", "xr", "xl", "xg"), symmetrize: int = 1) -> None:
+                             prefix: tuple = ("m", "bl", "bg", "xr", "xl", "xg"), symmetrize: int = 1,
+                             kinds: tuple = ("bl", "bg")) -> None:
     """RGF over the batch in ``b``, split into ``streams`` energy slices on
     side streams so the latency-bound inversion panels of one slice overlap
     the DMMA GEMMs of another (energies are independent)."""
@@ -180,9 +196,11 @@ def rgf_selected_solve_split(lib, b: dict, ne: int, n_b: int, bs: int, dev, stre
             sl = lambda key: p(b[key][a:z])
             rc = lib.negf_rgf_selected_solve_batched(
                 z - a, n_b, bs, sl(f"{m}_diag"), sl(f"{m}_upper"), sl(f"{m}_lower"),
-                sl(f"{bl}_diag"), sl(f"{bl}_upper"), sl(f"{bg}_diag"), sl(f"{bg}_upper"),
-                sl(f"{xr}_diag"), sl(f"{xr}_upper"), sl(f"{xr}_lower"), sl(f"{xl}_diag"), sl(f"{xl}_upper"),
-                sl(f"{xg}_diag"), sl(f"{xg}_upper"), symmetrize, p(b["rgf_status"][a:z]), None, p(ws), nbytes,
+                sl(f"{bl}_diag") if "bl" in kinds else None, sl(f"{bl}_upper") if "bl" in kinds else None,
+                sl(f"{bg}_diag") if "bg" in kinds else None, sl(f"{bg}_upper") if "bg" in kinds else None,
+                sl(f"{xr}_diag"), sl(f"{xr}_upper"), sl(f"{xr}_lower"),
+                sl(f"{xl}_diag") if "bl" in kinds else None, sl(f"{xl}_upper") if "bl" in kinds else None,
+                sl(f"{xg}_diag") if "bg" in kinds else None, sl(f"{xg}_upper") if "bg" in kinds else None, symmetrize, p(b["rgf_status"][a:z]), None, p(ws), nbytes,
                 st_obj.cuda_stream)
             _lib.check(rc, "negf_rgf_selected_solve_batched")
     if parts > 1:
@@ -200,10 +218,10 @@ RESULT_KEYS = {
 
 
 def ballistic_run(h, energies, eta: float, contacts: Contacts, surface_tol: float = 1e-8,
-                  batch: int | None = None, device="cuda") -> dict[str, np.ndarray]:
+                  batch: int | None = None, device="cuda", greater: str = "recursion") -> dict[str, np.ndarray]:
     """scba_run(v_mat=None) equivalent (scba.py:951-1011): host arrays with
     the ScbaResult field names."""
-    solver = CarrierSolver(h, eta, contacts, surface_tol, device=device)
+    solver = CarrierSolver(h, eta, contacts, surface_tol, device=device, greater=greater)
     energies = np.asarray(energies, dtype=float)
     ne = len(energies)
     batch = batch or ne
@@ -261,13 +279,14 @@ class ObservableAccumulator:
 
 
 def ballistic_observables(h, energies, eta: float, contacts: Contacts, surface_tol: float = 1e-8,
-                          batch: int | None = None, device="cuda", solver: CarrierSolver | None = None):
+                          batch: int | None = None, device="cuda", solver: CarrierSolver | None = None,
+                          greater: str = "recursion"):
     """Public end-to-end ballistic API: host H blocks + energy grid in, host
     observables out. Every G block is computed on the device; only the
     reduced observables cross back to the host."""
     energies = np.asarray(energies, dtype=float)
     if solver is None:
-        solver = CarrierSolver(h, eta, contacts, surface_tol, device=device)
+        solver = CarrierSolver(h, eta, contacts, surface_tol, device=device, greater=greater)
     else:
         solver.set_hamiltonian(h)
     ne = len(energies)

@@ -131,3 +131,29 @@ int add_identity(z_t* Y, long long sY, int n, int batch, double2 s, cudaStream_t
 }
 
 }  // namespace negf
+
+extern "C" int negf_greater_from_identity(int n_e, int n_b, int bs, const void* xl_diag,
+                                          const void* xl_upper, const void* xr_diag,
+                                          const void* xr_upper, const void* xr_lower,
+                                          void* xg_diag, void* xg_upper, void* stream) {
+  using namespace negf;
+  if (n_e < 0 || n_b < 1 || bs < 1 || !xl_diag || !xr_diag || !xg_diag) return -1;
+  if (n_b > 1 && (!xl_upper || !xr_upper || !xr_lower || !xg_upper)) return -1;
+  if (n_e == 0) return 0;
+  const long long n2 = (long long)bs * bs;
+  EwGroup g;
+  g.n = 0; g.rows = bs; g.cols = bs;
+  auto add = [&](z_t* out, const z_t* l, const z_t* r, const z_t* rh, int batch) {
+    EwDesc& d = g.d[g.n++];
+    d.batch = batch; d.nterms = 3; d.out = out; d.sOut = n2;
+    d.X[0] = l; d.sX[0] = n2; d.opH[0] = 0; d.coef[0] = make_double2(1, 0);
+    d.X[1] = r; d.sX[1] = n2; d.opH[1] = 0; d.coef[1] = make_double2(1, 0);
+    d.X[2] = rh; d.sX[2] = n2; d.opH[2] = 1; d.coef[2] = make_double2(-1, 0);
+  };
+  // X^>_ii = X^<_ii + X^R_ii - X^R_ii^dag ; X^>_{i,i+1} = X^<_{i,i+1} + X^R_{i,i+1} - X^R_{i+1,i}^dag
+  add((z_t*)xg_diag, (const z_t*)xl_diag, (const z_t*)xr_diag, (const z_t*)xr_diag, n_e * n_b);
+  if (n_b > 1)
+    add((z_t*)xg_upper, (const z_t*)xl_upper, (const z_t*)xr_upper, (const z_t*)xr_lower,
+        n_e * (n_b - 1));
+  return ew_group_launch(g, (cudaStream_t)stream);
+}

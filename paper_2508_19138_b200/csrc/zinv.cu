@@ -134,117 +134,182 @@ __global__ void zinv_small_kernel(const z_t* __restrict__ S, long long sS, int l
 
 // ---------------------------------------------------------------------------
 // Blocked path.
-// Panel LU (rows k0..n-1, columns k0..k0+nb-1) in smem; writes pivots and Pinv.
-__global__ void zinv_panel_kernel(const z_t* __restrict__ A, long long sA, int n, int k0, int nb,
-                                  int* ipiv, z_t* pinv, double* umaxmin, InvAux aux) {
-  extern __shared__ __align__(16) unsigned char raw[];
-  const int rows = n - k0;
-  const int ld = nb + 1;
-  z_t* p = reinterpret_cast<z_t*>(raw);
-  __shared__ double sv[32];
-  __shared__ int si[32];
+// Panel LU (candidate rows k0..n-1, columns k0..k0+NB-1) held in REGISTERS:
+// TPR = NB/16 threads per row, 16 columns each, so the rank-1 updates are
+// register FMAs and a column step costs one block argmax (shuffles + barrier)
+// and one pivot-row broadcast through smem (barrier). Rows are never moved:
+// a pivoted row retires from the active set, and LAPACK's row order is
+// tracked through each row's position (pos), which reproduces zgetf2's pivot
+// choice including its first-index tie break. Outputs: the LAPACK-equivalent
+// interchange sequence ipiv, the net row permutation as a move list, and
+// Pinv = (pivot block)^-1 = U^-1 L^-1.
+template <int NB>
+__global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__ A, long long sA,
+                                                         int n, int k0, int w, int* ipiv, z_t* pinv,
+                                                         double* umaxmin, int* moves, InvAux aux) {
+  constexpr int TPR = NB / 16;  // threads per row
+  constexpr int LD = NB + 1;
+  __shared__ z_t prow_s[NB];          // pivot row broadcast
+  __shared__ z_t blk[NB * LD];        // pivot rows (L\U) in pivot order, for Pinv
+  __shared__ int posinv_s[1024];      // final position -> physical row
+  __shared__ double rv[32];
+  __shared__ int ri[32], rp[32];
   __shared__ int sbad;
   __shared__ double smax, smin;
   const int b = blockIdx.x;
   if (aux.active && !aux.active[b]) return;
+  const int rows = n - k0;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int r = tid / TPR, h = tid % TPR;  // my row, my 16-column half
+  const bool have = r < rows;
   const z_t* a = A + (long long)b * sA;
-  for (int e = threadIdx.x; e < rows * nb; e += blockDim.x) {
-    int i = e / nb, j = e % nb;
-    p[i * ld + j] = a[(long long)(k0 + i) * n + k0 + j];
-  }
-  if (threadIdx.x == 0) {
+  z_t v[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+    v[c] = (have && 16 * h + c < w) ? a[(long long)(k0 + r) * n + k0 + 16 * h + c] : make_double2(0.0, 0.0);
+  bool act = have;
+  int pos = r;
+  if (tid == 0) {
     sbad = 0;
     smax = k0 == 0 ? 0.0 : umaxmin[2 * b];
     smin = k0 == 0 ? INFINITY : umaxmin[2 * b + 1];
   }
-  __syncthreads();
-  for (int j = 0; j < nb; ++j) {
-    double v = -1.0;
-    int idx = rows;
-    for (int i = j + threadIdx.x; i < rows; i += blockDim.x) {
-      double c = zabs1(p[i * ld + j]);
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    if (j >= w) break;
+    const int hj = j / 16, cj = j % 16;
+    // (1) argmax over active rows of |re|+|im| in column j; ties -> smallest position
+    double bv = -1.0;
+    int br = 1 << 30, bp = 1 << 30;
+    if (act && h == hj) {
+      double c = zabs1(v[cj]);
       if (c != c) c = INFINITY;
-      if (c > v) { v = c; idx = i; }
+      bv = c; br = r; bp = pos;
     }
-    double bv; int pr;
-    block_argmax(v, idx, sv, si, bv, pr);
-    if (threadIdx.x == 0) ipiv[(long long)b * n + k0 + j] = k0 + pr;
-    if (pr != j)
-      for (int c = threadIdx.x; c < nb; c += blockDim.x) {
-        z_t t = p[j * ld + c]; p[j * ld + c] = p[pr * ld + c]; p[pr * ld + c] = t;
-      }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_down_sync(0xffffffffu, bv, o);
+      const int orow = __shfl_down_sync(0xffffffffu, br, o);
+      const int opos = __shfl_down_sync(0xffffffffu, bp, o);
+      if (ov > bv || (ov == bv && opos < bp)) { bv = ov; br = orow; bp = opos; }
+    }
+    if (lane == 0) { rv[warp] = bv; ri[warp] = br; rp[warp] = bp; }
     __syncthreads();
-    const z_t pv = p[j * ld + j];
-    if (threadIdx.x == 0) {
-      double m = hypot(pv.x, pv.y);
+    bv = rv[0]; br = ri[0]; bp = rp[0];
+    for (int w2 = 1; w2 < nw; ++w2)
+      if (rv[w2] > bv || (rv[w2] == bv && rp[w2] < bp)) { bv = rv[w2]; br = ri[w2]; bp = rp[w2]; }
+    // (2) pivot row broadcast
+    if (act && r == br) {
+#pragma unroll
+      for (int c = 0; c < 16; ++c) prow_s[16 * h + c] = v[c];
+    }
+    __syncthreads();
+    const z_t pv = prow_s[j];
+    // (3) multipliers and rank-1 update of the other active rows (registers)
+    // column-j value of my row, from the thread holding it (all lanes shuffle)
+    z_t own = v[cj];
+    if (TPR > 1) {
+      own.x = __shfl_sync(0xffffffffu, own.x, (lane & ~(TPR - 1)) | hj);
+      own.y = __shfl_sync(0xffffffffu, own.y, (lane & ~(TPR - 1)) | hj);
+    }
+    if (act && r == br) {
+      act = false;
+      pos = j;
+    } else if (act) {
+      const z_t l = zmul(own, zinv(pv));
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const int gc = 16 * h + c;
+        if (gc > j) v[c] = zsub(v[c], zmul(l, prow_s[gc]));
+        else if (gc == j) v[c] = l;
+      }
+      if (pos == j) pos = bp;  // LAPACK interchange: the row at position j moves to bp
+    } else if (have && pos == j) {
+      pos = bp;
+    }
+    if (tid == 0) {
+      ipiv[(long long)b * n + k0 + j] = k0 + bp;
+      const double m = hypot(pv.x, pv.y);
       if (!(m > 0.0) || !isfinite(m)) sbad = 1;
       smax = fmax(smax, m);
       smin = fmin(smin, m);
     }
-    const z_t ip = zinv(pv);
-    const int nr = rows - j - 1, nc = nb - j - 1;
-    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
-      z_t* l = &p[(j + 1 + i) * ld + j];
-      *l = zmul(*l, ip);
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < nr * nc; e += blockDim.x) {
-      int i = j + 1 + e / nc, c = j + 1 + e % nc;
-      p[i * ld + c] = zsub(p[i * ld + c], zmul(p[i * ld + j], p[j * ld + c]));
-    }
-    __syncthreads();
   }
-  // Pinv = U^-1 L^-1 of the top nb x nb block; one thread per column of the identity.
-  z_t* q = p + rows * ld;  // nb x nb scratch, ld
-  for (int c = threadIdx.x; c < nb; c += blockDim.x) {
-    // forward: L y = e_c (unit lower)
-    for (int i = 0; i < nb; ++i) {
-      z_t s = zmake(i == c ? 1.0 : 0.0, 0.0);
-      for (int k = 0; k < i; ++k) s = zsub(s, zmul(p[i * ld + k], q[k * ld + c]));
-      q[i * ld + c] = s;
-    }
-    // backward: U x = y
-    for (int i = nb - 1; i >= 0; --i) {
-      z_t s = q[i * ld + c];
-      for (int k = i + 1; k < nb; ++k) s = zsub(s, zmul(p[i * ld + k], q[k * ld + c]));
-      q[i * ld + c] = zmul(s, zinv(p[i * ld + i]));
+  // pivot rows -> blk (pivot order), positions -> posinv
+  if (have) {
+    posinv_s[pos] = r;
+    if (pos < w) {
+#pragma unroll
+      for (int c = 0; c < 16; ++c) blk[pos * LD + 16 * h + c] = v[c];
     }
   }
   __syncthreads();
-  z_t* pi = pinv + (long long)b * nb * nb;
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) pi[e] = q[(e / nb) * ld + e % nb];
-  if (threadIdx.x == 0) {
+  // Pinv = U^-1 L^-1: warp-parallel substitutions, lane = row, one identity column per pass
+  if (lane < 32) {
+    for (int c = warp; c < w; c += nw) {
+      z_t y = zmake(lane == c ? 1.0 : 0.0, 0.0);
+      for (int k = 0; k < w; ++k) {
+        const z_t yk = make_double2(__shfl_sync(0xffffffffu, y.x, k), __shfl_sync(0xffffffffu, y.y, k));
+        if (lane > k && lane < w) y = zsub(y, zmul(blk[lane * LD + k], yk));
+      }
+      for (int k = w - 1; k >= 0; --k) {
+        z_t xk = make_double2(__shfl_sync(0xffffffffu, y.x, k), __shfl_sync(0xffffffffu, y.y, k));
+        xk = zmul(xk, zinv(blk[k * LD + k]));
+        if (lane == k) y = xk;
+        if (lane < k) y = zsub(y, zmul(blk[lane * LD + k], xk));
+      }
+      if (lane < w) pinv[(long long)b * w * w + lane * w + c] = y;
+    }
+  }
+  // net row permutation as a move list (warp 0, ballot compaction)
+  if (warp == 0) {
+    int* mv = moves + (long long)b * (4 * NB + 1);
+    int cnt = 0;
+    for (int t0 = 0; t0 < rows; t0 += 32) {
+      const int t = t0 + lane;
+      const bool moved = t < rows && posinv_s[t] != t;
+      const unsigned m = __ballot_sync(0xffffffffu, moved);
+      if (moved) {
+        const int slot = cnt + __popc(m & ((1u << lane) - 1));
+        if (slot < 2 * w) {
+          mv[1 + 2 * slot] = t;
+          mv[2 + 2 * slot] = posinv_s[t];
+        }
+      }
+      cnt += __popc(m);
+    }
+    if (lane == 0) mv[0] = cnt < 2 * w ? cnt : 2 * w;
+  }
+  if (tid == 0) {
     umaxmin[2 * b] = smax;
     umaxmin[2 * b + 1] = smin;
     if (sbad && aux.status) atomicCAS(aux.status + b, 0, aux.status_code);
   }
 }
 
-// Apply the panel's row interchanges to every column, and emit
+// Apply the panel's net row permutation (move list from the panel kernel) to
+// every column as an independent gather (one thread per column, staged in
+// its own smem slice, so no load waits on a previous store), and emit
 // C' = A[:,K] with rows K zeroed   (n x nb)
 // R  = A[K,:]                      (nb x n)
-__global__ void zinv_swap_kernel(z_t* A, long long sA, int n, int k0, int nb, const int* ipiv,
-                                 z_t* Cp, z_t* R, const int* active) {
+__global__ void zinv_swap_kernel(z_t* A, long long sA, int n, int k0, int nb, const int* moves,
+                                 int mv_stride, z_t* Cp, z_t* R, const int* active) {
+  extern __shared__ __align__(16) z_t stage[];  // [2*nb][blockDim.x]
   const int b = blockIdx.y;
   if (active && !active[b]) return;
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   z_t* a = A + (long long)b * sA;
-  const int* pv = ipiv + (long long)b * n;
+  const int* mv = moves + (long long)b * mv_stride;
+  const int cnt = mv[0];
   if (col < n) {
-    for (int j = 0; j < nb; ++j) {
-      int r = pv[k0 + j];
-      if (r != k0 + j) {
-        z_t t = a[(long long)(k0 + j) * n + col];
-        a[(long long)(k0 + j) * n + col] = a[(long long)r * n + col];
-        a[(long long)r * n + col] = t;
-      }
-    }
+    for (int m = 0; m < cnt; ++m)
+      stage[m * blockDim.x + threadIdx.x] = a[(long long)(k0 + mv[2 + 2 * m]) * n + col];
+    for (int m = 0; m < cnt; ++m)
+      a[(long long)(k0 + mv[1 + 2 * m]) * n + col] = stage[m * blockDim.x + threadIdx.x];
     z_t* rr = R + (long long)b * nb * n;
     for (int j = 0; j < nb; ++j) rr[(long long)j * n + col] = a[(long long)(k0 + j) * n + col];
   }
-  // The CTA owning columns K (k0 is a multiple of the 128-column tile when
-  // nb divides 128; otherwise two CTAs share the range) copies the swapped
-  // panel columns cooperatively, rows K zeroed.
+  // The CTA(s) owning columns K copy the swapped panel columns cooperatively.
   const int c0 = blockIdx.x * blockDim.x, c1 = c0 + blockDim.x;
   const int lo = k0 > c0 ? k0 : c0, hi = (k0 + nb) < c1 ? (k0 + nb) : c1;
   if (lo >= hi) return;
@@ -303,11 +368,13 @@ __global__ void zinv_unpermute_kernel(const z_t* __restrict__ A, long long sA, i
 size_t zinv_workspace_bytes(int n, int batch) {
   if (n <= kInvSmallMax) return 0;
   const int nb = zinv_panel_width(n);
-  size_t per = sizeof(int) * n + sizeof(double) * 2 + sizeof(z_t) * ((size_t)nb * nb + 2 * (size_t)n * nb);
-  return (per * batch + 1024) + 256 * 4;
+  size_t per = sizeof(int) * n + sizeof(double) * 2 + sizeof(z_t) * ((size_t)nb * nb + 2 * (size_t)n * nb) +
+               sizeof(int) * (4 * (size_t)nb + 1);
+  return (per * batch + 1024) + 256 * 6;
 }
 
 int zinv_panel_width(int n) {
+  // register panel: n * (nb/16) threads <= 512 per CTA
   if (n <= 256) return 32;
   return 16;
 }
@@ -341,22 +408,31 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
   z_t* pinv = reinterpret_cast<z_t*>(take(sizeof(z_t) * (size_t)nb * nb * batch));
   z_t* Cp = reinterpret_cast<z_t*>(take(sizeof(z_t) * (size_t)n * nb * batch));
   z_t* R = reinterpret_cast<z_t*>(take(sizeof(z_t) * (size_t)n * nb * batch));
-  size_t panel_smem = (size_t)(n + nb) * (nb + 1) * sizeof(z_t);
+  int* moves = reinterpret_cast<int*>(take(sizeof(int) * (4 * (size_t)nb + 1) * batch));
   static bool attr2 = false;
   if (!attr2) {
-    NEGF_CUDA_CHECK(cudaFuncSetAttribute(zinv_panel_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NEGF_CUDA_CHECK(cudaFuncSetAttribute(zinv_swap_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr2 = true;
   }
-  if (panel_smem > 220 * 1024) return -5;
+  if (n * (nb / 16) > 1024 || n > 1024) return -5;
+  const int panel_threads = ((n * (nb / 16) + 31) / 32) * 32;
   for (int k0 = 0; k0 < n; k0 += nb) {
     const int w = nb < n - k0 ? nb : n - k0;  // last panel may be narrower
-    dim3 g((n + 127) / 128, batch);
+    dim3 g((n + 63) / 64, batch);
     {
     ProfScope ps_(PROF_ZINV, stream);
-    zinv_panel_kernel<<<batch, 256, panel_smem, stream>>>(S, sS, n, k0, w, ipiv, pinv, umm, aux);
+    {
+    ProfScope psp_(5, stream);
+    if (nb == 32)
+      zinv_panel_kernel<32><<<batch, panel_threads, 0, stream>>>(S, sS, n, k0, w, ipiv, pinv, umm, moves, aux);
+    else
+      zinv_panel_kernel<16><<<batch, panel_threads, 0, stream>>>(S, sS, n, k0, w, ipiv, pinv, umm, moves, aux);
     NEGF_LAUNCHED();
-    zinv_swap_kernel<<<g, 128, 0, stream>>>(S, sS, n, k0, w, ipiv, Cp, R, aux.active);
+    }
+    ProfScope pss_(6, stream);
+    zinv_swap_kernel<<<g, 64, 2 * (size_t)w * 64 * sizeof(z_t), stream>>>(S, sS, n, k0, w, moves,
+                                                                          4 * nb + 1, Cp, R, aux.active);
     NEGF_LAUNCHED();
     }
     // T = Pinv R, staged in the caller's destination X (w x n per matrix;
@@ -405,10 +481,12 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
     rc = zgemm_group_launch(grp, stream);
     if (rc) return rc;
     ProfScope ps2_(PROF_ZINV, stream);
-    zinv_rows_kernel<<<g, 128, 0, stream>>>(S, sS, n, k0, w, T, sX, pinv, aux.active);
+    ProfScope ps2b_(7, stream);
+    zinv_rows_kernel<<<g, 64, 0, stream>>>(S, sS, n, k0, w, T, sX, pinv, aux.active);
     NEGF_LAUNCHED();
   }
   ProfScope ps3_(PROF_ZINV, stream);
+  ProfScope ps3b_(8, stream);
   zinv_unpermute_kernel<<<batch, 256, n * sizeof(int), stream>>>(S, sS, n, ipiv, umm, X, sX, ldx,
                                                                  aux);
   NEGF_LAUNCHED();

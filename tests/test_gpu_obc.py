@@ -63,20 +63,24 @@ def test_sancho_not_converged_raises(cuda):
         obc_sancho_rubio(c, tol=1e-14, max_iter=3)
 
 
-def test_ballistic_matches_reference_scba_run(golden, cuda):
+@pytest.mark.parametrize("greater", ["recursion", "identity"])
+def test_ballistic_matches_reference_scba_run(golden, cuda, greater):
     g = golden("golden_ballistic_small.npz")
     h = orc.chain_device(5, 3)
-    out = ballistic_run(h, np.linspace(-2.0, 2.0, 16), 1e-3, Contacts(0.1, -0.1, 0.05), 1e-8, device=cuda)
+    out = ballistic_run(h, np.linspace(-2.0, 2.0, 16), 1e-3, Contacts(0.1, -0.1, 0.05), 1e-8, device=cuda,
+                        greater=greater)
     for k, v in out.items():
         assert rel(v, g[k]) < TOL, k
 
 
-@pytest.mark.parametrize("nb,bs,ne,batch", [(8, 48, 12, 5), (4, 96, 6, 6), (3, 130, 3, 2)])
-def test_ballistic_matches_oracle(cuda, nb, bs, ne, batch):
+@pytest.mark.parametrize("nb,bs,ne,batch", [(8, 48, 12, 5), (4, 96, 6, 6), (3, 130, 3, 2), (6, 256, 4, 4)])
+@pytest.mark.parametrize("greater", ["recursion", "identity"])
+def test_ballistic_matches_oracle(cuda, nb, bs, ne, batch, greater):
     h = orc.chain_device(nb, bs)
     energies = np.linspace(-1.0, 1.0, ne)
     ref = orc.ballistic(h, energies, 1e-3, 0.1, -0.1, 0.05, tol=1e-8)
-    out = ballistic_run(h, energies, 1e-3, Contacts(0.1, -0.1, 0.05), 1e-8, batch=batch, device=cuda)
+    out = ballistic_run(h, energies, 1e-3, Contacts(0.1, -0.1, 0.05), 1e-8, batch=batch, device=cuda,
+                        greater=greater)
     for k, v in out.items():
         assert rel(v, ref[k]) < TOL, k
 

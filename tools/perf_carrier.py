@@ -19,8 +19,10 @@ for spec in sys.argv[3:]:
     reps = 2
     for _ in range(reps):
         b = solver.solve(e, n_e=batch, check=False)
+    th = (time.perf_counter() - t0) / reps
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / reps
+    print(f"  host enqueue {th*1e3:.1f} ms/batch", flush=True)
     solver.check_status(b)
     print(f"{nb_}x{bs} batch={batch} streams={streams} algo={algo} overlap={ov}: {dt*1e3:.1f} ms/batch  {batch/dt:.1f} energies/s  "
           f"model {8.0*bs**3*(38*nb_-33)*batch/dt/1e12:.2f} TF", flush=True)
