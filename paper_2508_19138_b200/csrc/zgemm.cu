@@ -321,6 +321,9 @@ int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
     if (g.d[i].N > mx) mx = g.d[i].N;
   }
   if (mx <= 32) return launch_cfg<CfgSmall>(g, stream);
+  int mm = 0;
+  for (int i = 0; i < g.n; ++i) mm = g.d[i].M > mm ? g.d[i].M : mm;
+  if (mm <= 32 && (gemm_algo() == 2 || gemm_algo() == 4)) return launch_cfg<CfgGauss3>(g, stream);  // short M
   switch (gemm_algo()) {
     case 1: return launch_cfg<CfgGauss>(g, stream);
     case 2: return launch_cfg<CfgGauss2>(g, stream);

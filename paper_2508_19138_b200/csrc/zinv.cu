@@ -302,12 +302,28 @@ __global__ void zinv_swap_kernel(z_t* A, long long sA, int n, int k0, int nb, co
   const int* mv = moves + (long long)b * mv_stride;
   const int cnt = mv[0];
   if (col < n) {
-    for (int m = 0; m < cnt; ++m)
-      stage[m * blockDim.x + threadIdx.x] = a[(long long)(k0 + mv[2 + 2 * m]) * n + col];
+    // loads in chunks of 8 so 8 independent global reads are in flight per thread
+    for (int m0 = 0; m0 < cnt; m0 += 8) {
+      z_t t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (m0 + u < cnt) t[u] = a[(long long)(k0 + mv[2 + 2 * (m0 + u)]) * n + col];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (m0 + u < cnt) stage[(m0 + u) * blockDim.x + threadIdx.x] = t[u];
+    }
     for (int m = 0; m < cnt; ++m)
       a[(long long)(k0 + mv[1 + 2 * m]) * n + col] = stage[m * blockDim.x + threadIdx.x];
     z_t* rr = R + (long long)b * nb * n;
-    for (int j = 0; j < nb; ++j) rr[(long long)j * n + col] = a[(long long)(k0 + j) * n + col];
+    for (int j0 = 0; j0 < nb; j0 += 8) {
+      z_t t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j0 + u < nb) t[u] = a[(long long)(k0 + j0 + u) * n + col];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j0 + u < nb) rr[(long long)(j0 + u) * n + col] = t[u];
+    }
   }
   // The CTA(s) owning columns K copy the swapped panel columns cooperatively.
   const int c0 = blockIdx.x * blockDim.x, c1 = c0 + blockDim.x;
@@ -338,28 +354,46 @@ __global__ void zinv_rows_kernel(z_t* A, long long sA, int n, int k0, int nb, co
     a[(long long)(k0 + r) * n + col] = inK ? pi[r * nb + col - k0] : t[(long long)r * n + col];
 }
 
-// X = inv(PA) P: undo the interchanges on the columns while copying out.
-__global__ void zinv_unpermute_kernel(const z_t* __restrict__ A, long long sA, int n,
-                                      const int* ipiv, const double* umaxmin, z_t* X,
-                                      long long sX, int ldx, InvAux aux) {
-  extern __shared__ int perm[];
+// X = inv(PA) P: the row interchanges are undone on the columns (LAPACK
+// zgetri order: for k = n-1 .. 0 swap columns k <-> ipiv[k]). perm is built
+// once per matrix (ipiv staged in smem), then a wide grid does the copy.
+__global__ void zinv_perm_kernel(int n, const int* ipiv, const double* umaxmin, int* perm_out,
+                                 InvAux aux) {
+  extern __shared__ int sm_i[];
+  int* pv = sm_i;
+  int* perm = sm_i + n;
   const int b = blockIdx.x;
   if (aux.active && !aux.active[b]) return;
-  const int* pv = ipiv + (long long)b * n;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    pv[j] = ipiv[(long long)b * n + j];
+    perm[j] = j;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    for (int j = 0; j < n; ++j) perm[j] = j;
     for (int k = n - 1; k >= 0; --k) {
-      int r = pv[k];
-      int t = perm[k]; perm[k] = perm[r]; perm[r] = t;
+      const int r = pv[k];
+      const int t = perm[k]; perm[k] = perm[r]; perm[r] = t;
     }
     if (aux.u_spread) aux.u_spread[(long long)b * aux.spread_stride] = umaxmin[2 * b] / umaxmin[2 * b + 1];
   }
   __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) perm_out[(long long)b * n + j] = perm[j];
+}
+
+__global__ void zinv_unpermute_kernel(const z_t* __restrict__ A, long long sA, int n,
+                                      const int* perm_g, z_t* X, long long sX, int ldx,
+                                      const int* active) {
+  extern __shared__ int perm[];
+  const int b = blockIdx.y;
+  if (active && !active[b]) return;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) perm[j] = perm_g[(long long)b * n + j];
+  __syncthreads();
   const z_t* a = A + (long long)b * sA;
   z_t* x = X + (long long)b * sX;
-  for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) {
-    int i = (int)(e / n), j = (int)(e % n);
-    x[(long long)i * ldx + j] = a[(long long)i * n + perm[j]];
+  const int r0 = blockIdx.x * 8;
+  for (int e = threadIdx.x; e < 8 * n; e += blockDim.x) {
+    const int i = r0 + e / n, j = e % n;
+    if (i < n) x[(long long)i * ldx + j] = a[(long long)i * n + perm[j]];
   }
 }
 
@@ -487,8 +521,11 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
   }
   ProfScope ps3_(PROF_ZINV, stream);
   ProfScope ps3b_(8, stream);
-  zinv_unpermute_kernel<<<batch, 256, n * sizeof(int), stream>>>(S, sS, n, ipiv, umm, X, sX, ldx,
-                                                                 aux);
+  int* perm = reinterpret_cast<int*>(Cp);  // C' scratch is free after the last sweep (n nb complex >= n ints)
+  zinv_perm_kernel<<<batch, 128, 2 * n * sizeof(int), stream>>>(n, ipiv, umm, perm, aux);
+  NEGF_LAUNCHED();
+  dim3 gu((n + 7) / 8, batch);
+  zinv_unpermute_kernel<<<gu, 256, n * sizeof(int), stream>>>(S, sS, n, perm, X, sX, ldx, aux.active);
   NEGF_LAUNCHED();
   return 0;
 }
