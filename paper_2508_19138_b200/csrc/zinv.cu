@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
   constexpr int TPR = NB / 16;  // threads per row
   constexpr int LD = NB + 1;
   __shared__ z_t prow_s[NB];          // pivot row broadcast
+  __shared__ z_t ip_s;                // 1 / pivot
   __shared__ z_t blk[NB * LD];        // pivot rows (L\U) in pivot order, for Pinv
   __shared__ int posinv_s[1024];      // final position -> physical row
   __shared__ double rv[32];
@@ -175,39 +176,72 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
     smax = k0 == 0 ? 0.0 : umaxmin[2 * b];
     smin = k0 == 0 ? INFINITY : umaxmin[2 * b + 1];
   }
-#pragma unroll
-  for (int j = 0; j < NB; ++j) {
-    if (j >= w) break;
+  // The column loop stays rolled: unrolling it multiplies the code by NB and
+  // the kernel then runs out of the instruction cache. Register elements are
+  // selected with predicated moves instead of runtime indexing.
+#pragma unroll 1
+  for (int j = 0; j < w; ++j) {
     const int hj = j / 16, cj = j % 16;
-    // (1) argmax over active rows of |re|+|im| in column j; ties -> smallest position
-    double bv = -1.0;
-    int br = 1 << 30, bp = 1 << 30;
+    z_t vj = v[0];
+#pragma unroll
+    for (int c = 1; c < 16; ++c)
+      if (c == cj) vj = v[c];
+    // (1) argmax over active rows of |re|+|im| in column j; ties -> smallest
+    // LAPACK position. Non-negative doubles order like their bit patterns, so
+    // the warp stage is three REDUX ops (high word, low word, min position).
+    double bv = 0.0;
+    int bp = 0x7fffffff;
     if (act && h == hj) {
-      double c = zabs1(v[cj]);
+      double c = zabs1(vj);
       if (c != c) c = INFINITY;
-      bv = c; br = r; bp = pos;
+      bv = c;
+      bp = pos;
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_down_sync(0xffffffffu, bv, o);
-      const int orow = __shfl_down_sync(0xffffffffu, br, o);
-      const int opos = __shfl_down_sync(0xffffffffu, bp, o);
-      if (ov > bv || (ov == bv && opos < bp)) { bv = ov; br = orow; bp = opos; }
+    int br;
+    {
+      const unsigned long long key = __double_as_longlong(bv);
+      const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+      const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+      const bool best = hi == mhi && lo == mlo;
+      const int mpos = (int)__reduce_min_sync(0xffffffffu, best ? (unsigned)bp : 0x7fffffffu);
+      const unsigned who = __ballot_sync(0xffffffffu, best && bp == mpos);
+      const int src = who ? __ffs(who) - 1 : 0;
+      br = __shfl_sync(0xffffffffu, r, src);
+      if (lane == 0) {
+        rv[warp] = __longlong_as_double(((unsigned long long)mhi << 32) | mlo);
+        ri[warp] = mpos == 0x7fffffff ? -1 : br;
+        rp[warp] = mpos;
+      }
     }
-    if (lane == 0) { rv[warp] = bv; ri[warp] = br; rp[warp] = bp; }
     __syncthreads();
-    bv = rv[0]; br = ri[0]; bp = rp[0];
-    for (int w2 = 1; w2 < nw; ++w2)
-      if (rv[w2] > bv || (rv[w2] == bv && rp[w2] < bp)) { bv = rv[w2]; br = ri[w2]; bp = rp[w2]; }
-    // (2) pivot row broadcast
+    {  // cross-warp stage, redundantly in every warp (lanes < nw hold the entries)
+      const double wv = lane < nw ? rv[lane] : 0.0;
+      const int wp = lane < nw ? rp[lane] : 0x7fffffff;
+      const int wr = lane < nw ? ri[lane] : -1;
+      const unsigned long long key = __double_as_longlong(wv);
+      const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+      const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+      const bool best = hi == mhi && lo == mlo && wr >= 0;
+      const int mpos = (int)__reduce_min_sync(0xffffffffu, best ? (unsigned)wp : 0x7fffffffu);
+      const unsigned who = __ballot_sync(0xffffffffu, best && wp == mpos);
+      const int src = who ? __ffs(who) - 1 : 0;
+      br = __shfl_sync(0xffffffffu, wr, src);
+      bp = mpos;
+    }
+    // (2) pivot row broadcast (+ its reciprocal pivot, computed once)
     if (act && r == br) {
 #pragma unroll
       for (int c = 0; c < 16; ++c) prow_s[16 * h + c] = v[c];
+      if (h == hj) ip_s = zinv(vj);
     }
     __syncthreads();
     const z_t pv = prow_s[j];
+    const z_t ipv = ip_s;
     // (3) multipliers and rank-1 update of the other active rows (registers)
     // column-j value of my row, from the thread holding it (all lanes shuffle)
-    z_t own = v[cj];
+    z_t own = vj;
     if (TPR > 1) {
       own.x = __shfl_sync(0xffffffffu, own.x, (lane & ~(TPR - 1)) | hj);
       own.y = __shfl_sync(0xffffffffu, own.y, (lane & ~(TPR - 1)) | hj);
@@ -216,7 +250,7 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
       act = false;
       pos = j;
     } else if (act) {
-      const z_t l = zmul(own, zinv(pv));
+      const z_t l = zmul(own, ipv);
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         const int gc = 16 * h + c;

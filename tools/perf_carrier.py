@@ -8,10 +8,12 @@ dev = torch.device('cuda')
 h = toys.chain_device(nb_, bs)
 from paper_2508_19138_b200 import _lib
 for spec in sys.argv[3:]:
-    batch, streams, algo, ov = (int(x) for x in spec.split('x'))
+    batch, streams, algo, ov = (int(x.replace("m", "-")) for x in spec.split("x"))
     _lib.load().negf_set_gemm_algo(algo)
     _lib.load().negf_set_rgf_overlap(ov)
-    solver = CarrierSolver(h, 1e-3, Contacts(0.1, -0.1, 0.05), 1e-8, device=dev, streams=streams)
+    solver = CarrierSolver(h, 1e-3, Contacts(0.1, -0.1, 0.05), 1e-8, device=dev, streams=streams,
+                           greater="identity" if streams < 0 else "recursion")
+    streams = abs(streams)
     e = np.linspace(-2, 2, batch)
     solver.solve(e, n_e=batch)
     torch.cuda.synchronize()
