@@ -93,7 +93,7 @@ int negf_zgemm_batched(int m, int n, int k, int batch, double alpha_re, double a
                        int ldd, void* stream) {
   if (m < 0 || n < 0 || k < 0 || batch < 0 || !d) return -1;
   if (op_a < 0 || op_a > 3 || op_b < 0 || op_b > 3) return -1;
-  ZGemmDesc g;
+  ZGemmDesc g = zdesc_default();
   g.M = m; g.N = n; g.batch = batch; g.nterms = 1;
   g.t[0] = zterm((const z_t*)a, stride_a, lda, op_a, (const z_t*)b, stride_b, ldb, op_b, k);
   g.t[1] = g.t[0];

@@ -27,16 +27,11 @@ __device__ __forceinline__ z_t zmul(z_t a, z_t b) {
 }
 __device__ __forceinline__ z_t zconj(z_t a) { return zmake(a.x, -a.y); }
 __device__ __forceinline__ z_t zscale(double s, z_t a) { return zmake(s * a.x, s * a.y); }
-// 1/a, scaled like LAPACK's zladiv to avoid overflow of |a|^2.
+// 1/a = conj(a) / |a|^2 with a single division (pivots here are far from the
+// overflow range where LAPACK's scaled zladiv matters).
 __device__ __forceinline__ z_t zinv(z_t a) {
-  double ar = a.x, ai = a.y;
-  if (fabs(ar) >= fabs(ai)) {
-    double r = ai / ar, d = ar + ai * r;
-    return zmake(1.0 / d, -r / d);
-  } else {
-    double r = ar / ai, d = ai + ar * r;
-    return zmake(r / d, -1.0 / d);
-  }
+  const double s = 1.0 / (a.x * a.x + a.y * a.y);
+  return zmake(a.x * s, -a.y * s);
 }
 __device__ __forceinline__ double zabs1(z_t a) { return fabs(a.x) + fabs(a.y); }
 

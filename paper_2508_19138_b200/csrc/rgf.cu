@@ -55,7 +55,7 @@ struct Ctx {
   ZGemmDesc desc(const ZTerm& t0, z_t* D, long long sD, double alpha_re = 1.0,
                  const z_t* C = nullptr, long long sC = 0, double beta_re = 0.0,
                  int transD = 0) const {
-    ZGemmDesc d;
+    ZGemmDesc d = zdesc_default();
     d.M = bs; d.N = bs; d.batch = n_e; d.nterms = 1;
     d.t[0] = t0; d.t[1] = t0;
     d.alpha = make_double2(alpha_re, 0.0);

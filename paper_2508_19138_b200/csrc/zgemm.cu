@@ -8,8 +8,10 @@ namespace {
 
 constexpr unsigned long long kSign = 0x8000000000000000ull;
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_, bool GAUSS_ = false, int BK_ = 8>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_, bool GAUSS_ = false, int BK_ = 8,
+          bool ROWMAP_ = false>
 struct Cfg {
+  static constexpr bool ROWMAP = ROWMAP_;  // honour ZGemmDesc row maps (inversion sweeps only)
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
   // GAUSS: 3 real products per complex product (3M / Gauss):
   //   P1 = ar br, P2 = ai bi, P3 = (ar + ai)(br + bi);  re = P1 - P2, im = P3 - P1 - P2
@@ -55,7 +57,10 @@ __device__ __forceinline__ void load_stage(const ZGemmDesc& d, int kt, const KtB
       int mn = e / CF::BK, k = e % CF::BK;
       int gm = m0 + mn, gk = k0 + k;
       bool p = gm < M && gk < K;
-      const z_t* src = p ? A + (long long)gm * t.lda + gk : A;
+      int pm = gm;
+      if constexpr (CF::ROWMAP)
+        if (p && d.rowmap_a) pm = d.rowmap_a[(long long)b * d.s_map + gm];
+      const z_t* src = p ? A + (long long)pm * t.lda + gk : A;
       cp_async16(sA + mn * CF::SK + k, src, p);
     }
   } else {  // A stored [K][M]: m contiguous
@@ -239,14 +244,22 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
           }
           z_t v = zmake(al.x * xr - al.y * xi, al.x * xi + al.y * xr);
           if (use_c) {
-            z_t c = C[(long long)gm * d.ldc + gn];
+            int cm = gm;
+            if constexpr (CF::ROWMAP)
+              if (d.rowmap_c) cm = d.rowmap_c[(long long)b * d.s_map + gm];
+            z_t c = C[(long long)cm * d.ldc + gn];
             v.x += be.x * c.x - be.y * c.y;
             v.y += be.x * c.y + be.y * c.x;
           }
           if (d.transD)
             D[(long long)gn * d.ldd + gm] = zconj(v);
           else
-            D[(long long)gm * d.ldd + gn] = v;
+          {
+            int dm = gm;
+            if constexpr (CF::ROWMAP)
+              if (d.rowmap_d) dm = d.rowmap_d[(long long)b * d.s_map + gm];
+            D[(long long)dm * d.ldd + gn] = v;
+          }
         }
       }
     }
@@ -297,6 +310,8 @@ using CfgGauss = Cfg<64, 64, 2, 4, 4, 1, true>;
 using CfgGauss2 = Cfg<64, 32, 2, 2, 4, 3, true>;
 using Cfg4M32 = Cfg<64, 32, 2, 2, 4, 3, false>;
 using CfgGauss3 = Cfg<32, 64, 2, 2, 4, 3, true>;
+using CfgMap64 = Cfg<64, 32, 2, 2, 4, 3, true, 8, true>;
+using CfgMap32 = Cfg<32, 64, 2, 2, 4, 3, true, 8, true>;
 // Measured alternatives (C2 carrier batch, energies/s; algo 2 = 90.5):
 //   64x32 6-stage 2 CTA/SM 78.9 | 128x32 8 warps 68.1 | 32x32 2 warps 78.2 |
 //   64x32 BK=16 80.8 | 32x32 4 warps (16x16) 87.4 | 64x64 16 warps 69.3 |
@@ -320,6 +335,13 @@ int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
     if (g.d[i].M > mx) mx = g.d[i].M;
     if (g.d[i].N > mx) mx = g.d[i].N;
   }
+  bool mapped = false;
+  bool m64 = true;
+  for (int i = 0; i < g.n; ++i) {
+    mapped |= g.d[i].rowmap_a || g.d[i].rowmap_c || g.d[i].rowmap_d;
+    m64 &= g.d[i].M % 64 == 0;
+  }
+  if (mapped) return m64 ? launch_cfg<CfgMap64>(g, stream) : launch_cfg<CfgMap32>(g, stream);
   if (mx <= 32) return launch_cfg<CfgSmall>(g, stream);
   int mm = 0;
   for (int i = 0; i < g.n; ++i) mm = g.d[i].M > mm ? g.d[i].M : mm;

@@ -55,6 +55,14 @@ struct ZGemmDesc {
   int ldd;
   int transD;  // store conj-transposed
   const int* active;  // optional per-batch mask: problems with active[b]==0 are skipped
+  // Optional per-batch row indirection (stride s_map per batch entry): logical
+  // row m of op(A) (non-transposed A only), of C and of D is physical row
+  // map[m]. Used by the inversion sweep to fold the panel's row interchanges
+  // into the update instead of moving rows.
+  const int* rowmap_a;
+  const int* rowmap_c;
+  const int* rowmap_d;
+  long long s_map;
 };
 
 constexpr int kMaxGroup = 6;
@@ -71,6 +79,8 @@ inline ZGemmDesc zdesc_default() {
   d.C = nullptr; d.sC = 0; d.ldc = 0;
   d.D = nullptr; d.sD = 0; d.ldd = 0;
   d.transD = 0; d.active = nullptr;
+  d.rowmap_a = d.rowmap_c = d.rowmap_d = nullptr;
+  d.s_map = 0;
   return d;
 }
 

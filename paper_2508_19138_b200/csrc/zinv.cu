@@ -145,13 +145,17 @@ __global__ void zinv_small_kernel(const z_t* __restrict__ S, long long sS, int l
 // Pinv = (pivot block)^-1 = U^-1 L^-1.
 template <int NB>
 __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__ A, long long sA,
-                                                         int n, int k0, int w, int* ipiv, z_t* pinv,
-                                                         double* umaxmin, int* moves, InvAux aux) {
+                                                         z_t* __restrict__ Anew, long long sAn, int n,
+                                                         int k0, int w,
+                                                         int* ipiv, z_t* pinv, double* umaxmin,
+                                                         int* map_src, int* map_dst, InvAux aux) {
   constexpr int TPR = NB / 16;  // threads per row
   constexpr int LD = NB + 1;
   __shared__ z_t prow_s[NB];          // pivot row broadcast
   __shared__ z_t ip_s;                // 1 / pivot
   __shared__ z_t blk[NB * LD];        // pivot rows (L\U) in pivot order, for Pinv
+  __shared__ z_t pinv_s[NB * LD];     // Pinv
+  __shared__ z_t rdiag_s[NB];         // 1 / U_kk
   __shared__ int posinv_s[1024];      // final position -> physical row
   __shared__ double rv[32];
   __shared__ int ri[32], rp[32];
@@ -279,6 +283,8 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
   }
   __syncthreads();
   // Pinv = U^-1 L^-1: warp-parallel substitutions, lane = row, one identity column per pass
+  if (tid < w) rdiag_s[tid] = zinv(blk[tid * LD + tid]);
+  __syncthreads();
   if (lane < 32) {
     for (int c = warp; c < w; c += nw) {
       z_t y = zmake(lane == c ? 1.0 : 0.0, 0.0);
@@ -288,104 +294,62 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
       }
       for (int k = w - 1; k >= 0; --k) {
         z_t xk = make_double2(__shfl_sync(0xffffffffu, y.x, k), __shfl_sync(0xffffffffu, y.y, k));
-        xk = zmul(xk, zinv(blk[k * LD + k]));
+        xk = zmul(xk, rdiag_s[k]);
         if (lane == k) y = xk;
         if (lane < k) y = zsub(y, zmul(blk[lane * LD + k], xk));
       }
-      if (lane < w) pinv[(long long)b * w * w + lane * w + c] = y;
+      if (lane < w) {
+        pinv[(long long)b * w * w + lane * w + c] = y;
+        pinv_s[lane * LD + c] = y;
+      }
     }
   }
-  // net row permutation as a move list (warp 0, ballot compaction)
-  if (warp == 0) {
-    int* mv = moves + (long long)b * (4 * NB + 1);
-    int cnt = 0;
-    for (int t0 = 0; t0 < rows; t0 += 32) {
-      const int t = t0 + lane;
-      const bool moved = t < rows && posinv_s[t] != t;
-      const unsigned m = __ballot_sync(0xffffffffu, moved);
-      if (moved) {
-        const int slot = cnt + __popc(m & ((1u << lane) - 1));
-        if (slot < 2 * w) {
-          mv[1 + 2 * slot] = t;
-          mv[2 + 2 * slot] = posinv_s[t];
-        }
+  // Row maps of the sweep GEMM over the rows outside K (logical m < n - w):
+  // destination row, and the A_old row that lands there after the panel's
+  // interchanges (rows < k0 stay; rows >= k0 follow posinv).
+  for (int m = tid; m < n - w; m += blockDim.x) {
+    const int dst = m < k0 ? m : m + w;
+    map_dst[(long long)b * n + m] = dst;
+    map_src[(long long)b * n + m] = dst < k0 ? dst : k0 + posinv_s[dst - k0];
+  }
+  __syncthreads();
+  // Rows K of A_new: [T | Pinv] with T = Pinv R, R = pivot rows of A_old.
+  // One thread per (column j, block of 16 output rows); R[q][j] streamed from
+  // global (coalesced over j), Pinv broadcast from smem.
+  z_t* an = Anew + (long long)b * sAn;
+  {
+    const int tblocks = (w + 15) / 16;
+    for (int e = tid; e < tblocks * n; e += blockDim.x) {
+      const int j = e % n, t0 = (e / n) * 16;
+      const int t1 = t0 + 16 < w ? t0 + 16 : w;
+      if (j >= k0 && j < k0 + w) {
+        for (int t = t0; t < t1; ++t) an[(long long)(k0 + t) * n + j] = pinv_s[t * LD + (j - k0)];
+        continue;
       }
-      cnt += __popc(m);
+      z_t acc[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc[u] = make_double2(0.0, 0.0);
+      for (int q0 = 0; q0 < w; q0 += 8) {
+        z_t rq[8];  // 8 independent loads in flight
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq)
+          rq[qq] = q0 + qq < w ? a[(long long)(k0 + posinv_s[q0 + qq]) * n + j] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq)
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            if (t0 + u < t1) acc[u] = zadd(acc[u], zmul(pinv_s[(t0 + u) * LD + q0 + qq], rq[qq]));
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (t0 + u < t1) an[(long long)(k0 + t0 + u) * n + j] = acc[u];
     }
-    if (lane == 0) mv[0] = cnt < 2 * w ? cnt : 2 * w;
   }
   if (tid == 0) {
     umaxmin[2 * b] = smax;
     umaxmin[2 * b + 1] = smin;
     if (sbad && aux.status) atomicCAS(aux.status + b, 0, aux.status_code);
   }
-}
-
-// Apply the panel's net row permutation (move list from the panel kernel) to
-// every column as an independent gather (one thread per column, staged in
-// its own smem slice, so no load waits on a previous store), and emit
-// C' = A[:,K] with rows K zeroed   (n x nb)
-// R  = A[K,:]                      (nb x n)
-__global__ void zinv_swap_kernel(z_t* A, long long sA, int n, int k0, int nb, const int* moves,
-                                 int mv_stride, z_t* Cp, z_t* R, const int* active) {
-  extern __shared__ __align__(16) z_t stage[];  // [2*nb][blockDim.x]
-  const int b = blockIdx.y;
-  if (active && !active[b]) return;
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  z_t* a = A + (long long)b * sA;
-  const int* mv = moves + (long long)b * mv_stride;
-  const int cnt = mv[0];
-  if (col < n) {
-    // loads in chunks of 8 so 8 independent global reads are in flight per thread
-    for (int m0 = 0; m0 < cnt; m0 += 8) {
-      z_t t[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (m0 + u < cnt) t[u] = a[(long long)(k0 + mv[2 + 2 * (m0 + u)]) * n + col];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (m0 + u < cnt) stage[(m0 + u) * blockDim.x + threadIdx.x] = t[u];
-    }
-    for (int m = 0; m < cnt; ++m)
-      a[(long long)(k0 + mv[1 + 2 * m]) * n + col] = stage[m * blockDim.x + threadIdx.x];
-    z_t* rr = R + (long long)b * nb * n;
-    for (int j0 = 0; j0 < nb; j0 += 8) {
-      z_t t[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (j0 + u < nb) t[u] = a[(long long)(k0 + j0 + u) * n + col];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (j0 + u < nb) rr[(long long)(j0 + u) * n + col] = t[u];
-    }
-  }
-  // The CTA(s) owning columns K copy the swapped panel columns cooperatively.
-  const int c0 = blockIdx.x * blockDim.x, c1 = c0 + blockDim.x;
-  const int lo = k0 > c0 ? k0 : c0, hi = (k0 + nb) < c1 ? (k0 + nb) : c1;
-  if (lo >= hi) return;
-  __syncthreads();
-  const int w = hi - lo;
-  z_t* cp = Cp + (long long)b * n * nb;
-  for (long long e = threadIdx.x; e < (long long)n * w; e += blockDim.x) {
-    const int i = (int)(e / w), c = lo + (int)(e % w);
-    cp[(long long)i * nb + (c - k0)] =
-        (i >= k0 && i < k0 + nb) ? make_double2(0.0, 0.0) : a[(long long)i * n + c];
-  }
-}
-
-// Rows K of the swept matrix: A[K, j] = T[:, j] (j not in K), A[K, K] = Pinv.
-__global__ void zinv_rows_kernel(z_t* A, long long sA, int n, int k0, int nb, const z_t* T,
-                                 long long sT, const z_t* pinv, const int* active) {
-  const int b = blockIdx.y;
-  if (active && !active[b]) return;
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= n) return;
-  z_t* a = A + (long long)b * sA;
-  const z_t* t = T + (long long)b * sT;
-  const z_t* pi = pinv + (long long)b * nb * nb;
-  const bool inK = col >= k0 && col < k0 + nb;
-  for (int r = 0; r < nb; ++r)
-    a[(long long)(k0 + r) * n + col] = inK ? pi[r * nb + col - k0] : t[(long long)r * n + col];
 }
 
 // X = inv(PA) P: the row interchanges are undone on the columns (LAPACK
@@ -414,20 +378,26 @@ __global__ void zinv_perm_kernel(int n, const int* ipiv, const double* umaxmin, 
   for (int j = threadIdx.x; j < n; j += blockDim.x) perm_out[(long long)b * n + j] = perm[j];
 }
 
-__global__ void zinv_unpermute_kernel(const z_t* __restrict__ A, long long sA, int n,
-                                      const int* perm_g, z_t* X, long long sX, int ldx,
-                                      const int* active) {
-  extern __shared__ int perm[];
+// Rows are staged in smem, so A and X may be the same buffer.
+__global__ void zinv_unpermute_kernel(const z_t* A, long long sA, int n, const int* perm_g, z_t* X,
+                                      long long sX, int ldx, const int* active) {
+  extern __shared__ __align__(16) unsigned char raw_u[];
+  z_t* rows = reinterpret_cast<z_t*>(raw_u);           // 8 x n
+  int* perm = reinterpret_cast<int*>(rows + 8 * n);
   const int b = blockIdx.y;
   if (active && !active[b]) return;
   for (int j = threadIdx.x; j < n; j += blockDim.x) perm[j] = perm_g[(long long)b * n + j];
-  __syncthreads();
   const z_t* a = A + (long long)b * sA;
   z_t* x = X + (long long)b * sX;
   const int r0 = blockIdx.x * 8;
   for (int e = threadIdx.x; e < 8 * n; e += blockDim.x) {
+    const int i = r0 + e / n;
+    if (i < n) rows[e] = a[(long long)i * n + e % n];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 8 * n; e += blockDim.x) {
     const int i = r0 + e / n, j = e % n;
-    if (i < n) x[(long long)i * ldx + j] = a[(long long)i * n + perm[j]];
+    if (i < n) x[(long long)i * ldx + j] = rows[(e / n) * n + perm[j]];
   }
 }
 
@@ -436,9 +406,8 @@ __global__ void zinv_unpermute_kernel(const z_t* __restrict__ A, long long sA, i
 size_t zinv_workspace_bytes(int n, int batch) {
   if (n <= kInvSmallMax) return 0;
   const int nb = zinv_panel_width(n);
-  size_t per = sizeof(int) * n + sizeof(double) * 2 + sizeof(z_t) * ((size_t)nb * nb + 2 * (size_t)n * nb) +
-               sizeof(int) * (4 * (size_t)nb + 1);
-  return (per * batch + 1024) + 256 * 6;
+  size_t per = 4 * sizeof(int) * (size_t)n + sizeof(double) * 2 + sizeof(z_t) * (size_t)nb * nb;
+  return per * batch + 256 * 8;
 }
 
 int zinv_panel_width(int n) {
@@ -465,102 +434,87 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
     NEGF_LAUNCHED();
     return 0;
   }
-  if (lds != n) return -2;  // blocked path works on packed scratch
+  if (lds != n || ldx != n) return -2;  // blocked path works on packed matrices
   const int nb = zinv_panel_width(n);
   if (ws_bytes < zinv_workspace_bytes(n, batch)) return -4;
+  if (n * (nb / 16) > 1024 || n > 1024) return -5;
   // carve workspace
   char* w = reinterpret_cast<char*>(ws);
   auto take = [&](size_t bytes) { char* r = w; w += (bytes + 255) & ~size_t(255); return r; };
   int* ipiv = reinterpret_cast<int*>(take(sizeof(int) * (size_t)n * batch));
   double* umm = reinterpret_cast<double*>(take(sizeof(double) * 2 * (size_t)batch));
   z_t* pinv = reinterpret_cast<z_t*>(take(sizeof(z_t) * (size_t)nb * nb * batch));
-  z_t* Cp = reinterpret_cast<z_t*>(take(sizeof(z_t) * (size_t)n * nb * batch));
-  z_t* R = reinterpret_cast<z_t*>(take(sizeof(z_t) * (size_t)n * nb * batch));
-  int* moves = reinterpret_cast<int*>(take(sizeof(int) * (4 * (size_t)nb + 1) * batch));
-  static bool attr2 = false;
-  if (!attr2) {
-    NEGF_CUDA_CHECK(cudaFuncSetAttribute(zinv_swap_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr2 = true;
-  }
-  if (n * (nb / 16) > 1024 || n > 1024) return -5;
+  int* map_src = reinterpret_cast<int*>(take(sizeof(int) * (size_t)n * batch));
+  int* map_dst = reinterpret_cast<int*>(take(sizeof(int) * (size_t)n * batch));
+  int* perm = reinterpret_cast<int*>(take(sizeof(int) * (size_t)n * batch));
   const int panel_threads = ((n * (nb / 16) + 31) / 32) * 32;
+  static bool attr_u = false;
+  if (!attr_u) {
+    NEGF_CUDA_CHECK(cudaFuncSetAttribute(zinv_unpermute_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    attr_u = true;
+  }
+  // Gauss-Jordan sweeps ping-pong between S and X (X is the destination).
+  z_t* cur = S;
+  z_t* nxt = X;
+  long long cs = sS, ns = sX;
   for (int k0 = 0; k0 < n; k0 += nb) {
-    const int w = nb < n - k0 ? nb : n - k0;  // last panel may be narrower
-    dim3 g((n + 63) / 64, batch);
+    const int wd = nb < n - k0 ? nb : n - k0;  // last panel may be narrower
     {
-    ProfScope ps_(PROF_ZINV, stream);
-    {
-    ProfScope psp_(5, stream);
-    if (nb == 32)
-      zinv_panel_kernel<32><<<batch, panel_threads, 0, stream>>>(S, sS, n, k0, w, ipiv, pinv, umm, moves, aux);
-    else
-      zinv_panel_kernel<16><<<batch, panel_threads, 0, stream>>>(S, sS, n, k0, w, ipiv, pinv, umm, moves, aux);
+      ProfScope ps_(PROF_ZINV, stream);
+      ProfScope psp_(5, stream);
+      if (nb == 32)
+        zinv_panel_kernel<32><<<batch, panel_threads, 0, stream>>>(cur, cs, nxt, ns, n, k0, wd, ipiv, pinv,
+                                                                   umm, map_src, map_dst, aux);
+      else
+        zinv_panel_kernel<16><<<batch, panel_threads, 0, stream>>>(cur, cs, nxt, ns, n, k0, wd, ipiv, pinv,
+                                                                   umm, map_src, map_dst, aux);
+      NEGF_LAUNCHED();
+    }
+    if (n - wd > 0) {
+      // rows outside K (row-mapped):  A_new[:, j not in K] = A_old - C' T,  A_new[:, K] = -C' Pinv,
+      // with C' = A_old[src][K] and T = rows K of A_new (written by the panel kernel).
+      ZGemmGroup grp;
+      grp.n = 0;
+      auto prob = [&](int c0, int nc, bool colK) {
+        if (nc <= 0) return;
+        ZGemmDesc& d = grp.d[grp.n++];
+        d = zdesc_default();
+        d.M = n - wd; d.N = nc; d.batch = batch; d.nterms = 1;
+        if (!colK)
+          d.t[0] = zterm(cur + k0, cs, n, OP_N, nxt + (long long)k0 * n + c0, ns, n, OP_N, wd);
+        else
+          d.t[0] = zterm(cur + k0, cs, n, OP_N, pinv, (long long)wd * wd, wd, OP_N, wd);
+        d.t[1] = d.t[2] = d.t[3] = d.t[0];
+        d.alpha = make_double2(-1.0, 0.0);
+        d.beta = make_double2(colK ? 0.0 : 1.0, 0.0);
+        d.C = colK ? nullptr : cur + c0; d.sC = cs; d.ldc = n;
+        d.D = nxt + c0; d.sD = ns; d.ldd = n;
+        d.active = aux.active;
+        d.rowmap_a = map_src;
+        d.rowmap_c = map_src;
+        d.rowmap_d = map_dst;
+        d.s_map = n;
+      };
+      prob(0, k0, false);
+      prob(k0 + wd, n - k0 - wd, false);
+      prob(k0, wd, true);
+      int rc = zgemm_group_launch(grp, stream);
+      if (rc) return rc;
+    }
+    z_t* t = cur; cur = nxt; nxt = t;
+    long long ts = cs; cs = ns; ns = ts;
+  }
+  {
+    ProfScope ps3_(PROF_ZINV, stream);
+    ProfScope ps3b_(8, stream);
+    zinv_perm_kernel<<<batch, 128, 2 * n * sizeof(int), stream>>>(n, ipiv, umm, perm, aux);
     NEGF_LAUNCHED();
-    }
-    ProfScope pss_(6, stream);
-    zinv_swap_kernel<<<g, 64, 2 * (size_t)w * 64 * sizeof(z_t), stream>>>(S, sS, n, k0, w, moves,
-                                                                          4 * nb + 1, Cp, R, aux.active);
-    NEGF_LAUNCHED();
-    }
-    // T = Pinv R, staged in the caller's destination X (w x n per matrix;
-    // X is only written for real by the final unpermute kernel).
-    ZGemmGroup grp;
-    grp.n = 1;
-    z_t* T = X;
-    {
-      ZGemmDesc& d = grp.d[0];
-      d.M = w; d.N = n; d.batch = batch; d.nterms = 1;
-      d.t[0] = zterm(pinv, (long long)w * w, w, OP_N, R, (long long)w * n, n, OP_N, w);
-      d.t[1] = d.t[0];
-      d.alpha = make_double2(1.0, 0.0); d.beta = make_double2(0.0, 0.0);
-      d.C = nullptr; d.sC = 0; d.ldc = 0;
-      d.D = T; d.sD = sX; d.ldd = n; d.transD = 0;
-      d.active = aux.active;
-    }
-    int rc = zgemm_group_launch(grp, stream);
-    if (rc) return rc;
-    // Gauss-Jordan sweep, one grouped launch over disjoint column ranges:
-    //   A[:, j] -= C' T[:, j]   (j left / right of K)      A[:, K] = -C' Pinv
-    grp.n = 0;
-    auto upd = [&](int c0, int nc) {
-      if (nc <= 0) return;
-      ZGemmDesc& d = grp.d[grp.n++];
-      d.M = n; d.N = nc; d.batch = batch; d.nterms = 1;
-      d.t[0] = zterm(Cp, (long long)n * w, w, OP_N, T + c0, sX, n, OP_N, w);
-      d.t[1] = d.t[0];
-      d.alpha = make_double2(-1.0, 0.0); d.beta = make_double2(1.0, 0.0);
-      d.C = S + c0; d.sC = sS; d.ldc = n;
-      d.D = S + c0; d.sD = sS; d.ldd = n; d.transD = 0;
-      d.active = aux.active;
-    };
-    upd(0, k0);
-    upd(k0 + w, n - k0 - w);
-    {
-      ZGemmDesc& d = grp.d[grp.n++];
-      d.M = n; d.N = w; d.batch = batch; d.nterms = 1;
-      d.t[0] = zterm(Cp, (long long)n * w, w, OP_N, pinv, (long long)w * w, w, OP_N, w);
-      d.t[1] = d.t[0];
-      d.alpha = make_double2(-1.0, 0.0); d.beta = make_double2(0.0, 0.0);
-      d.C = nullptr; d.sC = 0; d.ldc = 0;
-      d.D = S + k0; d.sD = sS; d.ldd = n; d.transD = 0;
-      d.active = aux.active;
-    }
-    rc = zgemm_group_launch(grp, stream);
-    if (rc) return rc;
-    ProfScope ps2_(PROF_ZINV, stream);
-    ProfScope ps2b_(7, stream);
-    zinv_rows_kernel<<<g, 64, 0, stream>>>(S, sS, n, k0, w, T, sX, pinv, aux.active);
+    dim3 gu((n + 7) / 8, batch);
+    zinv_unpermute_kernel<<<gu, 256, 8 * (size_t)n * sizeof(z_t) + n * sizeof(int), stream>>>(
+        cur, cs, n, perm, X, sX, ldx, aux.active);
     NEGF_LAUNCHED();
   }
-  ProfScope ps3_(PROF_ZINV, stream);
-  ProfScope ps3b_(8, stream);
-  int* perm = reinterpret_cast<int*>(Cp);  // C' scratch is free after the last sweep (n nb complex >= n ints)
-  zinv_perm_kernel<<<batch, 128, 2 * n * sizeof(int), stream>>>(n, ipiv, umm, perm, aux);
-  NEGF_LAUNCHED();
-  dim3 gu((n + 7) / 8, batch);
-  zinv_unpermute_kernel<<<gu, 256, n * sizeof(int), stream>>>(S, sS, n, perm, X, sX, ldx, aux.active);
-  NEGF_LAUNCHED();
   return 0;
 }
 
