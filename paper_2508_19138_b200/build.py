@@ -72,8 +72,11 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
         if len(procs) >= (jobs or os.cpu_count() or 4):
             _drain(procs)
     _drain(procs)
-    newest = max(o.stat().st_mtime for o in objs)
-    if not LIB.exists() or LIB.stat().st_mtime < newest:
+    # relink whenever the SET of objects differs from what the library was linked from
+    manifest = BUILD / "libnegf_b200.manifest"
+    want = "\n".join(o.name for o in objs)
+    have = manifest.read_text() if manifest.exists() else ""
+    if not LIB.exists() or have != want:
         cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB) + ".tmp", *map(str, objs), "-lcudart"]
         if verbose:
             print(" ".join(cmd), flush=True)
@@ -81,6 +84,7 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
         if out.returncode != 0:
             raise RuntimeError(f"link failed:\n{out.stdout}\n{out.stderr}")
         os.replace(str(LIB) + ".tmp", LIB)
+        manifest.write_text(want)
     return LIB
 
 

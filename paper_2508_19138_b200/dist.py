@@ -100,3 +100,20 @@ class Transposer:
         out_splits = [(s.stop - s.start) * self.n_own_e for s in self.r_sl]
         recv = self._a2a(send, in_splits, out_splits)
         return recv.view(self.n_entries, self.n_own_e)
+
+
+TO_ENTRY_MAJOR = "to_entry_major"
+TO_ENERGY_MAJOR = "to_energy_major"
+
+
+def transpose_distribution(comm: Comm, local_part, direction: str, n_entries: int, n_e: int):
+    """scba.py:342-368 semantics for one quantity, as an all-to-all: the
+    reference returns the replicated full array; here each rank receives only
+    the slab it owns (entry rows for to_entry_major, energy columns for
+    to_energy_major), which is all any caller on the hot path reads."""
+    tr = Transposer(comm, n_entries, n_e)
+    if direction == TO_ENTRY_MAJOR:
+        return tr.to_entry_major(local_part)
+    if direction == TO_ENERGY_MAJOR:
+        return tr.to_energy_major(local_part)
+    raise ValueError(f"unknown transpose direction {direction!r}")

@@ -207,6 +207,56 @@ class ScbaState:
         return self.lesser, self.greater, self.ret_upper, self.ret_lower
 
 
+@dataclass(frozen=True)
+class EnergyGrid:
+    """device.py:39-73: uniform energy axis (linspace) with broadening eta."""
+
+    e_min: float
+    e_max: float
+    n_e: int
+    eta: float = 1e-3
+
+    def __post_init__(self) -> None:
+        if self.n_e < 2:
+            raise ValueError(f"n_e must be at least 2, got {self.n_e}")
+        if not self.e_max > self.e_min:
+            raise ValueError(f"need e_max > e_min, got [{self.e_min}, {self.e_max}]")
+        if not self.eta > 0.0:
+            raise ValueError(f"eta must be positive, got {self.eta}")
+
+    @property
+    def de(self) -> float:
+        return (self.e_max - self.e_min) / (self.n_e - 1)
+
+    @property
+    def energies(self) -> np.ndarray:
+        return np.linspace(self.e_min, self.e_max, self.n_e)
+
+
+def _stacks(m):
+    """Block stacks from either (diag, upper, lower) arrays or any object with
+    the BlockMatrix API (ours or the reference's)."""
+    if hasattr(m, "get_block"):
+        from .blocks import tridiag_arrays
+
+        if m.block_bandwidth > 3:
+            raise ValueError("the hot path takes block-tridiagonal H and V")
+        return tridiag_arrays(m)
+    return m
+
+
+def scba_run_reference_api(h_mat, v_mat, grid, contacts, options: ScbaOptions | None = None,
+                           comm: Comm | None = None, initial_sigma: ScbaState | None = None,
+                           device="cuda") -> dict:
+    """scba.py:865 signature: BlockMatrix H / V (or None), an EnergyGrid-like
+    grid (energies, eta) and a ContactConfig-like object (mu_left, mu_right,
+    kT). The spatial-partition ``plan`` argument of the reference is not part
+    of this path (energy sharding via ``comm`` only)."""
+    c = Contacts(contacts.mu_left, contacts.mu_right, contacts.kT)
+    return scba_run(_stacks(h_mat), None if v_mat is None else _stacks(v_mat), grid.energies, grid.eta, c,
+                    options, device=device, comm=comm, initial_sigma=initial_sigma)
+
+
 def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOptions | None = None,
              device="cuda", keep_g: bool = True, initial_sigma: ScbaState | None = None,
              comm: Comm | None = None, profile: bool = False, sigma_to_host: bool = True) -> dict:

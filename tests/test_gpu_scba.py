@@ -101,3 +101,27 @@ def test_scba_c1_matches_oracle_two_iterations(cuda):
     res = scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=2, tol=1e-12), device=cuda)
     for k in ref:
         assert rel(res[k], ref[k]) < TOL, k
+
+
+def test_scba_reference_api_with_blockmatrix_inputs(golden, cuda):
+    """scba.py:865 call shape: BlockMatrix H/V, EnergyGrid, ContactConfig-like."""
+    from paper_2508_19138_b200 import BlockMatrix
+    from paper_2508_19138_b200.scba import EnergyGrid, scba_run_reference_api
+    from types import SimpleNamespace
+
+    def bm(stacks):
+        d, u, l = stacks
+        m = BlockMatrix(d.shape[0], d.shape[-1])
+        for i in range(d.shape[0]):
+            m.set_block(i, i, d[i])
+            if i + 1 < d.shape[0]:
+                m.set_block(i, i + 1, u[i])
+                m.set_block(i + 1, i, l[i])
+        return m
+
+    g = golden("golden_scba_small.npz")
+    res = scba_run_reference_api(bm(orc.chain_device(6, 4)), bm(orc.coulomb_matrix(6, 4)), EnergyGrid(-2.0, 2.0, 32),
+                                 SimpleNamespace(mu_left=0.1, mu_right=-0.1, kT=0.05),
+                                 ScbaOptions(max_iter=3, tol=1e-12), device=cuda)
+    for k in ("g_r_diag", "g_lesser_upper", "sigma_lesser", "sigma_ret_lower", "residuals"):
+        assert rel(res[k], g[k]) < TOL, k
