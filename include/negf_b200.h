@@ -122,7 +122,11 @@ int negf_zinv_batched(int n, int batch, void* s, void* x, int* status, double* u
 size_t negf_sancho_workspace_bytes(int batch, int bs);
 int negf_obc_sancho_batched(int batch, int bs, const void* m, const void* n, const void* np,
                             double tol, int max_iter, void* x, int* status, int* iters,
-                            double* resid, void* workspace, size_t workspace_bytes, void* stream);
+                            double* resid, const int* select, void* workspace,
+                            size_t workspace_bytes, void* stream);
+/* select[batch] (device int, may be NULL = all): solve only problems with
+ * select[b] != 0; the others keep x and get status 0, iters 0 (the direct leg
+ * of the memoizer below). */
 
 /* sigma_lg_obc (obc.py:460-486), batched: Sigma^R = n x n',
  * Sigma^< = -f (Sigma^R - Sigma^R^dag), Sigma^> = (1-f)(Sigma^R - Sigma^R^dag)
@@ -142,8 +146,26 @@ int negf_sigma_lg_obc_batched(int batch, int bs, const void* x, const void* n, c
  * ported). bs <= 6000. */
 size_t negf_stein_workspace_bytes(int batch, int bs);
 int negf_stein_batched(int batch, int bs, const void* a, const void* q, void* w, double tol,
-                       int max_iter, const void* v0, int* status, int* iters, void* workspace,
-                       size_t workspace_bytes, void* stream);
+                       int max_iter, const void* v0, int* status, int* iters, const int* select,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* Runtime OBC memoizer, batched: the refresh leg of memoized_obc
+ * (obc.py:519-600; _memo_refresh :551-600). map 0 = surface fixed point
+ * x <- (m - n x n')^-1 (fixed_point_step, obc.py:138-141; n_kind must be 1),
+ * map 1 = Stein map w <- q + a w a^dag (scba.py:653-655) for n_kind kinds
+ * sharing a[s] (problem p = k*n_side + s, q[p]). x0[p]: cached block, used
+ * where has[p] != 0. Per problem: two trial updates give delta1, delta2,
+ * rho = delta2/delta1 and tail = rho/(1-rho); refresh only if
+ * delta2 rho^(n_fpi-2) tail < tol, stopping once last*tail < tol within
+ * n_fpi updates. Accepted iterates go to out[p] with used[p] = 1; every
+ * other problem (no cache, non-finite or singular update, rho >= 1, budget
+ * spent) gets need_direct[p] = 1 for the caller's direct solve (Sancho /
+ * Stein with select = need_direct). Synchronises `stream` once per update. */
+size_t negf_memo_workspace_bytes(int map, int n_side, int n_kind, int bs);
+int negf_memo_refresh_batched(int map, int n_side, int n_kind, int bs, const void* m, const void* n,
+                              const void* np, const void* a, const void* q, int n_fpi, double tol,
+                              const void* x0, const int* has, void* out, int* need_direct, int* used,
+                              void* workspace, size_t workspace_bytes, void* stream);
 
 /* Carrier-side contact closure of an assembled batch (scba.py:755-774):
  * for the left (corner 0) and right (corner n_b-1) leads, solve the surface
@@ -157,7 +179,18 @@ int negf_g_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
                      const void* m_lower, void* bl_diag, void* bg_diag, const double* f_left,
                      const double* f_right, double tol, int max_iter, void* sl_left,
                      void* sg_left, void* sl_right, void* sg_right, int* status, int* iters,
-                     double* resid, void* workspace, size_t workspace_bytes, void* stream);
+                     double* resid, void* memo_cache, int* memo_has, int* memo_used,
+                     long long memo_ld, int n_fpi, double memo_tol, void* workspace,
+                     size_t workspace_bytes, void* stream);
+/* Memoizer (optional; memo_cache NULL = direct Sancho for every problem, the
+ * reference with MemoizerOptions(enabled=False)): memo_cache holds the cached
+ * surface of side g (0 left, 1 right) and batch energy e at block
+ * g*memo_ld + e (memo_ld >= n_e: the caller's energies per side, pointer
+ * already offset to this batch); memo_has/memo_used [2][memo_ld] ints. Cached
+ * problems are refreshed (negf_memo_refresh_batched, n_fpi, memo_tol), the
+ * rest solved by Sancho; every result is written back to the cache
+ * (has = 1) and used[] = 1 marks memoized calls (the reference's
+ * cache.stats). */
 
 /* Carrier system assembly (scba.py:670-727) for n_e energies:
  *   M_ii = (E + i eta) I - H_ii - SR_ii,  M_{i,i+-1} = -H - SR,
@@ -260,8 +293,14 @@ int negf_w_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
                      const void* m_lower, void* bl_diag, const void* bl_upper, void* bg_diag,
                      const void* bg_upper, double surface_tol, int max_sweeps, double stein_tol,
                      int stein_max_iter, const void* v0, int* status, int* iters,
-                     int* stein_status, int* stein_iters, void* workspace,
+                     int* stein_status, int* stein_iters, void* memo_r_cache, int* memo_r_has,
+                     int* memo_r_used, void* memo_lg_cache, int* memo_lg_has, int* memo_lg_used,
+                     long long memo_ld, int n_fpi_r, int n_fpi_lg, double memo_tol, void* workspace,
                      size_t workspace_bytes, void* stream);
+/* Memoizer (optional, as for negf_g_obc_apply): memo_r_* cache the W
+ * surfaces (key (W, side, e, R), [2 sides][memo_ld]), memo_lg_* the Stein
+ * solutions (key (W, side, e, kind), [2 kinds][2 sides][memo_ld]); budgets
+ * n_fpi_r / n_fpi_lg (SurfaceCache.n_fpi, obc.py:504-512). */
 
 /* ---- (6) mixing and residual (scba.py:478-481, 1155-1167) ----------------
  * s_k <- (1 - alpha) s_k + alpha r_k elementwise over n complex values, for

@@ -304,6 +304,89 @@ def stein_direct(a, q):
         return np.linalg.solve(lhs, q.ravel(order="F")).reshape((n, n), order="F")
 
 
+# -- runtime memoization (obc.py:490-608) --------------------------------------
+
+
+class SurfaceCache:
+    """obc.py:498-515: cached surface blocks keyed by (subsystem, side,
+    energy index, kind) plus direct/memoized call counters."""
+
+    def __init__(self, n_fpi_retarded: int = 20, n_fpi_lg: int = 10) -> None:
+        self.n_fpi_retarded, self.n_fpi_lg = n_fpi_retarded, n_fpi_lg
+        self.entries: dict = {}
+        self.stats = {"direct_calls": 0, "memoized_calls": 0}
+
+    def n_fpi(self, kind: str) -> int:
+        return self.n_fpi_retarded if kind == "R" else self.n_fpi_lg
+
+
+def fixed_point_step(m, n, n_prime, x):
+    """obc.py:138-141: x <- (m - n x n')^-1 (raises OracleSingular)."""
+    inv, _ = lu_inverse(m - (n @ x) @ n_prime)
+    return inv
+
+
+def _memo_direct(key, direct, cache):
+    """obc.py:603-608."""
+    x = direct()
+    cache.entries[key] = np.asarray(x)
+    cache.stats["direct_calls"] += 1
+    return x
+
+
+def _memo_accept(key, x, cache):
+    cache.entries[key] = x
+    cache.stats["memoized_calls"] += 1
+    return x
+
+
+def memoized_obc(key, direct, iterative, cache: SurfaceCache, n_fpi: int, tol: float):
+    """obc.py:519-600: two trial fixed-point updates from the cached block give
+    the update size and a contraction estimate rho; refresh with the budget
+    n_fpi only when the budgeted tail delta2 rho^(n_fpi-2) rho/(1-rho) < tol,
+    stop early once the tail bound is below tol, else solve directly. Any
+    non-finite iterate or singular update falls back to the direct solver."""
+    x0 = cache.entries.get(key)
+    if x0 is None:
+        return _memo_direct(key, direct, cache)
+    try:
+        with np.errstate(over="ignore", invalid="ignore"):
+            x1 = iterative(x0)
+            d1, s1 = np.linalg.norm(x1 - x0), np.linalg.norm(x1)
+            if not np.isfinite(d1) or s1 == 0 or not np.all(np.isfinite(x1)):
+                return _memo_direct(key, direct, cache)
+            delta1 = d1 / s1
+            if delta1 == 0.0:
+                return _memo_accept(key, x1, cache)
+            x2 = iterative(x1)
+            d2, s2 = np.linalg.norm(x2 - x1), np.linalg.norm(x2)
+            if not np.isfinite(d2) or s2 == 0 or not np.all(np.isfinite(x2)):
+                return _memo_direct(key, direct, cache)
+            delta2 = d2 / s2
+            if delta2 <= 1e-14:
+                return _memo_accept(key, x2, cache)
+            rho = delta2 / delta1
+            if rho >= 1.0:
+                return _memo_direct(key, direct, cache)
+            tail = rho / (1.0 - rho)
+            if delta2 * rho ** max(0, n_fpi - 2) * tail >= tol:
+                return _memo_direct(key, direct, cache)
+            x, last = x2, delta2
+            for _ in range(max(0, n_fpi - 2)):
+                if last * tail < tol:
+                    break
+                x_new = iterative(x)
+                if not np.all(np.isfinite(x_new)):
+                    return _memo_direct(key, direct, cache)
+                last = np.linalg.norm(x_new - x) / max(np.linalg.norm(x_new), 1e-300)
+                x = x_new
+            if last * tail >= tol:
+                return _memo_direct(key, direct, cache)
+            return _memo_accept(key, x, cache)
+    except (OracleSingular, OracleConvergence, ValueError, np.linalg.LinAlgError):
+        return _memo_direct(key, direct, cache)
+
+
 # -- carrier system (scba.py:670-775) ------------------------------------------
 
 
@@ -328,10 +411,12 @@ def assemble_g(energies, eta, h, f_bath, sr=None, sl=None, sg=None):
     return (md, mu, ml), (np.ascontiguousarray(bld), blu), (np.ascontiguousarray(bgd), bgu)
 
 
-def g_closure(m, bl, bg, energies, mu_left, mu_right, kT, tol):
+def g_closure(m, bl, bg, energies, mu_left, mu_right, kT, tol, cache: SurfaceCache | None = None,
+              tol_memo: float = 0.0):
     """scba.py:755-774: per side, Sancho on the contact cell (_lead_cell,
     scba.py:558-574), sigma_lg_obc, corner updates. In place; returns the
-    boundary lesser/greater self-energies {side: (sl, sg)} (n_e, bs, bs)."""
+    boundary lesser/greater self-energies {side: (sl, sg)} (n_e, bs, bs).
+    With ``cache`` the surface goes through memoized_obc (scba.py:577-614)."""
     md, mu, ml = m
     n_b = md.shape[1]
     out = {}
@@ -343,7 +428,7 @@ def g_closure(m, bl, bg, energies, mu_left, mu_right, kT, tol):
                 cell = (md[e, 0], ml[e, 0], mu[e, 0])
             else:
                 cell = (md[e, n_b - 1], mu[e, n_b - 2], ml[e, n_b - 2])
-            x, _, _ = sancho_rubio(*cell, tol=tol)
+            x = _surface(cell, "G", side, e, tol, cache, tol_memo)
             sr, s_l, s_g = sigma_lg_obc(x, mu_c, kT, E, cell[1], cell[2])
             md[e, c] = md[e, c] - sr
             bl[0][e, c] = bl[0][e, c] + s_l
@@ -352,6 +437,15 @@ def g_closure(m, bl, bg, energies, mu_left, mu_right, kT, tol):
             sgs.append(s_g)
         out[side] = (np.stack(sls), np.stack(sgs))
     return out
+
+
+def _surface(cell, subsystem, side, e, tol, cache, tol_memo):
+    """_retarded_surface (scba.py:577-614) with the Sancho direct solver."""
+    direct = lambda: sancho_rubio(*cell, tol=tol)[0]
+    if cache is None:
+        return direct()
+    return memoized_obc((subsystem, side, e, "R"), direct, lambda x: fixed_point_step(*cell, x), cache,
+                        cache.n_fpi("R"), tol_memo)
 
 
 def ballistic(h, energies, eta, mu_left, mu_right, kT, tol=1e-8):
@@ -593,8 +687,10 @@ def w_system(v, pr, pl, pg):
     return (md, mu, ml), srcs
 
 
-def w_closure(m, srcs, surface_tol):
-    """scba.py:839-858 + _lead_lg_boundary (:617-664), W surface by Sancho."""
+def w_closure(m, srcs, surface_tol, cache: SurfaceCache | None = None, tol_memo: float = 0.0):
+    """scba.py:839-858 + _lead_lg_boundary (:617-664), W surface by Sancho;
+    with ``cache`` both the surface and the Stein solve are memoized
+    (scba.py:647-658)."""
     md, mu, ml = m
     ne, n = md.shape[:2]
     cells = {}
@@ -605,7 +701,7 @@ def w_closure(m, srcs, surface_tol):
                 cell = (md[e, 0], ml[e, 0], mu[e, 0])
             else:
                 cell = (md[e, n - 1], mu[e, n - 2], ml[e, n - 2])
-            x, _, _ = sancho_rubio(*cell, tol=surface_tol)
+            x = _surface(cell, "W", side, e, surface_tol, cache, tol_memo)
             xs.append((cell, x))
         cells[side] = xs
     for side in ("left", "right"):
@@ -620,7 +716,11 @@ def w_closure(m, srcs, surface_tol):
                 q0 = bd[e, j] - (y - _h(y))
                 a = x @ n_dn
                 q = (x @ q0) @ _h(x)
-                wl = stein_direct(a, q)
+                if cache is None:
+                    wl = stein_direct(a, q)
+                else:
+                    wl = memoized_obc(("W", side, e, kind), lambda: stein_direct(a, q),
+                                      lambda w: q + (a @ w) @ _h(a), cache, cache.n_fpi(kind), tol_memo)
                 t = n_dn @ x
                 bd[e, j] = bd[e, j] + (-(t @ b_in) - (b_out @ _h(x)) @ _h(n_dn) + (n_dn @ wl) @ _h(n_dn))
     for side in ("left", "right"):
@@ -634,10 +734,12 @@ def w_closure(m, srcs, surface_tol):
 
 
 def scba(h, v, energies, eta, mu_left, mu_right, kT, max_iter=1, tol=1e-12, mixing=0.3,
-         surface_tol=1e-8):
-    """scba_run(retarded_method='sancho', memoizer off, W surface by Sancho).
-    Returns the ScbaResult arrays (G at the start of the last iteration, mixed
-    Sigma after it) plus 'residuals'."""
+         surface_tol=1e-8, memoizer: tuple[int, int] | None = None):
+    """scba_run(retarded_method='sancho', W surface by Sancho). ``memoizer``
+    = (n_fpi_retarded, n_fpi_lg) enables the OBC memoizer with tol/10
+    (scba.py:906-911); None = memoizer off. Returns the ScbaResult arrays (G
+    at the start of the last iteration, mixed Sigma after it), 'residuals'
+    and 'cache_stats_by_iteration'."""
     energies = np.asarray(energies, dtype=float)
     ne = len(energies)
     de = (energies[-1] - energies[0]) / (ne - 1)
@@ -649,12 +751,15 @@ def scba(h, v, energies, eta, mu_left, mu_right, kT, max_iter=1, tol=1e-12, mixi
     sig = {k: np.zeros((n_ent, ne), complex) for k in ("lesser", "greater", "ret_upper", "ret_lower")}
     f_bath = fermi(energies, 0.5 * (mu_left + mu_right), kT)
     residuals = []
+    cache = SurfaceCache(*memoizer) if memoizer is not None else None
+    tol_memo = tol / 10.0
+    stats_by_it = []
     for it in range(max_iter):
         sr = scatter_retarded(sig["ret_upper"], sig["ret_lower"], n_b, bs)
         sl = scatter_lg(sig["lesser"], n_b, bs)
         sg = scatter_lg(sig["greater"], n_b, bs)
         m, bl, bg = assemble_g(energies, eta, h, f_bath, sr=sr, sl=sl, sg=sg)
-        obc = g_closure(m, bl, bg, energies, mu_left, mu_right, kT, surface_tol)
+        obc = g_closure(m, bl, bg, energies, mu_left, mu_right, kT, surface_tol, cache, tol_memo)
         sol = rgf_selected(*m, {"<": bl, ">": bg}, symmetrize=True)
         result = {
             "g_r_diag": sol["xr_diag"], "g_r_upper": sol["xr_upper"], "g_r_lower": sol["xr_lower"],
@@ -668,7 +773,7 @@ def scba(h, v, energies, eta, mu_left, mu_right, kT, max_iter=1, tol=1e-12, mixi
         pl, pg, pru, prl = polarization(gl, gg, diag_mask, de)
         pr = scatter_retarded(pru, prl, n_b, bs)
         mw, srcs = w_system(v, pr, scatter_lg(pl, n_b, bs), scatter_lg(pg, n_b, bs))
-        w_closure(mw, srcs, surface_tol)
+        w_closure(mw, srcs, surface_tol, cache, tol_memo)
         wsol = rgf_selected(*mw, srcs, symmetrize=True)
         wl = gather_entries(wsol["x<_diag"], wsol["x<_upper"])
         wg = gather_entries(wsol["x>_diag"], wsol["x>_upper"])
@@ -681,8 +786,11 @@ def scba(h, v, energies, eta, mu_left, mu_right, kT, max_iter=1, tol=1e-12, mixi
         scale = max(max(float(np.max(np.abs(tr_old[k]))) for k in tr_old),
                     max(float(np.max(np.abs(tr_new[k]))) for k in tr_new))
         residuals.append(delta / (scale + 1e-300))
+        if cache is not None:
+            stats_by_it.append(dict(cache.stats))
         if residuals[-1] < tol:
             break
     result.update({"sigma_" + k: v_ for k, v_ in sig.items()})
     result["residuals"] = np.asarray(residuals)
+    result["cache_stats_by_iteration"] = stats_by_it
     return result

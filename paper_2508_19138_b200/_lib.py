@@ -43,15 +43,18 @@ _SIGNATURES: dict[str, tuple] = {
     "negf_zinv_workspace_bytes": (_sz, [_i, _i]),
     "negf_zinv_batched": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "negf_sancho_workspace_bytes": (_sz, [_i, _i]),
-    "negf_obc_sancho_batched": (_i, [_i, _i, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "negf_obc_sancho_batched": (_i, [_i, _i, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "negf_sigma_lg_obc_workspace_bytes": (_sz, [_i, _i]),
     "negf_sigma_lg_obc_batched": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "negf_stein_workspace_bytes": (_sz, [_i, _i]),
-    "negf_stein_batched": (_i, [_i, _i, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "negf_stein_batched": (_i, [_i, _i, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "negf_memo_workspace_bytes": (_sz, [_i, _i, _i, _i]),
+    "negf_memo_refresh_batched": (_i, [_i, _i, _i, _i] + [_vp] * 5 + [_i, _d] + [_vp] * 6 + [_sz, _vp]),
     "negf_g_obc_workspace_bytes": (_sz, [_i, _i]),
     "negf_g_obc_apply": (
         _i,
-        [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp],
+        [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+         _vp, _vp, _vp, _ll, _i, _d, _vp, _sz, _vp],
     ),
     "negf_g_assemble": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _d] + [_vp] * 7 + [_vp] * 7 + [_vp]),
     "negf_observables": (_i, [_i, _i, _i] + [_vp] * 14),
@@ -66,7 +69,8 @@ _SIGNATURES: dict[str, tuple] = {
     "negf_w_assemble_workspace_bytes": (_sz, [_i, _i, _i]),
     "negf_w_assemble": (_i, [_i, _i, _i] + [_vp] * 18 + [_sz, _vp]),
     "negf_w_obc_workspace_bytes": (_sz, [_i, _i]),
-    "negf_w_obc_apply": (_i, [_i, _i, _i] + [_vp] * 7 + [_d, _i, _d, _i] + [_vp] * 6 + [_sz, _vp]),
+    "negf_w_obc_apply": (_i, [_i, _i, _i] + [_vp] * 7 + [_d, _i, _d, _i] + [_vp] * 5 + [_vp] * 6
+                         + [_ll, _i, _i, _d, _vp, _sz, _vp]),
     "negf_mix": (_i, [_ll, _d] + [_vp] * 9),
     "negf_diag_traces": (_i, [_vp, _ll, _i, _vp, _i, _i, _vp, _vp]),
     "negf_prof_enable": (None, [_i]),

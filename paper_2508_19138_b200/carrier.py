@@ -122,10 +122,13 @@ class CarrierSolver:
 
     # -- solve -------------------------------------------------------------
     def solve(self, energies, sigma: dict | None = None, n_e: int | None = None,
-              check: bool = True, energies_dev: torch.Tensor | None = None) -> dict[str, torch.Tensor]:
+              check: bool = True, energies_dev: torch.Tensor | None = None,
+              memo: tuple | None = None) -> dict[str, torch.Tensor]:
         """Solve the carrier system at ``energies`` (host array). ``sigma`` holds
         scattering self-energy blocks, energy-major: keys sr_diag/sr_upper/
-        sr_lower, sl_diag/sl_upper, sg_diag/sg_upper (any subset)."""
+        sr_lower, sl_diag/sl_upper, sg_diag/sg_upper (any subset). ``memo`` =
+        (SurfaceCache, ld, e0, tol_memo) routes the contact surfaces through
+        the OBC memoizer (scba.py:577-614), cache columns e0:e0+n_e of ld."""
         lib, p = self.lib, _lib.ptr
         energies = np.asarray(energies, dtype=np.float64)
         ne = len(energies)
@@ -150,12 +153,22 @@ class CarrierSolver:
         _lib.check(rc, "negf_g_assemble")
         nbytes = lib.negf_g_obc_workspace_bytes(ne, self.bs)
         ws = _lib.workspace(nbytes, self.dev)
+        mc = mh = mu_ = None
+        ld, n_fpi, tol_memo = 0, 20, 0.0
+        if memo is not None:
+            cache, ld, e0, tol_memo = memo
+            xs, hs, us = cache.slot(("G", "R"), 2, ld, self.bs, self.dev)
+            mc, mh, mu_ = xs[0, e0], hs[0, e0:], us[0, e0:]
+            n_fpi = cache.n_fpi("R")
         rc = lib.negf_g_obc_apply(
             ne, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]), p(b["bl_diag"]),
             p(b["bg_diag"]), p(b["f_left"]), p(b["f_right"]), self.surface_tol, self.max_sweeps,
             p(b["sl_left"]), p(b["sg_left"]), p(b["sl_right"]), p(b["sg_right"]),
-            p(b["obc_status"]), p(b["obc_iters"]), p(b["obc_resid"]), p(ws), nbytes, st)
+            p(b["obc_status"]), p(b["obc_iters"]), p(b["obc_resid"]), p(mc), p(mh), p(mu_), ld, n_fpi,
+            tol_memo, p(ws), nbytes, st)
         _lib.check(rc, "negf_g_obc_apply")
+        if memo is not None:
+            cache.record(us, e0, ne)
         if check:
             raise_on_obc_status(b["obc_status"].cpu().numpy(), b["obc_iters"].cpu().numpy(),
                                 b["obc_resid"].cpu().numpy(), self.max_sweeps, self.surface_tol, "G contact")

@@ -1,5 +1,6 @@
 // extern "C" entry points declared in include/negf_b200.h.
 #include "../../include/negf_b200.h"
+#include "memo.cuh"
 #include "obc.cuh"
 #include "rgf.cuh"
 #include "zgemm.cuh"
@@ -121,12 +122,29 @@ size_t negf_sancho_workspace_bytes(int batch, int bs) { return sancho_workspace_
 
 int negf_obc_sancho_batched(int batch, int bs, const void* m, const void* n, const void* np,
                             double tol, int max_iter, void* x, int* status, int* iters,
-                            double* resid, void* workspace, size_t workspace_bytes, void* stream) {
+                            double* resid, const int* select, void* workspace,
+                            size_t workspace_bytes, void* stream) {
   if (batch < 0 || bs < 1 || !m || !n || !np || !x || !status || !iters) return -1;
   if (!(tol > 0.0) || max_iter < 1) return -1;
   return sancho_batched((const z_t*)m, (const z_t*)n, (const z_t*)np, batch, bs, tol, max_iter,
                         (z_t*)x, status, iters, resid, workspace, workspace_bytes,
-                        (cudaStream_t)stream);
+                        (cudaStream_t)stream, select);
+}
+
+size_t negf_memo_workspace_bytes(int map, int n_side, int n_kind, int bs) {
+  return memo_workspace_bytes(map, n_side, n_kind, bs);
+}
+
+int negf_memo_refresh_batched(int map, int n_side, int n_kind, int bs, const void* m, const void* n,
+                              const void* np, const void* a, const void* q, int n_fpi, double tol,
+                              const void* x0, const int* has, void* out, int* need_direct, int* used,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  if (n_side < 0 || n_kind < 1 || bs < 1 || n_fpi < 2 || !x0 || !has || !out || !need_direct || !used) return -1;
+  if (map == MEMO_SURFACE && (!m || !n || !np || n_kind != 1)) return -1;
+  if (map == MEMO_STEIN && (!a || !q)) return -1;
+  return memo_refresh(map, n_side, n_kind, bs, (const z_t*)m, (const z_t*)n, (const z_t*)np, (const z_t*)a,
+                      (const z_t*)q, n_fpi, tol, (const z_t*)x0, has, (z_t*)out, need_direct, used, workspace,
+                      workspace_bytes, (cudaStream_t)stream);
 }
 
 size_t negf_sigma_lg_obc_workspace_bytes(int batch, int bs) {
@@ -149,10 +167,13 @@ int negf_g_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
                      const void* m_lower, void* bl_diag, void* bg_diag, const double* f_left,
                      const double* f_right, double tol, int max_iter, void* sl_left,
                      void* sg_left, void* sl_right, void* sg_right, int* status, int* iters,
-                     double* resid, void* workspace, size_t workspace_bytes, void* stream) {
+                     double* resid, void* memo_cache, int* memo_has, int* memo_used,
+                     long long memo_ld, int n_fpi, double memo_tol, void* workspace,
+                     size_t workspace_bytes, void* stream) {
   if (n_e < 0 || n_b < 2 || bs < 1 || !m_diag || !m_upper || !m_lower || !f_left || !f_right)
     return -1;
   if (!status || !iters) return -1;
+  if (memo_cache && (!memo_has || memo_ld < n_e || n_fpi < 2)) return -1;
   GObcArgs a;
   a.n_e = n_e; a.n_b = n_b; a.bs = bs;
   a.m_diag = (z_t*)m_diag; a.m_upper = (const z_t*)m_upper; a.m_lower = (const z_t*)m_lower;
@@ -161,6 +182,8 @@ int negf_g_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
   a.sl_left = (z_t*)sl_left; a.sg_left = (z_t*)sg_left;
   a.sl_right = (z_t*)sl_right; a.sg_right = (z_t*)sg_right;
   a.status = status; a.iters = iters; a.resid = resid;
+  a.memo_cache = (z_t*)memo_cache; a.memo_has = memo_has; a.memo_used = memo_used;
+  a.memo_ld = memo_ld; a.n_fpi = n_fpi; a.memo_tol = memo_tol;
   return g_obc_apply(a, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 

@@ -17,6 +17,7 @@
 // so every problem stops at exactly the sweep the reference would.
 #include "ew.cuh"
 #include "prof.cuh"
+#include "memo.cuh"
 #include "obc.cuh"
 #include "zgemm.cuh"
 #include "zinv.cuh"
@@ -51,9 +52,13 @@ __device__ double fro(const z_t* x, long long n2, double* red) {
 }
 
 __global__ void sancho_init_kernel(const z_t* n, const z_t* np, int bs, double* scale, int* active,
-                                   int* status, int* iters) {
+                                   int* status, int* iters, const int* select) {
   __shared__ double red[32];
   const int b = blockIdx.x;
+  if (select && !select[b]) {
+    if (threadIdx.x == 0) { active[b] = 0; scale[b] = 1.0; status[b] = OBC_OK; iters[b] = 0; }
+    return;
+  }
   const long long n2 = (long long)bs * bs;
   double a = fro(n + b * n2, n2, red), c = fro(np + b * n2, n2, red);
   if (threadIdx.x == 0) {
@@ -87,9 +92,10 @@ __global__ void sancho_check_kernel(const z_t* alpha, const z_t* beta, int bs, d
 }
 
 __global__ void sancho_finish_kernel(const z_t* x, const z_t* y, int bs, double thr, int* active,
-                                     int* inv_status, int* status, double* resid) {
+                                     int* inv_status, int* status, double* resid, const int* select) {
   __shared__ double red[32];
   const int b = blockIdx.x;
+  if (select && !select[b]) return;
   const long long n2 = (long long)bs * bs;
   const z_t* xb = x + b * n2;
   const z_t* yb = y + b * n2;
@@ -208,6 +214,11 @@ __global__ void g_assemble_kernel(GAssembleArgs a) {
   }
 }
 
+__global__ void count_active_kernel(const int* active, int n, int* n_act) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < n && active[b]) atomicAdd(n_act, 1);
+}
+
 #define RC(x) do { int _rc = (x); if (_rc) return _rc; } while (0)
 
 }  // namespace
@@ -219,7 +230,7 @@ size_t sancho_workspace_bytes(int batch, int bs) {
 
 int sancho_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs, double tol,
                    int max_iter, z_t* x, int* status, int* iters, double* resid, void* ws,
-                   size_t ws_bytes, cudaStream_t st) {
+                   size_t ws_bytes, cudaStream_t st, const int* select) {
   if (batch <= 0) return 0;
   if (ws_bytes < sancho_workspace_bytes(batch, bs)) return -4;
   const long long n2 = (long long)bs * bs;
@@ -250,7 +261,7 @@ int sancho_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs,
   NEGF_CUDA_CHECK(cudaMemsetAsync(inv_st, 0, sizeof(int) * batch, st));
   {
     ProfScope ps_sancho_init_kernel(PROF_OTHER, (cudaStream_t)(st));
-    sancho_init_kernel<<<batch, 256, 0, st>>>(n, np, bs, scale, active, status, iters);
+    sancho_init_kernel<<<batch, 256, 0, st>>>(n, np, bs, scale, active, status, iters, select);
     NEGF_LAUNCHED();
   }
   InvAux aux;
@@ -269,7 +280,17 @@ int sancho_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs,
     return d;
   };
   int h_active = batch;
-  for (int it = 1; it <= max_iter; ++it) {
+  if (select) {  // problems outside the selection never start
+    NEGF_CUDA_CHECK(cudaMemsetAsync(n_act, 0, sizeof(int), st));
+    {
+      ProfScope ps_count(PROF_OTHER, st);
+      count_active_kernel<<<(batch + 127) / 128, 128, 0, st>>>(active, batch, n_act);
+      NEGF_LAUNCHED();
+    }
+    NEGF_CUDA_CHECK(cudaMemcpyAsync(&h_active, n_act, sizeof(int), cudaMemcpyDeviceToHost, st));
+    NEGF_CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+  for (int it = 1; h_active > 0 && it <= max_iter; ++it) {
     NEGF_CUDA_CHECK(cudaMemcpyAsync(tb, b, bytes, cudaMemcpyDeviceToDevice, st));
     RC(zinv_batched(tb, n2, bs, g, n2, bs, bs, batch, aux, inv_ws, inv_bytes, st));
     ZGemmGroup G1;
@@ -302,23 +323,23 @@ int sancho_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs,
   }
   // x = s^-1 for every problem (s is consumed)
   InvAux aux2 = aux;
-  aux2.active = nullptr;
+  aux2.active = select;
   aux2.status = inv_st;
   RC(zinv_batched(s, n2, bs, x, n2, bs, bs, batch, aux2, inv_ws, inv_bytes, st));
   // residual: y = (m - n x n')^-1
   ZGemmGroup G3;
   G3.n = 1;
   G3.d[0] = desc(n, x, ag, 1.0, nullptr, 0.0);
-  G3.d[0].active = nullptr;
+  G3.d[0].active = select;
   RC(zgemm_group_launch(G3, st));
   G3.d[0] = desc(ag, np, tb, -1.0, m, 1.0);
-  G3.d[0].active = nullptr;
+  G3.d[0].active = select;
   RC(zgemm_group_launch(G3, st));
   RC(zinv_batched(tb, n2, bs, g, n2, bs, bs, batch, aux2, inv_ws, inv_bytes, st));
   const double thr = 10.0 * (tol > 1e-14 ? tol : 1e-14);
   {
     ProfScope ps_sancho_finish_kernel(PROF_OTHER, (cudaStream_t)(st));
-    sancho_finish_kernel<<<batch, 256, 0, st>>>(x, g, bs, thr, active, inv_st, status, resid);
+    sancho_finish_kernel<<<batch, 256, 0, st>>>(x, g, bs, thr, active, inv_st, status, resid, select);
     NEGF_LAUNCHED();
   }
   return 0;
@@ -326,7 +347,9 @@ int sancho_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs,
 
 size_t g_obc_workspace_bytes(int n_e, int bs) {
   size_t blk = a256(sizeof(z_t) * (size_t)2 * n_e * bs * bs);
-  return 6 * blk + sancho_workspace_bytes(2 * n_e, bs);
+  size_t solver = sancho_workspace_bytes(2 * n_e, bs);
+  size_t memo = memo_workspace_bytes(MEMO_SURFACE, 2 * n_e, 1, bs);
+  return 6 * blk + (solver > memo ? solver : memo) + 3 * a256(sizeof(int) * 2 * (size_t)n_e + 64);
 }
 
 int g_obc_apply(const GObcArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
@@ -344,8 +367,11 @@ int g_obc_apply(const GObcArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
   z_t* xr = (z_t*)w; w += blk;
   z_t* t1 = (z_t*)w; w += blk;
   z_t* sig = (z_t*)w; w += blk;
+  int* has_buf = (int*)w; w += a256(sizeof(int) * 2 * (size_t)ne + 64);
+  int* need = (int*)w; w += a256(sizeof(int) * 2 * (size_t)ne + 64);
+  int* used_buf = (int*)w; w += a256(sizeof(int) * 2 * (size_t)ne + 64);
   void* sws = w;
-  size_t sbytes = ws_bytes - 6 * blk;
+  size_t sbytes = ws_bytes - (size_t)(w - reinterpret_cast<char*>(ws));
   // gather contact cells: side 0 = left (corner 0), side 1 = right (corner n_b-1)
   auto gather = [&](z_t* dst, const z_t* src, long long stride) -> int {
     NEGF_CUDA_CHECK(cudaMemcpy2DAsync(dst, n2 * sizeof(z_t), src, stride * sizeof(z_t), n2 * sizeof(z_t),
@@ -359,8 +385,18 @@ int g_obc_apply(const GObcArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
   RC(gather(cn + hn, a.m_upper + (nb - 2) * n2, so));    // n  = M_{N-2,N-1}
   RC(gather(cnp, a.m_upper, so));                        // n' = M_01
   RC(gather(cnp + hn, a.m_lower + (nb - 2) * n2, so));   // n' = M_{N-1,N-2}
-  RC(sancho_batched(cm, cn, cnp, 2 * ne, bs, a.tol, a.max_iter, xr, a.status, a.iters, a.resid, sws,
-                    sbytes, st));
+  if (a.memo_cache) {
+    // refresh cached surfaces first (staged through t1); Sancho only where rejected
+    RC(memo_gather(a.memo_cache, a.memo_ld, a.memo_has, a.memo_ld, 2, ne, bs, t1, has_buf, st));
+    RC(memo_refresh(MEMO_SURFACE, 2 * ne, 1, bs, cm, cn, cnp, nullptr, nullptr, a.n_fpi, a.memo_tol, t1,
+                    has_buf, xr, need, used_buf, sws, sbytes, st));
+    RC(sancho_batched(cm, cn, cnp, 2 * ne, bs, a.tol, a.max_iter, xr, a.status, a.iters, a.resid, sws,
+                      sbytes, st, need));
+    RC(memo_store(xr, used_buf, 2, ne, bs, a.memo_cache, a.memo_ld, a.memo_has, a.memo_used, a.memo_ld, st));
+  } else {
+    RC(sancho_batched(cm, cn, cnp, 2 * ne, bs, a.tol, a.max_iter, xr, a.status, a.iters, a.resid, sws,
+                      sbytes, st));
+  }
   // Sigma^R_obc = n x n'
   ZGemmDesc d = zdesc_default();
   d.M = bs; d.N = bs; d.batch = 2 * ne;

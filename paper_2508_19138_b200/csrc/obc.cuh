@@ -18,7 +18,9 @@ enum ObcStatus : int {
 size_t sancho_workspace_bytes(int batch, int bs);
 int sancho_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs, double tol,
                    int max_iter, z_t* x, int* status, int* iters, double* resid, void* ws,
-                   size_t ws_bytes, cudaStream_t st);
+                   size_t ws_bytes, cudaStream_t st, const int* select = nullptr);
+// (select, optional: only problems with select[b] != 0 are solved; x, status,
+// iters and resid of the others are left as they are, status 0, iters 0.)
 
 // G-side closure of one batch: per side, read the contact cell from the
 // assembled M (energy-major tridiagonal), solve the surface problem, and
@@ -42,6 +44,15 @@ struct GObcArgs {
   int* status;  // [2][n_e]
   int* iters;   // [2][n_e]
   double* resid;  // [2][n_e]
+  // OBC memoizer (obc.py:519-608), optional (memo_cache null: direct Sancho
+  // everywhere). memo_cache: side g's block e at memo_cache + (g*memo_ld+e)*bs^2;
+  // memo_has / memo_used: [2][memo_ld] ints (in/out; out).
+  z_t* memo_cache = nullptr;
+  int* memo_has = nullptr;
+  int* memo_used = nullptr;
+  long long memo_ld = 0;
+  int n_fpi = 20;
+  double memo_tol = 0.0;
 };
 size_t g_obc_workspace_bytes(int n_e, int bs);
 int g_obc_apply(const GObcArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);

@@ -16,9 +16,12 @@
 // The W retarded surface block is computed by Sancho-Rubio decimation
 // (the reference hard-codes Beyn here, scba.py:844; on the reference's
 // weak-V inputs both agree to ~1e-16).
+#include <algorithm>
+
 #include "../../include/negf_b200.h"
 #include "ew.cuh"
 #include "prof.cuh"
+#include "memo.cuh"
 #include "obc.cuh"
 #include "zgemm.cuh"
 
@@ -256,12 +259,25 @@ __global__ void stein_step_kernel(z_t* w, const z_t* upd, long long n2, double t
 // default_rng(5), generated by the caller); rho >= 1 -> OBC_SPECTRAL.
 // One CTA per problem, one warp per row of a (coalesced), v in smem.
 __global__ void stein_init_kernel(const z_t* a, long long n2, int bs, const z_t* v0, int n_side,
-                                  int n_kind, int* active, int* iters, int* status) {
+                                  int n_kind, int* active, int* iters, int* status, const int* select) {
   extern __shared__ __align__(16) z_t vsh[];  // v (bs) then w (bs)
   __shared__ double red[32];
   __shared__ double s_rho;
   __shared__ int s_zero;
   const int s = blockIdx.x;  // (side, e) problem
+  if (select) {  // memoized problems (select 0) keep their value and never start
+    int any = 0;
+    for (int k = 0; k < n_kind; ++k) any |= select[k * n_side + s];
+    if (!any) {
+      if (threadIdx.x == 0)
+        for (int k = 0; k < n_kind; ++k) {
+          active[k * n_side + s] = 0;
+          iters[k * n_side + s] = 0;
+          status[k * n_side + s] = OBC_OK;
+        }
+      return;
+    }
+  }
   const z_t* A = a + s * n2;
   z_t* v = vsh;
   z_t* w = vsh + bs;
@@ -303,9 +319,10 @@ __global__ void stein_init_kernel(const z_t* a, long long n2, int bs, const z_t*
     const bool ok = rho < 1.0;
     for (int k = 0; k < n_kind; ++k) {
       const int p = k * n_side + s;
-      active[p] = ok ? 1 : 0;
+      const bool sel = !select || select[p];
+      active[p] = ok && sel ? 1 : 0;
       iters[p] = 0;
-      status[p] = ok ? OBC_OK : OBC_SPECTRAL;
+      status[p] = ok || !sel ? OBC_OK : OBC_SPECTRAL;
     }
   }
 }
@@ -335,7 +352,7 @@ size_t stein_workspace_bytes(int n_side, int n_kind, int bs) {
 
 int stein_batched(const z_t* a, const z_t* q, z_t* w, int n_side, int n_kind, int bs, double tol,
                   int max_iter, int* status, int* iters, const z_t* v0, void* ws, size_t ws_bytes,
-                  cudaStream_t st) {
+                  cudaStream_t st, const int* select = nullptr) {
   if (ws_bytes < stein_workspace_bytes(n_side, n_kind, bs)) return -4;
   const long long n2 = (long long)bs * bs;
   const size_t blk = sizeof(z_t) * (size_t)n2;
@@ -348,11 +365,15 @@ int stein_batched(const z_t* a, const z_t* q, z_t* w, int n_side, int n_kind, in
   int* side_active = (int*)p; p += a256(sizeof(int) * (size_t)n_side + 64);
   int* n_act = (int*)p;
   NEGF_CUDA_CHECK(cudaMemcpyAsync(ak, a, n_side * blk, cudaMemcpyDeviceToDevice, st));
-  NEGF_CUDA_CHECK(cudaMemcpyAsync(w, q, (size_t)n_kind * n_side * blk, cudaMemcpyDeviceToDevice, st));
+  if (select) {
+    RC(copy_selected(w, q, n2, select, n_kind * n_side, st));
+  } else {
+    NEGF_CUDA_CHECK(cudaMemcpyAsync(w, q, (size_t)n_kind * n_side * blk, cudaMemcpyDeviceToDevice, st));
+  }
   {
     ProfScope ps_stein_init_kernel(PROF_OTHER, (cudaStream_t)(st));
     stein_init_kernel<<<n_side, 256, 2 * (size_t)bs * sizeof(z_t), st>>>(a, n2, bs, v0, n_side, n_kind,
-                                                                          active, iters, status);
+                                                                          active, iters, status, select);
     NEGF_LAUNCHED();
   }
   for (int it = 1; it <= max_iter; ++it) {
@@ -414,21 +435,23 @@ extern "C" {
 size_t negf_w_obc_workspace_bytes(int n_e, int bs) {
   const size_t blk = sizeof(z_t) * (size_t)bs * bs;
   const int ns = 2 * n_e, np = 4 * n_e;
-  return 7 * a256(ns * blk) + 7 * a256(np * blk) + sancho_workspace_bytes(ns, bs) +
-         stein_workspace_bytes(ns, 2, bs) + 4 * a256(sizeof(int) * np + 64);
+  const size_t sancho = sancho_workspace_bytes(ns, bs), memo_r = memo_workspace_bytes(MEMO_SURFACE, ns, 1, bs);
+  const size_t stein = stein_workspace_bytes(ns, 2, bs), memo_s = memo_workspace_bytes(MEMO_STEIN, ns, 2, bs);
+  return 7 * a256(ns * blk) + 7 * a256(np * blk) + (sancho > memo_r ? sancho : memo_r) +
+         (stein > memo_s ? stein : memo_s) + 4 * a256(sizeof(int) * np + 64);
 }
 
 size_t negf_stein_workspace_bytes(int batch, int bs) { return stein_workspace_bytes(batch, 1, bs); }
 
 // stein_geometric (obc.py:427-447) for `batch` independent problems.
 int negf_stein_batched(int batch, int bs, const void* a, const void* q, void* w, double tol,
-                       int max_iter, const void* v0, int* status, int* iters, void* workspace,
-                       size_t workspace_bytes, void* stream) {
+                       int max_iter, const void* v0, int* status, int* iters, const int* select,
+                       void* workspace, size_t workspace_bytes, void* stream) {
   if (batch < 0 || bs < 1 || !a || !q || !w || !v0 || !status || !iters || max_iter < 1) return -1;
   if (bs > 6000) return -1;  // v0 / w staging in shared memory
   if (batch == 0) return 0;
   return stein_batched((const z_t*)a, (const z_t*)q, (z_t*)w, batch, 1, bs, tol, max_iter, status,
-                       iters, (const z_t*)v0, workspace, workspace_bytes, (cudaStream_t)stream);
+                       iters, (const z_t*)v0, workspace, workspace_bytes, (cudaStream_t)stream, select);
 }
 
 // W-side contact closure (scba.py:839-858), in place on the assembled batch.
@@ -437,8 +460,12 @@ int negf_w_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
                      const void* m_lower, void* bl_diag, const void* bl_upper, void* bg_diag,
                      const void* bg_upper, double surface_tol, int max_sweeps, double stein_tol,
                      int stein_max_iter, const void* v0, int* status, int* iters,
-                     int* stein_status, int* stein_iters, void* workspace,
+                     int* stein_status, int* stein_iters, void* memo_r_cache, int* memo_r_has,
+                     int* memo_r_used, void* memo_lg_cache, int* memo_lg_has, int* memo_lg_used,
+                     long long memo_ld, int n_fpi_r, int n_fpi_lg, double memo_tol, void* workspace,
                      size_t workspace_bytes, void* stream) {
+  if ((memo_r_cache && (!memo_r_has || memo_ld < n_e)) || (memo_lg_cache && (!memo_lg_has || memo_ld < n_e)))
+    return -1;
   if (n_e < 0 || n_b < 2 || bs < 1 || !m_diag || !m_upper || !m_lower || !status || !iters ||
       !stein_status || !stein_iters || !v0 || bs > 6000)
     return -1;
@@ -455,8 +482,13 @@ int negf_w_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
       *t = take(ns * blk), *a = take(ns * blk), *u0 = take(ns * blk);
   z_t *Y = take(np * blk), *Q0 = take(np * blk), *TMP = take(np * blk), *Qm = take(np * blk),
       *Wl = take(np * blk), *U1 = take(np * blk), *U2 = take(np * blk);
-  void* sws = p; p += sancho_workspace_bytes(ns, bs);
-  void* tws = p; p += stein_workspace_bytes(ns, 2, bs);
+  const size_t s_bytes = std::max(sancho_workspace_bytes(ns, bs), memo_workspace_bytes(MEMO_SURFACE, ns, 1, bs));
+  const size_t t_bytes = std::max(stein_workspace_bytes(ns, 2, bs), memo_workspace_bytes(MEMO_STEIN, ns, 2, bs));
+  void* sws = p; p += s_bytes;
+  void* tws = p; p += t_bytes;
+  int* has_buf = (int*)p; p += a256(sizeof(int) * np + 64);
+  int* need = (int*)p; p += a256(sizeof(int) * np + 64);
+  int* used_buf = (int*)p; p += a256(sizeof(int) * np + 64);
   (void)u0;
   const long long hn = (long long)ne * n2;
   auto gather = [&](z_t* dst, const z_t* src, long long stride) -> int {
@@ -473,8 +505,17 @@ int negf_w_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
   RC(gather(cn + hn, mu + (nb - 2) * n2, so));
   RC(gather(cnp, mu, so));
   RC(gather(cnp + hn, ml + (nb - 2) * n2, so));
-  RC(sancho_batched(cm, cn, cnp, ns, bs, surface_tol, max_sweeps, xr, status, iters, nullptr, sws,
-                    sancho_workspace_bytes(ns, bs), st));
+  if (memo_r_cache) {  // memoized W surfaces, key (W, side, e, R); staged through t
+    RC(memo_gather((const z_t*)memo_r_cache, memo_ld, memo_r_has, memo_ld, 2, ne, bs, t, has_buf, st));
+    RC(memo_refresh(MEMO_SURFACE, ns, 1, bs, cm, cn, cnp, nullptr, nullptr, n_fpi_r, memo_tol, t, has_buf, xr,
+                    need, used_buf, sws, s_bytes, st));
+    RC(sancho_batched(cm, cn, cnp, ns, bs, surface_tol, max_sweeps, xr, status, iters, nullptr, sws, s_bytes, st,
+                      need));
+    RC(memo_store(xr, used_buf, 2, ne, bs, (z_t*)memo_r_cache, memo_ld, memo_r_has, memo_r_used, memo_ld, st));
+  } else {
+    RC(sancho_batched(cm, cn, cnp, ns, bs, surface_tol, max_sweeps, xr, status, iters, nullptr, sws, s_bytes,
+                      st));
+  }
   auto D1 = [&](const z_t* A, long long sA, int oA, const z_t* B, long long sB, int oB, z_t* Dp,
                 long long sDp, int batch, bool neg = false) {
     ZGemmDesc d = zdesc_default();
@@ -530,9 +571,17 @@ int negf_w_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
       g.d[k] = D1(TMP + (long long)k * ns * n2, n2, OP_N, xr, n2, OP_H, Qm + (long long)k * ns * n2, n2, ns);
     RC(zgemm_group_launch(g, st));
   }
-  RC(stein_batched(a, Qm, Wl, ns, 2, bs, stein_tol, stein_max_iter, stein_status, stein_iters,
-                   (const z_t*)v0, tws,
-                   stein_workspace_bytes(ns, 2, bs), st));
+  if (memo_lg_cache) {  // memoized Stein solves, key (W, side, e, kind); staged through TMP
+    RC(memo_gather((const z_t*)memo_lg_cache, memo_ld, memo_lg_has, memo_ld, 4, ne, bs, TMP, has_buf, st));
+    RC(memo_refresh(MEMO_STEIN, ns, 2, bs, nullptr, nullptr, nullptr, a, Qm, n_fpi_lg, memo_tol, TMP, has_buf, Wl,
+                    need, used_buf, tws, t_bytes, st));
+    RC(stein_batched(a, Qm, Wl, ns, 2, bs, stein_tol, stein_max_iter, stein_status, stein_iters, (const z_t*)v0,
+                     tws, t_bytes, st, need));
+    RC(memo_store(Wl, used_buf, 4, ne, bs, (z_t*)memo_lg_cache, memo_ld, memo_lg_has, memo_lg_used, memo_ld, st));
+  } else {
+    RC(stein_batched(a, Qm, Wl, ns, 2, bs, stein_tol, stein_max_iter, stein_status, stein_iters, (const z_t*)v0,
+                     tws, t_bytes, st));
+  }
   // u1 = B_out x^dag (left B_out = B_01, right B_out = -B_{N-2,N-1}^dag); u2 = n wl
   {
     ZGemmGroup g;

@@ -72,9 +72,11 @@ def raise_on_obc_status(status: np.ndarray, iters: np.ndarray, resid: np.ndarray
 
 
 def sancho_batched(m: torch.Tensor, n: torch.Tensor, n_prime: torch.Tensor, tol: float = 1e-12,
-                   max_iter: int = 100, check: bool = True):
+                   max_iter: int = 100, check: bool = True, select: torch.Tensor | None = None,
+                   out: torch.Tensor | None = None):
     """Sancho-Rubio for a batch (batch, bs, bs) of complex128 CUDA tensors.
-    Returns (x, iters, status, resid) tensors."""
+    Returns (x, iters, status, resid) tensors. ``select`` (int32 per problem)
+    restricts the solve to select != 0; the others keep ``out``'s values."""
     if tol <= 0:
         raise ValueError(f"tol must be positive, got {tol}")
     lib = _lib.load()
@@ -83,7 +85,7 @@ def sancho_batched(m: torch.Tensor, n: torch.Tensor, n_prime: torch.Tensor, tol:
         if t.dtype != torch.complex128 or not t.is_cuda or tuple(t.shape) != (batch, bs, bs) or not t.is_contiguous():
             raise ValueError("m, n, n_prime must be contiguous complex128 CUDA tensors of one shape")
     dev = m.device
-    x = torch.empty_like(m)
+    x = torch.empty_like(m) if out is None else out
     status = torch.zeros(batch, dtype=torch.int32, device=dev)
     iters = torch.zeros(batch, dtype=torch.int32, device=dev)
     resid = torch.zeros(batch, dtype=torch.float64, device=dev)
@@ -91,7 +93,8 @@ def sancho_batched(m: torch.Tensor, n: torch.Tensor, n_prime: torch.Tensor, tol:
     ws = _lib.workspace(nbytes, dev)
     rc = lib.negf_obc_sancho_batched(batch, bs, m.data_ptr(), n.data_ptr(), n_prime.data_ptr(), tol,
                                      max_iter, x.data_ptr(), status.data_ptr(), iters.data_ptr(),
-                                     resid.data_ptr(), ws.data_ptr(), nbytes, _lib.stream_ptr(dev))
+                                     resid.data_ptr(), _lib.ptr(select), ws.data_ptr(), nbytes,
+                                     _lib.stream_ptr(dev))
     _lib.check(rc, "negf_obc_sancho_batched")
     if check:
         raise_on_obc_status(status.cpu().numpy(), iters.cpu().numpy(), resid.cpu().numpy(), max_iter, tol)
@@ -137,19 +140,22 @@ def sigma_lg_obc(x_r, contact_mu: float, kT: float, energy: float, couplings, de
     return ObcSigma(sr[0].cpu().numpy(), sl[0].cpu().numpy(), sg[0].cpu().numpy())
 
 
-def stein_batched(a: torch.Tensor, q: torch.Tensor, tol: float = 1e-12, max_iter: int = 100, check: bool = True):
-    """Geometric Stein w - a w a^dag = q for a batch (batch, bs, bs)."""
+def stein_batched(a: torch.Tensor, q: torch.Tensor, tol: float = 1e-12, max_iter: int = 100, check: bool = True,
+                  select: torch.Tensor | None = None, out: torch.Tensor | None = None):
+    """Geometric Stein w - a w a^dag = q for a batch (batch, bs, bs);
+    ``select`` / ``out`` as in sancho_batched."""
     lib = _lib.load()
     batch, bs = a.shape[0], a.shape[-1]
     dev = a.device
-    w = torch.empty_like(q)
+    w = torch.empty_like(q) if out is None else out
     status = torch.zeros(batch, dtype=torch.int32, device=dev)
     iters = torch.zeros(batch, dtype=torch.int32, device=dev)
     nbytes = lib.negf_stein_workspace_bytes(batch, bs)
     ws = _lib.workspace(nbytes, dev)
     v0 = _lib.power_start_vector(bs, dev)
     rc = lib.negf_stein_batched(batch, bs, a.data_ptr(), q.data_ptr(), w.data_ptr(), tol, max_iter, v0.data_ptr(),
-                                status.data_ptr(), iters.data_ptr(), ws.data_ptr(), nbytes, _lib.stream_ptr(dev))
+                                status.data_ptr(), iters.data_ptr(), _lib.ptr(select), ws.data_ptr(), nbytes,
+                                _lib.stream_ptr(dev))
     _lib.check(rc, "negf_stein_batched")
     if check:
         st = status.cpu().numpy()
@@ -191,3 +197,96 @@ def fixed_point_step(c, x, device="cuda"):
     if int(status.item()):
         raise SingularBlockError("singular surface update")
     return out.cpu().numpy()
+
+
+# -- runtime memoization (obc.py:490-608) --------------------------------------
+
+MEMO_SURFACE, MEMO_STEIN = 0, 1
+
+
+class SurfaceCache:
+    """obc.py:498-515 on the device: cached surface / Stein blocks in slots
+    named (subsystem, kind-class), each (n_seg, ld, bs, bs) complex128 with
+    (n_seg, ld) int32 has/used flags -- the reference's dict keyed by
+    (subsystem, side, energy index, kind), laid out so one batch of energies
+    is a strided slab. ``stats`` counts direct and memoized calls like the
+    reference (read lazily: one device reduction per snapshot)."""
+
+    def __init__(self, n_fpi_retarded: int = 20, n_fpi_lg: int = 10) -> None:
+        if n_fpi_retarded < 2 or n_fpi_lg < 2:
+            raise ValueError("refresh budgets must be at least 2")
+        self.n_fpi_retarded, self.n_fpi_lg = n_fpi_retarded, n_fpi_lg
+        self.slots: dict[tuple, tuple[torch.Tensor, torch.Tensor, torch.Tensor]] = {}
+        self._calls = 0
+        self._memo = None
+
+    def n_fpi(self, kind: str) -> int:
+        return self.n_fpi_retarded if kind == "R" else self.n_fpi_lg
+
+    def slot(self, name: tuple, n_seg: int, ld: int, bs: int, device):
+        s = self.slots.get(name)
+        if s is None:
+            dev = torch.device(device)
+            s = (torch.zeros((n_seg, ld, bs, bs), dtype=torch.complex128, device=dev),
+                 torch.zeros((n_seg, ld), dtype=torch.int32, device=dev),
+                 torch.zeros((n_seg, ld), dtype=torch.int32, device=dev))
+            self.slots[name] = s
+            if self._memo is None:
+                self._memo = torch.zeros((), dtype=torch.int64, device=dev)
+        return s
+
+    def record(self, used: torch.Tensor, e0: int, n_e: int) -> None:
+        """Count the calls of one batch (columns e0:e0+n_e of a used array)."""
+        u = used[:, e0:e0 + n_e]
+        self._calls += u.numel()
+        self._memo += u.sum()
+
+    @property
+    def stats(self) -> dict[str, int]:
+        memo = int(self._memo.item()) if self._memo is not None else 0
+        return {"direct_calls": self._calls - memo, "memoized_calls": memo}
+
+    def hit_rate(self) -> float:
+        st = self.stats
+        total = st["direct_calls"] + st["memoized_calls"]
+        return st["memoized_calls"] / total if total else 0.0
+
+
+def memo_refresh_batched(kind: int, x0: torch.Tensor, has: torch.Tensor, n_fpi: int, tol: float,
+                         m=None, n=None, n_prime=None, a=None, q=None, n_kind: int = 1):
+    """The refresh leg of memoized_obc for a batch (negf_memo_refresh_batched).
+    Returns (out, need_direct, used); out holds the accepted iterates."""
+    lib = _lib.load()
+    p_all, bs = x0.shape[0], x0.shape[-1]
+    n_side = p_all // n_kind
+    dev = x0.device
+    out = torch.zeros_like(x0)
+    need = torch.zeros(p_all, dtype=torch.int32, device=dev)
+    used = torch.zeros(p_all, dtype=torch.int32, device=dev)
+    nbytes = lib.negf_memo_workspace_bytes(kind, n_side, n_kind, bs)
+    ws = _lib.workspace(nbytes, dev)
+    p = _lib.ptr
+    rc = lib.negf_memo_refresh_batched(kind, n_side, n_kind, bs, p(m), p(n), p(n_prime), p(a), p(q), n_fpi, tol,
+                                       p(x0), p(has), p(out), p(need), p(used), p(ws), nbytes, _lib.stream_ptr(dev))
+    _lib.check(rc, "negf_memo_refresh_batched")
+    return out, need, used
+
+
+def memoized_surface_batched(m: torch.Tensor, n: torch.Tensor, n_prime: torch.Tensor, x0: torch.Tensor,
+                             has: torch.Tensor, n_fpi: int = 20, tol: float = 1e-6, surface_tol: float = 1e-8,
+                             max_iter: int = 100):
+    """memoized_obc (obc.py:519-608) for a batch of surface problems with the
+    fixed_point_step refresh and Sancho-Rubio as the direct solver.
+    Returns (x, used): used[b] = 1 where the cached block was refreshed."""
+    out, need, used = memo_refresh_batched(MEMO_SURFACE, x0, has, n_fpi, tol, m=m, n=n, n_prime=n_prime)
+    sancho_batched(m, n, n_prime, surface_tol, max_iter, select=need, out=out)
+    return out, used
+
+
+def memoized_stein_batched(a: torch.Tensor, q: torch.Tensor, w0: torch.Tensor, has: torch.Tensor,
+                           n_fpi: int = 10, tol: float = 1e-6, stein_tol: float = 1e-12, max_iter: int = 100):
+    """memoized_obc with the Stein map w <- q + a w a^dag and the geometric
+    Stein solve as the direct solver (scba.py:647-658)."""
+    out, need, used = memo_refresh_batched(MEMO_STEIN, w0, has, n_fpi, tol, a=a, q=q)
+    stein_batched(a, q, stein_tol, max_iter, select=need, out=out)
+    return out, used

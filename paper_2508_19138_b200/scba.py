@@ -38,8 +38,22 @@ Z = torch.complex128
 
 
 @dataclass(frozen=True)
+class MemoizerOptions:
+    """scba.py:143-154: budgets of the runtime direct-vs-refresh choice."""
+
+    enabled: bool = True
+    n_fpi_retarded: int = 20
+    n_fpi_lg: int = 10
+
+    def __post_init__(self) -> None:
+        if self.n_fpi_retarded < 2 or self.n_fpi_lg < 2:
+            raise ValueError("refresh budgets must be at least 2")
+
+
+@dataclass(frozen=True)
 class ScbaOptions:
-    """scba.py:157-190 (retarded_method fixed to Sancho-Rubio, memoizer off)."""
+    """scba.py:157-190 (retarded_method fixed to Sancho-Rubio). The memoizer
+    tolerance is tol / 10 as in the reference (scba.py:911)."""
 
     max_iter: int = 50
     tol: float = 1e-5
@@ -48,6 +62,7 @@ class ScbaOptions:
     stein_tol: float = 1e-12
     stein_max_iter: int = 100
     batch: int | None = None  # energies per device batch (None: all)
+    memoizer: MemoizerOptions = field(default_factory=MemoizerOptions)
 
     def __post_init__(self) -> None:
         if self.max_iter < 1:
@@ -135,8 +150,9 @@ class ScreenedSolver:
         self._buf, self._n_e = b, n_e
         return b
 
-    def solve(self, n_e: int, check: bool = True, timer=None) -> dict:
-        """Inputs in buffers pr_*/pl_*/pg_* (filled by the caller)."""
+    def solve(self, n_e: int, check: bool = True, timer=None, memo: tuple | None = None) -> dict:
+        """Inputs in buffers pr_*/pl_*/pg_* (filled by the caller). ``memo`` =
+        (SurfaceCache, ld, e0, tol_memo) as in CarrierSolver.solve."""
         import contextlib
 
         T = timer or (lambda name: contextlib.nullcontext())
@@ -157,12 +173,23 @@ class ScreenedSolver:
         _t.__enter__()
         nbytes = lib.negf_w_obc_workspace_bytes(n_e, self.bs)
         ws = _lib.workspace(nbytes, self.dev)
+        memo_args = [None] * 6 + [0, 20, 10, 0.0]
+        if memo is not None:
+            cache, ld, e0, tol_memo = memo
+            xr, hr, ur = cache.slot(("W", "R"), 2, ld, self.bs, self.dev)
+            xl, hl, ul = cache.slot(("W", "lg"), 4, ld, self.bs, self.dev)
+            memo_args = [p(xr[0, e0]), p(hr[0, e0:]), p(ur[0, e0:]), p(xl[0, e0]), p(hl[0, e0:]), p(ul[0, e0:]),
+                         ld, cache.n_fpi("R"), cache.n_fpi("<"), tol_memo]
         rc = lib.negf_w_obc_apply(n_e, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]),
                                   p(b["bl_diag"]), p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]),
                                   o.surface_tol, 100, o.stein_tol, o.stein_max_iter,
                                   p(_lib.power_start_vector(self.bs, self.dev)), p(b["obc_status"]),
-                                  p(b["obc_iters"]), p(b["stein_status"]), p(b["stein_iters"]), p(ws), nbytes, st)
+                                  p(b["obc_iters"]), p(b["stein_status"]), p(b["stein_iters"]), *memo_args,
+                                  p(ws), nbytes, st)
         _lib.check(rc, "negf_w_obc_apply")
+        if memo is not None:
+            cache.record(ur, e0, n_e)
+            cache.record(ul, e0, n_e)
         if check:
             raise_on_obc_status(b["obc_status"].cpu().numpy(), b["obc_iters"].cpu().numpy(), None, 100,
                                 o.surface_tol, "W contact")
@@ -315,6 +342,14 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
                 timings[self.name] = timings.get(self.name, 0.0) + _time.perf_counter() - self.t0
 
     iter_times = []
+    cache = None
+    if options.memoizer.enabled:
+        from .obc import SurfaceCache
+
+        cache = SurfaceCache(options.memoizer.n_fpi_retarded, options.memoizer.n_fpi_lg)
+    tol_memo = options.tol / 10.0
+    stats_by_it = []
+    memo = (lambda e0: (cache, max(n_own, 1), e0, tol_memo)) if cache is not None else (lambda e0: None)
     for it in range(max_iter):
         torch.cuda.synchronize(dev)
         t_iter = _time.perf_counter()
@@ -335,7 +370,7 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
                 lay.unpack_lg(sig.lesser, e0, nb_, blocks["sl_diag"], blocks["sl_upper"])
                 lay.unpack_lg(sig.greater, e0, nb_, blocks["sg_diag"], blocks["sg_upper"])
             with _T("G: OBC+RGF"):
-                b = carrier.solve(my_e[e0:e1], sigma=blocks, n_e=nb_)
+                b = carrier.solve(my_e[e0:e1], sigma=blocks, n_e=nb_, memo=memo(e0))
             with _T("layout"):
                 lay.pack(b["xl_diag"], b["xl_upper"], gl_c, e0)
                 lay.pack(b["xg_diag"], b["xg_upper"], gg_c, e0)
@@ -346,6 +381,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             result = {k: np.concatenate(vv) for k, vv in g_host.items()}
         if v is None:
             residuals.append(0.0)
+            if cache is not None:
+                stats_by_it.append(cache.stats)
             break
         # 2. G^<> to entry-major (all-to-all), polarization on own entry rows
         with _T("transpose"):
@@ -366,7 +403,7 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
                 lay.unpack_retarded(pru, prl, e0, nb_, wb["pr_diag"], wb["pr_upper"], wb["pr_lower"])
                 lay.unpack_lg(pl, e0, nb_, wb["pl_diag"], wb["pl_upper"])
                 lay.unpack_lg(pg, e0, nb_, wb["pg_diag"], wb["pg_upper"])
-            wb = screened.solve(nb_, timer=_T)
+            wb = screened.solve(nb_, timer=_T, memo=memo(e0))
             with _T("layout"):
                 lay.pack(wb["wl_diag"], wb["wl_upper"], wl_c, e0)
                 lay.pack(wb["wg_diag"], wb["wg_upper"], wg_c, e0)
@@ -395,6 +432,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         delta, scale = comm.allreduce_max([delta, scale], dev)
         residuals.append(delta / (scale + 1e-300))
         del raw
+        if cache is not None:
+            stats_by_it.append(cache.stats)
         iter_times.append(_time.perf_counter() - t_iter)
         if residuals[-1] < options.tol:
             break
@@ -409,4 +448,6 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     result["energy_slice"] = own
     result["transpose_bytes"] = tr.bytes_moved
     result["timings"] = timings
+    result["cache_stats"] = cache.stats if cache is not None else {"direct_calls": 0, "memoized_calls": 0}
+    result["cache_stats_by_iteration"] = stats_by_it
     return result

@@ -105,13 +105,13 @@ def make_conv():
     np.savez_compressed(OUT / "golden_conv.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
 
 
-def scba_case(nb, bs, ne, iters, ballistic=False):
+def scba_case(nb, bs, ne, iters, ballistic=False, memo=False):
     h = toys.chain_device(nb, bs)
     v = None if ballistic else toys.coulomb_matrix(nb, bs)
     grid = EnergyGrid(-2.0, 2.0, ne, eta=1e-3)
     contacts = scba.ContactConfig(mu_left=0.1, mu_right=-0.1, kT=0.05)
-    opts = scba.ScbaOptions(max_iter=iters, tol=1e-12, mixing=0.3, retarded_method="sancho",
-                            memoizer=scba.MemoizerOptions(enabled=False))
+    opts = scba.ScbaOptions(max_iter=iters, tol=1e-5 if memo else 1e-12, mixing=0.3, retarded_method="sancho",
+                            memoizer=scba.MemoizerOptions(enabled=memo))
     with threadpool_limits(1):
         return scba.scba_run(h, v, grid, contacts, opts)
 
@@ -179,6 +179,78 @@ def make_scba():
     out["obs_terminal_right"] = np.array(scba.terminal_current(res, "right"))
     out["obs_landauer"] = np.array(scba.landauer_current(h, res.grid, res.contacts))
     np.savez_compressed(OUT / "golden_ballistic_small.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
+
+
+def make_memo():
+    """memoized_obc (obc.py:519-608) decisions and values, and scba_run with
+    the memoizer on (reference default; tol 1e-5 -> tol_memo 1e-6)."""
+    out = {}
+    k = 0
+    for seed in range(4):
+        for de, eta, n_fpi, tol in ((0.0, 0.05, 20, 1e-6), (1e-7, 0.05, 20, 1e-6), (1e-4, 0.05, 20, 1e-6),
+                                    (1e-3, 0.02, 10, 1e-8), (3e-2, 0.05, 20, 1e-6), (0.4, 0.05, 20, 1e-6),
+                                    (1e-3, 1e-3, 20, 1e-6)):
+            c0 = toys.random_lead(seed, 6, energy=0.2, eta=eta)
+            c1 = toys.random_lead(seed, 6, energy=0.2 + de, eta=eta)
+            cache = obc.SurfaceCache()
+            key = ("G", "left", 0, "R")
+            obc.memoized_obc(key, lambda: obc.obc_sancho_rubio(c0, tol=1e-8).x_r,
+                             lambda x: obc.fixed_point_step(c0, x), cache, n_fpi, tol)
+            x0 = np.array(cache.entries[key].value)
+            x = obc.memoized_obc(key, lambda: obc.obc_sancho_rubio(c1, tol=1e-8).x_r,
+                                 lambda x: obc.fixed_point_step(c1, x), cache, n_fpi, tol)
+            p = f"r{k}_"
+            out[p + "m"], out[p + "n"], out[p + "np"] = c1.m, c1.n, c1.n_prime
+            out[p + "x0"], out[p + "x"] = x0, np.asarray(x)
+            out[p + "cfg"] = np.array([n_fpi, tol])
+            out[p + "memoized"] = np.array(cache.stats["memoized_calls"])
+            k += 1
+    out["n_r"] = np.array(k)
+    rng = np.random.default_rng(21)
+    k = 0
+    for rad in (0.3, 0.7, 0.95):
+        for pert in (0.0, 1e-9, 1e-5, 1e-2, 1.0):
+            a = rng.standard_normal((5, 5)) + 1j * rng.standard_normal((5, 5))
+            a *= rad / max(abs(np.linalg.eigvals(a)))
+            q = rng.standard_normal((5, 5)) + 1j * rng.standard_normal((5, 5))
+            q = q + q.conj().T
+            w0 = obc.stein_geometric(a, q) + pert * (rng.standard_normal((5, 5)) + 0j)
+            cache = obc.SurfaceCache()
+            key = ("W", "left", 0, "<")
+            cache.entries[key] = obc.CacheEntry(w0)
+            w = obc.memoized_obc(key, lambda: scba._stein_direct(a, q),
+                                 lambda w: q + a @ w @ a.conj().T, cache, 10, 1e-6)
+            p = f"s{k}_"
+            out[p + "a"], out[p + "q"], out[p + "w0"], out[p + "w"] = a, q, w0, np.asarray(w)
+            out[p + "memoized"] = np.array(cache.stats["memoized_calls"])
+            k += 1
+    out["n_s"] = np.array(k)
+    np.savez_compressed(OUT / "golden_memo.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
+    # scba_run, memoizer on
+    out = {}
+    res = scba_case(6, 4, 32, 4, memo=True)
+    for f in RESULT_FIELDS:
+        out[f] = getattr(res, f)
+    for f in ("lesser", "greater", "ret_upper", "ret_lower"):
+        out["sigma_" + f] = getattr(res.sigma, f)
+    out["residuals"] = np.asarray(res.residuals)
+    out["cache_stats"] = np.array([[s_["direct_calls"], s_["memoized_calls"]] for s_ in res.cache_stats_by_iteration])
+    out["config"] = np.array([6, 4, 32, 4])
+    np.savez_compressed(OUT / "golden_scba_memo_small.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
+    out = {}
+    res = scba_case(16, 32, 128, 3, memo=True)
+    rng = np.random.default_rng(98)
+    for f in RESULT_FIELDS:
+        a = getattr(res, f)
+        out[f + "_chk"] = np.tensordot(a, rng.standard_normal(a.shape[1:]), axes=a.ndim - 1)
+    for f in ("lesser", "greater", "ret_upper", "ret_lower"):
+        a = getattr(res.sigma, f)
+        out["sigma_" + f + "_chk"] = a.T @ rng.standard_normal(a.shape[0])
+        out["sigma_" + f + "_fro"] = np.array(np.linalg.norm(a))
+    out["residuals"] = np.asarray(res.residuals)
+    out["cache_stats"] = np.array([[s_["direct_calls"], s_["memoized_calls"]] for s_ in res.cache_stats_by_iteration])
+    out["config"] = np.array([16, 32, 128, 3])
+    np.savez_compressed(OUT / "golden_scba_memo_c1.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
 
 
 if __name__ == "__main__":

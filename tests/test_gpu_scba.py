@@ -8,7 +8,9 @@ import torch
 
 import negf_oracle as orc
 from paper_2508_19138_b200.carrier import Contacts
-from paper_2508_19138_b200.scba import EntryLayout, ScbaOptions, ScreenedSolver, scba_run
+from paper_2508_19138_b200.scba import EntryLayout, MemoizerOptions, ScbaOptions, ScreenedSolver, scba_run
+
+MEMO_OFF = MemoizerOptions(enabled=False)
 from test_oracle_golden import check_c1
 
 pytestmark = pytest.mark.gpu
@@ -78,7 +80,7 @@ def test_scba_small_matches_reference_scba_run(golden, cuda):
     """3 GW iterations, 6x4 chain + Coulomb, 32 energies (batches of 10)."""
     g = golden("golden_scba_small.npz")
     res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
-                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=3, tol=1e-12, batch=10), device=cuda)
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=3, tol=1e-12, batch=10, memoizer=MEMO_OFF), device=cuda)
     for k in g.files:
         if k.startswith(("ver_", "config")):
             continue
@@ -89,7 +91,7 @@ def test_scba_c1_matches_reference_scba_run(golden, cuda):
     """C1: 16 blocks x 32 orbitals, 128 energies, one GW iteration."""
     g = golden("golden_scba_c1.npz")
     res = scba_run(orc.chain_device(16, 32), orc.coulomb_matrix(16, 32), np.linspace(-2.0, 2.0, 128), 1e-3,
-                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=1, tol=1e-12, batch=64), device=cuda)
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=1, tol=1e-12, batch=64, memoizer=MEMO_OFF), device=cuda)
     check_c1(res, g, tol=TOL)
 
 
@@ -98,9 +100,10 @@ def test_scba_c1_matches_oracle_two_iterations(cuda):
     h, v = orc.chain_device(16, 32), orc.coulomb_matrix(16, 32)
     e = np.linspace(-2.0, 2.0, 128)
     ref = orc.scba(h, v, e, 1e-3, 0.1, -0.1, 0.05, max_iter=2)
-    res = scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=2, tol=1e-12), device=cuda)
+    res = scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=2, tol=1e-12, memoizer=MEMO_OFF), device=cuda)
     for k in ref:
-        assert rel(res[k], ref[k]) < TOL, k
+        if k != "cache_stats_by_iteration":
+            assert rel(res[k], ref[k]) < TOL, k
 
 
 def test_scba_reference_api_with_blockmatrix_inputs(golden, cuda):
@@ -122,6 +125,6 @@ def test_scba_reference_api_with_blockmatrix_inputs(golden, cuda):
     g = golden("golden_scba_small.npz")
     res = scba_run_reference_api(bm(orc.chain_device(6, 4)), bm(orc.coulomb_matrix(6, 4)), EnergyGrid(-2.0, 2.0, 32),
                                  SimpleNamespace(mu_left=0.1, mu_right=-0.1, kT=0.05),
-                                 ScbaOptions(max_iter=3, tol=1e-12), device=cuda)
+                                 ScbaOptions(max_iter=3, tol=1e-12, memoizer=MEMO_OFF), device=cuda)
     for k in ("g_r_diag", "g_lesser_upper", "sigma_lesser", "sigma_ret_lower", "residuals"):
         assert rel(res[k], g[k]) < TOL, k

@@ -173,3 +173,41 @@ def check_c1(res, g, tol=1e-10):
         assert rel(a.T @ rng.standard_normal(a.shape[0]), g["sigma_" + f + "_chk"]) < tol, f
         assert abs(np.linalg.norm(a) - float(g["sigma_" + f + "_fro"])) < tol * float(g["sigma_" + f + "_fro"])
     assert rel(res["residuals"], g["residuals"]) < tol
+
+
+def test_oracle_memoized_obc_matches_reference(golden):
+    """memoized_obc (obc.py:519-608): same refresh/direct decision and value
+    as the reference on primed caches (surface fixed point and Stein)."""
+    g = golden("golden_memo.npz")
+    for k in range(int(g["n_r"])):
+        p = f"r{k}_"
+        m, n, npr = g[p + "m"], g[p + "n"], g[p + "np"]
+        n_fpi, tol = int(g[p + "cfg"][0]), float(g[p + "cfg"][1])
+        cache = orc.SurfaceCache()
+        cache.entries["k"] = g[p + "x0"]
+        x = orc.memoized_obc("k", lambda: orc.sancho_rubio(m, n, npr, tol=1e-8)[0],
+                             lambda x: orc.fixed_point_step(m, n, npr, x), cache, n_fpi, tol)
+        assert cache.stats["memoized_calls"] == int(g[p + "memoized"]), k
+        assert rel(x, g[p + "x"]) < 1e-12, k
+    for k in range(int(g["n_s"])):
+        p = f"s{k}_"
+        a, q = g[p + "a"], g[p + "q"]
+        cache = orc.SurfaceCache()
+        cache.entries["k"] = g[p + "w0"]
+        w = orc.memoized_obc("k", lambda: orc.stein_direct(a, q), lambda w: q + a @ w @ a.conj().T, cache, 10, 1e-6)
+        assert cache.stats["memoized_calls"] == int(g[p + "memoized"]), k
+        assert rel(w, g[p + "w"]) < 1e-12, k
+
+
+def test_oracle_scba_memoizer_matches_reference(golden):
+    """scba_run with the OBC memoizer on (reference default, tol 1e-5): 4
+    iterations, per-iteration direct/memoized counts and every array."""
+    g = golden("golden_scba_memo_small.npz")
+    res = orc.scba(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3, 0.1, -0.1,
+                   0.05, max_iter=4, tol=1e-5, memoizer=(20, 10))
+    stats = np.array([[s["direct_calls"], s["memoized_calls"]] for s in res["cache_stats_by_iteration"]])
+    np.testing.assert_array_equal(stats, g["cache_stats"])
+    for k in g.files:
+        if k.startswith(("ver_", "config", "cache_stats")):
+            continue
+        assert rel(res[k], g[k]) < 1e-9, k
