@@ -138,6 +138,44 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
     cp_async_commit();
   }
 
+  // Epilogue operands: this thread's C fragment (and its row maps) are loaded
+  // as one batch of independent loads -- for the short-K row-mapped sweeps
+  // before the main loop, so their latency hides behind it; otherwise after.
+  const double2 al = d.alpha, be = d.beta;
+  const bool use_c = d.C != nullptr && (be.x != 0.0 || be.y != 0.0);
+  const z_t* C = use_c ? d.C + (long long)b * d.sC : nullptr;
+  const int er = lane >> 2, eq = lane & 3;
+  // The row maps are read before the main loop; C is read in the epilogue one
+  // fragment row (2*TN independent loads) at a time.
+  constexpr int CI = 1;
+  int crow[CF::TM], drow[CF::TM];
+  z_t cfrag[CI][CF::TN][2];
+  auto map_rows = [&]() {
+#pragma unroll
+    for (int i = 0; i < CF::TM; ++i) {
+      const int gm = m0 + wm * CF::WTM + i * 8 + er;
+      crow[i] = drow[i] = gm;
+      if constexpr (CF::ROWMAP) {
+        if (gm < d.M) {
+          if (d.rowmap_c) crow[i] = d.rowmap_c[(long long)b * d.s_map + gm];
+          if (d.rowmap_d) drow[i] = d.rowmap_d[(long long)b * d.s_map + gm];
+        }
+      }
+    }
+  };
+  auto load_c_row = [&](int i, int slot) {
+    const int gm = m0 + wm * CF::WTM + i * 8 + er;
+#pragma unroll
+    for (int j = 0; j < CF::TN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gn = n0 + wn * CF::WTN + j * 8 + 2 * eq + h;
+        cfrag[slot][j][h] = (use_c && gm < d.M && gn < d.N) ? C[(long long)crow[i] * d.ldc + gn]
+                                                            : make_double2(0.0, 0.0);
+      }
+  };
+  map_rows();
+
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<CF::STAGES - 2>();
     __syncthreads();
@@ -222,19 +260,16 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
   cp_async_wait<0>();
 
   // Epilogue: value = alpha*acc + beta*C, stored plain or conj-transposed.
-  const double2 al = d.alpha, be = d.beta;
-  const bool use_c = d.C != nullptr && (be.x != 0.0 || be.y != 0.0);
-  const z_t* C = use_c ? d.C + (long long)b * d.sC : nullptr;
   z_t* D = d.D + (long long)b * d.sD;
-  const int r = lane >> 2, q = lane & 3;
 #pragma unroll
-  for (int i = 0; i < CF::TM; ++i)
+  for (int i = 0; i < CF::TM; ++i) {
+    load_c_row(i, 0);
 #pragma unroll
     for (int j = 0; j < CF::TN; ++j) {
-      const int gm = m0 + wm * CF::WTM + i * 8 + r;
+      const int gm = m0 + wm * CF::WTM + i * 8 + er;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int gn = n0 + wn * CF::WTN + j * 8 + 2 * q + h;
+        const int gn = n0 + wn * CF::WTN + j * 8 + 2 * eq + h;
         if (gm < d.M && gn < d.N) {
           double xr = acc_re[i][j][h], xi = acc_im[i][j][h];
           if constexpr (CF::GAUSS) {
@@ -243,26 +278,17 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
             xi = acc_s[i][j][h] - p1 - p2;
           }
           z_t v = zmake(al.x * xr - al.y * xi, al.x * xi + al.y * xr);
-          if (use_c) {
-            int cm = gm;
-            if constexpr (CF::ROWMAP)
-              if (d.rowmap_c) cm = d.rowmap_c[(long long)b * d.s_map + gm];
-            z_t c = C[(long long)cm * d.ldc + gn];
-            v.x += be.x * c.x - be.y * c.y;
-            v.y += be.x * c.y + be.y * c.x;
-          }
+          const z_t c = cfrag[0][j][h];
+          v.x += be.x * c.x - be.y * c.y;
+          v.y += be.x * c.y + be.y * c.x;
           if (d.transD)
             D[(long long)gn * d.ldd + gm] = zconj(v);
           else
-          {
-            int dm = gm;
-            if constexpr (CF::ROWMAP)
-              if (d.rowmap_d) dm = d.rowmap_d[(long long)b * d.s_map + gm];
-            D[(long long)dm * d.ldd + gn] = v;
-          }
+            D[(long long)drow[i] * d.ldd + gn] = v;
         }
       }
     }
+  }
 }
 
 template <class CF>
