@@ -9,9 +9,13 @@ namespace {
 constexpr unsigned long long kSign = 0x8000000000000000ull;
 
 template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_, bool GAUSS_ = false, int BK_ = 8,
-          bool ROWMAP_ = false>
+          bool ROWMAP_ = false, bool SWZ_ = false>
 struct Cfg {
   static constexpr bool ROWMAP = ROWMAP_;  // honour ZGemmDesc row maps (inversion sweeps only)
+  // SWZ: k-contiguous tiles unpadded, element (mn, k) at mn*BK + (k ^ 4*(mn&1))
+  // (XOR swizzle instead of the +4 pad: same conflict-free fragment reads,
+  // a third less shared memory at BK = 8, a fifth at BK = 16)
+  static constexpr bool SWZ = SWZ_;
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
   // GAUSS: 3 real products per complex product (3M / Gauss):
   //   P1 = ar br, P2 = ai bi, P3 = (ar + ai)(br + bi);  re = P1 - P2, im = P3 - P1 - P2
@@ -22,7 +26,7 @@ struct Cfg {
   static constexpr int WTN = BN / WN;
   static constexpr int TM = WTM / 8;  // 8x8 DMMA tiles per warp
   static constexpr int TN = WTN / 8;
-  static constexpr int SK = BK + 4;   // k-contiguous row stride
+  static constexpr int SK = SWZ ? BK : BK + 4;  // k-contiguous row stride
   static constexpr int SMA = BM + 2;  // mn-contiguous row stride (A)
   static constexpr int SMB = BN + 2;  // mn-contiguous row stride (B)
   static constexpr int A_ELEMS = (BM * SK > BK * SMA) ? BM * SK : BK * SMA;
@@ -41,6 +45,13 @@ struct KtBounds {
     return term == 0 ? 0 : term == 1 ? b1 : term == 2 ? b2 : b3;
   }
 };
+
+// k-contiguous smem index of (mn, k)
+template <class CF>
+__device__ __forceinline__ int kc_idx(int mn, int k) {
+  if constexpr (CF::SWZ) return mn * CF::SK + (k ^ ((mn & 1) << 2));
+  else return mn * CF::SK + k;
+}
 
 template <class CF>
 __device__ __forceinline__ void load_stage(const ZGemmDesc& d, int kt, const KtBounds& kb, int b,
@@ -61,7 +72,7 @@ __device__ __forceinline__ void load_stage(const ZGemmDesc& d, int kt, const KtB
       if constexpr (CF::ROWMAP)
         if (p && d.rowmap_a) pm = d.rowmap_a[(long long)b * d.s_map + gm];
       const z_t* src = p ? A + (long long)pm * t.lda + gk : A;
-      cp_async16(sA + mn * CF::SK + k, src, p);
+      cp_async16(sA + kc_idx<CF>(mn, k), src, p);
     }
   } else {  // A stored [K][M]: m contiguous
 #pragma unroll
@@ -89,7 +100,7 @@ __device__ __forceinline__ void load_stage(const ZGemmDesc& d, int kt, const KtB
       int gn = n0 + mn, gk = k0 + k;
       bool p = gn < N && gk < K;
       const z_t* src = p ? B + (long long)gn * t.ldb + gk : B;
-      cp_async16(sB + mn * CF::SK + k, src, p);
+      cp_async16(sB + kc_idx<CF>(mn, k), src, p);
     }
   }
 }
@@ -203,17 +214,20 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
 #pragma unroll
     for (int k4 = 0; k4 < CF::BK / 4; ++k4) {
       const int kk = k4 * 4 + q;
+      // k-contiguous reads: row parity of (.. + r) is r&1 (row bases are multiples of 8)
+      const int kka = (CF::SWZ && a_kc) ? (kk ^ ((r & 1) << 2)) : kk;
+      const int kkb = (CF::SWZ && b_kc) ? (kk ^ ((r & 1) << 2)) : kk;
       double ar[CF::TM], ai[CF::TM], nai[CF::TM], br[CF::TN], bi[CF::TN];
 #pragma unroll
       for (int i = 0; i < CF::TM; ++i) {
-        z_t v = sA[(wm * CF::WTM + i * 8 + r) * a_smn + kk * a_sk];
+        z_t v = sA[(wm * CF::WTM + i * 8 + r) * a_smn + kka * a_sk];
         ar[i] = dneg_if(v.x, negm);
         ai[i] = dneg_if(v.y, negm ^ conjA);
         nai[i] = dneg_if(ai[i], kSign);
       }
 #pragma unroll
       for (int j = 0; j < CF::TN; ++j) {
-        z_t v = sB[(wn * CF::WTN + j * 8 + r) * b_smn + kk * b_sk];
+        z_t v = sB[(wn * CF::WTN + j * 8 + r) * b_smn + kkb * b_sk];
         br[j] = v.x;
         bi[j] = dneg_if(v.y, conjB);
       }
@@ -333,15 +347,25 @@ using CfgBig = Cfg<64, 64, 2, 2, 4, 2>;
 using CfgSmall = Cfg<32, 32, 1, 1, 4, 4>;
 // 3M variant: warp tile 32x16 keeps the three accumulator sets in registers
 using CfgGauss = Cfg<64, 64, 2, 4, 4, 1, true>;
-using CfgGauss2 = Cfg<64, 32, 2, 2, 4, 3, true>;
+// default (algo 2): 3M, 64x32 CTA tiles of 4 warps, 3 CTAs/SM, BK = 16 with a
+// 2-stage cp.async pipeline and XOR-swizzled k-contiguous tiles (50 KB smem):
+// 96 DMMAs per warp between barriers
+using CfgGauss2 = Cfg<64, 32, 2, 2, 2, 3, true, 16, false, true>;
+using CfgGauss2S = Cfg<32, 64, 2, 2, 2, 3, true, 16, false, true>;  // short M
 using Cfg4M32 = Cfg<64, 32, 2, 2, 4, 3, false>;
 using CfgGauss3 = Cfg<32, 64, 2, 2, 4, 3, true>;
+using CfgGauss2P = Cfg<64, 32, 2, 2, 4, 3, true>;  // BK = 8, 4 stages, padded tiles
+using CfgG32s2 = Cfg<64, 32, 2, 2, 2, 2, true, 32, false, true>;
 using CfgMap64 = Cfg<64, 32, 2, 2, 4, 3, true, 8, true>;
 using CfgMap32 = Cfg<32, 64, 2, 2, 4, 3, true, 8, true>;
-// Measured alternatives (C2 carrier batch, energies/s; algo 2 = 90.5):
-//   64x32 6-stage 2 CTA/SM 78.9 | 128x32 8 warps 68.1 | 32x32 2 warps 78.2 |
-//   64x32 BK=16 80.8 | 32x32 4 warps (16x16) 87.4 | 64x64 16 warps 69.3 |
-//   64x32 8 warps (16x16) 84.5  -> occupancy of 12 warps with 32x16 warp tiles wins.
+using CfgMap64S = Cfg<64, 32, 2, 2, 2, 3, true, 16, true, true>;
+using CfgMap32S = Cfg<32, 64, 2, 2, 2, 3, true, 16, true, true>;
+// Measured alternatives (C2 carrier batch, energies/s, greater by identity):
+//   algo 2 (64x32, BK16, 2 stages, swizzled) 142.4 | 64x32 BK8 4 stages padded 137.9 |
+//   32x64 BK16 swizzled 140.0 | 64x32 BK32 2 CTA/SM 133.5 | 64x32 BK16 4 CTA/SM (spills) 109.4
+// Earlier (recursion for G^>, BK8 padded family): 64x32 6-stage 2 CTA/SM 78.9 | 128x32 8 warps
+//   68.1 | 32x32 2 warps 78.2 | 32x32 4 warps (16x16) 87.4 | 64x64 16 warps 69.3 vs 90.5.
+static int g_map_cfg = 0;
 
 }  // namespace
 
@@ -352,7 +376,12 @@ using CfgMap32 = Cfg<32, 64, 2, 2, 4, 3, true, 8, true>;
 // bound keeps every parity test at the 1e-9 bar.
 static int g_algo = 2;
 int gemm_algo() { return g_algo; }
-void set_gemm_algo(int a) { g_algo = a; }
+// algo >= 10: algo - 10 for the products, swizzled BK = 16 tiles for the
+// row-mapped inversion sweeps (experiment switch)
+void set_gemm_algo(int a) {
+  g_map_cfg = a >= 10 ? 1 : 0;
+  g_algo = a >= 10 ? a - 10 : a;
+}
 
 int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
   if (g.n <= 0) return 0;
@@ -367,16 +396,24 @@ int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
     mapped |= g.d[i].rowmap_a || g.d[i].rowmap_c || g.d[i].rowmap_d;
     m64 &= g.d[i].M % 64 == 0;
   }
-  if (mapped) return m64 ? launch_cfg<CfgMap64>(g, stream) : launch_cfg<CfgMap32>(g, stream);
+  if (mapped) {
+    if (g_map_cfg == 1) return m64 ? launch_cfg<CfgMap64S>(g, stream) : launch_cfg<CfgMap32S>(g, stream);
+    return m64 ? launch_cfg<CfgMap64>(g, stream) : launch_cfg<CfgMap32>(g, stream);
+  }
   if (mx <= 32) return launch_cfg<CfgSmall>(g, stream);
   int mm = 0;
   for (int i = 0; i < g.n; ++i) mm = g.d[i].M > mm ? g.d[i].M : mm;
-  if (mm <= 32 && (gemm_algo() == 2 || gemm_algo() == 4)) return launch_cfg<CfgGauss3>(g, stream);  // short M
+  if (mm <= 32) {  // short M
+    if (gemm_algo() == 2) return launch_cfg<CfgGauss2S>(g, stream);
+    if (gemm_algo() >= 4) return launch_cfg<CfgGauss3>(g, stream);
+  }
   switch (gemm_algo()) {
     case 1: return launch_cfg<CfgGauss>(g, stream);
     case 2: return launch_cfg<CfgGauss2>(g, stream);
     case 3: return launch_cfg<Cfg4M32>(g, stream);
     case 4: return launch_cfg<CfgGauss3>(g, stream);
+    case 5: return launch_cfg<CfgGauss2P>(g, stream);
+    case 6: return launch_cfg<CfgG32s2>(g, stream);
     default: return launch_cfg<CfgBig>(g, stream);
   }
 }
