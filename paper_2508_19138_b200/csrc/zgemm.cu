@@ -156,9 +156,12 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
   const bool use_c = d.C != nullptr && (be.x != 0.0 || be.y != 0.0);
   const z_t* C = use_c ? d.C + (long long)b * d.sC : nullptr;
   const int er = lane >> 2, eq = lane & 3;
-  // The row maps are read before the main loop; C is read in the epilogue one
-  // fragment row (2*TN independent loads) at a time.
-  constexpr int CI = 1;
+  // The row maps are read before the main loop. C is read in the epilogue one
+  // fragment row (2*TN independent loads) at a time -- or, for 4M row-mapped
+  // configs, as a whole fragment before the main loop (measured slower for
+  // the inversion sweeps: 255 registers, 2 CTAs/SM; kept for experiments).
+  constexpr bool PREC = CF::ROWMAP && !CF::GAUSS;
+  constexpr int CI = PREC ? CF::TM : 1;
   int crow[CF::TM], drow[CF::TM];
   z_t cfrag[CI][CF::TN][2];
   auto map_rows = [&]() {
@@ -186,6 +189,10 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
       }
   };
   map_rows();
+  if constexpr (PREC) {
+#pragma unroll
+    for (int i = 0; i < CF::TM; ++i) load_c_row(i, i);
+  }
 
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<CF::STAGES - 2>();
@@ -277,7 +284,7 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
   z_t* D = d.D + (long long)b * d.sD;
 #pragma unroll
   for (int i = 0; i < CF::TM; ++i) {
-    load_c_row(i, 0);
+    if constexpr (!PREC) load_c_row(i, 0);
 #pragma unroll
     for (int j = 0; j < CF::TN; ++j) {
       const int gm = m0 + wm * CF::WTM + i * 8 + er;
@@ -292,7 +299,7 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
             xi = acc_s[i][j][h] - p1 - p2;
           }
           z_t v = zmake(al.x * xr - al.y * xi, al.x * xi + al.y * xr);
-          const z_t c = cfrag[0][j][h];
+          const z_t c = cfrag[PREC ? i : 0][j][h];
           v.x += be.x * c.x - be.y * c.y;
           v.y += be.x * c.y + be.y * c.x;
           if (d.transD)

@@ -6,7 +6,8 @@ from paper_2508_19138_b200.carrier import CarrierSolver, Contacts
 nb_, bs, batch = (int(x) for x in sys.argv[1:4])
 ov = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 lib = _lib.load(); lib.negf_set_rgf_overlap(ov)
-solver = CarrierSolver(toys.chain_device(nb_, bs), 1e-3, Contacts(0.1, -0.1, 0.05), 1e-8)
+greater = sys.argv[5] if len(sys.argv) > 5 else "identity"
+solver = CarrierSolver(toys.chain_device(nb_, bs), 1e-3, Contacts(0.1, -0.1, 0.05), 1e-8, greater=greater)
 e = np.linspace(-2, 2, batch)
 solver.solve(e, n_e=batch); torch.cuda.synchronize()
 lib.negf_prof_reset(); lib.negf_prof_enable(1)
