@@ -334,10 +334,13 @@ def run_native(args):
     if rank == 0:
         gemm_avg_ms = g_ms.value / max(g_n.value, 1)
         achieved = g_fl.value / (g_ms.value * 1e-3) / 1e12 if g_ms.value > 0 else 0.0
-        traffic = None
+        traffic, traffic_note = None, None
         tf = ROOT / "profiles" / "zgemm_traffic.json"
         if tf.exists():
-            traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+            tj = json.loads(tf.read_text())
+            traffic = tj.get("dram_bytes_per_launch")
+            traffic_note = (f"one ncu --set full capture ({tj.get('launch')}): dram read+write per launch vs "
+                            f"{tj.get('algorithmic_bytes_per_launch')} algorithmic bytes; {tj.get('source')}")
         rgf_model = model_flops_per_energy(n_b, bs, 1 if args.greater == "identity" else 2) * total_e
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -359,7 +362,7 @@ def run_native(args):
                         if args.greater == "identity" else "G^> by its own Keldysh recursion (reference algorithm)"),
             "roofline": {"bound": "tensor", "kernel": "zgemm_kernel (DMMA m8n8k4 f64)", "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-                         "traffic": traffic,
+                         "traffic": traffic, "traffic_basis": traffic_note,
                          "achieved_basis": f"algorithmic 8*M*N*K*batch flops of the {g_n.value} ZGEMM launches of one "
                                            f"{batch}-energy batch / their CUDA-event time ({gemm_avg_ms:.3f} ms avg), "
                                            f"measured in bench.py right after the timed region with the forward-sweep "
