@@ -302,6 +302,50 @@ int negf_w_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
  * solutions (key (W, side, e, kind), [2 kinds][2 sides][memo_ld]); budgets
  * n_fpi_r / n_fpi_lg (SurfaceCache.n_fpi, obc.py:504-512). */
 
+/* ---- (5b) spatial domain decomposition (negfgw/dist.py) ------------------
+ * Partition-local pieces of dist_selected_solve (dist.py:622-717) for a
+ * batch of n_e energies; the caller (paper_2508_19138_b200/dd.py) runs one
+ * partition per GPU, all-gathers the boundary contributions over NCCL and
+ * solves the reduced chain (dist.py:486-561) on every rank with
+ * negf_rgf_sweeps_batched / negf_rgf_selected_solve_batched. Inputs are the
+ * partition's own energy-major stacks (w blocks; upper/lower w-1); source
+ * kinds may be NULL. Workspace: negf_dd_workspace_bytes(n_e, bs). */
+size_t negf_dd_workspace_bytes(int n_e, int bs);
+/* _schur_tail (dist.py:365-385): after the forward sweep of an end
+ * partition (x_fwd / xl_fwd / xg_fwd = the forward diagonal stacks),
+ * s = M[w-1,w-1] - M[w-1,w-2] x_{w-2} M[w-2,w-1] and the effective sources
+ * b = B[w-1,w-1] + a xl_{w-2} a^H - (y - y^H), y = a x_{w-2} B[w-2,w-1];
+ * outputs [n_e][bs][bs]. */
+int negf_dd_schur_tail(int n_e, int w, int bs, const void* m_diag, const void* m_upper,
+                       const void* m_lower, const void* bl_diag, const void* bl_upper,
+                       const void* bg_diag, const void* bg_upper, const void* x_fwd,
+                       const void* xl_fwd, const void* xg_fwd, void* s_out, void* bl_out,
+                       void* bg_out, void* workspace, size_t workspace_bytes, void* stream);
+/* _middle_sweep (dist.py:388-448): two-sided Schur elimination of blocks
+ * 1..w-2. s_out [4][n_e] = s_aa, s_ab, s_ba, s_bb; bl_out/bg_out [3][n_e] =
+ * b_aa, b_ab, b_bb. status[e] = 1 + i when the Schur block of step i is
+ * singular (0 ok). */
+int negf_dd_middle_sweep(int n_e, int w, int bs, const void* m_diag, const void* m_upper,
+                         const void* m_lower, const void* bl_diag, const void* bl_upper,
+                         const void* bg_diag, const void* bg_upper, void* s_out, void* bl_out,
+                         void* bg_out, int* status, void* workspace, size_t workspace_bytes,
+                         void* stream);
+/* _fold_corner (dist.py:451-473), in place on diagonal block j of the
+ * partition: M_jj -= m_out x_env m_in; B_jj += -(m_out x_env) B_in
+ * - B_out x_env^H m_out^H + m_out xl_env m_out^H. The stored coupling source
+ * block Bc is B_in = Bc, B_out = -Bc^H for the left corner (side 0) and
+ * B_out = Bc, B_in = -Bc^H for the right corner (side 1). Blocks [n_e]. */
+int negf_dd_fold_corner(int n_e, int w, int bs, int j, int side, void* m_diag, void* bl_diag,
+                        void* bg_diag, const void* m_out, const void* m_in, const void* bl_couple,
+                        const void* bg_couple, const void* x_env, const void* xl_env,
+                        const void* xg_env, void* workspace, size_t workspace_bytes, void* stream);
+/* reverse_blocks: block order reversed. Full storage (lower_in != NULL):
+ * upper'[t] = lower[w-2-t], lower'[t] = upper[w-2-t]; lg-compressed
+ * (lower_in == NULL): upper'[t] = -upper[w-2-t]^H. */
+int negf_dd_reverse_chain(int n_e, int w, int bs, const void* diag_in, const void* upper_in,
+                          const void* lower_in, void* diag_out, void* upper_out, void* lower_out,
+                          void* stream);
+
 /* ---- (6) mixing and residual (scba.py:478-481, 1155-1167) ----------------
  * s_k <- (1 - alpha) s_k + alpha r_k elementwise over n complex values, for
  * each non-NULL pair. diag_traces: tr[b][e] = sum_r x[diag_rows[b*bs + r]][e]

@@ -57,29 +57,45 @@ def _inv_batch(s: np.ndarray, step: int) -> np.ndarray:
 # -- RGF selected solve ------------------------------------------------------
 
 
-def rgf_selected(m_diag, m_up, m_lo, b_lg: dict | None = None, symmetrize: bool = False) -> dict:
-    """Selected blocks of X^R = M^-1 and X^lg = M^-1 B^lg M^-dag.
-
-    Restates rgf.py:113-129 (forward_retarded), rgf.py:132-149 (forward_lg),
-    rgf.py:152-183 (rgf_retarded backward), rgf.py:186-229
-    (rgf_lesser_greater backward) and rgf.py:82-88 (symmetrize), vectorised
-    over the energy axis. ``b_lg`` maps kind ('<', '>') to (diag, upper).
-    """
+def rgf_forward(m_diag, m_up, m_lo, b_lg: dict | None = None):
+    """forward_retarded (rgf.py:113-129) and forward_lg (rgf.py:132-149):
+    returns (x_fwd list, {kind: xl_fwd list})."""
     b_lg = b_lg or {}
     n = m_diag.shape[1]
-    # forward retarded: x_i = (M_ii - M_{i,i-1} x_{i-1} M_{i-1,i})^-1
+    # x_i = (M_ii - M_{i,i-1} x_{i-1} M_{i-1,i})^-1
     xf = [None] * n
     for i in range(n):
         s = m_diag[:, i]
         if i > 0:
             s = s - (m_lo[:, i - 1] @ xf[i - 1]) @ m_up[:, i - 1]
         xf[i] = _inv_batch(s, i)
+    xlf = {}
+    for kind, src in b_lg.items():
+        bd, bu = src[0], src[1]
+        xl = [None] * n
+        for i in range(n):
+            b = bd[:, i]
+            if i > 0:
+                a = m_lo[:, i - 1]
+                y = (a @ xf[i - 1]) @ bu[:, i - 1]
+                b = b + (a @ xl[i - 1]) @ _h(a) - (y - _h(y))
+            xl[i] = (xf[i] @ b) @ _h(xf[i])
+        xlf[kind] = xl
+    return xf, xlf
+
+
+def rgf_backward(m_diag, m_up, m_lo, b_lg: dict | None, xf, xlf, x_last=None, xl_last: dict | None = None,
+                 symmetrize: bool = False) -> dict:
+    """rgf_retarded (rgf.py:152-183) and rgf_lesser_greater (rgf.py:186-229)
+    from the forward intermediates; ``x_last`` / ``xl_last`` seed the exact
+    last diagonal blocks (as dist.py:692-697 does)."""
+    b_lg = b_lg or {}
+    n = m_diag.shape[1]
     out = {}
-    # backward retarded
     xr_d = [None] * n
     xr_u = [None] * (n - 1)
     xr_l = [None] * (n - 1)
-    xr_d[n - 1] = xf[n - 1]
+    xr_d[n - 1] = xf[n - 1] if x_last is None else x_last
     for i in range(n - 2, -1, -1):
         t = xf[i] @ m_up[:, i]
         u = t @ xr_d[i + 1]
@@ -91,22 +107,14 @@ def rgf_selected(m_diag, m_up, m_lo, b_lg: dict | None = None, symmetrize: bool 
     out["xr_upper"] = np.stack(xr_u, 1) if n > 1 else np.zeros_like(m_up)
     out["xr_lower"] = np.stack(xr_l, 1) if n > 1 else np.zeros_like(m_up)
     for kind, src in b_lg.items():
-        bd, bu = src[0], src[1]
+        bu = src[1]
         # explicit lower source blocks (FULL-storage sources, e.g. the W
         # system of scba.py:793-796); default: implied -B_{i,i+1}^dag
         bl = src[2] if len(src) > 2 else -_h(bu)
-        # forward lesser/greater
-        xl = [None] * n
-        for i in range(n):
-            b = bd[:, i]
-            if i > 0:
-                a = m_lo[:, i - 1]
-                y = (a @ xf[i - 1]) @ bu[:, i - 1]
-                b = b + (a @ xl[i - 1]) @ _h(a) - (y - _h(y))
-            xl[i] = (xf[i] @ b) @ _h(xf[i])
+        xl = xlf[kind]
         d = [None] * n
         up = [None] * (n - 1)
-        d[n - 1] = xl[n - 1]
+        d[n - 1] = xl[n - 1] if xl_last is None else xl_last[kind]
         for i in range(n - 2, -1, -1):
             x = xf[i]
             t = x @ m_up[:, i]
@@ -123,6 +131,198 @@ def rgf_selected(m_diag, m_up, m_lo, b_lg: dict | None = None, symmetrize: bool 
             dd = 0.5 * (dd - _h(dd))
         out[f"x{kind}_diag"] = dd
         out[f"x{kind}_upper"] = np.stack(up, 1) if n > 1 else np.zeros_like(bu)
+    return out
+
+
+def rgf_selected(m_diag, m_up, m_lo, b_lg: dict | None = None, symmetrize: bool = False) -> dict:
+    """Selected blocks of X^R = M^-1 and X^lg = M^-1 B^lg M^-dag.
+
+    Restates rgf.py:113-129 (forward_retarded), rgf.py:132-149 (forward_lg),
+    rgf.py:152-183 (rgf_retarded backward), rgf.py:186-229
+    (rgf_lesser_greater backward) and rgf.py:82-88 (symmetrize), vectorised
+    over the energy axis. ``b_lg`` maps kind ('<', '>') to (diag, upper).
+    """
+    xf, xlf = rgf_forward(m_diag, m_up, m_lo, b_lg)
+    return rgf_backward(m_diag, m_up, m_lo, b_lg, xf, xlf, symmetrize=symmetrize)
+
+
+# -- spatial domain decomposition (dist.py:69-717), partitions run in turn ----
+
+
+def make_partition_plan(n_blocks: int, p_s: int) -> list[tuple[int, int]]:
+    """dist.py:104-127: balanced contiguous ranges, leftovers to the middles."""
+    if p_s < 1 or (p_s > 1 and n_blocks < 2 * p_s):
+        raise ValueError(f"{n_blocks} blocks cannot feed {p_s} partitions of >= 2 blocks")
+    base, rem = divmod(n_blocks, p_s)
+    widths = [base] * p_s
+    middles = list(range(1, p_s - 1)) or [0]
+    order = middles + [r for r in range(p_s) if r not in middles]
+    for k in range(rem):
+        widths[order[k % len(order)]] += 1
+    ranges, start = [], 0
+    for w in widths:
+        ranges.append((start, start + w - 1))
+        start += w
+    return ranges
+
+
+def reverse_chain(md, mu, ml):
+    """blocks.py reverse_blocks for a full-storage tridiagonal chain."""
+    return md[:, ::-1].copy(), ml[:, ::-1].copy(), mu[:, ::-1].copy()
+
+
+def reverse_lg(bd, bu):
+    """reverse_blocks for lg-compressed sources: B_rev[t, t+1] = B[w-1-t, w-2-t] = -B[w-2-t, w-1-t]^dag."""
+    return bd[:, ::-1].copy(), -_h(bu[:, ::-1])
+
+
+def schur_tail(md, mu, ml, b_lg, xf, xlf):
+    """dist.py:365-385: Schur complement and effective source at the last
+    block after the forward elimination of the blocks before it."""
+    last = md.shape[1] - 1
+    a = ml[:, last - 1]
+    t = a @ xf[last - 1]
+    s = md[:, last] - t @ mu[:, last - 1]
+    b_out = {}
+    for k, (bd, bu) in b_lg.items():
+        y = t @ bu[:, last - 1]
+        b_out[k] = bd[:, last] + (a @ xlf[k][last - 1]) @ _h(a) - (y - _h(y))
+    return s, b_out
+
+
+def middle_sweep(md, mu, ml, b_lg):
+    """dist.py:388-448: two-sided Schur elimination of interior blocks
+    1..w-2; returns the 2x2 corner system and its sources per kind."""
+    w = md.shape[1]
+    kinds = list(b_lg)
+    s_a = md[:, 0]
+    b_a = {k: b_lg[k][0][:, 0] for k in kinds}
+    if w == 2:
+        return {"s_aa": s_a, "s_ab": mu[:, 0], "s_ba": ml[:, 0], "s_bb": md[:, 1], "b_aa": b_a,
+                "b_ab": {k: b_lg[k][1][:, 0] for k in kinds}, "b_bb": {k: b_lg[k][0][:, 1] for k in kinds}}
+    f, f_p, s_i = mu[:, 0], ml[:, 0], md[:, 1]
+    b_ai = {k: b_lg[k][1][:, 0] for k in kinds}
+    b_i = {k: b_lg[k][0][:, 1] for k in kinds}
+    for i in range(1, w - 1):
+        y = _inv_batch(s_i, i)
+        fy = f @ y
+        m_dn, m_up = ml[:, i], mu[:, i]
+        my = m_dn @ y
+        s_a = s_a - fy @ f_p
+        for k in kinds:
+            bd, bu = b_lg[k]
+            ybh = (y @ b_i[k]) @ _h(y)
+            fyb = f @ ybh
+            myb = m_dn @ ybh
+            t1 = my @ bu[:, i]
+            b_a[k] = b_a[k] + fy @ _h(b_ai[k]) - b_ai[k] @ _h(fy) + fyb @ _h(f)
+            b_ai[k] = -(fy @ bu[:, i]) - b_ai[k] @ _h(my) + fyb @ _h(m_dn)
+            b_i[k] = bd[:, i + 1] - t1 + _h(t1) + myb @ _h(m_dn)
+        f, f_p = -(fy @ m_up), -(my @ f_p)
+        s_i = md[:, i + 1] - my @ m_up
+    return {"s_aa": s_a, "s_ab": f, "s_ba": f_p, "s_bb": s_i, "b_aa": b_a, "b_ab": b_ai, "b_bb": b_i}
+
+
+def fold_corner(md, b_lg, j, m_out, m_in, b_out, b_in, x_env, xl_env):
+    """dist.py:451-473 (in place on md and the source diagonals)."""
+    t = m_out @ x_env
+    md[:, j] = md[:, j] - t @ m_in
+    for k, (bd, _bu) in b_lg.items():
+        bd[:, j] = bd[:, j] + (-(t @ b_in[k]) - (b_out[k] @ _h(x_env)) @ _h(m_out) + (m_out @ xl_env[k]) @ _h(m_out))
+
+
+def dd_selected(m_diag, m_up, m_lo, b_lg: dict, ranges) -> dict:
+    """dist_selected_solve (dist.py:622-717) with the partitions of ``ranges``
+    executed one after another: local eliminations (ends: forward sweep +
+    Schur tail, the bottom on the reversed chain; middles: two-sided sweep),
+    the reduced boundary chain (dist.py:486-561), then local recovery (ends:
+    backward sweep seeded with the exact boundary block; middles: corner
+    folds + local selected solve) and assembly (dist.py:587-619)."""
+    p_s = len(ranges)
+    if p_s == 1:
+        return rgf_selected(m_diag, m_up, m_lo, b_lg)
+    n = m_diag.shape[1]
+    kinds = list(b_lg)
+    loc, contribs = [], []
+    for r, (a, b) in enumerate(ranges):
+        if r == 0 or r == p_s - 1:
+            lo_, hi_ = (0, b) if r == 0 else (a, n - 1)
+            md, mu, ml = m_diag[:, lo_:hi_ + 1].copy(), m_up[:, lo_:hi_].copy(), m_lo[:, lo_:hi_].copy()
+            bl = {k: (b_lg[k][0][:, lo_:hi_ + 1].copy(), b_lg[k][1][:, lo_:hi_].copy()) for k in kinds}
+            if r == p_s - 1:
+                md, mu, ml = reverse_chain(md, mu, ml)
+                bl = {k: reverse_lg(*bl[k]) for k in kinds}
+            xf, xlf = rgf_forward(md, mu, ml, bl)
+            contribs.append(schur_tail(md, mu, ml, bl, xf, xlf))
+            loc.append((md, mu, ml, bl, xf, xlf))
+        else:
+            md, mu, ml = m_diag[:, a:b + 1].copy(), m_up[:, a:b].copy(), m_lo[:, a:b].copy()
+            bl = {k: (b_lg[k][0][:, a:b + 1].copy(), b_lg[k][1][:, a:b].copy()) for k in kinds}
+            contribs.append(middle_sweep(md, mu, ml, bl))
+            loc.append((md, mu, ml, bl, None, None))
+    # reduced chain over the boundary nodes
+    nodes = [ranges[0][1]] + [x for a, b in ranges[1:-1] for x in (a, b)] + [ranges[-1][0]]
+    nr = len(nodes)
+    ne, bs = m_diag.shape[0], m_diag.shape[-1]
+    z = lambda k: np.zeros((ne, k, bs, bs), complex)
+    rd, ru, rl = z(nr), z(nr - 1), z(nr - 1)
+    rb = {k: (z(nr), z(nr - 1)) for k in kinds}
+    s_top, b_top = contribs[0]
+    rd[:, 0] = s_top
+    for k in kinds:
+        rb[k][0][:, 0] = b_top[k]
+    for j in range(1, p_s - 1):
+        sw, p0, p1 = contribs[j], 2 * j - 1, 2 * j
+        rd[:, p0], rd[:, p1], ru[:, p0], rl[:, p0] = sw["s_aa"], sw["s_bb"], sw["s_ab"], sw["s_ba"]
+        for k in kinds:
+            rb[k][0][:, p0], rb[k][0][:, p1], rb[k][1][:, p0] = sw["b_aa"][k], sw["b_bb"][k], sw["b_ab"][k]
+    s_bot, b_bot = contribs[-1]
+    rd[:, nr - 1] = s_bot
+    for k in kinds:
+        rb[k][0][:, nr - 1] = b_bot[k]
+    for p0 in range(0, nr - 1, 2):
+        g = nodes[p0]
+        ru[:, p0], rl[:, p0] = m_up[:, g], m_lo[:, g]
+        for k in kinds:
+            rb[k][1][:, p0] = b_lg[k][1][:, g]
+    xf_r, xlf_r = rgf_forward(rd, ru, rl, rb)
+    sol_r = rgf_backward(rd, ru, rl, rb, xf_r, xlf_r)
+    rvd, rvu, rvl = reverse_chain(rd, ru, rl)
+    xf_v, xlf_v = rgf_forward(rvd, rvu, rvl, {k: reverse_lg(*rb[k]) for k in kinds})
+    out = {"xr_diag": np.zeros_like(m_diag), "xr_upper": np.zeros_like(m_up), "xr_lower": np.zeros_like(m_up)}
+    for k in kinds:
+        out[f"x{k}_diag"] = np.zeros_like(m_diag)
+        out[f"x{k}_upper"] = np.zeros_like(m_up)
+    for r, (a, b) in enumerate(ranges):
+        md, mu, ml, bl, xf, xlf = loc[r]
+        w = b - a + 1
+        if r == 0 or r == p_s - 1:
+            node = 0 if r == 0 else nr - 1
+            sol = rgf_backward(md, mu, ml, bl, xf, xlf, x_last=sol_r["xr_diag"][:, node],
+                               xl_last={k: sol_r[f"x{k}_diag"][:, node] for k in kinds})
+            if r == p_s - 1:  # back to global order (dist.py:564-584)
+                sol = {"xr_diag": sol["xr_diag"][:, ::-1], "xr_upper": sol["xr_lower"][:, ::-1],
+                       "xr_lower": sol["xr_upper"][:, ::-1],
+                       **{f"x{k}_diag": sol[f"x{k}_diag"][:, ::-1] for k in kinds},
+                       **{f"x{k}_upper": -_h(sol[f"x{k}_upper"][:, ::-1]) for k in kinds}}
+        else:
+            left, right = 2 * r - 2, nr - 1 - (2 * r + 1)
+            fold_corner(md, bl, 0, m_lo[:, a - 1], m_up[:, a - 1], {k: -_h(b_lg[k][1][:, a - 1]) for k in kinds},
+                        {k: b_lg[k][1][:, a - 1] for k in kinds}, xf_r[left], {k: xlf_r[k][left] for k in kinds})
+            fold_corner(md, bl, w - 1, m_up[:, b], m_lo[:, b], {k: b_lg[k][1][:, b] for k in kinds},
+                        {k: -_h(b_lg[k][1][:, b]) for k in kinds}, xf_v[right], {k: xlf_v[k][right] for k in kinds})
+            sol = rgf_selected(md, mu, ml, bl)
+        out["xr_diag"][:, a:b + 1] = sol["xr_diag"]
+        out["xr_upper"][:, a:b] = sol["xr_upper"]
+        out["xr_lower"][:, a:b] = sol["xr_lower"]
+        for k in kinds:
+            out[f"x{k}_diag"][:, a:b + 1] = sol[f"x{k}_diag"]
+            out[f"x{k}_upper"][:, a:b] = sol[f"x{k}_upper"]
+    for p0 in range(0, nr - 1, 2):  # cross-partition blocks from the reduced solve
+        g = nodes[p0]
+        out["xr_upper"][:, g], out["xr_lower"][:, g] = sol_r["xr_upper"][:, p0], sol_r["xr_lower"][:, p0]
+        for k in kinds:
+            out[f"x{k}_upper"][:, g] = sol_r[f"x{k}_upper"][:, p0]
     return out
 
 

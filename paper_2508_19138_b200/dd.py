@@ -1,0 +1,447 @@
+"""Spatial domain decomposition of the selected solve over GPUs (drop-in for
+negfgw.dist.dist_selected_solve, dist.py:750-784), batched over energies.
+
+The block chain is split into contiguous partitions (make_partition_plan,
+dist.py:104-127), one per rank / GPU:
+
+1. local elimination -- end partitions: forward sweep
+   (negf_rgf_sweeps_batched mode 1; the bottom one on its reversed chain,
+   negf_dd_reverse_chain) and the Schur tail at the boundary block
+   (negf_dd_schur_tail); middles: two-sided sweep (negf_dd_middle_sweep);
+2. the boundary contributions (plus each partition's right coupling blocks)
+   are all-gathered over NCCL and EVERY rank assembles and solves the reduced
+   chain of 2P-2 nodes on its own GPU (dist.py:486-561) -- no root rank, no
+   scatter of environments;
+3. local recovery -- ends: backward sweep seeded with the exact boundary
+   block (mode 2); middles: both corners folded with the connected
+   environments (negf_dd_fold_corner) and a local selected solve.
+
+Outputs stay partition-local (plus the cross-partition blocks at each
+partition's right boundary); the reference's final gather + bcast
+(dist.py:712-717) is only done by the reference-signature wrapper
+``dist_selected_solve``. ``comm=None`` runs all partitions in one process on
+one device (same arithmetic, partition by partition).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import SingularBlockError
+from .rgf import KIND_GREATER, KIND_LESSER, SelectedSolution, raise_on_status, selected_solve_batched
+
+Z = torch.complex128
+_TAG = {KIND_LESSER: "xl", KIND_GREATER: "xg"}
+
+
+class PartitionError(ValueError):
+    """dist.py PartitionError: a plan that cannot tile the chain."""
+
+
+@dataclass(frozen=True)
+class PartitionPlan:
+    """dist.py:69-101: contiguous split of the block chain, one range per rank."""
+
+    n_blocks: int
+    ranges: tuple[tuple[int, int], ...]
+
+    def __post_init__(self) -> None:
+        if not self.ranges:
+            raise PartitionError("plan needs at least one partition")
+        expect = 0
+        for a, b in self.ranges:
+            if a != expect or b < a:
+                raise PartitionError(f"ranges must tile the chain, got {self.ranges}")
+            expect = b + 1
+        if expect != self.n_blocks:
+            raise PartitionError(f"ranges cover {expect} blocks, chain has {self.n_blocks}")
+        if self.p_s > 1 and any(b - a + 1 < 2 for a, b in self.ranges):
+            raise PartitionError(f"every partition needs at least 2 blocks, got {self.ranges}")
+
+    @property
+    def p_s(self) -> int:
+        return len(self.ranges)
+
+    def width(self, rank: int) -> int:
+        a, b = self.ranges[rank]
+        return b - a + 1
+
+    def nodes(self) -> list[int]:
+        """dist.py:476-483: global indices of the reduced-chain nodes."""
+        out = [self.ranges[0][1]]
+        for a, b in self.ranges[1:-1]:
+            out.extend((a, b))
+        out.append(self.ranges[-1][0])
+        return out
+
+
+def make_partition_plan(n_blocks: int, p_s: int) -> PartitionPlan:
+    """dist.py:104-127: balanced split, leftover blocks to the middles first."""
+    if p_s < 1:
+        raise PartitionError(f"p_s must be positive, got {p_s}")
+    if p_s > 1 and n_blocks < 2 * p_s:
+        raise PartitionError(f"{n_blocks} blocks cannot feed {p_s} partitions of >= 2 blocks")
+    base, rem = divmod(n_blocks, p_s)
+    widths = [base] * p_s
+    middles = list(range(1, p_s - 1)) or [0]
+    order = middles + [r for r in range(p_s) if r not in middles]
+    for k in range(rem):
+        widths[order[k % len(order)]] += 1
+    ranges, start = [], 0
+    for w in widths:
+        ranges.append((start, start + w - 1))
+        start += w
+    return PartitionPlan(n_blocks, tuple(ranges))
+
+
+# -- partition-local inputs ------------------------------------------------------
+
+
+@dataclass
+class Partition:
+    """One rank's share: its own stacks (n_e, w, bs, bs) / (n_e, w-1, ...)
+    and the coupling blocks to its neighbours (n_e, bs, bs) -- left:
+    M[a,a-1], M[a-1,a], B[a-1,a]; right: M[b,b+1], M[b+1,b], B[b,b+1]."""
+
+    rank: int
+    a: int
+    b: int
+    md: torch.Tensor
+    mu: torch.Tensor
+    ml: torch.Tensor
+    src: dict  # kind -> (diag, upper)
+    left: tuple | None = None   # (m_out, m_in, {kind: B[a-1,a]})
+    right: tuple | None = None  # (m_out, m_in, {kind: B[b,b+1]})
+
+    @property
+    def w(self) -> int:
+        return self.b - self.a + 1
+
+
+def partition_inputs(md, mu, ml, src: dict, plan: PartitionPlan, rank: int) -> Partition:
+    """Slice rank's partition (+ halo couplings) out of full device stacks."""
+    a, b = plan.ranges[rank]
+    n = plan.n_blocks
+    c = lambda t: t.contiguous()
+    part = Partition(rank, a, b, c(md[:, a:b + 1]), c(mu[:, a:b]), c(ml[:, a:b]),
+                     {k: (c(d[:, a:b + 1]), c(u[:, a:b])) for k, (d, u) in src.items()})
+    if a > 0:
+        part.left = (c(ml[:, a - 1]), c(mu[:, a - 1]), {k: c(u[:, a - 1]) for k, (_d, u) in src.items()})
+    if b < n - 1:
+        part.right = (c(mu[:, b]), c(ml[:, b]), {k: c(u[:, b]) for k, (_d, u) in src.items()})
+    return part
+
+
+# -- native pieces -----------------------------------------------------------------
+
+
+def _ws(n_e: int, bs: int, dev):
+    lib = _lib.load()
+    nbytes = lib.negf_dd_workspace_bytes(n_e, bs)
+    return _lib.workspace(nbytes, dev), nbytes
+
+
+def _reverse(d, u, lo=None):
+    """negf_dd_reverse_chain: full storage when ``lo`` is given, else lg."""
+    lib = _lib.load()
+    n_e, w = d.shape[0], d.shape[1]
+    bs = d.shape[-1]
+    od, ou = torch.empty_like(d), torch.empty_like(u)
+    ol = torch.empty_like(u) if lo is not None else None
+    rc = lib.negf_dd_reverse_chain(n_e, w, bs, d.data_ptr(), u.data_ptr(), _lib.ptr(lo), od.data_ptr(),
+                                   ou.data_ptr(), _lib.ptr(ol), _lib.stream_ptr(d.device))
+    _lib.check(rc, "negf_dd_reverse_chain")
+    return (od, ou, ol) if lo is not None else (od, ou)
+
+
+def _sweeps(mode: int, md, mu, ml, src: dict, out: dict, symmetrize: bool = False, fwd_given: bool = False,
+            status: torch.Tensor | None = None):
+    """negf_rgf_sweeps_batched on device stacks; ``out`` holds xr_*/xl_*/xg_*."""
+    lib = _lib.load()
+    n_e, n, bs = md.shape[0], md.shape[1], md.shape[-1]
+    dev = md.device
+    p = _lib.ptr
+    st = torch.zeros(n_e, dtype=torch.int32, device=dev) if status is None else status
+    nbytes = lib.negf_rgf_workspace_bytes(n_e, n, bs)
+    ws = _lib.workspace(nbytes, dev)
+    bl = src.get(KIND_LESSER, (None, None))
+    bg = src.get(KIND_GREATER, (None, None))
+    rc = lib.negf_rgf_sweeps_batched(
+        mode, 1 if fwd_given else 0, n_e, n, bs, p(md), p(mu), p(ml), p(bl[0]), p(bl[1]), p(bg[0]), p(bg[1]),
+        p(out["xr_diag"]), p(out["xr_upper"]), p(out["xr_lower"]), p(out.get("xl_diag")), p(out.get("xl_upper")),
+        p(out.get("xg_diag")), p(out.get("xg_upper")), 1 if symmetrize else 0, p(st), None, p(ws), nbytes,
+        _lib.stream_ptr(dev))
+    _lib.check(rc, "negf_rgf_sweeps_batched")
+    return st
+
+
+def _alloc(n_e, n, bs, kinds, dev):
+    z = dict(dtype=Z, device=dev)
+    out = {"xr_diag": torch.empty((n_e, n, bs, bs), **z), "xr_upper": torch.empty((n_e, n - 1, bs, bs), **z),
+           "xr_lower": torch.empty((n_e, n - 1, bs, bs), **z)}
+    for k in kinds:
+        out[_TAG[k] + "_diag"] = torch.empty((n_e, n, bs, bs), **z)
+        out[_TAG[k] + "_upper"] = torch.empty((n_e, n - 1, bs, bs), **z)
+    return out
+
+
+# -- the three phases ------------------------------------------------------------------
+
+
+def _n_slots(nk: int) -> int:
+    return 4 + 3 * nk + 2 + nk
+
+
+def _phase1(part: Partition, p_s: int, kinds: list) -> tuple[torch.Tensor, dict]:
+    """Local elimination; returns this rank's payload (slots, n_e, bs, bs) and
+    the state phase 3 needs."""
+    lib = _lib.load()
+    md, n_e, bs, w = part.md, part.md.shape[0], part.md.shape[-1], part.w
+    dev = md.device
+    nk = len(kinds)
+    pay = torch.zeros((_n_slots(nk), n_e, bs, bs), dtype=Z, device=dev)
+    ws, nbytes = _ws(n_e, bs, dev)
+    p = _lib.ptr
+    state: dict = {}
+    if part.rank == 0 or part.rank == p_s - 1:
+        mdl, mul, mll, srcl = part.md, part.mu, part.ml, dict(part.src)
+        if part.rank == p_s - 1:  # bottom: eliminate toward the interior on the reversed chain
+            mdl, mul, mll = _reverse(mdl, mul, mll)
+            srcl = {k: _reverse(*srcl[k]) for k in kinds}
+        out = _alloc(n_e, w, bs, kinds, dev)
+        st = _sweeps(1, mdl, mul, mll, srcl, out)
+        raise_on_status(st)
+        bo = {k: pay[4 + 3 * i] for i, k in enumerate(kinds)}
+        rc = lib.negf_dd_schur_tail(
+            n_e, w, bs, p(mdl), p(mul), p(mll), p(srcl.get(KIND_LESSER, (None,))[0]),
+            p(srcl.get(KIND_LESSER, (None, None))[1]), p(srcl.get(KIND_GREATER, (None,))[0]),
+            p(srcl.get(KIND_GREATER, (None, None))[1]), p(out["xr_diag"]), p(out.get("xl_diag")),
+            p(out.get("xg_diag")), p(pay[0]), p(bo.get(KIND_LESSER)), p(bo.get(KIND_GREATER)), p(ws), nbytes,
+            _lib.stream_ptr(dev))
+        _lib.check(rc, "negf_dd_schur_tail")
+        state.update(chain=(mdl, mul, mll, srcl), out=out)
+    else:
+        st = torch.zeros(n_e, dtype=torch.int32, device=dev)
+        bl = part.src.get(KIND_LESSER, (None, None))
+        bg = part.src.get(KIND_GREATER, (None, None))
+        i_l = kinds.index(KIND_LESSER) if KIND_LESSER in kinds else None
+        i_g = kinds.index(KIND_GREATER) if KIND_GREATER in kinds else None
+        rc = lib.negf_dd_middle_sweep(
+            n_e, w, bs, p(part.md), p(part.mu), p(part.ml), p(bl[0]), p(bl[1]), p(bg[0]), p(bg[1]), p(pay[0]),
+            p(pay[4 + 3 * i_l]) if i_l is not None else None, p(pay[4 + 3 * i_g]) if i_g is not None else None,
+            p(st), p(ws), nbytes, _lib.stream_ptr(dev))
+        _lib.check(rc, "negf_dd_middle_sweep")
+        bad = np.flatnonzero(st.cpu().numpy())
+        if bad.size:
+            raise SingularBlockError(f"singular Schur complement at middle sweep step {int(st[bad[0]]) - 1}")
+    if part.right is not None:  # couplings to the next partition (reduced-chain cross blocks)
+        m_out, m_in, bc = part.right
+        pay[4 + 3 * nk].copy_(m_out)
+        pay[5 + 3 * nk].copy_(m_in)
+        for i, k in enumerate(kinds):
+            pay[6 + 3 * nk + i].copy_(bc[k])
+    return pay, state
+
+
+def _reduced(pays: list, plan: PartitionPlan, kinds: list) -> dict:
+    """dist.py:486-561 on the device: assemble the 2P-2 node chain from the
+    gathered payloads, forward + backward sweeps, reversed forward sweep."""
+    p_s, nk = plan.p_s, len(kinds)
+    n_e, bs = pays[0].shape[1], pays[0].shape[-1]
+    dev = pays[0].device
+    nodes = plan.nodes()
+    nr = len(nodes)
+    z = lambda k: torch.zeros((n_e, k, bs, bs), dtype=Z, device=dev)
+    rd, ru, rl = z(nr), z(nr - 1), z(nr - 1)
+    rb = {k: (z(nr), z(nr - 1)) for k in kinds}
+    for r in range(p_s):
+        pay = pays[r]
+        if r == 0 or r == p_s - 1:
+            node = 0 if r == 0 else nr - 1
+            rd[:, node] = pay[0]
+            for i, k in enumerate(kinds):
+                rb[k][0][:, node] = pay[4 + 3 * i]
+        else:
+            p0, p1 = 2 * r - 1, 2 * r
+            rd[:, p0], ru[:, p0], rl[:, p0], rd[:, p1] = pay[0], pay[1], pay[2], pay[3]
+            for i, k in enumerate(kinds):
+                rb[k][0][:, p0], rb[k][1][:, p0], rb[k][0][:, p1] = pay[4 + 3 * i], pay[5 + 3 * i], pay[6 + 3 * i]
+        if r < p_s - 1:  # cross coupling between node 2r and 2r+1 (the right boundary of r)
+            p0 = 2 * r
+            ru[:, p0], rl[:, p0] = pay[4 + 3 * nk], pay[5 + 3 * nk]
+            for i, k in enumerate(kinds):
+                rb[k][1][:, p0] = pay[6 + 3 * nk + i]
+    out = _alloc(n_e, nr, bs, kinds, dev)
+    raise_on_status(_sweeps(1, rd, ru, rl, rb, out))
+    fwd = {"x": out["xr_diag"].clone(), **{k: out[_TAG[k] + "_diag"].clone() for k in kinds}}
+    raise_on_status(_sweeps(2, rd, ru, rl, rb, out))
+    vd, vu, vl = _reverse(rd, ru, rl)
+    vb = {k: _reverse(*rb[k]) for k in kinds}
+    rev = _alloc(n_e, nr, bs, kinds, dev)
+    raise_on_status(_sweeps(1, vd, vu, vl, vb, rev))
+    return {"sol": out, "fwd": fwd, "rev": rev, "nr": nr}
+
+
+def _phase3(part: Partition, p_s: int, kinds: list, state: dict, red: dict, symmetrize: bool) -> dict:
+    lib = _lib.load()
+    n_e, bs, w = part.md.shape[0], part.md.shape[-1], part.w
+    dev = part.md.device
+    sol_r, nr = red["sol"], red["nr"]
+    if part.rank == 0 or part.rank == p_s - 1:
+        node = 0 if part.rank == 0 else nr - 1
+        mdl, mul, mll, srcl = state["chain"]
+        out = state["out"]
+        out["xr_diag"][:, w - 1] = sol_r["xr_diag"][:, node]
+        for k in kinds:
+            out[_TAG[k] + "_diag"][:, w - 1] = sol_r[_TAG[k] + "_diag"][:, node]
+        raise_on_status(_sweeps(2, mdl, mul, mll, srcl, out, symmetrize=symmetrize))
+        if part.rank == p_s - 1:  # back to global order (dist.py:564-584)
+            d, u, lo = _reverse(out["xr_diag"], out["xr_upper"], out["xr_lower"])
+            res = {"xr_diag": d, "xr_upper": u, "xr_lower": lo}
+            for k in kinds:
+                res[_TAG[k] + "_diag"], res[_TAG[k] + "_upper"] = _reverse(out[_TAG[k] + "_diag"],
+                                                                            out[_TAG[k] + "_upper"])
+            return res
+        return out
+    # middle: fold both connected environments into the corners, then solve locally
+    md, src = part.md.clone(), {k: (d.clone(), u) for k, (d, u) in part.src.items()}
+    ws, nbytes = _ws(n_e, bs, dev)
+    p = _lib.ptr
+    r = part.rank
+    left, right_rev = 2 * r - 2, nr - 1 - (2 * r + 1)
+    envs = ((0, 0, part.left, red["fwd"]["x"][:, left].contiguous(),
+             {k: red["fwd"][k][:, left].contiguous() for k in kinds}),
+            (w - 1, 1, part.right, red["rev"]["xr_diag"][:, right_rev].contiguous(),
+             {k: red["rev"][_TAG[k] + "_diag"][:, right_rev].contiguous() for k in kinds}))
+    for j, side, halo, x_env, xl_env in envs:
+        m_out, m_in, bc = halo
+        rc = lib.negf_dd_fold_corner(
+            n_e, w, bs, j, side, p(md), p(src[KIND_LESSER][0]) if KIND_LESSER in src else None,
+            p(src[KIND_GREATER][0]) if KIND_GREATER in src else None, p(m_out), p(m_in), p(bc.get(KIND_LESSER)),
+            p(bc.get(KIND_GREATER)), p(x_env), p(xl_env.get(KIND_LESSER)), p(xl_env.get(KIND_GREATER)), p(ws),
+            nbytes, _lib.stream_ptr(dev))
+        _lib.check(rc, "negf_dd_fold_corner")
+    return selected_solve_batched(md, part.mu, part.ml, src.get(KIND_LESSER), src.get(KIND_GREATER),
+                                  symmetrize=symmetrize)
+
+
+def _cross(red: dict, plan: PartitionPlan, rank: int, kinds: list) -> dict | None:
+    """Cross-partition blocks at rank's right boundary from the reduced solve."""
+    if rank >= plan.p_s - 1:
+        return None
+    p0 = 2 * rank
+    sol = red["sol"]
+    out = {"xr_upper": sol["xr_upper"][:, p0].clone(), "xr_lower": sol["xr_lower"][:, p0].clone()}
+    for k in kinds:
+        out[_TAG[k] + "_upper"] = sol[_TAG[k] + "_upper"][:, p0].clone()
+    return out
+
+
+# -- drivers -----------------------------------------------------------------------------
+
+
+def dd_selected_solve_batched(part: Partition, plan: PartitionPlan, group=None, symmetrize: bool = False,
+                              kinds: list | None = None) -> tuple[dict, dict | None]:
+    """One rank of the distributed solve (torch.distributed, one GPU per
+    partition; rank = partition index). Returns (local selected blocks,
+    cross blocks at the right boundary or None)."""
+    import torch.distributed as dist
+
+    kinds = kinds if kinds is not None else [k for k in (KIND_LESSER, KIND_GREATER) if k in part.src]
+    p_s = plan.p_s
+    pay, state = _phase1(part, p_s, kinds)
+    flat = torch.view_as_real(pay).reshape(-1)
+    gathered = torch.empty(p_s * flat.numel(), dtype=flat.dtype, device=flat.device)
+    dist.all_gather_into_tensor(gathered, flat, group=group)
+    pays = [torch.view_as_complex(x.view(-1, 2)).view(pay.shape) for x in gathered.chunk(p_s)]
+    red = _reduced(pays, plan, kinds)
+    return _phase3(part, p_s, kinds, state, red, symmetrize), _cross(red, plan, part.rank, kinds)
+
+
+def dd_selected_solve_local(md, mu, ml, src: dict, plan: PartitionPlan, symmetrize: bool = False) -> dict:
+    """All partitions in this process on one device (same arithmetic as the
+    distributed solve); returns full stacks in global block order."""
+    kinds = [k for k in (KIND_LESSER, KIND_GREATER) if k in src]
+    p_s = plan.p_s
+    if p_s == 1:
+        return selected_solve_batched(md, mu, ml, src.get(KIND_LESSER), src.get(KIND_GREATER), symmetrize=symmetrize)
+    parts = [partition_inputs(md, mu, ml, src, plan, r) for r in range(p_s)]
+    ph1 = [_phase1(p, p_s, kinds) for p in parts]
+    red = _reduced([x[0] for x in ph1], plan, kinds)
+    locs = [_phase3(parts[r], p_s, kinds, ph1[r][1], red, symmetrize) for r in range(p_s)]
+    crosses = [_cross(red, plan, r, kinds) for r in range(p_s)]
+    return assemble(locs, crosses, plan, kinds)
+
+
+def assemble(locs: list, crosses: list, plan: PartitionPlan, kinds: list) -> dict:
+    """dist.py:587-619: partition blocks + cross blocks into full stacks."""
+    n = plan.n_blocks
+    n_e, bs = locs[0]["xr_diag"].shape[0], locs[0]["xr_diag"].shape[-1]
+    dev = locs[0]["xr_diag"].device
+    out = _alloc(n_e, n, bs, kinds, dev)
+    for (a, b), loc, cr in zip(plan.ranges, locs, crosses):
+        out["xr_diag"][:, a:b + 1] = loc["xr_diag"]
+        out["xr_upper"][:, a:b] = loc["xr_upper"]
+        out["xr_lower"][:, a:b] = loc["xr_lower"]
+        for k in kinds:
+            out[_TAG[k] + "_diag"][:, a:b + 1] = loc[_TAG[k] + "_diag"]
+            out[_TAG[k] + "_upper"][:, a:b] = loc[_TAG[k] + "_upper"]
+        if cr is not None:
+            for key, v in cr.items():
+                out[key][:, b] = v
+    return out
+
+
+def dist_selected_solve(m_tilde, b_lesser=None, b_greater=None, plan: PartitionPlan | None = None, comm=None,
+                        device="cuda"):
+    """dist.py:750-784 signature. ``comm``: a dist.Comm (torch.distributed,
+    one GPU per rank) or None (all partitions in this process). Every rank
+    returns the complete SelectedSolution (gathered like the reference) and
+    a stats dict."""
+    import time
+
+    from .blocks import lg_arrays, to_device, tridiag_arrays
+
+    dev = torch.device(device)
+    size = comm.size if comm is not None else 1
+    if plan is None:
+        plan = make_partition_plan(m_tilde.n_blocks, size)
+    if plan.n_blocks != m_tilde.n_blocks:
+        raise PartitionError(f"plan covers {plan.n_blocks} blocks, matrix has {m_tilde.n_blocks}")
+    if comm is not None and comm.size > 1 and plan.p_s != comm.size:
+        raise PartitionError(f"plan has {plan.p_s} partitions but communicator has {comm.size} ranks")
+    if m_tilde.block_bandwidth > 3:
+        raise PartitionError(f"solver expects a block-tridiagonal system, bandwidth {m_tilde.block_bandwidth}")
+    d, u, lo = tridiag_arrays(m_tilde)
+    md, mu, ml = (to_device(x[None], dev) for x in (d, u, lo))
+    src = {}
+    for k, b in ((KIND_LESSER, b_lesser), (KIND_GREATER, b_greater)):
+        if b is not None:
+            bd, bu = lg_arrays(b)
+            src[k] = (to_device(bd[None], dev), to_device(bu[None], dev))
+    kinds = list(src)
+    t0 = time.perf_counter()
+    if comm is None or comm.size == 1:
+        full = dd_selected_solve_local(md, mu, ml, src, plan)
+    else:
+        import torch.distributed as dist
+
+        part = partition_inputs(md, mu, ml, src, plan, comm.rank)
+        loc, cr = dd_selected_solve_batched(part, plan, comm.group, kinds=kinds)
+        objs = [None] * comm.size
+        dist.all_gather_object(objs, ({k: v.cpu() for k, v in loc.items()},
+                                      None if cr is None else {k: v.cpu() for k, v in cr.items()}), group=comm.group)
+        full = assemble([{k: v.to(dev) for k, v in o[0].items()} for o in objs],
+                        [None if o[1] is None else {k: v.to(dev) for k, v in o[1].items()} for o in objs], plan, kinds)
+    wall = time.perf_counter() - t0
+    n, bs = m_tilde.n_blocks, m_tilde.block_size
+    h = {k: v[0].cpu().numpy() for k, v in full.items()}
+    sol = SelectedSolution(n, bs, list(h["xr_diag"]), list(h["xr_upper"]), list(h["xr_lower"]))
+    for k in kinds:
+        sol.x_lg_diag[k] = list(h[_TAG[k] + "_diag"])
+        sol.x_lg_upper[k] = list(h[_TAG[k] + "_upper"])
+    return sol, {"plan": plan, "wall": wall}

@@ -253,6 +253,34 @@ def make_memo():
     np.savez_compressed(OUT / "golden_scba_memo_c1.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
 
 
+def make_dd():
+    """dist_selected_solve (dist.py:750-784) run by the reference itself over
+    spmd_run thread ranks: partition plans, full solutions and the
+    sequential selected_solve of the same systems."""
+    from negfgw import dist
+
+    out = {}
+    cases = [(11, 8, 5, 2), (12, 9, 4, 3), (13, 12, 6, 4), (14, 10, 3, 4), (15, 7, 8, 3)]
+    out["n_cases"] = np.array(len(cases))
+    for c, (seed, nb, bs, p_s) in enumerate(cases):
+        m, bl, bg = toys.random_bt_system(seed, n_blocks=nb, block_size=bs)
+        plan = dist.make_partition_plan(nb, p_s)
+
+        def body(comm):
+            return dist.dist_selected_solve(m, bl, bg, plan=plan, comm=comm)
+
+        sol, _ = dist.spmd_run(body, p_s)[0]
+        p = f"c{c}_"
+        out[p + "cfg"] = np.array([seed, nb, bs, p_s])
+        out[p + "ranges"] = np.array(plan.ranges)
+        out[p + "m_diag"], out[p + "m_upper"], out[p + "m_lower"] = stack_bt(m)
+        for tag, b in (("l", bl), ("g", bg)):
+            out[p + f"b{tag}_diag"] = np.stack([b.get_block(i, i) for i in range(nb)])
+            out[p + f"b{tag}_upper"] = np.stack([b.get_block(i, i + 1) for i in range(nb - 1)])
+        sol_arrays(sol, p, out)
+    np.savez_compressed(OUT / "golden_dd.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rgf", "obc", "conv", "scba"]
     for w in which:

@@ -211,3 +211,24 @@ def test_oracle_scba_memoizer_matches_reference(golden):
         if k.startswith(("ver_", "config", "cache_stats")):
             continue
         assert rel(res[k], g[k]) < 1e-9, k
+
+
+@pytest.mark.parametrize("c", range(5))
+def test_oracle_dd_matches_reference_dist_selected_solve(golden, c):
+    """dist_selected_solve (dist.py:750) run by the reference over spmd_run
+    ranks vs the oracle's partition-by-partition restatement; plans equal."""
+    g = golden("golden_dd.npz")
+    p = f"c{c}_"
+    seed, nb, bs, p_s = (int(x) for x in g[p + "cfg"])
+    ranges = orc.make_partition_plan(nb, p_s)
+    assert [tuple(r) for r in g[p + "ranges"].tolist()] == ranges
+    m = (g[p + "m_diag"][None], g[p + "m_upper"][None], g[p + "m_lower"][None])
+    b = {"<": (g[p + "bl_diag"][None], g[p + "bl_upper"][None]),
+         ">": (g[p + "bg_diag"][None], g[p + "bg_upper"][None])}
+    out = orc.dd_selected(*m, b, ranges)
+    for key, ref in (("xr_diag", "xr_diag"), ("xr_upper", "xr_upper"), ("xr_lower", "xr_lower"),
+                     ("x<_diag", "xl_diag"), ("x<_upper", "xl_upper"), ("x>_diag", "xg_diag"),
+                     ("x>_upper", "xg_upper")):
+        assert rel(out[key][0], g[p + ref]) < 1e-12, key
+    seq = orc.rgf_selected(*m, b)
+    assert rel(out["x<_diag"], seq["x<_diag"]) < 1e-10
