@@ -42,9 +42,9 @@ def _worker(rank, world, port, n_entries, n_e, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_entries,n_e", [(37, 11), (8, 2), (101, 64)])
-def test_alltoall_transposes_world2(n_entries, n_e):
-    world = 2
+@pytest.mark.parametrize("world,n_entries,n_e", [(2, 37, 11), (2, 8, 2), (2, 101, 64), (3, 37, 11), (4, 101, 64),
+                                                 (4, 23808 // 16, 128)])
+def test_alltoall_transposes(world, n_entries, n_e):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
@@ -57,7 +57,7 @@ def test_alltoall_transposes_world2(n_entries, n_e):
         assert p.exitcode == 0
     for rank, ok1, ok2, red, moved in res:
         assert ok1 and ok2, rank
-        assert red == [1.0, 0.0]
+        assert red == [float(world - 1), 0.0]
         assert moved > 0
 
 
