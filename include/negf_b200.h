@@ -27,7 +27,8 @@ int negf_abi_version(void);
 /* Complex block-product algorithm of the DMMA GEMM (process-wide):
  * 0 = 4 real products per complex product,
  * 1 = 3M/Gauss (3 real products, 64x64 tiles), 2 = 3M with 64x32 tiles (default),
- * 3 = 4M with 64x32 tiles, 4 = 3M with 32x64 tiles.
+ * 3 = 4M with 64x32 tiles, 4 = 3M with 32x64 tiles, 5 = 3M 64x32 with BK=8 padded
+ * tiles, 6 = 3M BK=32; +10 selects swizzled BK=16 row-mapped inversion sweeps.
  * 3M trades ~25% of the FP64 tensor work for a normwise error bound that is
  * still O(eps |A||B|). */
 int negf_set_gemm_algo(int algo);
@@ -48,7 +49,9 @@ int negf_set_rgf_overlap(int on);
  * kind (its outputs are then not touched).
  * status[n_e] (device int): 0, or 1 + forward step of the first singular
  * Schur complement (rgf.py:121-126 SingularBlockError). u_spread[n_e][n_b]
- * (device double, may be NULL): LU pivot spread per step (rgf.py:44-49).  */
+ * (device double, may be NULL): LU pivot spread per step (rgf.py:44-49).
+ * Block size bs <= 512 (the pivoted inverse's register panel is one CTA;
+ * larger blocks return -5). */
 size_t negf_rgf_workspace_bytes(int n_e, int n_b, int bs);
 int negf_rgf_selected_solve_batched(
     int n_e, int n_b, int bs,

@@ -118,9 +118,13 @@ def exported_symbols() -> list[str]:
     return list(_SIGNATURES)
 
 
+_CODES = {-1: "invalid argument", -2: "unsupported leading dimension", -4: "workspace too small",
+          -5: "block size above 512 (the pivoted inverse's register panel is one CTA)"}
+
+
 def check(rc: int, what: str) -> None:
     if rc != 0:
-        raise NativeLibraryError(f"{what} failed with code {rc}")
+        raise NativeLibraryError(f"{what} failed with code {rc} ({_CODES.get(rc, 'CUDA error')})")
 
 
 def ptr(t: torch.Tensor | None) -> int | None:

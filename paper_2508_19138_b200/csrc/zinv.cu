@@ -437,7 +437,7 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
   if (lds != n || ldx != n) return -2;  // blocked path works on packed matrices
   const int nb = zinv_panel_width(n);
   if (ws_bytes < zinv_workspace_bytes(n, batch)) return -4;
-  if (n * (nb / 16) > 1024 || n > 1024) return -5;
+  if (n * (nb / 16) > 512 || n > 512) return -5;  // register panel: one CTA of <= 512 threads
   // carve workspace
   char* w = reinterpret_cast<char*>(ws);
   auto take = [&](size_t bytes) { char* r = w; w += (bytes + 255) & ~size_t(255); return r; };
