@@ -12,7 +12,10 @@ from pathlib import Path
 
 import torch
 
-_LIB_PATH = Path(__file__).resolve().parent / "libnegf_b200.so"
+import os
+
+# NEGF_B200_LIB: load another build of the library (kernel experiments)
+_LIB_PATH = Path(os.environ.get("NEGF_B200_LIB", Path(__file__).resolve().parent / "libnegf_b200.so"))
 _lib: C.CDLL | None = None
 
 _vp = C.c_void_p

@@ -367,6 +367,10 @@ using CfgMap64 = Cfg<64, 32, 2, 2, 4, 3, true, 8, true>;
 using CfgMap32 = Cfg<32, 64, 2, 2, 4, 3, true, 8, true>;
 using CfgMap64S = Cfg<64, 32, 2, 2, 2, 3, true, 16, true, true>;
 using CfgMap32S = Cfg<32, 64, 2, 2, 2, 3, true, 16, true, true>;
+using CfgMapT = Cfg<32, 32, 2, 2, 2, 5, true, 16, true, true>;   // 16x16 warp tiles, 5 CTAs/SM
+using CfgMapT4 = Cfg<32, 32, 2, 2, 2, 5, false, 16, true, true>; // 4M, 5 CTAs/SM
+using CfgMapU = Cfg<16, 64, 1, 4, 2, 5, true, 16, true, true>;   // 16x16 warp tiles, 16-row CTAs
+using CfgMapV = Cfg<32, 32, 2, 2, 2, 6, true, 16, true, true>;   // 6 CTAs/SM
 // Measured alternatives (C2 carrier batch, energies/s, greater by identity):
 //   algo 2 (64x32, BK16, 2 stages, swizzled) 142.4 | 64x32 BK8 4 stages padded 137.9 |
 //   32x64 BK16 swizzled 140.0 | 64x32 BK32 2 CTA/SM 133.5 | 64x32 BK16 4 CTA/SM (spills) 109.4
@@ -383,11 +387,11 @@ static int g_map_cfg = 0;
 // bound keeps every parity test at the 1e-9 bar.
 static int g_algo = 2;
 int gemm_algo() { return g_algo; }
-// algo >= 10: algo - 10 for the products, swizzled BK = 16 tiles for the
-// row-mapped inversion sweeps (experiment switch)
+// algo = 10 * m + p: product config p, row-mapped inversion-sweep config m
+// (0 = 32x32 tiles, 3M, BK 16, 5 CTAs/SM [default]; 1..5 alternatives)
 void set_gemm_algo(int a) {
-  g_map_cfg = a >= 10 ? 1 : 0;
-  g_algo = a >= 10 ? a - 10 : a;
+  g_map_cfg = a / 10;
+  g_algo = a % 10;
 }
 
 int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
@@ -403,9 +407,15 @@ int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
     mapped |= g.d[i].rowmap_a || g.d[i].rowmap_c || g.d[i].rowmap_d;
     m64 &= g.d[i].M % 64 == 0;
   }
-  if (mapped) {
-    if (g_map_cfg == 1) return m64 ? launch_cfg<CfgMap64S>(g, stream) : launch_cfg<CfgMap32S>(g, stream);
-    return m64 ? launch_cfg<CfgMap64>(g, stream) : launch_cfg<CfgMap32>(g, stream);
+  if (mapped) {  // inversion sweeps (K <= 32): occupancy wins over tile size
+    switch (g_map_cfg) {
+      case 1: return m64 ? launch_cfg<CfgMap64>(g, stream) : launch_cfg<CfgMap32>(g, stream);
+      case 2: return m64 ? launch_cfg<CfgMap64S>(g, stream) : launch_cfg<CfgMap32S>(g, stream);
+      case 3: return launch_cfg<CfgMapT4>(g, stream);
+      case 4: return launch_cfg<CfgMapU>(g, stream);
+      case 5: return launch_cfg<CfgMapV>(g, stream);
+      default: return launch_cfg<CfgMapT>(g, stream);
+    }
   }
   if (mx <= 32) return launch_cfg<CfgSmall>(g, stream);
   int mm = 0;

@@ -47,7 +47,7 @@ def test_zgemm_matches_torch(cuda, m, n, k, op_a, op_b, algo):
 
 
 @pytest.mark.parametrize("n", [1, 2, 5, 32, 63, 64, 96, 128, 256, 512])
-@pytest.mark.parametrize("algo", [2, 12])
+@pytest.mark.parametrize("algo", [2, 12, 22, 32, 42, 52])
 def test_zinv_matches_numpy(cuda, n, algo):
     rng = np.random.default_rng(n)
     batch = 4
