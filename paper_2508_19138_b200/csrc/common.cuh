@@ -26,6 +26,13 @@ __device__ __forceinline__ z_t zmul(z_t a, z_t b) {
   return zmake(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 __device__ __forceinline__ z_t zconj(z_t a) { return zmake(a.x, -a.y); }
+// c + a*b and c - a*b as four FMAs (zadd(c, zmul(a, b)) compiles to six FP64 ops)
+__device__ __forceinline__ z_t zfma(z_t a, z_t b, z_t c) {
+  return zmake(fma(-a.y, b.y, fma(a.x, b.x, c.x)), fma(a.y, b.x, fma(a.x, b.y, c.y)));
+}
+__device__ __forceinline__ z_t zfms(z_t a, z_t b, z_t c) {
+  return zmake(fma(a.y, b.y, fma(-a.x, b.x, c.x)), fma(-a.y, b.x, fma(-a.x, b.y, c.y)));
+}
 __device__ __forceinline__ z_t zscale(double s, z_t a) { return zmake(s * a.x, s * a.y); }
 // 1/a = conj(a) / |a|^2 with a single division (pivots here are far from the
 // overflow range where LAPACK's scaled zladiv matters).

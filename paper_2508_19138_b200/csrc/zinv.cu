@@ -180,6 +180,9 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
     smax = k0 == 0 ? 0.0 : umaxmin[2 * b];
     smin = k0 == 0 ? INFINITY : umaxmin[2 * b + 1];
   }
+#ifdef NEGF_EXP_TIMING
+  long long clk0 = clock64();
+#endif
   // The column loop stays rolled: unrolling it multiplies the code by NB and
   // the kernel then runs out of the instruction cache. Register elements are
   // selected with predicated moves instead of runtime indexing.
@@ -258,7 +261,7 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         const int gc = 16 * h + c;
-        if (gc > j) v[c] = zsub(v[c], zmul(l, prow_s[gc]));
+        if (gc > j) v[c] = zfms(l, prow_s[gc], v[c]);
         else if (gc == j) v[c] = l;
       }
       if (pos == j) pos = bp;  // LAPACK interchange: the row at position j moves to bp
@@ -273,6 +276,10 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
       smin = fmin(smin, m);
     }
   }
+#ifdef NEGF_EXP_TIMING
+  __syncthreads();
+  long long clk1 = clock64();
+#endif
   // pivot rows -> blk (pivot order), positions -> posinv
   if (have) {
     posinv_s[pos] = r;
@@ -286,18 +293,22 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
   if (tid < w) rdiag_s[tid] = zinv(blk[tid * LD + tid]);
   __syncthreads();
 #ifndef NEGF_EXP_SKIP_PINV
+  // Column c of L^-1 is zero above c, so its forward pass starts at k = c;
+  // the second pass of each warp takes the mirrored column (w-1-warp) so every
+  // warp runs the same number of steps.
   if (lane < 32) {
-    for (int c = warp; c < w; c += nw) {
+    for (int pass = 0, c0 = warp; c0 < w; ++pass, c0 += nw) {
+      const int c = pass ? w - 1 - (c0 - nw) : c0;
       z_t y = zmake(lane == c ? 1.0 : 0.0, 0.0);
-      for (int k = 0; k < w; ++k) {
+      for (int k = c; k < w; ++k) {
         const z_t yk = make_double2(__shfl_sync(0xffffffffu, y.x, k), __shfl_sync(0xffffffffu, y.y, k));
-        if (lane > k && lane < w) y = zsub(y, zmul(blk[lane * LD + k], yk));
+        if (lane > k && lane < w) y = zfms(blk[lane * LD + k], yk, y);
       }
       for (int k = w - 1; k >= 0; --k) {
         z_t xk = make_double2(__shfl_sync(0xffffffffu, y.x, k), __shfl_sync(0xffffffffu, y.y, k));
         xk = zmul(xk, rdiag_s[k]);
         if (lane == k) y = xk;
-        if (lane < k) y = zsub(y, zmul(blk[lane * LD + k], xk));
+        if (lane < k) y = zfms(blk[lane * LD + k], xk, y);
       }
       if (lane < w) {
         pinv[(long long)b * w * w + lane * w + c] = y;
@@ -305,6 +316,10 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
       }
     }
   }
+#endif
+#ifdef NEGF_EXP_TIMING
+  __syncthreads();
+  long long clk2 = clock64();
 #endif
   // Row maps of the sweep GEMM over the rows outside K (logical m < n - w):
   // destination row, and the A_old row that lands there after the panel's
@@ -315,22 +330,28 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
     map_src[(long long)b * n + m] = dst < k0 ? dst : k0 + posinv_s[dst - k0];
   }
   __syncthreads();
+#ifdef NEGF_EXP_TIMING
+  long long clk3 = clock64();
+#endif
   // Rows K of A_new: [T | Pinv] with T = Pinv R, R = pivot rows of A_old.
-  // One thread per (column j, block of 16 output rows); R[q][j] streamed from
-  // global (coalesced over j), Pinv broadcast from smem.
+  // One thread per (column j, block of TB output rows); R[q][j] streamed from
+  // global (coalesced over j), Pinv broadcast from smem. TB = 8 keeps the
+  // accumulators + loads in flight inside the 128-register budget of the
+  // 512-thread CTA (16 rows spilled and ran 8x slower).
   z_t* an = Anew + (long long)b * sAn;
   {
-    const int tblocks = (w + 15) / 16;
+    constexpr int TB = 8;
+    const int tblocks = (w + TB - 1) / TB;
     for (int e = tid; e < tblocks * n; e += blockDim.x) {
-      const int j = e % n, t0 = (e / n) * 16;
-      const int t1 = t0 + 16 < w ? t0 + 16 : w;
+      const int j = e % n, t0 = (e / n) * TB;
+      const int t1 = t0 + TB < w ? t0 + TB : w;
       if (j >= k0 && j < k0 + w) {
         for (int t = t0; t < t1; ++t) an[(long long)(k0 + t) * n + j] = pinv_s[t * LD + (j - k0)];
         continue;
       }
-      z_t acc[16];
+      z_t acc[TB];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) acc[u] = make_double2(0.0, 0.0);
+      for (int u = 0; u < TB; ++u) acc[u] = make_double2(0.0, 0.0);
 #ifdef NEGF_EXP_SKIP_T
       if (w < 0)
 #endif
@@ -338,18 +359,27 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
         z_t rq[8];  // 8 independent loads in flight
 #pragma unroll
         for (int qq = 0; qq < 8; ++qq)
+#ifdef NEGF_EXP_T_NOLOAD
+          rq[qq] = make_double2(1.0 + j, q0 + qq);
+#else
           rq[qq] = q0 + qq < w ? a[(long long)(k0 + posinv_s[q0 + qq]) * n + j] : make_double2(0.0, 0.0);
+#endif
 #pragma unroll
         for (int qq = 0; qq < 8; ++qq)
 #pragma unroll
-          for (int u = 0; u < 16; ++u)
-            if (t0 + u < t1) acc[u] = zadd(acc[u], zmul(pinv_s[(t0 + u) * LD + q0 + qq], rq[qq]));
+          for (int u = 0; u < TB; ++u)
+            acc[u] = zfma(pinv_s[(t0 + u) * LD + q0 + qq], rq[qq], acc[u]);
       }
 #pragma unroll
-      for (int u = 0; u < 16; ++u)
+      for (int u = 0; u < TB; ++u)
         if (t0 + u < t1) an[(long long)(k0 + t0 + u) * n + j] = acc[u];
     }
   }
+#ifdef NEGF_EXP_TIMING
+  __syncthreads();
+  if (tid == 0 && b == 0 && k0 == 64)
+    printf("PANELCLK cols %lld pinv %lld maps %lld T %lld\n", clk1 - clk0, clk2 - clk1, clk3 - clk2, clock64() - clk3);
+#endif
   if (tid == 0) {
     umaxmin[2 * b] = smax;
     umaxmin[2 * b + 1] = smin;
