@@ -292,7 +292,6 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
   // Pinv = U^-1 L^-1: warp-parallel substitutions, lane = row, one identity column per pass
   if (tid < w) rdiag_s[tid] = zinv(blk[tid * LD + tid]);
   __syncthreads();
-#ifndef NEGF_EXP_SKIP_PINV
   // Column c of L^-1 is zero above c, so its forward pass starts at k = c;
   // the second pass of each warp takes the mirrored column (w-1-warp) so every
   // warp runs the same number of steps.
@@ -316,7 +315,6 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
       }
     }
   }
-#endif
 #ifdef NEGF_EXP_TIMING
   __syncthreads();
   long long clk2 = clock64();
@@ -352,18 +350,11 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
       z_t acc[TB];
 #pragma unroll
       for (int u = 0; u < TB; ++u) acc[u] = make_double2(0.0, 0.0);
-#ifdef NEGF_EXP_SKIP_T
-      if (w < 0)
-#endif
       for (int q0 = 0; q0 < w; q0 += 8) {
         z_t rq[8];  // 8 independent loads in flight
 #pragma unroll
         for (int qq = 0; qq < 8; ++qq)
-#ifdef NEGF_EXP_T_NOLOAD
-          rq[qq] = make_double2(1.0 + j, q0 + qq);
-#else
           rq[qq] = q0 + qq < w ? a[(long long)(k0 + posinv_s[q0 + qq]) * n + j] : make_double2(0.0, 0.0);
-#endif
 #pragma unroll
         for (int qq = 0; qq < 8; ++qq)
 #pragma unroll
@@ -534,10 +525,8 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
       prob(0, k0, false);
       prob(k0 + wd, n - k0 - wd, false);
       prob(k0, wd, true);
-#ifndef NEGF_EXP_SKIP_SWEEP
       int rc = zgemm_group_launch(grp, stream);
       if (rc) return rc;
-#endif
     }
     z_t* t = cur; cur = nxt; nxt = t;
     long long ts = cs; cs = ns; ns = ts;
