@@ -166,6 +166,15 @@ class ClockSampler:
 # -- native arm ------------------------------------------------------------------
 
 
+def hbm_peak_gbs() -> float:
+    """Measured HBM copy bandwidth (read + write bytes) of this pool's B200s
+    (MEASURED_PEAKS.json, driver-written); else the recipe's fallback."""
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6500.0
+
+
 def fp64_peak_probe(dev) -> float:
     """cuBLAS ZGEMM 4096^3 (torch.matmul complex128): the FP64 roofline
     denominator, measured live (MEASURED_PEAKS.json has no FP64 entry)."""
@@ -415,6 +424,32 @@ def run_scgw(args, dev, world, rank, barrier) -> dict:
     # two iterations; the second (warm buffers, nonzero Sigma) is the timed one
     res = scba_run(h, v, e, w["eta"], contacts, opts, device=dev, keep_g=False, comm=comm, sigma_to_host=False)
     dt = res["iteration_s"][-1]
+    # HBM roofline of the convolution and E<->nnz layout kernels: one more
+    # iteration with the CUDA-event profiler on (algorithmic read+write bytes
+    # per launch recorded by the library) against MEASURED_PEAKS.json's copy
+    # bandwidth
+    import ctypes
+
+    from paper_2508_19138_b200 import _lib
+
+    lib = _lib.load()
+    lib.negf_prof_reset()
+    lib.negf_prof_enable(1)
+    scba_run(h, v, e, w["eta"], contacts, ScbaOptions(max_iter=1, tol=1e-5, batch=min(128, ne_rank)), device=dev,
+             keep_g=False, comm=comm, sigma_to_host=False)
+    torch.cuda.synchronize(dev)
+    lib.negf_prof_enable(0)
+    hbm = {}
+    peak = hbm_peak_gbs()
+    for cls, name, per in ((9, "conv (P and Sigma FFT kernels)", "96 B (P) / 128 B (Sigma) per entry-energy"),
+                           (10, "E<->nnz pack/unpack", "32 B per entry-energy (pack); entries + blocks (unpack)")):
+        c_ms, c_fl, c_by, c_n = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
+        _lib.check(lib.negf_prof_query(cls, ctypes.byref(c_ms), ctypes.byref(c_fl), ctypes.byref(c_by),
+                                       ctypes.byref(c_n)), "negf_prof_query")
+        gbs = c_by.value / (c_ms.value * 1e-3) / 1e9 if c_ms.value > 0 else 0.0
+        hbm[name] = {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                     "launches": c_n.value, "ms": c_ms.value, "algorithmic_bytes": per}
+    lib.negf_prof_reset()
     t = torch.tensor([dt], dtype=torch.float64, device=dev)
     if world > 1:
         import torch.distributed as dist
@@ -429,7 +464,8 @@ def run_scgw(args, dev, world, rank, barrier) -> dict:
             "rgf_tflops_model_GW": flops / dt / 1e12,
             "transpose_bytes_rank0": int(res["transpose_bytes"]),
             "residual": float(res["residuals"][-1]),
-            "obc_memoizer": {"enabled": True, "cache_stats_by_iteration_rank0": res["cache_stats_by_iteration"]}}
+            "obc_memoizer": {"enabled": True, "cache_stats_by_iteration_rank0": res["cache_stats_by_iteration"]},
+            "hbm_roofline": hbm}
 
 
 # -- reference arm -----------------------------------------------------------------

@@ -222,8 +222,9 @@ int negf_observables(int n_e, int n_b, int bs, const void* gr_diag, const void* 
 /* ---- (3) energy convolutions (negfgw/convolve.py) -----------------------
  * Entry-major series: row r of an array is the energy series of one matrix
  * entry, x[r][0..n_e) complex128, rows contiguous (stride n_e).
- * L: power-of-two circular length >= 2 n_e - 1. tw[L/2] = exp(-2 pi i k/L).
- * kf/kcf[L]: spectrum (bit-reversed order) of the causal kernel
+ * L: power-of-two circular length >= max(8, 2 n_e - 1), L <= 4096.
+ * tw[L] = exp(-2 pi i k/L).
+ * kf/kcf[L]: spectrum (natural order) of the causal kernel
  * K = ifft_m(theta), m = scipy next_fast_len(2 n_e) made even, and of conj(K),
  * laid out circularly on L (see paper_2508_19138_b200/conv.py ConvPlan).
  * diag[r] (uint8, may be NULL): 1 for row == col entries, which are projected

@@ -21,15 +21,6 @@ MODE_CORRELATION = "correlation"
 _PLANS: dict[tuple, "ConvPlan"] = {}
 
 
-def _bitrev(L: int) -> np.ndarray:
-    bits = L.bit_length() - 1
-    idx = np.arange(L)
-    out = np.zeros(L, dtype=np.int64)
-    for b in range(bits):
-        out |= ((idx >> b) & 1) << (bits - 1 - b)
-    return out
-
-
 def retarded_padding(n: int) -> int:
     """convolve.py:118-121: m = next_fast_len(2N), forced even."""
     m = next_fast_len(2 * n)
@@ -39,16 +30,18 @@ def retarded_padding(n: int) -> int:
 
 
 class ConvPlan:
-    """Tables for series of length n on a power-of-two circular grid L >= 2n-1."""
+    """Tables for series of length n on a power-of-two circular grid
+    L >= max(8, 2n-1): twiddles exp(-2 pi i k / L), k < L, and the causal
+    kernel spectra in natural order."""
 
     def __init__(self, n: int, device) -> None:
         self.n = n
         self.dev = torch.device(device)
-        L = 2
+        L = 8
         while L < 2 * n - 1:
             L *= 2
         self.L = L
-        k = np.arange(L // 2)
+        k = np.arange(L)
         tw = np.exp(-2j * np.pi * k / L)
         m = retarded_padding(n)
         theta = np.zeros(m)
@@ -59,9 +52,8 @@ class ConvPlan:
         kc[:n] = km[:n]
         if n > 1:
             kc[L - np.arange(1, n)] = km[m - np.arange(1, n)]
-        br = _bitrev(L)
-        kf = np.fft.fft(kc)[br]
-        kcf = np.fft.fft(np.conj(kc))[br]
+        kf = np.fft.fft(kc)
+        kcf = np.fft.fft(np.conj(kc))
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.complex128)).to(self.dev)
         self.tw, self.kf, self.kcf = t(tw), t(kf), t(kcf)
 

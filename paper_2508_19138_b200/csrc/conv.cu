@@ -14,11 +14,11 @@
 // lags |n| < N, whose spectrum on the L grid (kf, and kcf for conj(K)) is
 // precomputed once per N on the host.
 //
-// One CTA owns one entry row: the series live in shared memory (2 x L
-// complex), forward transforms are in-place radix-2 decimation-in-frequency
-// (natural -> bit-reversed), pointwise products happen in bit-reversed order,
-// inverse transforms are decimation-in-time (bit-reversed -> natural), so no
-// permutation pass is ever needed. Polarization uses
+// One CTA of L/8 threads owns one entry row (HBM traffic: one read of the
+// input series, one write of the outputs): radix-8 Stockham transforms with
+// the data in registers and padded shared memory only between passes (see
+// the row FFT engine below); spectra stay in natural order, so pointwise
+// products and the next transform need no permutation. Polarization uses
 //   P^<_hat = G^<_hat * (-conj G^>_hat)   and   P^>[k] = conj(p^<[-k]),
 // i.e. one inverse transform yields both P^< and P^>.
 #include "../../include/negf_b200.h"
@@ -28,53 +28,160 @@
 namespace negf {
 namespace {
 
-__device__ __forceinline__ void fft_dif(z_t* x, int L, const z_t* __restrict__ tw) {
-  for (int h = L >> 1, ts = 1; h >= 1; h >>= 1, ts <<= 1) {
-    for (int j = threadIdx.x; j < (L >> 1); j += blockDim.x) {
-      const int pos = j & (h - 1);
-      const int i0 = ((j - pos) << 1) + pos, i1 = i0 + h;
-      const z_t a = x[i0], b = x[i1];
-      x[i0] = zadd(a, b);
-      x[i1] = zmul(zsub(a, b), __ldg(&tw[pos * ts]));
-    }
-    __syncthreads();
-  }
+// ---------------------------------------------------------------------------
+// Row FFT engine: radix-8 Stockham (auto-sort) passes with the data of a
+// pass held in registers, shared memory only for the exchange between
+// passes. A CTA of L/8 threads owns one row; thread t holds the 8 elements
+// at positions t + s*L/8 (s = 0..7). Every pass READS exactly those
+// positions, and the last pass WRITES them (Stockham with Ns*R = L), so the
+// spectrum left in registers by a forward transform is where the pointwise
+// products and the next inverse transform expect it: consecutive transforms
+// never round-trip through shared memory. log2(L) = 3 p8 + (log2 Rs): the
+// small radix Rs in {2, 4} runs first in forward and last in inverse
+// transforms (the same positions rule holds for it). Shared indices are
+// padded by one element per 8 (conflict-free 16-byte accesses).
+
+__device__ __forceinline__ int pidx(int i) { return i + (i >> 3); }
+
+template <bool INV>
+__device__ __forceinline__ z_t rot(z_t a) {  // * (-i) forward, * (+i) inverse
+  return INV ? zmake(-a.y, a.x) : zmake(a.y, -a.x);
 }
 
-__device__ __forceinline__ void fft_dif2(z_t* x, z_t* y, int L, const z_t* __restrict__ tw) {
-  for (int h = L >> 1, ts = 1; h >= 1; h >>= 1, ts <<= 1) {
-    for (int j = threadIdx.x; j < (L >> 1); j += blockDim.x) {
-      const int pos = j & (h - 1);
-      const int i0 = ((j - pos) << 1) + pos, i1 = i0 + h;
-      const z_t w = __ldg(&tw[pos * ts]);
-      z_t a = x[i0], b = x[i1];
-      x[i0] = zadd(a, b);
-      x[i1] = zmul(zsub(a, b), w);
-      a = y[i0]; b = y[i1];
-      y[i0] = zadd(a, b);
-      y[i1] = zmul(zsub(a, b), w);
-    }
-    __syncthreads();
-  }
+template <bool INV>
+__device__ __forceinline__ void dft2(z_t& a, z_t& b) {
+  const z_t t = a;
+  a = zadd(t, b);
+  b = zsub(t, b);
 }
 
-// unscaled inverse: bit-reversed -> natural
-__device__ __forceinline__ void ifft_dit2(z_t* x, z_t* y, int L, const z_t* __restrict__ tw) {
-  for (int h = 1, ts = L >> 1; h < L; h <<= 1, ts >>= 1) {
-    for (int j = threadIdx.x; j < (L >> 1); j += blockDim.x) {
-      const int pos = j & (h - 1);
-      const int i0 = ((j - pos) << 1) + pos, i1 = i0 + h;
-      const z_t w = zconj(__ldg(&tw[pos * ts]));
-      z_t a = x[i0], t = zmul(x[i1], w);
-      x[i0] = zadd(a, t);
-      x[i1] = zsub(a, t);
-      if (y) {
-        a = y[i0]; t = zmul(y[i1], w);
-        y[i0] = zadd(a, t);
-        y[i1] = zsub(a, t);
+template <bool INV>
+__device__ __forceinline__ void dft4(z_t& v0, z_t& v1, z_t& v2, z_t& v3) {
+  const z_t t0 = zadd(v0, v2), t1 = zsub(v0, v2), t2 = zadd(v1, v3), t3 = rot<INV>(zsub(v1, v3));
+  v0 = zadd(t0, t2);
+  v1 = zadd(t1, t3);
+  v2 = zsub(t0, t2);
+  v3 = zsub(t1, t3);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft8(z_t* v) {
+  z_t e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+  z_t o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+  dft4<INV>(e0, e1, e2, e3);
+  dft4<INV>(o0, o1, o2, o3);
+  const double h = 0.70710678118654752440;
+  // o1 *= W8, o2 *= W8^2, o3 *= W8^3 with W8 = exp(-/+ i pi/4)
+  o1 = INV ? zmake(h * (o1.x - o1.y), h * (o1.x + o1.y)) : zmake(h * (o1.x + o1.y), h * (o1.y - o1.x));
+  o2 = rot<INV>(o2);
+  o3 = INV ? zmake(-h * (o3.x + o3.y), h * (o3.x - o3.y)) : zmake(h * (o3.y - o3.x), -h * (o3.x + o3.y));
+  v[0] = zadd(e0, o0); v[4] = zsub(e0, o0);
+  v[1] = zadd(e1, o1); v[5] = zsub(e1, o1);
+  v[2] = zadd(e2, o2); v[6] = zsub(e2, o2);
+  v[3] = zadd(e3, o3); v[7] = zsub(e3, o3);
+}
+
+struct RowGeom {
+  int L, Q;    // Q = L/8 threads carry data
+  int p8, rs;  // radix-8 passes, small radix (0, 2 or 4)
+  int t;
+  bool act;
+};
+
+__device__ __forceinline__ RowGeom row_geom(int L) {
+  RowGeom g;
+  g.L = L;
+  g.Q = L >> 3;
+  const int m = 31 - __clz(L);
+  g.p8 = m / 3;
+  g.rs = (m % 3) ? (1 << (m % 3)) : 0;
+  g.t = threadIdx.x;
+  g.act = g.t < g.Q;
+  return g;
+}
+
+// One Stockham pass of radix R on NA arrays held in registers (in place).
+// R is a template parameter so every register index is static.
+template <bool INV, int NA, int R>
+__device__ __forceinline__ void pass_compute(z_t (*v)[8], const RowGeom& g, int Ns, const z_t* __restrict__ tw) {
+  constexpr int NB = 8 / R;  // butterflies per thread; element r of butterfly u in slot u + r*NB
+#pragma unroll
+  for (int u = 0; u < NB; ++u) {
+    const int j = g.t + u * g.Q, k = j & (Ns - 1);
+    if (Ns > 1) {
+      // one table twiddle per butterfly, its powers by multiplication (the
+      // L1/shared pipe, not FP64, bounds these kernels)
+      const int step = k * (g.L / (Ns * R));
+      z_t w1 = __ldg(&tw[step]);
+      if (INV) w1 = zconj(w1);
+      z_t w = w1;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        if (r > 1) w = zmul(w, w1);
+#pragma unroll
+        for (int a = 0; a < NA; ++a) v[a][u + r * NB] = zmul(v[a][u + r * NB], w);
       }
     }
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      if constexpr (R == 8) dft8<INV>(v[a]);
+      else if constexpr (R == 4) dft4<INV>(v[a][u], v[a][u + 2], v[a][u + 4], v[a][u + 6]);
+      else dft2<INV>(v[a][u], v[a][u + 4]);
+    }
+  }
+}
+
+template <int NA, int R>
+__device__ __forceinline__ void pass_store(z_t (*v)[8], z_t* const* sm, const RowGeom& g, int Ns) {
+  constexpr int NB = 8 / R;
+#pragma unroll
+  for (int u = 0; u < NB; ++u) {
+    const int j = g.t + u * g.Q, k = j & (Ns - 1);
+    const int base = (j - k) * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int a = 0; a < NA; ++a) sm[a][pidx(base + r * Ns)] = v[a][u + r * NB];
+  }
+}
+
+template <bool INV, int NA, int R>
+__device__ __forceinline__ void fft_pass(z_t (*v)[8], z_t* const* sm, const RowGeom& g, int Ns,
+                                         const z_t* __restrict__ tw, bool load, bool store) {
+  if (load) {
+    if (g.act) {
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+#pragma unroll
+        for (int a = 0; a < NA; ++a) v[a][s] = sm[a][pidx(g.t + s * g.Q)];
+    }
     __syncthreads();
+  }
+  if (g.act) pass_compute<INV, NA, R>(v, g, Ns, tw);
+  if (store) {
+    if (g.act) pass_store<NA, R>(v, sm, g, Ns);
+    __syncthreads();
+  }
+}
+
+// Forward (INV = false) or unscaled inverse transform of NA rows in registers.
+template <bool INV, int NA>
+__device__ void fft_rows(z_t (*v)[8], z_t* const* sm, const RowGeom& g, const z_t* __restrict__ tw) {
+  const int npass = g.p8 + (g.rs ? 1 : 0);
+  int Ns = 1;
+  for (int p = 0; p < npass; ++p) {
+    const bool small = g.rs && (INV ? p == npass - 1 : p == 0);
+    const bool load = p > 0, store = p != npass - 1;
+    if (!small) {
+      fft_pass<INV, NA, 8>(v, sm, g, Ns, tw, load, store);
+      Ns *= 8;
+    } else if (g.rs == 4) {
+      fft_pass<INV, NA, 4>(v, sm, g, Ns, tw, load, store);
+      Ns *= 4;
+    } else {
+      fft_pass<INV, NA, 2>(v, sm, g, Ns, tw, load, store);
+      Ns *= 2;
+    }
   }
 }
 
@@ -83,149 +190,203 @@ __device__ __forceinline__ z_t proj(z_t v, bool diag) {
   return diag ? make_double2(0.0, v.y) : v;
 }
 
-// d = x^> - x^< (length n, zero padded in smem B) -> r_up = K*d, r_lo = -conj(conj(K)*d)
-__device__ __forceinline__ void retarded_tail(z_t* A, z_t* B, int n, int L, const z_t* tw,
-                                              const z_t* kf, const z_t* kcf, z_t* r_up, z_t* r_lo) {
-  fft_dif(B, L, tw);
-  for (int q = threadIdx.x; q < L; q += blockDim.x) {
-    const z_t d = B[q];
-    A[q] = zmul(d, __ldg(&kf[q]));
-    B[q] = zmul(d, __ldg(&kcf[q]));
+// d (registers, natural positions) -> r_up = K*d, r_lo = -conj(conj(K)*d)
+__device__ void retarded_tail(z_t* d, z_t* A, z_t* B, const RowGeom& g, int n, const z_t* tw, const z_t* kf,
+                              const z_t* kcf, z_t* r_up, z_t* r_lo) {
+  z_t* sB[1] = {B};
+  z_t dv[1][8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) dv[0][s] = d[s];
+  fft_rows<false, 1>(dv, sB, g, tw);
+  z_t xy[2][8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int q = g.t + s * g.Q;
+    xy[0][s] = g.act ? zmul(dv[0][s], __ldg(&kf[q])) : make_double2(0.0, 0.0);
+    xy[1][s] = g.act && kcf ? zmul(dv[0][s], __ldg(&kcf[q])) : make_double2(0.0, 0.0);
   }
-  __syncthreads();
-  ifft_dit2(A, B, L, tw);
-  const double inv = 1.0 / L;
-  for (int k = threadIdx.x; k < n; k += blockDim.x) {
-    if (r_up) r_up[k] = zscale(inv, A[k]);
-    if (r_lo) r_lo[k] = zscale(-inv, zconj(B[k]));
+  z_t* sAB[2] = {A, B};
+  fft_rows<true, 2>(xy, sAB, g, tw);
+  const double inv = 1.0 / g.L;
+  if (g.act) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int k = g.t + s * g.Q;
+      if (k < n) {
+        if (r_up) r_up[k] = zscale(inv, xy[0][s]);
+        if (r_lo) r_lo[k] = zscale(-inv, zconj(xy[1][s]));
+      }
+    }
   }
 }
 
-__global__ void pol_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg, int n, int L,
-                           const z_t* __restrict__ tw, const z_t* __restrict__ kf,
-                           const z_t* __restrict__ kcf, const unsigned char* __restrict__ diag,
-                           double2 scale, z_t* pl, z_t* pg, z_t* pr_up, z_t* pr_lo) {
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT) pol_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg, int n,
+                                                  int L, const z_t* __restrict__ tw, const z_t* __restrict__ kf,
+                                                  const z_t* __restrict__ kcf,
+                                                  const unsigned char* __restrict__ diag, double2 scale, z_t* pl,
+                                                  z_t* pg, z_t* pr_up, z_t* pr_lo) {
   extern __shared__ __align__(16) z_t sm[];
   z_t* A = sm;
-  z_t* B = sm + L;
+  z_t* B = sm + pidx(L);
+  const RowGeom g = row_geom(L);
   const long long row = blockIdx.x;
   const long long o = row * n;
   const bool dg = diag && diag[row];
-  for (int k = threadIdx.x; k < L; k += blockDim.x) {
-    A[k] = k < n ? gl[o + k] : make_double2(0.0, 0.0);
-    B[k] = k < n ? gg[o + k] : make_double2(0.0, 0.0);
+  z_t v[2][8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int k = g.t + s * g.Q;
+    const bool in = g.act && k < n;
+    v[0][s] = in ? gl[o + k] : make_double2(0.0, 0.0);
+    v[1][s] = in ? gg[o + k] : make_double2(0.0, 0.0);
+  }
+  z_t* sAB[2] = {A, B};
+  fft_rows<false, 2>(v, sAB, g, tw);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) v[0][s] = zmul(v[0][s], make_double2(-v[1][s].x, v[1][s].y));  // * (-conj G^>)
+  z_t* sA[1] = {A};
+  fft_rows<true, 1>(v, sA, g, tw);
+  // P^>[k] = conj(p[-k]): exchange p through shared memory
+  if (g.act) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) A[pidx(g.t + s * g.Q)] = v[0][s];
   }
   __syncthreads();
-  fft_dif2(A, B, L, tw);
-  for (int q = threadIdx.x; q < L; q += blockDim.x) {
-    const z_t b = B[q];
-    A[q] = zmul(A[q], make_double2(-b.x, b.y));  // * (-conj b)
-  }
-  __syncthreads();
-  ifft_dit2(A, nullptr, L, tw);
-  const z_t s = zscale(1.0 / L, scale);
-  for (int k = threadIdx.x; k < L; k += blockDim.x) {
-    z_t d = make_double2(0.0, 0.0);
-    if (k < n) {
-      const z_t lo = proj(zmul(s, A[k]), dg);
-      const z_t gr = proj(zmul(s, zconj(A[(L - k) & (L - 1)])), dg);
+  const z_t sc = zscale(1.0 / L, scale);
+  z_t d[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int k = g.t + s * g.Q;
+    d[s] = make_double2(0.0, 0.0);
+    if (g.act && k < n) {
+      const z_t lo = proj(zmul(sc, v[0][s]), dg);
+      const z_t gr = proj(zmul(sc, zconj(A[pidx((L - k) & (L - 1))])), dg);
       pl[o + k] = lo;
       pg[o + k] = gr;
-      d = zsub(gr, lo);
+      d[s] = zsub(gr, lo);
     }
-    B[k] = d;
   }
   __syncthreads();
-  retarded_tail(A, B, n, L, tw, kf, kcf, pr_up ? pr_up + o : nullptr, pr_lo ? pr_lo + o : nullptr);
+  retarded_tail(d, A, B, g, n, tw, kf, kcf, pr_up ? pr_up + o : nullptr, pr_lo ? pr_lo + o : nullptr);
 }
 
-__global__ void sigma_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg,
-                             const z_t* __restrict__ wl, const z_t* __restrict__ wg,
-                             const long long* __restrict__ w_rows, int n, int L,
-                             const z_t* __restrict__ tw, const z_t* __restrict__ kf,
-                             const z_t* __restrict__ kcf, const unsigned char* __restrict__ diag,
-                             double2 scale, z_t* sl, z_t* sg, z_t* sr_up, z_t* sr_lo) {
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT) sigma_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg,
+                                                    const z_t* __restrict__ wl, const z_t* __restrict__ wg,
+                                                    const long long* __restrict__ w_rows, int n, int L,
+                                                    const z_t* __restrict__ tw, const z_t* __restrict__ kf,
+                                                    const z_t* __restrict__ kcf,
+                                                    const unsigned char* __restrict__ diag, double2 scale, z_t* sl,
+                                                    z_t* sg, z_t* sr_up, z_t* sr_lo) {
   extern __shared__ __align__(16) z_t sm[];
   z_t* A = sm;
-  z_t* B = sm + L;
+  z_t* B = sm + pidx(L);
+  const RowGeom g = row_geom(L);
   const long long row = blockIdx.x;
   const long long o = row * n;
   const long long ow = (w_rows ? w_rows[row] : row) * n;
   const bool dg = diag && diag[row];
-  const z_t s = zscale(1.0 / L, scale);
+  const z_t sc = zscale(1.0 / L, scale);
+  z_t* sAB[2] = {A, B};
+  z_t* sA[1] = {A};
+  z_t v[2][8];
+#pragma unroll 1
   for (int kind = 0; kind < 2; ++kind) {
-    const z_t* g = kind ? gg : gl;
-    const z_t* w = kind ? wg : wl;
+    const z_t* gx = kind ? gg : gl;
+    const z_t* wx = kind ? wg : wl;
     z_t* out = kind ? sg : sl;
-    for (int k = threadIdx.x; k < L; k += blockDim.x) {
-      A[k] = k < n ? g[o + k] : make_double2(0.0, 0.0);
-      B[k] = k < n ? w[ow + k] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int k = g.t + s * g.Q;
+      const bool in = g.act && k < n;
+      v[0][s] = in ? gx[o + k] : make_double2(0.0, 0.0);
+      v[1][s] = in ? wx[ow + k] : make_double2(0.0, 0.0);
     }
-    __syncthreads();
-    fft_dif2(A, B, L, tw);
-    for (int q = threadIdx.x; q < L; q += blockDim.x) A[q] = zmul(A[q], B[q]);
-    __syncthreads();
-    ifft_dit2(A, nullptr, L, tw);
-    for (int k = threadIdx.x; k < n; k += blockDim.x) out[o + k] = proj(zmul(s, A[k]), dg);
-    __syncthreads();
+    fft_rows<false, 2>(v, sAB, g, tw);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) v[0][s] = zmul(v[0][s], v[1][s]);
+    fft_rows<true, 1>(v, sA, g, tw);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int k = g.t + s * g.Q;
+      // after the second kind, v[1] <- d = Sigma^> - Sigma^<, Sigma^< re-read
+      // from the values this thread wrote itself
+      v[1][s] = make_double2(0.0, 0.0);
+      if (g.act && k < n) {
+        const z_t val = proj(zmul(sc, v[0][s]), dg);
+        out[o + k] = val;
+        if (kind == 1) v[1][s] = zsub(val, sl[o + k]);
+      }
+    }
   }
-  // each thread re-reads only the values it wrote itself
-  for (int k = threadIdx.x; k < L; k += blockDim.x)
-    B[k] = k < n ? zsub(sg[o + k], sl[o + k]) : make_double2(0.0, 0.0);
-  __syncthreads();
-  retarded_tail(A, B, n, L, tw, kf, kcf, sr_up ? sr_up + o : nullptr, sr_lo ? sr_lo + o : nullptr);
+  retarded_tail(v[1], A, B, g, n, tw, kf, kcf, sr_up ? sr_up + o : nullptr, sr_lo ? sr_lo + o : nullptr);
 }
 
 // Generic convolve_energy (convolve.py:39-71): mode 0 convolution, 1 correlation.
-__global__ void conv_kernel(const z_t* __restrict__ x1, const z_t* __restrict__ x2, int n, int L,
-                            int mode, const z_t* __restrict__ tw, double2 scale, z_t* out) {
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT) conv_kernel(const z_t* __restrict__ x1, const z_t* __restrict__ x2, int n,
+                                                   int L, int mode, const z_t* __restrict__ tw, double2 scale,
+                                                   z_t* out) {
   extern __shared__ __align__(16) z_t sm[];
   z_t* A = sm;
-  z_t* B = sm + L;
+  z_t* B = sm + pidx(L);
+  const RowGeom g = row_geom(L);
   const long long o = (long long)blockIdx.x * n;
-  for (int k = threadIdx.x; k < L; k += blockDim.x) {
-    A[k] = k < n ? x1[o + k] : make_double2(0.0, 0.0);
+  z_t v[2][8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int k = g.t + s * g.Q;
+    v[0][s] = g.act && k < n ? x1[o + k] : make_double2(0.0, 0.0);
     // correlation: y[j] = x2[-j] placed circularly
-    z_t v = make_double2(0.0, 0.0);
-    if (mode == 0) {
-      if (k < n) v = x2[o + k];
-    } else {
-      const int j = (L - k) & (L - 1);
-      if (j < n) v = x2[o + j];
-    }
-    B[k] = v;
+    const int j = mode == 0 ? k : ((L - k) & (L - 1));
+    v[1][s] = g.act && j < n ? x2[o + j] : make_double2(0.0, 0.0);
   }
-  __syncthreads();
-  fft_dif2(A, B, L, tw);
-  for (int q = threadIdx.x; q < L; q += blockDim.x) A[q] = zmul(A[q], B[q]);
-  __syncthreads();
-  ifft_dit2(A, nullptr, L, tw);
-  const z_t s = zscale(1.0 / L, scale);
-  for (int k = threadIdx.x; k < n; k += blockDim.x) out[o + k] = zmul(s, A[k]);
+  z_t* sAB[2] = {A, B};
+  fft_rows<false, 2>(v, sAB, g, tw);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) v[0][s] = zmul(v[0][s], v[1][s]);
+  z_t* sA[1] = {A};
+  fft_rows<true, 1>(v, sA, g, tw);
+  const z_t sc = zscale(1.0 / L, scale);
+  if (g.act) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int k = g.t + s * g.Q;
+      if (k < n) out[o + k] = zmul(sc, v[0][s]);
+    }
+  }
 }
 
-__global__ void ret_kernel(const z_t* __restrict__ xl, const z_t* __restrict__ xg, int n, int L,
-                           const z_t* __restrict__ tw, const z_t* __restrict__ kf, z_t* out) {
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT) ret_kernel(const z_t* __restrict__ xl, const z_t* __restrict__ xg, int n,
+                                                  int L, const z_t* __restrict__ tw, const z_t* __restrict__ kf,
+                                                  z_t* out) {
   extern __shared__ __align__(16) z_t sm[];
   z_t* A = sm;
-  z_t* B = sm + L;
+  z_t* B = sm + pidx(L);
+  const RowGeom g = row_geom(L);
   const long long o = (long long)blockIdx.x * n;
-  for (int k = threadIdx.x; k < L; k += blockDim.x)
-    B[k] = k < n ? zsub(xg[o + k], xl[o + k]) : make_double2(0.0, 0.0);
-  __syncthreads();
-  retarded_tail(A, B, n, L, tw, kf, kf, out + o, nullptr);
+  z_t d[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int k = g.t + s * g.Q;
+    d[s] = g.act && k < n ? zsub(xg[o + k], xl[o + k]) : make_double2(0.0, 0.0);
+  }
+  retarded_tail(d, A, B, g, n, tw, kf, nullptr, out + o, nullptr);
 }
 
-int threads_for(int L) { return L >= 512 ? 256 : (L / 2 >= 32 ? L / 2 : 32); }
+int threads_for(int L) { return L / 8 >= 32 ? L / 8 : 32; }
+
+size_t smem_for(int L) { return 2 * (size_t)(L + L / 8) * sizeof(z_t); }
 
 int smem_setup(const void* fn, int L) {
-  size_t need = 2 * (size_t)L * sizeof(z_t);
-  if (need > 200 * 1024) return -5;
+  if (smem_for(L) > 200 * 1024 || L / 8 > 512) return -5;
   NEGF_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   return 0;
 }
 
-bool pow2(int L) { return L >= 2 && (L & (L - 1)) == 0; }
+bool pow2(int L) { return L >= 8 && (L & (L - 1)) == 0; }
 
 }  // namespace
 }  // namespace negf
@@ -242,11 +403,13 @@ int negf_conv_polarization(long long n_rows, int n_e, int L, const void* gl, con
       !pl || !pg)
     return -1;
   if (n_rows == 0) return 0;
-  int rc = smem_setup((const void*)pol_kernel, L);
+  int rc = smem_setup((const void*)pol_kernel<256>, L) || smem_setup((const void*)pol_kernel<512>, L);
   if (rc) return rc;
   {
-    ProfScope ps_pol_kernel(PROF_OTHER, (cudaStream_t)(stream));
-    pol_kernel<<<(unsigned)n_rows, threads_for(L), 2 * (size_t)L * sizeof(z_t), (cudaStream_t)stream>>>(
+    // algorithmic HBM bytes: read G^<, G^> rows, write P^<, P^>, P^R_up, P^R_lo (96 B per entry-energy)
+    ProfSpan ps_pol_kernel(PROF_CONV, (cudaStream_t)(stream), 0.0, 96.0 * (double)n_rows * n_e);
+    auto* kfn = L / 8 <= 256 ? pol_kernel<256> : pol_kernel<512>;
+    kfn<<<(unsigned)n_rows, threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
         (const z_t*)gl, (const z_t*)gg, n_e, L, (const z_t*)tw, (const z_t*)kf, (const z_t*)kcf, diag,
         make_double2(scale_re, scale_im), (z_t*)pl, (z_t*)pg, (z_t*)pr_up, (z_t*)pr_lo);
     NEGF_LAUNCHED();
@@ -262,11 +425,13 @@ int negf_conv_sigma(long long n_rows, int n_e, int L, const void* gl, const void
       !kf || !kcf || !sl || !sg)
     return -1;
   if (n_rows == 0) return 0;
-  int rc = smem_setup((const void*)sigma_kernel, L);
+  int rc = smem_setup((const void*)sigma_kernel<256>, L) || smem_setup((const void*)sigma_kernel<512>, L);
   if (rc) return rc;
   {
-    ProfScope ps_sigma_kernel(PROF_OTHER, (cudaStream_t)(stream));
-    sigma_kernel<<<(unsigned)n_rows, threads_for(L), 2 * (size_t)L * sizeof(z_t), (cudaStream_t)stream>>>(
+    // read G^<, G^>, W^<, W^> rows, write four Sigma series (128 B per entry-energy)
+    ProfSpan ps_sigma_kernel(PROF_CONV, (cudaStream_t)(stream), 0.0, 128.0 * (double)n_rows * n_e);
+    auto* kfn = L / 8 <= 256 ? sigma_kernel<256> : sigma_kernel<512>;
+    kfn<<<(unsigned)n_rows, threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
         (const z_t*)gl, (const z_t*)gg, (const z_t*)wl, (const z_t*)wg, w_rows, n_e, L, (const z_t*)tw,
         (const z_t*)kf, (const z_t*)kcf, diag, make_double2(scale_re, scale_im), (z_t*)sl, (z_t*)sg,
         (z_t*)sr_up, (z_t*)sr_lo);
@@ -282,11 +447,12 @@ int negf_convolve_energy(long long n_rows, int n_e, int L, const void* x1, const
       !x2 || !tw || !out)
     return -1;
   if (n_rows == 0) return 0;
-  int rc = smem_setup((const void*)conv_kernel, L);
+  int rc = smem_setup((const void*)conv_kernel<256>, L) || smem_setup((const void*)conv_kernel<512>, L);
   if (rc) return rc;
   {
     ProfScope ps_conv_kernel(PROF_OTHER, (cudaStream_t)(stream));
-    conv_kernel<<<(unsigned)n_rows, threads_for(L), 2 * (size_t)L * sizeof(z_t), (cudaStream_t)stream>>>(
+    auto* kfn = L / 8 <= 256 ? conv_kernel<256> : conv_kernel<512>;
+    kfn<<<(unsigned)n_rows, threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
         (const z_t*)x1, (const z_t*)x2, n_e, L, mode, (const z_t*)tw, make_double2(scale_re, scale_im),
         (z_t*)out);
     NEGF_LAUNCHED();
@@ -301,11 +467,12 @@ int negf_retarded_from_lg(long long n_rows, int n_e, int L, const void* x_lesser
       !kf || !out)
     return -1;
   if (n_rows == 0) return 0;
-  int rc = smem_setup((const void*)ret_kernel, L);
+  int rc = smem_setup((const void*)ret_kernel<256>, L) || smem_setup((const void*)ret_kernel<512>, L);
   if (rc) return rc;
   {
     ProfScope ps_ret_kernel(PROF_OTHER, (cudaStream_t)(stream));
-    ret_kernel<<<(unsigned)n_rows, threads_for(L), 2 * (size_t)L * sizeof(z_t), (cudaStream_t)stream>>>(
+    auto* kfn = L / 8 <= 256 ? ret_kernel<256> : ret_kernel<512>;
+    kfn<<<(unsigned)n_rows, threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
         (const z_t*)x_lesser, (const z_t*)x_greater, n_e, L, (const z_t*)tw, (const z_t*)kf, (z_t*)out);
     NEGF_LAUNCHED();
   }

@@ -148,7 +148,7 @@ int negf_pack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* x_diag,
   Pat p = make_pat(n_b, bs);
   dim3 grid((unsigned)((p.n_entries + T - 1) / T), (n_e + T - 1) / T), block(T, 8);
   {
-    ProfScope ps_pack_lg_kernel(PROF_OTHER, (cudaStream_t)(stream));
+    ProfSpan ps_pack_lg_kernel(PROF_LAYOUT, (cudaStream_t)(stream), 0.0, 32.0 * (double)p.n_entries * n_e);
     pack_lg_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(p, tri_q, n_e, (const z_t*)x_diag,
                                                              (const z_t*)x_upper, (z_t*)out, ld, e0);
     NEGF_LAUNCHED();
@@ -164,7 +164,8 @@ int negf_unpack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* in, l
   Pat p = make_pat(n_b, bs);
   dim3 grid((unsigned)((p.n_entries + T - 1) / T), (n_e + T - 1) / T), block(T, 8);
   {
-    ProfScope ps_unpack_kernel(PROF_OTHER, (cudaStream_t)(stream));
+    const double blocks = (2.0 * n_b - 1.0) * bs * bs;  // diag + upper blocks written
+    ProfSpan ps_unpack_kernel(PROF_LAYOUT, (cudaStream_t)(stream), 0.0, 16.0 * ((double)p.n_entries + blocks) * n_e);
     unpack_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(p, tri_q, n_e, (const z_t*)in, nullptr, ld,
                                                             e0, 0, (z_t*)x_diag, (z_t*)x_upper, nullptr);
     NEGF_LAUNCHED();
@@ -183,7 +184,9 @@ int negf_unpack_retarded(int n_e, int n_b, int bs, const int* tri_q, const void*
   Pat p = make_pat(n_b, bs);
   dim3 grid((unsigned)((p.n_entries + T - 1) / T), (n_e + T - 1) / T), block(T, 8);
   {
-    ProfScope ps_unpack_kernel(PROF_OTHER, (cudaStream_t)(stream));
+    const double blocks = (3.0 * n_b - 2.0) * bs * bs;  // diag + upper + lower blocks written
+    ProfSpan ps_unpack_kernel(PROF_LAYOUT, (cudaStream_t)(stream), 0.0,
+                              16.0 * (2.0 * (double)p.n_entries + blocks) * n_e);
     unpack_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(
         p, tri_q, n_e, (const z_t*)in_upper, (const z_t*)in_lower, ld, e0, 1, (z_t*)x_diag,
         (z_t*)x_upper, (z_t*)x_lower);
