@@ -152,6 +152,18 @@ int negf_stein_batched(int batch, int bs, const void* a, const void* q, void* w,
                        int max_iter, const void* v0, int* status, int* iters, const int* select,
                        void* workspace, size_t workspace_bytes, void* stream);
 
+/* Beyn contour moments (obc_beyn, obc.py:198-296, nearest-neighbour stencil
+ * [n', m, n]) for `batch` surface problems: a0 = sum_k w_k P(z_k)^-1 probe,
+ * a1 = sum_k w_k z_k P(z_k)^-1 probe with P(z) = n' + z m + z^2 n. z, w: HOST
+ * arrays of n_quad complex numbers (interleaved re, im); probe [bs][bs]
+ * device (the seeded probe, numpy default_rng(1278)). status[b] = 1 + k when
+ * P(z_k) is singular (the reference's "contour node" SingularBlockError).
+ * The SVD / eigen / pseudo-inverse steps follow in obc.py. */
+size_t negf_beyn_workspace_bytes(int batch, int bs);
+int negf_beyn_moments(int batch, int bs, int n_quad, const void* m, const void* n, const void* np,
+                      const double* z, const double* w, const void* probe, void* a0, void* a1,
+                      int* status, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Runtime OBC memoizer, batched: the refresh leg of memoized_obc
  * (obc.py:519-600; _memo_refresh :551-600). map 0 = surface fixed point
  * x <- (m - n x n')^-1 (fixed_point_step, obc.py:138-141; n_kind must be 1),

@@ -457,6 +457,47 @@ def sancho_rubio(m, n, n_prime, tol: float = 1e-12, max_iter: int = 100):
     raise OracleConvergence("not converged")
 
 
+BEYN_PROBE_SEED = 1278  # obc.py:47
+
+
+def beyn(m, n, n_prime, n_quad: int = 16, radius: float = 1.0, center: complex = 0.0, svd_tol: float = 1e-8,
+         probe_seed: int = BEYN_PROBE_SEED):
+    """obc_beyn (obc.py:198-296) for a nearest-neighbour lead (stencil
+    [n', m, n], N_U = 1): contour moments of P(z)^-1 = (n' + z m + z^2 n)^-1
+    against a seeded probe, rank-revealing SVD, the small eigenproblem, the
+    decaying modes |mu| < 1 - 1e-8, then x = (m + n F)^-1 with
+    F = Phi diag(mu) Phi^+. Returns (x, n_modes)."""
+    bs = m.shape[0]
+    if np.allclose(n, 0):
+        return lu_inverse(m)[0], 0
+    rng = np.random.default_rng(probe_seed)
+    probe = rng.standard_normal((bs, bs)) + 1j * rng.standard_normal((bs, bs))
+    a0 = np.zeros((bs, bs), complex)
+    a1 = np.zeros((bs, bs), complex)
+    for k in range(n_quad):
+        z = center + radius * np.exp(2j * np.pi * k / n_quad)
+        pz = n_prime + z * m + z * z * n
+        rz = sla.lu_solve(sla.lu_factor(pz, check_finite=False), probe, check_finite=False)
+        w = (z - center) / n_quad
+        a0 += w * rz
+        a1 += w * z * rz
+    u, sig, wh = np.linalg.svd(a0)
+    rank = int(np.sum(sig > svd_tol * sig[0])) if sig[0] > 0 else 0
+    if rank == 0:
+        return lu_inverse(m)[0], 0
+    u = u[:, :rank]
+    w_red = wh.conj().T[:, :rank]
+    b_small = (u.conj().T @ a1 @ w_red) / sig[:rank]
+    mu, vecs = np.linalg.eig(b_small)
+    keep = np.abs(mu) < 1.0 - 1e-8
+    mu, vecs = mu[keep], vecs[:, keep]
+    if mu.size == 0:
+        return lu_inverse(m)[0], 0
+    phi = u @ vecs
+    f_mat = (phi * mu[None, :]) @ np.linalg.pinv(phi)
+    return lu_inverse(m + n @ f_mat)[0], int(mu.size)
+
+
 def sigma_lg_obc(x_r, mu, kT, energy, n, n_prime):
     """obc.py:460-486."""
     sr = (n @ x_r) @ n_prime

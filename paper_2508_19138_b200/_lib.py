@@ -51,6 +51,8 @@ _SIGNATURES: dict[str, tuple] = {
     "negf_sigma_lg_obc_batched": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "negf_stein_workspace_bytes": (_sz, [_i, _i]),
     "negf_stein_batched": (_i, [_i, _i, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "negf_beyn_workspace_bytes": (_sz, [_i, _i]),
+    "negf_beyn_moments": (_i, [_i, _i, _i] + [_vp] * 3 + [_vp, _vp] + [_vp] * 4 + [_vp, _sz, _vp]),
     "negf_memo_workspace_bytes": (_sz, [_i, _i, _i, _i]),
     "negf_memo_refresh_batched": (_i, [_i, _i, _i, _i] + [_vp] * 5 + [_i, _d] + [_vp] * 6 + [_sz, _vp]),
     "negf_g_obc_workspace_bytes": (_sz, [_i, _i]),

@@ -290,3 +290,125 @@ def memoized_stein_batched(a: torch.Tensor, q: torch.Tensor, w0: torch.Tensor, h
     out, need, used = memo_refresh_batched(MEMO_STEIN, w0, has, n_fpi, tol, a=a, q=q)
     stein_batched(a, q, stein_tol, max_iter, select=need, out=out)
     return out, used
+
+
+# -- Beyn contour-integral solver (obc.py:184-296) ---------------------------------
+
+BEYN_PROBE_SEED = 1278  # obc.py:47
+
+
+@dataclass
+class BeynResult:
+    """obc.py:89-94."""
+
+    x_r: np.ndarray
+    n_modes: int
+    residual: float
+    no_modes_warning: bool = False
+
+
+_PROBES: dict = {}
+
+
+def _probe(bs: int, dev, seed: int = BEYN_PROBE_SEED) -> torch.Tensor:
+    key = (bs, dev.type, dev.index, seed)
+    if key not in _PROBES:
+        rng = np.random.default_rng(seed)
+        pr = rng.standard_normal((bs, bs)) + 1j * rng.standard_normal((bs, bs))
+        _PROBES[key] = torch.from_numpy(pr).to(dev)
+    return _PROBES[key]
+
+
+def beyn_batched(m: torch.Tensor, n: torch.Tensor, n_prime: torch.Tensor, n_quad: int = 16, radius: float = 1.0,
+                 center: complex = 0.0, svd_tol: float = 1e-8):
+    """obc_beyn for a batch (batch, bs, bs) of nearest-neighbour leads
+    (stencil [n', m, n]). Contour moments on the device
+    (negf_beyn_moments: batched P(z)^-1 over the quadrature nodes), then per
+    problem the rank-revealing SVD, the reduced eigenproblem and the
+    pseudo-inverse (cuSOLVER via torch.linalg, rcond 1e-15 like numpy),
+    and x = (m + n F)^-1 with the library's batched inverse.
+    Returns (x, n_modes) -- n_modes = 0 marks the reference's fallback
+    x = m^-1 (decoupled lead, zero rank or no decaying modes)."""
+    if n_quad < 8:
+        raise ValueError(f"need at least 8 quadrature nodes, got {n_quad}")
+    if not 0 < radius <= 1:
+        raise ValueError(f"radius must lie in (0, 1], got {radius}")
+    lib = _lib.load()
+    batch, bs = m.shape[0], m.shape[-1]
+    dev = m.device
+    zs = center + radius * np.exp(2j * np.pi * np.arange(n_quad) / n_quad)
+    ws_ = (zs - center) / n_quad
+    zh = np.ascontiguousarray(np.stack([zs.real, zs.imag], 1).reshape(-1))
+    wh = np.ascontiguousarray(np.stack([ws_.real, ws_.imag], 1).reshape(-1))
+    a0, a1 = torch.empty_like(m), torch.empty_like(m)
+    status = torch.zeros(batch, dtype=torch.int32, device=dev)
+    nbytes = lib.negf_beyn_workspace_bytes(batch, bs)
+    ws = _lib.workspace(nbytes, dev)
+    import ctypes
+
+    dp = ctypes.POINTER(ctypes.c_double)
+    rc = lib.negf_beyn_moments(batch, bs, n_quad, m.data_ptr(), n.data_ptr(), n_prime.data_ptr(),
+                               zh.ctypes.data_as(dp), wh.ctypes.data_as(dp), _probe(bs, dev).data_ptr(),
+                               a0.data_ptr(), a1.data_ptr(), status.data_ptr(), ws.data_ptr(), nbytes,
+                               _lib.stream_ptr(dev))
+    _lib.check(rc, "negf_beyn_moments")
+    st = status.cpu().numpy()
+    if np.any(st):
+        b = int(np.flatnonzero(st)[0])
+        raise SingularBlockError(f"singular contour node {int(st[b]) - 1} (Beyn problem {b})")
+    u, sig, vh = torch.linalg.svd(a0)
+    sig_h = sig.cpu().numpy()
+    decoupled = (n.abs().amax(dim=(1, 2)) == 0).cpu().numpy()
+    target = m.clone()
+    modes = np.zeros(batch, dtype=np.int64)
+    f_all = torch.zeros_like(m)
+    for b in range(batch):
+        if decoupled[b] or not sig_h[b, 0] > 0:
+            continue
+        rank = int(np.sum(sig_h[b] > svd_tol * sig_h[b, 0]))
+        if rank == 0:
+            continue
+        ub = u[b, :, :rank]
+        w_red = vh[b].conj().T[:, :rank]
+        b_small = (ub.conj().T @ a1[b] @ w_red) / sig[b, :rank]
+        mu, vecs = torch.linalg.eig(b_small)
+        keep = mu.abs() < 1.0 - 1e-8
+        mu, vecs = mu[keep], vecs[:, keep]
+        if mu.numel() == 0:
+            continue
+        phi = ub @ vecs
+        f_all[b] = (phi * mu[None, :]) @ torch.linalg.pinv(phi, rtol=1e-15)
+        modes[b] = int(mu.numel())
+    # x = (m + n F)^-1 (problems without modes keep F = 0: x = m^-1)
+    st_ = _lib.stream_ptr(dev)
+    rc = lib.negf_zgemm_batched(bs, bs, bs, batch, 1.0, 0.0, n.data_ptr(), bs * bs, bs, 0, f_all.data_ptr(),
+                                bs * bs, bs, 0, 1.0, 0.0, m.data_ptr(), bs * bs, bs, target.data_ptr(), bs * bs, bs,
+                                st_)
+    _lib.check(rc, "negf_zgemm_batched")
+    x = torch.empty_like(m)
+    inv_status = torch.zeros(batch, dtype=torch.int32, device=dev)
+    nbytes = lib.negf_zinv_workspace_bytes(bs, batch)
+    ws = _lib.workspace(nbytes, dev)
+    rc = lib.negf_zinv_batched(bs, batch, target.data_ptr(), x.data_ptr(), inv_status.data_ptr(), None,
+                               ws.data_ptr(), nbytes, st_)
+    _lib.check(rc, "negf_zinv_batched")
+    if int(inv_status.amax().item()):
+        raise SingularBlockError("singular surface matrix m + n F")
+    return x, modes
+
+
+def obc_beyn(m_tilde_blocks, contour: dict | None = None, svd_tol: float = 1e-8, probe_seed: int = BEYN_PROBE_SEED,
+             device="cuda") -> BeynResult:
+    """obc.py:198-296 signature for a nearest-neighbour stencil [n', m, n]
+    (N_U = 1; longer stencils are outside the hot path)."""
+    if len(m_tilde_blocks) != 3:
+        raise ValueError("the GPU Beyn solver takes nearest-neighbour stencils [n', m, n]")
+    if probe_seed != BEYN_PROBE_SEED:
+        raise ValueError("only the reference probe seed is supported")
+    params = {"radius": 1.0, "center": 0.0, "n_quad": 16}
+    params.update(contour or {})
+    dev = torch.device(device)
+    npr, m, n = (_t(b, dev)[None] for b in m_tilde_blocks)
+    x, modes = beyn_batched(m, n, npr, int(params["n_quad"]), float(params["radius"]), complex(params["center"]),
+                            svd_tol)
+    return BeynResult(x[0].cpu().numpy(), int(modes[0]), float("nan"), no_modes_warning=int(modes[0]) == 0)

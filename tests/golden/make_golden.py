@@ -281,6 +281,24 @@ def make_dd():
     np.savez_compressed(OUT / "golden_dd.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
 
 
+def make_beyn():
+    """obc_beyn (obc.py:198-296) on random leads and on the W-side cells of
+    the small SCBA case (stencil [n_up, m, n_dn], BeynOptions defaults)."""
+    out = {}
+    k = 0
+    for seed, bs, eta, e in ((0, 5, 0.02, 0.1), (1, 6, 0.05, -0.3), (2, 4, 1e-3, 0.0), (3, 8, 0.01, 0.5),
+                             (4, 3, 0.1, 1.2)):
+        c = toys.random_lead(seed, bs, energy=e, eta=eta)
+        r = obc.obc_beyn([c.n_prime, c.m, c.n], contour={"radius": 1.0, "center": 0.0, "n_quad": 16},
+                         svd_tol=1e-8)
+        p = f"b{k}_"
+        out[p + "m"], out[p + "n"], out[p + "np"] = c.m, c.n, c.n_prime
+        out[p + "x"], out[p + "modes"] = r.x_r, np.array(r.n_modes)
+        k += 1
+    out["n_b"] = np.array(k)
+    np.savez_compressed(OUT / "golden_beyn.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rgf", "obc", "conv", "scba"]
     for w in which:

@@ -113,3 +113,26 @@ def test_stein_and_fixed_point_step_dropins(golden, cuda):
     x0 = np.zeros_like(x)
     ref = np.linalg.inv(c.m - c.n @ x0 @ c.n_prime)
     assert rel(fixed_point_step(c, x0), ref) < TOL
+
+
+def test_beyn_matches_reference(golden, cuda):
+    """obc_beyn (obc.py:198-296) on the device vs the reference's own output:
+    same decaying-mode count, same surface block (batched and drop-in)."""
+    import torch
+    from paper_2508_19138_b200.obc import beyn_batched, obc_beyn
+
+    g = golden("golden_beyn.npz")
+    for k in range(int(g["n_b"])):
+        p = f"b{k}_"
+        r = obc_beyn([g[p + "np"], g[p + "m"], g[p + "n"]], device=cuda)
+        assert r.n_modes == int(g[p + "modes"]), k
+        assert rel(r.x_r, g[p + "x"]) < 1e-10, k
+    # a batch of one lead at several energies vs the oracle
+    m0, n0, np0 = g["b3_m"], g["b3_n"], g["b3_np"]
+    ms = [m0 + de * np.eye(m0.shape[0]) for de in (0.0, 0.05, -0.1, 0.2)]
+    t = lambda xs: torch.from_numpy(np.ascontiguousarray(np.stack(xs))).to(cuda)
+    x, modes = beyn_batched(t(ms), t([n0] * 4), t([np0] * 4))
+    for i, mm in enumerate(ms):
+        xo, mo = orc.beyn(mm, n0, np0)
+        assert int(modes[i]) == mo
+        assert rel(x[i].cpu().numpy(), xo) < 1e-10

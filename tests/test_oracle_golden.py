@@ -232,3 +232,16 @@ def test_oracle_dd_matches_reference_dist_selected_solve(golden, c):
         assert rel(out[key][0], g[p + ref]) < 1e-12, key
     seq = orc.rgf_selected(*m, b)
     assert rel(out["x<_diag"], seq["x<_diag"]) < 1e-10
+
+
+def test_oracle_beyn_matches_reference(golden):
+    """obc_beyn (obc.py:198-296) vs the oracle restatement: same mode count,
+    same surface block. (On these in-band random leads Beyn keeps fewer
+    decaying modes than bs and differs from the Sancho-Rubio fixed point --
+    the reference behaviour SURVEY §0.4 documents; the goldens pin it.)"""
+    g = golden("golden_beyn.npz")
+    for k in range(int(g["n_b"])):
+        p = f"b{k}_"
+        x, modes = orc.beyn(g[p + "m"], g[p + "n"], g[p + "np"])
+        assert modes == int(g[p + "modes"]), k
+        assert rel(x, g[p + "x"]) < 1e-12, k
