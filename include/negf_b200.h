@@ -311,12 +311,15 @@ int negf_w_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
                      int stein_max_iter, const void* v0, int* status, int* iters,
                      int* stein_status, int* stein_iters, void* memo_r_cache, int* memo_r_has,
                      int* memo_r_used, void* memo_lg_cache, int* memo_lg_has, int* memo_lg_used,
-                     long long memo_ld, int n_fpi_r, int n_fpi_lg, double memo_tol, void* workspace,
-                     size_t workspace_bytes, void* stream);
+                     long long memo_ld, int n_fpi_r, int n_fpi_lg, double memo_tol,
+                     const void* x_surface, void* workspace, size_t workspace_bytes, void* stream);
 /* Memoizer (optional, as for negf_g_obc_apply): memo_r_* cache the W
  * surfaces (key (W, side, e, R), [2 sides][memo_ld]), memo_lg_* the Stein
  * solutions (key (W, side, e, kind), [2 kinds][2 sides][memo_ld]); budgets
- * n_fpi_r / n_fpi_lg (SurfaceCache.n_fpi, obc.py:504-512). */
+ * n_fpi_r / n_fpi_lg (SurfaceCache.n_fpi, obc.py:504-512).
+ * x_surface (optional, [2][n_e][bs][bs]): retarded surface blocks computed by
+ * the caller (the reference's Beyn solve, scba.py:844); replaces the Sancho /
+ * memoized surface step. */
 
 /* ---- (5b) spatial domain decomposition (negfgw/dist.py) ------------------
  * Partition-local pieces of dist_selected_solve (dist.py:622-717) for a

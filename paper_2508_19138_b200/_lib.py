@@ -75,7 +75,7 @@ _SIGNATURES: dict[str, tuple] = {
     "negf_w_assemble": (_i, [_i, _i, _i] + [_vp] * 18 + [_sz, _vp]),
     "negf_w_obc_workspace_bytes": (_sz, [_i, _i]),
     "negf_w_obc_apply": (_i, [_i, _i, _i] + [_vp] * 7 + [_d, _i, _d, _i] + [_vp] * 5 + [_vp] * 6
-                         + [_ll, _i, _i, _d, _vp, _sz, _vp]),
+                         + [_ll, _i, _i, _d, _vp, _vp, _sz, _vp]),
     "negf_dd_workspace_bytes": (_sz, [_i, _i]),
     "negf_dd_schur_tail": (_i, [_i, _i, _i] + [_vp] * 13 + [_vp, _sz, _vp]),
     "negf_dd_middle_sweep": (_i, [_i, _i, _i] + [_vp] * 10 + [_vp, _vp, _sz, _vp]),

@@ -462,8 +462,8 @@ int negf_w_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
                      int stein_max_iter, const void* v0, int* status, int* iters,
                      int* stein_status, int* stein_iters, void* memo_r_cache, int* memo_r_has,
                      int* memo_r_used, void* memo_lg_cache, int* memo_lg_has, int* memo_lg_used,
-                     long long memo_ld, int n_fpi_r, int n_fpi_lg, double memo_tol, void* workspace,
-                     size_t workspace_bytes, void* stream) {
+                     long long memo_ld, int n_fpi_r, int n_fpi_lg, double memo_tol,
+                     const void* x_surface, void* workspace, size_t workspace_bytes, void* stream) {
   if ((memo_r_cache && (!memo_r_has || memo_ld < n_e)) || (memo_lg_cache && (!memo_lg_has || memo_ld < n_e)))
     return -1;
   if (n_e < 0 || n_b < 2 || bs < 1 || !m_diag || !m_upper || !m_lower || !status || !iters ||
@@ -505,7 +505,11 @@ int negf_w_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
   RC(gather(cn + hn, mu + (nb - 2) * n2, so));
   RC(gather(cnp, mu, so));
   RC(gather(cnp + hn, ml + (nb - 2) * n2, so));
-  if (memo_r_cache) {  // memoized W surfaces, key (W, side, e, R); staged through t
+  if (x_surface) {  // surfaces supplied by the caller (e.g. Beyn, obc.py:198-296)
+    NEGF_CUDA_CHECK(cudaMemcpyAsync(xr, x_surface, ns * blk, cudaMemcpyDeviceToDevice, st));
+    NEGF_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(int) * ns, st));
+    NEGF_CUDA_CHECK(cudaMemsetAsync(iters, 0, sizeof(int) * ns, st));
+  } else if (memo_r_cache) {  // memoized W surfaces, key (W, side, e, R); staged through t
     RC(memo_gather((const z_t*)memo_r_cache, memo_ld, memo_r_has, memo_ld, 2, ne, bs, t, has_buf, st));
     RC(memo_refresh(MEMO_SURFACE, ns, 1, bs, cm, cn, cnp, nullptr, nullptr, n_fpi_r, memo_tol, t, has_buf, xr,
                     need, used_buf, sws, s_bytes, st));

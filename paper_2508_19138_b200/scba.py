@@ -38,6 +38,23 @@ Z = torch.complex128
 
 
 @dataclass(frozen=True)
+class BeynOptions:
+    """scba.py:124-140: contour parameters of the Beyn boundary solver."""
+
+    n_quad: int = 16
+    radius: float = 1.0
+    svd_tol: float = 1e-8
+
+    def __post_init__(self) -> None:
+        if self.n_quad < 8:
+            raise ValueError(f"need at least 8 quadrature nodes, got {self.n_quad}")
+        if not 0 < self.radius <= 1:
+            raise ValueError(f"radius must lie in (0, 1], got {self.radius}")
+        if self.svd_tol <= 0:
+            raise ValueError(f"svd_tol must be positive, got {self.svd_tol}")
+
+
+@dataclass(frozen=True)
 class MemoizerOptions:
     """scba.py:143-154: budgets of the runtime direct-vs-refresh choice."""
 
@@ -63,6 +80,10 @@ class ScbaOptions:
     stein_max_iter: int = 100
     batch: int | None = None  # energies per device batch (None: all)
     memoizer: MemoizerOptions = field(default_factory=MemoizerOptions)
+    # W retarded surface: "sancho" (default; equal to Beyn on the reference's
+    # weak-V inputs) or "beyn" (the reference's choice, scba.py:844)
+    w_retarded_method: str = "sancho"
+    beyn: BeynOptions = field(default_factory=lambda: BeynOptions())
 
     def __post_init__(self) -> None:
         if self.max_iter < 1:
@@ -71,6 +92,8 @@ class ScbaOptions:
             raise ValueError(f"tol must be positive, got {self.tol}")
         if not 0 < self.mixing <= 1:
             raise ValueError(f"mixing must lie in (0, 1], got {self.mixing}")
+        if self.w_retarded_method not in ("sancho", "beyn"):
+            raise ValueError(f"unknown W retarded method {self.w_retarded_method!r}")
 
 
 class EntryLayout:
@@ -122,6 +145,39 @@ class EntryLayout:
 
 class ScreenedSolver:
     """Batched W solve: assembly + contact closure + RGF (scba.py:1059-1103)."""
+
+    def _beyn_surfaces(self, b: dict, n_e: int, memo) -> torch.Tensor:
+        """W retarded surfaces by Beyn (the reference's choice, scba.py:844),
+        through the memoizer like _retarded_surface (scba.py:577-614): cached
+        problems are refreshed with fixed_point_step, Beyn solves the rest.
+        Returns [2 sides][n_e] surface blocks."""
+        from .obc import MEMO_SURFACE, beyn_batched, memo_refresh_batched
+
+        nb = self.n_b
+        # contact cells (scba.py:558-574): left m = M_00, n = M_10, n' = M_01;
+        # right m = M_{N-1,N-1}, n = M_{N-2,N-1}, n' = M_{N-1,N-2}
+        m = torch.cat([b["m_diag"][:, 0], b["m_diag"][:, nb - 1]])
+        n = torch.cat([b["m_lower"][:, 0], b["m_upper"][:, nb - 2]])
+        npr = torch.cat([b["m_upper"][:, 0], b["m_lower"][:, nb - 2]])
+        o = self.opt.beyn
+        if memo is None:
+            x, _ = beyn_batched(m, n, npr, o.n_quad, o.radius, 0.0, o.svd_tol)
+            return x
+        cache, ld, e0, tol_memo = memo
+        xs, hs, us = cache.slot(("W", "R"), 2, ld, self.bs, self.dev)
+        x0 = torch.cat([xs[0, e0:e0 + n_e], xs[1, e0:e0 + n_e]])
+        has = torch.cat([hs[0, e0:e0 + n_e], hs[1, e0:e0 + n_e]]).contiguous()
+        x, need, used = memo_refresh_batched(MEMO_SURFACE, x0, has, cache.n_fpi("R"), tol_memo, m=m, n=n, n_prime=npr)
+        idx = torch.nonzero(need).flatten()
+        if idx.numel():
+            xb, _ = beyn_batched(m[idx].contiguous(), n[idx].contiguous(), npr[idx].contiguous(), o.n_quad, o.radius,
+                                 0.0, o.svd_tol)
+            x[idx] = xb
+        xs[0, e0:e0 + n_e], xs[1, e0:e0 + n_e] = x[:n_e], x[n_e:]
+        hs[:, e0:e0 + n_e] = 1
+        us[0, e0:e0 + n_e], us[1, e0:e0 + n_e] = used[:n_e], used[n_e:]
+        cache.record(us, e0, n_e)
+        return x
 
     def __init__(self, v, options: ScbaOptions, device) -> None:
         self.dev = torch.device(device)
@@ -180,15 +236,20 @@ class ScreenedSolver:
             xl, hl, ul = cache.slot(("W", "lg"), 4, ld, self.bs, self.dev)
             memo_args = [p(xr[0, e0]), p(hr[0, e0:]), p(ur[0, e0:]), p(xl[0, e0]), p(hl[0, e0:]), p(ul[0, e0:]),
                          ld, cache.n_fpi("R"), cache.n_fpi("<"), tol_memo]
+        x_surface = None
+        if o.w_retarded_method == "beyn":
+            x_surface = self._beyn_surfaces(b, n_e, memo)
+            memo_args[:3] = [None] * 3
         rc = lib.negf_w_obc_apply(n_e, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]),
                                   p(b["bl_diag"]), p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]),
                                   o.surface_tol, 100, o.stein_tol, o.stein_max_iter,
                                   p(_lib.power_start_vector(self.bs, self.dev)), p(b["obc_status"]),
                                   p(b["obc_iters"]), p(b["stein_status"]), p(b["stein_iters"]), *memo_args,
-                                  p(ws), nbytes, st)
+                                  p(x_surface), p(ws), nbytes, st)
         _lib.check(rc, "negf_w_obc_apply")
         if memo is not None:
-            cache.record(ur, e0, n_e)
+            if x_surface is None:
+                cache.record(ur, e0, n_e)
             cache.record(ul, e0, n_e)
         if check:
             raise_on_obc_status(b["obc_status"].cpu().numpy(), b["obc_iters"].cpu().numpy(), None, 100,

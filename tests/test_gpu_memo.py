@@ -117,3 +117,17 @@ def test_scba_memoizer_off_counts_direct_calls(cuda):
                    Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=2, memoizer=MemoizerOptions(enabled=False)),
                    device=cuda)
     assert res["cache_stats_by_iteration"] == []
+
+
+def test_scba_memoizer_with_beyn_w_surface(golden, cuda):
+    """Memoizer on with Beyn as the W surfaces' direct solver -- the reference's
+    exact configuration: arrays and per-iteration call counts."""
+    g = golden("golden_scba_memo_small.npz")
+    res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=4, batch=10, w_retarded_method="beyn"),
+                   device=cuda)
+    np.testing.assert_array_equal(_stats(res), g["cache_stats"])
+    for k in g.files:
+        if k.startswith(("ver_", "config", "cache_stats")):
+            continue
+        assert rel(res[k], g[k]) < TOL, k

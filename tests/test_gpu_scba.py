@@ -128,3 +128,15 @@ def test_scba_reference_api_with_blockmatrix_inputs(golden, cuda):
                                  ScbaOptions(max_iter=3, tol=1e-12, memoizer=MEMO_OFF), device=cuda)
     for k in ("g_r_diag", "g_lesser_upper", "sigma_lesser", "sigma_ret_lower", "residuals"):
         assert rel(res[k], g[k]) < TOL, k
+
+
+def test_scba_with_beyn_w_surface_matches_reference(golden, cuda):
+    """W retarded surface by Beyn, as the reference hard-codes (scba.py:844)."""
+    g = golden("golden_scba_small.npz")
+    res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=3, tol=1e-12, batch=16, memoizer=MEMO_OFF,
+                                                          w_retarded_method="beyn"), device=cuda)
+    for k in g.files:
+        if k.startswith(("ver_", "config")):
+            continue
+        assert rel(res[k], g[k]) < TOL, k
