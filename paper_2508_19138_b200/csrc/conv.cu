@@ -221,7 +221,7 @@ __device__ void retarded_tail(z_t* d, z_t* A, z_t* B, const RowGeom& g, int n, c
 }
 
 template <int MAXT>
-__global__ void __launch_bounds__(MAXT) pol_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg, int n,
+__global__ void __launch_bounds__(MAXT, MAXT == 256 ? 2 : 1) pol_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg, int n,
                                                   int L, const z_t* __restrict__ tw, const z_t* __restrict__ kf,
                                                   const z_t* __restrict__ kcf,
                                                   const unsigned char* __restrict__ diag, double2 scale, z_t* pl,
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(MAXT) sigma_kernel(const z_t* __restrict__ gl,
 
 // Generic convolve_energy (convolve.py:39-71): mode 0 convolution, 1 correlation.
 template <int MAXT>
-__global__ void __launch_bounds__(MAXT) conv_kernel(const z_t* __restrict__ x1, const z_t* __restrict__ x2, int n,
+__global__ void __launch_bounds__(MAXT, MAXT == 256 ? 2 : 1) conv_kernel(const z_t* __restrict__ x1, const z_t* __restrict__ x2, int n,
                                                    int L, int mode, const z_t* __restrict__ tw, double2 scale,
                                                    z_t* out) {
   extern __shared__ __align__(16) z_t sm[];
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(MAXT) conv_kernel(const z_t* __restrict__ x1, 
 }
 
 template <int MAXT>
-__global__ void __launch_bounds__(MAXT) ret_kernel(const z_t* __restrict__ xl, const z_t* __restrict__ xg, int n,
+__global__ void __launch_bounds__(MAXT, MAXT == 256 ? 2 : 1) ret_kernel(const z_t* __restrict__ xl, const z_t* __restrict__ xg, int n,
                                                   int L, const z_t* __restrict__ tw, const z_t* __restrict__ kf,
                                                   z_t* out) {
   extern __shared__ __align__(16) z_t sm[];
