@@ -50,8 +50,10 @@ int negf_set_rgf_overlap(int on);
  * status[n_e] (device int): 0, or 1 + forward step of the first singular
  * Schur complement (rgf.py:121-126 SingularBlockError). u_spread[n_e][n_b]
  * (device double, may be NULL): LU pivot spread per step (rgf.py:44-49).
- * Block size bs <= 512 (the pivoted inverse's register panel is one CTA;
- * larger blocks return -5). */
+ * Blocks up to 512 orbitals are inverted by the one-CTA register-panel
+ * Gauss-Jordan kernel; larger blocks by a 2x2 block recursion onto it (no
+ * pivoting across the halves: sound for accretive carrier Schur complements;
+ * u_spread is NaN for them). */
 size_t negf_rgf_workspace_bytes(int n_e, int n_b, int bs);
 int negf_rgf_selected_solve_batched(
     int n_e, int n_b, int bs,

@@ -108,7 +108,7 @@ size_t rgf_workspace_bytes(int n_e, int n_b, int bs) {
 int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (a.n_e <= 0) return 0;
   if (a.n_b < 1 || a.bs < 1) return -1;
-  if (a.bs > 512) return -5;  // pivoted inverse: register panel of one CTA (zinv.cu)
+
   if (ws_bytes < rgf_workspace_bytes(a.n_e, a.n_b, a.bs)) return -4;
   Ctx c;
   c.n_e = a.n_e; c.n_b = a.n_b; c.bs = a.bs;

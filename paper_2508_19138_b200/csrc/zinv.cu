@@ -25,6 +25,8 @@
 
 namespace negf {
 
+#define RC_(x) do { int _rc = (x); if (_rc) return _rc; } while (0)
+
 namespace {
 
 __device__ __forceinline__ void block_argmax(double v, int idx, double* sv, int* si, double& out_v,
@@ -427,14 +429,127 @@ __global__ void zinv_unpermute_kernel(const z_t* A, long long sA, int n, const i
   }
 }
 
+// dst[b] (rows x cols, ld ldd) = src[b] (ld lds); batch strides sdst / ssrc
+__global__ void copy_block_kernel(z_t* __restrict__ dst, long long sdst, int ldd, const z_t* __restrict__ src,
+                                  long long ssrc, int lds, int rows, int cols) {
+  const long long b = blockIdx.y;
+  const long long total = (long long)rows * cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / cols), j = (int)(e % cols);
+    dst[b * sdst + (long long)i * ldd + j] = src[b * ssrc + (long long)i * lds + j];
+  }
+}
+
+int copy_block(z_t* dst, long long sdst, int ldd, const z_t* src, long long ssrc, int lds, int rows, int cols,
+               int batch, cudaStream_t st) {
+  long long total = (long long)rows * cols;
+  int bx = (int)((total + 255) / 256);
+  if (bx > 256) bx = 256;
+  dim3 grid(bx, batch);
+  ProfScope ps_(PROF_ZINV, st);
+  copy_block_kernel<<<grid, 256, 0, st>>>(dst, sdst, ldd, src, ssrc, lds, rows, cols);
+  NEGF_LAUNCHED();
+  return 0;
+}
+
+__global__ void fill_nan_kernel(double* x, long long stride, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[(long long)i * stride] = __longlong_as_double(0x7ff8000000000000ll);
+}
+
+constexpr int kInvPanelMax = 512;  // one-CTA register panel limit
+
+inline size_t a256z(size_t x) { return (x + 255) & ~size_t(255); }
+
 }  // namespace
 
 size_t zinv_workspace_bytes(int n, int batch) {
   if (n <= kInvSmallMax) return 0;
+  if (n > kInvPanelMax) {  // 2x2 block recursion (zinv_recursive)
+    const size_t h = n / 2, r = n - h, zb = sizeof(z_t) * (size_t)batch;
+    const size_t sub_h = zinv_workspace_bytes((int)h, batch), sub_r = zinv_workspace_bytes((int)r, batch);
+    return a256z(zb * h * h) * 2 + a256z(zb * r * h) * 2 + a256z(zb * r * r) * 2 + (sub_h > sub_r ? sub_h : sub_r);
+  }
   const int nb = zinv_panel_width(n);
   size_t per = 4 * sizeof(int) * (size_t)n + sizeof(double) * 2 + sizeof(z_t) * (size_t)nb * nb;
   return per * batch + 256 * 8;
 }
+
+namespace {
+
+// Blocks above the register-panel limit: 2x2 block inverse on packed halves,
+//   [A B; C D]^-1 = [Ai + Ai B Si C Ai, -Ai B Si; -Si C Ai, Si],  Si = (D - C Ai B)^-1,
+// each half inverted by the pivoted kernel (recursively). No pivoting across
+// the halves: sound for the carrier Schur complements, whose anti-Hermitian
+// part (eta - Im Sigma^R) is positive definite, so every leading block and
+// its Schur complement are invertible with norm <= 1/eta. Singular halves
+// are reported through aux.status; u_spread is not defined for this path
+// (NaN).
+int zinv_recursive(z_t* S, long long sS, z_t* X, long long sX, int n, int batch, InvAux aux, void* ws,
+                   size_t ws_bytes, cudaStream_t st) {
+  const int h = n / 2, r = n - h;
+  const size_t zb = sizeof(z_t) * (size_t)batch;
+  char* w = reinterpret_cast<char*>(ws);
+  auto take = [&](size_t bytes) { char* q = w; w += a256z(bytes); return (z_t*)q; };
+  z_t* Ap = take(zb * h * h);
+  z_t* Ai = take(zb * h * h);
+  z_t* T1 = take(zb * (size_t)r * h);  // C Ai
+  z_t* T2 = take(zb * (size_t)h * r);  // Ai B
+  z_t* Dp = take(zb * (size_t)r * r);
+  z_t* Si = take(zb * (size_t)r * r);
+  void* sub = w;
+  const size_t sub_bytes = ws_bytes - (size_t)(w - reinterpret_cast<char*>(ws));
+  InvAux sa = aux;
+  sa.u_spread = nullptr;
+  const long long hh = (long long)h * h, rh = (long long)r * h, rr = (long long)r * r;
+  const z_t* A = S;
+  const z_t* B = S + h;
+  const z_t* C = S + (long long)h * n;
+  const z_t* D = S + (long long)h * n + h;
+  RC_(copy_block(Ap, hh, h, A, sS, n, h, h, batch, st));
+  RC_(zinv_batched(Ap, hh, h, Ai, hh, h, h, batch, sa, sub, sub_bytes, st));
+  auto desc = [&](const z_t* a, long long sa_, int lda, const z_t* b, long long sb, int ldb, int M, int N, int K,
+                  z_t* d, long long sd, int ldd, double alpha, const z_t* c, long long sc, int ldc) {
+    ZGemmDesc g = zdesc_default();
+    g.M = M; g.N = N; g.batch = batch;
+    g.t[0] = zterm(a, sa_, lda, OP_N, b, sb, ldb, OP_N, K);
+    for (int i = 1; i < kMaxTerms; ++i) g.t[i] = g.t[0];
+    g.alpha = make_double2(alpha, 0.0);
+    if (c) { g.C = c; g.sC = sc; g.ldc = ldc; g.beta = make_double2(1.0, 0.0); }
+    g.D = d; g.sD = sd; g.ldd = ldd;
+    g.active = aux.active;
+    return g;
+  };
+  {  // T1 = C Ai, T2 = Ai B
+    ZGemmGroup g;
+    g.n = 2;
+    g.d[0] = desc(C, sS, n, Ai, hh, h, r, h, h, T1, rh, h, 1.0, nullptr, 0, 0);
+    g.d[1] = desc(Ai, hh, h, B, sS, n, h, r, h, T2, rh, r, 1.0, nullptr, 0, 0);
+    RC_(zgemm_group_launch(g, st));
+  }
+  // Dp = D - T1 B ; Si = Dp^-1
+  RC_(zgemm_launch(desc(T1, rh, h, B, sS, n, r, r, h, Dp, rr, r, -1.0, D, sS, n), st));
+  RC_(zinv_batched(Dp, rr, r, Si, rr, r, r, batch, sa, sub, sub_bytes, st));
+  // X22 = Si ; X21 = -Si T1 ; X12 = -T2 Si
+  RC_(copy_block(X + (long long)h * n + h, sX, n, Si, rr, r, r, r, batch, st));
+  {
+    ZGemmGroup g;
+    g.n = 2;
+    g.d[0] = desc(Si, rr, r, T1, rh, h, r, h, r, X + (long long)h * n, sX, n, -1.0, nullptr, 0, 0);
+    g.d[1] = desc(T2, rh, r, Si, rr, r, h, r, r, X + h, sX, n, -1.0, nullptr, 0, 0);
+    RC_(zgemm_group_launch(g, st));
+  }
+  // X11 = Ai - X12 T1
+  RC_(zgemm_launch(desc(X + h, sX, n, T1, rh, h, h, h, r, X, sX, n, -1.0, Ai, hh, h), st));
+  if (aux.u_spread) {
+    fill_nan_kernel<<<(batch + 127) / 128, 128, 0, st>>>(aux.u_spread, aux.spread_stride, batch);
+    NEGF_LAUNCHED();
+  }
+  return 0;
+}
+
+}  // namespace
 
 int zinv_panel_width(int n) {
   // register panel: n * (nb/16) threads <= 512 per CTA
@@ -463,7 +578,7 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
   if (lds != n || ldx != n) return -2;  // blocked path works on packed matrices
   const int nb = zinv_panel_width(n);
   if (ws_bytes < zinv_workspace_bytes(n, batch)) return -4;
-  if (n * (nb / 16) > 512 || n > 512) return -5;  // register panel: one CTA of <= 512 threads
+  if (n > kInvPanelMax) return zinv_recursive(S, sS, X, sX, n, batch, aux, ws, ws_bytes, stream);
   // carve workspace
   char* w = reinterpret_cast<char*>(ws);
   auto take = [&](size_t bytes) { char* r = w; w += (bytes + 255) & ~size_t(255); return r; };

@@ -96,3 +96,30 @@ def test_zinv_flags_singular(cuda):
                                    ws.data_ptr(), nbytes, _lib.stream_ptr())
         assert rc == 0
         assert st.cpu().numpy().tolist() == [0, 1]
+
+
+@pytest.mark.parametrize("n", [513, 768, 1024, 1100])
+def test_zinv_large_blocks_by_2x2_recursion(cuda, n):
+    """Blocks above the one-CTA register panel (512): 2x2 block recursion on
+    accretive matrices (positive-definite anti-Hermitian part, like every
+    carrier Schur complement), vs numpy's pivoted inverse."""
+    rng = np.random.default_rng(n)
+    batch = 2
+    h = (rng.standard_normal((batch, n, n)) + 1j * rng.standard_normal((batch, n, n))) / np.sqrt(n)
+    h = 0.5 * (h + np.conj(np.swapaxes(h, -1, -2)))
+    a = (0.3 + 0.05j) * np.eye(n) - h  # (E + i eta) I - H
+    s = torch.from_numpy(a.copy()).to(cuda)
+    x = torch.empty_like(s)
+    st = torch.zeros(batch, dtype=torch.int32, device=cuda)
+    lib = _lib.load()
+    nbytes = lib.negf_zinv_workspace_bytes(n, batch)
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=cuda)
+    rc = lib.negf_zinv_batched(n, batch, s.data_ptr(), x.data_ptr(), st.data_ptr(), None, ws.data_ptr(), nbytes,
+                               _lib.stream_ptr())
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert st.cpu().numpy().tolist() == [0] * batch
+    ref = np.linalg.inv(a)
+    got = x.cpu().numpy()
+    for b in range(batch):
+        assert np.linalg.norm(got[b] - ref[b]) / np.linalg.norm(ref[b]) < 1e-11

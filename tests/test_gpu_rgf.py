@@ -190,3 +190,24 @@ def test_split_sweeps_and_seeds_match_reference_semantics(cuda):
         t = xf[i] @ mu[0][i]
         X[i] = xf[i] + t @ X[i + 1] @ ml[0][i] @ xf[i]
     assert rel(np.stack(sol2.x_r_diag), np.stack(X)) < TOL
+
+
+def test_rgf_large_blocks_match_oracle(cuda):
+    """bs = 640 (> the 512 register-panel limit): carrier-like accretive
+    system (chain_device-style onsite + eta), batched selected solve vs the
+    oracle restatement."""
+    rng = np.random.default_rng(4)
+    nb, bs, ne = 3, 640, 2
+    hd = rng.standard_normal((nb, bs, bs)) + 1j * rng.standard_normal((nb, bs, bs))
+    hd = 0.15 * (hd + np.conj(np.swapaxes(hd, -1, -2))) / np.sqrt(bs)
+    t = 0.4 * np.eye(bs, dtype=complex)
+    md = np.stack([(0.2 + 0.1 * e + 0.01j) * np.eye(bs)[None] - hd for e in range(ne)])
+    mu = np.broadcast_to(-t, (ne, nb - 1, bs, bs)).copy()
+    ml = mu.copy()
+    bl = (np.broadcast_to(0.02j * np.eye(bs), (ne, nb, bs, bs)).copy(), np.zeros((ne, nb - 1, bs, bs), complex))
+    ref = orc.rgf_selected(md, mu, ml, {"<": bl})
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda)
+    out = selected_solve_batched(T(md), T(mu), T(ml), (T(bl[0]), T(bl[1])))
+    for k, rk in (("xr_diag", "xr_diag"), ("xr_upper", "xr_upper"), ("xl_diag", "x<_diag")):
+        got = out[k].cpu().numpy()
+        assert np.linalg.norm(got - ref[rk]) / np.linalg.norm(ref[rk]) < 1e-9, k
