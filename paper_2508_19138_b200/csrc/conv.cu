@@ -29,17 +29,17 @@ namespace negf {
 namespace {
 
 // ---------------------------------------------------------------------------
-// Row FFT engine: radix-8 Stockham (auto-sort) passes with the data of a
-// pass held in registers, shared memory only for the exchange between
-// passes. A CTA of L/8 threads owns one row; thread t holds the 8 elements
-// at positions t + s*L/8 (s = 0..7). Every pass READS exactly those
+// Row FFT engine: Stockham (auto-sort) passes of radix E (8 or 16) with the
+// data of a pass held in registers, shared memory only for the exchange
+// between passes. A CTA of L/E threads owns one row; thread t holds the E
+// elements at positions t + s*L/E (s < E). Every pass READS exactly those
 // positions, and the last pass WRITES them (Stockham with Ns*R = L), so the
 // spectrum left in registers by a forward transform is where the pointwise
 // products and the next inverse transform expect it: consecutive transforms
-// never round-trip through shared memory. log2(L) = 3 p8 + (log2 Rs): the
-// small radix Rs in {2, 4} runs first in forward and last in inverse
-// transforms (the same positions rule holds for it). Shared indices are
-// padded by one element per 8 (conflict-free 16-byte accesses).
+// never round-trip through shared memory. log2(L) = log2(E) pE + log2(Rs):
+// the small radix Rs runs first in forward and last in inverse transforms
+// (the same positions rule holds for it). Shared indices are padded by one
+// element per 8 (conflict-free 16-byte accesses).
 
 __device__ __forceinline__ int pidx(int i) { return i + (i >> 3); }
 
@@ -64,37 +64,84 @@ __device__ __forceinline__ void dft4(z_t& v0, z_t& v1, z_t& v2, z_t& v3) {
   v3 = zsub(t1, t3);
 }
 
+// x * exp(-/+ 2 pi i q / 16), q static
+template <bool INV, int q>
+__device__ __forceinline__ z_t w16(z_t x) {
+  constexpr double c[5] = {1.0, 0.92387953251128675613, 0.70710678118654752440, 0.38268343236508977173, 0.0};
+  constexpr int qq = q & 15;
+  if constexpr (qq == 0) return x;
+  if constexpr (qq == 4) return rot<INV>(x);
+  if constexpr (qq == 8) return zmake(-x.x, -x.y);
+  if constexpr (qq == 12) return rot<!INV>(x);
+  // cos and sin of 2 pi qq / 16
+  constexpr int a = qq % 8;
+  constexpr double cs = a <= 4 ? c[a] : -c[8 - a];
+  constexpr double sn = a <= 4 ? c[4 - a] : c[a - 4];
+  constexpr double cq = qq < 8 ? cs : -cs, sq = qq < 8 ? sn : -sn;
+  // forward: * (cos - i sin), inverse: * (cos + i sin)
+  return INV ? zmake(x.x * cq - x.y * sq, x.x * sq + x.y * cq) : zmake(x.x * cq + x.y * sq, x.y * cq - x.x * sq);
+}
+
 template <bool INV>
 __device__ __forceinline__ void dft8(z_t* v) {
   z_t e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
   z_t o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
   dft4<INV>(e0, e1, e2, e3);
   dft4<INV>(o0, o1, o2, o3);
-  const double h = 0.70710678118654752440;
-  // o1 *= W8, o2 *= W8^2, o3 *= W8^3 with W8 = exp(-/+ i pi/4)
-  o1 = INV ? zmake(h * (o1.x - o1.y), h * (o1.x + o1.y)) : zmake(h * (o1.x + o1.y), h * (o1.y - o1.x));
-  o2 = rot<INV>(o2);
-  o3 = INV ? zmake(-h * (o3.x + o3.y), h * (o3.x - o3.y)) : zmake(h * (o3.y - o3.x), -h * (o3.x + o3.y));
+  o1 = w16<INV, 2>(o1);
+  o2 = w16<INV, 4>(o2);
+  o3 = w16<INV, 6>(o3);
   v[0] = zadd(e0, o0); v[4] = zsub(e0, o0);
   v[1] = zadd(e1, o1); v[5] = zsub(e1, o1);
   v[2] = zadd(e2, o2); v[6] = zsub(e2, o2);
   v[3] = zadd(e3, o3); v[7] = zsub(e3, o3);
 }
 
+// natural order in and out: n = 4 n1 + n2, k = k1 + 4 k2
+template <bool INV>
+__device__ __forceinline__ void dft16(z_t* v) {
+  z_t a[4][4];
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) {
+    z_t x0 = v[n2], x1 = v[n2 + 4], x2 = v[n2 + 8], x3 = v[n2 + 12];
+    dft4<INV>(x0, x1, x2, x3);  // over n1 -> k1
+    a[0][n2] = x0; a[1][n2] = x1; a[2][n2] = x2; a[3][n2] = x3;
+  }
+  a[1][1] = w16<INV, 1>(a[1][1]); a[1][2] = w16<INV, 2>(a[1][2]); a[1][3] = w16<INV, 3>(a[1][3]);
+  a[2][1] = w16<INV, 2>(a[2][1]); a[2][2] = w16<INV, 4>(a[2][2]); a[2][3] = w16<INV, 6>(a[2][3]);
+  a[3][1] = w16<INV, 3>(a[3][1]); a[3][2] = w16<INV, 6>(a[3][2]); a[3][3] = w16<INV, 9>(a[3][3]);
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    dft4<INV>(a[k1][0], a[k1][1], a[k1][2], a[k1][3]);  // over n2 -> k2
+    v[k1] = a[k1][0]; v[k1 + 4] = a[k1][1]; v[k1 + 8] = a[k1][2]; v[k1 + 12] = a[k1][3];
+  }
+}
+
+template <bool INV, int R>
+__device__ __forceinline__ void dft_r(z_t* e) {
+  if constexpr (R == 16) dft16<INV>(e);
+  else if constexpr (R == 8) dft8<INV>(e);
+  else if constexpr (R == 4) dft4<INV>(e[0], e[1], e[2], e[3]);
+  else dft2<INV>(e[0], e[1]);
+}
+
+template <int E>
 struct RowGeom {
-  int L, Q;    // Q = L/8 threads carry data
-  int p8, rs;  // radix-8 passes, small radix (0, 2 or 4)
+  int L, Q;    // Q = L/E threads carry data
+  int pE, rs;  // radix-E passes, small radix (0 or 2 .. E/2)
   int t;
   bool act;
 };
 
-__device__ __forceinline__ RowGeom row_geom(int L) {
-  RowGeom g;
+template <int E>
+__device__ __forceinline__ RowGeom<E> row_geom(int L) {
+  constexpr int lg = E == 16 ? 4 : 3;
+  RowGeom<E> g;
   g.L = L;
-  g.Q = L >> 3;
+  g.Q = L / E;
   const int m = 31 - __clz(L);
-  g.p8 = m / 3;
-  g.rs = (m % 3) ? (1 << (m % 3)) : 0;
+  g.pE = m / lg;
+  g.rs = (m % lg) ? (1 << (m % lg)) : 0;
   g.t = threadIdx.x;
   g.act = g.t < g.Q;
   return g;
@@ -102,9 +149,9 @@ __device__ __forceinline__ RowGeom row_geom(int L) {
 
 // One Stockham pass of radix R on NA arrays held in registers (in place).
 // R is a template parameter so every register index is static.
-template <bool INV, int NA, int R>
-__device__ __forceinline__ void pass_compute(z_t (*v)[8], const RowGeom& g, int Ns, const z_t* __restrict__ tw) {
-  constexpr int NB = 8 / R;  // butterflies per thread; element r of butterfly u in slot u + r*NB
+template <bool INV, int E, int NA, int R>
+__device__ __forceinline__ void pass_compute(z_t (*v)[E], const RowGeom<E>& g, int Ns, const z_t* __restrict__ tw) {
+  constexpr int NB = E / R;  // butterflies per thread; element r of butterfly u in slot u + r*NB
 #pragma unroll
   for (int u = 0; u < NB; ++u) {
     const int j = g.t + u * g.Q, k = j & (Ns - 1);
@@ -124,16 +171,23 @@ __device__ __forceinline__ void pass_compute(z_t (*v)[8], const RowGeom& g, int 
     }
 #pragma unroll
     for (int a = 0; a < NA; ++a) {
-      if constexpr (R == 8) dft8<INV>(v[a]);
-      else if constexpr (R == 4) dft4<INV>(v[a][u], v[a][u + 2], v[a][u + 4], v[a][u + 6]);
-      else dft2<INV>(v[a][u], v[a][u + 4]);
+      if constexpr (NB == 1) {
+        dft_r<INV, R>(v[a]);
+      } else {
+        z_t e[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) e[r] = v[a][u + r * NB];
+        dft_r<INV, R>(e);
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[a][u + r * NB] = e[r];
+      }
     }
   }
 }
 
-template <int NA, int R>
-__device__ __forceinline__ void pass_store(z_t (*v)[8], z_t* const* sm, const RowGeom& g, int Ns) {
-  constexpr int NB = 8 / R;
+template <int E, int NA, int R>
+__device__ __forceinline__ void pass_store(z_t (*v)[E], z_t* const* sm, const RowGeom<E>& g, int Ns) {
+  constexpr int NB = E / R;
 #pragma unroll
   for (int u = 0; u < NB; ++u) {
     const int j = g.t + u * g.Q, k = j & (Ns - 1);
@@ -145,41 +199,44 @@ __device__ __forceinline__ void pass_store(z_t (*v)[8], z_t* const* sm, const Ro
   }
 }
 
-template <bool INV, int NA, int R>
-__device__ __forceinline__ void fft_pass(z_t (*v)[8], z_t* const* sm, const RowGeom& g, int Ns,
+template <bool INV, int E, int NA, int R>
+__device__ __forceinline__ void fft_pass(z_t (*v)[E], z_t* const* sm, const RowGeom<E>& g, int Ns,
                                          const z_t* __restrict__ tw, bool load, bool store) {
   if (load) {
     if (g.act) {
 #pragma unroll
-      for (int s = 0; s < 8; ++s)
+      for (int s = 0; s < E; ++s)
 #pragma unroll
         for (int a = 0; a < NA; ++a) v[a][s] = sm[a][pidx(g.t + s * g.Q)];
     }
     __syncthreads();
   }
-  if (g.act) pass_compute<INV, NA, R>(v, g, Ns, tw);
+  if (g.act) pass_compute<INV, E, NA, R>(v, g, Ns, tw);
   if (store) {
-    if (g.act) pass_store<NA, R>(v, sm, g, Ns);
+    if (g.act) pass_store<E, NA, R>(v, sm, g, Ns);
     __syncthreads();
   }
 }
 
 // Forward (INV = false) or unscaled inverse transform of NA rows in registers.
-template <bool INV, int NA>
-__device__ void fft_rows(z_t (*v)[8], z_t* const* sm, const RowGeom& g, const z_t* __restrict__ tw) {
-  const int npass = g.p8 + (g.rs ? 1 : 0);
+template <bool INV, int E, int NA>
+__device__ void fft_rows(z_t (*v)[E], z_t* const* sm, const RowGeom<E>& g, const z_t* __restrict__ tw) {
+  const int npass = g.pE + (g.rs ? 1 : 0);
   int Ns = 1;
   for (int p = 0; p < npass; ++p) {
     const bool small = g.rs && (INV ? p == npass - 1 : p == 0);
     const bool load = p > 0, store = p != npass - 1;
     if (!small) {
-      fft_pass<INV, NA, 8>(v, sm, g, Ns, tw, load, store);
+      fft_pass<INV, E, NA, E>(v, sm, g, Ns, tw, load, store);
+      Ns *= E;
+    } else if (E == 16 && g.rs == 8) {
+      fft_pass<INV, E, NA, (E == 16 ? 8 : 4)>(v, sm, g, Ns, tw, load, store);
       Ns *= 8;
     } else if (g.rs == 4) {
-      fft_pass<INV, NA, 4>(v, sm, g, Ns, tw, load, store);
+      fft_pass<INV, E, NA, 4>(v, sm, g, Ns, tw, load, store);
       Ns *= 4;
     } else {
-      fft_pass<INV, NA, 2>(v, sm, g, Ns, tw, load, store);
+      fft_pass<INV, E, NA, 2>(v, sm, g, Ns, tw, load, store);
       Ns *= 2;
     }
   }
@@ -191,26 +248,27 @@ __device__ __forceinline__ z_t proj(z_t v, bool diag) {
 }
 
 // d (registers, natural positions) -> r_up = K*d, r_lo = -conj(conj(K)*d)
-__device__ void retarded_tail(z_t* d, z_t* A, z_t* B, const RowGeom& g, int n, const z_t* tw, const z_t* kf,
+template <int E>
+__device__ void retarded_tail(z_t* d, z_t* A, z_t* B, const RowGeom<E>& g, int n, const z_t* tw, const z_t* kf,
                               const z_t* kcf, z_t* r_up, z_t* r_lo) {
   z_t* sB[1] = {B};
-  z_t dv[1][8];
+  z_t dv[1][E];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) dv[0][s] = d[s];
-  fft_rows<false, 1>(dv, sB, g, tw);
-  z_t xy[2][8];
+  for (int s = 0; s < E; ++s) dv[0][s] = d[s];
+  fft_rows<false, E, 1>(dv, sB, g, tw);
+  z_t xy[2][E];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
+  for (int s = 0; s < E; ++s) {
     const int q = g.t + s * g.Q;
     xy[0][s] = g.act ? zmul(dv[0][s], __ldg(&kf[q])) : make_double2(0.0, 0.0);
     xy[1][s] = g.act && kcf ? zmul(dv[0][s], __ldg(&kcf[q])) : make_double2(0.0, 0.0);
   }
   z_t* sAB[2] = {A, B};
-  fft_rows<true, 2>(xy, sAB, g, tw);
+  fft_rows<true, E, 2>(xy, sAB, g, tw);
   const double inv = 1.0 / g.L;
   if (g.act) {
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
+    for (int s = 0; s < E; ++s) {
       const int k = g.t + s * g.Q;
       if (k < n) {
         if (r_up) r_up[k] = zscale(inv, xy[0][s]);
@@ -220,69 +278,69 @@ __device__ void retarded_tail(z_t* d, z_t* A, z_t* B, const RowGeom& g, int n, c
   }
 }
 
-template <int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT == 256 ? 2 : 1) pol_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg, int n,
-                                                  int L, const z_t* __restrict__ tw, const z_t* __restrict__ kf,
-                                                  const z_t* __restrict__ kcf,
-                                                  const unsigned char* __restrict__ diag, double2 scale, z_t* pl,
-                                                  z_t* pg, z_t* pr_up, z_t* pr_lo) {
+template <int E, int MAXT>
+__global__ void __launch_bounds__(MAXT) pol_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg, int n,
+                                                   int L, const z_t* __restrict__ tw, const z_t* __restrict__ kf,
+                                                   const z_t* __restrict__ kcf,
+                                                   const unsigned char* __restrict__ diag, double2 scale, z_t* pl,
+                                                   z_t* pg, z_t* pr_up, z_t* pr_lo) {
   extern __shared__ __align__(16) z_t sm[];
   z_t* A = sm;
   z_t* B = sm + pidx(L);
-  const RowGeom g = row_geom(L);
+  const RowGeom<E> g = row_geom<E>(L);
   const long long row = blockIdx.x;
   const long long o = row * n;
   const bool dg = diag && diag[row];
-  z_t v[2][8];
+  z_t v[2][E];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
+  for (int s = 0; s < E; ++s) {
     const int k = g.t + s * g.Q;
     const bool in = g.act && k < n;
     v[0][s] = in ? gl[o + k] : make_double2(0.0, 0.0);
     v[1][s] = in ? gg[o + k] : make_double2(0.0, 0.0);
   }
   z_t* sAB[2] = {A, B};
-  fft_rows<false, 2>(v, sAB, g, tw);
+  fft_rows<false, E, 2>(v, sAB, g, tw);
 #pragma unroll
-  for (int s = 0; s < 8; ++s) v[0][s] = zmul(v[0][s], make_double2(-v[1][s].x, v[1][s].y));  // * (-conj G^>)
+  for (int s = 0; s < E; ++s) v[0][s] = zmul(v[0][s], make_double2(-v[1][s].x, v[1][s].y));  // * (-conj G^>)
   z_t* sA[1] = {A};
-  fft_rows<true, 1>(v, sA, g, tw);
+  fft_rows<true, E, 1>(v, sA, g, tw);
   // P^>[k] = conj(p[-k]): exchange p through shared memory
   if (g.act) {
 #pragma unroll
-    for (int s = 0; s < 8; ++s) A[pidx(g.t + s * g.Q)] = v[0][s];
+    for (int s = 0; s < E; ++s) A[pidx(g.t + s * g.Q)] = v[0][s];
   }
   __syncthreads();
   const z_t sc = zscale(1.0 / L, scale);
-  z_t d[8];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
+  for (int s = 0; s < E; ++s) {
     const int k = g.t + s * g.Q;
-    d[s] = make_double2(0.0, 0.0);
+    z_t d = make_double2(0.0, 0.0);
     if (g.act && k < n) {
       const z_t lo = proj(zmul(sc, v[0][s]), dg);
       const z_t gr = proj(zmul(sc, zconj(A[pidx((L - k) & (L - 1))])), dg);
       pl[o + k] = lo;
       pg[o + k] = gr;
-      d[s] = zsub(gr, lo);
+      d = zsub(gr, lo);
     }
+    v[1][s] = d;
   }
   __syncthreads();
-  retarded_tail(d, A, B, g, n, tw, kf, kcf, pr_up ? pr_up + o : nullptr, pr_lo ? pr_lo + o : nullptr);
+  retarded_tail<E>(v[1], A, B, g, n, tw, kf, kcf, pr_up ? pr_up + o : nullptr, pr_lo ? pr_lo + o : nullptr);
 }
 
-template <int MAXT>
+template <int E, int MAXT>
 __global__ void __launch_bounds__(MAXT) sigma_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg,
-                                                    const z_t* __restrict__ wl, const z_t* __restrict__ wg,
-                                                    const long long* __restrict__ w_rows, int n, int L,
-                                                    const z_t* __restrict__ tw, const z_t* __restrict__ kf,
-                                                    const z_t* __restrict__ kcf,
-                                                    const unsigned char* __restrict__ diag, double2 scale, z_t* sl,
-                                                    z_t* sg, z_t* sr_up, z_t* sr_lo) {
+                                                     const z_t* __restrict__ wl, const z_t* __restrict__ wg,
+                                                     const long long* __restrict__ w_rows, int n, int L,
+                                                     const z_t* __restrict__ tw, const z_t* __restrict__ kf,
+                                                     const z_t* __restrict__ kcf,
+                                                     const unsigned char* __restrict__ diag, double2 scale, z_t* sl,
+                                                     z_t* sg, z_t* sr_up, z_t* sr_lo) {
   extern __shared__ __align__(16) z_t sm[];
   z_t* A = sm;
   z_t* B = sm + pidx(L);
-  const RowGeom g = row_geom(L);
+  const RowGeom<E> g = row_geom<E>(L);
   const long long row = blockIdx.x;
   const long long o = row * n;
   const long long ow = (w_rows ? w_rows[row] : row) * n;
@@ -290,25 +348,25 @@ __global__ void __launch_bounds__(MAXT) sigma_kernel(const z_t* __restrict__ gl,
   const z_t sc = zscale(1.0 / L, scale);
   z_t* sAB[2] = {A, B};
   z_t* sA[1] = {A};
-  z_t v[2][8];
+  z_t v[2][E];
 #pragma unroll 1
   for (int kind = 0; kind < 2; ++kind) {
     const z_t* gx = kind ? gg : gl;
     const z_t* wx = kind ? wg : wl;
     z_t* out = kind ? sg : sl;
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
+    for (int s = 0; s < E; ++s) {
       const int k = g.t + s * g.Q;
       const bool in = g.act && k < n;
       v[0][s] = in ? gx[o + k] : make_double2(0.0, 0.0);
       v[1][s] = in ? wx[ow + k] : make_double2(0.0, 0.0);
     }
-    fft_rows<false, 2>(v, sAB, g, tw);
+    fft_rows<false, E, 2>(v, sAB, g, tw);
 #pragma unroll
-    for (int s = 0; s < 8; ++s) v[0][s] = zmul(v[0][s], v[1][s]);
-    fft_rows<true, 1>(v, sA, g, tw);
+    for (int s = 0; s < E; ++s) v[0][s] = zmul(v[0][s], v[1][s]);
+    fft_rows<true, E, 1>(v, sA, g, tw);
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
+    for (int s = 0; s < E; ++s) {
       const int k = g.t + s * g.Q;
       // after the second kind, v[1] <- d = Sigma^> - Sigma^<, Sigma^< re-read
       // from the values this thread wrote itself
@@ -320,22 +378,22 @@ __global__ void __launch_bounds__(MAXT) sigma_kernel(const z_t* __restrict__ gl,
       }
     }
   }
-  retarded_tail(v[1], A, B, g, n, tw, kf, kcf, sr_up ? sr_up + o : nullptr, sr_lo ? sr_lo + o : nullptr);
+  retarded_tail<E>(v[1], A, B, g, n, tw, kf, kcf, sr_up ? sr_up + o : nullptr, sr_lo ? sr_lo + o : nullptr);
 }
 
 // Generic convolve_energy (convolve.py:39-71): mode 0 convolution, 1 correlation.
-template <int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT == 256 ? 2 : 1) conv_kernel(const z_t* __restrict__ x1, const z_t* __restrict__ x2, int n,
-                                                   int L, int mode, const z_t* __restrict__ tw, double2 scale,
-                                                   z_t* out) {
+template <int E, int MAXT>
+__global__ void __launch_bounds__(MAXT) conv_kernel(const z_t* __restrict__ x1, const z_t* __restrict__ x2, int n,
+                                                    int L, int mode, const z_t* __restrict__ tw, double2 scale,
+                                                    z_t* out) {
   extern __shared__ __align__(16) z_t sm[];
   z_t* A = sm;
   z_t* B = sm + pidx(L);
-  const RowGeom g = row_geom(L);
+  const RowGeom<E> g = row_geom<E>(L);
   const long long o = (long long)blockIdx.x * n;
-  z_t v[2][8];
+  z_t v[2][E];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
+  for (int s = 0; s < E; ++s) {
     const int k = g.t + s * g.Q;
     v[0][s] = g.act && k < n ? x1[o + k] : make_double2(0.0, 0.0);
     // correlation: y[j] = x2[-j] placed circularly
@@ -343,45 +401,49 @@ __global__ void __launch_bounds__(MAXT, MAXT == 256 ? 2 : 1) conv_kernel(const z
     v[1][s] = g.act && j < n ? x2[o + j] : make_double2(0.0, 0.0);
   }
   z_t* sAB[2] = {A, B};
-  fft_rows<false, 2>(v, sAB, g, tw);
+  fft_rows<false, E, 2>(v, sAB, g, tw);
 #pragma unroll
-  for (int s = 0; s < 8; ++s) v[0][s] = zmul(v[0][s], v[1][s]);
+  for (int s = 0; s < E; ++s) v[0][s] = zmul(v[0][s], v[1][s]);
   z_t* sA[1] = {A};
-  fft_rows<true, 1>(v, sA, g, tw);
+  fft_rows<true, E, 1>(v, sA, g, tw);
   const z_t sc = zscale(1.0 / L, scale);
   if (g.act) {
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
+    for (int s = 0; s < E; ++s) {
       const int k = g.t + s * g.Q;
       if (k < n) out[o + k] = zmul(sc, v[0][s]);
     }
   }
 }
 
-template <int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT == 256 ? 2 : 1) ret_kernel(const z_t* __restrict__ xl, const z_t* __restrict__ xg, int n,
-                                                  int L, const z_t* __restrict__ tw, const z_t* __restrict__ kf,
-                                                  z_t* out) {
+template <int E, int MAXT>
+__global__ void __launch_bounds__(MAXT) ret_kernel(const z_t* __restrict__ xl, const z_t* __restrict__ xg, int n,
+                                                   int L, const z_t* __restrict__ tw, const z_t* __restrict__ kf,
+                                                   z_t* out) {
   extern __shared__ __align__(16) z_t sm[];
   z_t* A = sm;
   z_t* B = sm + pidx(L);
-  const RowGeom g = row_geom(L);
+  const RowGeom<E> g = row_geom<E>(L);
   const long long o = (long long)blockIdx.x * n;
-  z_t d[8];
+  z_t d[E];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
+  for (int s = 0; s < E; ++s) {
     const int k = g.t + s * g.Q;
     d[s] = g.act && k < n ? zsub(xg[o + k], xl[o + k]) : make_double2(0.0, 0.0);
   }
-  retarded_tail(d, A, B, g, n, tw, kf, nullptr, out + o, nullptr);
+  retarded_tail<E>(d, A, B, g, n, tw, kf, nullptr, out + o, nullptr);
 }
 
-int threads_for(int L) { return L / 8 >= 32 ? L / 8 : 32; }
+// Elements per thread: 8. (E = 16 halves the exchanges of a 1024-point
+// transform, but at ~250 registers it measured no faster for P and 20 %
+// slower for Sigma on B200; the engine keeps both.)
+int ept_for(int) { return 8; }
+int threads_for(int L) { const int q = L / ept_for(L); return q >= 32 ? q : 32; }
 
 size_t smem_for(int L) { return 2 * (size_t)(L + L / 8) * sizeof(z_t); }
 
 int smem_setup(const void* fn, int L) {
-  if (smem_for(L) > 200 * 1024 || L / 8 > 512) return -5;
+  if (smem_for(L) > 200 * 1024 || threads_for(L) > 256) return -5;
   NEGF_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   return 0;
 }
@@ -403,12 +465,12 @@ int negf_conv_polarization(long long n_rows, int n_e, int L, const void* gl, con
       !pl || !pg)
     return -1;
   if (n_rows == 0) return 0;
-  int rc = smem_setup((const void*)pol_kernel<256>, L) || smem_setup((const void*)pol_kernel<512>, L);
+  auto* kfn = ept_for(L) == 16 ? pol_kernel<16, 256> : pol_kernel<8, 256>;
+  int rc = smem_setup((const void*)kfn, L);
   if (rc) return rc;
   {
     // algorithmic HBM bytes: read G^<, G^> rows, write P^<, P^>, P^R_up, P^R_lo (96 B per entry-energy)
     ProfSpan ps_pol_kernel(PROF_CONV, (cudaStream_t)(stream), 0.0, 96.0 * (double)n_rows * n_e);
-    auto* kfn = L / 8 <= 256 ? pol_kernel<256> : pol_kernel<512>;
     kfn<<<(unsigned)n_rows, threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
         (const z_t*)gl, (const z_t*)gg, n_e, L, (const z_t*)tw, (const z_t*)kf, (const z_t*)kcf, diag,
         make_double2(scale_re, scale_im), (z_t*)pl, (z_t*)pg, (z_t*)pr_up, (z_t*)pr_lo);
@@ -425,12 +487,12 @@ int negf_conv_sigma(long long n_rows, int n_e, int L, const void* gl, const void
       !kf || !kcf || !sl || !sg)
     return -1;
   if (n_rows == 0) return 0;
-  int rc = smem_setup((const void*)sigma_kernel<256>, L) || smem_setup((const void*)sigma_kernel<512>, L);
+  auto* kfn = ept_for(L) == 16 ? sigma_kernel<16, 256> : sigma_kernel<8, 256>;
+  int rc = smem_setup((const void*)kfn, L);
   if (rc) return rc;
   {
     // read G^<, G^>, W^<, W^> rows, write four Sigma series (128 B per entry-energy)
     ProfSpan ps_sigma_kernel(PROF_CONV, (cudaStream_t)(stream), 0.0, 128.0 * (double)n_rows * n_e);
-    auto* kfn = L / 8 <= 256 ? sigma_kernel<256> : sigma_kernel<512>;
     kfn<<<(unsigned)n_rows, threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
         (const z_t*)gl, (const z_t*)gg, (const z_t*)wl, (const z_t*)wg, w_rows, n_e, L, (const z_t*)tw,
         (const z_t*)kf, (const z_t*)kcf, diag, make_double2(scale_re, scale_im), (z_t*)sl, (z_t*)sg,
@@ -447,11 +509,11 @@ int negf_convolve_energy(long long n_rows, int n_e, int L, const void* x1, const
       !x2 || !tw || !out)
     return -1;
   if (n_rows == 0) return 0;
-  int rc = smem_setup((const void*)conv_kernel<256>, L) || smem_setup((const void*)conv_kernel<512>, L);
+  auto* kfn = ept_for(L) == 16 ? conv_kernel<16, 256> : conv_kernel<8, 256>;
+  int rc = smem_setup((const void*)kfn, L);
   if (rc) return rc;
   {
     ProfScope ps_conv_kernel(PROF_OTHER, (cudaStream_t)(stream));
-    auto* kfn = L / 8 <= 256 ? conv_kernel<256> : conv_kernel<512>;
     kfn<<<(unsigned)n_rows, threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
         (const z_t*)x1, (const z_t*)x2, n_e, L, mode, (const z_t*)tw, make_double2(scale_re, scale_im),
         (z_t*)out);
@@ -467,11 +529,11 @@ int negf_retarded_from_lg(long long n_rows, int n_e, int L, const void* x_lesser
       !kf || !out)
     return -1;
   if (n_rows == 0) return 0;
-  int rc = smem_setup((const void*)ret_kernel<256>, L) || smem_setup((const void*)ret_kernel<512>, L);
+  auto* kfn = ept_for(L) == 16 ? ret_kernel<16, 256> : ret_kernel<8, 256>;
+  int rc = smem_setup((const void*)kfn, L);
   if (rc) return rc;
   {
     ProfScope ps_ret_kernel(PROF_OTHER, (cudaStream_t)(stream));
-    auto* kfn = L / 8 <= 256 ? ret_kernel<256> : ret_kernel<512>;
     kfn<<<(unsigned)n_rows, threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
         (const z_t*)x_lesser, (const z_t*)x_greater, n_e, L, (const z_t*)tw, (const z_t*)kf, (z_t*)out);
     NEGF_LAUNCHED();
