@@ -443,7 +443,7 @@ int threads_for(int L) { const int q = L / ept_for(L); return q >= 32 ? q : 32; 
 size_t smem_for(int L) { return 2 * (size_t)(L + L / 8) * sizeof(z_t); }
 
 int smem_setup(const void* fn, int L) {
-  if (smem_for(L) > 200 * 1024 || threads_for(L) > 256) return -5;
+  if (smem_for(L) > 200 * 1024 || threads_for(L) > 512) return -5;
   NEGF_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   return 0;
 }
@@ -465,7 +465,7 @@ int negf_conv_polarization(long long n_rows, int n_e, int L, const void* gl, con
       !pl || !pg)
     return -1;
   if (n_rows == 0) return 0;
-  auto* kfn = ept_for(L) == 16 ? pol_kernel<16, 256> : pol_kernel<8, 256>;
+  auto* kfn = threads_for(L) > 256 ? pol_kernel<8, 512> : pol_kernel<8, 256>;
   int rc = smem_setup((const void*)kfn, L);
   if (rc) return rc;
   {
@@ -487,7 +487,7 @@ int negf_conv_sigma(long long n_rows, int n_e, int L, const void* gl, const void
       !kf || !kcf || !sl || !sg)
     return -1;
   if (n_rows == 0) return 0;
-  auto* kfn = ept_for(L) == 16 ? sigma_kernel<16, 256> : sigma_kernel<8, 256>;
+  auto* kfn = threads_for(L) > 256 ? sigma_kernel<8, 512> : sigma_kernel<8, 256>;
   int rc = smem_setup((const void*)kfn, L);
   if (rc) return rc;
   {
@@ -509,7 +509,7 @@ int negf_convolve_energy(long long n_rows, int n_e, int L, const void* x1, const
       !x2 || !tw || !out)
     return -1;
   if (n_rows == 0) return 0;
-  auto* kfn = ept_for(L) == 16 ? conv_kernel<16, 256> : conv_kernel<8, 256>;
+  auto* kfn = threads_for(L) > 256 ? conv_kernel<8, 512> : conv_kernel<8, 256>;
   int rc = smem_setup((const void*)kfn, L);
   if (rc) return rc;
   {
@@ -529,7 +529,7 @@ int negf_retarded_from_lg(long long n_rows, int n_e, int L, const void* x_lesser
       !kf || !out)
     return -1;
   if (n_rows == 0) return 0;
-  auto* kfn = ept_for(L) == 16 ? ret_kernel<16, 256> : ret_kernel<8, 256>;
+  auto* kfn = threads_for(L) > 256 ? ret_kernel<8, 512> : ret_kernel<8, 256>;
   int rc = smem_setup((const void*)kfn, L);
   if (rc) return rc;
   {
