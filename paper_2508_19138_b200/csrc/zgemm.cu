@@ -363,6 +363,9 @@ using Cfg4M32 = Cfg<64, 32, 2, 2, 4, 3, false>;
 using CfgGauss3 = Cfg<32, 64, 2, 2, 4, 3, true>;
 using CfgGauss2P = Cfg<64, 32, 2, 2, 4, 3, true>;  // BK = 8, 4 stages, padded tiles
 using CfgG32s2 = Cfg<64, 32, 2, 2, 2, 2, true, 32, false, true>;
+using CfgW8 = Cfg<64, 32, 4, 2, 2, 2, true, 16, false, true>;    // 8 warps of 16x16, 3M
+using CfgT5 = Cfg<32, 32, 2, 2, 2, 5, true, 16, false, true>;    // 4 warps of 16x16, 5 CTAs/SM
+using CfgW8b = Cfg<64, 64, 4, 2, 2, 1, true, 16, false, true>;   // 8 warps of 16x32
 using CfgMap64 = Cfg<64, 32, 2, 2, 4, 3, true, 8, true>;
 using CfgMap32 = Cfg<32, 64, 2, 2, 4, 3, true, 8, true>;
 using CfgMap64S = Cfg<64, 32, 2, 2, 2, 3, true, 16, true, true>;
@@ -372,7 +375,8 @@ using CfgMapT4 = Cfg<32, 32, 2, 2, 2, 5, false, 16, true, true>; // 4M, 5 CTAs/S
 using CfgMapU = Cfg<16, 64, 1, 4, 2, 5, true, 16, true, true>;   // 16x16 warp tiles, 16-row CTAs
 using CfgMapV = Cfg<32, 32, 2, 2, 2, 6, true, 16, true, true>;   // 6 CTAs/SM
 // Measured alternatives (C2 carrier batch, energies/s, greater by identity):
-//   algo 2 (64x32, BK16, 2 stages, swizzled) 142.4 | 64x32 BK8 4 stages padded 137.9 |
+//   algo 2 (64x32, BK16, 2 stages, swizzled) 149.2 | 7: 8 warps of 16x16 133.8 | 8: 32x32, 5 CTAs/SM 142.6 |
+//   earlier: algo 2 142.4 (before the sweep/panel work) | 64x32 BK8 4 stages padded 137.9 |
 //   32x64 BK16 swizzled 140.0 | 64x32 BK32 2 CTA/SM 133.5 | 64x32 BK16 4 CTA/SM (spills) 109.4
 // Earlier (recursion for G^>, BK8 padded family): 64x32 6-stage 2 CTA/SM 78.9 | 128x32 8 warps
 //   68.1 | 32x32 2 warps 78.2 | 32x32 4 warps (16x16) 87.4 | 64x64 16 warps 69.3 vs 90.5.
@@ -431,6 +435,9 @@ int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
     case 4: return launch_cfg<CfgGauss3>(g, stream);
     case 5: return launch_cfg<CfgGauss2P>(g, stream);
     case 6: return launch_cfg<CfgG32s2>(g, stream);
+    case 7: return launch_cfg<CfgW8>(g, stream);
+    case 8: return launch_cfg<CfgT5>(g, stream);
+    case 9: return launch_cfg<CfgW8b>(g, stream);
     default: return launch_cfg<CfgBig>(g, stream);
   }
 }

@@ -98,6 +98,29 @@ def make_partition_plan(n_blocks: int, p_s: int) -> PartitionPlan:
     return PartitionPlan(n_blocks, tuple(ranges))
 
 
+def balanced_partition_plan(n_blocks: int, p_s: int, middle_cost: float = 2.0) -> PartitionPlan:
+    """A plan for throughput rather than reference layout: a middle partition
+    costs about ``middle_cost`` times an end partition per block (two-sided
+    sweep + full local solve vs one forward + one backward sweep), so ends get
+    proportionally more blocks. Any PartitionPlan is valid input to
+    dist_selected_solve (the result is the same selected solution)."""
+    if p_s <= 2:
+        return make_partition_plan(n_blocks, p_s)
+    n_mid = p_s - 2
+    w_end = n_blocks / (2 + n_mid / middle_cost)
+    ends = max(2, int(round(w_end)))
+    rest = n_blocks - 2 * ends
+    base, rem = divmod(rest, n_mid)
+    if base < 2:
+        return make_partition_plan(n_blocks, p_s)
+    widths = [ends] + [base + (1 if i < rem else 0) for i in range(n_mid)] + [ends]
+    ranges, start = [], 0
+    for w in widths:
+        ranges.append((start, start + w - 1))
+        start += w
+    return PartitionPlan(n_blocks, tuple(ranges))
+
+
 # -- partition-local inputs ------------------------------------------------------
 
 

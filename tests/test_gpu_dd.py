@@ -93,3 +93,20 @@ def test_dd_over_nccl_ranks(cuda):
                              capture_output=True, text=True, timeout=600)
         assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
         assert "DD_CHECK" in out.stdout
+
+
+def test_dd_balanced_plan_gives_the_same_solution(cuda):
+    from paper_2508_19138_b200.dd import balanced_partition_plan
+
+    nb, bs, ne = 20, 48, 2
+    sys_ = [orc.random_bt_system(300 + e, n_blocks=nb, block_size=bs) for e in range(ne)]
+    md, mu, ml = (np.concatenate([s[i] for s in sys_]) for i in range(3))
+    src = {k: tuple(np.concatenate([s[3][k][i] for s in sys_]) for i in range(2)) for k in ("<", ">")}
+    seq = orc.rgf_selected(md, mu, ml, src)
+    for p_s in (3, 4, 5):
+        plan = balanced_partition_plan(nb, p_s)
+        assert plan.ranges[0][1] - plan.ranges[0][0] > plan.ranges[1][1] - plan.ranges[1][0]
+        out = dd_selected_solve_local(t(md, cuda), t(mu, cuda), t(ml, cuda),
+                                      {k: (t(d, cuda), t(u, cuda)) for k, (d, u) in src.items()}, plan)
+        for mine, rk in (("xr_diag", "xr_diag"), ("xl_upper", "x<_upper"), ("xg_diag", "x>_diag")):
+            assert rel(out[mine].cpu().numpy(), seq[rk]) < TOL, (p_s, mine)

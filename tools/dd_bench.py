@@ -6,7 +6,8 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 import torch, torch.distributed as dist
-from paper_2508_19138_b200.dd import dd_selected_solve_batched, make_partition_plan, partition_inputs
+from paper_2508_19138_b200.dd import (balanced_partition_plan, dd_selected_solve_batched, make_partition_plan,
+                                      partition_inputs)
 from paper_2508_19138_b200.rgf import selected_solve_batched
 
 nb, bs, ne = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (32, 1024, 2)))
@@ -21,7 +22,8 @@ g = torch.Generator(device=dev).manual_seed(0)
 r = lambda *s: torch.complex(torch.randn(*s, generator=g, device=dev, dtype=torch.float64),
                              torch.randn(*s, generator=g, device=dev, dtype=torch.float64)) * (1.0 / bs ** 0.5)
 eye = torch.eye(bs, dtype=torch.complex128, device=dev)
-plan = make_partition_plan(nb, world)
+balanced = len(sys.argv) > 4 and sys.argv[4] == "balanced"
+plan = balanced_partition_plan(nb, world) if balanced else make_partition_plan(nb, world)
 a, b = plan.ranges[rank]
 # each rank builds only its partition + halo (same seeded full chain on every rank, sliced)
 md = r(ne, nb, bs, bs) + (4 + 1j) * eye
