@@ -144,12 +144,14 @@ class CarrierSolver:
         s = sigma or {}
         st = _lib.stream_ptr(self.dev)
         hd, hu, hl = self.h
+        # with G^> from the identity the greater source B^> is never read
+        bg_d, bg_u = (None, None) if self.greater == "identity" else (p(b["bg_diag"]), p(b["bg_upper"]))
         rc = lib.negf_g_assemble(
             ne, self.n_b, self.bs, p(hd), p(hu), p(hl), p(b["energy"]), p(b["f_bath"]), self.eta,
             p(s.get("sr_diag")), p(s.get("sr_upper")), p(s.get("sr_lower")),
             p(s.get("sl_diag")), p(s.get("sl_upper")), p(s.get("sg_diag")), p(s.get("sg_upper")),
             p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]), p(b["bl_diag"]), p(b["bl_upper"]),
-            p(b["bg_diag"]), p(b["bg_upper"]), st)
+            bg_d, bg_u, st)
         _lib.check(rc, "negf_g_assemble")
         nbytes = lib.negf_g_obc_workspace_bytes(ne, self.bs)
         ws = _lib.workspace(nbytes, self.dev)
@@ -162,7 +164,7 @@ class CarrierSolver:
             n_fpi = cache.n_fpi("R")
         rc = lib.negf_g_obc_apply(
             ne, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]), p(b["bl_diag"]),
-            p(b["bg_diag"]), p(b["f_left"]), p(b["f_right"]), self.surface_tol, self.max_sweeps,
+            bg_d, p(b["f_left"]), p(b["f_right"]), self.surface_tol, self.max_sweeps,
             p(b["sl_left"]), p(b["sg_left"]), p(b["sl_right"]), p(b["sg_right"]),
             p(b["obc_status"]), p(b["obc_iters"]), p(b["obc_resid"]), p(mc), p(mh), p(mu_), ld, n_fpi,
             tol_memo, p(ws), nbytes, st)
