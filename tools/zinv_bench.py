@@ -17,8 +17,9 @@ nb = lib.negf_zinv_workspace_bytes(n, batch)
 ws = torch.empty(nb, dtype=torch.uint8, device=dev)
 def run():
     s.copy_(a)
-    return lib.negf_zinv_batched(n, batch, s.data_ptr(), x.data_ptr(), st.data_ptr(), None, ws.data_ptr(), nb,
-                                 _lib.stream_ptr())
+    rc = lib.negf_zinv_batched(n, batch, s.data_ptr(), x.data_ptr(), st.data_ptr(), None, ws.data_ptr(), nb,
+                               _lib.stream_ptr())
+    assert rc == 0, rc
 run(); torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 reps = 20
