@@ -71,8 +71,8 @@ def model_flops_per_energy(n_b: int, bs: int, kinds: int = 2) -> float:
 
 
 def exec_rgf_flops_per_energy(n_b: int, bs: int) -> float:
-    """This implementation: 31 n_b - 27 block products + n_b inversions (8 bs^3)."""
-    return 8.0 * bs ** 3 * (32 * n_b - 27)
+    """This implementation: 29 n_b - 25 block products + n_b inversions (8 bs^3)."""
+    return 8.0 * bs ** 3 * (30 * n_b - 25)
 
 
 # -- CPU legs (oracle port) ---------------------------------------------------

@@ -15,12 +15,15 @@
 // Reuse versus the reference's 43 N_B - 39 products per energy:
 //   * A_i = M_{i,i-1} x_{i-1} is shared by the retarded Schur update and y;
 //   * t, u (= -X_up), mx are shared by the retarded and both Keldysh passes;
-//   * z - y = u mxl - p u^dag is one two-term product, so
-//     (z - z^dag) - (y - y^dag) = v - v^dag needs one product;
+//   * with Q = p^dag + mxl (p = x_i B_{i,i+1}, mxl = M_{i+1,i} xl_i) the
+//     backward terms (z - z^dag) - (y - y^dag) = v - v^dag,
+//     v = u mxl - p u^dag, equal -R + R^dag with R = X_up Q: one product
+//     instead of two;
 //   * t X t^dag reuses W = X t^dag, which also feeds the lower block:
-//     lower = -X_{i+1} (p^dag + mxl) - W  (p = x_i B_{i,i+1}; the reference's
-//     X_{i+1} B_{i+1,i} x_i^dag equals -X_{i+1} p^dag by the lg symmetry of B).
-// => 31 N_B - 27 products + N_B inversions per energy (both kinds).
+//     lower = -X_{i+1} Q - W  (the reference's X_{i+1} B_{i+1,i} x_i^dag
+//     equals -X_{i+1} p^dag by the lg symmetry of B).
+// => 29 N_B - 25 products + N_B inversions per energy (both kinds;
+//    18 N_B - 16 with one Keldysh kind).
 // x_fwd lives in xr_diag and xl_fwd in xl_diag: each is overwritten in place
 // by the backward pass once its last reader has run.
 #include "ew.cuh"
@@ -313,23 +316,28 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
       G.add(c.desc(c.term(Ld(k, i + 1), sd, OP_N, tA, st1, OP_H), c.K(k, 3), st1));
     }
     RC(G.run(st));
-    // G3: X_ii = x_i - X_up mx (in place); v_k = -X_up mxl_k + p_k X_up^dag
+    // Q_k = p_k^dag + mxl_k
+    for (int q = 0; q < nk; ++q) {
+      int k = kinds[q];
+      E.add(c.K(k, 5), st1, ne, {c.K(k, 0), c.K(k, 1)}, {st1, st1}, {1, 0}, {1.0, 1.0});
+    }
+    if (nk) RC(E.run(st));
+    // G3: X_ii = x_i - X_up mx (in place); R_k = X_up Q_k. With
+    // v = -X_up mxl + p X_up^dag (rgf.py:209-226's z - y terms):
+    //   v - v^dag = -X_up (mxl + p^dag) + (mxl + p^dag)^dag X_up^dag = -R + R^dag,
+    // one product where the direct form takes two.
     G.add(c.desc(c.term(Xu(i), so, OP_N, tS, st1, OP_N), Xd(i), sd, -1.0, Xd(i), sd, 1.0));
     for (int q = 0; q < nk; ++q) {
       int k = kinds[q];
-      ZGemmDesc d = c.desc(c.term(Xu(i), so, OP_N, c.K(k, 1), st1, OP_N, true), c.K(k, 2), st1);
-      d.nterms = 2;
-      d.t[1] = c.term(c.K(k, 0), st1, OP_N, Xu(i), so, OP_H);
-      G.add(d);
+      G.add(c.desc(c.term(Xu(i), so, OP_N, c.K(k, 5), st1, OP_N), c.K(k, 2), st1));
     }
     RC(G.run(st));
     if (nk == 0) continue;
-    // E_k = xl_k,i + v_k - v_k^dag ; Q_k = p_k^dag + mxl_k
+    // E_k = xl_k,i - R_k + R_k^dag
     for (int q = 0; q < nk; ++q) {
       int k = kinds[q];
       E.add(c.K(k, 4), st1, ne, {Ld(k, i), c.K(k, 2), c.K(k, 2)}, {sd, st1, st1}, {0, 0, 1},
-            {1.0, 1.0, -1.0});
-      E.add(c.K(k, 5), st1, ne, {c.K(k, 0), c.K(k, 1)}, {st1, st1}, {1, 0}, {1.0, 1.0});
+            {1.0, -1.0, 1.0});
     }
     RC(E.run(st));
     // G4: XL_k,ii = t W_k + E_k ; XL_k,up = (X_{i+1} Q_k + W_k)^dag
