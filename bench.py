@@ -71,8 +71,8 @@ def model_flops_per_energy(n_b: int, bs: int, kinds: int = 2) -> float:
 
 
 def exec_rgf_flops_per_energy(n_b: int, bs: int) -> float:
-    """This implementation: 29 n_b - 25 block products + n_b inversions (8 bs^3)."""
-    return 8.0 * bs ** 3 * (30 * n_b - 25)
+    """This implementation: 27 n_b - 23 block products + n_b inversions (8 bs^3)."""
+    return 8.0 * bs ** 3 * (28 * n_b - 23)
 
 
 # -- CPU legs (oracle port) ---------------------------------------------------

@@ -15,15 +15,14 @@
 // Reuse versus the reference's 43 N_B - 39 products per energy:
 //   * A_i = M_{i,i-1} x_{i-1} is shared by the retarded Schur update and y;
 //   * t, u (= -X_up), mx are shared by the retarded and both Keldysh passes;
-//   * with Q = p^dag + mxl (p = x_i B_{i,i+1}, mxl = M_{i+1,i} xl_i) the
-//     backward terms (z - z^dag) - (y - y^dag) = v - v^dag,
-//     v = u mxl - p u^dag, equal -R + R^dag with R = X_up Q: one product
-//     instead of two;
-//   * t X t^dag reuses W = X t^dag, which also feeds the lower block:
-//     lower = -X_{i+1} Q - W  (the reference's X_{i+1} B_{i+1,i} x_i^dag
-//     equals -X_{i+1} p^dag by the lg symmetry of B).
-// => 29 N_B - 25 products + N_B inversions per energy (both kinds;
-//    18 N_B - 16 with one Keldysh kind).
+//   * with Q = p^dag + mxl (p = x_i B_{i,i+1}, mxl = M_{i+1,i} xl_i) and
+//     T = X_{i+1} Q, W = XL_{i+1} t^dag, the lower block is -T - W (the
+//     reference's X_{i+1} B_{i+1,i} x_i^dag equals -X_{i+1} p^dag by the lg
+//     symmetry of B) and the diagonal update t W + (z - z^dag) - (y - y^dag)
+//     is the anti-Hermitian part of Z = t (W + 2T): one product where the
+//     direct form takes three (see the backward sweep; B^lg anti-Hermitian).
+// => 27 N_B - 23 products + N_B inversions per energy (both kinds;
+//    17 N_B - 15 with one Keldysh kind).
 // x_fwd lives in xr_diag and xl_fwd in xl_diag: each is overwritten in place
 // by the backward pass once its last reader has run.
 #include "ew.cuh"
@@ -322,33 +321,39 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
       E.add(c.K(k, 5), st1, ne, {c.K(k, 0), c.K(k, 1)}, {st1, st1}, {1, 0}, {1.0, 1.0});
     }
     if (nk) RC(E.run(st));
-    // G3: X_ii = x_i - X_up mx (in place); R_k = X_up Q_k. With
-    // v = -X_up mxl + p X_up^dag (rgf.py:209-226's z - y terms):
-    //   v - v^dag = -X_up (mxl + p^dag) + (mxl + p^dag)^dag X_up^dag = -R + R^dag,
-    // one product where the direct form takes two.
+    // G3: X_ii = x_i - X_up mx (in place); T_k = X_{i+1} Q_k.
+    // The Keldysh diagonal is XL_ii = xl_i + t W + (z - z^dag) - (y - y^dag):
+    //   (z - z^dag) - (y - y^dag) = v - v^dag with v = -X_up mxl + p X_up^dag
+    //   = -X_up Q + Q^dag X_up^dag = t T - (t T)^dag          (X_up = -t X_{i+1})
+    // and t W = t XL_{i+1} t^dag is anti-Hermitian (B^lg is, so is XL), hence
+    //   XL_ii = xl_i + (Z - Z^dag)/2 with Z = t (W + 2 T):
+    // one product where the direct form takes three (t W, u mxl, p u^dag).
     G.add(c.desc(c.term(Xu(i), so, OP_N, tS, st1, OP_N), Xd(i), sd, -1.0, Xd(i), sd, 1.0));
     for (int q = 0; q < nk; ++q) {
       int k = kinds[q];
-      G.add(c.desc(c.term(Xu(i), so, OP_N, c.K(k, 5), st1, OP_N), c.K(k, 2), st1));
+      G.add(c.desc(c.term(Xd(i + 1), sd, OP_N, c.K(k, 5), st1, OP_N), c.K(k, 2), st1));
     }
     RC(G.run(st));
     if (nk == 0) continue;
-    // E_k = xl_k,i - R_k + R_k^dag
+    // F_k = W_k + 2 T_k ; XL_k,up = T_k^dag + W_k^dag  (= (-lower)^dag, lower = -T - W)
     for (int q = 0; q < nk; ++q) {
       int k = kinds[q];
-      E.add(c.K(k, 4), st1, ne, {Ld(k, i), c.K(k, 2), c.K(k, 2)}, {sd, st1, st1}, {0, 0, 1},
-            {1.0, -1.0, 1.0});
+      E.add(c.K(k, 4), st1, ne, {c.K(k, 3), c.K(k, 2)}, {st1, st1}, {0, 0}, {1.0, 2.0});
+      E.add(Lu(k, i), so, ne, {c.K(k, 2), c.K(k, 3)}, {st1, st1}, {1, 1}, {1.0, 1.0});
     }
     RC(E.run(st));
-    // G4: XL_k,ii = t W_k + E_k ; XL_k,up = (X_{i+1} Q_k + W_k)^dag
+    // G4: Z_k = t F_k
     for (int q = 0; q < nk; ++q) {
       int k = kinds[q];
-      G.add(c.desc(c.term(tA, st1, OP_N, c.K(k, 3), st1, OP_N), Ld(k, i), sd, 1.0, c.K(k, 4), st1,
-                   1.0));
-      G.add(c.desc(c.term(Xd(i + 1), sd, OP_N, c.K(k, 5), st1, OP_N), Lu(k, i), so, 1.0,
-                   c.K(k, 3), st1, 1.0, /*transD=*/1));
+      G.add(c.desc(c.term(tA, st1, OP_N, c.K(k, 4), st1, OP_N), c.K(k, 0), st1));
     }
     RC(G.run(st));
+    // XL_k,ii = xl_k,i + (Z_k - Z_k^dag)/2 (in place)
+    for (int q = 0; q < nk; ++q) {
+      int k = kinds[q];
+      E.add(Ld(k, i), sd, ne, {Ld(k, i), c.K(k, 0), c.K(k, 0)}, {sd, st1, st1}, {0, 0, 1}, {1.0, 0.5, -0.5});
+    }
+    RC(E.run(st));
   }
   if (a.symmetrize)
     for (int q = 0; q < nk; ++q) RC(antiherm_inplace(a.xl_diag[kinds[q]], bs2, bs, ne * n, st));

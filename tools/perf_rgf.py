@@ -23,7 +23,7 @@ for ne in [int(x) for x in (sys.argv[3].split(',') if len(sys.argv) > 3 else ['1
         selected_solve_batched(md, mu, ml, bl, bg, symmetrize=True, out=out, check=False)
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    f_exec = 8.0 * bs ** 3 * (30 * nb_ - 25) * ne
+    f_exec = 8.0 * bs ** 3 * (28 * nb_ - 23) * ne
     f_model = 8.0 * bs ** 3 * (38 * nb_ - 33) * ne
     print(f"n_b={nb_} bs={bs} n_e={ne}: {ms:.1f} ms/solve  {ne / ms * 1e3:.1f} energies/s  "
           f"exec {f_exec / ms / 1e9:.2f} TFLOP/s  model {f_model / ms / 1e9:.2f} TFLOP/s", flush=True)
