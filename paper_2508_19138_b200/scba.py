@@ -212,21 +212,34 @@ class ScreenedSolver:
         import contextlib
 
         T = timer or (lambda name: contextlib.nullcontext())
-        lib, p, b, o = self.lib, _lib.ptr, self.buffers(n_e), self.opt
-        st = _lib.stream_ptr(self.dev)
+        b = self.buffers(n_e)
+        with T("W: assembly"):
+            self._assemble(b, n_e)
+        with T("W: OBC (Sancho+Stein)"):
+            self._closure(b, n_e, memo, check)
+        with T("W: RGF"):
+            self._rgf(b, n_e)
+        if check:
+            raise_on_status(b["rgf_status"])
+        return b
+
+    def _assemble(self, b: dict, n_e: int) -> None:
+        """scba.py:784-796: M_W = I - trunc3(V P^R), B^<> = trunc3((V P^<>) V)."""
+        lib, p = self.lib, _lib.ptr
         vd, vu, vl = self.v
-        _t = T("W: assembly")
-        _t.__enter__()
         nbytes = lib.negf_w_assemble_workspace_bytes(n_e, self.n_b, self.bs)
         ws = _lib.workspace(nbytes, self.dev)
         rc = lib.negf_w_assemble(n_e, self.n_b, self.bs, p(vd), p(vu), p(vl), p(b["pr_diag"]), p(b["pr_upper"]),
                                  p(b["pr_lower"]), p(b["pl_diag"]), p(b["pl_upper"]), p(b["pg_diag"]),
                                  p(b["pg_upper"]), p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]),
-                                 p(b["bl_diag"]), p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]), p(ws), nbytes, st)
+                                 p(b["bl_diag"]), p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]), p(ws), nbytes,
+                                 _lib.stream_ptr(self.dev))
         _lib.check(rc, "negf_w_assemble")
-        _t.__exit__()
-        _t = T("W: OBC (Sancho+Stein)")
-        _t.__enter__()
+
+    def _closure(self, b: dict, n_e: int, memo, check: bool) -> None:
+        """scba.py:839-858: surfaces (Sancho, or Beyn like the reference), Stein
+        corner sources, both through the memoizer when it is on."""
+        lib, p, o = self.lib, _lib.ptr, self.opt
         nbytes = lib.negf_w_obc_workspace_bytes(n_e, self.bs)
         ws = _lib.workspace(nbytes, self.dev)
         memo_args = [None] * 6 + [0, 20, 10, 0.0]
@@ -245,7 +258,7 @@ class ScreenedSolver:
                                   o.surface_tol, 100, o.stein_tol, o.stein_max_iter,
                                   p(_lib.power_start_vector(self.bs, self.dev)), p(b["obc_status"]),
                                   p(b["obc_iters"]), p(b["stein_status"]), p(b["stein_iters"]), *memo_args,
-                                  p(x_surface), p(ws), nbytes, st)
+                                  p(x_surface), p(ws), nbytes, _lib.stream_ptr(self.dev))
         _lib.check(rc, "negf_w_obc_apply")
         if memo is not None:
             if x_surface is None:
@@ -259,9 +272,10 @@ class ScreenedSolver:
                 raise SpectralRadiusError("W boundary Stein: spectral radius estimate >= 1 (Kronecker fallback not ported)")
             if np.any(ss):
                 raise ConvergenceError(f"geometric Stein did not reach tol {o.stein_tol} in {o.stein_max_iter} squarings")
-        _t.__exit__()
-        _t = T("W: RGF")
-        _t.__enter__()
+
+    def _rgf(self, b: dict, n_e: int) -> None:
+        """Selected solve of the W system, symmetrized (scba.py:1084-1087)."""
+        lib, p = self.lib, _lib.ptr
         nbytes = lib.negf_rgf_workspace_bytes(n_e, self.n_b, self.bs)
         ws = _lib.workspace(nbytes, self.dev)
         b["rgf_status"].zero_()
@@ -269,12 +283,8 @@ class ScreenedSolver:
             n_e, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]), p(b["bl_diag"]),
             p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]), p(b["wr_diag"]), p(b["wr_upper"]),
             p(b["wr_lower"]), p(b["wl_diag"]), p(b["wl_upper"]), p(b["wg_diag"]), p(b["wg_upper"]), 1,
-            p(b["rgf_status"]), None, p(ws), nbytes, st)
+            p(b["rgf_status"]), None, p(ws), nbytes, _lib.stream_ptr(self.dev))
         _lib.check(rc, "negf_rgf_selected_solve_batched")
-        _t.__exit__()
-        if check:
-            raise_on_status(b["rgf_status"])
-        return b
 
 
 @dataclass
