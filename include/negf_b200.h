@@ -133,6 +133,15 @@ int negf_obc_sancho_batched(int batch, int bs, const void* m, const void* n, con
  * select[b] != 0; the others keep x and get status 0, iters 0 (the direct leg
  * of the memoizer below). */
 
+/* obc_fixed_point (obc.py:108-135), batched: x <- (m - n x n')^-1 from x0
+ * (NULL = zeros) until |x_new - x|_F / |x_new|_F < tol; status as Sancho's
+ * (1 singular update, 2 not converged in max_iter), iters, resid (may be NULL:
+ * the final relative update). Synchronises `stream` every 16 updates. */
+size_t negf_fixed_point_workspace_bytes(int batch, int bs);
+int negf_obc_fixed_point_batched(int batch, int bs, const void* m, const void* n, const void* np, const void* x0,
+                                 double tol, int max_iter, void* x, int* status, int* iters, double* resid,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+
 /* sigma_lg_obc (obc.py:460-486), batched: Sigma^R = n x n',
  * Sigma^< = -f (Sigma^R - Sigma^R^dag), Sigma^> = (1-f)(Sigma^R - Sigma^R^dag)
  * with f[b] = fermi(E_b - mu) (device double). Outputs may be NULL. */

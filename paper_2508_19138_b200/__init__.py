@@ -41,11 +41,13 @@ from .obc import (
     SurfaceCache,
     SurfaceResult,
     beyn_batched,
+    fixed_point_batched,
     fixed_point_step,
     memoized_stein_batched,
     memoized_surface_batched,
     obc_beyn,
     obc_sancho_rubio,
+    obc_fixed_point,
     sancho_batched,
     sigma_lg_obc,
     stein_geometric,
@@ -58,7 +60,7 @@ __all__ = [
     "Contacts", "ContactConfig", "ballistic_observables", "ballistic_run", "convolve_energy", "retarded_from_lg",
     "PartitionPlan", "balanced_partition_plan", "dist_selected_solve", "make_partition_plan", "energy_chunks",
     "transpose_distribution", "ContactBlocks", "ObcSigma", "SurfaceCache", "SurfaceResult", "beyn_batched",
-    "fixed_point_step", "memoized_stein_batched", "memoized_surface_batched", "obc_beyn", "obc_sancho_rubio",
+    "fixed_point_batched", "fixed_point_step", "memoized_stein_batched", "memoized_surface_batched", "obc_beyn", "obc_fixed_point", "obc_sancho_rubio",
     "sancho_batched", "sigma_lg_obc", "stein_geometric", "BeynOptions", "EnergyGrid", "MemoizerOptions",
     "ScbaOptions", "scba_run", "scba_run_reference_api",
     "FULL", "LG_COMPRESSED", "BlockMatrix",

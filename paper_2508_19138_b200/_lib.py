@@ -47,6 +47,8 @@ _SIGNATURES: dict[str, tuple] = {
     "negf_zinv_batched": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "negf_sancho_workspace_bytes": (_sz, [_i, _i]),
     "negf_obc_sancho_batched": (_i, [_i, _i, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "negf_fixed_point_workspace_bytes": (_sz, [_i, _i]),
+    "negf_obc_fixed_point_batched": (_i, [_i, _i] + [_vp] * 4 + [_d, _i] + [_vp] * 4 + [_vp, _sz, _vp]),
     "negf_sigma_lg_obc_workspace_bytes": (_sz, [_i, _i]),
     "negf_sigma_lg_obc_batched": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "negf_stein_workspace_bytes": (_sz, [_i, _i]),

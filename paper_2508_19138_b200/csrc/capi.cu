@@ -131,6 +131,16 @@ int negf_obc_sancho_batched(int batch, int bs, const void* m, const void* n, con
                         (cudaStream_t)stream, select);
 }
 
+size_t negf_fixed_point_workspace_bytes(int batch, int bs) { return fixed_point_workspace_bytes(batch, bs); }
+
+int negf_obc_fixed_point_batched(int batch, int bs, const void* m, const void* n, const void* np, const void* x0,
+                                 double tol, int max_iter, void* x, int* status, int* iters, double* resid,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+  if (batch < 0 || bs < 1 || !m || !n || !np || !x || !status || !iters || !(tol > 0.0) || max_iter < 1) return -1;
+  return fixed_point_batched((const z_t*)m, (const z_t*)n, (const z_t*)np, batch, bs, (const z_t*)x0, tol, max_iter,
+                             (z_t*)x, status, iters, resid, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
 size_t negf_memo_workspace_bytes(int map, int n_side, int n_kind, int bs) {
   return memo_workspace_bytes(map, n_side, n_kind, bs);
 }

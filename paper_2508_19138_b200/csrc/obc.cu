@@ -214,6 +214,72 @@ __global__ void g_assemble_kernel(GAssembleArgs a) {
   }
 }
 
+// obc_fixed_point convergence test (obc.py:122-133): x <- x_new on active
+// problems; freeze those with |x_new - x| / |x_new| < tol.
+__global__ void fp_step_kernel(z_t* x, const z_t* xn, long long n2, double tol, int* active, const int* inv_st,
+                               int* status, int* iters, double* resid, int it, int* n_act) {
+  __shared__ double red[2][32];
+  __shared__ int s_keep;
+  const int b = blockIdx.x;
+  if (!active[b]) return;
+  z_t* X = x + b * n2;
+  const z_t* XN = xn + b * n2;
+  double d2 = 0.0, c2 = 0.0;
+  for (long long e = threadIdx.x; e < n2; e += blockDim.x) {
+    const z_t v = XN[e], u = X[e];
+    const double dr = v.x - u.x, di = v.y - u.y;
+    d2 += dr * dr + di * di;
+    c2 += v.x * v.x + v.y * v.y;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    d2 += __shfl_down_sync(0xffffffffu, d2, o);
+    c2 += __shfl_down_sync(0xffffffffu, c2, o);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { red[0][w] = d2; red[1][w] = c2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double D = 0.0, C = 0.0;
+    for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) { D += red[0][i]; C += red[1][i]; }
+    int keep = 1;
+    if (inv_st[b]) {
+      status[b] = OBC_SINGULAR;
+      iters[b] = it;
+      active[b] = 0;
+      keep = 0;
+    } else {
+      const double num = sqrt(D), den = sqrt(C);
+      if (den > 0.0 && num / den < tol) {
+        active[b] = 0;
+        iters[b] = it;
+        if (resid) resid[b] = num / den;
+      } else {
+        atomicAdd(n_act, 1);
+      }
+    }
+    s_keep = keep;
+  }
+  __syncthreads();
+  if (s_keep)
+    for (long long e = threadIdx.x; e < n2; e += blockDim.x) X[e] = XN[e];
+}
+
+__global__ void fp_init_kernel(int* active, int* status, int* iters, int n) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  active[b] = 1;
+  status[b] = OBC_OK;
+  iters[b] = 0;
+}
+
+__global__ void fp_finish_kernel(const int* active, int* status, int* iters, int max_iter, int n) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < n && active[b] && status[b] == OBC_OK) {
+    status[b] = OBC_NOT_CONVERGED;
+    iters[b] = max_iter;
+  }
+}
+
 __global__ void count_active_kernel(const int* active, int n, int* n_act) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < n && active[b]) atomicAdd(n_act, 1);
@@ -340,6 +406,73 @@ int sancho_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs,
   {
     ProfScope ps_sancho_finish_kernel(PROF_OTHER, (cudaStream_t)(st));
     sancho_finish_kernel<<<batch, 256, 0, st>>>(x, g, bs, thr, active, inv_st, status, resid, select);
+    NEGF_LAUNCHED();
+  }
+  return 0;
+}
+
+size_t fixed_point_workspace_bytes(int batch, int bs) {
+  const size_t blk = a256(sizeof(z_t) * (size_t)batch * bs * bs);
+  return 3 * blk + a256(zinv_workspace_bytes(bs, batch)) + 4 * a256(sizeof(int) * (size_t)batch + 64);
+}
+
+int fixed_point_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs, const z_t* x0, double tol,
+                        int max_iter, z_t* x, int* status, int* iters, double* resid, void* ws, size_t ws_bytes,
+                        cudaStream_t st) {
+  if (batch <= 0) return 0;
+  if (ws_bytes < fixed_point_workspace_bytes(batch, bs)) return -4;
+  const long long n2 = (long long)bs * bs;
+  const size_t bytes = sizeof(z_t) * (size_t)batch * n2;
+  char* w = reinterpret_cast<char*>(ws);
+  auto take = [&](size_t b_) { char* r = w; w += a256(b_); return r; };
+  z_t* T = (z_t*)take(bytes);
+  z_t* S = (z_t*)take(bytes);
+  z_t* XN = (z_t*)take(bytes);
+  int* active = (int*)take(sizeof(int) * batch + 64);
+  int* inv_st = (int*)take(sizeof(int) * batch + 64);
+  int* n_act = (int*)take(sizeof(int) * 4 + 64);
+  take(sizeof(int) * batch + 64);
+  void* inv_ws = w;
+  const size_t inv_bytes = zinv_workspace_bytes(bs, batch);
+  if (x0) NEGF_CUDA_CHECK(cudaMemcpyAsync(x, x0, bytes, cudaMemcpyDeviceToDevice, st));
+  else NEGF_CUDA_CHECK(cudaMemsetAsync(x, 0, bytes, st));
+  {
+    ProfScope ps(PROF_OTHER, st);
+    fp_init_kernel<<<(batch + 127) / 128, 128, 0, st>>>(active, status, iters, batch);
+    NEGF_LAUNCHED();
+  }
+  InvAux aux;
+  aux.status = inv_st; aux.status_code = 1; aux.u_spread = nullptr; aux.spread_stride = 0; aux.active = active;
+  int h_act = batch;
+  for (int it = 1; it <= max_iter && h_act > 0; ++it) {
+    ZGemmDesc d = zdesc_default();  // T = n x ; S = m - T n'
+    d.M = bs; d.N = bs; d.batch = batch; d.active = active;
+    d.t[0] = zterm(n, n2, bs, OP_N, x, n2, bs, OP_N, bs);
+    for (int i = 1; i < kMaxTerms; ++i) d.t[i] = d.t[0];
+    d.D = T; d.sD = n2; d.ldd = bs;
+    RC(zgemm_launch(d, st));
+    d.t[0] = zterm(T, n2, bs, OP_N, np, n2, bs, OP_N, bs);
+    for (int i = 1; i < kMaxTerms; ++i) d.t[i] = d.t[0];
+    d.alpha = make_double2(-1.0, 0.0);
+    d.C = m; d.sC = n2; d.ldc = bs; d.beta = make_double2(1.0, 0.0);
+    d.D = S;
+    RC(zgemm_launch(d, st));
+    NEGF_CUDA_CHECK(cudaMemsetAsync(inv_st, 0, sizeof(int) * batch, st));
+    RC(zinv_batched(S, n2, bs, XN, n2, bs, bs, batch, aux, inv_ws, inv_bytes, st));
+    NEGF_CUDA_CHECK(cudaMemsetAsync(n_act, 0, sizeof(int), st));
+    {
+      ProfScope ps(PROF_OTHER, st);
+      fp_step_kernel<<<batch, 256, 0, st>>>(x, XN, n2, tol, active, inv_st, status, iters, resid, it, n_act);
+      NEGF_LAUNCHED();
+    }
+    if ((it & 15) == 0 || it == max_iter) {  // host check every 16 updates
+      NEGF_CUDA_CHECK(cudaMemcpyAsync(&h_act, n_act, sizeof(int), cudaMemcpyDeviceToHost, st));
+      NEGF_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+  }
+  {
+    ProfScope ps(PROF_OTHER, st);
+    fp_finish_kernel<<<(batch + 127) / 128, 128, 0, st>>>(active, status, iters, max_iter, batch);
     NEGF_LAUNCHED();
   }
   return 0;

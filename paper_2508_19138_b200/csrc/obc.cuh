@@ -22,6 +22,14 @@ int sancho_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs,
 // (select, optional: only problems with select[b] != 0 are solved; x, status,
 // iters and resid of the others are left as they are, status 0, iters 0.)
 
+// obc_fixed_point (obc.py:108-135) for `batch` problems: x <- (m - n x n')^-1
+// from x0 (NULL: zeros) until |x_new - x|_F / |x_new|_F < tol; frozen problems
+// stop updating. status: OBC_OK / OBC_SINGULAR / OBC_NOT_CONVERGED.
+size_t fixed_point_workspace_bytes(int batch, int bs);
+int fixed_point_batched(const z_t* m, const z_t* n, const z_t* np, int batch, int bs, const z_t* x0, double tol,
+                        int max_iter, z_t* x, int* status, int* iters, double* resid, void* ws, size_t ws_bytes,
+                        cudaStream_t st);
+
 // G-side closure of one batch: per side, read the contact cell from the
 // assembled M (energy-major tridiagonal), solve the surface problem, and
 // fold Sigma^R_obc, Sigma^<_obc, Sigma^>_obc into the corner blocks.

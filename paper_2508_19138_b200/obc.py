@@ -412,3 +412,37 @@ def obc_beyn(m_tilde_blocks, contour: dict | None = None, svd_tol: float = 1e-8,
     x, modes = beyn_batched(m, n, npr, int(params["n_quad"]), float(params["radius"]), complex(params["center"]),
                             svd_tol)
     return BeynResult(x[0].cpu().numpy(), int(modes[0]), float("nan"), no_modes_warning=int(modes[0]) == 0)
+
+
+def fixed_point_batched(m: torch.Tensor, n: torch.Tensor, n_prime: torch.Tensor, x0: torch.Tensor | None = None,
+                        tol: float = 1e-10, max_iter: int = 5000):
+    """obc_fixed_point for a batch: returns (x, iters, status, resid) tensors
+    (status 0 converged, 1 singular update, 2 not converged)."""
+    if tol <= 0:
+        raise ValueError(f"tol must be positive, got {tol}")
+    lib = _lib.load()
+    batch, bs = m.shape[0], m.shape[-1]
+    dev = m.device
+    x = torch.empty_like(m)
+    status = torch.zeros(batch, dtype=torch.int32, device=dev)
+    iters = torch.zeros(batch, dtype=torch.int32, device=dev)
+    resid = torch.full((batch,), float("nan"), dtype=torch.float64, device=dev)
+    nbytes = lib.negf_fixed_point_workspace_bytes(batch, bs)
+    ws = _lib.workspace(nbytes, dev)
+    rc = lib.negf_obc_fixed_point_batched(batch, bs, m.data_ptr(), n.data_ptr(), n_prime.data_ptr(), _lib.ptr(x0),
+                                          tol, max_iter, x.data_ptr(), status.data_ptr(), iters.data_ptr(),
+                                          resid.data_ptr(), ws.data_ptr(), nbytes, _lib.stream_ptr(dev))
+    _lib.check(rc, "negf_obc_fixed_point_batched")
+    return x, iters, status, resid
+
+
+def obc_fixed_point(c, x0=None, max_iter: int = 5000, tol: float = 1e-10, device="cuda") -> SurfaceResult:
+    """obc.py:108-135 signature: direct iteration x <- (m - n x n')^-1 from x0
+    (default 0); not converging is reported (converged=False), not raised."""
+    dev = torch.device(device)
+    x, iters, status, resid = fixed_point_batched(_t(c.m, dev)[None], _t(c.n, dev)[None], _t(c.n_prime, dev)[None],
+                                                  None if x0 is None else _t(x0, dev)[None], tol, max_iter)
+    st, it = int(status[0]), int(iters[0])
+    if st == OBC_SINGULAR:
+        raise SingularBlockError(f"singular surface update at fixed-point iteration {it}")
+    return SurfaceResult(x[0].cpu().numpy(), it, st == OBC_OK, float(resid[0]))
