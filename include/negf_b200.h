@@ -206,8 +206,8 @@ int negf_g_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
                      const double* f_right, double tol, int max_iter, void* sl_left,
                      void* sg_left, void* sl_right, void* sg_right, int* status, int* iters,
                      double* resid, void* memo_cache, int* memo_has, int* memo_used,
-                     long long memo_ld, int n_fpi, double memo_tol, void* workspace,
-                     size_t workspace_bytes, void* stream);
+                     long long memo_ld, int n_fpi, double memo_tol, const void* x_surface,
+                     void* workspace, size_t workspace_bytes, void* stream);
 /* Memoizer (optional; memo_cache NULL = direct Sancho for every problem, the
  * reference with MemoizerOptions(enabled=False)): memo_cache holds the cached
  * surface of side g (0 left, 1 right) and batch energy e at block
@@ -216,7 +216,9 @@ int negf_g_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
  * problems are refreshed (negf_memo_refresh_batched, n_fpi, memo_tol), the
  * rest solved by Sancho; every result is written back to the cache
  * (has = 1) and used[] = 1 marks memoized calls (the reference's
- * cache.stats). */
+ * cache.stats). x_surface (optional, [2][n_e][bs][bs]): surface blocks from
+ * the caller's solver (Beyn / fixed point, scba.py:577-614); replaces the
+ * Sancho and memoizer step. */
 
 /* Carrier system assembly (scba.py:670-727) for n_e energies:
  *   M_ii = (E + i eta) I - H_ii - SR_ii,  M_{i,i+-1} = -H - SR,

@@ -61,7 +61,7 @@ _SIGNATURES: dict[str, tuple] = {
     "negf_g_obc_apply": (
         _i,
         [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-         _vp, _vp, _vp, _ll, _i, _d, _vp, _sz, _vp],
+         _vp, _vp, _vp, _ll, _i, _d, _vp, _vp, _sz, _vp],
     ),
     "negf_g_assemble": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _d] + [_vp] * 7 + [_vp] * 7 + [_vp]),
     "negf_observables": (_i, [_i, _i, _i] + [_vp] * 14),

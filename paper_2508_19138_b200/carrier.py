@@ -48,13 +48,21 @@ class CarrierSolver:
 
     def __init__(self, h, eta: float, contacts: Contacts, surface_tol: float = 1e-8,
                  max_sweeps: int = 100, device="cuda", streams: int = 1,
-                 greater: str = "recursion") -> None:
+                 greater: str = "recursion", retarded_method: str = "sancho", beyn=None) -> None:
         """``greater``: "recursion" runs the greater Keldysh pass like the
         reference; "identity" derives G^> = G^< + G^R - G^R^dag on the
         selected blocks (exact for the carrier system), saving
         ~40% of the RGF work."""
         if greater not in ("recursion", "identity"):
             raise ValueError(f"unknown greater mode {greater!r}")
+        if retarded_method not in ("sancho", "beyn", "fixed_point"):
+            raise ValueError(f"unknown retarded method {retarded_method!r}")
+        self.retarded_method = retarded_method
+        if beyn is None:
+            from .scba import BeynOptions
+
+            beyn = BeynOptions()
+        self.beyn = beyn
         self.greater = greater
         self.dev = torch.device(device)
         self.lib = _lib.load()
@@ -157,7 +165,13 @@ class CarrierSolver:
         ws = _lib.workspace(nbytes, self.dev)
         mc = mh = mu_ = None
         ld, n_fpi, tol_memo = 0, 20, 0.0
-        if memo is not None:
+        x_surface = None
+        if self.retarded_method != "sancho":
+            from .obc import contact_cells, solve_surfaces
+
+            x_surface = solve_surfaces(*contact_cells(b["m_diag"], b["m_upper"], b["m_lower"]),
+                                       self.retarded_method, memo, ("G", "R"), self.surface_tol, self.beyn)
+        elif memo is not None:
             cache, ld, e0, tol_memo = memo
             xs, hs, us = cache.slot(("G", "R"), 2, ld, self.bs, self.dev)
             mc, mh, mu_ = xs[0, e0], hs[0, e0:], us[0, e0:]
@@ -167,9 +181,9 @@ class CarrierSolver:
             bg_d, p(b["f_left"]), p(b["f_right"]), self.surface_tol, self.max_sweeps,
             p(b["sl_left"]), p(b["sg_left"]), p(b["sl_right"]), p(b["sg_right"]),
             p(b["obc_status"]), p(b["obc_iters"]), p(b["obc_resid"]), p(mc), p(mh), p(mu_), ld, n_fpi,
-            tol_memo, p(ws), nbytes, st)
+            tol_memo, p(x_surface), p(ws), nbytes, st)
         _lib.check(rc, "negf_g_obc_apply")
-        if memo is not None:
+        if memo is not None and x_surface is None:
             cache.record(us, e0, ne)
         if check:
             raise_on_obc_status(b["obc_status"].cpu().numpy(), b["obc_iters"].cpu().numpy(),

@@ -178,8 +178,8 @@ int negf_g_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
                      const double* f_right, double tol, int max_iter, void* sl_left,
                      void* sg_left, void* sl_right, void* sg_right, int* status, int* iters,
                      double* resid, void* memo_cache, int* memo_has, int* memo_used,
-                     long long memo_ld, int n_fpi, double memo_tol, void* workspace,
-                     size_t workspace_bytes, void* stream) {
+                     long long memo_ld, int n_fpi, double memo_tol, const void* x_surface,
+                     void* workspace, size_t workspace_bytes, void* stream) {
   if (n_e < 0 || n_b < 2 || bs < 1 || !m_diag || !m_upper || !m_lower || !f_left || !f_right)
     return -1;
   if (!status || !iters) return -1;
@@ -194,6 +194,7 @@ int negf_g_obc_apply(int n_e, int n_b, int bs, void* m_diag, const void* m_upper
   a.status = status; a.iters = iters; a.resid = resid;
   a.memo_cache = (z_t*)memo_cache; a.memo_has = memo_has; a.memo_used = memo_used;
   a.memo_ld = memo_ld; a.n_fpi = n_fpi; a.memo_tol = memo_tol;
+  a.x_surface = (const z_t*)x_surface;
   return g_obc_apply(a, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 

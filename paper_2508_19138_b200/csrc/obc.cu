@@ -518,7 +518,11 @@ int g_obc_apply(const GObcArgs& a, void* ws, size_t ws_bytes, cudaStream_t st) {
   RC(gather(cn + hn, a.m_upper + (nb - 2) * n2, so));    // n  = M_{N-2,N-1}
   RC(gather(cnp, a.m_upper, so));                        // n' = M_01
   RC(gather(cnp + hn, a.m_lower + (nb - 2) * n2, so));   // n' = M_{N-1,N-2}
-  if (a.memo_cache) {
+  if (a.x_surface) {  // surfaces supplied by the caller (Beyn / fixed point, scba.py:577-614)
+    NEGF_CUDA_CHECK(cudaMemcpyAsync(xr, a.x_surface, 2 * half, cudaMemcpyDeviceToDevice, st));
+    NEGF_CUDA_CHECK(cudaMemsetAsync(a.status, 0, sizeof(int) * 2 * ne, st));
+    NEGF_CUDA_CHECK(cudaMemsetAsync(a.iters, 0, sizeof(int) * 2 * ne, st));
+  } else if (a.memo_cache) {
     // refresh cached surfaces first (staged through t1); Sancho only where rejected
     RC(memo_gather(a.memo_cache, a.memo_ld, a.memo_has, a.memo_ld, 2, ne, bs, t1, has_buf, st));
     RC(memo_refresh(MEMO_SURFACE, 2 * ne, 1, bs, cm, cn, cnp, nullptr, nullptr, a.n_fpi, a.memo_tol, t1,

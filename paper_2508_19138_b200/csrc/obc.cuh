@@ -61,6 +61,8 @@ struct GObcArgs {
   long long memo_ld = 0;
   int n_fpi = 20;
   double memo_tol = 0.0;
+  // optional [2][n_e] surface blocks computed by the caller (replaces Sancho)
+  const z_t* x_surface = nullptr;
 };
 size_t g_obc_workspace_bytes(int n_e, int bs);
 int g_obc_apply(const GObcArgs& a, void* ws, size_t ws_bytes, cudaStream_t st);

@@ -446,3 +446,53 @@ def obc_fixed_point(c, x0=None, max_iter: int = 5000, tol: float = 1e-10, device
     if st == OBC_SINGULAR:
         raise SingularBlockError(f"singular surface update at fixed-point iteration {it}")
     return SurfaceResult(x[0].cpu().numpy(), it, st == OBC_OK, float(resid[0]))
+
+
+def solve_surfaces(m: torch.Tensor, n: torch.Tensor, n_prime: torch.Tensor, method: str, memo=None,
+                   slot: tuple = ("G", "R"), surface_tol: float = 1e-8, beyn=None) -> torch.Tensor:
+    """_retarded_surface (scba.py:577-614) for a batch of contact cells
+    stacked [2 sides][n_e]: the direct solver ``method`` ("beyn" or
+    "fixed_point"; Sancho runs inside the library's closure kernels), through
+    the memoizer when ``memo`` = (SurfaceCache, ld, e0, tol_memo) is given:
+    cached problems are refreshed with fixed_point_step, the direct solver
+    runs on the rest only, and every result goes back to the cache."""
+    if method == "beyn":
+        o = beyn
+        direct = lambda a, b_, c_: beyn_batched(a, b_, c_, o.n_quad, o.radius, 0.0, o.svd_tol)[0]
+    elif method == "fixed_point":
+        def direct(a, b_, c_):
+            x, it, st, _ = fixed_point_batched(a, b_, c_, None, surface_tol)
+            stn = st.cpu().numpy()
+            if np.any(stn == OBC_SINGULAR):
+                b0 = int(np.flatnonzero(stn == OBC_SINGULAR)[0])
+                raise SingularBlockError(f"singular surface update at fixed-point iteration {int(it[b0])}")
+            return x  # like the reference, an unconverged iterate is used as is
+    else:
+        raise ValueError(f"unknown retarded method {method!r}")
+    if memo is None:
+        return direct(m, n, n_prime)
+    cache, ld, e0, tol_memo = memo
+    ne = m.shape[0] // 2
+    xs, hs, us = cache.slot(slot, 2, ld, m.shape[-1], m.device)
+    x0 = torch.cat([xs[0, e0:e0 + ne], xs[1, e0:e0 + ne]])
+    has = torch.cat([hs[0, e0:e0 + ne], hs[1, e0:e0 + ne]]).contiguous()
+    x, need, used = memo_refresh_batched(MEMO_SURFACE, x0, has, cache.n_fpi("R"), tol_memo, m=m, n=n, n_prime=n_prime)
+    idx = torch.nonzero(need).flatten()
+    if idx.numel():
+        x[idx] = direct(m[idx].contiguous(), n[idx].contiguous(), n_prime[idx].contiguous())
+    xs[0, e0:e0 + ne], xs[1, e0:e0 + ne] = x[:ne], x[ne:]
+    hs[:, e0:e0 + ne] = 1
+    us[0, e0:e0 + ne], us[1, e0:e0 + ne] = used[:ne], used[ne:]
+    cache.record(us, e0, ne)
+    return x
+
+
+def contact_cells(m_diag: torch.Tensor, m_upper: torch.Tensor, m_lower: torch.Tensor):
+    """_lead_cell (scba.py:558-574) for both sides, stacked [2 sides][n_e]:
+    left m = M_00, n = M_10, n' = M_01; right m = M_{N-1,N-1},
+    n = M_{N-2,N-1}, n' = M_{N-1,N-2}."""
+    nb = m_diag.shape[1]
+    m = torch.cat([m_diag[:, 0], m_diag[:, nb - 1]])
+    n = torch.cat([m_lower[:, 0], m_upper[:, nb - 2]])
+    npr = torch.cat([m_upper[:, 0], m_lower[:, nb - 2]])
+    return m, n, npr

@@ -80,6 +80,10 @@ class ScbaOptions:
     stein_max_iter: int = 100
     batch: int | None = None  # energies per device batch (None: all)
     memoizer: MemoizerOptions = field(default_factory=MemoizerOptions)
+    # carrier retarded surfaces (scba.py:577-614): "sancho" (default here; the
+    # reference defaults to "beyn", which SURVEY §0.4 finds wrong in band),
+    # "beyn" or "fixed_point"
+    retarded_method: str = "sancho"
     # W retarded surface: "sancho" (default; equal to Beyn on the reference's
     # weak-V inputs) or "beyn" (the reference's choice, scba.py:844)
     w_retarded_method: str = "sancho"
@@ -92,8 +96,10 @@ class ScbaOptions:
             raise ValueError(f"tol must be positive, got {self.tol}")
         if not 0 < self.mixing <= 1:
             raise ValueError(f"mixing must lie in (0, 1], got {self.mixing}")
-        if self.w_retarded_method not in ("sancho", "beyn"):
+        if self.w_retarded_method not in ("sancho", "beyn", "fixed_point"):
             raise ValueError(f"unknown W retarded method {self.w_retarded_method!r}")
+        if self.retarded_method not in ("sancho", "beyn", "fixed_point"):
+            raise ValueError(f"unknown retarded method {self.retarded_method!r}")
 
 
 class EntryLayout:
@@ -145,39 +151,6 @@ class EntryLayout:
 
 class ScreenedSolver:
     """Batched W solve: assembly + contact closure + RGF (scba.py:1059-1103)."""
-
-    def _beyn_surfaces(self, b: dict, n_e: int, memo) -> torch.Tensor:
-        """W retarded surfaces by Beyn (the reference's choice, scba.py:844),
-        through the memoizer like _retarded_surface (scba.py:577-614): cached
-        problems are refreshed with fixed_point_step, Beyn solves the rest.
-        Returns [2 sides][n_e] surface blocks."""
-        from .obc import MEMO_SURFACE, beyn_batched, memo_refresh_batched
-
-        nb = self.n_b
-        # contact cells (scba.py:558-574): left m = M_00, n = M_10, n' = M_01;
-        # right m = M_{N-1,N-1}, n = M_{N-2,N-1}, n' = M_{N-1,N-2}
-        m = torch.cat([b["m_diag"][:, 0], b["m_diag"][:, nb - 1]])
-        n = torch.cat([b["m_lower"][:, 0], b["m_upper"][:, nb - 2]])
-        npr = torch.cat([b["m_upper"][:, 0], b["m_lower"][:, nb - 2]])
-        o = self.opt.beyn
-        if memo is None:
-            x, _ = beyn_batched(m, n, npr, o.n_quad, o.radius, 0.0, o.svd_tol)
-            return x
-        cache, ld, e0, tol_memo = memo
-        xs, hs, us = cache.slot(("W", "R"), 2, ld, self.bs, self.dev)
-        x0 = torch.cat([xs[0, e0:e0 + n_e], xs[1, e0:e0 + n_e]])
-        has = torch.cat([hs[0, e0:e0 + n_e], hs[1, e0:e0 + n_e]]).contiguous()
-        x, need, used = memo_refresh_batched(MEMO_SURFACE, x0, has, cache.n_fpi("R"), tol_memo, m=m, n=n, n_prime=npr)
-        idx = torch.nonzero(need).flatten()
-        if idx.numel():
-            xb, _ = beyn_batched(m[idx].contiguous(), n[idx].contiguous(), npr[idx].contiguous(), o.n_quad, o.radius,
-                                 0.0, o.svd_tol)
-            x[idx] = xb
-        xs[0, e0:e0 + n_e], xs[1, e0:e0 + n_e] = x[:n_e], x[n_e:]
-        hs[:, e0:e0 + n_e] = 1
-        us[0, e0:e0 + n_e], us[1, e0:e0 + n_e] = used[:n_e], used[n_e:]
-        cache.record(us, e0, n_e)
-        return x
 
     def __init__(self, v, options: ScbaOptions, device) -> None:
         self.dev = torch.device(device)
@@ -250,8 +223,11 @@ class ScreenedSolver:
             memo_args = [p(xr[0, e0]), p(hr[0, e0:]), p(ur[0, e0:]), p(xl[0, e0]), p(hl[0, e0:]), p(ul[0, e0:]),
                          ld, cache.n_fpi("R"), cache.n_fpi("<"), tol_memo]
         x_surface = None
-        if o.w_retarded_method == "beyn":
-            x_surface = self._beyn_surfaces(b, n_e, memo)
+        if o.w_retarded_method != "sancho":  # the reference's Beyn (scba.py:844)
+            from .obc import contact_cells, solve_surfaces
+
+            x_surface = solve_surfaces(*contact_cells(b["m_diag"], b["m_upper"], b["m_lower"]),
+                                       o.w_retarded_method, memo, ("W", "R"), o.surface_tol, o.beyn)
             memo_args[:3] = [None] * 3
         rc = lib.negf_w_obc_apply(n_e, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]),
                                   p(b["bl_diag"]), p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]),
@@ -374,7 +350,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     energies = np.asarray(energies, dtype=float)
     ne = len(energies)
     de = (energies[-1] - energies[0]) / (ne - 1)
-    carrier = CarrierSolver(h, eta, contacts, options.surface_tol, device=dev)
+    carrier = CarrierSolver(h, eta, contacts, options.surface_tol, device=dev,
+                            retarded_method=options.retarded_method, beyn=options.beyn)
     n_b, bs = carrier.n_b, carrier.bs
     lay = EntryLayout(n_b, bs, dev)
     tr = Transposer(comm, lay.n_entries, ne)

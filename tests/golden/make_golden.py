@@ -105,12 +105,12 @@ def make_conv():
     np.savez_compressed(OUT / "golden_conv.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
 
 
-def scba_case(nb, bs, ne, iters, ballistic=False, memo=False):
+def scba_case(nb, bs, ne, iters, ballistic=False, memo=False, method="sancho"):
     h = toys.chain_device(nb, bs)
     v = None if ballistic else toys.coulomb_matrix(nb, bs)
     grid = EnergyGrid(-2.0, 2.0, ne, eta=1e-3)
     contacts = scba.ContactConfig(mu_left=0.1, mu_right=-0.1, kT=0.05)
-    opts = scba.ScbaOptions(max_iter=iters, tol=1e-5 if memo else 1e-12, mixing=0.3, retarded_method="sancho",
+    opts = scba.ScbaOptions(max_iter=iters, tol=1e-5 if memo else 1e-12, mixing=0.3, retarded_method=method,
                             memoizer=scba.MemoizerOptions(enabled=memo))
     with threadpool_limits(1):
         return scba.scba_run(h, v, grid, contacts, opts)
@@ -297,6 +297,21 @@ def make_beyn():
         k += 1
     out["n_b"] = np.array(k)
     np.savez_compressed(OUT / "golden_beyn.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
+
+
+def make_methods():
+    """scba_run with the other carrier retarded methods (scba.py:577-614):
+    the reference default "beyn" and "fixed_point", 6x4 chain, 32 energies,
+    2 GW iterations, memoizer off."""
+    for method in ("beyn", "fixed_point"):
+        out = {}
+        res = scba_case(6, 4, 32, 2, method=method)
+        for f in RESULT_FIELDS:
+            out[f] = getattr(res, f)
+        for f in ("lesser", "greater", "ret_upper", "ret_lower"):
+            out["sigma_" + f] = getattr(res.sigma, f)
+        out["residuals"] = np.asarray(res.residuals)
+        np.savez_compressed(OUT / f"golden_scba_{method}.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
 
 
 if __name__ == "__main__":

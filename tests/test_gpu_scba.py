@@ -140,3 +140,18 @@ def test_scba_with_beyn_w_surface_matches_reference(golden, cuda):
         if k.startswith(("ver_", "config")):
             continue
         assert rel(res[k], g[k]) < TOL, k
+
+
+@pytest.mark.parametrize("method", ["beyn", "fixed_point"])
+def test_scba_carrier_retarded_methods_match_reference(golden, cuda, method):
+    """retarded_method (scba.py:577-614): the reference default "beyn" and
+    "fixed_point" for the carrier contacts (W by Beyn like the reference)."""
+    g = golden(f"golden_scba_{method}.npz")
+    res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=2, tol=1e-12, batch=16, memoizer=MEMO_OFF,
+                                                          retarded_method=method, w_retarded_method="beyn"),
+                   device=cuda)
+    for k in g.files:
+        if k.startswith(("ver_", "config")):
+            continue
+        assert rel(res[k], g[k]) < TOL, k
