@@ -378,6 +378,17 @@ int negf_dd_reverse_chain(int n_e, int w, int bs, const void* diag_in, const voi
                           const void* lower_in, void* diag_out, void* upper_out, void* lower_out,
                           void* stream);
 
+/* Keldysh identity defects (scba.py:1223-1248), the per-iteration
+ * diagnostics of ScbaResult.identity_defects. out[2] (device double, zeroed
+ * by the caller) accumulates max |(X^> - X^<) - (X^R - X^R^dag)| and the scale
+ * max |X^R - X^R^dag| over every stored block (upper blocks against
+ * X^R_up - X^R_lo^dag); the entry form takes entry-major series. */
+int negf_g_identity_defect(int n_e, int n_b, int bs, const void* xr_diag, const void* xr_upper,
+                           const void* xr_lower, const void* xl_diag, const void* xl_upper, const void* xg_diag,
+                           const void* xg_upper, double* out, void* stream);
+int negf_entry_identity_defect(long long n, const void* lesser, const void* greater, const void* ret_upper,
+                               const void* ret_lower, double* out, void* stream);
+
 /* ---- (6) mixing and residual (scba.py:478-481, 1155-1167) ----------------
  * s_k <- (1 - alpha) s_k + alpha r_k elementwise over n complex values, for
  * each non-NULL pair. diag_traces: tr[b][e] = sum_r x[diag_rows[b*bs + r]][e]

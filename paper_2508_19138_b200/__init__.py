@@ -52,7 +52,7 @@ from .obc import (
     sigma_lg_obc,
     stein_geometric,
 )
-from .scba import BeynOptions, EnergyGrid, MemoizerOptions, ScbaOptions, scba_run, scba_run_reference_api
+from .scba import BeynOptions, EnergyGrid, MemoizerOptions, ScbaOptions, ScbaResult, scba_run, scba_run_reference_api
 
 ContactConfig = Contacts  # scba.py:101-121 name
 
@@ -62,7 +62,7 @@ __all__ = [
     "transpose_distribution", "ContactBlocks", "ObcSigma", "SurfaceCache", "SurfaceResult", "beyn_batched",
     "fixed_point_batched", "fixed_point_step", "memoized_stein_batched", "memoized_surface_batched", "obc_beyn", "obc_fixed_point", "obc_sancho_rubio",
     "sancho_batched", "sigma_lg_obc", "stein_geometric", "BeynOptions", "EnergyGrid", "MemoizerOptions",
-    "ScbaOptions", "scba_run", "scba_run_reference_api",
+    "ScbaOptions", "ScbaResult", "scba_run", "scba_run_reference_api",
     "FULL", "LG_COMPRESSED", "BlockMatrix",
     "C_OBSERVABLE", "C_POLARIZATION", "C_SIGMA", "KT_DEFAULT",
     "BlockStructureError", "ConvergenceError", "NegfError", "SingularBlockError", "SpectralRadiusError",

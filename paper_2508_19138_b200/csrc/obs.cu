@@ -75,6 +75,76 @@ __global__ void observables_kernel(int n_b, int bs, const z_t* gr, const z_t* gl
   }
 }
 
+// max |v| over the block into out (as the bit pattern of a non-negative double)
+__device__ void block_max_to(double v, unsigned long long* out, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) m = fmax(m, red[i]);
+    atomicMax(out, (unsigned long long)__double_as_longlong(m));
+  }
+  __syncthreads();
+}
+
+// G identity defect (scba.py:1223-1238): max |X^> - X^< - (X^R - X^R^dag)| over
+// the diagonal blocks and |X^>_up - X^<_up - (X^R_up - X^R_lo^dag)| over the
+// upper blocks, and max |X^R - X^R^dag| (resp. |X^R_up - X^R_lo^dag|) as the
+// scale. grid (blocks of tiles, n_e * (2 n_b - 1)); one 32x32 tile per CTA.
+__global__ void g_defect_kernel(int n_b, int bs, const z_t* rd, const z_t* ru, const z_t* rl, const z_t* ld,
+                                const z_t* lu, const z_t* gd, const z_t* gu, unsigned long long* out) {
+  __shared__ z_t tt[32][33];
+  __shared__ double red[32];
+  const int nblk = 2 * n_b - 1;
+  const int e = blockIdx.y / nblk, q = blockIdx.y % nblk;
+  const bool diag = q < n_b;
+  const int i = diag ? q : q - n_b;
+  const long long n2 = (long long)bs * bs;
+  const long long od = ((long long)e * n_b + i) * n2, oo = ((long long)e * (n_b - 1) + i) * n2;
+  const z_t* R = diag ? rd + od : ru + oo;
+  const z_t* RH = diag ? rd + od : rl + oo;  // block whose dagger is subtracted
+  const z_t* L = diag ? ld + od : lu + oo;
+  const z_t* G = diag ? gd + od : gu + oo;
+  const int tiles_c = (bs + 31) / 32;
+  const int r0 = (blockIdx.x / tiles_c) * 32, c0 = (blockIdx.x % tiles_c) * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int k = ty; k < 32; k += 8) {
+    const int rr = c0 + k, cc = r0 + tx;
+    if (rr < bs && cc < bs) tt[k][tx] = RH[(long long)rr * bs + cc];
+  }
+  __syncthreads();
+  double dmax = 0.0, smax = 0.0;
+  for (int k = ty; k < 32; k += 8) {
+    const int r = r0 + k, c = c0 + tx;
+    if (r >= bs || c >= bs) continue;
+    const long long x = (long long)r * bs + c;
+    const z_t gam = zsub(R[x], zconj(tt[tx][k]));
+    const z_t diff = zsub(G[x], L[x]);
+    dmax = fmax(dmax, hypot(diff.x - gam.x, diff.y - gam.y));
+    smax = fmax(smax, hypot(gam.x, gam.y));
+  }
+  block_max_to(dmax, out, red);
+  block_max_to(smax, out + 1, red);
+}
+
+// entry-major defect (scba.py:1241-1248): max |(g - l) - (ru - conj rl)|, max |ru - conj rl|
+__global__ void entry_defect_kernel(long long n, const z_t* l, const z_t* g, const z_t* ru, const z_t* rl,
+                                    unsigned long long* out) {
+  __shared__ double red[32];
+  double dmax = 0.0, smax = 0.0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    const z_t gam = zsub(ru[k], zconj(rl[k]));
+    const z_t diff = zsub(g[k], l[k]);
+    dmax = fmax(dmax, hypot(diff.x - gam.x, diff.y - gam.y));
+    smax = fmax(smax, hypot(gam.x, gam.y));
+  }
+  block_max_to(dmax, out, red);
+  block_max_to(smax, out + 1, red);
+}
+
 }  // namespace
 }  // namespace negf
 
@@ -102,3 +172,42 @@ extern "C" int negf_observables(int n_e, int n_b, int bs, const void* gr_diag,
   }
   return 0;
 }
+
+extern "C" {
+
+int negf_g_identity_defect(int n_e, int n_b, int bs, const void* xr_diag, const void* xr_upper,
+                           const void* xr_lower, const void* xl_diag, const void* xl_upper, const void* xg_diag,
+                           const void* xg_upper, double* out, void* stream) {
+  if (n_e < 0 || n_b < 1 || bs < 1 || !xr_diag || !xl_diag || !xg_diag || !out) return -1;
+  if (n_b > 1 && (!xr_upper || !xr_lower || !xl_upper || !xg_upper)) return -1;
+  if (n_e == 0) return 0;
+  const int tiles = ((bs + 31) / 32) * ((bs + 31) / 32);
+  dim3 grid(tiles, n_e * (2 * n_b - 1)), block(32, 8);
+  {
+    negf::ProfScope ps(negf::PROF_OTHER, (cudaStream_t)stream);
+    negf::g_defect_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(
+        n_b, bs, (const negf::z_t*)xr_diag, (const negf::z_t*)xr_upper, (const negf::z_t*)xr_lower,
+        (const negf::z_t*)xl_diag, (const negf::z_t*)xl_upper, (const negf::z_t*)xg_diag, (const negf::z_t*)xg_upper,
+        (unsigned long long*)out);
+    NEGF_LAUNCHED();
+  }
+  return 0;
+}
+
+int negf_entry_identity_defect(long long n, const void* lesser, const void* greater, const void* ret_upper,
+                               const void* ret_lower, double* out, void* stream) {
+  if (n < 0 || !lesser || !greater || !ret_upper || !ret_lower || !out) return -1;
+  if (n == 0) return 0;
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  {
+    negf::ProfScope ps(negf::PROF_OTHER, (cudaStream_t)stream);
+    negf::entry_defect_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        n, (const negf::z_t*)lesser, (const negf::z_t*)greater, (const negf::z_t*)ret_upper,
+        (const negf::z_t*)ret_lower, (unsigned long long*)out);
+    NEGF_LAUNCHED();
+  }
+  return 0;
+}
+
+}  // extern "C"

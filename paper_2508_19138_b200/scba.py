@@ -88,6 +88,8 @@ class ScbaOptions:
     # weak-V inputs) or "beyn" (the reference's choice, scba.py:844)
     w_retarded_method: str = "sancho"
     beyn: BeynOptions = field(default_factory=lambda: BeynOptions())
+    # scba.py:943: a warm-start initial_sigma is used only when reset_sigma is False
+    reset_sigma: bool = True
 
     def __post_init__(self) -> None:
         if self.max_iter < 1:
@@ -319,6 +321,39 @@ def _stacks(m):
     return m
 
 
+class ScbaResult(dict):
+    """Result of scba_run (scba.py:196-240 ScbaResult): a dict of host arrays
+    whose keys are also readable as attributes (result.g_r_diag,
+    result.converged, result.identity_defects, ...)."""
+
+    def __getattr__(self, name):
+        try:
+            return self[name]
+        except KeyError:
+            raise AttributeError(name) from None
+
+
+def g_identity_defect(b: dict, n_e: int, n_b: int, bs: int, out: torch.Tensor) -> None:
+    """scba.py:1223-1238 on the device: accumulates max |X^> - X^< - (X^R - X^R^dag)|
+    and max |X^R - X^R^dag| over the stored blocks into out[0:2] (max-combined)."""
+    up = lambda k: b[k].data_ptr() if n_b > 1 else None
+    rc = _lib.load().negf_g_identity_defect(n_e, n_b, bs, b["xr_diag"].data_ptr(), up("xr_upper"), up("xr_lower"),
+                                            b["xl_diag"].data_ptr(), up("xl_upper"), b["xg_diag"].data_ptr(),
+                                            up("xg_upper"), out.data_ptr(), _lib.stream_ptr(out.device))
+    _lib.check(rc, "negf_g_identity_defect")
+
+
+def entry_identity_defect(lesser, greater, ret_upper, ret_lower, out: torch.Tensor) -> None:
+    """scba.py:1241-1248 on the device for entry-major series (P or Sigma rows)."""
+    for x in (lesser, greater, ret_upper, ret_lower):
+        if x.dtype != Z or not x.is_contiguous() or x.shape != lesser.shape:
+            raise ValueError("identity defect needs contiguous complex128 series of one shape")
+    rc = _lib.load().negf_entry_identity_defect(lesser.numel(), lesser.data_ptr(), greater.data_ptr(),
+                                                ret_upper.data_ptr(), ret_lower.data_ptr(), out.data_ptr(),
+                                                _lib.stream_ptr(out.device))
+    _lib.check(rc, "negf_entry_identity_defect")
+
+
 def scba_run_reference_api(h_mat, v_mat, grid, contacts, options: ScbaOptions | None = None,
                            comm: Comm | None = None, initial_sigma: ScbaState | None = None,
                            device="cuda") -> dict:
@@ -333,7 +368,7 @@ def scba_run_reference_api(h_mat, v_mat, grid, contacts, options: ScbaOptions | 
 
 def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOptions | None = None,
              device="cuda", keep_g: bool = True, initial_sigma: ScbaState | None = None,
-             comm: Comm | None = None, profile: bool = False, sigma_to_host: bool = True) -> dict:
+             comm: Comm | None = None, profile: bool = False, sigma_to_host: bool = True) -> "ScbaResult":
     """SCBA on one GPU or energy-sharded over ``comm`` (one rank per GPU).
 
     ``h``/``v`` are (diag, upper, lower) block stacks; ``v=None`` runs the
@@ -360,7 +395,12 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     my_e = energies[own]
     diag_rows = lay.diag[tr.own_r].contiguous()
     batch = options.batch or max(n_own, 1)
-    sig = initial_sigma or ScbaState.zeros(lay.n_entries, n_own, dev)
+    sig = ScbaState.zeros(lay.n_entries, n_own, dev)
+    if initial_sigma is not None and not options.reset_sigma:
+        if tuple(initial_sigma.lesser.shape) != (lay.n_entries, n_own):
+            raise ValueError(f"warm-start state has shape {tuple(initial_sigma.lesser.shape)}, "
+                             f"expected {(lay.n_entries, n_own)}")
+        sig = ScbaState(*(torch.as_tensor(x, dtype=Z, device=dev).clone() for x in initial_sigma.as_tuple()))
     if v is None:
         max_iter = 1
     else:
@@ -371,6 +411,9 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     cols = lambda: torch.empty((lay.n_entries, n_own), dtype=Z, device=dev)
     result: dict = {}
     residuals = []
+    identity_defects: list[dict[str, float]] = []
+    converged = v is None
+    n_iter = 0
     blocks = None
     timings: dict[str, float] = {}
     import time as _time
@@ -399,8 +442,11 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     stats_by_it = []
     memo = (lambda e0: (cache, max(n_own, 1), e0, tol_memo)) if cache is not None else (lambda e0: None)
     for it in range(max_iter):
+        n_iter = it + 1
         torch.cuda.synchronize(dev)
         t_iter = _time.perf_counter()
+        # identity-defect accumulators (G, P, Sigma) x (defect, scale), scba.py:1002-1006
+        defects = torch.zeros(6, dtype=torch.float64, device=dev)
         g_host = {k: [] for k in RESULT_KEYS} if keep_g else None
         gl_c, gg_c = cols(), cols()
         # 1. carrier solve per energy batch of this rank
@@ -419,6 +465,7 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
                 lay.unpack_lg(sig.greater, e0, nb_, blocks["sg_diag"], blocks["sg_upper"])
             with _T("G: OBC+RGF"):
                 b = carrier.solve(my_e[e0:e1], sigma=blocks, n_e=nb_, memo=memo(e0))
+            g_identity_defect(b, nb_, n_b, bs, defects[0:2])
             with _T("layout"):
                 lay.pack(b["xl_diag"], b["xl_upper"], gl_c, e0)
                 lay.pack(b["xg_diag"], b["xg_upper"], gg_c, e0)
@@ -428,6 +475,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         if keep_g and n_own:
             result = {k: np.concatenate(vv) for k, vv in g_host.items()}
         if v is None:
+            d = comm.allreduce_max(defects[0:2].tolist(), dev)
+            identity_defects.append({"G": d[0] / (d[1] + 1e-300)})
             residuals.append(0.0)
             if cache is not None:
                 stats_by_it.append(cache.stats)
@@ -438,6 +487,7 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         del gl_c, gg_c
         with _T("convolution"):
             p_rows = polarization(gl, gg, diag_rows, de)
+        entry_identity_defect(*p_rows, defects[2:4])
         with _T("transpose"):
             pl, pg, pru, prl = (tr.to_energy_major(x) for x in p_rows)
         del p_rows
@@ -462,6 +512,7 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         # 4. self-energy on own entry rows, back to energy-major columns
         with _T("convolution"):
             s_rows = self_energy(gl, gg, wl, wg, None, diag_rows, de)
+        entry_identity_defect(*s_rows, defects[4:6])
         with _T("transpose"):
             raw = tuple(tr.to_energy_major(x) for x in s_rows)
         del s_rows
@@ -479,11 +530,14 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         scale = max(mx(to), mx(tn))
         delta, scale = comm.allreduce_max([delta, scale], dev)
         residuals.append(delta / (scale + 1e-300))
+        d = comm.allreduce_max(defects.tolist(), dev)
+        identity_defects.append({k: d[2 * j] / (d[2 * j + 1] + 1e-300) for j, k in enumerate(("G", "P", "Sigma"))})
         del raw
         if cache is not None:
             stats_by_it.append(cache.stats)
         iter_times.append(_time.perf_counter() - t_iter)
         if residuals[-1] < options.tol:
+            converged = True
             break
         if len(residuals) >= 11 and residuals[-1] > 5.0 * residuals[-11]:
             raise ConvergenceError(f"residual grew from {residuals[-11]:.3e} to {residuals[-1]:.3e} over 10 iterations")
@@ -492,10 +546,14 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             result["sigma_" + k] = t.cpu().numpy()
     result["iteration_s"] = iter_times
     result["residuals"] = np.asarray(residuals)
+    result["identity_defects"] = identity_defects
+    result["converged"] = converged
+    result["n_iter"] = n_iter
+    result["n_blocks"], result["block_size"] = n_b, bs
     result["state"] = sig
     result["energy_slice"] = own
     result["transpose_bytes"] = tr.bytes_moved
     result["timings"] = timings
     result["cache_stats"] = cache.stats if cache is not None else {"direct_calls": 0, "memoized_calls": 0}
     result["cache_stats_by_iteration"] = stats_by_it
-    return result
+    return ScbaResult(result)

@@ -155,3 +155,75 @@ def test_scba_carrier_retarded_methods_match_reference(golden, cuda, method):
         if k.startswith(("ver_", "config")):
             continue
         assert rel(res[k], g[k]) < TOL, k
+
+
+def _np_g_defect(xr_d, xr_u, xr_l, xl_d, xl_u, xg_d, xg_u):
+    """scba.py:1223-1238 restated over stacked (n_e, n_b, bs, bs) arrays."""
+    h = lambda a: np.conj(np.swapaxes(a, -1, -2))
+    gam_d, gam_u = xr_d - h(xr_d), xr_u - h(xr_l)
+    d = max(np.max(np.abs((xg_d - xl_d) - gam_d)), np.max(np.abs((xg_u - xl_u) - gam_u)) if xr_u.size else 0.0)
+    s = max(np.max(np.abs(gam_d)), np.max(np.abs(gam_u)) if xr_u.size else 0.0)
+    return d, s
+
+
+@pytest.mark.parametrize("n_e,n_b,bs", [(3, 4, 7), (2, 3, 40), (1, 1, 33)])
+def test_identity_defect_kernels_match_numpy(cuda, n_e, n_b, bs):
+    from paper_2508_19138_b200.scba import entry_identity_defect, g_identity_defect
+
+    rng = np.random.default_rng(n_b * bs)
+    z = lambda *s: rng.standard_normal(s) + 1j * rng.standard_normal(s)
+    a = dict(xr_diag=z(n_e, n_b, bs, bs), xr_upper=z(n_e, n_b - 1, bs, bs), xr_lower=z(n_e, n_b - 1, bs, bs),
+             xl_diag=z(n_e, n_b, bs, bs), xl_upper=z(n_e, n_b - 1, bs, bs), xg_diag=z(n_e, n_b, bs, bs),
+             xg_upper=z(n_e, n_b - 1, bs, bs))
+    out = torch.zeros(2, dtype=torch.float64, device=cuda)
+    g_identity_defect({k: t(v, cuda) for k, v in a.items()}, n_e, n_b, bs, out)
+    d, s = _np_g_defect(*a.values())
+    np.testing.assert_allclose(out.cpu().numpy(), [d, s], rtol=1e-14)
+    ser = [z(57, 13) for _ in range(4)]
+    out.zero_()
+    entry_identity_defect(*(t(x, cuda) for x in ser), out)
+    gam = ser[2] - np.conj(ser[3])
+    ref = [np.max(np.abs((ser[1] - ser[0]) - gam)), np.max(np.abs(gam))]
+    np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=1e-14)
+
+
+def test_scba_identity_defects_and_result_fields(golden, cuda):
+    """ScbaResult.identity_defects (scba.py:1155-1166): one {"G","P","Sigma"}
+    record per iteration at roundoff level (the reference's own run of this
+    case gives 1e-16..1e-15), the G entry equal to the defect of the returned
+    last-iteration G; converged / n_iter and attribute access as ScbaResult."""
+    g = golden("golden_scba_small.npz")
+    res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=3, tol=1e-12, batch=10, memoizer=MEMO_OFF), device=cuda)
+    assert len(res.identity_defects) == 3 and res.n_iter == 3 and res.converged is False
+    for d in res.identity_defects:
+        assert set(d) == {"G", "P", "Sigma"} and max(d.values()) < 1e-12
+    dg, sg = _np_g_defect(res.g_r_diag, res.g_r_upper, res.g_r_lower, res.g_lesser_diag, res.g_lesser_upper,
+                          res.g_greater_diag, res.g_greater_upper)
+    assert abs(res.identity_defects[-1]["G"] - dg / sg) <= 1e-6 * dg / sg + 1e-300
+    assert rel(res.residuals, g["residuals"]) < TOL
+    ball = scba_run(orc.chain_device(5, 3), None, np.linspace(-2.0, 2.0, 16), 1e-3, Contacts(0.1, -0.1, 0.05),
+                    device=cuda)
+    assert ball.converged and ball.n_iter == 1 and list(ball.identity_defects[0]) == ["G"]
+    assert ball.identity_defects[0]["G"] < 1e-12
+
+
+def test_scba_warm_start_reset_sigma(cuda):
+    """scba.py:943-949: initial_sigma is ignored unless reset_sigma=False; a
+    converged state fed back converges at once; a wrong shape is a ValueError."""
+    h, v, e = orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32)
+    c = Contacts(0.1, -0.1, 0.05)
+    first = scba_run(h, v, e, 1e-3, c, ScbaOptions(max_iter=80, tol=1e-8, memoizer=MEMO_OFF), device=cuda)
+    assert first.converged
+    cold = scba_run(h, v, e, 1e-3, c, ScbaOptions(max_iter=2, tol=1e-8, memoizer=MEMO_OFF), device=cuda,
+                    initial_sigma=first.state)
+    assert rel(cold.residuals, first.residuals[:2]) < TOL  # reset_sigma=True: cold start
+    warm = scba_run(h, v, e, 1e-3, c, ScbaOptions(max_iter=80, tol=1e-8, memoizer=MEMO_OFF, reset_sigma=False),
+                    device=cuda, initial_sigma=first.state)
+    assert warm.converged and warm.n_iter <= 2
+    from paper_2508_19138_b200.scba import ScbaState
+
+    bad = ScbaState.zeros(7, 32, cuda)
+    with pytest.raises(ValueError, match="warm-start"):
+        scba_run(h, v, e, 1e-3, c, ScbaOptions(max_iter=2, reset_sigma=False, memoizer=MEMO_OFF), device=cuda,
+                 initial_sigma=bad)
