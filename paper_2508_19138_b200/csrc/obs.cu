@@ -78,13 +78,14 @@ __global__ void observables_kernel(int n_b, int bs, const z_t* gr, const z_t* gl
 // max |v| over the block into out (as the bit pattern of a non-negative double)
 __device__ void block_max_to(double v, unsigned long long* out, double* red) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;  // 1-D or 2-D blocks of whole warps
+  const int lane = tid & 31, w = tid >> 5;
   __syncthreads();
   if (lane == 0) red[w] = v;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     double m = 0.0;
-    for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) m = fmax(m, red[i]);
+    for (int i = 0; i < (int)(blockDim.x * blockDim.y + 31) / 32; ++i) m = fmax(m, red[i]);
     atomicMax(out, (unsigned long long)__double_as_longlong(m));
   }
   __syncthreads();
