@@ -125,16 +125,27 @@ __device__ __forceinline__ void dft_r(z_t* e) {
   else dft2<INV>(e[0], e[1]);
 }
 
+// Short rows (Q = L/E < PACK_T threads) are packed PACK_T / Q to a CTA of
+// PACK_T threads, each row with its own shared-memory slice: one row per CTA
+// at L = 16 would run 2 of 32 threads and launch one CTA per entry row.
+constexpr int PACK_T = 128;
+
+__host__ __device__ __forceinline__ int rows_per_cta(int L, int E) {
+  const int q = L / E;
+  return q < PACK_T ? PACK_T / q : 1;
+}
+
 template <int E>
 struct RowGeom {
   int L, Q;    // Q = L/E threads carry data
   int pE, rs;  // radix-E passes, small radix (0 or 2 .. E/2)
   int t;
+  int sub;     // row slot within the CTA
   bool act;
 };
 
 template <int E>
-__device__ __forceinline__ RowGeom<E> row_geom(int L) {
+__device__ __forceinline__ RowGeom<E> row_geom(int L, long long n_rows, long long& row) {
   constexpr int lg = E == 16 ? 4 : 3;
   RowGeom<E> g;
   g.L = L;
@@ -142,8 +153,12 @@ __device__ __forceinline__ RowGeom<E> row_geom(int L) {
   const int m = 31 - __clz(L);
   g.pE = m / lg;
   g.rs = (m % lg) ? (1 << (m % lg)) : 0;
-  g.t = threadIdx.x;
-  g.act = g.t < g.Q;
+  const int rpc = rows_per_cta(L, E);
+  g.t = rpc > 1 ? threadIdx.x % g.Q : threadIdx.x;
+  g.sub = rpc > 1 ? threadIdx.x / g.Q : 0;
+  row = (long long)blockIdx.x * rpc + g.sub;
+  g.act = g.t < g.Q && row < n_rows;
+  if (row >= n_rows) row = n_rows - 1;  // idle slot: keep table reads in bounds
   return g;
 }
 
@@ -283,12 +298,12 @@ __global__ void __launch_bounds__(MAXT) pol_kernel(const z_t* __restrict__ gl, c
                                                    int L, const z_t* __restrict__ tw, const z_t* __restrict__ kf,
                                                    const z_t* __restrict__ kcf,
                                                    const unsigned char* __restrict__ diag, double2 scale, z_t* pl,
-                                                   z_t* pg, z_t* pr_up, z_t* pr_lo) {
+                                                   z_t* pg, z_t* pr_up, z_t* pr_lo, long long n_rows) {
   extern __shared__ __align__(16) z_t sm[];
-  z_t* A = sm;
-  z_t* B = sm + pidx(L);
-  const RowGeom<E> g = row_geom<E>(L);
-  const long long row = blockIdx.x;
+  long long row;
+  const RowGeom<E> g = row_geom<E>(L, n_rows, row);
+  z_t* A = sm + 2 * g.sub * pidx(L);
+  z_t* B = A + pidx(L);
   const long long o = row * n;
   const bool dg = diag && diag[row];
   z_t v[2][E];
@@ -336,12 +351,12 @@ __global__ void __launch_bounds__(MAXT) sigma_kernel(const z_t* __restrict__ gl,
                                                      const z_t* __restrict__ tw, const z_t* __restrict__ kf,
                                                      const z_t* __restrict__ kcf,
                                                      const unsigned char* __restrict__ diag, double2 scale, z_t* sl,
-                                                     z_t* sg, z_t* sr_up, z_t* sr_lo) {
+                                                     z_t* sg, z_t* sr_up, z_t* sr_lo, long long n_rows) {
   extern __shared__ __align__(16) z_t sm[];
-  z_t* A = sm;
-  z_t* B = sm + pidx(L);
-  const RowGeom<E> g = row_geom<E>(L);
-  const long long row = blockIdx.x;
+  long long row;
+  const RowGeom<E> g = row_geom<E>(L, n_rows, row);
+  z_t* A = sm + 2 * g.sub * pidx(L);
+  z_t* B = A + pidx(L);
   const long long o = row * n;
   const long long ow = (w_rows ? w_rows[row] : row) * n;
   const bool dg = diag && diag[row];
@@ -385,12 +400,13 @@ __global__ void __launch_bounds__(MAXT) sigma_kernel(const z_t* __restrict__ gl,
 template <int E, int MAXT>
 __global__ void __launch_bounds__(MAXT) conv_kernel(const z_t* __restrict__ x1, const z_t* __restrict__ x2, int n,
                                                     int L, int mode, const z_t* __restrict__ tw, double2 scale,
-                                                    z_t* out) {
+                                                    z_t* out, long long n_rows) {
   extern __shared__ __align__(16) z_t sm[];
-  z_t* A = sm;
-  z_t* B = sm + pidx(L);
-  const RowGeom<E> g = row_geom<E>(L);
-  const long long o = (long long)blockIdx.x * n;
+  long long row;
+  const RowGeom<E> g = row_geom<E>(L, n_rows, row);
+  z_t* A = sm + 2 * g.sub * pidx(L);
+  z_t* B = A + pidx(L);
+  const long long o = row * n;
   z_t v[2][E];
 #pragma unroll
   for (int s = 0; s < E; ++s) {
@@ -419,12 +435,13 @@ __global__ void __launch_bounds__(MAXT) conv_kernel(const z_t* __restrict__ x1, 
 template <int E, int MAXT>
 __global__ void __launch_bounds__(MAXT) ret_kernel(const z_t* __restrict__ xl, const z_t* __restrict__ xg, int n,
                                                    int L, const z_t* __restrict__ tw, const z_t* __restrict__ kf,
-                                                   z_t* out) {
+                                                   z_t* out, long long n_rows) {
   extern __shared__ __align__(16) z_t sm[];
-  z_t* A = sm;
-  z_t* B = sm + pidx(L);
-  const RowGeom<E> g = row_geom<E>(L);
-  const long long o = (long long)blockIdx.x * n;
+  long long row;
+  const RowGeom<E> g = row_geom<E>(L, n_rows, row);
+  z_t* A = sm + 2 * g.sub * pidx(L);
+  z_t* B = A + pidx(L);
+  const long long o = row * n;
   z_t d[E];
 #pragma unroll
   for (int s = 0; s < E; ++s) {
@@ -438,9 +455,14 @@ __global__ void __launch_bounds__(MAXT) ret_kernel(const z_t* __restrict__ xl, c
 // transform, but at ~250 registers it measured no faster for P and 20 %
 // slower for Sigma on B200; the engine keeps both.)
 int ept_for(int) { return 8; }
-int threads_for(int L) { const int q = L / ept_for(L); return q >= 32 ? q : 32; }
+int threads_for(int L) { const int q = L / ept_for(L); return q >= PACK_T ? q : PACK_T; }
 
-size_t smem_for(int L) { return 2 * (size_t)(L + L / 8) * sizeof(z_t); }
+size_t smem_for(int L) { return (size_t)rows_per_cta(L, ept_for(L)) * 2 * (L + L / 8) * sizeof(z_t); }
+
+unsigned grid_for(long long n_rows, int L) {
+  const int r = rows_per_cta(L, ept_for(L));
+  return (unsigned)((n_rows + r - 1) / r);
+}
 
 int smem_setup(const void* fn, int L) {
   if (smem_for(L) > 200 * 1024 || threads_for(L) > 512) return -5;
@@ -471,9 +493,9 @@ int negf_conv_polarization(long long n_rows, int n_e, int L, const void* gl, con
   {
     // algorithmic HBM bytes: read G^<, G^> rows, write P^<, P^>, P^R_up, P^R_lo (96 B per entry-energy)
     ProfSpan ps_pol_kernel(PROF_CONV, (cudaStream_t)(stream), 0.0, 96.0 * (double)n_rows * n_e);
-    kfn<<<(unsigned)n_rows, threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
+    kfn<<<grid_for(n_rows, L), threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
         (const z_t*)gl, (const z_t*)gg, n_e, L, (const z_t*)tw, (const z_t*)kf, (const z_t*)kcf, diag,
-        make_double2(scale_re, scale_im), (z_t*)pl, (z_t*)pg, (z_t*)pr_up, (z_t*)pr_lo);
+        make_double2(scale_re, scale_im), (z_t*)pl, (z_t*)pg, (z_t*)pr_up, (z_t*)pr_lo, n_rows);
     NEGF_LAUNCHED();
   }
   return 0;
@@ -493,10 +515,10 @@ int negf_conv_sigma(long long n_rows, int n_e, int L, const void* gl, const void
   {
     // read G^<, G^>, W^<, W^> rows, write four Sigma series (128 B per entry-energy)
     ProfSpan ps_sigma_kernel(PROF_CONV, (cudaStream_t)(stream), 0.0, 128.0 * (double)n_rows * n_e);
-    kfn<<<(unsigned)n_rows, threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
+    kfn<<<grid_for(n_rows, L), threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
         (const z_t*)gl, (const z_t*)gg, (const z_t*)wl, (const z_t*)wg, w_rows, n_e, L, (const z_t*)tw,
         (const z_t*)kf, (const z_t*)kcf, diag, make_double2(scale_re, scale_im), (z_t*)sl, (z_t*)sg,
-        (z_t*)sr_up, (z_t*)sr_lo);
+        (z_t*)sr_up, (z_t*)sr_lo, n_rows);
     NEGF_LAUNCHED();
   }
   return 0;
@@ -514,9 +536,9 @@ int negf_convolve_energy(long long n_rows, int n_e, int L, const void* x1, const
   if (rc) return rc;
   {
     ProfScope ps_conv_kernel(PROF_OTHER, (cudaStream_t)(stream));
-    kfn<<<(unsigned)n_rows, threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
+    kfn<<<grid_for(n_rows, L), threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
         (const z_t*)x1, (const z_t*)x2, n_e, L, mode, (const z_t*)tw, make_double2(scale_re, scale_im),
-        (z_t*)out);
+        (z_t*)out, n_rows);
     NEGF_LAUNCHED();
   }
   return 0;
@@ -534,8 +556,8 @@ int negf_retarded_from_lg(long long n_rows, int n_e, int L, const void* x_lesser
   if (rc) return rc;
   {
     ProfScope ps_ret_kernel(PROF_OTHER, (cudaStream_t)(stream));
-    kfn<<<(unsigned)n_rows, threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
-        (const z_t*)x_lesser, (const z_t*)x_greater, n_e, L, (const z_t*)tw, (const z_t*)kf, (z_t*)out);
+    kfn<<<grid_for(n_rows, L), threads_for(L), smem_for(L), (cudaStream_t)stream>>>(
+        (const z_t*)x_lesser, (const z_t*)x_greater, n_e, L, (const z_t*)tw, (const z_t*)kf, (z_t*)out, n_rows);
     NEGF_LAUNCHED();
   }
   return 0;

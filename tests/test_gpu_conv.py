@@ -36,10 +36,10 @@ def test_convolutions_match_oracle_sizes(cuda, ne):
     assert rel(conv.retarded_from_lg(x1, x2), orc.retarded_from_lg(x1, x2)) < TOL
 
 
-@pytest.mark.parametrize("ne", [16, 128, 2048])
-def test_fused_polarization_and_sigma_match_oracle(cuda, ne):
+@pytest.mark.parametrize("ne,rows", [(3, 517), (8, 37), (16, 37), (16, 1001), (128, 37), (300, 75), (2048, 37)])
+def test_fused_polarization_and_sigma_match_oracle(cuda, ne, rows):
+    """Short series pack several entry rows per CTA (ragged last CTA covered)."""
     rng = np.random.default_rng(7 + ne)
-    rows = 37
     mk = lambda: rng.standard_normal((rows, ne)) + 1j * rng.standard_normal((rows, ne))
     gl, gg, wl, wg = mk(), mk(), mk(), mk()
     diag = rng.random(rows) < 0.3
