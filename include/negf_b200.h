@@ -310,8 +310,11 @@ int negf_w_assemble(int n_e, int n_b, int bs, const void* v_diag, const void* v_
                     const void* pr_lower, const void* pl_diag, const void* pl_upper,
                     const void* pg_diag, const void* pg_upper, void* m_diag, void* m_upper,
                     void* m_lower, void* bl_diag, void* bl_upper, void* bg_diag, void* bg_upper,
-                    void* workspace, size_t workspace_bytes, void* stream);
-/* W contact closure in place (scba.py:839-858, _lead_lg_boundary :617-664):
+                    int v_real, void* workspace, size_t workspace_bytes, void* stream);
+/* v_real != 0: the caller guarantees imag(V) == 0 exactly (e.g. a real
+ * Coulomb matrix); each V product then skips the vanishing ai*bi Gauss
+ * product (2 instead of 3 real GEMMs, bitwise the same result).
+ * W contact closure in place (scba.py:839-858, _lead_lg_boundary :617-664):
  * Sancho surface block per side (status/iters [2][n_e], codes as
  * negf_obc_sancho_batched), geometric Stein per side and kind (stein_status/
  * stein_iters [2 kinds][2 sides][n_e]; 4 = spectral radius estimate >= 1,

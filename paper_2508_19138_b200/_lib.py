@@ -74,7 +74,7 @@ _SIGNATURES: dict[str, tuple] = {
     "negf_unpack_lg": (_i, [_i, _i, _i, _vp, _vp, _ll, _i, _vp, _vp, _vp]),
     "negf_unpack_retarded": (_i, [_i, _i, _i, _vp, _vp, _vp, _ll, _i, _vp, _vp, _vp, _vp]),
     "negf_w_assemble_workspace_bytes": (_sz, [_i, _i, _i]),
-    "negf_w_assemble": (_i, [_i, _i, _i] + [_vp] * 18 + [_sz, _vp]),
+    "negf_w_assemble": (_i, [_i, _i, _i] + [_vp] * 17 + [_i, _vp, _sz, _vp]),
     "negf_w_obc_workspace_bytes": (_sz, [_i, _i]),
     "negf_w_obc_apply": (_i, [_i, _i, _i] + [_vp] * 7 + [_d, _i, _d, _i] + [_vp] * 5 + [_vp] * 6
                          + [_ll, _i, _i, _d, _vp, _vp, _sz, _vp]),

@@ -53,6 +53,7 @@ struct Opnd {  // one operand block: pointer, energy stride, op flag
   long long s;
   int op;
   bool neg;
+  bool real = false;  // imaginary part exactly zero (a real V)
 };
 
 ZGemmDesc sum_desc(int bs, int ne, std::initializer_list<std::pair<Opnd, Opnd>> terms, z_t* D,
@@ -64,7 +65,7 @@ ZGemmDesc sum_desc(int bs, int ne, std::initializer_list<std::pair<Opnd, Opnd>> 
   for (auto& tb : terms) {
     const Opnd& a = tb.first;
     const Opnd& b = tb.second;
-    d.t[n++] = zterm(a.p, a.s, bs, a.op, b.p, b.s, bs, b.op, bs, a.neg != b.neg);
+    d.t[n++] = zterm(a.p, a.s, bs, a.op, b.p, b.s, bs, b.op, bs, a.neg != b.neg, a.real || b.real);
   }
   d.nterms = n;
   for (int i = n; i < kMaxTerms; ++i) d.t[i] = d.t[0];
@@ -94,7 +95,7 @@ int negf_w_assemble(int n_e, int n_b, int bs, const void* v_diag, const void* v_
                     const void* pr_lower, const void* pl_diag, const void* pl_upper,
                     const void* pg_diag, const void* pg_upper, void* m_diag, void* m_upper,
                     void* m_lower, void* bl_diag, void* bl_upper, void* bg_diag, void* bg_upper,
-                    void* workspace, size_t workspace_bytes, void* stream) {
+                    int v_real, void* workspace, size_t workspace_bytes, void* stream) {
   if (n_e < 0 || n_b < 2 || bs < 1) return -1;
   if (!v_diag || !v_upper || !v_lower || !pr_diag || !pr_upper || !pr_lower || !m_diag ||
       !m_upper || !m_lower)
@@ -104,9 +105,10 @@ int negf_w_assemble(int n_e, int n_b, int bs, const void* v_diag, const void* v_
   const long long n2 = (long long)bs * bs, sd = (long long)n_b * n2, so = (long long)(n_b - 1) * n2;
   const int nb = n_b;
   auto V = [&](int i, int j) -> Opnd {  // energy independent
-    if (i == j) return Opnd{(const z_t*)v_diag + i * n2, 0, OP_N, false};
-    if (j == i + 1) return Opnd{(const z_t*)v_upper + i * n2, 0, OP_N, false};
-    return Opnd{(const z_t*)v_lower + j * n2, 0, OP_N, false};  // (j+1, j)
+    const bool re = v_real != 0;
+    if (i == j) return Opnd{(const z_t*)v_diag + i * n2, 0, OP_N, false, re};
+    if (j == i + 1) return Opnd{(const z_t*)v_upper + i * n2, 0, OP_N, false, re};
+    return Opnd{(const z_t*)v_lower + j * n2, 0, OP_N, false, re};  // (j+1, j)
   };
   auto PR = [&](int i, int j) -> Opnd {
     if (i == j) return Opnd{(const z_t*)pr_diag + i * n2, sd, OP_N, false};

@@ -105,7 +105,9 @@ __device__ __forceinline__ void load_stage(const ZGemmDesc& d, int kt, const KtB
   }
 }
 
-template <class CF>
+// RV: every term of the group has a real operand (kTermReal), so the 3M
+// product ai*bi vanishes and is not issued (2 DMMA products per complex one).
+template <class CF, bool RV = false>
 __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_constant__ ZGemmGroup grp) {
   extern __shared__ __align__(16) z_t smem[];
   const ZGemmDesc& d = grp.d[blockIdx.z];
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
     const ZTerm& t = d.t[kb.term(kt)];
     const bool a_kc = !op_trans(t.opA);
     const bool b_kc = op_trans(t.opB);
-    const unsigned long long negm = t.neg ? kSign : 0ull;
+    const unsigned long long negm = (t.neg & 1) ? kSign : 0ull;
     const unsigned long long conjA = op_conj(t.opA) ? kSign : 0ull;
     const unsigned long long conjB = op_conj(t.opB) ? kSign : 0ull;
     // fragment addressing: element (mn, k) at mn*s_mn + k*s_k
@@ -267,10 +269,12 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
         for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
           for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
+        if constexpr (!RV) {
 #pragma unroll
-        for (int i = 0; i < CF::TM; ++i)
+          for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
-          for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], bi[j]);
+            for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], bi[j]);
+        }
 #pragma unroll
         for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
@@ -312,11 +316,11 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
   }
 }
 
-template <class CF>
+template <class CF, bool RV = false>
 int launch_cfg(const ZGemmGroup& g, cudaStream_t stream) {
   static bool attr_done = false;
   if (!attr_done) {
-    NEGF_CUDA_CHECK(cudaFuncSetAttribute(zgemm_kernel<CF>,
+    NEGF_CUDA_CHECK(cudaFuncSetAttribute(zgemm_kernel<CF, RV>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)CF::SMEM));
     attr_done = true;
@@ -333,7 +337,7 @@ int launch_cfg(const ZGemmGroup& g, cudaStream_t stream) {
   for (int i = 0; i < g.n; ++i)
     for (int t = 0; t < g.d[i].nterms; ++t) maxk = g.d[i].t[t].K > maxk ? g.d[i].t[t].K : maxk;
   const int tok = prof_begin(maxk <= 32 ? PROF_ZGEMM_SMALLK : PROF_ZGEMM, stream);
-  zgemm_kernel<CF><<<grid, CF::NT, CF::SMEM, stream>>>(g);
+  zgemm_kernel<CF, RV><<<grid, CF::NT, CF::SMEM, stream>>>(g);
   NEGF_LAUNCHED();
   if (tok >= 0) {
     double fl = 0.0, by = 0.0;
@@ -423,7 +427,13 @@ int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
   }
   if (mx <= 32) return launch_cfg<CfgSmall>(g, stream);
   int mm = 0;
-  for (int i = 0; i < g.n; ++i) mm = g.d[i].M > mm ? g.d[i].M : mm;
+  bool real = true;  // every term has a real operand: 2-product Gauss kernel
+  for (int i = 0; i < g.n; ++i) {
+    mm = g.d[i].M > mm ? g.d[i].M : mm;
+    for (int t = 0; t < g.d[i].nterms; ++t) real &= (g.d[i].t[t].neg & kTermReal) != 0;
+  }
+  if (real && gemm_algo() == 2)
+    return mm <= 32 ? launch_cfg<CfgGauss2S, true>(g, stream) : launch_cfg<CfgGauss2, true>(g, stream);
   if (mm <= 32) {  // short M
     if (gemm_algo() == 2) return launch_cfg<CfgGauss2S>(g, stream);
     if (gemm_algo() >= 4) return launch_cfg<CfgGauss3>(g, stream);

@@ -38,8 +38,11 @@ struct ZTerm {
   int ldb;
   int opB;
   int K;
-  int neg;  // 1: subtract this term
+  int neg;  // bit 0: subtract this term; bit 1 (kTermReal): A or B has an exactly
+            // zero imaginary part, so the 3M kernel skips the ai*bi product
 };
+
+constexpr int kTermReal = 2;
 
 constexpr int kMaxTerms = 4;
 
@@ -85,11 +88,11 @@ inline ZGemmDesc zdesc_default() {
 }
 
 inline ZTerm zterm(const z_t* A, long long sA, int lda, int opA, const z_t* B, long long sB,
-                   int ldb, int opB, int K, bool neg = false) {
+                   int ldb, int opB, int K, bool neg = false, bool real_operand = false) {
   ZTerm t;
   t.A = A; t.sA = sA; t.lda = lda; t.opA = opA;
   t.B = B; t.sB = sB; t.ldb = ldb; t.opB = opB;
-  t.K = K; t.neg = neg ? 1 : 0;
+  t.K = K; t.neg = (neg ? 1 : 0) | (real_operand ? kTermReal : 0);
   return t;
 }
 

@@ -76,6 +76,41 @@ def test_screened_solve_matches_oracle(cuda, n_b, bs, ne):
         assert rel(b[k].cpu().numpy(), ref[rk]) < TOL, k
 
 
+@pytest.mark.parametrize("complex_v", [False, True])
+def test_w_assembly_real_v_path(cuda, complex_v):
+    """A real V takes the 2-product Gauss path (ScreenedSolver.v_real): bitwise
+    equal to the general 3-product path; a complex V is detected and matches
+    the oracle's W system."""
+    rng = np.random.default_rng(3)
+    n_b, bs, ne = 5, 24, 3
+    v = orc.coulomb_matrix(n_b, bs)
+    if complex_v:
+        v = tuple(x + 1e-4j * rng.standard_normal(x.shape) for x in v)
+    mk = lambda *s: 0.3 * (rng.standard_normal(s) + 1j * rng.standard_normal(s))
+    pr = (mk(ne, n_b, bs, bs) - 1j * np.eye(bs), mk(ne, n_b - 1, bs, bs), mk(ne, n_b - 1, bs, bs))
+    pl = (mk(ne, n_b, bs, bs), mk(ne, n_b - 1, bs, bs))
+    pg = (mk(ne, n_b, bs, bs), mk(ne, n_b - 1, bs, bs))
+    outs = []
+    for force_complex in (False, True):
+        solver = ScreenedSolver(v, ScbaOptions(), cuda)
+        assert solver.v_real == (not complex_v)
+        if force_complex:
+            solver.v_real = False
+        b = solver.buffers(ne)
+        for k, a in (("pr_diag", pr[0]), ("pr_upper", pr[1]), ("pr_lower", pr[2]), ("pl_diag", pl[0]),
+                     ("pl_upper", pl[1]), ("pg_diag", pg[0]), ("pg_upper", pg[1])):
+            b[k].copy_(t(a, cuda))
+        solver._assemble(b, ne)
+        outs.append({k: b[k].cpu().numpy() for k in ("m_diag", "m_upper", "m_lower", "bl_diag", "bl_upper",
+                                                       "bg_diag", "bg_upper")})
+    for k in outs[0]:
+        np.testing.assert_array_equal(outs[0][k], outs[1][k])
+    mw, srcs = orc.w_system(v, pr, pl, pg)
+    for k, ref in (("m_diag", mw[0]), ("m_upper", mw[1]), ("m_lower", mw[2]), ("bl_diag", srcs["<"][0]),
+                   ("bl_upper", srcs["<"][1]), ("bg_diag", srcs[">"][0]), ("bg_upper", srcs[">"][1])):
+        assert rel(outs[0][k], ref) < 1e-12, k
+
+
 def test_scba_small_matches_reference_scba_run(golden, cuda):
     """3 GW iterations, 6x4 chain + Coulomb, 32 energies (batches of 10)."""
     g = golden("golden_scba_small.npz")
