@@ -137,7 +137,7 @@ __global__ void zinv_small_kernel(const z_t* __restrict__ S, long long sS, int l
 // ---------------------------------------------------------------------------
 // Blocked path.
 // Panel LU (candidate rows k0..n-1, columns k0..k0+NB-1) held in REGISTERS:
-// TPR = NB/16 threads per row, 16 columns each, so the rank-1 updates are
+// TPR = NB/16 threads per row, 16 interleaved columns each (slot c of thread h = column c*TPR + h), so the rank-1 updates are
 // register FMAs and a column step costs one block argmax (shuffles + barrier)
 // and one pivot-row broadcast through smem (barrier). Rows are never moved:
 // a pivoted row retires from the active set, and LAPACK's row order is
@@ -159,6 +159,8 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
   __shared__ z_t pinv_s[NB * LD];     // Pinv
   __shared__ z_t rdiag_s[NB];         // 1 / U_kk
   __shared__ int posinv_s[1024];      // final position -> physical row
+  __shared__ int piv_s[NB];           // pivot position chosen at each column
+  __shared__ z_t pval_s[NB];          // pivot values
   __shared__ double rv[32];
   __shared__ int ri[32], rp[32];
   __shared__ int sbad;
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
   z_t v[16];
 #pragma unroll
   for (int c = 0; c < 16; ++c)
-    v[c] = (have && 16 * h + c < w) ? a[(long long)(k0 + r) * n + k0 + 16 * h + c] : make_double2(0.0, 0.0);
+    v[c] = (have && c * TPR + h < w) ? a[(long long)(k0 + r) * n + k0 + c * TPR + h] : make_double2(0.0, 0.0);
   bool act = have;
   int pos = r;
   if (tid == 0) {
@@ -188,9 +190,15 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
   // The column loop stays rolled: unrolling it multiplies the code by NB and
   // the kernel then runs out of the instruction cache. Register elements are
   // selected with predicated moves instead of runtime indexing.
+#ifdef NEGF_EXP_TIMING
+  long long ph_a = 0, ph_b = 0, ph_c = 0, ph_d = 0, tq = clock64();
+#define PH(x) do { long long _t = clock64(); x += _t - tq; tq = _t; } while (0)
+#else
+#define PH(x) do { } while (0)
+#endif
 #pragma unroll 1
   for (int j = 0; j < w; ++j) {
-    const int hj = j / 16, cj = j % 16;
+    const int hj = j % TPR, cj = j / TPR;  // column j sits in slot cj of thread-column hj
     z_t vj = v[0];
 #pragma unroll
     for (int c = 1; c < 16; ++c)
@@ -223,6 +231,7 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
         rp[warp] = mpos;
       }
     }
+    PH(ph_a);
     __syncthreads();
     {  // cross-warp stage, redundantly in every warp (lanes < nw hold the entries)
       const double wv = lane < nw ? rv[lane] : 0.0;
@@ -239,13 +248,15 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
       br = __shfl_sync(0xffffffffu, wr, src);
       bp = mpos;
     }
+    PH(ph_b);
     // (2) pivot row broadcast (+ its reciprocal pivot, computed once)
     if (act && r == br) {
 #pragma unroll
-      for (int c = 0; c < 16; ++c) prow_s[16 * h + c] = v[c];
+      for (int c = 0; c < 16; ++c) prow_s[c * TPR + h] = v[c];
       if (h == hj) ip_s = zinv(vj);
     }
     __syncthreads();
+    PH(ph_c);
     const z_t pv = prow_s[j];
     const z_t ipv = ip_s;
     // (3) multipliers and rank-1 update of the other active rows (registers)
@@ -260,22 +271,48 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
       pos = j;
     } else if (act) {
       const z_t l = zmul(own, ipv);
+      // slots below cj hold factored columns on every thread
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
-        const int gc = 16 * h + c;
-        if (gc > j) v[c] = zfms(l, prow_s[gc], v[c]);
-        else if (gc == j) v[c] = l;
+        if (c >= cj) {
+          const int gc = c * TPR + h;
+          if (gc > j) v[c] = zfms(l, prow_s[gc], v[c]);
+          else if (gc == j) v[c] = l;
+        }
       }
       if (pos == j) pos = bp;  // LAPACK interchange: the row at position j moves to bp
     } else if (have && pos == j) {
       pos = bp;
     }
+    // pivot bookkeeping (ipiv, |pivot| range, singular flag) after the loop,
+    // off the column-to-column dependency chain
     if (tid == 0) {
-      ipiv[(long long)b * n + k0 + j] = k0 + bp;
-      const double m = hypot(pv.x, pv.y);
-      if (!(m > 0.0) || !isfinite(m)) sbad = 1;
-      smax = fmax(smax, m);
-      smin = fmin(smin, m);
+      piv_s[j] = bp;
+      pval_s[j] = pv;
+    }
+    PH(ph_d);
+  }
+#undef PH
+  __syncthreads();
+  if (warp == 0) {  // ipiv, |pivot| range and singularity over the panel's w pivots
+    double mx = 0.0, mn = INFINITY;
+    int bad = 0;
+    for (int q = lane; q < w; q += 32) {
+      ipiv[(long long)b * n + k0 + q] = k0 + piv_s[q];
+      const double m = hypot(pval_s[q].x, pval_s[q].y);
+      if (!(m > 0.0) || !isfinite(m)) bad = 1;
+      mx = fmax(mx, m);
+      mn = fmin(mn, m);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+      mn = fmin(mn, __shfl_down_sync(0xffffffffu, mn, o));
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      smax = fmax(smax, mx);
+      smin = fmin(smin, mn);
+      if (bad) sbad = 1;
     }
   }
 #ifdef NEGF_EXP_TIMING
@@ -287,7 +324,7 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
     posinv_s[pos] = r;
     if (pos < w) {
 #pragma unroll
-      for (int c = 0; c < 16; ++c) blk[pos * LD + 16 * h + c] = v[c];
+      for (int c = 0; c < 16; ++c) blk[pos * LD + c * TPR + h] = v[c];
     }
   }
   __syncthreads();
@@ -371,7 +408,8 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
 #ifdef NEGF_EXP_TIMING
   __syncthreads();
   if (tid == 0 && b == 0 && k0 == 64)
-    printf("PANELCLK cols %lld pinv %lld maps %lld T %lld\n", clk1 - clk0, clk2 - clk1, clk3 - clk2, clock64() - clk3);
+    printf("PANELCLK cols %lld pinv %lld maps %lld T %lld | argmax-warp %lld cross %lld bcast %lld update %lld\n",
+           clk1 - clk0, clk2 - clk1, clk3 - clk2, clock64() - clk3, ph_a, ph_b, ph_c, ph_d);
 #endif
   if (tid == 0) {
     umaxmin[2 * b] = smax;
