@@ -165,17 +165,33 @@ class ScreenedSolver:
         self.opt = options
         self._buf, self._n_e = None, 0
 
-    def buffers(self, n_e: int) -> dict:
+    def buffers(self, n_e: int, pool=()) -> dict:
+        """Block stacks of one energy batch. ``pool``: tensors of another stage
+        that is never live at the same time as the W solve (scba_run passes
+        the carrier's stacks), reused by shape so G and W do not both hold
+        C3-size block memory."""
         if self._buf is not None and self._n_e == n_e:
             return self._buf
         self._buf = None
         nb, bs, dev = self.n_b, self.bs, self.dev
         d, o = (n_e, nb, bs, bs), (n_e, nb - 1, bs, bs)
-        b = {k: torch.empty(d, dtype=Z, device=dev) for k in
-             ("pr_diag", "pl_diag", "pg_diag", "m_diag", "bl_diag", "bg_diag", "wr_diag", "wl_diag", "wg_diag")}
-        b.update({k: torch.empty(o, dtype=Z, device=dev) for k in
-                  ("pr_upper", "pr_lower", "pl_upper", "pg_upper", "m_upper", "m_lower", "bl_upper", "bg_upper",
-                   "wr_upper", "wr_lower", "wl_upper", "wg_upper")})
+        free = [x for x in pool if x.dtype == Z and x.is_contiguous()]
+
+        def take(shape):
+            for i, x in enumerate(free):
+                if tuple(x.shape) == shape:
+                    return free.pop(i)
+            return torch.empty(shape, dtype=Z, device=dev)
+
+        b = {k: take(d) for k in ("pr_diag", "pl_diag", "pg_diag", "m_diag", "bl_diag", "bg_diag")}
+        b.update({k: take(o) for k in
+                  ("pr_upper", "pr_lower", "pl_upper", "pg_upper", "m_upper", "m_lower", "bl_upper", "bg_upper")})
+        # P blocks are dead once M_W and B_W are assembled: the RGF writes W
+        # into them (7 fewer block stacks per batch)
+        for part in ("diag", "upper", "lower"):
+            b["wr_" + part] = b["pr_" + part]
+        for part in ("diag", "upper"):
+            b["wl_" + part], b["wg_" + part] = b["pl_" + part], b["pg_" + part]
         b["obc_status"] = torch.zeros(2 * n_e, dtype=torch.int32, device=dev)
         b["obc_iters"] = torch.zeros(2 * n_e, dtype=torch.int32, device=dev)
         b["stein_status"] = torch.zeros(4 * n_e, dtype=torch.int32, device=dev)
@@ -185,7 +201,8 @@ class ScreenedSolver:
         return b
 
     def solve(self, n_e: int, check: bool = True, timer=None, memo: tuple | None = None) -> dict:
-        """Inputs in buffers pr_*/pl_*/pg_* (filled by the caller). ``memo`` =
+        """Inputs in buffers pr_*/pl_*/pg_* (filled by the caller; the W outputs
+        wr_*/wl_*/wg_* reuse their storage). ``memo`` =
         (SurfaceCache, ld, e0, tol_memo) as in CarrierSolver.solve."""
         import contextlib
 
@@ -500,7 +517,11 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         for e0 in range(0, n_own, batch):
             e1 = min(n_own, e0 + batch)
             nb_ = e1 - e0
-            wb = screened.buffers(nb_)
+            # the carrier's stacks of this batch size are dead during the W stage
+            pool = list(blocks.values()) if blocks is not None and blocks["sr_diag"].shape[0] == nb_ else []
+            cb = carrier._buf if carrier._buf is not None and carrier._n_e == nb_ else {}
+            pool += [x for x in cb.values() if x.dim() == 4]
+            wb = screened.buffers(nb_, pool)
             with _T("layout"):
                 lay.unpack_retarded(pru, prl, e0, nb_, wb["pr_diag"], wb["pr_upper"], wb["pr_lower"])
                 lay.unpack_lg(pl, e0, nb_, wb["pl_diag"], wb["pl_upper"])
