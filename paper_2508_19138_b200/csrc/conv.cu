@@ -125,6 +125,8 @@ __device__ __forceinline__ void dft_r(z_t* e) {
   else dft2<INV>(e[0], e[1]);
 }
 
+// CTAs of PACK_T threads are register-capped for 3 resident CTAs per SM
+// (the Sigma kernel otherwise takes 173 registers and drops to 2).
 // Short rows (Q = L/E < PACK_T threads) are packed PACK_T / Q to a CTA of
 // PACK_T threads, each row with its own shared-memory slice: one row per CTA
 // at L = 16 would run 2 of 32 threads and launch one CTA per entry row.
@@ -294,7 +296,7 @@ __device__ void retarded_tail(z_t* d, z_t* A, z_t* B, const RowGeom<E>& g, int n
 }
 
 template <int E, int MAXT>
-__global__ void __launch_bounds__(MAXT) pol_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg, int n,
+__global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? 3 : MAXT == 256 ? 2 : 1) pol_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg, int n,
                                                    int L, const z_t* __restrict__ tw, const z_t* __restrict__ kf,
                                                    const z_t* __restrict__ kcf,
                                                    const unsigned char* __restrict__ diag, double2 scale, z_t* pl,
@@ -345,7 +347,7 @@ __global__ void __launch_bounds__(MAXT) pol_kernel(const z_t* __restrict__ gl, c
 }
 
 template <int E, int MAXT>
-__global__ void __launch_bounds__(MAXT) sigma_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg,
+__global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? 3 : MAXT == 256 ? 2 : 1) sigma_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg,
                                                      const z_t* __restrict__ wl, const z_t* __restrict__ wg,
                                                      const long long* __restrict__ w_rows, int n, int L,
                                                      const z_t* __restrict__ tw, const z_t* __restrict__ kf,
@@ -398,7 +400,7 @@ __global__ void __launch_bounds__(MAXT) sigma_kernel(const z_t* __restrict__ gl,
 
 // Generic convolve_energy (convolve.py:39-71): mode 0 convolution, 1 correlation.
 template <int E, int MAXT>
-__global__ void __launch_bounds__(MAXT) conv_kernel(const z_t* __restrict__ x1, const z_t* __restrict__ x2, int n,
+__global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? 3 : MAXT == 256 ? 2 : 1) conv_kernel(const z_t* __restrict__ x1, const z_t* __restrict__ x2, int n,
                                                     int L, int mode, const z_t* __restrict__ tw, double2 scale,
                                                     z_t* out, long long n_rows) {
   extern __shared__ __align__(16) z_t sm[];
@@ -433,7 +435,7 @@ __global__ void __launch_bounds__(MAXT) conv_kernel(const z_t* __restrict__ x1, 
 }
 
 template <int E, int MAXT>
-__global__ void __launch_bounds__(MAXT) ret_kernel(const z_t* __restrict__ xl, const z_t* __restrict__ xg, int n,
+__global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? 3 : MAXT == 256 ? 2 : 1) ret_kernel(const z_t* __restrict__ xl, const z_t* __restrict__ xg, int n,
                                                    int L, const z_t* __restrict__ tw, const z_t* __restrict__ kf,
                                                    z_t* out, long long n_rows) {
   extern __shared__ __align__(16) z_t sm[];
@@ -487,7 +489,7 @@ int negf_conv_polarization(long long n_rows, int n_e, int L, const void* gl, con
       !pl || !pg)
     return -1;
   if (n_rows == 0) return 0;
-  auto* kfn = threads_for(L) > 256 ? pol_kernel<8, 512> : pol_kernel<8, 256>;
+  auto* kfn = threads_for(L) > 256 ? pol_kernel<8, 512> : threads_for(L) > PACK_T ? pol_kernel<8, 256> : pol_kernel<8, PACK_T>;
   int rc = smem_setup((const void*)kfn, L);
   if (rc) return rc;
   {
@@ -509,7 +511,7 @@ int negf_conv_sigma(long long n_rows, int n_e, int L, const void* gl, const void
       !kf || !kcf || !sl || !sg)
     return -1;
   if (n_rows == 0) return 0;
-  auto* kfn = threads_for(L) > 256 ? sigma_kernel<8, 512> : sigma_kernel<8, 256>;
+  auto* kfn = threads_for(L) > 256 ? sigma_kernel<8, 512> : threads_for(L) > PACK_T ? sigma_kernel<8, 256> : sigma_kernel<8, PACK_T>;
   int rc = smem_setup((const void*)kfn, L);
   if (rc) return rc;
   {
@@ -531,7 +533,7 @@ int negf_convolve_energy(long long n_rows, int n_e, int L, const void* x1, const
       !x2 || !tw || !out)
     return -1;
   if (n_rows == 0) return 0;
-  auto* kfn = threads_for(L) > 256 ? conv_kernel<8, 512> : conv_kernel<8, 256>;
+  auto* kfn = threads_for(L) > 256 ? conv_kernel<8, 512> : threads_for(L) > PACK_T ? conv_kernel<8, 256> : conv_kernel<8, PACK_T>;
   int rc = smem_setup((const void*)kfn, L);
   if (rc) return rc;
   {
@@ -551,7 +553,7 @@ int negf_retarded_from_lg(long long n_rows, int n_e, int L, const void* x_lesser
       !kf || !out)
     return -1;
   if (n_rows == 0) return 0;
-  auto* kfn = threads_for(L) > 256 ? ret_kernel<8, 512> : ret_kernel<8, 256>;
+  auto* kfn = threads_for(L) > 256 ? ret_kernel<8, 512> : threads_for(L) > PACK_T ? ret_kernel<8, 256> : ret_kernel<8, PACK_T>;
   int rc = smem_setup((const void*)kfn, L);
   if (rc) return rc;
   {
