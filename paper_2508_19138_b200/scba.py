@@ -90,6 +90,10 @@ class ScbaOptions:
     beyn: BeynOptions = field(default_factory=lambda: BeynOptions())
     # scba.py:943: a warm-start initial_sigma is used only when reset_sigma is False
     reset_sigma: bool = True
+    # scba.py:171, 913-915: compare every selected solve with a dense inverse
+    # and every P / Sigma convolution with the direct sum (checks.py);
+    # ScbaResult.oracle_deviations = {"solve_vs_dense", "fft_vs_direct"}
+    oracle_mode: bool = False
 
     def __post_init__(self) -> None:
         if self.max_iter < 1:
@@ -461,6 +465,19 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         cache = SurfaceCache(options.memoizer.n_fpi_retarded, options.memoizer.n_fpi_lg)
     tol_memo = options.tol / 10.0
     stats_by_it = []
+    odev = {"solve_vs_dense": 0.0, "fft_vs_direct": 0.0} if options.oracle_mode else None
+
+    def solve_check(bb, w: bool) -> None:
+        from .checks import dense_solution_deviation
+
+        x = "w" if w else "x"
+        dv, sc = dense_solution_deviation(
+            (bb["m_diag"], bb["m_upper"], bb["m_lower"]),
+            {"<": (bb["bl_diag"], bb["bl_upper"]), ">": (bb["bg_diag"], bb["bg_upper"])},
+            (bb[x + "r_diag"], bb[x + "r_upper"], bb[x + "r_lower"]),
+            {"<": (bb[x + "l_diag"], bb[x + "l_upper"]), ">": (bb[x + "g_diag"], bb[x + "g_upper"])})
+        odev["solve_vs_dense"] = max(odev["solve_vs_dense"], dv / (sc + 1e-300))
+
     memo = (lambda e0: (cache, max(n_own, 1), e0, tol_memo)) if cache is not None else (lambda e0: None)
     for it in range(max_iter):
         n_iter = it + 1
@@ -487,6 +504,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             with _T("G: OBC+RGF"):
                 b = carrier.solve(my_e[e0:e1], sigma=blocks, n_e=nb_, memo=memo(e0))
             g_identity_defect(b, nb_, n_b, bs, defects[0:2])
+            if odev is not None:
+                solve_check(b, False)
             with _T("layout"):
                 lay.pack(b["xl_diag"], b["xl_upper"], gl_c, e0)
                 lay.pack(b["xg_diag"], b["xg_upper"], gg_c, e0)
@@ -509,6 +528,11 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         with _T("convolution"):
             p_rows = polarization(gl, gg, diag_rows, de)
         entry_identity_defect(*p_rows, defects[2:4])
+        if odev is not None:
+            from .checks import polarization_deviation
+
+            dv, sc = polarization_deviation(gl, gg, p_rows[0], p_rows[1], diag_rows, de)
+            odev["fft_vs_direct"] = max(odev["fft_vs_direct"], dv / (sc + 1e-300))
         with _T("transpose"):
             pl, pg, pru, prl = (tr.to_energy_major(x) for x in p_rows)
         del p_rows
@@ -527,6 +551,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
                 lay.unpack_lg(pl, e0, nb_, wb["pl_diag"], wb["pl_upper"])
                 lay.unpack_lg(pg, e0, nb_, wb["pg_diag"], wb["pg_upper"])
             wb = screened.solve(nb_, timer=_T, memo=memo(e0))
+            if odev is not None:
+                solve_check(wb, True)
             with _T("layout"):
                 lay.pack(wb["wl_diag"], wb["wl_upper"], wl_c, e0)
                 lay.pack(wb["wg_diag"], wb["wg_upper"], wg_c, e0)
@@ -538,6 +564,11 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         with _T("convolution"):
             s_rows = self_energy(gl, gg, wl, wg, None, diag_rows, de)
         entry_identity_defect(*s_rows, defects[4:6])
+        if odev is not None:
+            from .checks import self_energy_deviation
+
+            dv, sc = self_energy_deviation(gl, gg, wl, wg, s_rows[0], s_rows[1], diag_rows, de)
+            odev["fft_vs_direct"] = max(odev["fft_vs_direct"], dv / (sc + 1e-300))
         with _T("transpose"):
             raw = tuple(tr.to_energy_major(x) for x in s_rows)
         del s_rows
@@ -572,6 +603,11 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     result["iteration_s"] = iter_times
     result["residuals"] = np.asarray(residuals)
     result["identity_defects"] = identity_defects
+    if odev is not None:
+        o = comm.allreduce_max([odev["solve_vs_dense"], odev["fft_vs_direct"]], dev)
+        result["oracle_deviations"] = {"solve_vs_dense": o[0], "fft_vs_direct": o[1]}
+    else:
+        result["oracle_deviations"] = {}
     result["converged"] = converged
     result["n_iter"] = n_iter
     result["n_blocks"], result["block_size"] = n_b, bs

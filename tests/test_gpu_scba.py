@@ -262,3 +262,21 @@ def test_scba_warm_start_reset_sigma(cuda):
     with pytest.raises(ValueError, match="warm-start"):
         scba_run(h, v, e, 1e-3, c, ScbaOptions(max_iter=2, reset_sigma=False, memoizer=MEMO_OFF), device=cuda,
                  initial_sigma=bad)
+
+
+def test_scba_oracle_mode_deviations(golden, cuda):
+    """ScbaOptions.oracle_mode (scba.py:913-915): every G and W selected solve
+    against a dense inverse + triple product and every P / Sigma convolution
+    against the direct sum, reported like the reference's oracle_deviations;
+    results unchanged."""
+    g = golden("golden_scba_small.npz")
+    res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=3, tol=1e-12, batch=10, memoizer=MEMO_OFF,
+                                                          oracle_mode=True), device=cuda)
+    od = res.oracle_deviations
+    assert set(od) == {"solve_vs_dense", "fft_vs_direct"}
+    assert 0 < od["solve_vs_dense"] < 1e-10 and 0 < od["fft_vs_direct"] < 1e-10, od
+    assert rel(res["sigma_lesser"], g["sigma_lesser"]) < TOL
+    plain = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
+                     Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=1, memoizer=MEMO_OFF), device=cuda)
+    assert plain.oracle_deviations == {}
