@@ -53,6 +53,9 @@ class BeynOptions:
         if self.svd_tol <= 0:
             raise ValueError(f"svd_tol must be positive, got {self.svd_tol}")
 
+    def contour(self) -> dict:
+        return {"radius": self.radius, "center": 0.0, "n_quad": self.n_quad}
+
 
 @dataclass(frozen=True)
 class MemoizerOptions:
@@ -102,6 +105,8 @@ class ScbaOptions:
             raise ValueError(f"tol must be positive, got {self.tol}")
         if not 0 < self.mixing <= 1:
             raise ValueError(f"mixing must lie in (0, 1], got {self.mixing}")
+        if self.surface_tol <= 0:
+            raise ValueError(f"surface_tol must be positive, got {self.surface_tol}")
         if self.w_retarded_method not in ("sancho", "beyn", "fixed_point"):
             raise ValueError(f"unknown W retarded method {self.w_retarded_method!r}")
         if self.retarded_method not in ("sancho", "beyn", "fixed_point"):
