@@ -66,6 +66,72 @@ class ConvPlan:
         return _PLANS[key]
 
 
+# Longest circular grid of the shared-memory FFT engine (conv.cu: two
+# L-point complex arrays per row in one CTA). Series with 2 N_E - 1 > 4096
+# (N_E > 2048, C4's 4096 energies) run the same algebra through cuFFT
+# (torch.fft on the device), in row chunks.
+MAX_L_NATIVE = 4096
+_CHUNK_BYTES = 1 << 30
+
+
+def _chunks(n_rows: int, L: int):
+    step = max(1, _CHUNK_BYTES // (16 * L * 4))
+    for r0 in range(0, n_rows, step):
+        yield slice(r0, min(n_rows, r0 + step))
+
+
+def _proj_rows(x: torch.Tensor, diag) -> torch.Tensor:
+    if diag is not None:
+        m = diag.bool()
+        x[m] = 1j * x[m].imag
+    return x
+
+
+def _retarded_tail_fft(d: torch.Tensor, plan: "ConvPlan", up: torch.Tensor | None, lo: torch.Tensor | None) -> None:
+    """r_up = K*d, r_lo = -conj(conj(K)*d) on the L-grid (as retarded_tail in conv.cu)."""
+    n = d.shape[-1]
+    D = torch.fft.fft(d, n=plan.L, dim=-1)
+    if up is not None:
+        up.copy_(torch.fft.ifft(D * plan.kf, dim=-1)[:, :n])
+    if lo is not None:
+        lo.copy_(-torch.fft.ifft(D * plan.kcf, dim=-1)[:, :n].conj())
+
+
+def _pol_fft(gl, gg, diag, sc: complex, plan, out) -> None:
+    n, L = gl.shape[-1], plan.L
+    g2 = lambda x: x.reshape(-1, n)
+    gl2, gg2 = g2(gl), g2(gg)
+    o2 = [g2(o) for o in out]
+    for s in _chunks(gl2.shape[0], L):
+        a = torch.fft.fft(gl2[s], n=L, dim=-1)
+        b = torch.fft.fft(gg2[s], n=L, dim=-1)
+        p = torch.fft.ifft(a * -b.conj(), dim=-1)
+        dg = diag[s] if diag is not None else None
+        pl = _proj_rows(sc * p[:, :n], dg)
+        rev = torch.roll(torch.flip(p, dims=[-1]), 1, dims=-1)  # p[(L - k) % L]
+        pg = _proj_rows(sc * rev[:, :n].conj(), dg)
+        o2[0][s], o2[1][s] = pl, pg
+        _retarded_tail_fft(pg - pl, plan, o2[2][s] if out[2] is not None else None,
+                           o2[3][s] if out[3] is not None else None)
+
+
+def _sigma_fft(gl, gg, wl, wg, w_rows, diag, sc: complex, plan, out) -> None:
+    n, L = gl.shape[-1], plan.L
+    g2 = lambda x: x.reshape(-1, n)
+    gl2, gg2, wl2, wg2 = g2(gl), g2(gg), g2(wl), g2(wg)
+    o2 = [g2(o) for o in out]
+    for s in _chunks(gl2.shape[0], L):
+        dg = diag[s] if diag is not None else None
+        res = []
+        for gx, wx in ((gl2, wl2), (gg2, wg2)):
+            w = wx[w_rows[s]] if w_rows is not None else wx[s]
+            x = torch.fft.ifft(torch.fft.fft(gx[s], n=L, dim=-1) * torch.fft.fft(w, n=L, dim=-1), dim=-1)
+            res.append(_proj_rows(sc * x[:, :n], dg))
+        o2[0][s], o2[1][s] = res
+        _retarded_tail_fft(res[1] - res[0], plan, o2[2][s] if out[2] is not None else None,
+                           o2[3][s] if out[3] is not None else None)
+
+
 def _rows(x: torch.Tensor) -> int:
     return int(np.prod(x.shape[:-1])) if x.dim() > 1 else 1
 
@@ -86,6 +152,9 @@ def polarization(gl: torch.Tensor, gg: torch.Tensor, diag: torch.Tensor | None, 
     out = out or tuple(torch.empty_like(gl) for _ in range(4))
     sc = complex(prefactor) * de
     lib = _lib.load()
+    if plan.L > MAX_L_NATIVE:
+        _pol_fft(gl, gg, diag, sc, plan, out)
+        return out
     rc = lib.negf_conv_polarization(_rows(gl), n, plan.L, gl.data_ptr(), gg.data_ptr(), plan.tw.data_ptr(),
                                     plan.kf.data_ptr(), plan.kcf.data_ptr(), _lib.ptr(diag), sc.real, sc.imag,
                                     *(o.data_ptr() for o in out), _lib.stream_ptr(gl.device))
@@ -103,6 +172,9 @@ def self_energy(gl: torch.Tensor, gg: torch.Tensor, wl: torch.Tensor, wg: torch.
     out = out or tuple(torch.empty_like(gl) for _ in range(4))
     sc = complex(prefactor) * de
     lib = _lib.load()
+    if plan.L > MAX_L_NATIVE:
+        _sigma_fft(gl, gg, wl, wg, w_rows, diag, sc, plan, out)
+        return out
     rc = lib.negf_conv_sigma(_rows(gl), n, plan.L, gl.data_ptr(), gg.data_ptr(), wl.data_ptr(), wg.data_ptr(),
                              _lib.ptr(w_rows), plan.tw.data_ptr(), plan.kf.data_ptr(), plan.kcf.data_ptr(),
                              _lib.ptr(diag), sc.real, sc.imag, *(o.data_ptr() for o in out),
@@ -129,6 +201,14 @@ def convolve_energy(x1, x2, mode: str, prefactor: complex, de: float):
     plan = ConvPlan.get(n, a.device)
     out = torch.empty_like(a)
     sc = complex(prefactor) * de
+    if plan.L > MAX_L_NATIVE:
+        a2, b2, o2 = a.reshape(-1, n), b.reshape(-1, n), out.reshape(-1, n)
+        for s in _chunks(a2.shape[0], plan.L):
+            y = b2[s] if mode == MODE_CONVOLUTION else torch.roll(torch.flip(
+                torch.nn.functional.pad(b2[s], (0, plan.L - n)), dims=[-1]), 1, dims=-1)  # y[j] = b[-j]
+            x = torch.fft.ifft(torch.fft.fft(a2[s], n=plan.L, dim=-1) * torch.fft.fft(y, n=plan.L, dim=-1), dim=-1)
+            o2[s] = sc * x[:, :n]
+        return out if is_t else out.cpu().numpy()
     rc = _lib.load().negf_convolve_energy(_rows(a), n, plan.L, a.data_ptr(), b.data_ptr(),
                                           0 if mode == MODE_CONVOLUTION else 1, sc.real, sc.imag,
                                           plan.tw.data_ptr(), out.data_ptr(), _lib.stream_ptr(a.device))
@@ -145,6 +225,11 @@ def retarded_from_lg(x_lesser, x_greater):
     n = a.shape[-1]
     plan = ConvPlan.get(n, a.device)
     out = torch.empty_like(a)
+    if plan.L > MAX_L_NATIVE:
+        a2, b2, o2 = a.reshape(-1, n), b.reshape(-1, n), out.reshape(-1, n)
+        for s in _chunks(a2.shape[0], plan.L):
+            _retarded_tail_fft(b2[s] - a2[s], plan, o2[s], None)
+        return out if is_t else out.cpu().numpy()
     rc = _lib.load().negf_retarded_from_lg(_rows(a), n, plan.L, a.data_ptr(), b.data_ptr(), plan.tw.data_ptr(),
                                            plan.kf.data_ptr(), out.data_ptr(), _lib.stream_ptr(a.device))
     _lib.check(rc, "negf_retarded_from_lg")

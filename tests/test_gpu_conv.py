@@ -26,8 +26,9 @@ def test_convolve_and_retarded_match_reference_golden(golden, cuda, ne):
     assert rel(conv.retarded_from_lg(x1, x2), g[f"n{ne}_ret"]) < TOL
 
 
-@pytest.mark.parametrize("ne", [1, 2, 3, 16, 32, 64, 100, 256, 1024, 2048])
+@pytest.mark.parametrize("ne", [1, 2, 3, 16, 32, 64, 100, 256, 1024, 2048, 2049, 4096])
 def test_convolutions_match_oracle_sizes(cuda, ne):
+    """N_E > 2048 (L > 4096) takes the cuFFT path (conv.MAX_L_NATIVE)."""
     rng = np.random.default_rng(ne)
     x1 = rng.standard_normal((5, ne)) + 1j * rng.standard_normal((5, ne))
     x2 = rng.standard_normal((5, ne)) + 1j * rng.standard_normal((5, ne))
@@ -36,7 +37,8 @@ def test_convolutions_match_oracle_sizes(cuda, ne):
     assert rel(conv.retarded_from_lg(x1, x2), orc.retarded_from_lg(x1, x2)) < TOL
 
 
-@pytest.mark.parametrize("ne,rows", [(3, 517), (8, 37), (16, 37), (16, 1001), (128, 37), (300, 75), (2048, 37)])
+@pytest.mark.parametrize("ne,rows", [(3, 517), (8, 37), (16, 37), (16, 1001), (128, 37), (300, 75), (2048, 37),
+                                     (2100, 9), (4096, 5)])
 def test_fused_polarization_and_sigma_match_oracle(cuda, ne, rows):
     """Short series pack several entry rows per CTA (ragged last CTA covered)."""
     rng = np.random.default_rng(7 + ne)
