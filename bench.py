@@ -449,6 +449,8 @@ def run_scgw(args, dev, world, rank, barrier) -> dict:
         gbs = c_by.value / (c_ms.value * 1e-3) / 1e9 if c_ms.value > 0 else 0.0
         hbm[name] = {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                      "launches": c_n.value, "ms": c_ms.value, "algorithmic_bytes": per}
+        if cls == 9 and c_n.value == 0:
+            hbm[name]["note"] = "no native launches: N_E > 2048 runs the convolutions through cuFFT (conv.MAX_L_NATIVE)"
     lib.negf_prof_reset()
     t = torch.tensor([dt], dtype=torch.float64, device=dev)
     if world > 1:

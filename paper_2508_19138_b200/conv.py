@@ -70,7 +70,7 @@ class ConvPlan:
 # L-point complex arrays per row in one CTA). Series with 2 N_E - 1 > 4096
 # (N_E > 2048, C4's 4096 energies) run the same algebra through cuFFT
 # (torch.fft on the device), in row chunks.
-MAX_L_NATIVE = 4096
+MAX_L_NATIVE = int(__import__("os").environ.get("NEGF_CONV_MAX_L", "4096"))  # env: tests of the cuFFT leg
 _CHUNK_BYTES = 1 << 30
 
 
