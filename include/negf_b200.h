@@ -291,6 +291,16 @@ long long negf_pattern_entries(int n_b, int bs);
 int negf_pack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* x_diag,
                  const void* x_upper, void* out, long long ld, int e0, void* stream);
 /* _scatter_lg (scba.py:295-308): diagonal blocks get X[c][r] = -conj X[r][c]. */
+/* negf_pack_lg fused with the E -> nnz redistribution (scba.py:342-368,
+ * to_entry_major): entry row t goes to rank s with row_start[s] <= t <
+ * row_start[s+1] (device array, n_ranks + 1 values), written into dest[s]
+ * (device array of n_ranks device pointers -- peer memory mapped over NVLink,
+ * e.g. symmetric-memory buffers) at row t - row_start[s], column col0 + e of
+ * a row-major (rows, ld) complex128 array. n_ranks <= 16. The caller orders
+ * the peers' reads after all writes (a cross-rank barrier). */
+int negf_pack_lg_p2p(int n_e, int n_b, int bs, const int* tri_q, const void* x_diag, const void* x_upper,
+                     int n_ranks, const unsigned long long* dest, const long long* row_start, long long ld,
+                     int col0, void* stream);
 int negf_unpack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* in, long long ld,
                    int e0, void* x_diag, void* x_upper, void* stream);
 /* _scatter_retarded (scba.py:311-325): upper values at (r,c), lower values at

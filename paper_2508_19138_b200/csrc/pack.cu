@@ -70,6 +70,52 @@ __global__ void pack_lg_kernel(Pat p, const int* __restrict__ tri_q, int n_e,
   }
 }
 
+// blocks -> series, fused with the E -> nnz redistribution: entry row tt
+// belongs to rank s (row_start[s] <= tt < row_start[s+1]) and is written
+// straight into that rank's entry-major array (peer memory over NVLink,
+// ld = N_E columns, this rank's energies at column col0 + e). Each warp
+// stores 32 consecutive energies of one row (512 B runs).
+constexpr int kMaxRanks = 16;
+
+__global__ void pack_lg_p2p_kernel(Pat p, const int* __restrict__ tri_q, int n_e,
+                                   const z_t* __restrict__ xd, const z_t* __restrict__ xu, int n_ranks,
+                                   const unsigned long long* __restrict__ dest,
+                                   const long long* __restrict__ row_start, long long ld, int col0) {
+  __shared__ z_t tile[T][T + 1];
+  __shared__ long long rs[kMaxRanks + 1];
+  __shared__ unsigned long long ds[kMaxRanks];
+  const long long t0 = (long long)blockIdx.x * T;
+  const int eb = blockIdx.y * T;
+  const long long n2 = (long long)p.bs * p.bs;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * T + tx;
+  if (tid <= n_ranks) rs[tid] = row_start[tid];
+  if (tid < n_ranks) ds[tid] = dest[tid];
+  const long long t = t0 + tx;
+  int bi = 0, kind = 0, q = 0;
+  const bool ok = t < p.n_entries;
+  if (ok) locate(p, tri_q, t, bi, kind, q);
+  for (int k = ty; k < T; k += 8) {
+    const int e = eb + k;
+    if (ok && e < n_e) {
+      const z_t* src = kind == 0 ? xd + ((long long)e * p.n_b + bi) * n2
+                                 : xu + ((long long)e * (p.n_b - 1) + bi) * n2;
+      tile[k][tx] = src[q];
+    }
+  }
+  __syncthreads();
+  for (int k = ty; k < T; k += 8) {
+    const long long tt = t0 + k;
+    const int e = eb + tx;
+    if (tt < p.n_entries && e < n_e) {
+      int s = 0;
+      while (s + 1 < n_ranks && tt >= rs[s + 1]) ++s;
+      z_t* out = reinterpret_cast<z_t*>(ds[s]);
+      out[(tt - rs[s]) * ld + col0 + e] = tile[tx][k];
+    }
+  }
+}
+
 // series -> blocks. mode 0: lg (mirror rule on diagonal blocks);
 // mode 1: retarded (upper values at (r,c), lower values at (c,r)).
 __global__ void unpack_kernel(Pat p, const int* __restrict__ tri_q, int n_e,
@@ -151,6 +197,26 @@ int negf_pack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* x_diag,
     ProfSpan ps_pack_lg_kernel(PROF_LAYOUT, (cudaStream_t)(stream), 0.0, 32.0 * (double)p.n_entries * n_e);
     pack_lg_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(p, tri_q, n_e, (const z_t*)x_diag,
                                                              (const z_t*)x_upper, (z_t*)out, ld, e0);
+    NEGF_LAUNCHED();
+  }
+  return 0;
+}
+
+int negf_pack_lg_p2p(int n_e, int n_b, int bs, const int* tri_q, const void* x_diag, const void* x_upper,
+                     int n_ranks, const unsigned long long* dest, const long long* row_start, long long ld,
+                     int col0, void* stream) {
+  if (n_e < 0 || n_b < 1 || bs < 1 || !tri_q || !x_diag || n_ranks < 1 || n_ranks > kMaxRanks || !dest ||
+      !row_start || col0 < 0 || ld < col0 + n_e)
+    return -1;
+  if (n_b > 1 && !x_upper) return -1;
+  if (n_e == 0) return 0;
+  Pat p = make_pat(n_b, bs);
+  dim3 grid((unsigned)((p.n_entries + T - 1) / T), (n_e + T - 1) / T), block(T, 8);
+  {
+    ProfSpan ps_pack(PROF_LAYOUT, (cudaStream_t)(stream), 0.0, 32.0 * (double)p.n_entries * n_e);
+    pack_lg_p2p_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(p, tri_q, n_e, (const z_t*)x_diag,
+                                                                 (const z_t*)x_upper, n_ranks, dest, row_start,
+                                                                 ld, col0);
     NEGF_LAUNCHED();
   }
   return 0;

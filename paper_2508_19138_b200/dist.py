@@ -102,6 +102,46 @@ class Transposer:
         return recv.view(self.n_entries, self.n_own_e)
 
 
+class PeerEntryMajor:
+    """Entry-major arrays in symmetric memory (torch.distributed._symmetric_memory:
+    one allocation per rank, every peer's buffer mapped over NVLink), so the
+    pack kernel writes each entry row straight into its owner's array
+    (negf_pack_lg_p2p) -- the E -> nnz transpose fused with the pack, no
+    staging columns and no NCCL all-to-all. One buffer per quantity name,
+    (max entry chunk, N_E) complex128, reused across iterations."""
+
+    def __init__(self, tr: "Transposer", device) -> None:
+        import torch.distributed._symmetric_memory as symm
+
+        self.tr, self.dev, self.symm = tr, torch.device(device), symm
+        rows = max(s.stop - s.start for s in tr.r_sl)
+        self.shape = (rows, tr.n_e)
+        self.row_start = torch.tensor([s.start for s in tr.r_sl] + [tr.r_sl[-1].stop], dtype=torch.int64,
+                                      device=self.dev)
+        self._bufs: dict[str, tuple] = {}
+
+    def buffer(self, name: str):
+        """(local (n_own_entries, N_E) view, device array of the peers' base pointers, handle)."""
+        if name not in self._bufs:
+            t = self.symm.empty(self.shape, dtype=torch.complex128, device=self.dev)
+            group = self.tr.comm.group or dist.group.WORLD
+            h = self.symm.rendezvous(t, group.group_name)
+            ptrs = torch.tensor(list(h.buffer_ptrs), dtype=torch.int64, device=self.dev)
+            self._bufs[name] = (t, ptrs, h)
+        t, ptrs, h = self._bufs[name]
+        return t[:self.tr.n_own_r], ptrs, h
+
+    def barrier(self) -> None:
+        """Stream-ordered cross-rank barrier: every peer's writes into our
+        buffers are complete (and ours into theirs) before what follows."""
+        if self._bufs:
+            next(iter(self._bufs.values()))[2].barrier()
+
+    def count(self, n_cols: int) -> None:
+        """Bytes this rank wrote to peers for n_cols energy columns."""
+        self.tr.bytes_moved += 16 * n_cols * (self.tr.n_entries - self.tr.n_own_r)
+
+
 TO_ENTRY_MAJOR = "to_entry_major"
 TO_ENERGY_MAJOR = "to_energy_major"
 

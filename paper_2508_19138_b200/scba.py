@@ -21,6 +21,8 @@ transposes over NCCL all-to-all) is in ``dist.py``.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -140,6 +142,16 @@ class EntryLayout:
                                       x_upper.data_ptr(), out.data_ptr(), out.shape[-1], e0,
                                       _lib.stream_ptr(self.dev))
         _lib.check(rc, "negf_pack_lg")
+
+    def pack_p2p(self, x_diag, x_upper, peers, col0: int) -> None:
+        """pack fused with the E -> nnz transpose into the owners' symmetric
+        entry-major buffers (dist.PeerEntryMajor)."""
+        _, ptrs, _ = peers[1]
+        tr = peers[0].tr
+        rc = _lib.load().negf_pack_lg_p2p(x_diag.shape[0], self.n_b, self.bs, self.tri_q.data_ptr(),
+                                          x_diag.data_ptr(), x_upper.data_ptr(), tr.comm.size, ptrs.data_ptr(),
+                                          peers[0].row_start.data_ptr(), tr.n_e, col0, _lib.stream_ptr(self.dev))
+        _lib.check(rc, "negf_pack_lg_p2p")
 
     def unpack_lg(self, src, e0, n_e, x_diag, x_upper):
         rc = _lib.load().negf_unpack_lg(n_e, self.n_b, self.bs, self.tri_q.data_ptr(), src.data_ptr(), src.shape[-1],
@@ -420,6 +432,14 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     n_b, bs = carrier.n_b, carrier.bs
     lay = EntryLayout(n_b, bs, dev)
     tr = Transposer(comm, lay.n_entries, ne)
+    # multi-GPU GW: G^<> and W^<> reach their entry owners straight from the
+    # pack kernel through symmetric (NVLink-mapped) memory; P and Sigma go
+    # back by NCCL all-to-all. NEGF_PEER_TRANSPOSE=0 selects all-to-all for all.
+    peer = None
+    if comm.size > 1 and v is not None and os.environ.get("NEGF_PEER_TRANSPOSE", "1") != "0":
+        from .dist import PeerEntryMajor
+
+        peer = PeerEntryMajor(tr, dev)
     own = tr.own_e
     n_own = tr.n_own_e
     my_e = energies[own]
@@ -491,7 +511,12 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         # identity-defect accumulators (G, P, Sigma) x (defect, scale), scba.py:1002-1006
         defects = torch.zeros(6, dtype=torch.float64, device=dev)
         g_host = {k: [] for k in RESULT_KEYS} if keep_g else None
-        gl_c, gg_c = cols(), cols()
+        if peer is not None:  # E -> nnz fused into the pack (peer memory)
+            p_gl, p_gg = peer.buffer("gl"), peer.buffer("gg")
+            peer.barrier()  # every peer is done with last iteration's arrays
+            gl_c = gg_c = None
+        else:
+            gl_c, gg_c = cols(), cols()
         # 1. carrier solve per energy batch of this rank
         for e0 in range(0, n_own, batch):
             e1 = min(n_own, e0 + batch)
@@ -512,8 +537,13 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             if odev is not None:
                 solve_check(b, False)
             with _T("layout"):
-                lay.pack(b["xl_diag"], b["xl_upper"], gl_c, e0)
-                lay.pack(b["xg_diag"], b["xg_upper"], gg_c, e0)
+                if peer is not None:
+                    lay.pack_p2p(b["xl_diag"], b["xl_upper"], (peer, p_gl), own.start + e0)
+                    lay.pack_p2p(b["xg_diag"], b["xg_upper"], (peer, p_gg), own.start + e0)
+                    peer.count(2 * nb_)
+                else:
+                    lay.pack(b["xl_diag"], b["xl_upper"], gl_c, e0)
+                    lay.pack(b["xg_diag"], b["xg_upper"], gg_c, e0)
             if keep_g:
                 for k, src in RESULT_KEYS.items():
                     g_host[k].append(b[src].cpu().numpy())
@@ -528,7 +558,11 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             break
         # 2. G^<> to entry-major (all-to-all), polarization on own entry rows
         with _T("transpose"):
-            gl, gg = tr.to_entry_major(gl_c), tr.to_entry_major(gg_c)
+            if peer is not None:
+                peer.barrier()
+                gl, gg = p_gl[0], p_gg[0]
+            else:
+                gl, gg = tr.to_entry_major(gl_c), tr.to_entry_major(gg_c)
         del gl_c, gg_c
         with _T("convolution"):
             p_rows = polarization(gl, gg, diag_rows, de)
@@ -542,7 +576,11 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             pl, pg, pru, prl = (tr.to_energy_major(x) for x in p_rows)
         del p_rows
         # 3. screened interaction per batch of own energies
-        wl_c, wg_c = cols(), cols()
+        if peer is not None:
+            p_wl, p_wg = peer.buffer("wl"), peer.buffer("wg")
+            wl_c = wg_c = None
+        else:
+            wl_c, wg_c = cols(), cols()
         for e0 in range(0, n_own, batch):
             e1 = min(n_own, e0 + batch)
             nb_ = e1 - e0
@@ -559,11 +597,20 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             if odev is not None:
                 solve_check(wb, True)
             with _T("layout"):
-                lay.pack(wb["wl_diag"], wb["wl_upper"], wl_c, e0)
-                lay.pack(wb["wg_diag"], wb["wg_upper"], wg_c, e0)
+                if peer is not None:
+                    lay.pack_p2p(wb["wl_diag"], wb["wl_upper"], (peer, p_wl), own.start + e0)
+                    lay.pack_p2p(wb["wg_diag"], wb["wg_upper"], (peer, p_wg), own.start + e0)
+                    peer.count(2 * nb_)
+                else:
+                    lay.pack(wb["wl_diag"], wb["wl_upper"], wl_c, e0)
+                    lay.pack(wb["wg_diag"], wb["wg_upper"], wg_c, e0)
         del pl, pg, pru, prl
         with _T("transpose"):
-            wl, wg = tr.to_entry_major(wl_c), tr.to_entry_major(wg_c)
+            if peer is not None:
+                peer.barrier()
+                wl, wg = p_wl[0], p_wg[0]
+            else:
+                wl, wg = tr.to_entry_major(wl_c), tr.to_entry_major(wg_c)
         del wl_c, wg_c
         # 4. self-energy on own entry rows, back to energy-major columns
         with _T("convolution"):

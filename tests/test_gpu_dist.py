@@ -1,5 +1,8 @@
-"""Energy-sharded GW iteration over NCCL (all-to-all E<->nnz transposes) on
->= 2 GPUs vs the C1 reference golden (tools/dist_check.py under torchrun)."""
+"""Energy-sharded GW iteration on >= 2 GPUs vs the C1 reference golden and
+vs the same 3-iteration run on one GPU (tools/dist_check.py under torchrun):
+G^<> / W^<> reach their entry owners through the fused peer-memory pack
+(negf_pack_lg_p2p), P / Sigma return by NCCL all-to-all; the all-to-all-only
+path (NEGF_PEER_TRANSPOSE=0) is checked the same way."""
 
 import subprocess
 import sys
@@ -20,4 +23,17 @@ def test_energy_sharded_scba_matches_reference(cuda):
                           str(min(n, 4)), str(ROOT / "tools" / "dist_check.py")],
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
-    assert "DIST_CHECK" in out.stdout
+    assert "DIST_CHECK" in out.stdout and "DIST_CHECK_3IT" in out.stdout
+
+
+def test_energy_sharded_scba_all_to_all_only(cuda):
+    import os
+
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs (one rank per GPU; ranks never share a GPU)")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node", "2",
+                          str(ROOT / "tools" / "dist_check.py")], capture_output=True, text=True, timeout=600,
+                         env={**os.environ, "NEGF_PEER_TRANSPOSE": "0"})
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "peer_transpose=0" in out.stdout

@@ -48,4 +48,20 @@ worst = max(worst, rel(res["residuals"], g["residuals"]))
 if comm.rank == 0:
     print(f"DIST_CHECK world={comm.size} worst_rel={worst:.3e} ({which}) transpose_bytes_rank0={res['transpose_bytes']}")
     assert worst < 1e-9
+# three GW iterations (buffers reused across iterations) vs the same run on one GPU
+opts3 = ScbaOptions(max_iter=3, tol=1e-12, batch=40, memoizer=MemoizerOptions(enabled=False))
+args = (orc.chain_device(16, 32), orc.coulomb_matrix(16, 32), np.linspace(-2.0, 2.0, 128), 1e-3,
+        Contacts(0.1, -0.1, 0.05), opts3)
+res3 = scba_run(*args, device=dev, comm=comm)
+sig = {f: res3["sigma_" + f] for f in ("lesser", "greater", "ret_upper", "ret_lower")}
+parts = [None] * comm.size
+dist.all_gather_object(parts, (res3["energy_slice"].start, sig))
+if comm.rank == 0:
+    parts.sort(key=lambda x: x[0])
+    one = scba_run(*args, device=dev)
+    w3 = max(rel(np.concatenate([p[1][f] for p in parts], axis=1), one["sigma_" + f]) for f in sig)
+    w3 = max(w3, rel(res3["residuals"], one["residuals"]))
+    print(f"DIST_CHECK_3IT world={comm.size} worst_rel_vs_1gpu={w3:.3e} peer_transpose="
+          f"{os.environ.get('NEGF_PEER_TRANSPOSE', '1')}")
+    assert w3 < 1e-12
 dist.destroy_process_group()
