@@ -301,6 +301,17 @@ int negf_pack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* x_diag,
 int negf_pack_lg_p2p(int n_e, int n_b, int bs, const int* tri_q, const void* x_diag, const void* x_upper,
                      int n_ranks, const unsigned long long* dest, const long long* row_start, long long ld,
                      int col0, void* stream);
+/* nnz -> E redistribution fused with the unpack (scba.py:1053-1056 then
+ * _scatter_lg / _scatter_retarded): entry row t is read from rank s
+ * (row_start[s] <= t < row_start[s+1]) at row t - row_start[s], columns
+ * col0 .. col0 + n_e of its (rows, ld) entry-major array src_upper[s]
+ * (and src_lower[s] when retarded != 0: the retarded unpack), peer memory
+ * over NVLink. Writes the n_e energies' blocks like negf_unpack_lg /
+ * negf_unpack_retarded. n_ranks <= 16. */
+int negf_unpack_p2p(int n_e, int n_b, int bs, const int* tri_q, int retarded, int n_ranks,
+                    const unsigned long long* src_upper, const unsigned long long* src_lower,
+                    const long long* row_start, long long ld, int col0, void* x_diag, void* x_upper,
+                    void* x_lower, void* stream);
 int negf_unpack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* in, long long ld,
                    int e0, void* x_diag, void* x_upper, void* stream);
 /* _scatter_retarded (scba.py:311-325): upper values at (r,c), lower values at
@@ -409,6 +420,14 @@ int negf_entry_identity_defect(long long n, const void* lesser, const void* grea
 int negf_mix(long long n, double alpha, void* s_lesser, void* s_greater, void* s_ret_up,
              void* s_ret_lo, const void* r_lesser, const void* r_greater, const void* r_ret_up,
              const void* r_ret_lo, void* stream);
+/* negf_mix with the new Sigma read from its entry owners (fused nnz -> E,
+ * scba.py:1138-1141 then :478-481): state (n_rows, n_own) local arrays;
+ * src = device array of 4 * n_ranks pointers [lesser | greater | ret_up |
+ * ret_lo] x rank to (rows, ld) entry-major arrays; row q of the state mixes
+ * with row q - row_start[s] of rank s, columns col0 .. col0 + n_own. */
+int negf_mix_p2p(long long n_rows, int n_own, double alpha, void* s_lesser, void* s_greater, void* s_ret_up,
+                 void* s_ret_lo, int n_ranks, const unsigned long long* src, const long long* row_start,
+                 long long ld, int col0, void* stream);
 int negf_diag_traces(const void* x, long long ld, int n_e, const long long* diag_rows, int n_b,
                      int bs, void* tr, void* stream);
 

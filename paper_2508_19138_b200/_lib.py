@@ -86,6 +86,8 @@ _SIGNATURES: dict[str, tuple] = {
     "negf_g_identity_defect": (_i, [_i, _i, _i] + [_vp] * 9),
     "negf_entry_identity_defect": (_i, [_ll] + [_vp] * 6),
     "negf_pack_lg_p2p": (_i, [_i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _ll, _i, _vp]),
+    "negf_unpack_p2p": (_i, [_i, _i, _i, _vp, _i, _i, _vp, _vp, _vp, _ll, _i, _vp, _vp, _vp, _vp]),
+    "negf_mix_p2p": (_i, [_ll, _i, _d, _vp, _vp, _vp, _vp, _i, _vp, _vp, _ll, _i, _vp]),
     "negf_mix": (_i, [_ll, _d] + [_vp] * 9),
     "negf_diag_traces": (_i, [_vp, _ll, _i, _vp, _i, _i, _vp, _vp]),
     "negf_prof_enable": (None, [_i]),

@@ -118,21 +118,53 @@ __global__ void pack_lg_p2p_kernel(Pat p, const int* __restrict__ tri_q, int n_e
 
 // series -> blocks. mode 0: lg (mirror rule on diagonal blocks);
 // mode 1: retarded (upper values at (r,c), lower values at (c,r)).
+// Peer sources of the fused nnz -> E unpack: entry row tt lives on rank s
+// (row_start[s] <= tt < row_start[s+1]) at row tt - row_start[s] of that
+// rank's entry-major array(s).
+struct PeerSrc {
+  int n_ranks;
+  const unsigned long long* up;  // device arrays of n_ranks pointers
+  const unsigned long long* lo;
+  const long long* row_start;
+};
+
+template <bool P2P>
 __global__ void unpack_kernel(Pat p, const int* __restrict__ tri_q, int n_e,
                               const z_t* __restrict__ in_up, const z_t* __restrict__ in_lo,
-                              long long ld, int e0, int mode, z_t* xd, z_t* xu, z_t* xl) {
+                              long long ld, int e0, int mode, z_t* xd, z_t* xu, z_t* xl, PeerSrc ps) {
   __shared__ z_t tu[T][T + 1];
   __shared__ z_t tl[T][T + 1];
+  __shared__ long long rs[kMaxRanks + 1];
+  __shared__ unsigned long long su[kMaxRanks], sl[kMaxRanks];
   const long long t0 = (long long)blockIdx.x * T;
   const int eb = blockIdx.y * T;
   const long long n2 = (long long)p.bs * p.bs;
   const int tx = threadIdx.x, ty = threadIdx.y;
+  if constexpr (P2P) {
+    const int tid = ty * T + tx;
+    if (tid <= ps.n_ranks) rs[tid] = ps.row_start[tid];
+    if (tid < ps.n_ranks) {
+      su[tid] = ps.up[tid];
+      sl[tid] = ps.lo ? ps.lo[tid] : 0ull;
+    }
+    __syncthreads();
+  }
   for (int k = ty; k < T; k += 8) {
     const long long tt = t0 + k;
     const int e = eb + tx;
     if (tt < p.n_entries && e < n_e) {
-      tu[k][tx] = in_up[tt * ld + e0 + e];
-      if (mode == 1) tl[k][tx] = in_lo[tt * ld + e0 + e];
+      const z_t* up = in_up;
+      const z_t* lo = in_lo;
+      long long row = tt;
+      if constexpr (P2P) {
+        int s = 0;
+        while (s + 1 < ps.n_ranks && tt >= rs[s + 1]) ++s;
+        up = reinterpret_cast<const z_t*>(su[s]);
+        lo = reinterpret_cast<const z_t*>(sl[s]);
+        row = tt - rs[s];
+      }
+      tu[k][tx] = up[row * ld + e0 + e];
+      if (mode == 1) tl[k][tx] = lo[row * ld + e0 + e];
     }
   }
   __syncthreads();
@@ -232,8 +264,9 @@ int negf_unpack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* in, l
   {
     const double blocks = (2.0 * n_b - 1.0) * bs * bs;  // diag + upper blocks written
     ProfSpan ps_unpack_kernel(PROF_LAYOUT, (cudaStream_t)(stream), 0.0, 16.0 * ((double)p.n_entries + blocks) * n_e);
-    unpack_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(p, tri_q, n_e, (const z_t*)in, nullptr, ld,
-                                                            e0, 0, (z_t*)x_diag, (z_t*)x_upper, nullptr);
+    unpack_kernel<false><<<grid, block, 0, (cudaStream_t)stream>>>(p, tri_q, n_e, (const z_t*)in, nullptr, ld,
+                                                                   e0, 0, (z_t*)x_diag, (z_t*)x_upper, nullptr,
+                                                                   PeerSrc{});
     NEGF_LAUNCHED();
   }
   return 0;
@@ -253,9 +286,32 @@ int negf_unpack_retarded(int n_e, int n_b, int bs, const int* tri_q, const void*
     const double blocks = (3.0 * n_b - 2.0) * bs * bs;  // diag + upper + lower blocks written
     ProfSpan ps_unpack_kernel(PROF_LAYOUT, (cudaStream_t)(stream), 0.0,
                               16.0 * (2.0 * (double)p.n_entries + blocks) * n_e);
-    unpack_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(
+    unpack_kernel<false><<<grid, block, 0, (cudaStream_t)stream>>>(
         p, tri_q, n_e, (const z_t*)in_upper, (const z_t*)in_lower, ld, e0, 1, (z_t*)x_diag,
-        (z_t*)x_upper, (z_t*)x_lower);
+        (z_t*)x_upper, (z_t*)x_lower, PeerSrc{});
+    NEGF_LAUNCHED();
+  }
+  return 0;
+}
+
+int negf_unpack_p2p(int n_e, int n_b, int bs, const int* tri_q, int retarded, int n_ranks,
+                    const unsigned long long* src_upper, const unsigned long long* src_lower,
+                    const long long* row_start, long long ld, int col0, void* x_diag, void* x_upper,
+                    void* x_lower, void* stream) {
+  if (n_e < 0 || n_b < 1 || bs < 1 || !tri_q || n_ranks < 1 || n_ranks > kMaxRanks || !src_upper ||
+      !row_start || !x_diag || col0 < 0 || ld < col0 + n_e || (retarded && !src_lower))
+    return -1;
+  if (n_b > 1 && (!x_upper || (retarded && !x_lower))) return -1;
+  if (n_e == 0) return 0;
+  Pat p = make_pat(n_b, bs);
+  dim3 grid((unsigned)((p.n_entries + T - 1) / T), (n_e + T - 1) / T), block(T, 8);
+  {
+    const double blocks = (retarded ? 3.0 * n_b - 2.0 : 2.0 * n_b - 1.0) * bs * bs;
+    ProfSpan ps_unpack(PROF_LAYOUT, (cudaStream_t)(stream), 0.0,
+                       16.0 * ((retarded ? 2.0 : 1.0) * p.n_entries + blocks) * n_e);
+    unpack_kernel<true><<<grid, block, 0, (cudaStream_t)stream>>>(
+        p, tri_q, n_e, nullptr, nullptr, ld, col0, retarded ? 1 : 0, (z_t*)x_diag, (z_t*)x_upper,
+        (z_t*)x_lower, PeerSrc{n_ranks, src_upper, retarded ? src_lower : nullptr, row_start});
     NEGF_LAUNCHED();
   }
   return 0;

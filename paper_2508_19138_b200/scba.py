@@ -153,6 +153,18 @@ class EntryLayout:
                                           peers[0].row_start.data_ptr(), tr.n_e, col0, _lib.stream_ptr(self.dev))
         _lib.check(rc, "negf_pack_lg_p2p")
 
+    def unpack_p2p(self, peer, names, col0: int, n_e: int, x_diag, x_upper, x_lower=None) -> None:
+        """unpack fused with the nnz -> E transpose: reads the entry owners'
+        symmetric arrays (names: ("lg",) or (upper, lower) for retarded)."""
+        ptrs = [peer.buffer(k)[1] for k in names]
+        ret = len(names) == 2
+        rc = _lib.load().negf_unpack_p2p(n_e, self.n_b, self.bs, self.tri_q.data_ptr(), int(ret), peer.tr.comm.size,
+                                         ptrs[0].data_ptr(), ptrs[1].data_ptr() if ret else None,
+                                         peer.row_start.data_ptr(), peer.tr.n_e, col0, x_diag.data_ptr(),
+                                         x_upper.data_ptr(), x_lower.data_ptr() if ret else None,
+                                         _lib.stream_ptr(self.dev))
+        _lib.check(rc, "negf_unpack_p2p")
+
     def unpack_lg(self, src, e0, n_e, x_diag, x_upper):
         rc = _lib.load().negf_unpack_lg(n_e, self.n_b, self.bs, self.tri_q.data_ptr(), src.data_ptr(), src.shape[-1],
                                         e0, x_diag.data_ptr(), x_upper.data_ptr(), _lib.stream_ptr(self.dev))
@@ -432,9 +444,11 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     n_b, bs = carrier.n_b, carrier.bs
     lay = EntryLayout(n_b, bs, dev)
     tr = Transposer(comm, lay.n_entries, ne)
-    # multi-GPU GW: G^<> and W^<> reach their entry owners straight from the
-    # pack kernel through symmetric (NVLink-mapped) memory; P and Sigma go
-    # back by NCCL all-to-all. NEGF_PEER_TRANSPOSE=0 selects all-to-all for all.
+    # multi-GPU GW: every E <-> nnz switch runs through symmetric (NVLink-
+    # mapped) memory inside the layout kernels -- G^<> and W^<> are written
+    # into their entry owners' arrays by the pack, P is read from its owners
+    # by the W unpack and Sigma by the mixing; stream-ordered barriers order
+    # writers and readers. NEGF_PEER_TRANSPOSE=0 selects NCCL all-to-all.
     peer = None
     if comm.size > 1 and v is not None and os.environ.get("NEGF_PEER_TRANSPOSE", "1") != "0":
         from .dist import PeerEntryMajor
@@ -565,7 +579,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
                 gl, gg = tr.to_entry_major(gl_c), tr.to_entry_major(gg_c)
         del gl_c, gg_c
         with _T("convolution"):
-            p_rows = polarization(gl, gg, diag_rows, de)
+            p_out = tuple(peer.buffer(k)[0] for k in ("pl", "pg", "pru", "prl")) if peer is not None else None
+            p_rows = polarization(gl, gg, diag_rows, de, out=p_out)
         entry_identity_defect(*p_rows, defects[2:4])
         if odev is not None:
             from .checks import polarization_deviation
@@ -573,7 +588,12 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             dv, sc = polarization_deviation(gl, gg, p_rows[0], p_rows[1], diag_rows, de)
             odev["fft_vs_direct"] = max(odev["fft_vs_direct"], dv / (sc + 1e-300))
         with _T("transpose"):
-            pl, pg, pru, prl = (tr.to_energy_major(x) for x in p_rows)
+            if peer is not None:  # the W unpack reads the owners' P rows directly
+                peer.barrier()
+                peer.count(4 * n_own)
+                pl = pg = pru = prl = None
+            else:
+                pl, pg, pru, prl = (tr.to_energy_major(x) for x in p_rows)
         del p_rows
         # 3. screened interaction per batch of own energies
         if peer is not None:
@@ -590,9 +610,15 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             pool += [x for x in cb.values() if x.dim() == 4]
             wb = screened.buffers(nb_, pool)
             with _T("layout"):
-                lay.unpack_retarded(pru, prl, e0, nb_, wb["pr_diag"], wb["pr_upper"], wb["pr_lower"])
-                lay.unpack_lg(pl, e0, nb_, wb["pl_diag"], wb["pl_upper"])
-                lay.unpack_lg(pg, e0, nb_, wb["pg_diag"], wb["pg_upper"])
+                if peer is not None:
+                    c0 = own.start + e0
+                    lay.unpack_p2p(peer, ("pru", "prl"), c0, nb_, wb["pr_diag"], wb["pr_upper"], wb["pr_lower"])
+                    lay.unpack_p2p(peer, ("pl",), c0, nb_, wb["pl_diag"], wb["pl_upper"])
+                    lay.unpack_p2p(peer, ("pg",), c0, nb_, wb["pg_diag"], wb["pg_upper"])
+                else:
+                    lay.unpack_retarded(pru, prl, e0, nb_, wb["pr_diag"], wb["pr_upper"], wb["pr_lower"])
+                    lay.unpack_lg(pl, e0, nb_, wb["pl_diag"], wb["pl_upper"])
+                    lay.unpack_lg(pg, e0, nb_, wb["pg_diag"], wb["pg_upper"])
             wb = screened.solve(nb_, timer=_T, memo=memo(e0))
             if odev is not None:
                 solve_check(wb, True)
@@ -614,7 +640,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         del wl_c, wg_c
         # 4. self-energy on own entry rows, back to energy-major columns
         with _T("convolution"):
-            s_rows = self_energy(gl, gg, wl, wg, None, diag_rows, de)
+            s_out = tuple(peer.buffer(k)[0] for k in ("sl", "sg", "sru", "srl")) if peer is not None else None
+            s_rows = self_energy(gl, gg, wl, wg, None, diag_rows, de, out=s_out)
         entry_identity_defect(*s_rows, defects[4:6])
         if odev is not None:
             from .checks import self_energy_deviation
@@ -622,14 +649,26 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             dv, sc = self_energy_deviation(gl, gg, wl, wg, s_rows[0], s_rows[1], diag_rows, de)
             odev["fft_vs_direct"] = max(odev["fft_vs_direct"], dv / (sc + 1e-300))
         with _T("transpose"):
-            raw = tuple(tr.to_energy_major(x) for x in s_rows)
+            if peer is not None:  # the mixing reads the owners' Sigma rows directly
+                peer.barrier()
+                peer.count(4 * n_own)
+                raw = None
+            else:
+                raw = tuple(tr.to_energy_major(x) for x in s_rows)
         del s_rows
         del wl, wg, gl, gg
         # 5. mixing + residual (scba.py:1155-1177), max over ranks
         tr_old = [lay.traces(sig.lesser), lay.traces(sig.greater)]
-        rc = _lib.load().negf_mix(sig.lesser.numel(), options.mixing, *(x.data_ptr() for x in sig.as_tuple()),
-                                  *(x.data_ptr() for x in raw), _lib.stream_ptr(dev))
-        _lib.check(rc, "negf_mix")
+        if peer is not None:
+            src = torch.cat([peer.buffer(k)[1] for k in ("sl", "sg", "sru", "srl")])
+            rc = _lib.load().negf_mix_p2p(lay.n_entries, n_own, options.mixing, *(x.data_ptr() for x in sig.as_tuple()),
+                                          comm.size, src.data_ptr(), peer.row_start.data_ptr(), ne, own.start,
+                                          _lib.stream_ptr(dev))
+            _lib.check(rc, "negf_mix_p2p")
+        else:
+            rc = _lib.load().negf_mix(sig.lesser.numel(), options.mixing, *(x.data_ptr() for x in sig.as_tuple()),
+                                      *(x.data_ptr() for x in raw), _lib.stream_ptr(dev))
+            _lib.check(rc, "negf_mix")
         tr_new = [lay.traces(sig.lesser), lay.traces(sig.greater)]
         to = [t.cpu().numpy() for t in tr_old]
         tn = [t.cpu().numpy() for t in tr_new]
