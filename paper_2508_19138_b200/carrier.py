@@ -77,6 +77,7 @@ class CarrierSolver:
         self.max_sweeps = int(max_sweeps)
         self._buf: dict | None = None
         self._n_e = 0
+        self.dd = None  # (PartitionPlan, Comm): spatial domain decomposition of the RGF (scba_run plan=)
         self.streams = streams
         self._side_streams = [torch.cuda.Stream(self.dev) for _ in range(streams)] if streams > 1 else []
 
@@ -189,7 +190,16 @@ class CarrierSolver:
             raise_on_obc_status(b["obc_status"].cpu().numpy(), b["obc_iters"].cpu().numpy(),
                                 b["obc_resid"].cpu().numpy(), self.max_sweeps, self.surface_tol, "G contact")
         b["rgf_status"].zero_()
-        if self.greater == "identity":
+        if self.dd is not None:  # spatial mode of scba_run: all ranks solve this batch jointly
+            from .dd import dd_solve_into
+
+            dd_solve_into(b, *self.dd, kinds=("bl",) if self.greater == "identity" else ("bl", "bg"))
+            if self.greater == "identity":
+                rc = lib.negf_greater_from_identity(ne, self.n_b, self.bs, p(b["xl_diag"]), p(b["xl_upper"]),
+                                                    p(b["xr_diag"]), p(b["xr_upper"]), p(b["xr_lower"]),
+                                                    p(b["xg_diag"]), p(b["xg_upper"]), st)
+                _lib.check(rc, "negf_greater_from_identity")
+        elif self.greater == "identity":
             rgf_selected_solve_split(lib, b, ne, self.n_b, self.bs, self.dev, 1, [], kinds=("bl",))
             rc = lib.negf_greater_from_identity(ne, self.n_b, self.bs, p(b["xl_diag"]), p(b["xl_upper"]),
                                                 p(b["xr_diag"]), p(b["xr_upper"]), p(b["xr_lower"]),

@@ -468,3 +468,52 @@ def dist_selected_solve(m_tilde, b_lesser=None, b_greater=None, plan: PartitionP
         sol.x_lg_diag[k] = list(h[_TAG[k] + "_diag"])
         sol.x_lg_upper[k] = list(h[_TAG[k] + "_upper"])
     return sol, {"plan": plan, "wall": wall}
+
+
+def dd_solve_into(b: dict, plan: PartitionPlan, comm, prefix: tuple = ("m", "bl", "bg", "xr", "xl", "xg"),
+                  kinds: tuple = ("bl", "bg"), symmetrize: bool = True) -> None:
+    """Spatial selected solve of the full-chain batch in ``b`` (the buffers of
+    CarrierSolver / ScreenedSolver), all ranks of ``comm`` jointly, one
+    partition per rank; the outputs are gathered into the full stacks of
+    every rank, like the reference's dist_selected_solve inside scba_run
+    (scba.py:971-979, 1073-1083; dist.py:712-717). The partition blocks and
+    cross blocks travel in one padded NCCL all-gather."""
+    import torch.distributed as dist
+
+    m, bl, bg, xr, xl, xg = prefix
+    tags = {KIND_LESSER: (bl, xl), KIND_GREATER: (bg, xg)}
+    ks = [k for k, (s, _o) in tags.items() if s in kinds]
+    src = {k: (b[tags[k][0] + "_diag"], b[tags[k][0] + "_upper"]) for k in ks}
+    part = partition_inputs(b[m + "_diag"], b[m + "_upper"], b[m + "_lower"], src, plan, comm.rank)
+    loc, cr = dd_selected_solve_batched(part, plan, comm.group, symmetrize=symmetrize, kinds=ks)
+    lkeys = ["xr_diag", "xr_upper", "xr_lower"] + [_TAG[k] + s for k in ks for s in ("_diag", "_upper")]
+    ckeys = ["xr_upper", "xr_lower"] + [_TAG[k] + "_upper" for k in ks]
+    n_e, bs = b[m + "_diag"].shape[0], b[m + "_diag"].shape[-1]
+
+    def shapes(r: int) -> list:
+        a, z = plan.ranges[r]
+        out = [(n_e, z - a + 1 if key.endswith("_diag") else z - a, bs, bs) for key in lkeys]
+        return out + ([(n_e, bs, bs)] * len(ckeys) if r < plan.p_s - 1 else [])
+
+    sizes = [sum(int(np.prod(s)) for s in shapes(r)) for r in range(plan.p_s)]
+    mine = [loc[k].reshape(-1) for k in lkeys] + ([cr[k].reshape(-1) for k in ckeys] if cr is not None else [])
+    flat = torch.zeros(max(sizes), dtype=Z, device=b[m + "_diag"].device)
+    torch.cat(mine, out=flat[:sizes[comm.rank]])
+    bufs = [torch.empty_like(flat) for _ in range(plan.p_s)]
+    dist.all_gather([torch.view_as_real(x) for x in bufs], torch.view_as_real(flat), group=comm.group)
+    out_name = {"xr": xr, **{_TAG[k]: tags[k][1] for k in ks}}
+    for r, (a, z) in enumerate(plan.ranges):
+        off = 0
+        names = lkeys + (ckeys if r < plan.p_s - 1 else [])
+        for i, (key, shp) in enumerate(zip(names, shapes(r))):
+            cnt = int(np.prod(shp))
+            piece = bufs[r][off:off + cnt].view(shp)
+            off += cnt
+            tag, part_ = key.split("_")
+            dst = b[out_name[tag] + "_" + part_]
+            if i >= len(lkeys):  # cross block at the right boundary z
+                dst[:, z] = piece
+            elif part_ == "diag":
+                dst[:, a:z + 1] = piece
+            else:
+                dst[:, a:z] = piece

@@ -91,6 +91,21 @@ class Transposer:
             off += self.n_own_r * ne_s
         return torch.cat(parts, dim=1)
 
+    def rows_to_full(self, rows: torch.Tensor) -> torch.Tensor:
+        """(n_own_entries, N_E) -> (n_entries, N_E) on every rank: the
+        replicated result of the reference's to-energy-major transpose
+        (scba.py:342-368), needed only by the spatial mode of scba_run where
+        every rank solves every energy. One padded all-gather."""
+        if self.comm.size == 1:
+            return rows
+        m = max(s.stop - s.start for s in self.r_sl)
+        pad = torch.zeros((m, self.n_e), dtype=rows.dtype, device=rows.device)
+        pad[:self.n_own_r] = rows
+        bufs = [torch.empty_like(pad) for _ in range(self.comm.size)]
+        dist.all_gather([torch.view_as_real(x) for x in bufs], torch.view_as_real(pad), group=self.comm.group)
+        self.bytes_moved += 16 * self.n_own_r * self.n_e * (self.comm.size - 1)
+        return torch.cat([x[:s.stop - s.start] for x, s in zip(bufs, self.r_sl)])
+
     def to_energy_major(self, rows: torch.Tensor) -> torch.Tensor:
         """(n_own_entries, N_E) -> (n_entries, n_own_e)."""
         if self.comm.size == 1:

@@ -196,6 +196,7 @@ class ScreenedSolver:
         # lets the 3M GEMM skip its ai*bi product on every assembly term
         self.v_real = all(bool(torch.all(x.imag == 0)) for x in self.v)
         self.opt = options
+        self.dd = None  # (PartitionPlan, Comm) in the spatial mode of scba_run
         self._buf, self._n_e = None, 0
 
     def buffers(self, n_e: int, pool=()) -> dict:
@@ -308,6 +309,11 @@ class ScreenedSolver:
     def _rgf(self, b: dict, n_e: int) -> None:
         """Selected solve of the W system, symmetrized (scba.py:1084-1087)."""
         lib, p = self.lib, _lib.ptr
+        if self.dd is not None:  # spatial mode: all ranks solve the batch jointly (scba.py:1073-1083)
+            from .dd import dd_solve_into
+
+            dd_solve_into(b, *self.dd, prefix=("m", "bl", "bg", "wr", "wl", "wg"))
+            return
         nbytes = lib.negf_rgf_workspace_bytes(n_e, self.n_b, self.bs)
         ws = _lib.workspace(nbytes, self.dev)
         b["rgf_status"].zero_()
@@ -409,20 +415,21 @@ def entry_identity_defect(lesser, greater, ret_upper, ret_lower, out: torch.Tens
 
 
 def scba_run_reference_api(h_mat, v_mat, grid, contacts, options: ScbaOptions | None = None,
-                           comm: Comm | None = None, initial_sigma: ScbaState | None = None,
+                           comm: Comm | None = None, plan=None, initial_sigma: ScbaState | None = None,
                            device="cuda") -> dict:
     """scba.py:865 signature: BlockMatrix H / V (or None), an EnergyGrid-like
-    grid (energies, eta) and a ContactConfig-like object (mu_left, mu_right,
-    kT). The spatial-partition ``plan`` argument of the reference is not part
-    of this path (energy sharding via ``comm`` only)."""
+    grid (energies, eta), a ContactConfig-like object (mu_left, mu_right,
+    kT), ``comm`` for energy sharding and ``plan`` (dd.PartitionPlan) for
+    the spatial mode."""
     c = Contacts(contacts.mu_left, contacts.mu_right, contacts.kT)
     return scba_run(_stacks(h_mat), None if v_mat is None else _stacks(v_mat), grid.energies, grid.eta, c,
-                    options, device=device, comm=comm, initial_sigma=initial_sigma)
+                    options, device=device, comm=comm, initial_sigma=initial_sigma, plan=plan)
 
 
 def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOptions | None = None,
              device="cuda", keep_g: bool = True, initial_sigma: ScbaState | None = None,
-             comm: Comm | None = None, profile: bool = False, sigma_to_host: bool = True) -> "ScbaResult":
+             comm: Comm | None = None, profile: bool = False, sigma_to_host: bool = True,
+             plan=None) -> "ScbaResult":
     """SCBA on one GPU or energy-sharded over ``comm`` (one rank per GPU).
 
     ``h``/``v`` are (diag, upper, lower) block stacks; ``v=None`` runs the
@@ -432,7 +439,13 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     Returns host arrays named like ScbaResult fields for this rank's
     energies (G of the last iteration's carrier solve when keep_g), the
     mixed Sigma columns of this rank's energies ('sigma_lesser', ...),
-    'residuals' (global) and 'energy_slice'."""
+    'residuals' (global) and 'energy_slice'.
+
+    With ``plan.p_s > 1`` (a dd.PartitionPlan, p_s == comm.size) every energy
+    is solved jointly by all ranks over the spatial partitions (dd.py, the
+    reference's spatial mode, scba.py:878-880, 971-979, 1073-1083): Sigma is
+    replicated, P and Sigma are all-gathered after the convolutions, and each
+    rank still owns its energy chunk of the entry-major layout."""
     options = options or ScbaOptions()
     comm = comm or Comm()
     dev = torch.device(device)
@@ -444,26 +457,39 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     n_b, bs = carrier.n_b, carrier.bs
     lay = EntryLayout(n_b, bs, dev)
     tr = Transposer(comm, lay.n_entries, ne)
+    spatial = plan is not None and plan.p_s > 1
+    if spatial:
+        from .dd import PartitionError, make_partition_plan
+
+        if options.oracle_mode:
+            raise ValueError("oracle_mode supports only sequential solves")
+        if plan.n_blocks != n_b:
+            raise PartitionError(f"plan covers {plan.n_blocks} blocks, matrix has {n_b}")
+        if plan.p_s != comm.size:
+            raise PartitionError(f"plan has {plan.p_s} partitions but communicator has {comm.size} ranks")
+        carrier.dd = (plan, comm)
     # multi-GPU GW: every E <-> nnz switch runs through symmetric (NVLink-
     # mapped) memory inside the layout kernels -- G^<> and W^<> are written
     # into their entry owners' arrays by the pack, P is read from its owners
     # by the W unpack and Sigma by the mixing; stream-ordered barriers order
     # writers and readers. NEGF_PEER_TRANSPOSE=0 selects NCCL all-to-all.
     peer = None
-    if comm.size > 1 and v is not None and os.environ.get("NEGF_PEER_TRANSPOSE", "1") != "0":
+    if comm.size > 1 and v is not None and not spatial and os.environ.get("NEGF_PEER_TRANSPOSE", "1") != "0":
         from .dist import PeerEntryMajor
 
         peer = PeerEntryMajor(tr, dev)
     own = tr.own_e
     n_own = tr.n_own_e
-    my_e = energies[own]
+    # energies this rank solves: its chunk, or all of them in the spatial mode
+    s0, n_sol = (0, ne) if spatial else (own.start, n_own)
+    my_e = energies[s0:s0 + n_sol]
     diag_rows = lay.diag[tr.own_r].contiguous()
-    batch = options.batch or max(n_own, 1)
-    sig = ScbaState.zeros(lay.n_entries, n_own, dev)
+    batch = options.batch or max(n_sol, 1)
+    sig = ScbaState.zeros(lay.n_entries, n_sol, dev)
     if initial_sigma is not None and not options.reset_sigma:
-        if tuple(initial_sigma.lesser.shape) != (lay.n_entries, n_own):
+        if tuple(initial_sigma.lesser.shape) != (lay.n_entries, n_sol):
             raise ValueError(f"warm-start state has shape {tuple(initial_sigma.lesser.shape)}, "
-                             f"expected {(lay.n_entries, n_own)}")
+                             f"expected {(lay.n_entries, n_sol)}")
         sig = ScbaState(*(torch.as_tensor(x, dtype=Z, device=dev).clone() for x in initial_sigma.as_tuple()))
     if v is None:
         max_iter = 1
@@ -472,6 +498,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         screened = ScreenedSolver(v, options, dev)
         if screened.n_b != n_b or screened.bs != bs:
             raise ValueError("W blocking must match the carrier blocking (n_w == n_b, bs_w == bs)")
+        if spatial:  # the W chain gets its own even split (scba.py:930)
+            screened.dd = (make_partition_plan(n_b, plan.p_s), comm)
     cols = lambda: torch.empty((lay.n_entries, n_own), dtype=Z, device=dev)
     result: dict = {}
     residuals = []
@@ -517,7 +545,19 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             {"<": (bb[x + "l_diag"], bb[x + "l_upper"]), ">": (bb[x + "g_diag"], bb[x + "g_upper"])})
         odev["solve_vs_dense"] = max(odev["solve_vs_dense"], dv / (sc + 1e-300))
 
-    memo = (lambda e0: (cache, max(n_own, 1), e0, tol_memo)) if cache is not None else (lambda e0: None)
+    memo = (lambda e0: (cache, max(n_sol, 1), e0, tol_memo)) if cache is not None else (lambda e0: None)
+
+    def own_part(e0: int, nb_: int):
+        """(offset in the batch, count, column in the own chunk) of the batch's own energies."""
+        if not spatial:
+            return 0, nb_, e0
+        lo, hi = max(e0, own.start), min(e0 + nb_, own.stop)
+        return lo - e0, max(hi - lo, 0), lo - own.start
+
+    def pack_own(xd, xu, out, e0: int, nb_: int) -> None:
+        a, n, c = own_part(e0, nb_)
+        if n:
+            lay.pack(xd[a:a + n], xu[a:a + n], out, c)
     for it in range(max_iter):
         n_iter = it + 1
         torch.cuda.synchronize(dev)
@@ -532,8 +572,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         else:
             gl_c, gg_c = cols(), cols()
         # 1. carrier solve per energy batch of this rank
-        for e0 in range(0, n_own, batch):
-            e1 = min(n_own, e0 + batch)
+        for e0 in range(0, n_sol, batch):
+            e1 = min(n_sol, e0 + batch)
             nb_ = e1 - e0
             if blocks is None or blocks["sr_diag"].shape[0] != nb_:
                 d, o = (nb_, n_b, bs, bs), (nb_, n_b - 1, bs, bs)
@@ -556,11 +596,12 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
                     lay.pack_p2p(b["xg_diag"], b["xg_upper"], (peer, p_gg), own.start + e0)
                     peer.count(2 * nb_)
                 else:
-                    lay.pack(b["xl_diag"], b["xl_upper"], gl_c, e0)
-                    lay.pack(b["xg_diag"], b["xg_upper"], gg_c, e0)
+                    pack_own(b["xl_diag"], b["xl_upper"], gl_c, e0, nb_)
+                    pack_own(b["xg_diag"], b["xg_upper"], gg_c, e0, nb_)
             if keep_g:
+                a_, n_, _c = own_part(e0, nb_)
                 for k, src in RESULT_KEYS.items():
-                    g_host[k].append(b[src].cpu().numpy())
+                    g_host[k].append(b[src][a_:a_ + n_].cpu().numpy())
         if keep_g and n_own:
             result = {k: np.concatenate(vv) for k, vv in g_host.items()}
         if v is None:
@@ -593,7 +634,7 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
                 peer.count(4 * n_own)
                 pl = pg = pru = prl = None
             else:
-                pl, pg, pru, prl = (tr.to_energy_major(x) for x in p_rows)
+                pl, pg, pru, prl = ((tr.rows_to_full(x) if spatial else tr.to_energy_major(x)) for x in p_rows)
         del p_rows
         # 3. screened interaction per batch of own energies
         if peer is not None:
@@ -601,8 +642,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             wl_c = wg_c = None
         else:
             wl_c, wg_c = cols(), cols()
-        for e0 in range(0, n_own, batch):
-            e1 = min(n_own, e0 + batch)
+        for e0 in range(0, n_sol, batch):
+            e1 = min(n_sol, e0 + batch)
             nb_ = e1 - e0
             # the carrier's stacks of this batch size are dead during the W stage
             pool = list(blocks.values()) if blocks is not None and blocks["sr_diag"].shape[0] == nb_ else []
@@ -628,8 +669,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
                     lay.pack_p2p(wb["wg_diag"], wb["wg_upper"], (peer, p_wg), own.start + e0)
                     peer.count(2 * nb_)
                 else:
-                    lay.pack(wb["wl_diag"], wb["wl_upper"], wl_c, e0)
-                    lay.pack(wb["wg_diag"], wb["wg_upper"], wg_c, e0)
+                    pack_own(wb["wl_diag"], wb["wl_upper"], wl_c, e0, nb_)
+                    pack_own(wb["wg_diag"], wb["wg_upper"], wg_c, e0, nb_)
         del pl, pg, pru, prl
         with _T("transpose"):
             if peer is not None:
@@ -654,7 +695,7 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
                 peer.count(4 * n_own)
                 raw = None
             else:
-                raw = tuple(tr.to_energy_major(x) for x in s_rows)
+                raw = tuple((tr.rows_to_full(x) if spatial else tr.to_energy_major(x)) for x in s_rows)
         del s_rows
         del wl, wg, gl, gg
         # 5. mixing + residual (scba.py:1155-1177), max over ranks
@@ -690,7 +731,7 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             raise ConvergenceError(f"residual grew from {residuals[-11]:.3e} to {residuals[-1]:.3e} over 10 iterations")
     if v is not None and sigma_to_host:
         for k, t in zip(("lesser", "greater", "ret_upper", "ret_lower"), sig.as_tuple()):
-            result["sigma_" + k] = t.cpu().numpy()
+            result["sigma_" + k] = (t[:, own] if spatial else t).cpu().numpy()
     result["iteration_s"] = iter_times
     result["residuals"] = np.asarray(residuals)
     result["identity_defects"] = identity_defects

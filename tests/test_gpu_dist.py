@@ -37,3 +37,18 @@ def test_energy_sharded_scba_all_to_all_only(cuda):
                          env={**os.environ, "NEGF_PEER_TRANSPOSE": "0"})
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "peer_transpose=0" in out.stdout
+
+
+def test_spatial_scba_matches_reference(cuda):
+    """The reference's spatial mode (scba_run plan=, scba.py:878-880): every
+    energy solved jointly by 2 ranks over the partitions (dd.py), vs the C1
+    golden and vs the sequential run over 3 iterations."""
+    import os
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs (one rank per GPU; ranks never share a GPU)")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node", "2",
+                          str(ROOT / "tools" / "dist_check.py")], capture_output=True, text=True, timeout=600,
+                         env={**os.environ, "NEGF_SPATIAL": "1"})
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "spatial=1" in out.stdout and "DIST_CHECK_3IT" in out.stdout

@@ -280,3 +280,18 @@ def test_scba_oracle_mode_deviations(golden, cuda):
     plain = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
                      Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=1, memoizer=MEMO_OFF), device=cuda)
     assert plain.oracle_deviations == {}
+
+
+def test_scba_spatial_plan_preconditions(cuda):
+    """scba.py:890-892 / dist.py:767-778: oracle_mode is sequential only; the
+    plan must cover the chain and have one partition per rank."""
+    from paper_2508_19138_b200.dd import PartitionError, make_partition_plan
+
+    args = (orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 8), 1e-3,
+            Contacts(0.1, -0.1, 0.05))
+    with pytest.raises(ValueError, match="oracle_mode"):
+        scba_run(*args, ScbaOptions(max_iter=1, oracle_mode=True), device=cuda, plan=make_partition_plan(6, 2))
+    with pytest.raises(PartitionError, match="partitions"):
+        scba_run(*args, ScbaOptions(max_iter=1), device=cuda, plan=make_partition_plan(6, 2))
+    with pytest.raises(PartitionError, match="covers"):
+        scba_run(*args, ScbaOptions(max_iter=1), device=cuda, plan=make_partition_plan(8, 2))
