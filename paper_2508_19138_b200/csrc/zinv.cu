@@ -1,3 +1,4 @@
+#include <type_traits>
 // Batched complex-FP64 block inversion with partial pivoting (sm_100a).
 //
 // Replaces negfgw/_linalg.py:30-52 `invert` (scipy lu_factor + lu_solve(I)):
@@ -145,6 +146,14 @@ __global__ void zinv_small_kernel(const z_t* __restrict__ S, long long sS, int l
 // choice including its first-index tie break. Outputs: the LAPACK-equivalent
 // interchange sequence ipiv, the net row permutation as a move list, and
 // Pinv = (pivot block)^-1 = U^-1 L^-1.
+template <int I, int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<I + 1, N>(f);
+  }
+}
+
 template <int NB>
 __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__ A, long long sA,
                                                          z_t* __restrict__ Anew, long long sAn, int n,
@@ -187,22 +196,24 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
 #ifdef NEGF_EXP_TIMING
   long long clk0 = clock64();
 #endif
-  // The column loop stays rolled: unrolling it multiplies the code by NB and
-  // the kernel then runs out of the instruction cache. Register elements are
-  // selected with predicated moves instead of runtime indexing.
+  // Column loop: the register slot cj is a compile-time index (16 copies of
+  // the column body, the TPR thread-columns of a slot in a rolled loop), so
+  // v[cj] needs no select chain and the rank-1 update no per-slot predicates
+  // (128 x 256^2 inverse 1.52 -> 1.36 ms). Unrolling all NB columns instead
+  // overflows the instruction cache.
 #ifdef NEGF_EXP_TIMING
   long long ph_a = 0, ph_b = 0, ph_c = 0, ph_d = 0, tq = clock64();
 #define PH(x) do { long long _t = clock64(); x += _t - tq; tq = _t; } while (0)
 #else
 #define PH(x) do { } while (0)
 #endif
+  static_for<0, 16>([&](auto cjc) {
+  constexpr int cj = decltype(cjc)::value;
 #pragma unroll 1
-  for (int j = 0; j < w; ++j) {
-    const int hj = j % TPR, cj = j / TPR;  // column j sits in slot cj of thread-column hj
-    z_t vj = v[0];
-#pragma unroll
-    for (int c = 1; c < 16; ++c)
-      if (c == cj) vj = v[c];
+  for (int hj = 0; hj < TPR; ++hj) {
+    const int j = cj * TPR + hj;
+    if (j >= w) break;
+    const z_t vj = v[cj];
     // (1) argmax over active rows of |re|+|im| in column j; ties -> smallest
     // LAPACK position. Non-negative doubles order like their bit patterns, so
     // the warp stage is three REDUX ops (high word, low word, min position).
@@ -272,14 +283,10 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
     } else if (act) {
       const z_t l = zmul(own, ipv);
       // slots below cj hold factored columns on every thread
+      if (h > hj) v[cj] = zfms(l, prow_s[cj * TPR + h], v[cj]);
+      else if (h == hj) v[cj] = l;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        if (c >= cj) {
-          const int gc = c * TPR + h;
-          if (gc > j) v[c] = zfms(l, prow_s[gc], v[c]);
-          else if (gc == j) v[c] = l;
-        }
-      }
+      for (int c = cj + 1; c < 16; ++c) v[c] = zfms(l, prow_s[c * TPR + h], v[c]);
       if (pos == j) pos = bp;  // LAPACK interchange: the row at position j moves to bp
     } else if (have && pos == j) {
       pos = bp;
@@ -292,6 +299,7 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
     }
     PH(ph_d);
   }
+  });
 #undef PH
   __syncthreads();
   if (warp == 0) {  // ipiv, |pivot| range and singularity over the panel's w pivots
