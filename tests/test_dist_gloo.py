@@ -36,6 +36,9 @@ def _worker(rank, world, port, n_entries, n_e, q):
         ok1 = np.array_equal(rows.numpy(), full[tr.own_r])
         back = tr.to_energy_major(rows)
         ok2 = np.array_equal(back.numpy(), full[:, tr.own_e])
+        # spatial mode of scba_run: every rank gets all entry rows (replicated
+        # to-energy-major result of the reference, scba.py:342-368)
+        ok2 = ok2 and np.array_equal(tr.rows_to_full(rows).numpy(), full)
         red = comm.allreduce_max([float(rank), -float(rank)], torch.device("cpu"))
         q.put((rank, ok1, ok2, red, tr.bytes_moved))
     finally:
@@ -71,4 +74,4 @@ def test_energy_chunks_match_reference_rule():
 def test_serial_comm_transposes_are_identity():
     tr = Transposer(Comm(), 9, 5)
     x = torch.zeros(9, 5, dtype=torch.complex128)
-    assert tr.to_entry_major(x) is x and tr.to_energy_major(x) is x
+    assert tr.to_entry_major(x) is x and tr.to_energy_major(x) is x and tr.rows_to_full(x) is x
