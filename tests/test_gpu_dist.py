@@ -52,3 +52,14 @@ def test_spatial_scba_matches_reference(cuda):
                          env={**os.environ, "NEGF_SPATIAL": "1"})
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "spatial=1" in out.stdout and "DIST_CHECK_3IT" in out.stdout
+
+
+def test_spatial_scba_with_memoizer_matches_sequential(cuda):
+    """Spatial mode with the OBC memoizer on (the reference default): Sigma and
+    the per-iteration direct/memoized call counts equal the sequential run's."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs (one rank per GPU; ranks never share a GPU)")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node", "2",
+                          str(ROOT / "tools" / "spatial_memo_check.py")], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "SPATIAL_MEMO" in out.stdout and "counts_equal=True" in out.stdout
