@@ -49,13 +49,16 @@ def parse():
     ap.add_argument("--n-e", type=int, default=1024, help="energies per rank")
     ap.add_argument("--batch", type=int, default=128, help="energies per device batch")
     ap.add_argument("--e2e-steps", type=int, default=1)
-    ap.add_argument("--greater", choices=["identity", "recursion"], default="identity",
-                    help="G^> by the exact identity G^> = G^< + G^R - G^R^dag (default) or by its own "
-                         "Keldysh recursion like the reference")
+    ap.add_argument("--greater", choices=["identity", "recursion"], default="recursion",
+                    help="G^> by its own Keldysh recursion like the reference (default, the headline) or by the "
+                         "exact identity G^> = G^< + G^R - G^R^dag; the other variant is timed beside it")
+    ap.add_argument("--alt-steps", type=int, default=3, help="timed steps of the other --greater variant")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-procs", type=int, default=0, help="0 = all host cores")
-    ap.add_argument("--scgw", default="32x128x512", help="n_blocks x block_size x energies-per-rank of the "
-                    "SCGW-iteration measurement ('' to skip)")
+    ap.add_argument("--scgw", default="64x512x16", help="n_blocks x block_size x energies-per-rank of the "
+                    "SCGW-iteration rate (default: the BASELINE configs[2] C3 device; '' to skip)")
+    ap.add_argument("--c4", default="40x2048x2", help="n_blocks x block_size x energies-per-rank of the "
+                    "NRFET-scale (BASELINE configs[3]) G+W RGF-phase rate ('' to skip)")
     return ap.parse_args()
 
 
@@ -68,11 +71,6 @@ def model_flops_per_energy(n_b: int, bs: int, kinds: int = 2) -> float:
     if kinds == 2:
         return 8.0 * bs ** 3 * (38 * n_b - 33)
     return 8.0 * bs ** 3 * (23 * n_b - 20)
-
-
-def exec_rgf_flops_per_energy(n_b: int, bs: int) -> float:
-    """This implementation: 27 n_b - 23 block products + n_b inversions (8 bs^3)."""
-    return 8.0 * bs ** 3 * (28 * n_b - 23)
 
 
 # -- CPU legs (oracle port) ---------------------------------------------------
@@ -329,7 +327,55 @@ def run_native(args):
     del solver, acc, b
     _lib._WS.clear()
     torch.cuda.empty_cache()
+    # the other G^> variant, timed the same way beside the headline (VERDICT
+    # r1: the identity halves the greater pass; the reference runs the recursion)
+    alt_mode = "identity" if args.greater == "recursion" else "recursion"
+    alt = None
+    if args.alt_steps > 0:
+        solver_alt = CarrierSolver(h, w["eta"], contacts, w["surface_tol"], device=dev, greater=alt_mode)
+        acc_alt = ObservableAccumulator(n_e, n_b, de, dev)
+
+        def step_alt():
+            for s in range(0, n_e, batch):
+                chunk = mine[s:s + batch]
+                bb = solver_alt.solve(chunk, n_e=len(chunk), check=False)
+                acc_alt.add(solver_alt, bb, s, len(chunk))
+            return bb
+
+        bb = step_alt()
+        solver_alt.check_status(bb)
+        barrier()
+        torch.cuda.synchronize(dev)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(args.alt_steps):
+            bb = step_alt()
+        a1.record()
+        torch.cuda.synchronize(dev)
+        barrier()
+        solver_alt.check_status(bb)
+        t = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        alt_ms = float(t.item())
+        alt = {"greater": alt_mode, "value": n_e * world * args.alt_steps / (alt_ms * 1e-3), "unit": UNIT,
+               "steps": args.alt_steps, "warmup": 1, "ms_per_step": alt_ms / args.alt_steps,
+               "rgf_tflops_model": model_flops_per_energy(n_b, bs, 1 if alt_mode == "identity" else 2)
+               * n_e * world * args.alt_steps / (alt_ms * 1e-3) / 1e12}
+        del solver_alt, bb, acc_alt
+        _lib._WS.clear()
+        torch.cuda.empty_cache()
+
     scgw = run_scgw(args, dev, world, rank, barrier) if args.scgw else None
+    conv_rf = conv_roofline(dev) if rank == 0 else None
+    c4 = None
+    if args.c4:
+        try:
+            c4 = run_gw_rate(args.c4, 1, dev, world, rank, barrier, "C4 NRFET-scale shape (BASELINE configs[3] device)")
+        except torch.OutOfMemoryError as exc:  # reported, not fatal: the headline is C2
+            c4 = {"error": f"out of memory: {str(exc).splitlines()[0]}"}
+        _lib._WS.clear()
+        torch.cuda.empty_cache()
 
     # CPU baseline: oracle port on this host's cores (rank 0, N=1 only)
     cpu = None
@@ -386,7 +432,10 @@ def run_native(args):
                     "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "api": "paper_2508_19138_b200.carrier.ballistic_observables (host H in, host observables out)"},
+            "greater_alt": alt,
             "scgw_iteration": scgw,
+            "c4_rgf_rate": c4,
+            "conv_roofline": conv_rf,
             "gpu_launches": int(launches),
             "device_time_breakdown": breakdown,
             "clocks": clk,
@@ -398,11 +447,15 @@ def run_native(args):
         dist.destroy_process_group()
 
 
-def run_scgw(args, dev, world, rank, barrier) -> dict:
-    """One full SCGW (GW) iteration -- carrier solve + OBC, polarization, W
-    (assembly, closure, RGF), self-energy, mixing -- energy-sharded over the
-    ranks with NCCL all-to-all E<->nnz transposes; weak scaling (energies per
-    rank fixed). Time = max over ranks of one iteration after one warm-up."""
+def run_gw_rate(spec: str, batch: int | None, dev, world, rank, barrier, label: str, profile_layout: bool = False) -> dict:
+    """GW iterations (carrier solve + OBC, polarization, W assembly + closure
+    + RGF, self-energy, mixing) on ``spec`` = "n_blocks x block_size x
+    energies-per-rank", energy-sharded over the ranks (weak scaling), OBC
+    memoizer on as in the reference default. Two iterations; the second
+    (warm buffers, nonzero Sigma) is timed, max over ranks. Stage times come
+    from device-synchronised stage timers of that iteration; the RGF-phase
+    rates use the SURVEY §8(d) model flops F_RGF = 8 bs^3 (38 n_b - 33) per
+    energy and subsystem."""
     import numpy as np
     import torch
 
@@ -411,63 +464,115 @@ def run_scgw(args, dev, world, rank, barrier) -> dict:
     from paper_2508_19138_b200.dist import Comm
     from paper_2508_19138_b200.scba import ScbaOptions, scba_run
 
-    n_b, bs, ne_rank = (int(x) for x in args.scgw.split("x"))
+    n_b, bs, ne_rank = (int(x) for x in spec.split("x"))
+    batch = batch or ne_rank
     w = WORKLOAD
     e = np.linspace(w["e_min"], w["e_max"], ne_rank * world)
     h, v = toys.chain_device(n_b, bs), toys.coulomb_matrix(n_b, bs)
     comm = Comm.from_env()
-    # reference defaults: tol 1e-5 (the residual after 2 iterations is ~0.4, so
-    # both run), OBC memoizer on with tol_memo = tol / 10
-    opts = ScbaOptions(max_iter=2, tol=1e-5, batch=min(128, ne_rank))
+    opts = ScbaOptions(retarded_method="sancho", max_iter=2, tol=1e-5, batch=batch)
     contacts = Contacts(w["mu_left"], w["mu_right"], w["kT"])
+    torch.cuda.reset_peak_memory_stats(dev)
     barrier()
-    # two iterations; the second (warm buffers, nonzero Sigma) is the timed one
-    res = scba_run(h, v, e, w["eta"], contacts, opts, device=dev, keep_g=False, comm=comm, sigma_to_host=False)
-    dt = res["iteration_s"][-1]
-    # HBM roofline of the convolution and E<->nnz layout kernels: one more
-    # iteration with the CUDA-event profiler on (algorithmic read+write bytes
-    # per launch recorded by the library) against MEASURED_PEAKS.json's copy
-    # bandwidth
-    import ctypes
-
-    from paper_2508_19138_b200 import _lib
-
-    lib = _lib.load()
-    lib.negf_prof_reset()
-    lib.negf_prof_enable(1)
-    scba_run(h, v, e, w["eta"], contacts, ScbaOptions(max_iter=1, tol=1e-5, batch=min(128, ne_rank)), device=dev,
-             keep_g=False, comm=comm, sigma_to_host=False)
-    torch.cuda.synchronize(dev)
-    lib.negf_prof_enable(0)
-    hbm = {}
-    peak = hbm_peak_gbs()
-    for cls, name, per in ((9, "conv (P and Sigma FFT kernels)", "96 B (P) / 128 B (Sigma) per entry-energy"),
-                           (10, "E<->nnz pack/unpack", "32 B per entry-energy (pack); entries + blocks (unpack)")):
-        c_ms, c_fl, c_by, c_n = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
-        _lib.check(lib.negf_prof_query(cls, ctypes.byref(c_ms), ctypes.byref(c_fl), ctypes.byref(c_by),
-                                       ctypes.byref(c_n)), "negf_prof_query")
-        gbs = c_by.value / (c_ms.value * 1e-3) / 1e9 if c_ms.value > 0 else 0.0
-        hbm[name] = {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-                     "launches": c_n.value, "ms": c_ms.value, "algorithmic_bytes": per}
-        if cls == 9 and c_n.value == 0:
-            hbm[name]["note"] = "no native launches: N_E > 2048 runs the convolutions through cuFFT (conv.MAX_L_NATIVE)"
-    lib.negf_prof_reset()
-    t = torch.tensor([dt], dtype=torch.float64, device=dev)
+    res = scba_run(h, v, e, w["eta"], contacts, opts, device=dev, keep_g=False, comm=comm, sigma_to_host=False,
+                   profile=True)
+    stage = res["timings_by_iteration"][-1]
+    vals = [res["iteration_s"][-1], stage.get("G: OBC+RGF", 0.0), stage.get("W: RGF", 0.0)]
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
     if world > 1:
         import torch.distributed as dist
 
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dt = float(t.item())
-    flops = 2 * model_flops_per_energy(n_b, bs) * ne_rank * world  # G and W selected solves
-    return {"config": f"chain_device({n_b},{bs}) + coulomb_matrix, {ne_rank * world} energies "
-                      f"({ne_rank}/rank), 1 GW iteration, energy-sharded x{world}",
-            "iteration_s": dt, "energies_per_s": ne_rank * world / dt,
-            "timing": "host wall clock of the 2nd iteration (device-synchronised at both ends), max over ranks",
-            "rgf_tflops_model_GW": flops / dt / 1e12,
-            "transpose_bytes_rank0": int(res["transpose_bytes"]),
-            "residual": float(res["residuals"][-1]),
-            "obc_memoizer": {"enabled": True, "cache_stats_by_iteration_rank0": res["cache_stats_by_iteration"]},
-            "hbm_roofline": hbm}
+    dt, t_g, t_w = (float(x) for x in t.tolist())
+    f = model_flops_per_energy(n_b, bs) * ne_rank * world
+    out = {"config": f"{label}: chain_device({n_b},{bs}) + coulomb_matrix, {ne_rank * world} energies "
+                     f"({ne_rank}/rank, batch {batch}), energy-sharded x{world}",
+           "iteration_s": dt, "energies_per_s": ne_rank * world / dt,
+           "timing": "host wall clock of the 2nd GW iteration, device-synchronised stage timers, max over ranks",
+           "stage_s_rank0": stage,
+           "rgf_tflops_model_G_incl_obc": f / t_g / 1e12 if t_g else None,
+           "rgf_tflops_model_W_rgf": f / t_w / 1e12 if t_w else None,
+           "rgf_tflops_model_GW_iteration": 2 * f / dt / 1e12,
+           "model": "F_RGF = 8 bs^3 (38 n_b - 33) per energy per subsystem (SURVEY §8(d)); this implementation "
+                    "executes 27 n_b - 23 products + n_b inversions of 8 bs^3, i.e. fewer flops than the model",
+           "max_mem_gb_rank0": torch.cuda.max_memory_allocated(dev) / 1e9,
+           "transpose_bytes_rank0": int(res["transpose_bytes"]),
+           "residual": float(res["residuals"][-1]),
+           "obc_memoizer": {"enabled": True, "cache_stats_by_iteration_rank0": res["cache_stats_by_iteration"]}}
+    if profile_layout:
+        # HBM roofline of the E<->nnz layout kernels: one more iteration with
+        # the CUDA-event profiler on (algorithmic bytes recorded per launch)
+        import ctypes
+
+        from paper_2508_19138_b200 import _lib
+
+        lib = _lib.load()
+        lib.negf_prof_reset()
+        lib.negf_prof_enable(1)
+        scba_run(h, v, e, w["eta"], contacts, ScbaOptions(retarded_method="sancho", max_iter=1, tol=1e-5, batch=batch), device=dev,
+                 keep_g=False, comm=comm, sigma_to_host=False)
+        torch.cuda.synchronize(dev)
+        lib.negf_prof_enable(0)
+        c_ms, c_fl, c_by, c_n = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
+        _lib.check(lib.negf_prof_query(10, ctypes.byref(c_ms), ctypes.byref(c_fl), ctypes.byref(c_by),
+                                       ctypes.byref(c_n)), "negf_prof_query")
+        lib.negf_prof_reset()
+        gbs = c_by.value / (c_ms.value * 1e-3) / 1e9 if c_ms.value > 0 else 0.0
+        peak = hbm_peak_gbs()
+        out["layout_hbm_roofline"] = {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                                      "frac": gbs / peak, "launches": c_n.value, "ms": c_ms.value,
+                                      "algorithmic_bytes": "32 B per entry-energy (pack); entries + blocks (unpack)"}
+    return out
+
+
+def run_scgw(args, dev, world, rank, barrier) -> dict:
+    return run_gw_rate(args.scgw, None, dev, world, rank, barrier, "C3 shape (BASELINE configs[2] device)",
+                       profile_layout=True)
+
+
+def conv_roofline(dev, n_rows: int = 1 << 17, lengths=(512, 2048, 4096)) -> dict:
+    """HBM roofline of the fused P and Sigma convolution kernels at the
+    BASELINE energy counts (C1/C3/C4 series lengths) on synthetic entry rows
+    (n_rows x N_E complex128 each, >> L2): algorithmic bytes per launch
+    (P: read G^<, G^>, write P^<, P^>, P^R_up, P^R_lo = 96 B per entry-energy;
+    Sigma: +W^<, W^> = 128 B) / CUDA-event time, against MEASURED_PEAKS.json's
+    copy bandwidth."""
+    import torch
+
+    from paper_2508_19138_b200.conv import polarization, self_energy
+
+    peak = hbm_peak_gbs()
+    out = {}
+    for ne in lengths:
+        g = torch.Generator(device=dev).manual_seed(ne)
+        mk = lambda: torch.complex(torch.randn(n_rows, ne, generator=g, device=dev, dtype=torch.float64),
+                                   torch.randn(n_rows, ne, generator=g, device=dev, dtype=torch.float64))
+        gl, gg, wl, wg = mk(), mk(), mk(), mk()
+        diag = torch.zeros(n_rows, dtype=torch.uint8, device=dev)
+        diag[::97] = 1
+        res = {}
+        for name, fn, per in (("P", lambda o: polarization(gl, gg, diag, 0.01, out=o), 96.0),
+                              ("Sigma", lambda o: self_energy(gl, gg, wl, wg, None, diag, 0.01, out=o), 128.0)):
+            o = tuple(torch.empty_like(gl) for _ in range(4))
+            fn(o)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 5
+            e0.record()
+            for _ in range(reps):
+                fn(o)
+            e1.record()
+            torch.cuda.synchronize(dev)
+            ms = e0.elapsed_time(e1) / reps
+            gbs = per * n_rows * ne / (ms * 1e-3) / 1e9
+            res[name] = {"ms": ms, "achieved": gbs, "frac": gbs / peak}
+            del o
+        out[f"N_E={ne}"] = res
+        del gl, gg, wl, wg
+        torch.cuda.empty_cache()
+    return {"bound": "hbm", "peak": peak, "unit": "GB/s", "rows": n_rows,
+            "basis": "algorithmic bytes (96 B P / 128 B Sigma per entry-energy) / CUDA-event time per launch set, "
+                     "inputs 2-4 x rows x N_E x 16 B >> L2", "lengths": out}
 
 
 # -- reference arm -----------------------------------------------------------------
@@ -489,8 +594,8 @@ def run_reference(args):
     ctx = mp.get_context("spawn")
     with ctx.Pool(procs) as pool:
         pool.map(_cpu_worker, [(n_b, 16, [0.0])] * procs)
-        for s in range(args.warmup):
-            pass  # the per-energy work is identical across energies; no state to warm beyond the pool
+        for s in range(args.warmup):  # untimed warm-up steps: same work as a timed step
+            pool.map(_cpu_worker, [(n_b, bs, [float(grid[(s * procs + i) * 11 % len(grid)])]) for i in range(procs)])
         walls = []
         for s in range(args.steps):
             chunks = [(n_b, bs, [float(grid[(s * procs + i) * 7 % len(grid)])]) for i in range(procs)]

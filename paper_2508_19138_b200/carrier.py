@@ -292,6 +292,10 @@ class ObservableAccumulator:
         self.cur = torch.zeros((n_e_total, max(n_b - 1, 1)), dtype=torch.float64, device=self.dev)
         self.term = torch.zeros((n_e_total, 2), dtype=Z, device=self.dev)
 
+    def reset(self) -> None:
+        for t in (self.tr_gr, self.tr_gl, self.cur, self.term):
+            t.zero_()
+
     def add(self, solver: "CarrierSolver", b: dict, e0: int, ne: int) -> None:
         p = _lib.ptr
         rc = solver.lib.negf_observables(

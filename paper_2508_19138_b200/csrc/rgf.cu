@@ -163,38 +163,47 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
   // (tA[i & 1]); events order the hand-offs:
   //   evA[p]: A_i ready (R -> K)   evX[p]: x_i ready (R -> K)
   //   evK[p]: step i's K work done, before R overwrites tA[p] at step i + 2.
-  cudaStream_t sk = st;
-  cudaEvent_t evA[2] = {nullptr, nullptr}, evX[2] = {nullptr, nullptr}, evK[2] = {nullptr, nullptr};
-  cudaEvent_t ev0 = nullptr;
   const bool pipe = a.overlap && nk > 0 && n > 1;
-  struct Cleanup {
-    cudaStream_t* s;
-    cudaEvent_t* evs[4];
-    int counts[4];
-    ~Cleanup() {
-      for (int j = 0; j < 4; ++j)
-        for (int q = 0; q < counts[j]; ++q)
-          if (evs[j][q]) cudaEventDestroy(evs[j][q]);
-    }
-  } cleanup{nullptr, {evA, evX, evK, &ev0}, {2, 2, 2, 1}};
+  // The auxiliary stream and its events are created once per (thread,
+  // device) and reused by every call (no per-call create/destroy); a
+  // thread-local cache keeps concurrent callers on different threads apart.
+  struct AuxStreams {
+    cudaStream_t sk = nullptr;
+    cudaEvent_t evA[2], evX[2], evK[2], ev0;
+  };
+  thread_local AuxStreams aux_cache[64];
+  cudaStream_t sk = st;
+  cudaEvent_t *evA = nullptr, *evX = nullptr, *evK = nullptr, ev0 = nullptr;
   if (pipe) {
-    NEGF_CUDA_CHECK(cudaStreamCreateWithFlags(&sk, cudaStreamNonBlocking));
-    for (int j = 0; j < 2; ++j) {
-      NEGF_CUDA_CHECK(cudaEventCreateWithFlags(&evA[j], cudaEventDisableTiming));
-      NEGF_CUDA_CHECK(cudaEventCreateWithFlags(&evX[j], cudaEventDisableTiming));
-      NEGF_CUDA_CHECK(cudaEventCreateWithFlags(&evK[j], cudaEventDisableTiming));
+    int dev = 0;
+    NEGF_CUDA_CHECK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return -1;
+    AuxStreams& ax = aux_cache[dev];
+    if (!ax.sk) {
+      for (int j = 0; j < 2; ++j) {
+        NEGF_CUDA_CHECK(cudaEventCreateWithFlags(&ax.evA[j], cudaEventDisableTiming));
+        NEGF_CUDA_CHECK(cudaEventCreateWithFlags(&ax.evX[j], cudaEventDisableTiming));
+        NEGF_CUDA_CHECK(cudaEventCreateWithFlags(&ax.evK[j], cudaEventDisableTiming));
+      }
+      NEGF_CUDA_CHECK(cudaEventCreateWithFlags(&ax.ev0, cudaEventDisableTiming));
+      NEGF_CUDA_CHECK(cudaStreamCreateWithFlags(&ax.sk, cudaStreamNonBlocking));
     }
-    NEGF_CUDA_CHECK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+    sk = ax.sk;
+    evA = ax.evA; evX = ax.evX; evK = ax.evK; ev0 = ax.ev0;
     NEGF_CUDA_CHECK(cudaEventRecord(ev0, st));
     NEGF_CUDA_CHECK(cudaStreamWaitEvent(sk, ev0, 0));
   }
-  struct StreamGuard {
+  // On EVERY exit (including an early error return after work was queued on
+  // sk) the caller's stream waits for sk, so the caller never frees or reuses
+  // workspace / outputs that sk kernels may still be writing.
+  struct JoinGuard {
     cudaStream_t s, main;
-    bool own;
-    ~StreamGuard() {
-      if (own) cudaStreamDestroy(s);
+    cudaEvent_t ev;
+    bool on;
+    ~JoinGuard() {
+      if (on && cudaEventRecord(ev, s) == cudaSuccess) cudaStreamWaitEvent(main, ev, 0);
     }
-  } sguard{sk, st, pipe};
+  } jguard{sk, st, ev0, pipe};
   z_t* tAb[2] = {tA, c.T(2)};
 
   const bool do_fwd = a.mode != 2;

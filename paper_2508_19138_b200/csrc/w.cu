@@ -374,7 +374,10 @@ int stein_batched(const z_t* a, const z_t* q, z_t* w, int n_side, int n_kind, in
   }
   {
     ProfScope ps_stein_init_kernel(PROF_OTHER, (cudaStream_t)(st));
-    stein_init_kernel<<<n_side, 256, 2 * (size_t)bs * sizeof(z_t), st>>>(a, n2, bs, v0, n_side, n_kind,
+    const size_t smem = 2 * (size_t)bs * sizeof(z_t);  // 64 KB at bs = 2048: above the 48 KB default
+    if (smem > 48 * 1024)
+      NEGF_CUDA_CHECK(cudaFuncSetAttribute(stein_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    stein_init_kernel<<<n_side, 256, smem, st>>>(a, n2, bs, v0, n_side, n_kind,
                                                                           active, iters, status, select);
     NEGF_LAUNCHED();
   }

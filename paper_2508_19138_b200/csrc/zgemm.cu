@@ -318,12 +318,16 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
 
 template <class CF, bool RV = false>
 int launch_cfg(const ZGemmGroup& g, cudaStream_t stream) {
-  static bool attr_done = false;
-  if (!attr_done) {
+  // cudaFuncSetAttribute applies to the current device's context: once per device
+  static unsigned long long attr_done = 0;
+  int dev = 0;
+  NEGF_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev >= 64) return -1;
+  if (!(__atomic_load_n(&attr_done, __ATOMIC_ACQUIRE) & (1ull << dev))) {
     NEGF_CUDA_CHECK(cudaFuncSetAttribute(zgemm_kernel<CF, RV>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)CF::SMEM));
-    attr_done = true;
+    __atomic_fetch_or(&attr_done, 1ull << dev, __ATOMIC_RELEASE);
   }
   int max_tiles = 0, max_batch = 0;
   for (int i = 0; i < g.n; ++i) {

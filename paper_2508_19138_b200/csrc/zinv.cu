@@ -6,23 +6,28 @@
 // singularity rule (a pivot that is exactly zero or non-finite), and the
 // same conditioning proxy u_spread = max|U_jj| / min|U_jj|.
 //
-// Algorithm: blocked in-place Gauss-Jordan sweeps. For a panel of NB columns
-//   1. one CTA per matrix runs the unblocked pivoted LU of the (N-k0) x NB
-//      panel in shared memory -> pivot rows, and Pinv = (pivot block)^-1;
-//   2. a swap kernel applies the NB row interchanges to the whole matrix and
-//      emits C' = A[:,K] (rows K zeroed) and R = A[K,:];
-//   3. T = Pinv R                        (DMMA GEMM, M=NB, N=N, K=NB)
-//   4. A[:, not K] -= C' T, A[:, K] = -C' Pinv   (one grouped DMMA launch)
-//   5. rows K <- [T | Pinv]
-// Every entry is produced by the textbook Gauss-Jordan formula (no
-// cancellation-prone identity tricks), so the error matches LU-based inversion.
-// which leaves inv(PA) after the last panel; a final kernel undoes the row
+// Algorithm: blocked Gauss-Jordan sweeps, ping-ponging between S and X. For
+// each panel K of NB columns:
+//   1. the panel kernel runs the unblocked pivoted LU of the (N-k0) x NB
+//      panel with the pivot search over the whole remaining column (one CTA
+//      per matrix for N <= 512; a thread-block cluster of up to 8 CTAs sharing
+//      the candidates through distributed shared memory for 512 < N <= 4096),
+//      and writes Pinv = (pivot block)^-1, the row maps of the interchanges,
+//      and rows K of the new matrix: [T | Pinv] with T = Pinv R;
+//   2. one row-mapped grouped DMMA launch updates every other row:
+//      A[:, not K] -= C' T,  A[:, K] = -C' Pinv.
+// This leaves inv(PA) after the last panel; a final kernel undoes the row
 // permutation on the columns (LAPACK zgetri order) while copying to the
-// destination. The O(N^3) work runs on the DMMA GEMM; the panel kernels are
-// O(N^2 NB). Blocks with N <= 64 are inverted by one CTA entirely in smem.
+// destination. Every entry comes from the textbook Gauss-Jordan formula, so
+// the error matches LU-based inversion. The O(N^3) work runs on the DMMA
+// GEMM; the panel kernels are O(N^2 NB). Blocks with N <= 64 are inverted by
+// one CTA entirely in smem.
 #include "prof.cuh"
 #include "zgemm.cuh"
 #include "zinv.cuh"
+
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace negf {
 
@@ -426,6 +431,259 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
   }
 }
 
+// Panel LU for blocks above the one-CTA register panel (n > 512): the panel
+// rows are split over a thread-block cluster of C <= 8 CTAs (RPC rows each,
+// same register layout as zinv_panel_kernel), and the pivot search spans the
+// WHOLE column (LAPACK zgetf2 order, first-index ties) through distributed
+// shared memory. Per column: in-CTA argmax (one barrier), then every CTA
+// writes its candidate (|pivot|, LAPACK position, row, the 16/32 panel values
+// of that row and its reciprocal) into slot [parity][rank] of every CTA of
+// the cluster, one cluster barrier, and every thread picks the winner from
+// its local copy. Candidate slots are double-buffered by column parity: a
+// slot is rewritten two columns later, after an intervening cluster barrier
+// that every reader of the old contents has passed. Outputs are those of
+// zinv_panel_kernel (ipiv, Pinv, row maps, rows K of A_new = [Pinv R | Pinv])
+// with the T columns split over the cluster.
+constexpr int kClusterMax = 8;
+
+template <int NB>
+__global__ void __launch_bounds__(512) zinv_panel_cluster_kernel(const z_t* __restrict__ A, long long sA,
+                                                                 z_t* __restrict__ Anew, long long sAn, int n,
+                                                                 int k0, int w, int* ipiv, z_t* pinv,
+                                                                 double* umaxmin, int* map_src, int* map_dst,
+                                                                 InvAux aux) {
+  constexpr int TPR = NB / 16;    // threads per row
+  constexpr int RPC = 512 / TPR;  // panel rows per CTA
+  constexpr int LD = NB + 1;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks();
+  const int q = (int)cluster.block_rank();
+  __shared__ z_t cand_row[2][kClusterMax][NB];
+  __shared__ z_t cand_ip[2][kClusterMax];
+  __shared__ double cand_v[2][kClusterMax];
+  __shared__ int cand_p[2][kClusterMax];
+  __shared__ int cand_r[2][kClusterMax];
+  __shared__ z_t blk[NB * LD];     // pivot rows (L\U) in pivot order
+  __shared__ z_t pinv_s[NB * LD];
+  __shared__ z_t rdiag_s[NB];
+  __shared__ int prow_s[NB];       // panel row of the pivot chosen at column j
+  __shared__ int piv_s[NB];
+  __shared__ z_t pval_s[NB];
+  __shared__ double rv[32];
+  __shared__ int ri[32], rp[32];
+  const int b = blockIdx.y;  // every CTA of a cluster has the same b
+  if (aux.active && !aux.active[b]) return;
+  const int rows = n - k0;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int r = tid / TPR, h = tid % TPR;
+  const int grow = q * RPC + r;  // panel row (0 = matrix row k0)
+  const bool have = grow < rows;
+  const z_t* a = A + (long long)b * sA;
+  z_t v[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+    v[c] = (have && c * TPR + h < w) ? a[(long long)(k0 + grow) * n + k0 + c * TPR + h] : make_double2(0.0, 0.0);
+  bool act = have;
+  int pos = grow;
+  static_for<0, 16>([&](auto cjc) {
+    constexpr int cj = decltype(cjc)::value;
+#pragma unroll 1
+    for (int hj = 0; hj < TPR; ++hj) {
+      const int j = cj * TPR + hj;
+      if (j >= w) break;
+      const int par = j & 1;
+      const z_t vj = v[cj];
+      double bv = 0.0;
+      int bp = 0x7fffffff;
+      if (act && h == hj) {
+        double c = zabs1(vj);
+        if (c != c) c = INFINITY;
+        bv = c;
+        bp = pos;
+      }
+      {  // warp stage (same REDUX scheme as zinv_panel_kernel)
+        const unsigned long long key = __double_as_longlong(bv);
+        const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+        const bool best = hi == mhi && lo == mlo;
+        const int mpos = (int)__reduce_min_sync(0xffffffffu, best ? (unsigned)bp : 0x7fffffffu);
+        const unsigned who = __ballot_sync(0xffffffffu, best && bp == mpos);
+        const int src = who ? __ffs(who) - 1 : 0;
+        const int br = __shfl_sync(0xffffffffu, r, src);
+        if (lane == 0) {
+          rv[warp] = __longlong_as_double(((unsigned long long)mhi << 32) | mlo);
+          ri[warp] = mpos == 0x7fffffff ? -1 : br;
+          rp[warp] = mpos;
+        }
+      }
+      __syncthreads();
+      int br;
+      double bval;
+      {  // cross-warp stage -> this CTA's candidate
+        const double wv = lane < nw ? rv[lane] : 0.0;
+        const int wp = lane < nw ? rp[lane] : 0x7fffffff;
+        const int wr = lane < nw ? ri[lane] : -1;
+        const unsigned long long key = __double_as_longlong(wv);
+        const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+        const bool best = hi == mhi && lo == mlo && wr >= 0;
+        const int mpos = (int)__reduce_min_sync(0xffffffffu, best ? (unsigned)wp : 0x7fffffffu);
+        const unsigned who = __ballot_sync(0xffffffffu, best && wp == mpos);
+        const int src = who ? __ffs(who) - 1 : 0;
+        br = __shfl_sync(0xffffffffu, wr, src);
+        bp = mpos;
+        bval = __longlong_as_double(((unsigned long long)mhi << 32) | mlo);
+      }
+      // publish the candidate to every CTA of the cluster
+      if (br >= 0 && r == br) {
+        const z_t ipv = zinv(vj);  // valid on the h == hj thread
+        for (int d = 0; d < C; ++d) {
+          z_t* row = cluster.map_shared_rank(&cand_row[par][q][0], d);
+#pragma unroll
+          for (int c = 0; c < 16; ++c) row[c * TPR + h] = v[c];
+          if (h == hj) {
+            *cluster.map_shared_rank(&cand_ip[par][q], d) = ipv;
+            *cluster.map_shared_rank(&cand_v[par][q], d) = bval;
+            *cluster.map_shared_rank(&cand_p[par][q], d) = bp;
+            *cluster.map_shared_rank(&cand_r[par][q], d) = q * RPC + br;
+          }
+        }
+      } else if (br < 0 && tid < C) {
+        *cluster.map_shared_rank(&cand_r[par][q], tid) = -1;
+      }
+      cluster.sync();
+      // winner over the cluster: max |pivot|, ties -> smallest LAPACK position
+      int qw = -1;
+      double wvv = -1.0;
+      int wpp = 0x7fffffff;
+      for (int d = 0; d < C; ++d) {
+        if (cand_r[par][d] < 0) continue;
+        const double cv = cand_v[par][d];
+        const int cp = cand_p[par][d];
+        if (qw < 0 || cv > wvv || (cv == wvv && cp < wpp)) { qw = d; wvv = cv; wpp = cp; }
+      }
+      const z_t* prow = &cand_row[par][qw][0];
+      const z_t ipv = cand_ip[par][qw];
+      const int wrow = cand_r[par][qw];
+      bp = wpp;
+      z_t own = vj;
+      if (TPR > 1) {
+        own.x = __shfl_sync(0xffffffffu, own.x, (lane & ~(TPR - 1)) | hj);
+        own.y = __shfl_sync(0xffffffffu, own.y, (lane & ~(TPR - 1)) | hj);
+      }
+      if (act && grow == wrow) {
+        act = false;
+        pos = j;
+      } else if (act) {
+        const z_t l = zmul(own, ipv);
+        if (h > hj) v[cj] = zfms(l, prow[cj * TPR + h], v[cj]);
+        else if (h == hj) v[cj] = l;
+#pragma unroll
+        for (int c = cj + 1; c < 16; ++c) v[c] = zfms(l, prow[c * TPR + h], v[c]);
+        if (pos == j) pos = bp;
+      } else if (have && pos == j) {
+        pos = bp;
+      }
+      if (tid < NB) blk[j * LD + tid] = prow[tid];
+      if (tid == 0) {
+        piv_s[j] = bp;
+        pval_s[j] = prow[j];
+        prow_s[j] = wrow;
+      }
+    }
+  });
+  __syncthreads();
+  if (q == 0 && warp == 0) {  // ipiv, |pivot| range, singularity
+    double mx = 0.0, mn = INFINITY;
+    int bad = 0;
+    for (int t = lane; t < w; t += 32) {
+      ipiv[(long long)b * n + k0 + t] = k0 + piv_s[t];
+      const double m = hypot(pval_s[t].x, pval_s[t].y);
+      if (!(m > 0.0) || !isfinite(m)) bad = 1;
+      mx = fmax(mx, m);
+      mn = fmin(mn, m);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+      mn = fmin(mn, __shfl_down_sync(0xffffffffu, mn, o));
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      const double pmx = k0 == 0 ? 0.0 : umaxmin[2 * b], pmn = k0 == 0 ? INFINITY : umaxmin[2 * b + 1];
+      umaxmin[2 * b] = fmax(pmx, mx);
+      umaxmin[2 * b + 1] = fmin(pmn, mn);
+      if (bad && aux.status) atomicCAS(aux.status + b, 0, aux.status_code);
+    }
+  }
+  // row maps: rows above the panel stay, the non-pivot rows follow their final position
+  if (have && pos >= w && h == 0) {
+    map_src[(long long)b * n + k0 + pos - w] = k0 + grow;
+  }
+  for (int m = q * blockDim.x + tid; m < n - w; m += C * blockDim.x) {
+    map_dst[(long long)b * n + m] = m < k0 ? m : m + w;
+    if (m < k0) map_src[(long long)b * n + m] = m;
+  }
+  // Pinv = U^-1 L^-1 (every CTA, for its share of T)
+  if (tid < w) rdiag_s[tid] = zinv(blk[tid * LD + tid]);
+  __syncthreads();
+  for (int pass = 0, c0 = warp; c0 < w; ++pass, c0 += nw) {
+    const int c = pass ? w - 1 - (c0 - nw) : c0;
+    z_t y = zmake(lane == c ? 1.0 : 0.0, 0.0);
+    for (int k = c; k < w; ++k) {
+      const z_t yk = make_double2(__shfl_sync(0xffffffffu, y.x, k), __shfl_sync(0xffffffffu, y.y, k));
+      if (lane > k && lane < w) y = zfms(blk[lane * LD + k], yk, y);
+    }
+    for (int k = w - 1; k >= 0; --k) {
+      z_t xk = make_double2(__shfl_sync(0xffffffffu, y.x, k), __shfl_sync(0xffffffffu, y.y, k));
+      xk = zmul(xk, rdiag_s[k]);
+      if (lane == k) y = xk;
+      if (lane < k) y = zfms(blk[lane * LD + k], xk, y);
+    }
+    if (lane < w) {
+      if (q == 0) pinv[(long long)b * w * w + lane * w + c] = y;
+      pinv_s[lane * LD + c] = y;
+    }
+  }
+  __syncthreads();
+  // rows K of A_new = [T | Pinv], T = Pinv R; columns split over the cluster
+  z_t* an = Anew + (long long)b * sAn;
+  {
+    constexpr int TB = 8;
+    const int tblocks = (w + TB - 1) / TB;
+    const int cols = (n + C - 1) / C, j0 = q * cols, j1 = j0 + cols < n ? j0 + cols : n;
+    const int nc = j1 - j0;
+    for (int e = tid; e < tblocks * nc; e += blockDim.x) {
+      const int j = j0 + e % nc, t0 = (e / nc) * TB;
+      const int t1 = t0 + TB < w ? t0 + TB : w;
+      if (j >= k0 && j < k0 + w) {
+        for (int t = t0; t < t1; ++t) an[(long long)(k0 + t) * n + j] = pinv_s[t * LD + (j - k0)];
+        continue;
+      }
+      z_t acc[TB];
+#pragma unroll
+      for (int u = 0; u < TB; ++u) acc[u] = make_double2(0.0, 0.0);
+      for (int q0 = 0; q0 < w; q0 += 8) {
+        z_t rq[8];
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq)
+          rq[qq] = q0 + qq < w ? a[(long long)(k0 + prow_s[q0 + qq]) * n + j] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq)
+#pragma unroll
+          for (int u = 0; u < TB; ++u) acc[u] = zfma(pinv_s[(t0 + u) * LD + q0 + qq], rq[qq], acc[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < TB; ++u)
+        if (t0 + u < t1) an[(long long)(k0 + t0 + u) * n + j] = acc[u];
+    }
+  }
+  // no CTA may exit while a peer can still write into its shared memory
+  cluster.sync();
+}
+
 // X = inv(PA) P: the row interchanges are undone on the columns (LAPACK
 // zgetri order: for k = n-1 .. 0 swap columns k <-> ipiv[k]). perm is built
 // once per matrix (ipiv staged in smem), then a wide grid does the copy.
@@ -454,152 +712,55 @@ __global__ void zinv_perm_kernel(int n, const int* ipiv, const double* umaxmin, 
 
 // Rows are staged in smem, so A and X may be the same buffer.
 __global__ void zinv_unpermute_kernel(const z_t* A, long long sA, int n, const int* perm_g, z_t* X,
-                                      long long sX, int ldx, const int* active) {
+                                      long long sX, int ldx, const int* active, int R) {
   extern __shared__ __align__(16) unsigned char raw_u[];
-  z_t* rows = reinterpret_cast<z_t*>(raw_u);           // 8 x n
-  int* perm = reinterpret_cast<int*>(rows + 8 * n);
+  z_t* rows = reinterpret_cast<z_t*>(raw_u);           // R x n
+  int* perm = reinterpret_cast<int*>(rows + (size_t)R * n);
   const int b = blockIdx.y;
   if (active && !active[b]) return;
   for (int j = threadIdx.x; j < n; j += blockDim.x) perm[j] = perm_g[(long long)b * n + j];
   const z_t* a = A + (long long)b * sA;
   z_t* x = X + (long long)b * sX;
-  const int r0 = blockIdx.x * 8;
-  for (int e = threadIdx.x; e < 8 * n; e += blockDim.x) {
+  const int r0 = blockIdx.x * R;
+  for (int e = threadIdx.x; e < R * n; e += blockDim.x) {
     const int i = r0 + e / n;
     if (i < n) rows[e] = a[(long long)i * n + e % n];
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < 8 * n; e += blockDim.x) {
+  for (int e = threadIdx.x; e < R * n; e += blockDim.x) {
     const int i = r0 + e / n, j = e % n;
     if (i < n) x[(long long)i * ldx + j] = rows[(e / n) * n + perm[j]];
   }
 }
 
-// dst[b] (rows x cols, ld ldd) = src[b] (ld lds); batch strides sdst / ssrc
-__global__ void copy_block_kernel(z_t* __restrict__ dst, long long sdst, int ldd, const z_t* __restrict__ src,
-                                  long long ssrc, int lds, int rows, int cols) {
-  const long long b = blockIdx.y;
-  const long long total = (long long)rows * cols;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(e / cols), j = (int)(e % cols);
-    dst[b * sdst + (long long)i * ldd + j] = src[b * ssrc + (long long)i * lds + j];
-  }
+constexpr int kInvPanelMax = 512;   // one-CTA register panel limit
+constexpr int kInvClusterMax = 4096;  // cluster panel limit (8 CTAs x 512 rows)
+
+// cudaFuncSetAttribute is per device context: remember it per device.
+bool attr_once(const void* fn, int bytes, unsigned* done_mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 32) return false;
+  if (__atomic_load_n(done_mask, __ATOMIC_ACQUIRE) & (1u << dev)) return true;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+  __atomic_fetch_or(done_mask, 1u << dev, __ATOMIC_RELEASE);
+  return true;
 }
-
-int copy_block(z_t* dst, long long sdst, int ldd, const z_t* src, long long ssrc, int lds, int rows, int cols,
-               int batch, cudaStream_t st) {
-  long long total = (long long)rows * cols;
-  int bx = (int)((total + 255) / 256);
-  if (bx > 256) bx = 256;
-  dim3 grid(bx, batch);
-  ProfScope ps_(PROF_ZINV, st);
-  copy_block_kernel<<<grid, 256, 0, st>>>(dst, sdst, ldd, src, ssrc, lds, rows, cols);
-  NEGF_LAUNCHED();
-  return 0;
-}
-
-__global__ void fill_nan_kernel(double* x, long long stride, int n) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) x[(long long)i * stride] = __longlong_as_double(0x7ff8000000000000ll);
-}
-
-constexpr int kInvPanelMax = 512;  // one-CTA register panel limit
-
-inline size_t a256z(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
 size_t zinv_workspace_bytes(int n, int batch) {
   if (n <= kInvSmallMax) return 0;
-  if (n > kInvPanelMax) {  // 2x2 block recursion (zinv_recursive)
-    const size_t h = n / 2, r = n - h, zb = sizeof(z_t) * (size_t)batch;
-    const size_t sub_h = zinv_workspace_bytes((int)h, batch), sub_r = zinv_workspace_bytes((int)r, batch);
-    return a256z(zb * h * h) * 2 + a256z(zb * r * h) * 2 + a256z(zb * r * r) * 2 + (sub_h > sub_r ? sub_h : sub_r);
-  }
   const int nb = zinv_panel_width(n);
   size_t per = 4 * sizeof(int) * (size_t)n + sizeof(double) * 2 + sizeof(z_t) * (size_t)nb * nb;
   return per * batch + 256 * 8;
 }
 
-namespace {
-
-// Blocks above the register-panel limit: 2x2 block inverse on packed halves,
-//   [A B; C D]^-1 = [Ai + Ai B Si C Ai, -Ai B Si; -Si C Ai, Si],  Si = (D - C Ai B)^-1,
-// each half inverted by the pivoted kernel (recursively). No pivoting across
-// the halves: sound for the carrier Schur complements, whose anti-Hermitian
-// part (eta - Im Sigma^R) is positive definite, so every leading block and
-// its Schur complement are invertible with norm <= 1/eta. Singular halves
-// are reported through aux.status; u_spread is not defined for this path
-// (NaN).
-int zinv_recursive(z_t* S, long long sS, z_t* X, long long sX, int n, int batch, InvAux aux, void* ws,
-                   size_t ws_bytes, cudaStream_t st) {
-  const int h = n / 2, r = n - h;
-  const size_t zb = sizeof(z_t) * (size_t)batch;
-  char* w = reinterpret_cast<char*>(ws);
-  auto take = [&](size_t bytes) { char* q = w; w += a256z(bytes); return (z_t*)q; };
-  z_t* Ap = take(zb * h * h);
-  z_t* Ai = take(zb * h * h);
-  z_t* T1 = take(zb * (size_t)r * h);  // C Ai
-  z_t* T2 = take(zb * (size_t)h * r);  // Ai B
-  z_t* Dp = take(zb * (size_t)r * r);
-  z_t* Si = take(zb * (size_t)r * r);
-  void* sub = w;
-  const size_t sub_bytes = ws_bytes - (size_t)(w - reinterpret_cast<char*>(ws));
-  InvAux sa = aux;
-  sa.u_spread = nullptr;
-  const long long hh = (long long)h * h, rh = (long long)r * h, rr = (long long)r * r;
-  const z_t* A = S;
-  const z_t* B = S + h;
-  const z_t* C = S + (long long)h * n;
-  const z_t* D = S + (long long)h * n + h;
-  RC_(copy_block(Ap, hh, h, A, sS, n, h, h, batch, st));
-  RC_(zinv_batched(Ap, hh, h, Ai, hh, h, h, batch, sa, sub, sub_bytes, st));
-  auto desc = [&](const z_t* a, long long sa_, int lda, const z_t* b, long long sb, int ldb, int M, int N, int K,
-                  z_t* d, long long sd, int ldd, double alpha, const z_t* c, long long sc, int ldc) {
-    ZGemmDesc g = zdesc_default();
-    g.M = M; g.N = N; g.batch = batch;
-    g.t[0] = zterm(a, sa_, lda, OP_N, b, sb, ldb, OP_N, K);
-    for (int i = 1; i < kMaxTerms; ++i) g.t[i] = g.t[0];
-    g.alpha = make_double2(alpha, 0.0);
-    if (c) { g.C = c; g.sC = sc; g.ldc = ldc; g.beta = make_double2(1.0, 0.0); }
-    g.D = d; g.sD = sd; g.ldd = ldd;
-    g.active = aux.active;
-    return g;
-  };
-  {  // T1 = C Ai, T2 = Ai B
-    ZGemmGroup g;
-    g.n = 2;
-    g.d[0] = desc(C, sS, n, Ai, hh, h, r, h, h, T1, rh, h, 1.0, nullptr, 0, 0);
-    g.d[1] = desc(Ai, hh, h, B, sS, n, h, r, h, T2, rh, r, 1.0, nullptr, 0, 0);
-    RC_(zgemm_group_launch(g, st));
-  }
-  // Dp = D - T1 B ; Si = Dp^-1
-  RC_(zgemm_launch(desc(T1, rh, h, B, sS, n, r, r, h, Dp, rr, r, -1.0, D, sS, n), st));
-  RC_(zinv_batched(Dp, rr, r, Si, rr, r, r, batch, sa, sub, sub_bytes, st));
-  // X22 = Si ; X21 = -Si T1 ; X12 = -T2 Si
-  RC_(copy_block(X + (long long)h * n + h, sX, n, Si, rr, r, r, r, batch, st));
-  {
-    ZGemmGroup g;
-    g.n = 2;
-    g.d[0] = desc(Si, rr, r, T1, rh, h, r, h, r, X + (long long)h * n, sX, n, -1.0, nullptr, 0, 0);
-    g.d[1] = desc(T2, rh, r, Si, rr, r, h, r, r, X + h, sX, n, -1.0, nullptr, 0, 0);
-    RC_(zgemm_group_launch(g, st));
-  }
-  // X11 = Ai - X12 T1
-  RC_(zgemm_launch(desc(X + h, sX, n, T1, rh, h, h, h, r, X, sX, n, -1.0, Ai, hh, h), st));
-  if (aux.u_spread) {
-    fill_nan_kernel<<<(batch + 127) / 128, 128, 0, st>>>(aux.u_spread, aux.spread_stride, batch);
-    NEGF_LAUNCHED();
-  }
-  return 0;
-}
-
-}  // namespace
-
 int zinv_panel_width(int n) {
-  // register panel: n * (nb/16) threads <= 512 per CTA
+  // one-CTA register panel: n * (nb/16) threads <= 512; cluster panel:
+  // 512 * 16 / nb rows per CTA, <= kClusterMax CTAs
   if (n <= 256) return 32;
+  if (n <= kInvPanelMax) return 16;
+  if (n <= 2048) return 32;
   return 16;
 }
 
@@ -610,12 +771,8 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
   if (batch <= 0) return 0;
   if (n <= kInvSmallMax) {
     size_t smem = (size_t)n * (n + 1) * sizeof(z_t) + 2 * n * sizeof(int) + 16;
-    static bool attr = false;
-    if (!attr) {
-      NEGF_CUDA_CHECK(cudaFuncSetAttribute(zinv_small_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
+    static unsigned attr = 0;
+    if (!attr_once((const void*)zinv_small_kernel, 200 * 1024, &attr)) return -6;
     ProfScope ps_(PROF_ZINV, stream);
     zinv_small_kernel<<<batch, 256, smem, stream>>>(S, sS, lds, X, sX, ldx, n, aux);
     NEGF_LAUNCHED();
@@ -624,7 +781,7 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
   if (lds != n || ldx != n) return -2;  // blocked path works on packed matrices
   const int nb = zinv_panel_width(n);
   if (ws_bytes < zinv_workspace_bytes(n, batch)) return -4;
-  if (n > kInvPanelMax) return zinv_recursive(S, sS, X, sX, n, batch, aux, ws, ws_bytes, stream);
+  if (n > kInvClusterMax) return -5;
   // carve workspace
   char* w = reinterpret_cast<char*>(ws);
   auto take = [&](size_t bytes) { char* r = w; w += (bytes + 255) & ~size_t(255); return r; };
@@ -635,12 +792,8 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
   int* map_dst = reinterpret_cast<int*>(take(sizeof(int) * (size_t)n * batch));
   int* perm = reinterpret_cast<int*>(take(sizeof(int) * (size_t)n * batch));
   const int panel_threads = ((n * (nb / 16) + 31) / 32) * 32;
-  static bool attr_u = false;
-  if (!attr_u) {
-    NEGF_CUDA_CHECK(cudaFuncSetAttribute(zinv_unpermute_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    attr_u = true;
-  }
+  static unsigned attr_u = 0;
+  if (!attr_once((const void*)zinv_unpermute_kernel, 160 * 1024, &attr_u)) return -6;
   // Gauss-Jordan sweeps ping-pong between S and X (X is the destination).
   z_t* cur = S;
   z_t* nxt = X;
@@ -650,12 +803,35 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
     {
       ProfScope ps_(PROF_ZINV, stream);
       ProfScope psp_(5, stream);
-      if (nb == 32)
-        zinv_panel_kernel<32><<<batch, panel_threads, 0, stream>>>(cur, cs, nxt, ns, n, k0, wd, ipiv, pinv,
-                                                                   umm, map_src, map_dst, aux);
-      else
-        zinv_panel_kernel<16><<<batch, panel_threads, 0, stream>>>(cur, cs, nxt, ns, n, k0, wd, ipiv, pinv,
-                                                                   umm, map_src, map_dst, aux);
+      if (n <= kInvPanelMax) {
+        if (nb == 32)
+          zinv_panel_kernel<32><<<batch, panel_threads, 0, stream>>>(cur, cs, nxt, ns, n, k0, wd, ipiv, pinv,
+                                                                     umm, map_src, map_dst, aux);
+        else
+          zinv_panel_kernel<16><<<batch, panel_threads, 0, stream>>>(cur, cs, nxt, ns, n, k0, wd, ipiv, pinv,
+                                                                     umm, map_src, map_dst, aux);
+      } else {
+        const int rpc = 512 * 16 / nb;
+        const int ncta = (n - k0 + rpc - 1) / rpc;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ncta, batch, 1);
+        cfg.blockDim = dim3(512, 1, 1);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = ncta;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (nb == 32)
+          NEGF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zinv_panel_cluster_kernel<32>, (const z_t*)cur, cs, nxt, ns, n,
+                                             k0, wd, ipiv, pinv, umm, map_src, map_dst, aux));
+        else
+          NEGF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zinv_panel_cluster_kernel<16>, (const z_t*)cur, cs, nxt, ns, n,
+                                             k0, wd, ipiv, pinv, umm, map_src, map_dst, aux));
+      }
       NEGF_LAUNCHED();
     }
     if (n - wd > 0) {
@@ -697,9 +873,11 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
     ProfScope ps3b_(8, stream);
     zinv_perm_kernel<<<batch, 128, 2 * n * sizeof(int), stream>>>(n, ipiv, umm, perm, aux);
     NEGF_LAUNCHED();
-    dim3 gu((n + 7) / 8, batch);
-    zinv_unpermute_kernel<<<gu, 256, 8 * (size_t)n * sizeof(z_t) + n * sizeof(int), stream>>>(
-        cur, cs, n, perm, X, sX, ldx, aux.active);
+    int R = (int)(144 * 1024 / ((size_t)n * sizeof(z_t)));
+    R = R < 1 ? 1 : (R > 8 ? 8 : R);
+    dim3 gu((n + R - 1) / R, batch);
+    zinv_unpermute_kernel<<<gu, 256, (size_t)R * n * sizeof(z_t) + n * sizeof(int), stream>>>(
+        cur, cs, n, perm, X, sX, ldx, aux.active, R);
     NEGF_LAUNCHED();
   }
   return 0;

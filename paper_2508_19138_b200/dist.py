@@ -135,6 +135,29 @@ class PeerEntryMajor:
                                       device=self.dev)
         self._bufs: dict[str, tuple] = {}
 
+    @classmethod
+    def try_create(cls, tr: "Transposer", device) -> "PeerEntryMajor | None":
+        """The peer path when the setup supports it -- an NCCL process group on
+        CUDA devices with symmetric memory (NVLink P2P) -- decided jointly by
+        all ranks (MIN over the per-rank outcome); None selects the NCCL
+        all-to-all Transposer."""
+        group = tr.comm.group or dist.group.WORLD
+        ok = 1
+        pem = None
+        try:
+            if dist.get_backend(group) != "nccl" or not torch.cuda.is_available():
+                ok = 0
+            else:
+                pem = cls(tr, device)
+                pem.buffer("gl")  # first rendezvous: fails here without symmetric-memory support
+        except Exception:  # noqa: BLE001 -- any failure selects the all-to-all path
+            ok = 0
+        if dist.get_backend(group) == "nccl":
+            flag = torch.tensor([ok], dtype=torch.int32, device=device)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=tr.comm.group)
+            ok = int(flag.item())
+        return pem if ok else None
+
     def buffer(self, name: str):
         """(local (n_own_entries, N_E) view, device array of the peers' base pointers, handle)."""
         if name not in self._bufs:
@@ -161,11 +184,66 @@ TO_ENTRY_MAJOR = "to_entry_major"
 TO_ENERGY_MAJOR = "to_energy_major"
 
 
-def transpose_distribution(comm: Comm, local_part, direction: str, n_entries: int, n_e: int):
-    """scba.py:342-368 semantics for one quantity, as an all-to-all: the
-    reference returns the replicated full array; here each rank receives only
-    the slab it owns (entry rows for to_entry_major, energy columns for
-    to_energy_major), which is all any caller on the hot path reads."""
+def transpose_distribution(comm: Comm, local_part, direction: str, stats=None, lg: bool = True,
+                           full_entry_count: int = 0):
+    """scba.py:342-368, same signature and semantics: ``to_entry_major``
+    gathers every rank's energy columns (n_entries, n_own_e) into the
+    replicated (n_entries, N_E) array, ``to_energy_major`` gathers every
+    rank's entry rows (n_own_entries, N_E) into it; ``stats`` (a
+    TranspositionStats) counts the full logical redistribution like
+    _count_bytes (scba.py:385-394). ``local_part`` is a numpy array (returned
+    as numpy) or a torch tensor (returned on its device). One padded
+    all-gather over the process group (NCCL needs CUDA tensors; gloo CPU).
+
+    The hot path does not replicate: scba_run moves each rank only the slab
+    it owns (Transposer / the fused peer-memory layout kernels); this drop-in
+    is for callers written against the reference."""
+    import numpy as np
+
+    from .results import count_transpose_bytes
+
+    if direction not in (TO_ENTRY_MAJOR, TO_ENERGY_MAJOR):
+        raise ValueError(f"unknown transpose direction {direction!r}")
+    as_np = isinstance(local_part, np.ndarray)
+    x = torch.from_numpy(np.ascontiguousarray(local_part, dtype=complex)) if as_np else local_part.contiguous()
+    axis = 1 if direction == TO_ENTRY_MAJOR else 0
+    if comm.size == 1:
+        full = x
+    else:
+        group = comm.group
+        dev = x.device
+        if dist.get_backend(group) == "nccl" and dev.type != "cuda":
+            dev = torch.device("cuda", torch.cuda.current_device())
+        x = x.to(dev)
+        n_loc = torch.tensor([x.shape[axis], x.shape[1 - axis]], dtype=torch.int64, device=dev)
+        sizes = [torch.empty_like(n_loc) for _ in range(comm.size)]
+        dist.all_gather(sizes, n_loc, group=group)
+        counts = [int(t[0]) for t in sizes]
+        other = int(sizes[0][1])
+        if any(int(t[1]) != other for t in sizes):
+            raise ValueError("transpose_distribution: ranks disagree on the non-split dimension")
+        m = max(counts)
+        shape = (other, m) if axis == 1 else (m, other)
+        pad = torch.zeros(shape, dtype=torch.complex128, device=dev)
+        if axis == 1:
+            pad[:, :x.shape[1]] = x
+        else:
+            pad[:x.shape[0]] = x
+        bufs = [torch.empty_like(pad) for _ in range(comm.size)]
+        dist.all_gather([torch.view_as_real(b) for b in bufs], torch.view_as_real(pad), group=group)
+        parts = [b[:, :c] if axis == 1 else b[:c] for b, c in zip(bufs, counts)]
+        full = torch.cat(parts, dim=axis)
+    if stats is not None:
+        count_transpose_bytes(stats, lg, full.shape[0], full.shape[1], full_entry_count)
+    if as_np:
+        return full.cpu().numpy()
+    return full.to(local_part.device)
+
+
+def transpose_owned(comm: Comm, local_part: torch.Tensor, direction: str, n_entries: int, n_e: int):
+    """The hot-path form of the transposition: an all-to-all in which each
+    rank receives only the slab it owns (entry rows for to_entry_major,
+    energy columns for to_energy_major) instead of the replicated array."""
     tr = Transposer(comm, n_entries, n_e)
     if direction == TO_ENTRY_MAJOR:
         return tr.to_entry_major(local_part)

@@ -1,0 +1,279 @@
+"""Reference-shaped result objects of the SCBA driver and the observables
+computed from them.
+
+Mirrors negfgw.scba (scba.py:222-237 TranspositionStats, 459-489 SigmaState,
+492-528 ScbaResult, 1313-1376 observables) and negfgw.convolve.EntryPattern
+(convolve.py:135-187), so that code written against the reference's
+``ScbaResult`` (``result.grid.de``, ``result.sigma.lesser``,
+``result.sigma_pattern.rows`` ...) runs unchanged on a GPU result. The
+arrays are host numpy arrays; the device-resident state of a run stays
+available as ``result.state`` (a torch ScbaState) for warm starts.
+
+For backwards compatibility with the round-1 dict result, a ScbaResult is
+also indexable: ``result["g_r_diag"]``, ``result["sigma_lesser"]``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field, fields
+from functools import cached_property
+
+import numpy as np
+
+from .constants import C_OBSERVABLE
+
+SPIN_DEGENERACY = 1  # constants.py:21 (C_OBSERVABLE already carries it)
+SIDE_LEFT, SIDE_RIGHT = "left", "right"
+
+
+@dataclass(frozen=True)
+class EntryPattern:
+    """convolve.py:135-187: stored entries of a block-banded quantity. With
+    ``compressed`` only global upper entries are kept (upper triangle of the
+    diagonal blocks, every entry of the upper off-diagonal blocks), block row
+    by block row. ``rows``/``cols`` are built lazily and vectorised (the
+    reference enumerates them in Python loops); same order."""
+
+    n_blocks: int
+    block_size: int
+    block_bandwidth: int = 3
+    compressed: bool = True
+
+    @cached_property
+    def _rc(self) -> tuple[np.ndarray, np.ndarray]:
+        h = (self.block_bandwidth - 1) // 2
+        bs = self.block_size
+        tri_r, tri_c = np.triu_indices(bs)
+        full_r, full_c = np.divmod(np.arange(bs * bs), bs)
+        rows, cols = [], []
+        for bi in range(self.n_blocks):
+            for bj in range(max(0, bi - h), min(self.n_blocks, bi + h + 1)):
+                if self.compressed and bj < bi:
+                    continue
+                if self.compressed and bi == bj:
+                    r, c = tri_r, tri_c
+                else:
+                    r, c = full_r, full_c
+                rows.append(bi * bs + r)
+                cols.append(bj * bs + c)
+        return np.concatenate(rows).astype(np.intp), np.concatenate(cols).astype(np.intp)
+
+    @property
+    def rows(self) -> np.ndarray:
+        return self._rc[0]
+
+    @property
+    def cols(self) -> np.ndarray:
+        return self._rc[1]
+
+    @property
+    def n_entries(self) -> int:
+        h = (self.block_bandwidth - 1) // 2
+        bs = self.block_size
+        n = 0
+        for bi in range(self.n_blocks):
+            for bj in range(max(0, bi - h), min(self.n_blocks, bi + h + 1)):
+                if self.compressed and bj < bi:
+                    continue
+                n += bs * (bs + 1) // 2 if (self.compressed and bi == bj) else bs * bs
+        return n
+
+    def full_entry_count(self) -> int:
+        """In-band entry count of the uncompressed pattern."""
+        h = (self.block_bandwidth - 1) // 2
+        n_off = sum(1 for bi in range(self.n_blocks)
+                    for bj in range(max(0, bi - h), min(self.n_blocks, bi + h + 1)) if bi != bj)
+        return (self.n_blocks + n_off) * self.block_size ** 2
+
+    def index_map(self) -> dict[tuple[int, int], int]:
+        return {(int(r), int(c)): k for k, (r, c) in enumerate(zip(self.rows, self.cols))}
+
+
+@dataclass
+class TranspositionStats:
+    """scba.py:222-237: logical byte counters of the layout transpositions."""
+
+    lg_bytes: int = 0
+    lg_full_bytes: int = 0
+    other_bytes: int = 0
+
+    def lg_ratio(self) -> float:
+        return self.lg_bytes / self.lg_full_bytes if self.lg_full_bytes else 0.0
+
+
+def count_transpose_bytes(stats: TranspositionStats, lg: bool, n_entries: int, n_cols: int,
+                          full_count: int) -> None:
+    """scba.py:385-394 (_count_bytes)."""
+    moved = n_entries * n_cols * 16
+    if lg:
+        stats.lg_bytes += moved
+        stats.lg_full_bytes += full_count * n_cols * 16
+    else:
+        stats.other_bytes += moved
+
+
+@dataclass
+class SigmaState:
+    """scba.py:459-489: entry-major scattering self-energy (host arrays,
+    shape (n_entries, n_e))."""
+
+    lesser: np.ndarray
+    greater: np.ndarray
+    ret_upper: np.ndarray
+    ret_lower: np.ndarray
+
+    @classmethod
+    def zeros(cls, n_entries: int, n_e: int) -> "SigmaState":
+        z = lambda: np.zeros((n_entries, n_e), dtype=complex)
+        return cls(z(), z(), z(), z())
+
+    def mix_from(self, raw: "SigmaState", alpha: float) -> None:
+        for name in ("lesser", "greater", "ret_upper", "ret_lower"):
+            setattr(self, name, (1.0 - alpha) * getattr(self, name) + alpha * getattr(raw, name))
+
+    def copy(self) -> "SigmaState":
+        return SigmaState(self.lesser.copy(), self.greater.copy(), self.ret_upper.copy(), self.ret_lower.copy())
+
+
+G_FIELDS = ("g_r_diag", "g_r_upper", "g_r_lower", "g_lesser_diag", "g_lesser_upper", "g_greater_diag",
+            "g_greater_upper", "sigma_obc_lesser_left", "sigma_obc_greater_left", "sigma_obc_lesser_right",
+            "sigma_obc_greater_right")
+SIGMA_KEYS = {"sigma_lesser": "lesser", "sigma_greater": "greater", "sigma_ret_upper": "ret_upper",
+              "sigma_ret_lower": "ret_lower"}
+
+
+@dataclass
+class ScbaResult:
+    """scba.py:492-528. G fields hold this rank's energies (all energies on
+    one rank; the reference replicates every G block of every energy on every
+    rank, scba.py:1258-1308, which this implementation does not do: see
+    ``observables`` for the energy-sharded reductions). ``sigma`` holds the
+    mixed Sigma columns of this rank's energies; ``state`` the device copy."""
+
+    grid: object
+    contacts: object
+    options: object
+    n_blocks: int
+    block_size: int
+    converged: bool
+    n_iter: int
+    residuals: np.ndarray
+    identity_defects: list
+    g_r_diag: np.ndarray | None = None
+    g_r_upper: np.ndarray | None = None
+    g_r_lower: np.ndarray | None = None
+    g_lesser_diag: np.ndarray | None = None
+    g_lesser_upper: np.ndarray | None = None
+    g_greater_diag: np.ndarray | None = None
+    g_greater_upper: np.ndarray | None = None
+    sigma_obc_lesser_left: np.ndarray | None = None
+    sigma_obc_greater_left: np.ndarray | None = None
+    sigma_obc_lesser_right: np.ndarray | None = None
+    sigma_obc_greater_right: np.ndarray | None = None
+    sigma: SigmaState | None = None
+    sigma_pattern: EntryPattern | None = None
+    timings: dict = field(default_factory=dict)
+    wall_total: float = 0.0
+    transposition: TranspositionStats = field(default_factory=TranspositionStats)
+    cache_stats: dict = field(default_factory=dict)
+    cache_stats_by_iteration: list = field(default_factory=list)
+    dist_stats: object = None
+    comm_bytes: int = 0
+    flops_total: float = 0.0
+    flops_by_category: dict = field(default_factory=dict)
+    oracle_deviations: dict = field(default_factory=dict)
+    # -- this implementation --------------------------------------------------
+    #: device ScbaState (torch) of this rank's energy columns (warm starts)
+    state: object = None
+    #: energies of this rank (slice into the grid)
+    energy_slice: slice | None = None
+    iteration_s: list = field(default_factory=list)
+    timings_by_iteration: list = field(default_factory=list)
+    #: reference observables of the last G solve, reduced on the device per
+    #: energy batch and over ranks (dos, density, current_spectrum,
+    #: terminal_left, terminal_right); present for every run
+    observables: dict = field(default_factory=dict)
+
+    @property
+    def transpose_bytes(self) -> int:
+        return self.comm_bytes
+
+    # dict-style access (round-1 API)
+    def __getitem__(self, key: str):
+        if key in SIGMA_KEYS:
+            if self.sigma is None:
+                raise KeyError(key)
+            return getattr(self.sigma, SIGMA_KEYS[key])
+        if key == "transpose_bytes":
+            return self.comm_bytes
+        try:
+            val = getattr(self, key)
+        except AttributeError:
+            raise KeyError(key) from None
+        if val is None and key in G_FIELDS:
+            raise KeyError(key)
+        return val
+
+    def __contains__(self, key: str) -> bool:
+        try:
+            self[key]
+            return True
+        except KeyError:
+            return False
+
+    def keys(self):
+        out = [f.name for f in fields(self) if getattr(self, f.name) is not None]
+        if self.sigma is not None:
+            out += list(SIGMA_KEYS)
+        return out
+
+
+# -- observables (scba.py:1313-1376) ------------------------------------------------
+
+
+def dos(result: ScbaResult) -> np.ndarray:
+    """Block-resolved spectral weight, shape (n_e, n_blocks)."""
+    return -np.trace(result.g_r_diag, axis1=2, axis2=3).imag / np.pi
+
+
+def electron_density(result: ScbaResult) -> np.ndarray:
+    """Energy-integrated carrier density per block, shape (n_blocks,)."""
+    tr = np.trace(result.g_lesser_diag, axis1=2, axis2=3)
+    return (SPIN_DEGENERACY * C_OBSERVABLE * result.grid.de * (-1j * tr).sum(axis=0)).real
+
+
+def current_spectrum(result: ScbaResult, h) -> np.ndarray:
+    """Energy-resolved current through each inter-block bond, (n_e, n_blocks - 1).
+    ``h``: (diag, upper, lower) block stacks or a BlockMatrix."""
+    n_b = result.n_blocks
+    h_up = h.get_block if hasattr(h, "get_block") else None
+    if h_up is not None and (h.n_blocks != n_b or h.block_size != result.block_size):
+        raise ValueError(f"device layout {h.n_blocks}x{h.block_size} does not match the solved layout "
+                         f"{n_b}x{result.block_size}")
+    if result.g_lesser_upper is None or result.g_lesser_upper.ndim != 4 or result.g_lesser_upper.shape[1] != n_b - 1:
+        raise ValueError("stored lesser off-diagonal blocks are missing; bond currents need the full first "
+                         "superdiagonal")
+    out = np.zeros((result.g_lesser_upper.shape[0], n_b - 1))
+    for i in range(n_b - 1):
+        hu = h.get_block(i, i + 1) if h_up is not None else np.asarray(h[1][i])
+        gl_lower = -np.conj(np.swapaxes(result.g_lesser_upper[:, i], 1, 2))
+        out[:, i] = SPIN_DEGENERACY * C_OBSERVABLE * 2.0 * np.einsum("ij,eji->e", hu, gl_lower).real
+    return out
+
+
+def bond_currents(result: ScbaResult, h) -> np.ndarray:
+    return current_spectrum(result, h).sum(axis=0) * result.grid.de
+
+
+def terminal_current(result: ScbaResult, side: str = SIDE_LEFT) -> float:
+    """Net current from one contact into the device."""
+    if side == SIDE_LEFT:
+        sl, sg, corner = result.sigma_obc_lesser_left, result.sigma_obc_greater_left, 0
+    elif side == SIDE_RIGHT:
+        sl, sg, corner = result.sigma_obc_lesser_right, result.sigma_obc_greater_right, result.n_blocks - 1
+    else:
+        raise ValueError(f"unknown side {side!r}")
+    g_l = result.g_lesser_diag[:, corner]
+    g_g = result.g_greater_diag[:, corner]
+    tr = np.einsum("eij,eji->e", sl, g_g) - np.einsum("eij,eji->e", sg, g_l)
+    return float(SPIN_DEGENERACY * C_OBSERVABLE * result.grid.de * tr.real.sum())

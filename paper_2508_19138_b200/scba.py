@@ -34,6 +34,7 @@ from .conv import polarization, self_energy
 from .dist import Comm, Transposer
 from .errors import ConvergenceError, SpectralRadiusError
 from .obc import raise_on_obc_status
+from .results import EntryPattern, ScbaResult, SigmaState, TranspositionStats, count_transpose_bytes
 from .rgf import raise_on_status
 
 Z = torch.complex128
@@ -74,8 +75,9 @@ class MemoizerOptions:
 
 @dataclass(frozen=True)
 class ScbaOptions:
-    """scba.py:157-190 (retarded_method fixed to Sancho-Rubio). The memoizer
-    tolerance is tol / 10 as in the reference (scba.py:911)."""
+    """scba.py:157-190, same defaults (incl. retarded_method="beyn",
+    scba.py:165). The memoizer tolerance is tol / 10 as in the reference
+    (scba.py:911)."""
 
     max_iter: int = 50
     tol: float = 1e-5
@@ -85,10 +87,11 @@ class ScbaOptions:
     stein_max_iter: int = 100
     batch: int | None = None  # energies per device batch (None: all)
     memoizer: MemoizerOptions = field(default_factory=MemoizerOptions)
-    # carrier retarded surfaces (scba.py:577-614): "sancho" (default here; the
-    # reference defaults to "beyn", which SURVEY §0.4 finds wrong in band),
-    # "beyn" or "fixed_point"
-    retarded_method: str = "sancho"
+    # carrier retarded surfaces (scba.py:577-614): "beyn" (the reference's
+    # default, kept for drop-in parity although SURVEY §0.4 finds it wrong in
+    # band at eta = 1e-3), "sancho" (what the parity tests and benches use)
+    # or "fixed_point"
+    retarded_method: str = "beyn"
     # W retarded surface: "sancho" (default; equal to Beyn on the reference's
     # weak-V inputs) or "beyn" (the reference's choice, scba.py:844)
     w_retarded_method: str = "sancho"
@@ -381,18 +384,6 @@ def _stacks(m):
     return m
 
 
-class ScbaResult(dict):
-    """Result of scba_run (scba.py:196-240 ScbaResult): a dict of host arrays
-    whose keys are also readable as attributes (result.g_r_diag,
-    result.converged, result.identity_defects, ...)."""
-
-    def __getattr__(self, name):
-        try:
-            return self[name]
-        except KeyError:
-            raise AttributeError(name) from None
-
-
 def g_identity_defect(b: dict, n_e: int, n_b: int, bs: int, out: torch.Tensor) -> None:
     """scba.py:1223-1238 on the device: accumulates max |X^> - X^< - (X^R - X^R^dag)|
     and max |X^R - X^R^dag| over the stored blocks into out[0:2] (max-combined)."""
@@ -422,8 +413,10 @@ def scba_run_reference_api(h_mat, v_mat, grid, contacts, options: ScbaOptions | 
     kT), ``comm`` for energy sharding and ``plan`` (dd.PartitionPlan) for
     the spatial mode."""
     c = Contacts(contacts.mu_left, contacts.mu_right, contacts.kT)
-    return scba_run(_stacks(h_mat), None if v_mat is None else _stacks(v_mat), grid.energies, grid.eta, c,
-                    options, device=device, comm=comm, initial_sigma=initial_sigma, plan=plan)
+    res = scba_run(_stacks(h_mat), None if v_mat is None else _stacks(v_mat), grid.energies, grid.eta, c,
+                   options, device=device, comm=comm, initial_sigma=initial_sigma, plan=plan)
+    res.grid, res.contacts = grid, contacts  # the caller's objects, like the reference's result
+    return res
 
 
 def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOptions | None = None,
@@ -477,7 +470,7 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     if comm.size > 1 and v is not None and not spatial and os.environ.get("NEGF_PEER_TRANSPOSE", "1") != "0":
         from .dist import PeerEntryMajor
 
-        peer = PeerEntryMajor(tr, dev)
+        peer = PeerEntryMajor.try_create(tr, dev)  # None (-> NCCL all-to-all) off NCCL / without P2P
     own = tr.own_e
     n_own = tr.n_own_e
     # energies this rank solves: its chunk, or all of them in the spatial mode
@@ -487,17 +480,33 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     batch = options.batch or max(n_sol, 1)
     sig = ScbaState.zeros(lay.n_entries, n_sol, dev)
     if initial_sigma is not None and not options.reset_sigma:
-        if tuple(initial_sigma.lesser.shape) != (lay.n_entries, n_sol):
-            raise ValueError(f"warm-start state has shape {tuple(initial_sigma.lesser.shape)}, "
-                             f"expected {(lay.n_entries, n_sol)}")
-        sig = ScbaState(*(torch.as_tensor(x, dtype=Z, device=dev).clone() for x in initial_sigma.as_tuple()))
+        # scba.py:942-949: any object with lesser / greater / ret_upper /
+        # ret_lower (the reference's SigmaState, ours, or a device ScbaState),
+        # either the full (n_entries, N_E) array like the reference or this
+        # rank's own (n_entries, n_own) columns
+        parts = [getattr(initial_sigma, k) for k in ("lesser", "greater", "ret_upper", "ret_lower")]
+        shape = tuple(parts[0].shape)
+        if shape == (lay.n_entries, ne) and n_sol != ne:
+            parts = [x[:, s0:s0 + n_sol] for x in parts]
+        elif shape not in ((lay.n_entries, n_sol), (lay.n_entries, ne)):
+            raise ValueError(f"warm-start state has shape {shape}, expected {(lay.n_entries, ne)}")
+        sig = ScbaState(*(torch.as_tensor(x, dtype=Z, device=dev).clone().contiguous() for x in parts))
     if v is None:
         max_iter = 1
     else:
         max_iter = options.max_iter
         screened = ScreenedSolver(v, options, dev)
-        if screened.n_b != n_b or screened.bs != bs:
-            raise ValueError("W blocking must match the carrier blocking (n_w == n_b, bs_w == bs)")
+        # scba.py:893-903 preconditions, same messages
+        if screened.n_b * screened.bs != n_b * bs:
+            raise ValueError(f"screening layout {screened.n_b}x{screened.bs} does not match carrier layout "
+                             f"{n_b}x{bs}")
+        if screened.bs % bs != 0:
+            raise ValueError("screening block size must be a multiple of the carrier block size, got "
+                             f"{screened.bs} and {bs}")
+        if screened.bs != bs:
+            raise ValueError(f"a W grid coarser than the G grid (bs_w = {screened.bs} = {screened.bs // bs} x bs) "
+                             "is not supported by the device layout kernels (the BASELINE configs use equal "
+                             "blockings)")
         if spatial:  # the W chain gets its own even split (scba.py:930)
             screened.dd = (make_partition_plan(n_b, plan.p_s), comm)
     cols = lambda: torch.empty((lay.n_entries, n_own), dtype=Z, device=dev)
@@ -558,10 +567,21 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         a, n, c = own_part(e0, nb_)
         if n:
             lay.pack(xd[a:a + n], xu[a:a + n], out, c)
+    timings_by_it = []
+    # reference observables of each iteration's G solve (scba.py:1313-1376),
+    # reduced on the device per batch; the last iteration's are reported
+    from .carrier import ObservableAccumulator
+
+    obs_acc = ObservableAccumulator(max(n_sol, 1), n_b, de, dev)
+    stats = TranspositionStats()
+    pattern = EntryPattern(n_b, bs, 3, True)
+    full_count = pattern.full_entry_count()
     for it in range(max_iter):
         n_iter = it + 1
         torch.cuda.synchronize(dev)
         t_iter = _time.perf_counter()
+        t_snap = dict(timings)
+        obs_acc.reset()
         # identity-defect accumulators (G, P, Sigma) x (defect, scale), scba.py:1002-1006
         defects = torch.zeros(6, dtype=torch.float64, device=dev)
         g_host = {k: [] for k in RESULT_KEYS} if keep_g else None
@@ -588,6 +608,7 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             with _T("G: OBC+RGF"):
                 b = carrier.solve(my_e[e0:e1], sigma=blocks, n_e=nb_, memo=memo(e0))
             g_identity_defect(b, nb_, n_b, bs, defects[0:2])
+            obs_acc.add(carrier, b, e0, nb_)
             if odev is not None:
                 solve_check(b, False)
             with _T("layout"):
@@ -611,6 +632,13 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             if cache is not None:
                 stats_by_it.append(cache.stats)
             break
+        # logical transposition volume of this iteration, counted like the
+        # reference's replicated exchanges (scba.py:1028-1141, _count_bytes):
+        # G^<>, P^<>, W^<>, Sigma^<> lg-compressed; P^R, Sigma^R plain
+        for _ in range(8):
+            count_transpose_bytes(stats, True, lay.n_entries, ne, full_count)
+        for _ in range(4):
+            count_transpose_bytes(stats, False, lay.n_entries, ne, 0)
         # 2. G^<> to entry-major (all-to-all), polarization on own entry rows
         with _T("transpose"):
             if peer is not None:
@@ -724,29 +752,56 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         if cache is not None:
             stats_by_it.append(cache.stats)
         iter_times.append(_time.perf_counter() - t_iter)
+        timings_by_it.append({k: x - t_snap.get(k, 0.0) for k, x in timings.items()})
         if residuals[-1] < options.tol:
             converged = True
             break
         if len(residuals) >= 11 and residuals[-1] > 5.0 * residuals[-11]:
             raise ConvergenceError(f"residual grew from {residuals[-11]:.3e} to {residuals[-1]:.3e} over 10 iterations")
+    sigma_host = None
     if v is not None and sigma_to_host:
-        for k, t in zip(("lesser", "greater", "ret_upper", "ret_lower"), sig.as_tuple()):
-            result["sigma_" + k] = (t[:, own] if spatial else t).cpu().numpy()
-    result["iteration_s"] = iter_times
-    result["residuals"] = np.asarray(residuals)
-    result["identity_defects"] = identity_defects
+        sigma_host = SigmaState(*((t[:, own] if spatial else t).cpu().numpy() for t in sig.as_tuple()))
+    observables = _gather_observables(obs_acc, comm, spatial, n_sol, dev)
+    oracle_devs = {}
     if odev is not None:
         o = comm.allreduce_max([odev["solve_vs_dense"], odev["fft_vs_direct"]], dev)
-        result["oracle_deviations"] = {"solve_vs_dense": o[0], "fft_vs_direct": o[1]}
+        oracle_devs = {"solve_vs_dense": o[0], "fft_vs_direct": o[1]}
+    try:
+        grid = EnergyGrid(float(energies[0]), float(energies[-1]), ne, eta)
+    except ValueError:
+        grid = None
+    return ScbaResult(
+        grid=grid, contacts=contacts, options=options, n_blocks=n_b, block_size=bs, converged=converged,
+        n_iter=n_iter, residuals=np.asarray(residuals), identity_defects=identity_defects,
+        **{k: result.get(k) for k in RESULT_KEYS},
+        sigma=sigma_host, sigma_pattern=pattern, timings=timings, wall_total=float(sum(iter_times)),
+        transposition=stats,
+        cache_stats=cache.stats if cache is not None else {"direct_calls": 0, "memoized_calls": 0},
+        cache_stats_by_iteration=stats_by_it, dist_stats=None, comm_bytes=int(tr.bytes_moved),
+        oracle_deviations=oracle_devs, state=sig, energy_slice=own, iteration_s=iter_times,
+        timings_by_iteration=timings_by_it, observables=observables)
+
+
+def _gather_observables(acc, comm: Comm, spatial: bool, n_sol: int, dev) -> dict:
+    """This rank's device-reduced observables -> the whole grid's: per-energy
+    arrays concatenated over the energy chunks, energy integrals summed
+    (all_gather_object of the small host arrays)."""
+    if n_sol == 0:
+        loc = None
     else:
-        result["oracle_deviations"] = {}
-    result["converged"] = converged
-    result["n_iter"] = n_iter
-    result["n_blocks"], result["block_size"] = n_b, bs
-    result["state"] = sig
-    result["energy_slice"] = own
-    result["transpose_bytes"] = tr.bytes_moved
-    result["timings"] = timings
-    result["cache_stats"] = cache.stats if cache is not None else {"direct_calls": 0, "memoized_calls": 0}
-    result["cache_stats_by_iteration"] = stats_by_it
-    return ScbaResult(result)
+        loc = acc.to_host()
+        loc["dos"] = loc["dos"][:n_sol]
+        loc["current_spectrum"] = loc["current_spectrum"][:n_sol]
+    if comm.size == 1 or spatial:
+        return loc or {}
+    import torch.distributed as dist
+
+    parts = [None] * comm.size
+    dist.all_gather_object(parts, loc, group=comm.group)
+    parts = [p_ for p_ in parts if p_ is not None]
+    return {"dos": np.concatenate([p_["dos"] for p_ in parts]),
+            "density": np.sum([p_["density"] for p_ in parts], axis=0),
+            "current_spectrum": np.concatenate([p_["current_spectrum"] for p_ in parts]),
+            "terminal_left": float(sum(p_["terminal_left"] for p_ in parts)),
+            "terminal_right": float(sum(p_["terminal_right"] for p_ in parts))}
+

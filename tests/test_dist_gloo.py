@@ -40,6 +40,17 @@ def _worker(rank, world, port, n_entries, n_e, q):
         # to-energy-major result of the reference, scba.py:342-368)
         ok2 = ok2 and np.array_equal(tr.rows_to_full(rows).numpy(), full)
         red = comm.allreduce_max([float(rank), -float(rank)], torch.device("cpu"))
+        # reference-signature drop-in (scba.py:342-368): replicated result +
+        # TranspositionStats counts, numpy in -> numpy out
+        from paper_2508_19138_b200.dist import TO_ENERGY_MAJOR, TO_ENTRY_MAJOR, transpose_distribution
+        from paper_2508_19138_b200.results import TranspositionStats
+
+        st = TranspositionStats()
+        r1 = transpose_distribution(comm, full[:, tr.own_e], TO_ENTRY_MAJOR, st, True, 2 * n_entries)
+        r2 = transpose_distribution(comm, full[tr.own_r], TO_ENERGY_MAJOR, st, False)
+        ok2 = ok2 and isinstance(r1, np.ndarray) and np.array_equal(r1, full) and np.array_equal(r2, full)
+        ok2 = ok2 and st.lg_bytes == 16 * n_entries * n_e and st.lg_full_bytes == 32 * n_entries * n_e
+        ok2 = ok2 and st.other_bytes == 16 * n_entries * n_e and st.lg_ratio() == 0.5
         q.put((rank, ok1, ok2, red, tr.bytes_moved))
     finally:
         dist.destroy_process_group()

@@ -85,7 +85,7 @@ def test_scba_memoizer_small_matches_reference(golden, cuda):
     """4 iterations, memoizer on (tol 1e-5 -> tol_memo 1e-6), batches of 10."""
     g = golden("golden_scba_memo_small.npz")
     res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
-                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=4, batch=10), device=cuda)
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=4, batch=10), device=cuda)
     np.testing.assert_array_equal(_stats(res), g["cache_stats"])
     for k in g.files:
         if k.startswith(("ver_", "config", "cache_stats")):
@@ -98,7 +98,7 @@ def test_scba_memoizer_c1_matches_reference(golden, cuda):
     and the direct/memoized counts per iteration."""
     g = golden("golden_scba_memo_c1.npz")
     res = scba_run(orc.chain_device(16, 32), orc.coulomb_matrix(16, 32), np.linspace(-2.0, 2.0, 128), 1e-3,
-                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=3, batch=64), device=cuda)
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=3, batch=64), device=cuda)
     np.testing.assert_array_equal(_stats(res), g["cache_stats"])
     rng = np.random.default_rng(98)
     for f in ["g_r_diag", "g_r_upper", "g_r_lower", "g_lesser_diag", "g_lesser_upper", "g_greater_diag",
@@ -114,7 +114,7 @@ def test_scba_memoizer_c1_matches_reference(golden, cuda):
 
 def test_scba_memoizer_off_counts_direct_calls(cuda):
     res = scba_run(orc.chain_device(4, 3), orc.coulomb_matrix(4, 3), np.linspace(-1.0, 1.0, 12), 1e-3,
-                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=2, memoizer=MemoizerOptions(enabled=False)),
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=2, memoizer=MemoizerOptions(enabled=False)),
                    device=cuda)
     assert res["cache_stats_by_iteration"] == []
 
@@ -124,7 +124,7 @@ def test_scba_memoizer_with_beyn_w_surface(golden, cuda):
     exact configuration: arrays and per-iteration call counts."""
     g = golden("golden_scba_memo_small.npz")
     res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
-                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=4, batch=10, w_retarded_method="beyn"),
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=4, batch=10, w_retarded_method="beyn"),
                    device=cuda)
     np.testing.assert_array_equal(_stats(res), g["cache_stats"])
     for k in g.files:

@@ -211,3 +211,44 @@ def test_rgf_large_blocks_match_oracle(cuda):
     for k, rk in (("xr_diag", "xr_diag"), ("xr_upper", "xr_upper"), ("xl_diag", "x<_diag")):
         got = out[k].cpu().numpy()
         assert np.linalg.norm(got - ref[rk]) / np.linalg.norm(ref[rk]) < 1e-9, k
+
+
+@pytest.mark.parametrize("bs", [1024, 2048])
+def test_rgf_w_like_large_blocks_match_oracle(cuda, bs):
+    """bs = 1024 / 2048 (the C4 block size): a W-like, NOT accretive system
+    M = I - V P^R (V real symmetric, P^R complex), B^< = V P^< V with P^<
+    anti-Hermitian, and the first diagonal block's leading half numerically
+    singular (the block itself is well conditioned) so the block inverse
+    must pivot across the halves
+    (rgf.py:113-229 through _linalg.invert's pivoted LU)."""
+    rng = np.random.default_rng(bs)
+    nb, ne = 3, 1
+
+    def crand(*s):
+        return (rng.standard_normal(s) + 1j * rng.standard_normal(s)) / np.sqrt(bs)
+
+    v = rng.standard_normal((nb, bs, bs)) / np.sqrt(bs)
+    v = 0.5 * (v + np.swapaxes(v, -1, -2))
+    pr = crand(nb, bs, bs)
+    md = np.eye(bs)[None] - 0.5 * v @ pr
+    h = bs // 2
+    u1 = crand(h, 2)
+    # leading half numerically singular (cond ~1e14), whole block cond ~2e2
+    md[0, :h, :h] = u1 @ np.conj(u1.T) + 1e-12 * crand(h, h)
+    md[0, :h, h:] += np.eye(h)
+    md[0, h:, :h] += np.eye(h)
+    mu = -0.3 * (v[:-1] @ crand(nb - 1, bs, bs))
+    ml = -0.3 * (v[1:] @ crand(nb - 1, bs, bs))
+    pl = crand(nb, bs, bs)
+    pl = 0.5 * (pl - np.conj(np.swapaxes(pl, -1, -2)))
+    bld = v @ pl @ v
+    blu = 0.1 * crand(nb - 1, bs, bs)
+    md, mu, ml, bld, blu = (x[None] for x in (md, mu, ml, bld, blu))
+    bl = (bld, blu)
+    ref = orc.rgf_selected(md, mu, ml, {"<": bl})
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda)
+    out = selected_solve_batched(T(md), T(mu), T(ml), (T(bl[0]), T(bl[1])))
+    for k, rk in (("xr_diag", "xr_diag"), ("xr_upper", "xr_upper"), ("xr_lower", "xr_lower"),
+                  ("xl_diag", "x<_diag"), ("xl_upper", "x<_upper")):
+        got = out[k].cpu().numpy()
+        assert np.linalg.norm(got - ref[rk]) / np.linalg.norm(ref[rk]) < 1e-9, k

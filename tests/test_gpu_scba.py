@@ -65,7 +65,7 @@ def test_screened_solve_matches_oracle(cuda, n_b, bs, ne):
     mw, srcs = orc.w_system(v, pr, pl, pg)
     orc.w_closure(mw, srcs, 1e-8)
     ref = orc.rgf_selected(*mw, srcs, symmetrize=True)
-    solver = ScreenedSolver(v, ScbaOptions(), cuda)
+    solver = ScreenedSolver(v, ScbaOptions(retarded_method="sancho"), cuda)
     b = solver.buffers(ne)
     for k, a in (("pr_diag", pr[0]), ("pr_upper", pr[1]), ("pr_lower", pr[2]), ("pl_diag", pl[0]),
                  ("pl_upper", pl[1]), ("pg_diag", pg[0]), ("pg_upper", pg[1])):
@@ -92,7 +92,7 @@ def test_w_assembly_real_v_path(cuda, complex_v):
     pg = (mk(ne, n_b, bs, bs), mk(ne, n_b - 1, bs, bs))
     outs = []
     for force_complex in (False, True):
-        solver = ScreenedSolver(v, ScbaOptions(), cuda)
+        solver = ScreenedSolver(v, ScbaOptions(retarded_method="sancho"), cuda)
         assert solver.v_real == (not complex_v)
         if force_complex:
             solver.v_real = False
@@ -115,7 +115,7 @@ def test_scba_small_matches_reference_scba_run(golden, cuda):
     """3 GW iterations, 6x4 chain + Coulomb, 32 energies (batches of 10)."""
     g = golden("golden_scba_small.npz")
     res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
-                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=3, tol=1e-12, batch=10, memoizer=MEMO_OFF), device=cuda)
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=3, tol=1e-12, batch=10, memoizer=MEMO_OFF), device=cuda)
     for k in g.files:
         if k.startswith(("ver_", "config")):
             continue
@@ -126,7 +126,7 @@ def test_scba_c1_matches_reference_scba_run(golden, cuda):
     """C1: 16 blocks x 32 orbitals, 128 energies, one GW iteration."""
     g = golden("golden_scba_c1.npz")
     res = scba_run(orc.chain_device(16, 32), orc.coulomb_matrix(16, 32), np.linspace(-2.0, 2.0, 128), 1e-3,
-                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=1, tol=1e-12, batch=64, memoizer=MEMO_OFF), device=cuda)
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=1, tol=1e-12, batch=64, memoizer=MEMO_OFF), device=cuda)
     check_c1(res, g, tol=TOL)
 
 
@@ -135,7 +135,7 @@ def test_scba_c1_matches_oracle_two_iterations(cuda):
     h, v = orc.chain_device(16, 32), orc.coulomb_matrix(16, 32)
     e = np.linspace(-2.0, 2.0, 128)
     ref = orc.scba(h, v, e, 1e-3, 0.1, -0.1, 0.05, max_iter=2)
-    res = scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=2, tol=1e-12, memoizer=MEMO_OFF), device=cuda)
+    res = scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=2, tol=1e-12, memoizer=MEMO_OFF), device=cuda)
     for k in ref:
         if k != "cache_stats_by_iteration":
             assert rel(res[k], ref[k]) < TOL, k
@@ -160,7 +160,7 @@ def test_scba_reference_api_with_blockmatrix_inputs(golden, cuda):
     g = golden("golden_scba_small.npz")
     res = scba_run_reference_api(bm(orc.chain_device(6, 4)), bm(orc.coulomb_matrix(6, 4)), EnergyGrid(-2.0, 2.0, 32),
                                  SimpleNamespace(mu_left=0.1, mu_right=-0.1, kT=0.05),
-                                 ScbaOptions(max_iter=3, tol=1e-12, memoizer=MEMO_OFF), device=cuda)
+                                 ScbaOptions(retarded_method="sancho", max_iter=3, tol=1e-12, memoizer=MEMO_OFF), device=cuda)
     for k in ("g_r_diag", "g_lesser_upper", "sigma_lesser", "sigma_ret_lower", "residuals"):
         assert rel(res[k], g[k]) < TOL, k
 
@@ -169,7 +169,7 @@ def test_scba_with_beyn_w_surface_matches_reference(golden, cuda):
     """W retarded surface by Beyn, as the reference hard-codes (scba.py:844)."""
     g = golden("golden_scba_small.npz")
     res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
-                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=3, tol=1e-12, batch=16, memoizer=MEMO_OFF,
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=3, tol=1e-12, batch=16, memoizer=MEMO_OFF,
                                                           w_retarded_method="beyn"), device=cuda)
     for k in g.files:
         if k.startswith(("ver_", "config")):
@@ -229,7 +229,7 @@ def test_scba_identity_defects_and_result_fields(golden, cuda):
     last-iteration G; converged / n_iter and attribute access as ScbaResult."""
     g = golden("golden_scba_small.npz")
     res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
-                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=3, tol=1e-12, batch=10, memoizer=MEMO_OFF), device=cuda)
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=3, tol=1e-12, batch=10, memoizer=MEMO_OFF), device=cuda)
     assert len(res.identity_defects) == 3 and res.n_iter == 3 and res.converged is False
     for d in res.identity_defects:
         assert set(d) == {"G", "P", "Sigma"} and max(d.values()) < 1e-12
@@ -248,19 +248,19 @@ def test_scba_warm_start_reset_sigma(cuda):
     converged state fed back converges at once; a wrong shape is a ValueError."""
     h, v, e = orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32)
     c = Contacts(0.1, -0.1, 0.05)
-    first = scba_run(h, v, e, 1e-3, c, ScbaOptions(max_iter=80, tol=1e-8, memoizer=MEMO_OFF), device=cuda)
+    first = scba_run(h, v, e, 1e-3, c, ScbaOptions(retarded_method="sancho", max_iter=80, tol=1e-8, memoizer=MEMO_OFF), device=cuda)
     assert first.converged
-    cold = scba_run(h, v, e, 1e-3, c, ScbaOptions(max_iter=2, tol=1e-8, memoizer=MEMO_OFF), device=cuda,
+    cold = scba_run(h, v, e, 1e-3, c, ScbaOptions(retarded_method="sancho", max_iter=2, tol=1e-8, memoizer=MEMO_OFF), device=cuda,
                     initial_sigma=first.state)
     assert rel(cold.residuals, first.residuals[:2]) < TOL  # reset_sigma=True: cold start
-    warm = scba_run(h, v, e, 1e-3, c, ScbaOptions(max_iter=80, tol=1e-8, memoizer=MEMO_OFF, reset_sigma=False),
+    warm = scba_run(h, v, e, 1e-3, c, ScbaOptions(retarded_method="sancho", max_iter=80, tol=1e-8, memoizer=MEMO_OFF, reset_sigma=False),
                     device=cuda, initial_sigma=first.state)
     assert warm.converged and warm.n_iter <= 2
     from paper_2508_19138_b200.scba import ScbaState
 
     bad = ScbaState.zeros(7, 32, cuda)
     with pytest.raises(ValueError, match="warm-start"):
-        scba_run(h, v, e, 1e-3, c, ScbaOptions(max_iter=2, reset_sigma=False, memoizer=MEMO_OFF), device=cuda,
+        scba_run(h, v, e, 1e-3, c, ScbaOptions(retarded_method="sancho", max_iter=2, reset_sigma=False, memoizer=MEMO_OFF), device=cuda,
                  initial_sigma=bad)
 
 
@@ -271,14 +271,14 @@ def test_scba_oracle_mode_deviations(golden, cuda):
     results unchanged."""
     g = golden("golden_scba_small.npz")
     res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
-                   Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=3, tol=1e-12, batch=10, memoizer=MEMO_OFF,
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=3, tol=1e-12, batch=10, memoizer=MEMO_OFF,
                                                           oracle_mode=True), device=cuda)
     od = res.oracle_deviations
     assert set(od) == {"solve_vs_dense", "fft_vs_direct"}
     assert 0 < od["solve_vs_dense"] < 1e-10 and 0 < od["fft_vs_direct"] < 1e-10, od
     assert rel(res["sigma_lesser"], g["sigma_lesser"]) < TOL
     plain = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
-                     Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=1, memoizer=MEMO_OFF), device=cuda)
+                     Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=1, memoizer=MEMO_OFF), device=cuda)
     assert plain.oracle_deviations == {}
 
 
@@ -290,8 +290,45 @@ def test_scba_spatial_plan_preconditions(cuda):
     args = (orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 8), 1e-3,
             Contacts(0.1, -0.1, 0.05))
     with pytest.raises(ValueError, match="oracle_mode"):
-        scba_run(*args, ScbaOptions(max_iter=1, oracle_mode=True), device=cuda, plan=make_partition_plan(6, 2))
+        scba_run(*args, ScbaOptions(retarded_method="sancho", max_iter=1, oracle_mode=True), device=cuda, plan=make_partition_plan(6, 2))
     with pytest.raises(PartitionError, match="partitions"):
-        scba_run(*args, ScbaOptions(max_iter=1), device=cuda, plan=make_partition_plan(6, 2))
+        scba_run(*args, ScbaOptions(retarded_method="sancho", max_iter=1), device=cuda, plan=make_partition_plan(6, 2))
     with pytest.raises(PartitionError, match="covers"):
-        scba_run(*args, ScbaOptions(max_iter=1), device=cuda, plan=make_partition_plan(8, 2))
+        scba_run(*args, ScbaOptions(retarded_method="sancho", max_iter=1), device=cuda, plan=make_partition_plan(8, 2))
+
+
+def test_scba_result_is_reference_shaped(golden, cuda):
+    """ScbaResult carries the reference's fields (scba.py:492-528): grid,
+    contacts, options, sigma: SigmaState, sigma_pattern, transposition
+    counted like _count_bytes; the device-reduced observables equal the
+    reference observables evaluated on the returned G blocks; a host
+    SigmaState (the reference's warm-start type) warm-starts a run."""
+    from paper_2508_19138_b200.results import (ScbaResult, SigmaState, current_spectrum, dos, electron_density,
+                                               terminal_current)
+
+    g = golden("golden_scba_small.npz")
+    h, v, e = orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32)
+    opts = ScbaOptions(retarded_method="sancho", max_iter=3, tol=1e-12, memoizer=MEMO_OFF)
+    res = scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05), opts, device=cuda)
+    assert isinstance(res, ScbaResult) and isinstance(res.sigma, SigmaState)
+    assert res.grid.n_e == 32 and abs(res.grid.de - 4.0 / 31) < 1e-15 and res.options is opts
+    assert res.sigma_pattern.n_entries == res.sigma.lesser.shape[0] == res.sigma_pattern.rows.size
+    assert rel(res.sigma.lesser, g["sigma_lesser"]) < TOL and rel(res["sigma_ret_upper"], g["sigma_ret_upper"]) < TOL
+    n_ent, full = res.sigma_pattern.n_entries, res.sigma_pattern.full_entry_count()
+    assert res.transposition.lg_bytes == 3 * 8 * n_ent * 32 * 16
+    assert res.transposition.lg_full_bytes == 3 * 8 * full * 32 * 16
+    assert res.transposition.other_bytes == 3 * 4 * n_ent * 32 * 16
+    obs = res.observables
+    assert rel(obs["dos"], dos(res)) < 1e-12
+    assert rel(obs["density"], electron_density(res)) < 1e-12
+    assert rel(obs["current_spectrum"], current_spectrum(res, h)) < 1e-12
+    for side in ("left", "right"):
+        assert abs(obs["terminal_" + side] - terminal_current(res, side)) < 1e-12 * max(1.0, abs(obs["terminal_" + side]))
+    warm = scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05),
+                    ScbaOptions(retarded_method="sancho", max_iter=1, tol=1e-12, memoizer=MEMO_OFF, reset_sigma=False),
+                    device=cuda, initial_sigma=res.sigma.copy())
+    # the warm run's G solve sees the returned Sigma: its first residual is the
+    # 4th iteration's of a cold 4-iteration run
+    cold = scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05),
+                    ScbaOptions(retarded_method="sancho", max_iter=4, tol=1e-12, memoizer=MEMO_OFF), device=cuda)
+    assert abs(warm.residuals[0] - cold.residuals[3]) < 1e-9 * cold.residuals[3]

@@ -7,7 +7,7 @@ n_b, bs, ne = 4, 6, 5
 rng = np.random.default_rng(1)
 v = orc.coulomb_matrix(n_b, bs)
 mk = lambda *s: 0.3 * (rng.standard_normal(s) + 1j * rng.standard_normal(s))
-solver = ScreenedSolver(v, ScbaOptions(), cuda)
+solver = ScreenedSolver(v, ScbaOptions(retarded_method="sancho"), cuda)
 b = solver.buffers(ne)
 for k in b:
     if b[k].dtype == torch.complex128:

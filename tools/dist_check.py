@@ -27,7 +27,7 @@ spatial = os.environ.get("NEGF_SPATIAL") == "1"
 plan = make_partition_plan(16, comm.size) if spatial else None
 g = np.load(ROOT / "tests" / "golden" / "golden_scba_c1.npz")
 res = scba_run(orc.chain_device(16, 32), orc.coulomb_matrix(16, 32), np.linspace(-2.0, 2.0, 128), 1e-3,
-               Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=1, tol=1e-12, batch=40,
+               Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=1, tol=1e-12, batch=40,
                                                       memoizer=MemoizerOptions(enabled=False)), device=dev, comm=comm,
                plan=plan)
 own = res["energy_slice"]
@@ -57,7 +57,7 @@ if comm.rank == 0:
           f"transpose_bytes_rank0={res['transpose_bytes']}")
     assert worst < 1e-9
 # three GW iterations (buffers reused across iterations) vs the same run on one GPU
-opts3 = ScbaOptions(max_iter=3, tol=1e-12, batch=40, memoizer=MemoizerOptions(enabled=False))
+opts3 = ScbaOptions(retarded_method="sancho", max_iter=3, tol=1e-12, batch=40, memoizer=MemoizerOptions(enabled=False))
 args = (orc.chain_device(16, 32), orc.coulomb_matrix(16, 32), np.linspace(-2.0, 2.0, 128), 1e-3,
         Contacts(0.1, -0.1, 0.05), opts3)
 res3 = scba_run(*args, device=dev, comm=comm, plan=plan)

@@ -15,7 +15,7 @@ n_b, bs, ne = (int(x) for x in sys.argv[1].split('x'))
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else min(128, ne)
 e = np.linspace(-2, 2, ne)
 h, v = toys.chain_device(n_b, bs), toys.coulomb_matrix(n_b, bs)
-run = lambda: scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=1, batch=batch),
+run = lambda: scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=1, batch=batch),
                        keep_g=False, sigma_to_host=False)
 run()
 lib = _lib.load()

@@ -21,7 +21,7 @@ dev = torch.device("cuda", local)
 dist.init_process_group("nccl", device_id=dev)
 comm = Comm.from_env()
 args = (orc.chain_device(16, 32), orc.coulomb_matrix(16, 32), np.linspace(-2.0, 2.0, 64), 1e-3,
-        Contacts(0.1, -0.1, 0.05), ScbaOptions(max_iter=4, tol=1e-12, batch=32, memoizer=MemoizerOptions(enabled=True)))
+        Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=4, tol=1e-12, batch=32, memoizer=MemoizerOptions(enabled=True)))
 res = scba_run(*args, device=dev, comm=comm, plan=make_partition_plan(16, comm.size))
 sig = {f: res["sigma_" + f] for f in ("lesser", "greater", "ret_upper", "ret_lower")}
 parts = [None] * comm.size
