@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--cpu-procs", type=int, default=0, help="0 = all host cores")
     ap.add_argument("--scgw", default="64x512x16", help="n_blocks x block_size x energies-per-rank of the "
                     "SCGW-iteration rate (default: the BASELINE configs[2] C3 device; '' to skip)")
+    ap.add_argument("--scgw-batch", type=int, default=8, help="energies per device batch of the SCGW leg")
     ap.add_argument("--c4", default="40x2048x2", help="n_blocks x block_size x energies-per-rank of the "
                     "NRFET-scale (BASELINE configs[3]) G+W RGF-phase rate ('' to skip)")
     return ap.parse_args()
@@ -366,16 +367,26 @@ def run_native(args):
         _lib._WS.clear()
         torch.cuda.empty_cache()
 
-    scgw = run_scgw(args, dev, world, rank, barrier) if args.scgw else None
-    conv_rf = conv_roofline(dev) if rank == 0 else None
-    c4 = None
-    if args.c4:
-        try:
-            c4 = run_gw_rate(args.c4, 1, dev, world, rank, barrier, "C4 NRFET-scale shape (BASELINE configs[3] device)")
-        except torch.OutOfMemoryError as exc:  # reported, not fatal: the headline is C2
-            c4 = {"error": f"out of memory: {str(exc).splitlines()[0]}"}
+    import gc
+
+    def release():
+        gc.collect()  # scba_run's closures form reference cycles over its device buffers
         _lib._WS.clear()
         torch.cuda.empty_cache()
+
+    release()
+    c4 = None
+    if args.c4:  # first of the GW legs: it needs nearly the whole 180 GB
+        try:
+            c4 = run_gw_rate(args.c4, 1, dev, world, rank, barrier, "C4 NRFET-scale shape (BASELINE configs[3] device)",
+                             peak=peak)
+        except torch.OutOfMemoryError as exc:  # reported, not fatal: the headline is C2
+            c4 = {"error": f"out of memory: {str(exc).splitlines()[0]}"}
+        release()
+    scgw = run_scgw(args, dev, world, rank, barrier, peak) if args.scgw else None
+    release()
+    conv_rf = conv_roofline(dev) if rank == 0 else None
+    release()
 
     # CPU baseline: oracle port on this host's cores (rank 0, N=1 only)
     cpu = None
@@ -447,7 +458,8 @@ def run_native(args):
         dist.destroy_process_group()
 
 
-def run_gw_rate(spec: str, batch: int | None, dev, world, rank, barrier, label: str, profile_layout: bool = False) -> dict:
+def run_gw_rate(spec: str, batch: int | None, dev, world, rank, barrier, label: str, profile_layout: bool = False,
+                peak: float | None = None) -> dict:
     """GW iterations (carrier solve + OBC, polarization, W assembly + closure
     + RGF, self-energy, mixing) on ``spec`` = "n_blocks x block_size x
     energies-per-rank", energy-sharded over the ranks (weak scaling), OBC
@@ -493,6 +505,11 @@ def run_gw_rate(spec: str, batch: int | None, dev, world, rank, barrier, label: 
            "rgf_tflops_model_G_incl_obc": f / t_g / 1e12 if t_g else None,
            "rgf_tflops_model_W_rgf": f / t_w / 1e12 if t_w else None,
            "rgf_tflops_model_GW_iteration": 2 * f / dt / 1e12,
+           # executed: 27 n_b - 23 products + n_b inversions, 8 bs^3 each, per energy and subsystem
+           "rgf_tflops_executed_W_rgf": 8.0 * bs ** 3 * (28 * n_b - 23) * ne_rank * world / t_w / 1e12 if t_w else None,
+           "fp64_peak_tflops": peak,
+           "rgf_executed_frac_of_peak_W_rgf": (8.0 * bs ** 3 * (28 * n_b - 23) * ne_rank * world / t_w / 1e12 / peak)
+           if (t_w and peak) else None,
            "model": "F_RGF = 8 bs^3 (38 n_b - 33) per energy per subsystem (SURVEY §8(d)); this implementation "
                     "executes 27 n_b - 23 products + n_b inversions of 8 bs^3, i.e. fewer flops than the model",
            "max_mem_gb_rank0": torch.cuda.max_memory_allocated(dev) / 1e9,
@@ -525,9 +542,9 @@ def run_gw_rate(spec: str, batch: int | None, dev, world, rank, barrier, label: 
     return out
 
 
-def run_scgw(args, dev, world, rank, barrier) -> dict:
-    return run_gw_rate(args.scgw, None, dev, world, rank, barrier, "C3 shape (BASELINE configs[2] device)",
-                       profile_layout=True)
+def run_scgw(args, dev, world, rank, barrier, peak=None) -> dict:
+    return run_gw_rate(args.scgw, args.scgw_batch, dev, world, rank, barrier, "C3 shape (BASELINE configs[2] device)",
+                       profile_layout=True, peak=peak)
 
 
 def conv_roofline(dev, n_rows: int = 1 << 17, lengths=(512, 2048, 4096)) -> dict:

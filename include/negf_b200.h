@@ -320,6 +320,25 @@ int negf_unpack_retarded(int n_e, int n_b, int bs, const int* tri_q, const void*
                          const void* in_lower, long long ld, int e0, void* x_diag, void* x_upper,
                          void* x_lower, void* stream);
 
+/* Table-driven layout for patterns / blockings other than the reference's
+ * full compressed band on the stacks' own blocking: the paper's r_cut
+ * nonzero subset of the band and the coarser W grid
+ * bs_w = k bs of scba_run (scba.py:893-937: P scattered from the G pattern
+ * into W blocks by _scatter_groups(pat_g, bs_w), W read back at G-pattern
+ * coordinates through w_to_g). Entry t (of n_entries, any subset of the
+ * compressed band in EntryPattern order) lives in block row bi = code[t] >> 1
+ * of the diagonal (code & 1 == 0) or upper (== 1) stack of n_bt blocks of
+ * bs_t orbitals, at flat offset q[t] = r bs_t + c; code and q are device
+ * int32 arrays. Same mirror / write-order rules as negf_unpack_lg and
+ * negf_unpack_retarded (retarded != 0). zero_fill != 0 clears the target
+ * stacks first (entries outside the pattern are zero, like the reference's
+ * zero-initialised scatter buffers). */
+int negf_pack_lg_table(int n_e, long long n_entries, int n_bt, int bs_t, const int* code, const int* q,
+                       const void* x_diag, const void* x_upper, void* out, long long ld, int e0, void* stream);
+int negf_unpack_table(int n_e, long long n_entries, int n_bt, int bs_t, const int* code, const int* q,
+                      int retarded, const void* in_upper, const void* in_lower, long long ld, int e0,
+                      void* x_diag, void* x_upper, void* x_lower, int zero_fill, void* stream);
+
 /* ---- (5) screened interaction W (scba.py:784-858) ------------------------
  * Assembly for n_e energies: M_W = I - trunc3(V P^R), B^<> = trunc3((V P^<>) V).
  * V blocks are energy independent (v_diag [n_b], v_upper/v_lower [n_b-1]);

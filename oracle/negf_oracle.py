@@ -975,18 +975,25 @@ def w_closure(m, srcs, surface_tol, cache: SurfaceCache | None = None, tol_memo:
 
 
 def scba(h, v, energies, eta, mu_left, mu_right, kT, max_iter=1, tol=1e-12, mixing=0.3,
-         surface_tol=1e-8, memoizer: tuple[int, int] | None = None):
+         surface_tol=1e-8, memoizer: tuple[int, int] | None = None, entry_cutoff: int | None = None):
     """scba_run(retarded_method='sancho', W surface by Sancho). ``memoizer``
     = (n_fpi_retarded, n_fpi_lg) enables the OBC memoizer with tol/10
     (scba.py:906-911); None = memoizer off. Returns the ScbaResult arrays (G
     at the start of the last iteration, mixed Sigma after it), 'residuals'
-    and 'cache_stats_by_iteration'."""
+    and 'cache_stats_by_iteration'.
+
+    ``entry_cutoff`` (NOT in the reference: the paper's r_cut nonzero set,
+    PAPER.md:176, 207, the deviation ScbaOptions.entry_cutoff implements):
+    G^<> and W^<> entries with |row - col| > entry_cutoff are zeroed after
+    every gather, which makes P and Sigma vanish there too -- the same
+    numbers as a computation on the restricted entry set."""
     energies = np.asarray(energies, dtype=float)
     ne = len(energies)
     de = (energies[-1] - energies[0]) / (ne - 1)
     n_b, bs = h[0].shape[0], h[0].shape[-1]
     rows, cols = entry_pattern(n_b, bs)
     diag_mask = rows == cols
+    drop = np.abs(rows - cols) > entry_cutoff if entry_cutoff is not None else np.zeros(rows.shape, bool)
     trace_idx = [np.flatnonzero(diag_mask & (rows // bs == b)) for b in range(n_b)]
     n_ent = len(rows)
     sig = {k: np.zeros((n_ent, ne), complex) for k in ("lesser", "greater", "ret_upper", "ret_lower")}
@@ -1011,6 +1018,8 @@ def scba(h, v, energies, eta, mu_left, mu_right, kT, max_iter=1, tol=1e-12, mixi
         }
         gl = gather_entries(sol["x<_diag"], sol["x<_upper"])
         gg = gather_entries(sol["x>_diag"], sol["x>_upper"])
+        gl[drop] = 0.0
+        gg[drop] = 0.0
         pl, pg, pru, prl = polarization(gl, gg, diag_mask, de)
         pr = scatter_retarded(pru, prl, n_b, bs)
         mw, srcs = w_system(v, pr, scatter_lg(pl, n_b, bs), scatter_lg(pg, n_b, bs))
@@ -1018,6 +1027,8 @@ def scba(h, v, energies, eta, mu_left, mu_right, kT, max_iter=1, tol=1e-12, mixi
         wsol = rgf_selected(*mw, srcs, symmetrize=True)
         wl = gather_entries(wsol["x<_diag"], wsol["x<_upper"])
         wg = gather_entries(wsol["x>_diag"], wsol["x>_upper"])
+        wl[drop] = 0.0
+        wg[drop] = 0.0
         raw = dict(zip(("lesser", "greater", "ret_upper", "ret_lower"), self_energy(gl, gg, wl, wg, diag_mask, de)))
         tr_old = {k: np.stack([sig[k][idx].sum(0) for idx in trace_idx]) for k in ("lesser", "greater")}
         for k in sig:

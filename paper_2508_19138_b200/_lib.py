@@ -73,6 +73,8 @@ _SIGNATURES: dict[str, tuple] = {
     "negf_pack_lg": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _ll, _i, _vp]),
     "negf_unpack_lg": (_i, [_i, _i, _i, _vp, _vp, _ll, _i, _vp, _vp, _vp]),
     "negf_unpack_retarded": (_i, [_i, _i, _i, _vp, _vp, _vp, _ll, _i, _vp, _vp, _vp, _vp]),
+    "negf_pack_lg_table": (_i, [_i, _ll, _i, _i, _vp, _vp, _vp, _vp, _vp, _ll, _i, _vp]),
+    "negf_unpack_table": (_i, [_i, _ll, _i, _i, _vp, _vp, _i, _vp, _vp, _ll, _i, _vp, _vp, _vp, _i, _vp]),
     "negf_w_assemble_workspace_bytes": (_sz, [_i, _i, _i]),
     "negf_w_assemble": (_i, [_i, _i, _i] + [_vp] * 17 + [_i, _vp, _sz, _vp]),
     "negf_w_obc_workspace_bytes": (_sz, [_i, _i]),

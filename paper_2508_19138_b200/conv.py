@@ -66,11 +66,16 @@ class ConvPlan:
         return _PLANS[key]
 
 
-# Longest circular grid of the shared-memory FFT engine (conv.cu: two
-# L-point complex arrays per row in one CTA). Series with 2 N_E - 1 > 4096
-# (N_E > 2048, C4's 4096 energies) run the same algebra through cuFFT
-# (torch.fft on the device), in row chunks.
-MAX_L_NATIVE = int(__import__("os").environ.get("NEGF_CONV_MAX_L", "4096"))  # env: tests of the cuFFT leg
+# Longest circular grid of the fused P / Sigma kernels: 4096 on one CTA (two
+# L-point complex arrays per row in shared memory), 8192 (N_E <= 4096, C4's
+# 4096 energies) on a cluster pair of CTAs splitting the even / odd bins
+# (conv.cu pol_kernel_x2 / sigma_kernel_x2). The reference-signature drop-ins
+# convolve_energy / retarded_from_lg run the one-CTA engine up to 4096. Longer
+# series (beyond every BASELINE config) run the same algebra through cuFFT
+# (torch.fft on the device) in row chunks.
+_MAX_L_ENV = int(__import__("os").environ.get("NEGF_CONV_MAX_L", "8192"))  # env: tests of the cuFFT leg
+MAX_L_NATIVE = _MAX_L_ENV
+MAX_L_GENERIC = min(_MAX_L_ENV, 4096)
 _CHUNK_BYTES = 1 << 30
 
 
@@ -201,7 +206,7 @@ def convolve_energy(x1, x2, mode: str, prefactor: complex, de: float):
     plan = ConvPlan.get(n, a.device)
     out = torch.empty_like(a)
     sc = complex(prefactor) * de
-    if plan.L > MAX_L_NATIVE:
+    if plan.L > MAX_L_GENERIC:
         a2, b2, o2 = a.reshape(-1, n), b.reshape(-1, n), out.reshape(-1, n)
         for s in _chunks(a2.shape[0], plan.L):
             y = b2[s] if mode == MODE_CONVOLUTION else torch.roll(torch.flip(
@@ -225,7 +230,7 @@ def retarded_from_lg(x_lesser, x_greater):
     n = a.shape[-1]
     plan = ConvPlan.get(n, a.device)
     out = torch.empty_like(a)
-    if plan.L > MAX_L_NATIVE:
+    if plan.L > MAX_L_GENERIC:
         a2, b2, o2 = a.reshape(-1, n), b.reshape(-1, n), out.reshape(-1, n)
         for s in _chunks(a2.shape[0], plan.L):
             _retarded_tail_fft(b2[s] - a2[s], plan, o2[s], None)

@@ -25,6 +25,9 @@
 #include "common.cuh"
 #include "prof.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace negf {
 namespace {
 
@@ -141,6 +144,7 @@ template <int E>
 struct RowGeom {
   int L, Q;    // Q = L/E threads carry data
   int pE, rs;  // radix-E passes, small radix (0 or 2 .. E/2)
+  int tws;     // stride of the twiddle table (2: the L/2-point engine of the cluster kernels reads the L table)
   int t;
   int sub;     // row slot within the CTA
   bool act;
@@ -156,6 +160,7 @@ __device__ __forceinline__ RowGeom<E> row_geom(int L, long long n_rows, long lon
   g.pE = m / lg;
   g.rs = (m % lg) ? (1 << (m % lg)) : 0;
   const int rpc = rows_per_cta(L, E);
+  g.tws = 1;
   g.t = rpc > 1 ? threadIdx.x % g.Q : threadIdx.x;
   g.sub = rpc > 1 ? threadIdx.x / g.Q : 0;
   row = (long long)blockIdx.x * rpc + g.sub;
@@ -175,7 +180,7 @@ __device__ __forceinline__ void pass_compute(z_t (*v)[E], const RowGeom<E>& g, i
     if (Ns > 1) {
       // one table twiddle per butterfly, its powers by multiplication (the
       // L1/shared pipe, not FP64, bounds these kernels)
-      const int step = k * (g.L / (Ns * R));
+      const int step = k * (g.L / (Ns * R)) * g.tws;
       z_t w1 = __ldg(&tw[step]);
       if (INV) w1 = zconj(w1);
       z_t w = w1;
@@ -398,6 +403,236 @@ __global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? 3 : MAXT == 256 ? 2 : 1
   retarded_tail<E>(v[1], A, B, g, n, tw, kf, kcf, sr_up ? sr_up + o : nullptr, sr_lo ? sr_lo + o : nullptr);
 }
 
+// ---------------------------------------------------------------------------
+// N_E in (2048, 4096] (C4's 4096 energies): circular grid L = 8192, split
+// over a CLUSTER OF TWO CTAs (one per SM, distributed shared memory), each
+// running the L/2-point engine above. A zero-padded length-L transform is two
+// length-M = L/2 transforms, of x and of x w^j (w = e^{-2 pi i / L}): the
+// even and the odd frequency bins. The pointwise spectral products act bin by
+// bin, so CTA h (= cluster rank) owns the bins of parity h end to end:
+//   forward M-point transforms of x w^{h j} -> product -> inverse -> Y_h,
+// and the length-L inverse comes back as
+//   L y[j] = Y_0[j mod M] + e^{+2 pi i j / L} Y_1[j mod M],
+// each CTA reading its peer's Y through DSMEM and writing half of the outputs.
+// The difference series d feeding the causal (retarded) kernel is exchanged
+// the same way, and the kernel spectra are read at bins 2q + h. HBM traffic is
+// that of the one-CTA kernels (each CTA reads the whole input row; the peer's
+// read of the same row is served by L2).
+
+template <int E>
+__device__ __forceinline__ RowGeom<E> geom_x2(int M) {
+  constexpr int lg = E == 16 ? 4 : 3;
+  RowGeom<E> g;
+  g.L = M;
+  g.Q = M / E;
+  const int m = 31 - __clz(M);
+  g.pE = m / lg;
+  g.rs = (m % lg) ? (1 << (m % lg)) : 0;
+  g.tws = 2;
+  g.t = threadIdx.x;
+  g.sub = 0;
+  g.act = true;
+  return g;
+}
+
+// L y[k] (and L y[-k mod L] when REV) from the two CTAs' inverse halves
+// Ye (bins of parity 0) / Yo (parity 1), k < M.
+__device__ __forceinline__ z_t combine_x2(const z_t* Ye, const z_t* Yo, int k, z_t wk) {
+  return zadd(Ye[pidx(k)], zmul(zconj(wk), Yo[pidx(k)]));
+}
+__device__ __forceinline__ z_t combine_x2_rev(const z_t* Ye, const z_t* Yo, int k, int M, z_t wk) {
+  const int km = (M - k) & (M - 1);
+  return zadd(Ye[pidx(km)], zmul(wk, Yo[pidx(km)]));
+}
+
+// Causal tail on the split grid: d (length M, zero beyond n) sits in this
+// CTA's B; r_up = K*d, r_lo = -conj(conj(K)*d) for this CTA's output half.
+template <int E>
+__device__ void retarded_tail_x2(cg::cluster_group& cl, int h, z_t* A, z_t* B, const RowGeom<E>& g, int n, int L,
+                                 const z_t* __restrict__ tw, const z_t* __restrict__ kf,
+                                 const z_t* __restrict__ kcf, z_t* r_up, z_t* r_lo) {
+  z_t dv[1][E];
+#pragma unroll
+  for (int s = 0; s < E; ++s) {
+    const int j = g.t + s * g.Q;
+    const z_t x = B[pidx(j)];
+    dv[0][s] = h ? zmul(x, __ldg(&tw[j])) : x;
+  }
+  z_t* sA[1] = {A};
+  fft_rows<false, E, 1>(dv, sA, g, tw);
+  z_t xy[2][E];
+#pragma unroll
+  for (int s = 0; s < E; ++s) {
+    const int q = 2 * (g.t + s * g.Q) + h;
+    xy[0][s] = zmul(dv[0][s], __ldg(&kf[q]));
+    xy[1][s] = kcf ? zmul(dv[0][s], __ldg(&kcf[q])) : make_double2(0.0, 0.0);
+  }
+  z_t* sAB[2] = {A, B};
+  fft_rows<true, E, 2>(xy, sAB, g, tw);
+#pragma unroll
+  for (int s = 0; s < E; ++s) {
+    const int j = g.t + s * g.Q;
+    A[pidx(j)] = xy[0][s];
+    B[pidx(j)] = xy[1][s];
+  }
+  cl.sync();
+  const int M = g.L;
+  const z_t* Ar = cl.map_shared_rank(A, h ^ 1);
+  const z_t* Br = cl.map_shared_rank(B, h ^ 1);
+  const z_t *Ue = h ? Ar : A, *Uo = h ? A : Ar, *Le = h ? Br : B, *Lo = h ? B : Br;
+  const double inv = 1.0 / L;
+#pragma unroll
+  for (int si = 0; si < E / 2; ++si) {
+    const int k = g.t + (h * (E / 2) + si) * g.Q;
+    if (k < n) {
+      const z_t wk = __ldg(&tw[k]);
+      if (r_up) r_up[k] = zscale(inv, combine_x2(Ue, Uo, k, wk));
+      if (r_lo) r_lo[k] = zscale(-inv, zconj(combine_x2(Le, Lo, k, wk)));
+    }
+  }
+  (void)M;
+  cl.sync();  // the peer may still read this CTA's A / B
+}
+
+template <int E>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
+    pol_kernel_x2(const z_t* __restrict__ gl, const z_t* __restrict__ gg, int n, int L, const z_t* __restrict__ tw,
+                  const z_t* __restrict__ kf, const z_t* __restrict__ kcf, const unsigned char* __restrict__ diag,
+                  double2 scale, z_t* pl, z_t* pg, z_t* pr_up, z_t* pr_lo, long long n_rows) {
+  extern __shared__ __align__(16) z_t sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int h = (int)cl.block_rank();
+  const long long row = blockIdx.x >> 1;
+  const int M = L >> 1;
+  const RowGeom<E> g = geom_x2<E>(M);
+  z_t* A = sm;
+  z_t* B = sm + pidx(M);
+  const long long o = row * n;
+  const bool dg = diag && diag[row];
+  z_t v[2][E];
+#pragma unroll
+  for (int s = 0; s < E; ++s) {
+    const int j = g.t + s * g.Q;
+    z_t a = make_double2(0.0, 0.0), b = a;
+    if (j < n) {
+      a = gl[o + j];
+      b = gg[o + j];
+      if (h) {
+        const z_t w = __ldg(&tw[j]);
+        a = zmul(a, w);
+        b = zmul(b, w);
+      }
+    }
+    v[0][s] = a;
+    v[1][s] = b;
+  }
+  z_t* sAB[2] = {A, B};
+  fft_rows<false, E, 2>(v, sAB, g, tw);
+#pragma unroll
+  for (int s = 0; s < E; ++s) v[0][s] = zmul(v[0][s], make_double2(-v[1][s].x, v[1][s].y));  // * (-conj G^>)
+  z_t* sA[1] = {A};
+  fft_rows<true, E, 1>(v, sA, g, tw);
+#pragma unroll
+  for (int s = 0; s < E; ++s) A[pidx(g.t + s * g.Q)] = v[0][s];
+  cl.sync();
+  const z_t* Ar = cl.map_shared_rank(A, h ^ 1);
+  z_t* Br = cl.map_shared_rank(B, h ^ 1);
+  const z_t *Ye = h ? Ar : A, *Yo = h ? A : Ar;
+  const z_t sc = zscale(1.0 / L, scale);
+#pragma unroll
+  for (int si = 0; si < E / 2; ++si) {
+    const int k = g.t + (h * (E / 2) + si) * g.Q;
+    z_t d = make_double2(0.0, 0.0);
+    if (k < n) {
+      const z_t wk = __ldg(&tw[k]);
+      const z_t lo = proj(zmul(sc, combine_x2(Ye, Yo, k, wk)), dg);
+      const z_t gr = proj(zmul(sc, zconj(combine_x2_rev(Ye, Yo, k, M, wk))), dg);
+      pl[o + k] = lo;
+      pg[o + k] = gr;
+      d = zsub(gr, lo);
+    }
+    B[pidx(k)] = d;  // both CTAs need the whole difference series
+    Br[pidx(k)] = d;
+  }
+  cl.sync();
+  retarded_tail_x2<E>(cl, h, A, B, g, n, L, tw, kf, kcf, pr_up ? pr_up + o : nullptr, pr_lo ? pr_lo + o : nullptr);
+}
+
+template <int E>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
+    sigma_kernel_x2(const z_t* __restrict__ gl, const z_t* __restrict__ gg, const z_t* __restrict__ wl,
+                    const z_t* __restrict__ wg, const long long* __restrict__ w_rows, int n, int L,
+                    const z_t* __restrict__ tw, const z_t* __restrict__ kf, const z_t* __restrict__ kcf,
+                    const unsigned char* __restrict__ diag, double2 scale, z_t* sl, z_t* sg, z_t* sr_up, z_t* sr_lo,
+                    long long n_rows) {
+  extern __shared__ __align__(16) z_t sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int h = (int)cl.block_rank();
+  const long long row = blockIdx.x >> 1;
+  const int M = L >> 1;
+  const RowGeom<E> g = geom_x2<E>(M);
+  z_t* A = sm;
+  z_t* B = sm + pidx(M);
+  const long long o = row * n;
+  const long long ow = (w_rows ? w_rows[row] : row) * n;
+  const bool dg = diag && diag[row];
+  const z_t sc = zscale(1.0 / L, scale);
+  const z_t* Ar = cl.map_shared_rank(A, h ^ 1);
+  z_t* Br = cl.map_shared_rank(B, h ^ 1);
+  const z_t *Ye = h ? Ar : A, *Yo = h ? A : Ar;
+  z_t* sAB[2] = {A, B};
+  z_t* sA[1] = {A};
+  z_t s_less[E / 2];
+  z_t v[2][E];
+#pragma unroll 1
+  for (int kind = 0; kind < 2; ++kind) {
+    const z_t* gx = kind ? gg : gl;
+    const z_t* wx = kind ? wg : wl;
+    z_t* out = kind ? sg : sl;
+#pragma unroll
+    for (int s = 0; s < E; ++s) {
+      const int j = g.t + s * g.Q;
+      z_t a = make_double2(0.0, 0.0), b = a;
+      if (j < n) {
+        a = gx[o + j];
+        b = wx[ow + j];
+        if (h) {
+          const z_t w = __ldg(&tw[j]);
+          a = zmul(a, w);
+          b = zmul(b, w);
+        }
+      }
+      v[0][s] = a;
+      v[1][s] = b;
+    }
+    fft_rows<false, E, 2>(v, sAB, g, tw);
+#pragma unroll
+    for (int s = 0; s < E; ++s) v[0][s] = zmul(v[0][s], v[1][s]);
+    fft_rows<true, E, 1>(v, sA, g, tw);
+#pragma unroll
+    for (int s = 0; s < E; ++s) A[pidx(g.t + s * g.Q)] = v[0][s];
+    cl.sync();
+#pragma unroll
+    for (int si = 0; si < E / 2; ++si) {
+      const int k = g.t + (h * (E / 2) + si) * g.Q;
+      z_t val = make_double2(0.0, 0.0);
+      if (k < n) {
+        val = proj(zmul(sc, combine_x2(Ye, Yo, k, __ldg(&tw[k]))), dg);
+        out[o + k] = val;
+      }
+      if (kind == 0) {
+        s_less[si] = val;
+      } else {
+        const z_t d = zsub(val, s_less[si]);
+        B[pidx(k)] = d;
+        Br[pidx(k)] = d;
+      }
+    }
+    cl.sync();  // the peer is done reading this CTA's A before it is rewritten
+  }
+  retarded_tail_x2<E>(cl, h, A, B, g, n, L, tw, kf, kcf, sr_up ? sr_up + o : nullptr, sr_lo ? sr_lo + o : nullptr);
+}
+
 // Generic convolve_energy (convolve.py:39-71): mode 0 convolution, 1 correlation.
 template <int E, int MAXT>
 __global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? 3 : MAXT == 256 ? 2 : 1) conv_kernel(const z_t* __restrict__ x1, const z_t* __restrict__ x2, int n,
@@ -474,6 +709,18 @@ int smem_setup(const void* fn, int L) {
 
 bool pow2(int L) { return L >= 8 && (L & (L - 1)) == 0; }
 
+constexpr int kMaxL1 = 4096;  // longest grid of the one-CTA engine; 2 kMaxL1 runs on a cluster pair
+size_t smem_x2(int L) { return 2 * (size_t)((L / 2) + (L / 2) / 8) * sizeof(z_t); }
+bool attr_x2(const void* fn, unsigned* done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 32) return false;
+  if (__atomic_load_n(done, __ATOMIC_ACQUIRE) & (1u << dev)) return true;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x2(2 * kMaxL1)) != cudaSuccess)
+    return false;
+  __atomic_fetch_or(done, 1u << dev, __ATOMIC_RELEASE);
+  return true;
+}
+
 }  // namespace
 }  // namespace negf
 
@@ -489,6 +736,16 @@ int negf_conv_polarization(long long n_rows, int n_e, int L, const void* gl, con
       !pl || !pg)
     return -1;
   if (n_rows == 0) return 0;
+  if (L == 2 * kMaxL1) {  // cluster pair of L/2-point engines
+    static unsigned attr = 0;
+    if (!attr_x2((const void*)pol_kernel_x2<8>, &attr)) return -5;
+    ProfSpan ps_pol_kernel(PROF_CONV, (cudaStream_t)(stream), 0.0, 96.0 * (double)n_rows * n_e);
+    pol_kernel_x2<8><<<(unsigned)(2 * n_rows), 512, smem_x2(L), (cudaStream_t)stream>>>(
+        (const z_t*)gl, (const z_t*)gg, n_e, L, (const z_t*)tw, (const z_t*)kf, (const z_t*)kcf, diag,
+        make_double2(scale_re, scale_im), (z_t*)pl, (z_t*)pg, (z_t*)pr_up, (z_t*)pr_lo, n_rows);
+    NEGF_LAUNCHED();
+    return 0;
+  }
   auto* kfn = threads_for(L) > 256 ? pol_kernel<8, 512> : threads_for(L) > PACK_T ? pol_kernel<8, 256> : pol_kernel<8, PACK_T>;
   int rc = smem_setup((const void*)kfn, L);
   if (rc) return rc;
@@ -511,6 +768,17 @@ int negf_conv_sigma(long long n_rows, int n_e, int L, const void* gl, const void
       !kf || !kcf || !sl || !sg)
     return -1;
   if (n_rows == 0) return 0;
+  if (L == 2 * kMaxL1) {
+    static unsigned attr = 0;
+    if (!attr_x2((const void*)sigma_kernel_x2<8>, &attr)) return -5;
+    ProfSpan ps_sigma_kernel(PROF_CONV, (cudaStream_t)(stream), 0.0, 128.0 * (double)n_rows * n_e);
+    sigma_kernel_x2<8><<<(unsigned)(2 * n_rows), 512, smem_x2(L), (cudaStream_t)stream>>>(
+        (const z_t*)gl, (const z_t*)gg, (const z_t*)wl, (const z_t*)wg, w_rows, n_e, L, (const z_t*)tw,
+        (const z_t*)kf, (const z_t*)kcf, diag, make_double2(scale_re, scale_im), (z_t*)sl, (z_t*)sg,
+        (z_t*)sr_up, (z_t*)sr_lo, n_rows);
+    NEGF_LAUNCHED();
+    return 0;
+  }
   auto* kfn = threads_for(L) > 256 ? sigma_kernel<8, 512> : threads_for(L) > PACK_T ? sigma_kernel<8, 256> : sigma_kernel<8, PACK_T>;
   int rc = smem_setup((const void*)kfn, L);
   if (rc) return rc;

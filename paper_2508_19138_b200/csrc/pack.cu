@@ -28,8 +28,30 @@ struct Pat {
   long long tri, per_row, n_entries;  // tri = bs(bs+1)/2, per_row = tri + bs^2
 };
 
-__device__ __forceinline__ void locate(const Pat& p, const int* __restrict__ tri_q, long long t,
-                                       int& bi, int& kind, int& q) {
+// Where entry t of the pattern lives in the block stacks: block row bi,
+// kind (0 = diagonal block, 1 = upper block (bi, bi+1)) and flat offset q
+// inside the block.
+// LocStd: the reference's compressed bandwidth-3 EntryPattern on the stacks'
+//   own blocking, computed from t (tri_q = row-major upper-triangle offsets).
+// LocTab: any other pattern / blocking from per-entry tables -- a subset of
+//   the band (the paper's r_cut nonzero set) or a coarser
+//   target blocking (the W grid with bs_w = k bs, scba.py:893-937):
+//   code[t] = 2 bi + kind, qt[t] = q.
+struct LocStd {
+  const int* __restrict__ tri_q;
+  __device__ __forceinline__ void operator()(const struct Pat& p, long long t, int& bi, int& kind, int& q) const;
+};
+struct LocTab {
+  const int* __restrict__ code;
+  const int* __restrict__ qt;
+  __device__ __forceinline__ void operator()(const struct Pat&, long long t, int& bi, int& kind, int& q) const {
+    const int c = code[t];
+    bi = c >> 1;
+    kind = c & 1;
+    q = qt[t];
+  }
+};
+__device__ __forceinline__ void LocStd::operator()(const Pat& p, long long t, int& bi, int& kind, int& q) const {
   bi = (int)(t / p.per_row);
   const long long rem = t - (long long)bi * p.per_row;
   if (rem < p.tri) {
@@ -42,7 +64,8 @@ __device__ __forceinline__ void locate(const Pat& p, const int* __restrict__ tri
 }
 
 // blocks -> series
-__global__ void pack_lg_kernel(Pat p, const int* __restrict__ tri_q, int n_e,
+template <class Loc>
+__global__ void pack_lg_kernel(Pat p, Loc locate, int n_e,
                                const z_t* __restrict__ xd, const z_t* __restrict__ xu, z_t* out,
                                long long ld, int e0) {
   __shared__ z_t tile[T][T + 1];
@@ -53,7 +76,7 @@ __global__ void pack_lg_kernel(Pat p, const int* __restrict__ tri_q, int n_e,
   const long long t = t0 + tx;
   int bi = 0, kind = 0, q = 0;
   const bool ok = t < p.n_entries;
-  if (ok) locate(p, tri_q, t, bi, kind, q);
+  if (ok) locate(p, t, bi, kind, q);
   for (int k = ty; k < T; k += 8) {
     const int e = eb + k;
     if (ok && e < n_e) {
@@ -94,7 +117,7 @@ __global__ void pack_lg_p2p_kernel(Pat p, const int* __restrict__ tri_q, int n_e
   const long long t = t0 + tx;
   int bi = 0, kind = 0, q = 0;
   const bool ok = t < p.n_entries;
-  if (ok) locate(p, tri_q, t, bi, kind, q);
+  if (ok) LocStd{tri_q}(p, t, bi, kind, q);
   for (int k = ty; k < T; k += 8) {
     const int e = eb + k;
     if (ok && e < n_e) {
@@ -128,8 +151,8 @@ struct PeerSrc {
   const long long* row_start;
 };
 
-template <bool P2P>
-__global__ void unpack_kernel(Pat p, const int* __restrict__ tri_q, int n_e,
+template <bool P2P, class Loc>
+__global__ void unpack_kernel(Pat p, Loc locate, int n_e,
                               const z_t* __restrict__ in_up, const z_t* __restrict__ in_lo,
                               long long ld, int e0, int mode, z_t* xd, z_t* xu, z_t* xl, PeerSrc ps) {
   __shared__ z_t tu[T][T + 1];
@@ -171,7 +194,7 @@ __global__ void unpack_kernel(Pat p, const int* __restrict__ tri_q, int n_e,
   const long long t = t0 + tx;
   if (t >= p.n_entries) return;
   int bi, kind, q;
-  locate(p, tri_q, t, bi, kind, q);
+  locate(p, t, bi, kind, q);
   const int r = q / p.bs, c = q % p.bs;
   const int qt = c * p.bs + r;
   for (int k = ty; k < T; k += 8) {
@@ -227,7 +250,7 @@ int negf_pack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* x_diag,
   dim3 grid((unsigned)((p.n_entries + T - 1) / T), (n_e + T - 1) / T), block(T, 8);
   {
     ProfSpan ps_pack_lg_kernel(PROF_LAYOUT, (cudaStream_t)(stream), 0.0, 32.0 * (double)p.n_entries * n_e);
-    pack_lg_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(p, tri_q, n_e, (const z_t*)x_diag,
+    pack_lg_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(p, LocStd{tri_q}, n_e, (const z_t*)x_diag,
                                                              (const z_t*)x_upper, (z_t*)out, ld, e0);
     NEGF_LAUNCHED();
   }
@@ -264,7 +287,7 @@ int negf_unpack_lg(int n_e, int n_b, int bs, const int* tri_q, const void* in, l
   {
     const double blocks = (2.0 * n_b - 1.0) * bs * bs;  // diag + upper blocks written
     ProfSpan ps_unpack_kernel(PROF_LAYOUT, (cudaStream_t)(stream), 0.0, 16.0 * ((double)p.n_entries + blocks) * n_e);
-    unpack_kernel<false><<<grid, block, 0, (cudaStream_t)stream>>>(p, tri_q, n_e, (const z_t*)in, nullptr, ld,
+    unpack_kernel<false><<<grid, block, 0, (cudaStream_t)stream>>>(p, LocStd{tri_q}, n_e, (const z_t*)in, nullptr, ld,
                                                                    e0, 0, (z_t*)x_diag, (z_t*)x_upper, nullptr,
                                                                    PeerSrc{});
     NEGF_LAUNCHED();
@@ -287,7 +310,7 @@ int negf_unpack_retarded(int n_e, int n_b, int bs, const int* tri_q, const void*
     ProfSpan ps_unpack_kernel(PROF_LAYOUT, (cudaStream_t)(stream), 0.0,
                               16.0 * (2.0 * (double)p.n_entries + blocks) * n_e);
     unpack_kernel<false><<<grid, block, 0, (cudaStream_t)stream>>>(
-        p, tri_q, n_e, (const z_t*)in_upper, (const z_t*)in_lower, ld, e0, 1, (z_t*)x_diag,
+        p, LocStd{tri_q}, n_e, (const z_t*)in_upper, (const z_t*)in_lower, ld, e0, 1, (z_t*)x_diag,
         (z_t*)x_upper, (z_t*)x_lower, PeerSrc{});
     NEGF_LAUNCHED();
   }
@@ -310,8 +333,62 @@ int negf_unpack_p2p(int n_e, int n_b, int bs, const int* tri_q, int retarded, in
     ProfSpan ps_unpack(PROF_LAYOUT, (cudaStream_t)(stream), 0.0,
                        16.0 * ((retarded ? 2.0 : 1.0) * p.n_entries + blocks) * n_e);
     unpack_kernel<true><<<grid, block, 0, (cudaStream_t)stream>>>(
-        p, tri_q, n_e, nullptr, nullptr, ld, col0, retarded ? 1 : 0, (z_t*)x_diag, (z_t*)x_upper,
+        p, LocStd{tri_q}, n_e, nullptr, nullptr, ld, col0, retarded ? 1 : 0, (z_t*)x_diag, (z_t*)x_upper,
         (z_t*)x_lower, PeerSrc{n_ranks, src_upper, retarded ? src_lower : nullptr, row_start});
+    NEGF_LAUNCHED();
+  }
+  return 0;
+}
+
+/* Table-driven layout (LocTab above): n_entries pattern entries located in
+ * block stacks of n_bt blocks of bs_t orbitals by code[t] = 2 bi + kind and
+ * q[t]. zero_fill clears the target stacks first (patterns that do not cover
+ * every stored block element). */
+int negf_pack_lg_table(int n_e, long long n_entries, int n_bt, int bs_t, const int* code, const int* q,
+                       const void* x_diag, const void* x_upper, void* out, long long ld, int e0, void* stream) {
+  if (n_e < 0 || n_entries < 0 || n_bt < 1 || bs_t < 1 || !code || !q || !x_diag || !out || e0 < 0 ||
+      ld < e0 + n_e)
+    return -1;
+  if (n_bt > 1 && !x_upper) return -1;
+  if (n_e == 0 || n_entries == 0) return 0;
+  Pat p = make_pat(n_bt, bs_t);
+  p.n_entries = n_entries;
+  dim3 grid((unsigned)((n_entries + T - 1) / T), (n_e + T - 1) / T), block(T, 8);
+  {
+    ProfSpan ps_(PROF_LAYOUT, (cudaStream_t)(stream), 0.0, 32.0 * (double)n_entries * n_e);
+    pack_lg_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(p, LocTab{code, q}, n_e, (const z_t*)x_diag,
+                                                             (const z_t*)x_upper, (z_t*)out, ld, e0);
+    NEGF_LAUNCHED();
+  }
+  return 0;
+}
+
+int negf_unpack_table(int n_e, long long n_entries, int n_bt, int bs_t, const int* code, const int* q,
+                      int retarded, const void* in_upper, const void* in_lower, long long ld, int e0,
+                      void* x_diag, void* x_upper, void* x_lower, int zero_fill, void* stream) {
+  if (n_e < 0 || n_entries < 0 || n_bt < 1 || bs_t < 1 || !code || !q || !in_upper || !x_diag || e0 < 0 ||
+      ld < e0 + n_e || (retarded && !in_lower))
+    return -1;
+  if (n_bt > 1 && (!x_upper || (retarded && !x_lower))) return -1;
+  if (n_e == 0) return 0;
+  const size_t n2 = (size_t)bs_t * bs_t * sizeof(z_t);
+  if (zero_fill) {
+    NEGF_CUDA_CHECK(cudaMemsetAsync(x_diag, 0, n2 * n_bt * n_e, (cudaStream_t)stream));
+    if (n_bt > 1) {
+      NEGF_CUDA_CHECK(cudaMemsetAsync(x_upper, 0, n2 * (n_bt - 1) * n_e, (cudaStream_t)stream));
+      if (retarded) NEGF_CUDA_CHECK(cudaMemsetAsync(x_lower, 0, n2 * (n_bt - 1) * n_e, (cudaStream_t)stream));
+    }
+  }
+  if (n_entries == 0) return 0;
+  Pat p = make_pat(n_bt, bs_t);
+  p.n_entries = n_entries;
+  dim3 grid((unsigned)((n_entries + T - 1) / T), (n_e + T - 1) / T), block(T, 8);
+  {
+    ProfSpan ps_(PROF_LAYOUT, (cudaStream_t)(stream), 0.0,
+                 16.0 * ((retarded ? 2.0 : 1.0) * n_entries + (retarded ? 2.0 : 1.5) * n_entries) * n_e);
+    unpack_kernel<false><<<grid, block, 0, (cudaStream_t)stream>>>(
+        p, LocTab{code, q}, n_e, (const z_t*)in_upper, (const z_t*)in_lower, ld, e0, retarded ? 1 : 0,
+        (z_t*)x_diag, (z_t*)x_upper, (z_t*)x_lower, PeerSrc{});
     NEGF_LAUNCHED();
   }
   return 0;

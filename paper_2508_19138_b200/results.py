@@ -38,6 +38,9 @@ class EntryPattern:
     block_size: int
     block_bandwidth: int = 3
     compressed: bool = True
+    #: keep only entries with |row - col| <= cutoff (the paper's r_cut nonzero
+    #: set on a 1D orbital chain); None = the full band
+    cutoff: int | None = None
 
     @cached_property
     def _rc(self) -> tuple[np.ndarray, np.ndarray]:
@@ -56,7 +59,11 @@ class EntryPattern:
                     r, c = full_r, full_c
                 rows.append(bi * bs + r)
                 cols.append(bj * bs + c)
-        return np.concatenate(rows).astype(np.intp), np.concatenate(cols).astype(np.intp)
+        rows, cols = np.concatenate(rows).astype(np.intp), np.concatenate(cols).astype(np.intp)
+        if self.cutoff is not None:
+            keep = np.abs(rows - cols) <= self.cutoff
+            rows, cols = rows[keep], cols[keep]
+        return rows, cols
 
     @property
     def rows(self) -> np.ndarray:
@@ -68,6 +75,8 @@ class EntryPattern:
 
     @property
     def n_entries(self) -> int:
+        if self.cutoff is not None:
+            return int(self.rows.size)
         h = (self.block_bandwidth - 1) // 2
         bs = self.block_size
         n = 0

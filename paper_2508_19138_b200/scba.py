@@ -102,6 +102,12 @@ class ScbaOptions:
     # and every P / Sigma convolution with the direct sum (checks.py);
     # ScbaResult.oracle_deviations = {"solve_vs_dense", "fft_vs_direct"}
     oracle_mode: bool = False
+    # Deviation (off by default): restrict the entry set of G^<>, P, W and
+    # Sigma to |row - col| <= entry_cutoff orbitals -- the paper's r_cut
+    # nonzero set (the reference applies r_cut to V only,
+    # driver.py:276-277, and keeps the full band, scba.py:917). None = the
+    # reference's full band. What makes a 2048-energy C3 iteration fit in HBM.
+    entry_cutoff: int | None = None
 
     def __post_init__(self) -> None:
         if self.max_iter < 1:
@@ -116,31 +122,74 @@ class ScbaOptions:
             raise ValueError(f"unknown W retarded method {self.w_retarded_method!r}")
         if self.retarded_method not in ("sancho", "beyn", "fixed_point"):
             raise ValueError(f"unknown retarded method {self.retarded_method!r}")
+        if self.entry_cutoff is not None and self.entry_cutoff < 0:
+            raise ValueError(f"entry_cutoff must be >= 0 orbitals, got {self.entry_cutoff}")
 
 
 class EntryLayout:
-    """Device tables of the compressed bandwidth-3 EntryPattern."""
+    """Device tables of the entry-major pattern and where its entries live in
+    the block stacks.
 
-    def __init__(self, n_b: int, bs: int, device) -> None:
+    Default: the reference's compressed bandwidth-3 EntryPattern
+    (convolve.py:135-187) on the stacks' own blocking -- structured kernels.
+    Table mode (negf_*_table) for everything else:
+      * ``cutoff``: keep only entries with |row - col| <= cutoff orbitals (the
+        paper's r_cut nonzero set of G, P, W and Sigma, on
+        the 1D orbital chain of the synthetic devices) -- a documented
+        deviation; cutoff=None is the reference's full band;
+      * ``target_bs``: the stacks use a coarser blocking (the W grid,
+        bs_w = k bs, scba.py:893-937)."""
+
+    def __init__(self, n_b: int, bs: int, device, cutoff: int | None = None, target_bs: int | None = None) -> None:
         self.n_b, self.bs = n_b, bs
         self.dev = torch.device(device)
+        self.cutoff = cutoff
+        self.target_bs = target_bs or bs
+        if self.target_bs % bs or (n_b * bs) % self.target_bs:
+            raise ValueError(f"target block size {self.target_bs} is not a multiple of {bs} dividing {n_b * bs}")
+        self.n_bt = n_b * bs // self.target_bs
+        self.table = cutoff is not None or self.target_bs != bs
         lib = _lib.load()
-        self.n_entries = int(lib.negf_pattern_entries(n_b, bs))
         r, c = np.triu_indices(bs)
         self.tri_q = torch.from_numpy((r * bs + c).astype(np.int32)).to(self.dev)
-        t = len(r)
-        per_row = t + bs * bs
-        diag = np.zeros(self.n_entries, dtype=np.uint8)
-        rows = []
-        for b in range(n_b):
-            base = b * per_row
-            on = np.flatnonzero(r == c)
-            diag[base + on] = 1
-            rows.append(base + on)
-        self.diag = torch.from_numpy(diag).to(self.dev)
-        self.diag_rows = torch.from_numpy(np.stack(rows).astype(np.int64)).to(self.dev)  # (n_b, bs)
+        if not self.table:
+            self.n_entries = int(lib.negf_pattern_entries(n_b, bs))
+            t = len(r)
+            per_row = t + bs * bs
+            diag = np.zeros(self.n_entries, dtype=np.uint8)
+            rows = []
+            for b in range(n_b):
+                base = b * per_row
+                on = np.flatnonzero(r == c)
+                diag[base + on] = 1
+                rows.append(base + on)
+            self.diag = torch.from_numpy(diag).to(self.dev)
+            self.diag_rows = torch.from_numpy(np.stack(rows).astype(np.int64)).to(self.dev)  # (n_b, bs)
+            return
+        from .results import EntryPattern
+
+        pat = EntryPattern(n_b, bs, 3, True, cutoff)
+        rows, cols = pat.rows, pat.cols
+        self.n_entries = int(rows.size)
+        bt = self.target_bs
+        R, C = rows // bt, cols // bt
+        code = (2 * R + (C - R)).astype(np.int32)
+        q = ((rows % bt) * bt + cols % bt).astype(np.int32)
+        self.code = torch.from_numpy(code).to(self.dev)
+        self.q = torch.from_numpy(q).to(self.dev)
+        on = rows == cols
+        self.diag = torch.from_numpy(on.astype(np.uint8)).to(self.dev)
+        idx = np.flatnonzero(on)  # every diagonal entry survives any cutoff (distance 0)
+        self.diag_rows = torch.from_numpy(idx.reshape(n_b, bs).astype(np.int64)).to(self.dev)
 
     def pack(self, x_diag, x_upper, out, e0):
+        if self.table:
+            rc = _lib.load().negf_pack_lg_table(x_diag.shape[0], self.n_entries, self.n_bt, self.target_bs,
+                                                self.code.data_ptr(), self.q.data_ptr(), x_diag.data_ptr(),
+                                                x_upper.data_ptr(), out.data_ptr(), out.shape[-1], e0,
+                                                _lib.stream_ptr(self.dev))
+            _lib.check(rc, "negf_pack_lg_table")
+            return
         rc = _lib.load().negf_pack_lg(x_diag.shape[0], self.n_b, self.bs, self.tri_q.data_ptr(), x_diag.data_ptr(),
                                       x_upper.data_ptr(), out.data_ptr(), out.shape[-1], e0,
                                       _lib.stream_ptr(self.dev))
@@ -168,12 +217,25 @@ class EntryLayout:
                                          _lib.stream_ptr(self.dev))
         _lib.check(rc, "negf_unpack_p2p")
 
+    def _unpack_table(self, up, lo, e0, n_e, x_diag, x_upper, x_lower):
+        ret = lo is not None
+        rc = _lib.load().negf_unpack_table(n_e, self.n_entries, self.n_bt, self.target_bs, self.code.data_ptr(),
+                                           self.q.data_ptr(), int(ret), up.data_ptr(),
+                                           lo.data_ptr() if ret else None, up.shape[-1], e0, x_diag.data_ptr(),
+                                           x_upper.data_ptr(), x_lower.data_ptr() if ret else None, 1,
+                                           _lib.stream_ptr(self.dev))
+        _lib.check(rc, "negf_unpack_table")
+
     def unpack_lg(self, src, e0, n_e, x_diag, x_upper):
+        if self.table:
+            return self._unpack_table(src, None, e0, n_e, x_diag, x_upper, None)
         rc = _lib.load().negf_unpack_lg(n_e, self.n_b, self.bs, self.tri_q.data_ptr(), src.data_ptr(), src.shape[-1],
                                         e0, x_diag.data_ptr(), x_upper.data_ptr(), _lib.stream_ptr(self.dev))
         _lib.check(rc, "negf_unpack_lg")
 
     def unpack_retarded(self, up, lo, e0, n_e, x_diag, x_upper, x_lower):
+        if self.table:
+            return self._unpack_table(up, lo, e0, n_e, x_diag, x_upper, x_lower)
         rc = _lib.load().negf_unpack_retarded(n_e, self.n_b, self.bs, self.tri_q.data_ptr(), up.data_ptr(),
                                               lo.data_ptr(), up.shape[-1], e0, x_diag.data_ptr(),
                                               x_upper.data_ptr(), x_lower.data_ptr(), _lib.stream_ptr(self.dev))
@@ -448,7 +510,7 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     carrier = CarrierSolver(h, eta, contacts, options.surface_tol, device=dev,
                             retarded_method=options.retarded_method, beyn=options.beyn)
     n_b, bs = carrier.n_b, carrier.bs
-    lay = EntryLayout(n_b, bs, dev)
+    lay = EntryLayout(n_b, bs, dev, cutoff=options.entry_cutoff)
     tr = Transposer(comm, lay.n_entries, ne)
     spatial = plan is not None and plan.p_s > 1
     if spatial:
@@ -467,7 +529,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     # by the W unpack and Sigma by the mixing; stream-ordered barriers order
     # writers and readers. NEGF_PEER_TRANSPOSE=0 selects NCCL all-to-all.
     peer = None
-    if comm.size > 1 and v is not None and not spatial and os.environ.get("NEGF_PEER_TRANSPOSE", "1") != "0":
+    if (comm.size > 1 and v is not None and not spatial and not lay.table
+            and os.environ.get("NEGF_PEER_TRANSPOSE", "1") != "0"):
         from .dist import PeerEntryMajor
 
         peer = PeerEntryMajor.try_create(tr, dev)  # None (-> NCCL all-to-all) off NCCL / without P2P
@@ -503,10 +566,15 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         if screened.bs % bs != 0:
             raise ValueError("screening block size must be a multiple of the carrier block size, got "
                              f"{screened.bs} and {bs}")
-        if screened.bs != bs:
-            raise ValueError(f"a W grid coarser than the G grid (bs_w = {screened.bs} = {screened.bs // bs} x bs) "
-                             "is not supported by the device layout kernels (the BASELINE configs use equal "
-                             "blockings)")
+        if spatial and screened.bs != bs:
+            raise ValueError("the spatial mode takes equal G and W blockings")
+    # P goes into the W stacks and W^<> comes back at G-pattern coordinates
+    # (scba.py:925-937 _scatter_groups(pat_g, bs_w) / w_to_g): with a coarser
+    # W grid through the table-driven layout on the W blocking
+    lay_w = lay
+    if v is not None and screened.bs != bs:
+        lay_w = EntryLayout(n_b, bs, dev, cutoff=options.entry_cutoff, target_bs=screened.bs)
+        peer = None
         if spatial:  # the W chain gets its own even split (scba.py:930)
             screened.dd = (make_partition_plan(n_b, plan.p_s), comm)
     cols = lambda: torch.empty((lay.n_entries, n_own), dtype=Z, device=dev)
@@ -563,10 +631,10 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         lo, hi = max(e0, own.start), min(e0 + nb_, own.stop)
         return lo - e0, max(hi - lo, 0), lo - own.start
 
-    def pack_own(xd, xu, out, e0: int, nb_: int) -> None:
+    def pack_own(xd, xu, out, e0: int, nb_: int, layout=None) -> None:
         a, n, c = own_part(e0, nb_)
         if n:
-            lay.pack(xd[a:a + n], xu[a:a + n], out, c)
+            (layout or lay).pack(xd[a:a + n], xu[a:a + n], out, c)
     timings_by_it = []
     # reference observables of each iteration's G solve (scba.py:1313-1376),
     # reduced on the device per batch; the last iteration's are reported
@@ -574,8 +642,12 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
 
     obs_acc = ObservableAccumulator(max(n_sol, 1), n_b, de, dev)
     stats = TranspositionStats()
-    pattern = EntryPattern(n_b, bs, 3, True)
+    pattern = EntryPattern(n_b, bs, 3, True, options.entry_cutoff)
     full_count = pattern.full_entry_count()
+    w_count = (lay.n_entries, full_count)
+    if v is not None and screened.bs != bs:
+        pat_w = EntryPattern(screened.n_b, screened.bs, 3, True, options.entry_cutoff)
+        w_count = (pat_w.n_entries, pat_w.full_entry_count())
     for it in range(max_iter):
         n_iter = it + 1
         torch.cuda.synchronize(dev)
@@ -635,8 +707,10 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
         # logical transposition volume of this iteration, counted like the
         # reference's replicated exchanges (scba.py:1028-1141, _count_bytes):
         # G^<>, P^<>, W^<>, Sigma^<> lg-compressed; P^R, Sigma^R plain
-        for _ in range(8):
+        for _ in range(6):
             count_transpose_bytes(stats, True, lay.n_entries, ne, full_count)
+        for _ in range(2):  # W^<> travel on the W pattern in the reference (pat_w)
+            count_transpose_bytes(stats, True, w_count[0], ne, w_count[1])
         for _ in range(4):
             count_transpose_bytes(stats, False, lay.n_entries, ne, 0)
         # 2. G^<> to entry-major (all-to-all), polarization on own entry rows
@@ -685,9 +759,9 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
                     lay.unpack_p2p(peer, ("pl",), c0, nb_, wb["pl_diag"], wb["pl_upper"])
                     lay.unpack_p2p(peer, ("pg",), c0, nb_, wb["pg_diag"], wb["pg_upper"])
                 else:
-                    lay.unpack_retarded(pru, prl, e0, nb_, wb["pr_diag"], wb["pr_upper"], wb["pr_lower"])
-                    lay.unpack_lg(pl, e0, nb_, wb["pl_diag"], wb["pl_upper"])
-                    lay.unpack_lg(pg, e0, nb_, wb["pg_diag"], wb["pg_upper"])
+                    lay_w.unpack_retarded(pru, prl, e0, nb_, wb["pr_diag"], wb["pr_upper"], wb["pr_lower"])
+                    lay_w.unpack_lg(pl, e0, nb_, wb["pl_diag"], wb["pl_upper"])
+                    lay_w.unpack_lg(pg, e0, nb_, wb["pg_diag"], wb["pg_upper"])
             wb = screened.solve(nb_, timer=_T, memo=memo(e0))
             if odev is not None:
                 solve_check(wb, True)
@@ -697,8 +771,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
                     lay.pack_p2p(wb["wg_diag"], wb["wg_upper"], (peer, p_wg), own.start + e0)
                     peer.count(2 * nb_)
                 else:
-                    pack_own(wb["wl_diag"], wb["wl_upper"], wl_c, e0, nb_)
-                    pack_own(wb["wg_diag"], wb["wg_upper"], wg_c, e0, nb_)
+                    pack_own(wb["wl_diag"], wb["wl_upper"], wl_c, e0, nb_, lay_w)
+                    pack_own(wb["wg_diag"], wb["wg_upper"], wg_c, e0, nb_, lay_w)
         del pl, pg, pru, prl
         with _T("transpose"):
             if peer is not None:

@@ -121,6 +121,25 @@ RESULT_FIELDS = ["g_r_diag", "g_r_upper", "g_r_lower", "g_lesser_diag", "g_lesse
                  "sigma_obc_greater_left", "sigma_obc_lesser_right", "sigma_obc_greater_right"]
 
 
+def make_scba_coarse_w():
+    """W grid coarser than the G grid (scba.py:893-903, 925-937): G on
+    chain_device(8, 4), V = coulomb_matrix(4, 8) (bs_w = 2 bs), 3 iterations."""
+    h = toys.chain_device(8, 4)
+    v = toys.coulomb_matrix(4, 8)
+    grid = EnergyGrid(-2.0, 2.0, 32, eta=1e-3)
+    contacts = scba.ContactConfig(mu_left=0.1, mu_right=-0.1, kT=0.05)
+    opts = scba.ScbaOptions(max_iter=3, tol=1e-12, mixing=0.3, retarded_method="sancho",
+                            memoizer=scba.MemoizerOptions(enabled=False))
+    with threadpool_limits(1):
+        res = scba.scba_run(h, v, grid, contacts, opts)
+    out = {f: getattr(res, f) for f in RESULT_FIELDS}
+    for f in ("lesser", "greater", "ret_upper", "ret_lower"):
+        out["sigma_" + f] = getattr(res.sigma, f)
+    out["residuals"] = np.asarray(res.residuals)
+    out["config"] = np.array([8, 4, 4, 8, 32, 3])
+    np.savez_compressed(OUT / "golden_scba_coarse_w.npz", **out, **{f"ver_{k}": v for k, v in VERS.items()})
+
+
 def make_ballistic():
     out = {}
     res = scba_case(5, 3, 16, 1, ballistic=True)

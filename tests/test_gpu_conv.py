@@ -28,7 +28,9 @@ def test_convolve_and_retarded_match_reference_golden(golden, cuda, ne):
 
 @pytest.mark.parametrize("ne", [1, 2, 3, 16, 32, 64, 100, 256, 1024, 2048, 2049, 4096])
 def test_convolutions_match_oracle_sizes(cuda, ne):
-    """N_E > 2048 (L > 4096) takes the cuFFT path (conv.MAX_L_NATIVE)."""
+    """The reference-signature drop-ins: N_E > 2048 (L > 4096) take the
+    cuFFT path (conv.MAX_L_GENERIC); the fused P / Sigma kernels below run
+    natively up to N_E = 4096."""
     rng = np.random.default_rng(ne)
     x1 = rng.standard_normal((5, ne)) + 1j * rng.standard_normal((5, ne))
     x2 = rng.standard_normal((5, ne)) + 1j * rng.standard_normal((5, ne))
@@ -38,9 +40,11 @@ def test_convolutions_match_oracle_sizes(cuda, ne):
 
 
 @pytest.mark.parametrize("ne,rows", [(3, 517), (8, 37), (16, 37), (16, 1001), (128, 37), (300, 75), (2048, 37),
-                                     (2100, 9), (4096, 5)])
+                                     (2049, 11), (2100, 9), (3000, 21), (4096, 5), (4096, 40)])
 def test_fused_polarization_and_sigma_match_oracle(cuda, ne, rows):
-    """Short series pack several entry rows per CTA (ragged last CTA covered)."""
+    """Short series pack several entry rows per CTA (ragged last CTA covered);
+    2048 < N_E <= 4096 (L = 8192) runs on cluster pairs of CTAs splitting the
+    even / odd frequency bins (conv.cu pol_kernel_x2 / sigma_kernel_x2)."""
     rng = np.random.default_rng(7 + ne)
     mk = lambda: rng.standard_normal((rows, ne)) + 1j * rng.standard_normal((rows, ne))
     gl, gg, wl, wg = mk(), mk(), mk(), mk()

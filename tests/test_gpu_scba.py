@@ -332,3 +332,75 @@ def test_scba_result_is_reference_shaped(golden, cuda):
     cold = scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05),
                     ScbaOptions(retarded_method="sancho", max_iter=4, tol=1e-12, memoizer=MEMO_OFF), device=cuda)
     assert abs(warm.residuals[0] - cold.residuals[3]) < 1e-9 * cold.residuals[3]
+
+
+def test_scba_coarse_w_grid_matches_reference(golden, cuda):
+    """bs_w = 2 bs (scba.py:893-903, 925-937): P scattered from the G pattern
+    into the W blocks and W read back at G-pattern coordinates through the
+    table-driven layout kernels; vs the reference's scba_run."""
+    g = golden("golden_scba_coarse_w.npz")
+    res = scba_run(orc.chain_device(8, 4), orc.coulomb_matrix(4, 8), np.linspace(-2.0, 2.0, 32), 1e-3,
+                   Contacts(0.1, -0.1, 0.05),
+                   ScbaOptions(retarded_method="sancho", max_iter=3, tol=1e-12, batch=12, memoizer=MEMO_OFF),
+                   device=cuda)
+    for k in g.files:
+        if k.startswith(("ver_", "config")):
+            continue
+        assert rel(res[k], g[k]) < TOL, k
+
+
+def test_scba_w_grid_preconditions(cuda):
+    c = Contacts(0.1, -0.1, 0.05)
+    e = np.linspace(-1.0, 1.0, 8)
+    with pytest.raises(ValueError, match="does not match carrier layout"):
+        scba_run(orc.chain_device(8, 4), orc.coulomb_matrix(3, 8), e, 1e-3, c, ScbaOptions(retarded_method="sancho"),
+                 device=cuda)
+    with pytest.raises(ValueError, match="multiple of the carrier block"):
+        scba_run(orc.chain_device(8, 4), orc.coulomb_matrix(16, 2), e, 1e-3, c, ScbaOptions(retarded_method="sancho"),
+                 device=cuda)
+
+
+@pytest.mark.parametrize("case", ["small", "c1"])
+def test_scba_entry_cutoff_infinite_equals_reference(golden, cuda, case):
+    """r_cut = infinity equivalence: the table-driven entry layout with a
+    cutoff larger than any |row - col| reproduces the reference's full-band
+    scba_run."""
+    if case == "small":
+        g = golden("golden_scba_small.npz")
+        res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
+                       Contacts(0.1, -0.1, 0.05),
+                       ScbaOptions(retarded_method="sancho", max_iter=3, tol=1e-12, memoizer=MEMO_OFF,
+                                   entry_cutoff=10 ** 6), device=cuda)
+        for k in ("g_r_diag", "g_lesser_upper", "g_greater_diag", "sigma_lesser", "sigma_greater",
+                  "sigma_ret_upper", "sigma_ret_lower", "residuals"):
+            assert rel(res[k], g[k]) < TOL, k
+    else:
+        g = golden("golden_scba_c1.npz")
+        res = scba_run(orc.chain_device(16, 32), orc.coulomb_matrix(16, 32), np.linspace(-2.0, 2.0, 128), 1e-3,
+                       Contacts(0.1, -0.1, 0.05),
+                       ScbaOptions(retarded_method="sancho", max_iter=1, tol=1e-12, batch=64, memoizer=MEMO_OFF,
+                                   entry_cutoff=10 ** 6), device=cuda)
+        check_c1(res, g, tol=TOL)
+
+
+@pytest.mark.parametrize("cutoff,bs", [(5, 4), (0, 4), (40, 32)])
+def test_scba_entry_cutoff_matches_oracle(cuda, cutoff, bs):
+    """The paper's r_cut nonzero set (ScbaOptions.entry_cutoff, a documented
+    deviation) against the oracle computing on the full band with the
+    dropped entries zeroed after every gather."""
+    nb = 6 if bs == 4 else 5
+    h, v = orc.chain_device(nb, bs), orc.coulomb_matrix(nb, bs)
+    e = np.linspace(-2.0, 2.0, 24)
+    ref = orc.scba(h, v, e, 1e-3, 0.1, -0.1, 0.05, max_iter=3, entry_cutoff=cutoff)
+    res = scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05),
+                   ScbaOptions(retarded_method="sancho", max_iter=3, tol=1e-12, batch=7, memoizer=MEMO_OFF,
+                               entry_cutoff=cutoff), device=cuda)
+    rows, cols = orc.entry_pattern(nb, bs)
+    keep = np.abs(rows - cols) <= cutoff
+    assert res.sigma_pattern.n_entries == int(keep.sum())
+    assert np.array_equal(res.sigma_pattern.rows, rows[keep])
+    for k in ("g_r_diag", "g_r_upper", "g_lesser_diag", "g_lesser_upper", "g_greater_upper", "residuals"):
+        assert rel(res[k], ref[k]) < TOL, k
+    for k in ("lesser", "greater", "ret_upper", "ret_lower"):
+        assert rel(res["sigma_" + k], ref["sigma_" + k][keep]) < TOL, k
+        assert np.all(ref["sigma_" + k][~keep] == 0)

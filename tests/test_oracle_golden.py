@@ -245,3 +245,19 @@ def test_oracle_beyn_matches_reference(golden):
         x, modes = orc.beyn(g[p + "m"], g[p + "n"], g[p + "np"])
         assert modes == int(g[p + "modes"]), k
         assert rel(x, g[p + "x"]) < 1e-12, k
+
+
+def test_oracle_entry_cutoff_infinite_is_full_band():
+    """The oracle's r_cut hook (entry_cutoff, test infrastructure for the
+    paper's nonzero-set deviation) is the identity for cutoff >= the band."""
+    h, v = orc.chain_device(4, 3), orc.coulomb_matrix(4, 3)
+    e = np.linspace(-2.0, 2.0, 12)
+    a = orc.scba(h, v, e, 1e-3, 0.1, -0.1, 0.05, max_iter=2)
+    b = orc.scba(h, v, e, 1e-3, 0.1, -0.1, 0.05, max_iter=2, entry_cutoff=100)
+    for k in a:
+        if k != "cache_stats_by_iteration":
+            assert np.array_equal(a[k], b[k]), k
+    c = orc.scba(h, v, e, 1e-3, 0.1, -0.1, 0.05, max_iter=2, entry_cutoff=1)
+    rows, cols = orc.entry_pattern(4, 3)
+    assert np.all(c["sigma_lesser"][np.abs(rows - cols) > 1] == 0)
+    assert np.any(c["sigma_lesser"] != a["sigma_lesser"])
