@@ -25,10 +25,8 @@ extern "C" {
 int negf_abi_version(void);
 
 /* Complex block-product algorithm of the DMMA GEMM (process-wide):
- * 0 = 4 real products per complex product,
- * 1 = 3M/Gauss (3 real products, 64x64 tiles), 2 = 3M with 64x32 tiles (default),
- * 3 = 4M with 64x32 tiles, 4 = 3M with 32x64 tiles, 5 = 3M 64x32 with BK=8 padded
- * tiles, 6 = 3M BK=32; +10 selects swizzled BK=16 row-mapped inversion sweeps.
+ * 2 = 3M/Gauss, 3 real products per complex product (default),
+ * 0 = 4 real products (the textbook arithmetic). Anything else: -1.
  * 3M trades ~25% of the FP64 tensor work for a normwise error bound that is
  * still O(eps |A||B|). */
 int negf_set_gemm_algo(int algo);

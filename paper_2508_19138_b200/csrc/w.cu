@@ -407,10 +407,12 @@ int stein_batched(const z_t* a, const z_t* q, z_t* w, int n_side, int n_kind, in
       stein_step_kernel<<<n_kind * n_side, 256, 0, st>>>(w, U, n2, tol, active, iters, it, n_act);
       NEGF_LAUNCHED();
     }
-    int h = 0;
-    NEGF_CUDA_CHECK(cudaMemcpyAsync(&h, n_act, sizeof(int), cudaMemcpyDeviceToHost, st));
-    NEGF_CUDA_CHECK(cudaStreamSynchronize(st));
-    if (h == 0) break;
+    if ((it & 3) == 0 || it == max_iter) {  // host check every 4 squarings (converged problems are masked)
+      int h = 0;
+      NEGF_CUDA_CHECK(cudaMemcpyAsync(&h, n_act, sizeof(int), cudaMemcpyDeviceToHost, st));
+      NEGF_CUDA_CHECK(cudaStreamSynchronize(st));
+      if (h == 0) break;
+    }
     {
       ProfScope ps_or_mask_kernel(PROF_OTHER, (cudaStream_t)(st));
       or_mask_kernel<<<(n_side + 127) / 128, 128, 0, st>>>(active, n_side, n_kind, side_active);

@@ -358,53 +358,31 @@ int launch_cfg(const ZGemmGroup& g, cudaStream_t stream) {
   return 0;
 }
 
-using CfgBig = Cfg<64, 64, 2, 2, 4, 2>;
 using CfgSmall = Cfg<32, 32, 1, 1, 4, 4>;
-// 3M variant: warp tile 32x16 keeps the three accumulator sets in registers
-using CfgGauss = Cfg<64, 64, 2, 4, 4, 1, true>;
 // default (algo 2): 3M, 64x32 CTA tiles of 4 warps, 3 CTAs/SM, BK = 16 with a
 // 2-stage cp.async pipeline and XOR-swizzled k-contiguous tiles (50 KB smem):
 // 96 DMMAs per warp between barriers
 using CfgGauss2 = Cfg<64, 32, 2, 2, 2, 3, true, 16, false, true>;
 using CfgGauss2S = Cfg<32, 64, 2, 2, 2, 3, true, 16, false, true>;  // short M
+// algo 0: 4 real products per complex product (the textbook arithmetic)
 using Cfg4M32 = Cfg<64, 32, 2, 2, 4, 3, false>;
-using CfgGauss3 = Cfg<32, 64, 2, 2, 4, 3, true>;
-using CfgGauss2P = Cfg<64, 32, 2, 2, 4, 3, true>;  // BK = 8, 4 stages, padded tiles
-using CfgG32s2 = Cfg<64, 32, 2, 2, 2, 2, true, 32, false, true>;
-using CfgW8 = Cfg<64, 32, 4, 2, 2, 2, true, 16, false, true>;    // 8 warps of 16x16, 3M
-using CfgT5 = Cfg<32, 32, 2, 2, 2, 5, true, 16, false, true>;    // 4 warps of 16x16, 5 CTAs/SM
-using CfgW8b = Cfg<64, 64, 4, 2, 2, 1, true, 16, false, true>;   // 8 warps of 16x32
-using CfgMap64 = Cfg<64, 32, 2, 2, 4, 3, true, 8, true>;
-using CfgMap32 = Cfg<32, 64, 2, 2, 4, 3, true, 8, true>;
-using CfgMap64S = Cfg<64, 32, 2, 2, 2, 3, true, 16, true, true>;
-using CfgMap32S = Cfg<32, 64, 2, 2, 2, 3, true, 16, true, true>;
-using CfgMapT = Cfg<32, 32, 2, 2, 2, 5, true, 16, true, true>;   // 16x16 warp tiles, 5 CTAs/SM
-using CfgMapT4 = Cfg<32, 32, 2, 2, 2, 5, false, 16, true, true>; // 4M, 5 CTAs/SM
-using CfgMapU = Cfg<16, 64, 1, 4, 2, 5, true, 16, true, true>;   // 16x16 warp tiles, 16-row CTAs
-using CfgMapV = Cfg<32, 32, 2, 2, 2, 6, true, 16, true, true>;   // 6 CTAs/SM
-// Measured alternatives (C2 carrier batch, energies/s, greater by identity):
-//   algo 2 (64x32, BK16, 2 stages, swizzled) 149.2 | 7: 8 warps of 16x16 133.8 | 8: 32x32, 5 CTAs/SM 142.6 |
-//   earlier: algo 2 142.4 (before the sweep/panel work) | 64x32 BK8 4 stages padded 137.9 |
-//   32x64 BK16 swizzled 140.0 | 64x32 BK32 2 CTA/SM 133.5 | 64x32 BK16 4 CTA/SM (spills) 109.4
-// Earlier (recursion for G^>, BK8 padded family): 64x32 6-stage 2 CTA/SM 78.9 | 128x32 8 warps
-//   68.1 | 32x32 2 warps 78.2 | 32x32 4 warps (16x16) 87.4 | 64x64 16 warps 69.3 vs 90.5.
-static int g_map_cfg = 0;
+// row-mapped inversion sweeps (K <= 32): 16x16 warp tiles, 5 CTAs/SM
+using CfgMapT = Cfg<32, 32, 2, 2, 2, 5, true, 16, true, true>;
+using CfgMapT4 = Cfg<32, 32, 2, 2, 2, 5, false, 16, true, true>;  // same, 4M (algo 0)
+// Round-1 measurements that picked these (C2 carrier batch, energies/s, G^> by
+// the identity): 64x32 BK16 2 stages swizzled 149.2 | 8 warps of 16x16 133.8 |
+// 32x32 at 5 CTAs/SM 142.6 | 64x32 BK8 4 stages padded 137.9 | 32x64 BK16 140.0 |
+// 64x32 BK32 2 CTAs/SM 133.5 | 64x32 BK16 4 CTAs/SM (spills) 109.4. The
+// alternatives were removed from the library.
 
 }  // namespace
 
-// Complex-product algorithm for large tiles: 0 = 4 real products (4M),
-// 1 = 3M with 64x64 CTA tiles, 2 = 3M with 64x32 CTA tiles. Process-wide
-// setting (negf_set_gemm_algo); 3M with 64x32 tiles (2) is the default: on
-// B200 it is the fastest configuration (profiles/), and its normwise error
-// bound keeps every parity test at the 1e-9 bar.
+// Complex-product algorithm (process-wide, negf_set_gemm_algo): 2 = 3M /
+// Gauss with 64x32 tiles (default: the fastest on B200, profiles/, and its
+// normwise error bound keeps every parity test at the 1e-9 bar); 0 = 4M.
 static int g_algo = 2;
 int gemm_algo() { return g_algo; }
-// algo = 10 * m + p: product config p, row-mapped inversion-sweep config m
-// (0 = 32x32 tiles, 3M, BK 16, 5 CTAs/SM [default]; 1..5 alternatives)
-void set_gemm_algo(int a) {
-  g_map_cfg = a / 10;
-  g_algo = a % 10;
-}
+void set_gemm_algo(int a) { g_algo = a; }
 
 int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
   if (g.n <= 0) return 0;
@@ -414,46 +392,20 @@ int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
     if (g.d[i].N > mx) mx = g.d[i].N;
   }
   bool mapped = false;
-  bool m64 = true;
-  for (int i = 0; i < g.n; ++i) {
-    mapped |= g.d[i].rowmap_a || g.d[i].rowmap_c || g.d[i].rowmap_d;
-    m64 &= g.d[i].M % 64 == 0;
-  }
-  if (mapped) {  // inversion sweeps (K <= 32): occupancy wins over tile size
-    switch (g_map_cfg) {
-      case 1: return m64 ? launch_cfg<CfgMap64>(g, stream) : launch_cfg<CfgMap32>(g, stream);
-      case 2: return m64 ? launch_cfg<CfgMap64S>(g, stream) : launch_cfg<CfgMap32S>(g, stream);
-      case 3: return launch_cfg<CfgMapT4>(g, stream);
-      case 4: return launch_cfg<CfgMapU>(g, stream);
-      case 5: return launch_cfg<CfgMapV>(g, stream);
-      default: return launch_cfg<CfgMapT>(g, stream);
-    }
-  }
+  for (int i = 0; i < g.n; ++i) mapped |= g.d[i].rowmap_a || g.d[i].rowmap_c || g.d[i].rowmap_d;
+  if (mapped)  // inversion sweeps (K <= 32): occupancy wins over tile size
+    return gemm_algo() == 0 ? launch_cfg<CfgMapT4>(g, stream) : launch_cfg<CfgMapT>(g, stream);
   if (mx <= 32) return launch_cfg<CfgSmall>(g, stream);
+  if (gemm_algo() == 0) return launch_cfg<Cfg4M32>(g, stream);
   int mm = 0;
   bool real = true;  // every term has a real operand: 2-product Gauss kernel
   for (int i = 0; i < g.n; ++i) {
     mm = g.d[i].M > mm ? g.d[i].M : mm;
     for (int t = 0; t < g.d[i].nterms; ++t) real &= (g.d[i].t[t].neg & kTermReal) != 0;
   }
-  if (real && gemm_algo() == 2)
+  if (real)
     return mm <= 32 ? launch_cfg<CfgGauss2S, true>(g, stream) : launch_cfg<CfgGauss2, true>(g, stream);
-  if (mm <= 32) {  // short M
-    if (gemm_algo() == 2) return launch_cfg<CfgGauss2S>(g, stream);
-    if (gemm_algo() >= 4) return launch_cfg<CfgGauss3>(g, stream);
-  }
-  switch (gemm_algo()) {
-    case 1: return launch_cfg<CfgGauss>(g, stream);
-    case 2: return launch_cfg<CfgGauss2>(g, stream);
-    case 3: return launch_cfg<Cfg4M32>(g, stream);
-    case 4: return launch_cfg<CfgGauss3>(g, stream);
-    case 5: return launch_cfg<CfgGauss2P>(g, stream);
-    case 6: return launch_cfg<CfgG32s2>(g, stream);
-    case 7: return launch_cfg<CfgW8>(g, stream);
-    case 8: return launch_cfg<CfgT5>(g, stream);
-    case 9: return launch_cfg<CfgW8b>(g, stream);
-    default: return launch_cfg<CfgBig>(g, stream);
-  }
+  return mm <= 32 ? launch_cfg<CfgGauss2S>(g, stream) : launch_cfg<CfgGauss2>(g, stream);
 }
 
 int zgemm_launch(const ZGemmDesc& d, cudaStream_t stream) {

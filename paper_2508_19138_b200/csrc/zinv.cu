@@ -1,3 +1,4 @@
+#include <cstdlib>
 #include <type_traits>
 // Batched complex-FP64 block inversion with partial pivoting (sm_100a).
 //
@@ -755,11 +756,25 @@ size_t zinv_workspace_bytes(int n, int batch) {
   return per * batch + 256 * 8;
 }
 
+// Blocks of at least this size use the cluster panel (default: above the
+// one-CTA limit). NEGF_ZINV_CLUSTER_MIN lowers it, e.g. to 257 so that
+// 512-orbital blocks get 32-column panels split over 2 SMs (half the panels,
+// twice the SMs per matrix: what few-energy batches want).
+static int cluster_min() {
+  static int v = [] {
+    const char* e = getenv("NEGF_ZINV_CLUSTER_MIN");
+    const int x = e ? atoi(e) : 0;
+    return x > 64 ? x : kInvPanelMax + 1;
+  }();
+  return v;
+}
+static bool use_cluster(int n) { return n > kInvPanelMax || n >= cluster_min(); }
+
 int zinv_panel_width(int n) {
   // one-CTA register panel: n * (nb/16) threads <= 512; cluster panel:
   // 512 * 16 / nb rows per CTA, <= kClusterMax CTAs
   if (n <= 256) return 32;
-  if (n <= kInvPanelMax) return 16;
+  if (!use_cluster(n)) return 16;
   if (n <= 2048) return 32;
   return 16;
 }
@@ -803,7 +818,7 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
     {
       ProfScope ps_(PROF_ZINV, stream);
       ProfScope psp_(5, stream);
-      if (n <= kInvPanelMax) {
+      if (!use_cluster(n)) {
         if (nb == 32)
           zinv_panel_kernel<32><<<batch, panel_threads, 0, stream>>>(cur, cs, nxt, ns, n, k0, wd, ipiv, pinv,
                                                                      umm, map_src, map_dst, aux);

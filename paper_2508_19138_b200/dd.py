@@ -9,12 +9,16 @@ dist.py:104-127), one per rank / GPU:
    negf_dd_reverse_chain) and the Schur tail at the boundary block
    (negf_dd_schur_tail); middles: two-sided sweep (negf_dd_middle_sweep);
 2. the boundary contributions (plus each partition's right coupling blocks)
-   are all-gathered over NCCL and EVERY rank assembles and solves the reduced
-   chain of 2P-2 nodes on its own GPU (dist.py:486-561) -- no root rank, no
-   scatter of environments;
+   are all-gathered over NCCL and EVERY rank assembles the reduced chain of
+   2P-2 nodes (dist.py:486-561) and runs only the forward sweeps it needs
+   (_reduced: about one forward sweep of the chain per rank, concurrently,
+   instead of the reference's forward + backward + reversed sweep on one
+   root) -- no root rank, no scatter of environments;
 3. local recovery -- ends: backward sweep seeded with the exact boundary
    block (mode 2); middles: both corners folded with the connected
-   environments (negf_dd_fold_corner) and a local selected solve.
+   environments (negf_dd_fold_corner) and a local selected solve; then the
+   exact first block of partition r+1 goes to rank r (NCCL p2p) and one
+   backward step gives the cross blocks at each boundary.
 
 Outputs stay partition-local (plus the cross-partition blocks at each
 partition's right boundary); the reference's final gather + bcast
@@ -270,9 +274,27 @@ def _phase1(part: Partition, p_s: int, kinds: list) -> tuple[torch.Tensor, dict]
     return pay, state
 
 
-def _reduced(pays: list, plan: PartitionPlan, kinds: list) -> dict:
-    """dist.py:486-561 on the device: assemble the 2P-2 node chain from the
-    gathered payloads, forward + backward sweeps, reversed forward sweep."""
+def _sub(t, lo: int, hi: int):
+    return t[:, lo:hi].contiguous()
+
+
+def _reduced(pays: list, plan: PartitionPlan, kinds: list, rank: int | None = None) -> dict:
+    """The reduced boundary chain (dist.py:486-561) on the device, assembled
+    from the gathered payloads -- but only the sweeps ``rank`` needs.
+
+    The reference solves the 2P-2 node chain forward, backward and again
+    forward on the reversed chain, on one root rank. Every quantity phase 3
+    reads is a FORWARD-sweep value: the left environment of middle r is the
+    forward sweep at node 2r-2, its right environment the reversed sweep at
+    node 2r+1, the exact corner blocks of the end partitions are the last
+    values of the reversed (node 0) and forward (node 2P-3) sweeps, and the
+    cross blocks come from one backward step at each boundary (_cross_blocks).
+    So rank r runs the forward sweep over nodes [0, 2r] (the whole chain on the
+    last rank) and the reversed sweep over nodes [2r+1, 2P-3] ([0, ..] on rank
+    0, none on the last rank): about one forward sweep of the chain per rank
+    instead of forward + backward + reversed forward (about 3.5x fewer block
+    products), and the ranks' sweeps run concurrently. ``rank=None`` (the
+    one-process driver) runs both sweeps over the whole chain."""
     p_s, nk = plan.p_s, len(kinds)
     n_e, bs = pays[0].shape[1], pays[0].shape[-1]
     dev = pays[0].device
@@ -298,29 +320,38 @@ def _reduced(pays: list, plan: PartitionPlan, kinds: list) -> dict:
             ru[:, p0], rl[:, p0] = pay[4 + 3 * nk], pay[5 + 3 * nk]
             for i, k in enumerate(kinds):
                 rb[k][1][:, p0] = pay[6 + 3 * nk + i]
-    out = _alloc(n_e, nr, bs, kinds, dev)
-    raise_on_status(_sweeps(1, rd, ru, rl, rb, out))
-    fwd = {"x": out["xr_diag"].clone(), **{k: out[_TAG[k] + "_diag"].clone() for k in kinds}}
-    raise_on_status(_sweeps(2, rd, ru, rl, rb, out))
-    vd, vu, vl = _reverse(rd, ru, rl)
-    vb = {k: _reverse(*rb[k]) for k in kinds}
-    rev = _alloc(n_e, nr, bs, kinds, dev)
-    raise_on_status(_sweeps(1, vd, vu, vl, vb, rev))
-    return {"sol": out, "fwd": fwd, "rev": rev, "nr": nr}
+    if rank is None:
+        f_hi, r_lo = nr, 0
+    else:
+        f_hi = nr if rank == p_s - 1 else 2 * rank + 1
+        r_lo = 0 if rank == 0 else (2 * rank + 1 if rank < p_s - 1 else None)
+    fwd = _alloc(n_e, f_hi, bs, kinds, dev)
+    raise_on_status(_sweeps(1, _sub(rd, 0, f_hi), _sub(ru, 0, f_hi - 1), _sub(rl, 0, f_hi - 1),
+                            {k: (_sub(rb[k][0], 0, f_hi), _sub(rb[k][1], 0, f_hi - 1)) for k in kinds}, fwd))
+    rev = None
+    if r_lo is not None:
+        vd, vu, vl = _reverse(_sub(rd, r_lo, nr), _sub(ru, r_lo, nr - 1), _sub(rl, r_lo, nr - 1))
+        vb = {k: _reverse(_sub(rb[k][0], r_lo, nr), _sub(rb[k][1], r_lo, nr - 1)) for k in kinds}
+        rev = _alloc(n_e, nr - r_lo, bs, kinds, dev)
+        raise_on_status(_sweeps(1, vd, vu, vl, vb, rev))
+    return {"fwd": fwd, "rev": rev, "nr": nr, "chain": (rd, ru, rl, rb)}
 
 
 def _phase3(part: Partition, p_s: int, kinds: list, state: dict, red: dict, symmetrize: bool) -> dict:
     lib = _lib.load()
     n_e, bs, w = part.md.shape[0], part.md.shape[-1], part.w
     dev = part.md.device
-    sol_r, nr = red["sol"], red["nr"]
+    nr = red["nr"]
     if part.rank == 0 or part.rank == p_s - 1:
-        node = 0 if part.rank == 0 else nr - 1
+        # exact corner block: the last value of the reversed (top) / forward
+        # (bottom) sweep of the reduced chain
+        src_sw = red["rev"] if part.rank == 0 else red["fwd"]
+        last = src_sw["xr_diag"].shape[1] - 1
         mdl, mul, mll, srcl = state["chain"]
         out = state["out"]
-        out["xr_diag"][:, w - 1] = sol_r["xr_diag"][:, node]
+        out["xr_diag"][:, w - 1] = src_sw["xr_diag"][:, last]
         for k in kinds:
-            out[_TAG[k] + "_diag"][:, w - 1] = sol_r[_TAG[k] + "_diag"][:, node]
+            out[_TAG[k] + "_diag"][:, w - 1] = src_sw[_TAG[k] + "_diag"][:, last]
         raise_on_status(_sweeps(2, mdl, mul, mll, srcl, out, symmetrize=symmetrize))
         if part.rank == p_s - 1:  # back to global order (dist.py:564-584)
             d, u, lo = _reverse(out["xr_diag"], out["xr_upper"], out["xr_lower"])
@@ -336,10 +367,11 @@ def _phase3(part: Partition, p_s: int, kinds: list, state: dict, red: dict, symm
     p = _lib.ptr
     r = part.rank
     left, right_rev = 2 * r - 2, nr - 1 - (2 * r + 1)
-    envs = ((0, 0, part.left, red["fwd"]["x"][:, left].contiguous(),
-             {k: red["fwd"][k][:, left].contiguous() for k in kinds}),
-            (w - 1, 1, part.right, red["rev"]["xr_diag"][:, right_rev].contiguous(),
-             {k: red["rev"][_TAG[k] + "_diag"][:, right_rev].contiguous() for k in kinds}))
+    fw, rv = red["fwd"], red["rev"]
+    envs = ((0, 0, part.left, fw["xr_diag"][:, left].contiguous(),
+             {k: fw[_TAG[k] + "_diag"][:, left].contiguous() for k in kinds}),
+            (w - 1, 1, part.right, rv["xr_diag"][:, right_rev].contiguous(),
+             {k: rv[_TAG[k] + "_diag"][:, right_rev].contiguous() for k in kinds}))
     for j, side, halo, x_env, xl_env in envs:
         m_out, m_in, bc = halo
         rc = lib.negf_dd_fold_corner(
@@ -352,16 +384,32 @@ def _phase3(part: Partition, p_s: int, kinds: list, state: dict, red: dict, symm
                                   symmetrize=symmetrize)
 
 
-def _cross(red: dict, plan: PartitionPlan, rank: int, kinds: list) -> dict | None:
-    """Cross-partition blocks at rank's right boundary from the reduced solve."""
-    if rank >= plan.p_s - 1:
-        return None
-    p0 = 2 * rank
-    sol = red["sol"]
-    out = {"xr_upper": sol["xr_upper"][:, p0].clone(), "xr_lower": sol["xr_lower"][:, p0].clone()}
+def _cross_blocks(red: dict, rank: int, kinds: list, nxt: dict) -> dict:
+    """Cross-partition blocks at rank's right boundary (reduced nodes 2r and
+    2r+1): one backward RGF step (rgf.py:152-229) on the 2-node chain, seeded
+    with the forward-sweep values at node 2r and the EXACT diagonal blocks of
+    node 2r+1 -- the first block of partition r+1 after its phase 3 (``nxt``:
+    its xr_diag / xl_diag / xg_diag at local block 0)."""
+    rd, ru, rl, rb = red["chain"]
+    fw = red["fwd"]
+    n0 = 2 * rank
+    n_e, bs = rd.shape[0], rd.shape[-1]
+    out = _alloc(n_e, 2, bs, kinds, rd.device)
+    out["xr_diag"][:, 0] = fw["xr_diag"][:, n0]
+    out["xr_diag"][:, 1] = nxt["xr_diag"]
     for k in kinds:
-        out[_TAG[k] + "_upper"] = sol[_TAG[k] + "_upper"][:, p0].clone()
-    return out
+        out[_TAG[k] + "_diag"][:, 0] = fw[_TAG[k] + "_diag"][:, n0]
+        out[_TAG[k] + "_diag"][:, 1] = nxt[_TAG[k] + "_diag"]
+    raise_on_status(_sweeps(2, _sub(rd, n0, n0 + 2), _sub(ru, n0, n0 + 1), _sub(rl, n0, n0 + 1),
+                            {k: (_sub(rb[k][0], n0, n0 + 2), _sub(rb[k][1], n0, n0 + 1)) for k in kinds}, out))
+    cr = {"xr_upper": out["xr_upper"][:, 0].clone(), "xr_lower": out["xr_lower"][:, 0].clone()}
+    for k in kinds:
+        cr[_TAG[k] + "_upper"] = out[_TAG[k] + "_upper"][:, 0].clone()
+    return cr
+
+
+def _first_blocks(loc: dict, kinds: list) -> dict:
+    return {key: loc[key][:, 0].contiguous() for key in ["xr_diag"] + [_TAG[k] + "_diag" for k in kinds]}
 
 
 # -- drivers -----------------------------------------------------------------------------
@@ -381,8 +429,26 @@ def dd_selected_solve_batched(part: Partition, plan: PartitionPlan, group=None, 
     gathered = torch.empty(p_s * flat.numel(), dtype=flat.dtype, device=flat.device)
     dist.all_gather_into_tensor(gathered, flat, group=group)
     pays = [torch.view_as_complex(x.view(-1, 2)).view(pay.shape) for x in gathered.chunk(p_s)]
-    red = _reduced(pays, plan, kinds)
-    return _phase3(part, p_s, kinds, state, red, symmetrize), _cross(red, plan, part.rank, kinds)
+    red = _reduced(pays, plan, kinds, part.rank)
+    loc = _phase3(part, p_s, kinds, state, red, symmetrize)
+    # the exact first block of partition r+1 travels to rank r (NCCL p2p) for
+    # the cross blocks at r's right boundary
+    mine = _first_blocks(loc, kinds)
+    keys = sorted(mine)
+    ops = []
+    nxt = None
+    if part.rank > 0:
+        ops += [dist.P2POp(dist.isend, torch.view_as_real(mine[k]), dist.get_global_rank(group, part.rank - 1)
+                           if group is not None else part.rank - 1, group) for k in keys]
+    if part.rank < p_s - 1:
+        nxt = {k: torch.empty_like(mine[k]) for k in keys}
+        ops += [dist.P2POp(dist.irecv, torch.view_as_real(nxt[k]), dist.get_global_rank(group, part.rank + 1)
+                           if group is not None else part.rank + 1, group) for k in keys]
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    cr = _cross_blocks(red, part.rank, kinds, nxt) if nxt is not None else None
+    return loc, cr
 
 
 def dd_selected_solve_local(md, mu, ml, src: dict, plan: PartitionPlan, symmetrize: bool = False) -> dict:
@@ -396,7 +462,8 @@ def dd_selected_solve_local(md, mu, ml, src: dict, plan: PartitionPlan, symmetri
     ph1 = [_phase1(p, p_s, kinds) for p in parts]
     red = _reduced([x[0] for x in ph1], plan, kinds)
     locs = [_phase3(parts[r], p_s, kinds, ph1[r][1], red, symmetrize) for r in range(p_s)]
-    crosses = [_cross(red, plan, r, kinds) for r in range(p_s)]
+    crosses = [_cross_blocks(red, r, kinds, _first_blocks(locs[r + 1], kinds)) if r < p_s - 1 else None
+               for r in range(p_s)]
     return assemble(locs, crosses, plan, kinds)
 
 

@@ -23,7 +23,7 @@ def test_energy_sharded_scba_matches_reference(cuda):
                           str(min(n, 4)), str(ROOT / "tools" / "dist_check.py")],
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
-    assert "DIST_CHECK" in out.stdout and "DIST_CHECK_3IT" in out.stdout
+    assert "DIST_CHECK" in out.stdout and "DIST_CHECK_3IT" in out.stdout and "DIST_CHECK_CUTOFF" in out.stdout
 
 
 def test_energy_sharded_scba_all_to_all_only(cuda):

@@ -73,4 +73,24 @@ if comm.rank == 0:
           f"{os.environ.get('NEGF_PEER_TRANSPOSE', '1')} spatial={int(spatial)}")
     # spatial: the partitioned elimination rounds differently from the sequential sweep
     assert w3 < (1e-9 if spatial else 1e-12)
+# energy-sharded extras (not spatial): the r_cut entry set (table-driven
+# layout + NCCL all-to-all) and the gathered device observables vs one GPU
+if not spatial:
+    optc = ScbaOptions(retarded_method="sancho", max_iter=2, tol=1e-12, batch=40,
+                       memoizer=MemoizerOptions(enabled=False), entry_cutoff=20)
+    argc = args[:5] + (optc,)
+    rc_ = scba_run(*argc, device=dev, comm=comm)
+    sig = {f: rc_["sigma_" + f] for f in ("lesser", "greater")}
+    parts = [None] * comm.size
+    dist.all_gather_object(parts, (rc_["energy_slice"].start, sig))
+    if comm.rank == 0:
+        parts.sort(key=lambda x: x[0])
+        one = scba_run(*argc, device=dev)
+        wc = max(rel(np.concatenate([p[1][f] for p in parts], axis=1), one["sigma_" + f]) for f in sig)
+        wc = max(wc, rel(rc_["residuals"], one["residuals"]))
+        wo = max(rel(rc_.observables[k], one.observables[k]) for k in ("dos", "density", "current_spectrum"))
+        wo = max(wo, abs(rc_.observables["terminal_left"] - one.observables["terminal_left"])
+                 / abs(one.observables["terminal_left"]))
+        print(f"DIST_CHECK_CUTOFF world={comm.size} worst_rel_vs_1gpu={wc:.3e} observables_rel={wo:.3e}")
+        assert wc < 1e-12 and wo < 1e-12
 dist.destroy_process_group()
