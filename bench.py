@@ -376,7 +376,10 @@ def run_native(args):
 
     release()
     c4 = None
-    if args.c4:  # first of the GW legs: it needs nearly the whole 180 GB
+    if args.c4 and world > 1:
+        c4 = {"skipped": "single-GPU leg (one C4 energy pair needs ~180 GB of one B200; the energy-sharded run "
+                         "adds symmetric-memory exchange buffers)"}
+    if args.c4 and world == 1:  # first of the GW legs: it needs nearly the whole 180 GB
         try:
             c4 = run_gw_rate(args.c4, 1, dev, world, rank, barrier, "C4 NRFET-scale shape (BASELINE configs[3] device)",
                              peak=peak)

@@ -134,6 +134,10 @@ __device__ __forceinline__ void dft_r(z_t* e) {
 // PACK_T threads, each row with its own shared-memory slice: one row per CTA
 // at L = 16 would run 2 of 32 threads and launch one CTA per entry row.
 constexpr int PACK_T = 128;
+#ifndef NEGF_CONV_PACK_MINB
+#define NEGF_CONV_PACK_MINB 3
+#endif
+constexpr int kPackMinB = NEGF_CONV_PACK_MINB;  // resident CTAs per SM of the packed-row kernels
 
 __host__ __device__ __forceinline__ int rows_per_cta(int L, int E) {
   const int q = L / E;
@@ -301,7 +305,7 @@ __device__ void retarded_tail(z_t* d, z_t* A, z_t* B, const RowGeom<E>& g, int n
 }
 
 template <int E, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? 3 : MAXT == 256 ? 2 : 1) pol_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg, int n,
+__global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? kPackMinB : MAXT == 256 ? 2 : 1) pol_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg, int n,
                                                    int L, const z_t* __restrict__ tw, const z_t* __restrict__ kf,
                                                    const z_t* __restrict__ kcf,
                                                    const unsigned char* __restrict__ diag, double2 scale, z_t* pl,
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? 3 : MAXT == 256 ? 2 : 1
 }
 
 template <int E, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? 3 : MAXT == 256 ? 2 : 1) sigma_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg,
+__global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? kPackMinB : MAXT == 256 ? 2 : 1) sigma_kernel(const z_t* __restrict__ gl, const z_t* __restrict__ gg,
                                                      const z_t* __restrict__ wl, const z_t* __restrict__ wg,
                                                      const long long* __restrict__ w_rows, int n, int L,
                                                      const z_t* __restrict__ tw, const z_t* __restrict__ kf,
@@ -635,7 +639,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
 
 // Generic convolve_energy (convolve.py:39-71): mode 0 convolution, 1 correlation.
 template <int E, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? 3 : MAXT == 256 ? 2 : 1) conv_kernel(const z_t* __restrict__ x1, const z_t* __restrict__ x2, int n,
+__global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? kPackMinB : MAXT == 256 ? 2 : 1) conv_kernel(const z_t* __restrict__ x1, const z_t* __restrict__ x2, int n,
                                                     int L, int mode, const z_t* __restrict__ tw, double2 scale,
                                                     z_t* out, long long n_rows) {
   extern __shared__ __align__(16) z_t sm[];
@@ -670,7 +674,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? 3 : MAXT == 256 ? 2 : 1
 }
 
 template <int E, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? 3 : MAXT == 256 ? 2 : 1) ret_kernel(const z_t* __restrict__ xl, const z_t* __restrict__ xg, int n,
+__global__ void __launch_bounds__(MAXT, MAXT == PACK_T ? kPackMinB : MAXT == 256 ? 2 : 1) ret_kernel(const z_t* __restrict__ xl, const z_t* __restrict__ xg, int n,
                                                    int L, const z_t* __restrict__ tw, const z_t* __restrict__ kf,
                                                    z_t* out, long long n_rows) {
   extern __shared__ __align__(16) z_t sm[];

@@ -751,30 +751,36 @@ bool attr_once(const void* fn, int bytes, unsigned* done_mask) {
 
 size_t zinv_workspace_bytes(int n, int batch) {
   if (n <= kInvSmallMax) return 0;
-  const int nb = zinv_panel_width(n);
+  const int nb = zinv_panel_width(n, batch);
   size_t per = 4 * sizeof(int) * (size_t)n + sizeof(double) * 2 + sizeof(z_t) * (size_t)nb * nb;
   return per * batch + 256 * 8;
 }
 
-// Blocks of at least this size use the cluster panel (default: above the
-// one-CTA limit). NEGF_ZINV_CLUSTER_MIN lowers it, e.g. to 257 so that
-// 512-orbital blocks get 32-column panels split over 2 SMs (half the panels,
-// twice the SMs per matrix: what few-energy batches want).
+// Which panel kernel a (n, batch) inverse uses. Above 512 only the cluster
+// panel exists. For 256 < n <= 512 the cluster panel (32-column panels, 2 CTAs
+// of 256 rows per matrix) halves the panel count and gives the sweeps K = 32,
+// which wins once the batch fills the GPU (128 x 512^2: 9.4 vs 12.6 ms), while
+// at 8-16 matrices its per-column cluster barrier costs more than it gains
+// (2.0 vs 1.8 ms; profiles/zinv_cluster_r02.txt). NEGF_ZINV_CLUSTER_MIN=n
+// forces the cluster panel for blocks >= n at any batch.
 static int cluster_min() {
   static int v = [] {
     const char* e = getenv("NEGF_ZINV_CLUSTER_MIN");
     const int x = e ? atoi(e) : 0;
-    return x > 64 ? x : kInvPanelMax + 1;
+    return x > 256 ? x : kInvClusterMax + 1;
   }();
   return v;
 }
-static bool use_cluster(int n) { return n > kInvPanelMax || n >= cluster_min(); }
+constexpr int kClusterBatchMin = 64;
+static bool use_cluster(int n, int batch) {
+  return n > kInvPanelMax || (n > 256 && (batch >= kClusterBatchMin || n >= cluster_min()));
+}
 
-int zinv_panel_width(int n) {
+int zinv_panel_width(int n, int batch) {
   // one-CTA register panel: n * (nb/16) threads <= 512; cluster panel:
   // 512 * 16 / nb rows per CTA, <= kClusterMax CTAs
   if (n <= 256) return 32;
-  if (!use_cluster(n)) return 16;
+  if (!use_cluster(n, batch)) return 16;
   if (n <= 2048) return 32;
   return 16;
 }
@@ -794,7 +800,7 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
     return 0;
   }
   if (lds != n || ldx != n) return -2;  // blocked path works on packed matrices
-  const int nb = zinv_panel_width(n);
+  const int nb = zinv_panel_width(n, batch);
   if (ws_bytes < zinv_workspace_bytes(n, batch)) return -4;
   if (n > kInvClusterMax) return -5;
   // carve workspace
@@ -818,7 +824,7 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
     {
       ProfScope ps_(PROF_ZINV, stream);
       ProfScope psp_(5, stream);
-      if (!use_cluster(n)) {
+      if (!use_cluster(n, batch)) {
         if (nb == 32)
           zinv_panel_kernel<32><<<batch, panel_threads, 0, stream>>>(cur, cs, nxt, ns, n, k0, wd, ipiv, pinv,
                                                                      umm, map_src, map_dst, aux);

@@ -17,7 +17,7 @@ struct InvAux {
   const int* active;  // optional per-batch mask (skip matrices with active[b]==0)
 };
 
-int zinv_panel_width(int n);
+int zinv_panel_width(int n, int batch);
 size_t zinv_workspace_bytes(int n, int batch);
 // S is destroyed for n > 64. X must not alias S.
 int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, int n, int batch,

@@ -7,7 +7,7 @@ oracle restatement.
   ballistic, 4 energies over [-2, 2] eV, G^> by its own recursion (the
   reference algorithm) and by the identity (the bench's fast option).
 * C3 (configs[2] device): chain_device(64, 512) + coulomb_matrix, full GW
-  scba_run, 3 energies (-1, 0, 1 eV), 2 iterations, Sancho, memoizer off.
+  scba_run, 2 energies (-0.5, 0.5 eV), 2 iterations, Sancho, memoizer off.
 
 Full arrays at these shapes are GBs, so the fixtures hold per-(energy, block)
 weighted sums and norms plus 4096 sampled elements per field; all are
