@@ -362,23 +362,28 @@ def beyn_batched(m: torch.Tensor, n: torch.Tensor, n_prime: torch.Tensor, n_quad
     target = m.clone()
     modes = np.zeros(batch, dtype=np.int64)
     f_all = torch.zeros_like(m)
-    for b in range(batch):
-        if decoupled[b] or not sig_h[b, 0] > 0:
-            continue
-        rank = int(np.sum(sig_h[b] > svd_tol * sig_h[b, 0]))
-        if rank == 0:
-            continue
-        ub = u[b, :, :rank]
-        w_red = vh[b].conj().T[:, :rank]
-        b_small = (ub.conj().T @ a1[b] @ w_red) / sig[b, :rank]
+    # Reduced problems batched by numerical rank (cuSOLVER batched SVD /
+    # eig / pinv through torch.linalg): the decaying modes (|mu| < 1) are
+    # selected by zeroing the other eigenvector columns -- pinv of [Phi 0] is
+    # [pinv(Phi); 0], so F = Phi diag(mu) Phi^+ equals the per-problem form
+    # that drops them (obc.py:260-296).
+    valid = (~decoupled) & (sig_h[:, 0] > 0)
+    ranks = np.where(valid, np.sum(sig_h > svd_tol * sig_h[:, :1], axis=1), 0)
+    for r in np.unique(ranks[ranks > 0]):
+        idx_h = np.flatnonzero(ranks == r)
+        idx = torch.from_numpy(idx_h).to(dev)
+        ub = u[idx, :, :r]
+        w_red = vh[idx].conj().transpose(-1, -2)[:, :, :r]
+        b_small = (ub.conj().transpose(-1, -2) @ a1[idx] @ w_red) / sig[idx, :r].unsqueeze(-2)
         mu, vecs = torch.linalg.eig(b_small)
         keep = mu.abs() < 1.0 - 1e-8
-        mu, vecs = mu[keep], vecs[:, keep]
-        if mu.numel() == 0:
-            continue
-        phi = ub @ vecs
-        f_all[b] = (phi * mu[None, :]) @ torch.linalg.pinv(phi, rtol=1e-15)
-        modes[b] = int(mu.numel())
+        mu = mu * keep
+        phi = ub @ (vecs * keep.unsqueeze(-2))
+        f = (phi * mu.unsqueeze(-2)) @ torch.linalg.pinv(phi, rtol=1e-15)
+        n_keep = keep.sum(-1)
+        has = n_keep > 0
+        f_all[idx[has]] = f[has]
+        modes[idx_h] = n_keep.cpu().numpy()
     # x = (m + n F)^-1 (problems without modes keep F = 0: x = m^-1)
     st_ = _lib.stream_ptr(dev)
     rc = lib.negf_zgemm_batched(bs, bs, bs, batch, 1.0, 0.0, n.data_ptr(), bs * bs, bs, 0, f_all.data_ptr(),

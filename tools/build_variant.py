@@ -1,5 +1,5 @@
 """Build an experimental variant of the library with extra -D flags into
-paper_2508_19138_b200/exp/<name>.so (load it with NEGF_B200_LIB=...).
+paper_2508_19138_b200/variants/<name>.so (load it with NEGF_B200_LIB=...).
 Usage: python tools/build_variant.py NAME -DFOO -DBAR"""
 import subprocess, sys
 from pathlib import Path
@@ -7,7 +7,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 from paper_2508_19138_b200 import build as B
 name, flags = sys.argv[1], sys.argv[2:]
-out = ROOT / "paper_2508_19138_b200" / "exp"
+out = ROOT / "paper_2508_19138_b200" / "variants"  # travels with gpurun (*.so stays git-ignored)
 obj = ROOT / "build" / "exp" / name
 out.mkdir(parents=True, exist_ok=True); obj.mkdir(parents=True, exist_ok=True)
 nvcc = B._nvcc()

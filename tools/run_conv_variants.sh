@@ -1,5 +1,5 @@
 # conv roofline (bench.conv_roofline) with the default library and packed-row occupancy variants
-for lib in "" paper_2508_19138_b200/exp/pack4.so paper_2508_19138_b200/exp/pack5.so; do
+for lib in "" paper_2508_19138_b200/variants/pack4.so paper_2508_19138_b200/variants/pack5.so; do
   echo "== lib ${lib:-default}"
   NEGF_B200_LIB=${lib:-$PWD/paper_2508_19138_b200/libnegf_b200.so} timeout 300 python -c "
 import sys, json, torch; sys.argv=['x']; sys.path.insert(0,'.')
