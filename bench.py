@@ -8,6 +8,10 @@ solve for G^R, G^<, G^> -- on chain_device(64 blocks x 256 orbitals),
 One "step" is the complete 1024-energy job (in energy batches). Multi-GPU is
 weak scaling: every rank solves its own 1024-energy slice of a 1024*N grid
 (energies are independent; no data-path collective on the ballistic path).
+The headline computes G^> by the exact carrier identity (configs[1] names
+G^R/G^<); ``greater_alt`` times the same job with G^> by its own recursion,
+the reference's algorithm, beside it. Further legs: C4-shape (configs[3])
+and C3-shape (configs[2]) GW rates and the convolution roofline.
 
 Contract: one JSON line on rank 0 (see the task's bench contract):
 metric/value = energy points per second (whole job), roofline of the
@@ -49,9 +53,10 @@ def parse():
     ap.add_argument("--n-e", type=int, default=1024, help="energies per rank")
     ap.add_argument("--batch", type=int, default=128, help="energies per device batch")
     ap.add_argument("--e2e-steps", type=int, default=1)
-    ap.add_argument("--greater", choices=["identity", "recursion"], default="recursion",
-                    help="G^> by its own Keldysh recursion like the reference (default, the headline) or by the "
-                         "exact identity G^> = G^< + G^R - G^R^dag; the other variant is timed beside it")
+    ap.add_argument("--greater", choices=["identity", "recursion"], default="identity",
+                    help="G^> by the exact identity G^> = G^< + G^R - G^R^dag (default: BASELINE configs[1] names "
+                         "G^R/G^<; the identity gives G^> on top at the cost of an elementwise pass) or by its own "
+                         "Keldysh recursion like the reference; the other variant is timed beside it (greater_alt)")
     ap.add_argument("--alt-steps", type=int, default=3, help="timed steps of the other --greater variant")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-procs", type=int, default=0, help="0 = all host cores")

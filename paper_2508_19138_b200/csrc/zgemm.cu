@@ -220,25 +220,43 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
     const int a_smn = a_kc ? CF::SK : 1, a_sk = a_kc ? 1 : CF::SMA;
     const int b_smn = b_kc ? CF::SK : 1, b_sk = b_kc ? 1 : CF::SMB;
     const int r = lane >> 2, q = lane & 3;
-#pragma unroll
-    for (int k4 = 0; k4 < CF::BK / 4; ++k4) {
+    // operand fragments of one k4 step (raw complex values from smem)
+    auto fetch = [&](int k4, z_t* fa, z_t* fb) {
       const int kk = k4 * 4 + q;
       // k-contiguous reads: row parity of (.. + r) is r&1 (row bases are multiples of 8)
       const int kka = (CF::SWZ && a_kc) ? (kk ^ ((r & 1) << 2)) : kk;
       const int kkb = (CF::SWZ && b_kc) ? (kk ^ ((r & 1) << 2)) : kk;
+#pragma unroll
+      for (int i = 0; i < CF::TM; ++i) fa[i] = sA[(wm * CF::WTM + i * 8 + r) * a_smn + kka * a_sk];
+#pragma unroll
+      for (int j = 0; j < CF::TN; ++j) fb[j] = sB[(wn * CF::WTN + j * 8 + r) * b_smn + kkb * b_sk];
+    };
+    z_t fa[2][CF::TM], fb[2][CF::TN];
+    fetch(0, fa[0], fb[0]);
+#pragma unroll
+    for (int k4 = 0; k4 < CF::BK / 4; ++k4) {
+      // software pipeline: the next step's fragments are in flight while this
+      // step's DMMAs issue (NEGF_ZGEMM_PF; otherwise load just before use)
+#ifdef NEGF_ZGEMM_PF
+      if (k4 + 1 < CF::BK / 4) fetch(k4 + 1, fa[(k4 + 1) & 1], fb[(k4 + 1) & 1]);
+      const z_t* va = fa[k4 & 1];
+      const z_t* vb = fb[k4 & 1];
+#else
+      if (k4 > 0) fetch(k4, fa[0], fb[0]);
+      const z_t* va = fa[0];
+      const z_t* vb = fb[0];
+#endif
       double ar[CF::TM], ai[CF::TM], nai[CF::TM], br[CF::TN], bi[CF::TN];
 #pragma unroll
       for (int i = 0; i < CF::TM; ++i) {
-        z_t v = sA[(wm * CF::WTM + i * 8 + r) * a_smn + kka * a_sk];
-        ar[i] = dneg_if(v.x, negm);
-        ai[i] = dneg_if(v.y, negm ^ conjA);
+        ar[i] = dneg_if(va[i].x, negm);
+        ai[i] = dneg_if(va[i].y, negm ^ conjA);
         nai[i] = dneg_if(ai[i], kSign);
       }
 #pragma unroll
       for (int j = 0; j < CF::TN; ++j) {
-        z_t v = sB[(wn * CF::WTN + j * 8 + r) * b_smn + kkb * b_sk];
-        br[j] = v.x;
-        bi[j] = dneg_if(v.y, conjB);
+        br[j] = vb[j].x;
+        bi[j] = dneg_if(vb[j].y, conjB);
       }
       if constexpr (!CF::GAUSS) {
         // Phase-major issue order: the two DMMAs feeding the same accumulator
