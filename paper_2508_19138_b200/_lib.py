@@ -124,6 +124,9 @@ def load(require_gpu: bool = True) -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        algo = os.environ.get("NEGF_GEMM_ALGO")  # experiments: 0 = 4M, 2 = 3M cp.async, 3 = 3M bulk copies
+        if algo is not None and lib.negf_set_gemm_algo(int(algo)) != 0:
+            raise NativeLibraryError(f"NEGF_GEMM_ALGO={algo} is not a GEMM algorithm of this library")
         _lib = lib
     return _lib
 
@@ -133,7 +136,8 @@ def exported_symbols() -> list[str]:
 
 
 _CODES = {-1: "invalid argument", -2: "unsupported leading dimension", -4: "workspace too small",
-          -5: "block size above 512 (the pivoted inverse's register panel is one CTA)"}
+          -5: "size above the kernel's limit (pivoted inverse: 4096 orbitals; fused convolutions: 4096 energies)",
+          -6: "could not set the kernel's shared-memory attribute"}
 
 
 def check(rc: int, what: str) -> None:

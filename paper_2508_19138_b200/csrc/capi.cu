@@ -18,7 +18,7 @@ int negf_set_rgf_overlap(int on) {
 }
 
 int negf_set_gemm_algo(int algo) {
-  if (algo != 0 && algo != 2) return -1;
+  if (algo != 0 && algo != 2 && algo != 3) return -1;
   set_gemm_algo(algo);
   return 0;
 }

@@ -376,6 +376,304 @@ int launch_cfg(const ZGemmGroup& g, cudaStream_t stream) {
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised variant: operand tiles move global -> smem on the TMA
+// engine (cp.async.bulk, one bulk copy per contiguous tile row, completion
+// counted in bytes on an mbarrier) through a STAGES-deep ring of
+// full / empty mbarriers: one producer warp arms and issues the copies, the
+// 4 consumer warps wait on "full", run the DMMA step, and release the slot on
+// "empty" -- no __syncthreads and no per-thread LDGSTS address streams in the
+// main loop. Bulk copies land rows contiguously, so the k-contiguous tiles use
+// the +4 pad (conflict-free fragment reads) instead of the XOR swizzle.
+// Row-mapped problems (inversion sweeps) stay on the cp.async kernel.
+template <int BM_, int BN_, int BK_, int STAGES_, int MINB_>
+struct BulkCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int WM = 2, WN = 2, NCW = WM * WN;  // consumer warps
+  static constexpr int NT = (NCW + 1) * 32;            // + one producer warp
+  static constexpr int WTM = BM / WM, WTN = BN / WN, TM = WTM / 8, TN = WTN / 8;
+  static constexpr int SK = BK + 4, SMA = BM + 2, SMB = BN + 2;
+  static constexpr int A_ELEMS = (BM * SK > BK * SMA) ? BM * SK : BK * SMA;
+  static constexpr int B_ELEMS = (BN * SK > BK * SMB) ? BN * SK : BK * SMB;
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_ELEMS * sizeof(z_t) + 2 * STAGES * sizeof(unsigned long long);
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Producer side of one stage: every tile row of A and B as a bulk copy.
+template <class CF>
+__device__ __forceinline__ void bulk_stage(const ZGemmDesc& d, int kt, const KtBounds& kb, int b, int m0, int n0,
+                                           z_t* sA, z_t* sB, unsigned long long* full, int lane) {
+  const int term = kb.term(kt);
+  const ZTerm& t = d.t[term];
+  const int k0 = (kt - kb.base(term)) * CF::BK;
+  const z_t* A = t.A + (long long)b * t.sA;
+  const z_t* B = t.B + (long long)b * t.sB;
+  const int K = t.K, M = d.M, N = d.N;
+  const int vk = K - k0 < CF::BK ? K - k0 : CF::BK;
+  // zero tails first (generic stores), then arm the barrier, then the copies
+  auto rows = [&](auto&& fn) {  // fn(dst, src, cnt, len) for every row of both operands
+    if (!op_trans(t.opA)) {  // [M][K]: BM rows of BK
+      for (int r = lane; r < CF::BM; r += 32) {
+        const int gm = m0 + r;
+        fn(sA + r * CF::SK, A + (long long)gm * t.lda + k0, gm < M ? vk : 0, CF::BK);
+      }
+    } else {  // [K][M]: BK rows of BM
+      const int vm = M - m0 < CF::BM ? M - m0 : CF::BM;
+      for (int r = lane; r < CF::BK; r += 32) {
+        const int gk = k0 + r;
+        fn(sA + r * CF::SMA, A + (long long)gk * t.lda + m0, gk < K ? vm : 0, CF::BM);
+      }
+    }
+    if (!op_trans(t.opB)) {  // [K][N]: BK rows of BN
+      const int vn = N - n0 < CF::BN ? N - n0 : CF::BN;
+      for (int r = lane; r < CF::BK; r += 32) {
+        const int gk = k0 + r;
+        fn(sB + r * CF::SMB, B + (long long)gk * t.ldb + n0, gk < K ? vn : 0, CF::BN);
+      }
+    } else {  // [N][K]: BN rows of BK
+      for (int r = lane; r < CF::BN; r += 32) {
+        const int gn = n0 + r;
+        fn(sB + r * CF::SK, B + (long long)gn * t.ldb + k0, gn < N ? vk : 0, CF::BK);
+      }
+    }
+  };
+  unsigned bytes = 0;
+  rows([&](z_t* dst, const z_t*, int cnt, int len) {
+    for (int e = cnt > 0 ? cnt : 0; e < len; ++e) dst[e] = make_double2(0.0, 0.0);
+    bytes += cnt > 0 ? (unsigned)cnt * 16u : 0u;
+  });
+  bytes = __reduce_add_sync(0xffffffffu, bytes);
+  __syncwarp();
+  if (lane == 0) mbar_arrive_tx(full, bytes);
+  __syncwarp();
+  rows([&](z_t* dst, const z_t* src, int cnt, int) {
+    if (cnt > 0) bulk_g2s(dst, src, (unsigned)cnt * 16u, full);
+  });
+}
+
+template <class CF, bool RV = false>
+__global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_bulk_kernel(const __grid_constant__ ZGemmGroup grp) {
+  extern __shared__ __align__(16) z_t smem[];
+  const ZGemmDesc& d = grp.d[blockIdx.z];
+  const int tiles_n = (d.N + CF::BN - 1) / CF::BN;
+  const int tiles_m = (d.M + CF::BM - 1) / CF::BM;
+  if ((int)blockIdx.x >= tiles_m * tiles_n || (int)blockIdx.y >= d.batch) return;
+  if (d.active && !d.active[blockIdx.y]) return;
+  const int b = blockIdx.y;
+  const int m0 = (blockIdx.x / tiles_n) * CF::BM;
+  const int n0 = (blockIdx.x % tiles_n) * CF::BN;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + CF::STAGES * CF::STAGE_ELEMS);
+  unsigned long long* empty = full + CF::STAGES;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < CF::STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, CF::NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  KtBounds kb;
+  {
+    auto nk = [&](int i) { return i < d.nterms ? (d.t[i].K + CF::BK - 1) / CF::BK : 0; };
+    kb.b1 = nk(0);
+    kb.b2 = kb.b1 + nk(1);
+    kb.b3 = kb.b2 + nk(2);
+  }
+  const int KT = kb.b3 + (d.nterms > 3 ? (d.t[3].K + CF::BK - 1) / CF::BK : 0);
+  auto stageA = [&](int s) { return smem + s * CF::STAGE_ELEMS; };
+  auto stageB = [&](int s) { return smem + s * CF::STAGE_ELEMS + CF::A_ELEMS; };
+
+  if (warp == CF::NCW) {  // producer warp
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = kt % CF::STAGES, u = kt / CF::STAGES;
+      if (u > 0) mbar_wait(empty + s, (u - 1) & 1);
+      bulk_stage<CF>(d, kt, kb, b, m0, n0, stageA(s), stageB(s), full + s, lane);
+    }
+    return;
+  }
+
+  const int wm = warp / CF::WN, wn = warp % CF::WN;
+  double acc_re[CF::TM][CF::TN][2], acc_im[CF::TM][CF::TN][2], acc_s[CF::TM][CF::TN][2];
+#pragma unroll
+  for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+    for (int j = 0; j < CF::TN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) acc_re[i][j][h] = acc_im[i][j][h] = acc_s[i][j][h] = 0.0;
+  const int r = lane >> 2, q = lane & 3;
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % CF::STAGES;
+    mbar_wait(full + s, (kt / CF::STAGES) & 1);
+    const z_t* sA = stageA(s);
+    const z_t* sB = stageB(s);
+    const ZTerm& t = d.t[kb.term(kt)];
+    const bool a_kc = !op_trans(t.opA);
+    const bool b_kc = op_trans(t.opB);
+    const unsigned long long negm = (t.neg & 1) ? kSign : 0ull;
+    const unsigned long long conjA = op_conj(t.opA) ? kSign : 0ull;
+    const unsigned long long conjB = op_conj(t.opB) ? kSign : 0ull;
+    const int a_smn = a_kc ? CF::SK : 1, a_sk = a_kc ? 1 : CF::SMA;
+    const int b_smn = b_kc ? CF::SK : 1, b_sk = b_kc ? 1 : CF::SMB;
+#pragma unroll
+    for (int k4 = 0; k4 < CF::BK / 4; ++k4) {
+      const int kk = k4 * 4 + q;
+      double ar[CF::TM], ai[CF::TM], br[CF::TN], bi[CF::TN], as[CF::TM], bsum[CF::TN];
+#pragma unroll
+      for (int i = 0; i < CF::TM; ++i) {
+        const z_t v = sA[(wm * CF::WTM + i * 8 + r) * a_smn + kk * a_sk];
+        ar[i] = dneg_if(v.x, negm);
+        ai[i] = dneg_if(v.y, negm ^ conjA);
+        as[i] = ar[i] + ai[i];
+      }
+#pragma unroll
+      for (int j = 0; j < CF::TN; ++j) {
+        const z_t v = sB[(wn * CF::WTN + j * 8 + r) * b_smn + kk * b_sk];
+        br[j] = v.x;
+        bi[j] = dneg_if(v.y, conjB);
+        bsum[j] = br[j] + bi[j];
+      }
+      // 3M: acc_re <- ar br, acc_im <- ai bi, acc_s <- (ar+ai)(br+bi)
+#pragma unroll
+      for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+        for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
+      if constexpr (!RV) {
+#pragma unroll
+        for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+          for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], bi[j]);
+      }
+#pragma unroll
+      for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+        for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_s[i][j][0], acc_s[i][j][1], as[i], bsum[j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);
+  }
+
+  // Epilogue: value = alpha*acc + beta*C, stored plain or conj-transposed.
+  const double2 al = d.alpha, be = d.beta;
+  const bool use_c = d.C != nullptr && (be.x != 0.0 || be.y != 0.0);
+  const z_t* C = use_c ? d.C + (long long)b * d.sC : nullptr;
+  z_t* D = d.D + (long long)b * d.sD;
+  const int er = lane >> 2, eq = lane & 3;
+#pragma unroll
+  for (int i = 0; i < CF::TM; ++i) {
+    const int gm = m0 + wm * CF::WTM + i * 8 + er;
+    z_t cv[CF::TN][2];
+#pragma unroll
+    for (int j = 0; j < CF::TN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gn = n0 + wn * CF::WTN + j * 8 + 2 * eq + h;
+        cv[j][h] = (use_c && gm < d.M && gn < d.N) ? C[(long long)gm * d.ldc + gn] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+    for (int j = 0; j < CF::TN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gn = n0 + wn * CF::WTN + j * 8 + 2 * eq + h;
+        if (gm < d.M && gn < d.N) {
+          const double p1 = acc_re[i][j][h], p2 = acc_im[i][j][h];
+          const double xr = p1 - p2, xi = acc_s[i][j][h] - p1 - p2;
+          z_t v = zmake(al.x * xr - al.y * xi, al.x * xi + al.y * xr);
+          const z_t c = cv[j][h];
+          v.x += be.x * c.x - be.y * c.y;
+          v.y += be.x * c.y + be.y * c.x;
+          if (d.transD)
+            D[(long long)gn * d.ldd + gm] = zconj(v);
+          else
+            D[(long long)gm * d.ldd + gn] = v;
+        }
+      }
+  }
+}
+
+template <class CF, bool RV = false>
+int launch_bulk(const ZGemmGroup& g, cudaStream_t stream) {
+  static unsigned long long attr_done = 0;
+  int dev = 0;
+  NEGF_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev >= 64) return -1;
+  if (!(__atomic_load_n(&attr_done, __ATOMIC_ACQUIRE) & (1ull << dev))) {
+    NEGF_CUDA_CHECK(cudaFuncSetAttribute(zgemm_bulk_kernel<CF, RV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)CF::SMEM));
+    __atomic_fetch_or(&attr_done, 1ull << dev, __ATOMIC_RELEASE);
+  }
+  int max_tiles = 0, max_batch = 0;
+  for (int i = 0; i < g.n; ++i) {
+    int tm = (g.d[i].M + CF::BM - 1) / CF::BM, tn = (g.d[i].N + CF::BN - 1) / CF::BN;
+    if (tm * tn > max_tiles) max_tiles = tm * tn;
+    if (g.d[i].batch > max_batch) max_batch = g.d[i].batch;
+  }
+  if (max_tiles == 0 || max_batch == 0) return 0;
+  dim3 grid(max_tiles, max_batch, g.n);
+  int maxk = 0;
+  for (int i = 0; i < g.n; ++i)
+    for (int t = 0; t < g.d[i].nterms; ++t) maxk = g.d[i].t[t].K > maxk ? g.d[i].t[t].K : maxk;
+  const int tok = prof_begin(maxk <= 32 ? PROF_ZGEMM_SMALLK : PROF_ZGEMM, stream);
+  zgemm_bulk_kernel<CF, RV><<<grid, CF::NT, CF::SMEM, stream>>>(g);
+  NEGF_LAUNCHED();
+  if (tok >= 0) {
+    double fl = 0.0, by = 0.0;
+    for (int i = 0; i < g.n; ++i) {
+      const ZGemmDesc& d = g.d[i];
+      for (int t = 0; t < d.nterms; ++t) {
+        fl += 8.0 * d.M * d.N * (double)d.t[t].K * d.batch;
+        by += 16.0 * ((double)d.M * d.t[t].K + (double)d.t[t].K * d.N) * d.batch;
+      }
+      by += 16.0 * (double)d.M * d.N * d.batch * ((d.C && (d.beta.x != 0.0 || d.beta.y != 0.0)) ? 2 : 1);
+    }
+    prof_end(tok, stream, fl, by);
+  }
+  return 0;
+}
+
+// BK = 32 x 2 stages x 2 CTAs/SM measured best of the bulk family (8 x 1024^3:
+// 39.1 TFLOP/s algorithmic vs 36.2 for the cp.async kernel and 36.0 for cuBLAS;
+// BK 16 x 3 stages 24.9, BK 8 x 4 stages 19.0, BK 16 x 2 stages x 3 CTAs 32.5)
+#ifndef NEGF_BULK_BK
+#define NEGF_BULK_BK 32
+#endif
+#ifndef NEGF_BULK_STAGES
+#define NEGF_BULK_STAGES 2
+#endif
+#ifndef NEGF_BULK_MINB
+#define NEGF_BULK_MINB 2
+#endif
+using BulkGauss = BulkCfg<64, 32, NEGF_BULK_BK, NEGF_BULK_STAGES, NEGF_BULK_MINB>;
+
 using CfgSmall = Cfg<32, 32, 1, 1, 4, 4>;
 // default (algo 2): 3M, 64x32 CTA tiles of 4 warps, 3 CTAs/SM, BK = 16 with a
 // 2-stage cp.async pipeline and XOR-swizzled k-contiguous tiles (50 KB smem):
@@ -421,6 +719,8 @@ int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
     mm = g.d[i].M > mm ? g.d[i].M : mm;
     for (int t = 0; t < g.d[i].nterms; ++t) real &= (g.d[i].t[t].neg & kTermReal) != 0;
   }
+  if (gemm_algo() == 3 && mm > 32)  // TMA-engine bulk copies + mbarrier ring (warp-specialised)
+    return real ? launch_bulk<BulkGauss, true>(g, stream) : launch_bulk<BulkGauss>(g, stream);
   if (real)
     return mm <= 32 ? launch_cfg<CfgGauss2S, true>(g, stream) : launch_cfg<CfgGauss2, true>(g, stream);
   return mm <= 32 ? launch_cfg<CfgGauss2S>(g, stream) : launch_cfg<CfgGauss2>(g, stream);

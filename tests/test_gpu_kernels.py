@@ -23,7 +23,7 @@ def crand(shape, gen, dev):
 @pytest.mark.parametrize("m,n,k", [(8, 8, 4), (5, 7, 3), (32, 32, 32), (64, 64, 64), (100, 37, 70),
                                    (256, 256, 256), (33, 65, 129), (1, 1, 1)])
 @pytest.mark.parametrize("op_a,op_b", [(0, 0), (0, 3), (3, 0), (1, 2), (2, 1), (3, 3)])
-@pytest.mark.parametrize("algo", [0, 2])
+@pytest.mark.parametrize("algo", [0, 2, 3])
 def test_zgemm_matches_torch(cuda, m, n, k, op_a, op_b, algo):
     g = torch.Generator().manual_seed(m * 1000 + n * 10 + k + op_a * 7 + op_b)
     batch = 3
