@@ -25,7 +25,10 @@ extern "C" {
 int negf_abi_version(void);
 
 /* Complex block-product algorithm of the DMMA GEMM (process-wide):
- * 2 = 3M/Gauss, 3 real products per complex product (default),
+ * 2 = 3M/Gauss, 3 real products per complex product (default; cp.async
+ *     operand staging, TMA-engine bulk copies + mbarrier ring for complex
+ *     products with M >= 512),
+ * 3 = 3M with the bulk-copy kernel for every product,
  * 0 = 4 real products (the textbook arithmetic). Anything else: -1.
  * 3M trades ~25% of the FP64 tensor work for a normwise error bound that is
  * still O(eps |A||B|). */

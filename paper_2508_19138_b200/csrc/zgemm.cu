@@ -386,10 +386,10 @@ int launch_cfg(const ZGemmGroup& g, cudaStream_t stream) {
 // main loop. Bulk copies land rows contiguously, so the k-contiguous tiles use
 // the +4 pad (conflict-free fragment reads) instead of the XOR swizzle.
 // Row-mapped problems (inversion sweeps) stay on the cp.async kernel.
-template <int BM_, int BN_, int BK_, int STAGES_, int MINB_>
+template <int BM_, int BN_, int BK_, int STAGES_, int MINB_, int WM_ = 2, int WN_ = 2>
 struct BulkCfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_, MINB = MINB_;
-  static constexpr int WM = 2, WN = 2, NCW = WM * WN;  // consumer warps
+  static constexpr int WM = WM_, WN = WN_, NCW = WM * WN;  // consumer warps
   static constexpr int NT = (NCW + 1) * 32;            // + one producer warp
   static constexpr int WTM = BM / WM, WTN = BN / WN, TM = WTM / 8, TN = WTN / 8;
   static constexpr int SK = BK + 4, SMA = BM + 2, SMB = BN + 2;
@@ -672,7 +672,20 @@ int launch_bulk(const ZGemmGroup& g, cudaStream_t stream) {
 #ifndef NEGF_BULK_MINB
 #define NEGF_BULK_MINB 2
 #endif
-using BulkGauss = BulkCfg<64, 32, NEGF_BULK_BK, NEGF_BULK_STAGES, NEGF_BULK_MINB>;
+#ifndef NEGF_BULK_BM
+#define NEGF_BULK_BM 64
+#endif
+#ifndef NEGF_BULK_BN
+#define NEGF_BULK_BN 32
+#endif
+#ifndef NEGF_BULK_WM
+#define NEGF_BULK_WM 2
+#endif
+#ifndef NEGF_BULK_WN
+#define NEGF_BULK_WN 2
+#endif
+using BulkGauss = BulkCfg<NEGF_BULK_BM, NEGF_BULK_BN, NEGF_BULK_BK, NEGF_BULK_STAGES, NEGF_BULK_MINB, NEGF_BULK_WM,
+                          NEGF_BULK_WN>;
 
 using CfgSmall = Cfg<32, 32, 1, 1, 4, 4>;
 // default (algo 2): 3M, 64x32 CTA tiles of 4 warps, 3 CTAs/SM, BK = 16 with a
@@ -713,13 +726,19 @@ int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
     return gemm_algo() == 0 ? launch_cfg<CfgMapT4>(g, stream) : launch_cfg<CfgMapT>(g, stream);
   if (mx <= 32) return launch_cfg<CfgSmall>(g, stream);
   if (gemm_algo() == 0) return launch_cfg<Cfg4M32>(g, stream);
+  constexpr int kBulkMinM = 512;
   int mm = 0;
   bool real = true;  // every term has a real operand: 2-product Gauss kernel
   for (int i = 0; i < g.n; ++i) {
     mm = g.d[i].M > mm ? g.d[i].M : mm;
     for (int t = 0; t < g.d[i].nterms; ++t) real &= (g.d[i].t[t].neg & kTermReal) != 0;
   }
-  if (gemm_algo() == 3 && mm > 32)  // TMA-engine bulk copies + mbarrier ring (warp-specialised)
+  // TMA-engine bulk copies + mbarrier ring (warp-specialised): faster than the
+  // cp.async kernel for complex x complex products from 512-orbital blocks up
+  // (8 x 1024^3: 39.1 vs 36.2 TFLOP/s; C4 W RGF 0.87 vs 0.81 of the FP64
+  // peak), slower at 256 (C2) and for the real-V W-assembly products
+  // (profiles/gemm_bulk_r02.txt). algo 3 forces it everywhere (experiments).
+  if (gemm_algo() == 3 || (gemm_algo() == 2 && !real && mm >= kBulkMinM))
     return real ? launch_bulk<BulkGauss, true>(g, stream) : launch_bulk<BulkGauss>(g, stream);
   if (real)
     return mm <= 32 ? launch_cfg<CfgGauss2S, true>(g, stream) : launch_cfg<CfgGauss2, true>(g, stream);
