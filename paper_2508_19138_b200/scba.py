@@ -149,11 +149,10 @@ class EntryLayout:
             raise ValueError(f"target block size {self.target_bs} is not a multiple of {bs} dividing {n_b * bs}")
         self.n_bt = n_b * bs // self.target_bs
         self.table = cutoff is not None or self.target_bs != bs
-        lib = _lib.load()
         r, c = np.triu_indices(bs)
         self.tri_q = torch.from_numpy((r * bs + c).astype(np.int32)).to(self.dev)
         if not self.table:
-            self.n_entries = int(lib.negf_pattern_entries(n_b, bs))
+            self.n_entries = int(_lib.load().negf_pattern_entries(n_b, bs))
             t = len(r)
             per_row = t + bs * bs
             diag = np.zeros(self.n_entries, dtype=np.uint8)
