@@ -51,10 +51,9 @@ int negf_set_rgf_overlap(int on);
  * status[n_e] (device int): 0, or 1 + forward step of the first singular
  * Schur complement (rgf.py:121-126 SingularBlockError). u_spread[n_e][n_b]
  * (device double, may be NULL): LU pivot spread per step (rgf.py:44-49).
- * Blocks up to 512 orbitals are inverted by the one-CTA register-panel
- * Gauss-Jordan kernel; larger blocks by a 2x2 block recursion onto it (no
- * pivoting across the halves: sound for accretive carrier Schur complements;
- * u_spread is NaN for them). */
+ * Blocks up to 4096 orbitals are inverted by the pivoted Gauss-Jordan
+ * kernels (LAPACK zgetf2 pivot order over the whole column; one-CTA register
+ * panel up to 512, thread-block-cluster panel above). */
 size_t negf_rgf_workspace_bytes(int n_e, int n_b, int bs);
 int negf_rgf_selected_solve_batched(
     int n_e, int n_b, int bs,
@@ -108,7 +107,14 @@ int negf_zgemm_batched(int m, int n, int k, int batch,
                        const void* c, long long stride_c, int ldc,
                        void* d, long long stride_d, int ldd, void* stream);
 
-/* Batched pivoted inverse, replaces _linalg.invert (_linalg.py:30-52).
+/* Batched pivoted inverse, replaces _linalg.invert (_linalg.py:30-52):
+ * partial pivoting over the whole remaining column with LAPACK zgetf2's
+ * choice (max |re|+|im|, first index on ties), u_spread[b] (may be NULL) =
+ * max|U_jj| / min|U_jj| like scipy's LU. n <= 64: one CTA in smem;
+ * n <= 512: one CTA per matrix with the panel in registers; 512 < n <= 4096:
+ * a thread-block cluster of <= 8 CTAs per matrix exchanging the pivot
+ * candidates through distributed shared memory (also used for 256 < n <= 512
+ * when batch >= 64); n > 4096 returns -5.
  * s (n x n packed, stride n*n) is destroyed for n > 64. status[b] = 1 on an
  * exactly-zero or non-finite pivot. */
 size_t negf_zinv_workspace_bytes(int n, int batch);
@@ -123,8 +129,9 @@ int negf_zinv_batched(int n, int batch, void* s, void* x, int* status, double* u
  * check (> 10 max(tol, 1e-14) fails). m, n, np, x: [batch][bs][bs] device.
  * status[b] (device int): 0 ok, 1 singular block, 2 not converged in
  * max_iter sweeps, 3 residual check failed. iters[b]: sweeps used;
- * resid[b] (may be NULL): recursion residual. Synchronises `stream` once per
- * sweep (the convergence test). */
+ * resid[b] (may be NULL): recursion residual. Converged problems are masked
+ * on the device after every sweep; the host reads the active count (one
+ * stream synchronisation) every 4 sweeps. */
 size_t negf_sancho_workspace_bytes(int batch, int bs);
 int negf_obc_sancho_batched(int batch, int bs, const void* m, const void* n, const void* np,
                             double tol, int max_iter, void* x, int* status, int* iters,
@@ -248,7 +255,10 @@ int negf_observables(int n_e, int n_b, int bs, const void* gr_diag, const void* 
 /* ---- (3) energy convolutions (negfgw/convolve.py) -----------------------
  * Entry-major series: row r of an array is the energy series of one matrix
  * entry, x[r][0..n_e) complex128, rows contiguous (stride n_e).
- * L: power-of-two circular length >= max(8, 2 n_e - 1), L <= 4096.
+ * L: power-of-two circular length >= max(8, 2 n_e - 1); L <= 4096 on one CTA
+ * per row, L = 8192 (n_e <= 4096) for the fused P / Sigma kernels on a
+ * cluster pair of CTAs (even / odd frequency bins, halves combined through
+ * distributed shared memory); larger L returns -1 / -5.
  * tw[L] = exp(-2 pi i k/L).
  * kf/kcf[L]: spectrum (natural order) of the causal kernel
  * K = ifft_m(theta), m = scipy next_fast_len(2 n_e) made even, and of conj(K),
