@@ -21,8 +21,8 @@ def timeit(fn, reps=10):
     return e0.elapsed_time(e1) / reps
 ms = timeit(lambda: torch.bmm(A, B, out=D))
 print(f"cuBLAS bmm {b}x{n}^3: {ms:.3f} ms {fl / ms / 1e9:.2f} TFLOP/s", flush=True)
-for algo in [int(a) for a in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["2", "0", "1", "3", "5"])]:
-    lib.negf_set_gemm_algo(algo)
+for algo in [int(a) for a in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["2", "3", "0"])]:
+    assert lib.negf_set_gemm_algo(algo) == 0, algo
     ms = timeit(lambda: lib.negf_zgemm_batched(n, n, n, b, 1.0, 0.0, A.data_ptr(), n * n, n, 0, B.data_ptr(), n * n, n, 0,
                                                0.0, 0.0, None, 0, n, D.data_ptr(), n * n, n, _lib.stream_ptr()))
     print(f"negf algo {algo}: {ms:.3f} ms {fl / ms / 1e9:.2f} TFLOP/s (algorithmic)", flush=True)
