@@ -330,6 +330,21 @@ def run_native(args):
     e2e_s = float(t.item())
     d2h = ObservableAccumulator(n_e, n_b, de, dev).d2h_bytes()
 
+    # parity at the benchmarked shape, in the same run: the public API on the
+    # energies of the reference fixture tests/golden/golden_c2_ballistic.npz
+    # (the reference's own scba_run on chain_device(64, 256), 4 energies)
+    parity = None
+    gpath = ROOT / "tests" / "golden" / "golden_c2_ballistic.npz"
+    if rank == 0 and (n_b, bs) == (64, 256) and gpath.exists():
+        g = np.load(gpath)
+        ge = np.linspace(-2.0, 2.0, int(g["config"][2]))
+        po = ballistic_observables(h, ge, w["eta"], contacts, w["surface_tol"], solver=solver)
+        rel = lambda a, b_: float(np.linalg.norm(np.asarray(a) - b_) / np.linalg.norm(b_))
+        parity = {"reference_fixture": "tests/golden/golden_c2_ballistic.npz (reference scba_run, 4 energies)",
+                  "dos_rel_err": rel(po["dos"], g["obs_dos"]), "density_rel_err": rel(po["density"], g["obs_density"]),
+                  "terminal_left": [po["terminal_left"], float(g["obs_terminal_left"])],
+                  "terminal_right": [po["terminal_right"], float(g["obs_terminal_right"])],
+                  "bar": "1e-9 relative Frobenius (currents: see tests/test_gpu_large_shapes.py)"}
     del solver, acc, b
     _lib._WS.clear()
     torch.cuda.empty_cache()
@@ -459,7 +474,10 @@ def run_native(args):
             "device_time_breakdown": breakdown,
             "clocks": clk,
             "cpu_baseline": cpu,
-            "observables_check": {"terminal_left": obs["terminal_left"], "terminal_right": obs["terminal_right"]},
+            "observables_e2e": {"terminal_left": obs["terminal_left"], "terminal_right": obs["terminal_right"],
+                                "conservation": (abs(obs["terminal_left"] + obs["terminal_right"])
+                                                 / abs(obs["terminal_left"])) if obs["terminal_left"] else None},
+            "parity_check": parity,
         }
         print(json.dumps(out), flush=True)
     if world > 1:
