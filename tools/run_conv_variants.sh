@@ -1,3 +1,4 @@
+# build first: python tools/build_variant.py pack4 -DNEGF_CONV_PACK_MINB=4; pack5 -DNEGF_CONV_PACK_MINB=5
 # conv roofline (bench.conv_roofline) with the default library and packed-row occupancy variants
 for lib in "" paper_2508_19138_b200/variants/pack4.so paper_2508_19138_b200/variants/pack5.so; do
   echo "== lib ${lib:-default}"

@@ -1,3 +1,5 @@
+# build first: python tools/build_variant.py b8s4m3 -DNEGF_BULK_BK=8 -DNEGF_BULK_STAGES=4 -DNEGF_BULK_MINB=3;
+#   b16s2m3 -DNEGF_BULK_BK=16 -DNEGF_BULK_STAGES=2 -DNEGF_BULK_MINB=3; b32s2m2 -DNEGF_BULK_BK=32 -DNEGF_BULK_STAGES=2 -DNEGF_BULK_MINB=2
 # DMMA GEMM variants: cp.async kernel (algo 2) vs the TMA-engine bulk-copy + mbarrier kernel (algo 3),
 # bulk-kernel tile/stage variants built by tools/build_variant.py into paper_2508_19138_b200/variants/
 timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q -k "zgemm" 2>&1 | tail -2
