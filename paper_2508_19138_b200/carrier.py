@@ -200,7 +200,8 @@ class CarrierSolver:
                                                     p(b["xg_diag"]), p(b["xg_upper"]), st)
                 _lib.check(rc, "negf_greater_from_identity")
         elif self.greater == "identity":
-            rgf_selected_solve_split(lib, b, ne, self.n_b, self.bs, self.dev, 1, [], kinds=("bl",))
+            rgf_selected_solve_split(lib, b, ne, self.n_b, self.bs, self.dev, self.streams, self._side_streams,
+                                     kinds=("bl",))
             rc = lib.negf_greater_from_identity(ne, self.n_b, self.bs, p(b["xl_diag"]), p(b["xl_upper"]),
                                                 p(b["xr_diag"]), p(b["xr_upper"]), p(b["xr_lower"]),
                                                 p(b["xg_diag"]), p(b["xg_upper"]), st)

@@ -25,6 +25,8 @@
 //    17 N_B - 15 with one Keldysh kind).
 // x_fwd lives in xr_diag and xl_fwd in xl_diag: each is overwritten in place
 // by the backward pass once its last reader has run.
+#include <unordered_map>
+
 #include "ew.cuh"
 #include "rgf.cuh"
 #include "zgemm.cuh"
@@ -165,20 +167,21 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
   //   evK[p]: step i's K work done, before R overwrites tA[p] at step i + 2.
   const bool pipe = a.overlap && nk > 0 && n > 1;
   // The auxiliary stream and its events are created once per (thread,
-  // device) and reused by every call (no per-call create/destroy); a
-  // thread-local cache keeps concurrent callers on different threads apart.
+  // device, caller stream) and reused by every call (no per-call
+  // create/destroy); keying on the caller's stream keeps concurrent solves
+  // on different streams (carrier energy slices) and threads apart.
   struct AuxStreams {
     cudaStream_t sk = nullptr;
     cudaEvent_t evA[2], evX[2], evK[2], ev0;
   };
-  thread_local AuxStreams aux_cache[64];
+  thread_local std::unordered_map<unsigned long long, AuxStreams> aux_cache;
   cudaStream_t sk = st;
   cudaEvent_t *evA = nullptr, *evX = nullptr, *evK = nullptr, ev0 = nullptr;
   if (pipe) {
     int dev = 0;
     NEGF_CUDA_CHECK(cudaGetDevice(&dev));
-    if (dev < 0 || dev >= 64) return -1;
-    AuxStreams& ax = aux_cache[dev];
+    const unsigned long long key = (reinterpret_cast<unsigned long long>(st) << 6) ^ (unsigned long long)dev;
+    AuxStreams& ax = aux_cache[key];
     if (!ax.sk) {
       for (int j = 0; j < 2; ++j) {
         NEGF_CUDA_CHECK(cudaEventCreateWithFlags(&ax.evA[j], cudaEventDisableTiming));
