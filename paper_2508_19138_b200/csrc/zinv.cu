@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
 // that every reader of the old contents has passed. Outputs are those of
 // zinv_panel_kernel (ipiv, Pinv, row maps, rows K of A_new = [Pinv R | Pinv])
 // with the T columns split over the cluster.
-constexpr int kClusterMax = 8;
+constexpr int kClusterMax = 16;  // 8 portable; 16 with the non-portable cluster attribute
 
 template <int NB>
 __global__ void __launch_bounds__(512) zinv_panel_cluster_kernel(const z_t* __restrict__ A, long long sA,
@@ -459,13 +459,16 @@ __global__ void __launch_bounds__(512) zinv_panel_cluster_kernel(const z_t* __re
   cg::cluster_group cluster = cg::this_cluster();
   const int C = (int)cluster.num_blocks();
   const int q = (int)cluster.block_rank();
-  __shared__ z_t cand_row[2][kClusterMax][NB];
+  // the candidate rows are dead after the column loop: Pinv reuses their storage
+  constexpr int kCand = 2 * kClusterMax * NB, kPinv = NB * LD;
+  __shared__ z_t cand_pinv[kCand > kPinv ? kCand : kPinv];
+  auto cand_row = reinterpret_cast<z_t(*)[kClusterMax][NB]>(cand_pinv);
   __shared__ z_t cand_ip[2][kClusterMax];
   __shared__ double cand_v[2][kClusterMax];
   __shared__ int cand_p[2][kClusterMax];
   __shared__ int cand_r[2][kClusterMax];
   __shared__ z_t blk[NB * LD];     // pivot rows (L\U) in pivot order
-  __shared__ z_t pinv_s[NB * LD];
+  z_t* const pinv_s = cand_pinv;  // after the column loop (see cand_pinv)
   __shared__ z_t rdiag_s[NB];
   __shared__ int prow_s[NB];       // panel row of the pivot chosen at column j
   __shared__ int piv_s[NB];
@@ -735,6 +738,9 @@ __global__ void zinv_unpermute_kernel(const z_t* A, long long sA, int n, const i
 }
 
 constexpr int kInvPanelMax = 512;   // one-CTA register panel limit
+#ifndef NEGF_ZINV_NB32_MAX
+#define NEGF_ZINV_NB32_MAX 4096  // cluster panels of 32 columns (256 rows per CTA, up to 16 CTAs: non-portable above 8)
+#endif
 constexpr int kInvClusterMax = 4096;  // cluster panel limit (8 CTAs x 512 rows)
 
 // cudaFuncSetAttribute is per device context: remember it per device.
@@ -781,7 +787,7 @@ int zinv_panel_width(int n, int batch) {
   // 512 * 16 / nb rows per CTA, <= kClusterMax CTAs
   if (n <= 256) return 32;
   if (!use_cluster(n, batch)) return 16;
-  if (n <= 2048) return 32;
+  if (n <= NEGF_ZINV_NB32_MAX) return 32;
   return 16;
 }
 
@@ -846,6 +852,18 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
+        if (ncta > 8) {  // non-portable cluster size (B200: up to 16)
+          static unsigned np_done = 0;
+          int dv = 0;
+          NEGF_CUDA_CHECK(cudaGetDevice(&dv));
+          if (!(__atomic_load_n(&np_done, __ATOMIC_ACQUIRE) & (1u << dv))) {
+            NEGF_CUDA_CHECK(cudaFuncSetAttribute(zinv_panel_cluster_kernel<32>,
+                                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            NEGF_CUDA_CHECK(cudaFuncSetAttribute(zinv_panel_cluster_kernel<16>,
+                                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            __atomic_fetch_or(&np_done, 1u << dv, __ATOMIC_RELEASE);
+          }
+        }
         if (nb == 32)
           NEGF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zinv_panel_cluster_kernel<32>, (const z_t*)cur, cs, nxt, ns, n,
                                              k0, wd, ipiv, pinv, umm, map_src, map_dst, aux));
