@@ -112,7 +112,8 @@ int negf_zgemm_batched(int m, int n, int k, int batch,
  * choice (max |re|+|im|, first index on ties), u_spread[b] (may be NULL) =
  * max|U_jj| / min|U_jj| like scipy's LU. n <= 64: one CTA in smem;
  * n <= 512: one CTA per matrix with the panel in registers; 512 < n <= 4096:
- * a thread-block cluster of <= 8 CTAs per matrix exchanging the pivot
+ * a thread-block cluster of up to 16 CTAs (256 rows each; non-portable
+ * cluster size above 8) per matrix exchanging the pivot
  * candidates through distributed shared memory (also used for 256 < n <= 512
  * when batch >= 64); n > 4096 returns -5.
  * s (n x n packed, stride n*n) is destroyed for n > 64. status[b] = 1 on an

@@ -11,7 +11,7 @@
 // each panel K of NB columns:
 //   1. the panel kernel runs the unblocked pivoted LU of the (N-k0) x NB
 //      panel with the pivot search over the whole remaining column (one CTA
-//      per matrix for N <= 512; a thread-block cluster of up to 8 CTAs sharing
+//      per matrix for N <= 512; a thread-block cluster of up to 16 CTAs sharing
 //      the candidates through distributed shared memory for 512 < N <= 4096),
 //      and writes Pinv = (pivot block)^-1, the row maps of the interchanges,
 //      and rows K of the new matrix: [T | Pinv] with T = Pinv R;
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
 }
 
 // Panel LU for blocks above the one-CTA register panel (n > 512): the panel
-// rows are split over a thread-block cluster of C <= 8 CTAs (RPC rows each,
+// rows are split over a thread-block cluster of C <= 16 CTAs (RPC rows each,
 // same register layout as zinv_panel_kernel), and the pivot search spans the
 // WHOLE column (LAPACK zgetf2 order, first-index ties) through distributed
 // shared memory. Per column: in-CTA argmax (one barrier), then every CTA
@@ -741,7 +741,7 @@ constexpr int kInvPanelMax = 512;   // one-CTA register panel limit
 #ifndef NEGF_ZINV_NB32_MAX
 #define NEGF_ZINV_NB32_MAX 4096  // cluster panels of 32 columns (256 rows per CTA, up to 16 CTAs: non-portable above 8)
 #endif
-constexpr int kInvClusterMax = 4096;  // cluster panel limit (8 CTAs x 512 rows)
+constexpr int kInvClusterMax = 4096;  // cluster panel limit (16 CTAs x 256 rows)
 
 // cudaFuncSetAttribute is per device context: remember it per device.
 bool attr_once(const void* fn, int bytes, unsigned* done_mask) {
