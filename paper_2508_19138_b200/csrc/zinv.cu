@@ -447,14 +447,14 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
 // with the T columns split over the cluster.
 constexpr int kClusterMax = 16;  // 8 portable; 16 with the non-portable cluster attribute
 
-template <int NB>
-__global__ void __launch_bounds__(512) zinv_panel_cluster_kernel(const z_t* __restrict__ A, long long sA,
+template <int NB, int NT = 512>
+__global__ void __launch_bounds__(NT) zinv_panel_cluster_kernel(const z_t* __restrict__ A, long long sA,
                                                                  z_t* __restrict__ Anew, long long sAn, int n,
                                                                  int k0, int w, int* ipiv, z_t* pinv,
                                                                  double* umaxmin, int* map_src, int* map_dst,
                                                                  InvAux aux) {
-  constexpr int TPR = NB / 16;    // threads per row
-  constexpr int RPC = 512 / TPR;  // panel rows per CTA
+  constexpr int TPR = NB / 16;   // threads per row
+  constexpr int RPC = NT / TPR;  // panel rows per CTA
   constexpr int LD = NB + 1;
   cg::cluster_group cluster = cg::this_cluster();
   const int C = (int)cluster.num_blocks();
@@ -738,6 +738,9 @@ __global__ void zinv_unpermute_kernel(const z_t* A, long long sA, int n, const i
 }
 
 constexpr int kInvPanelMax = 512;   // one-CTA register panel limit
+#ifndef NEGF_ZINV_NT256_MAX
+#define NEGF_ZINV_NT256_MAX 1024  // 256-thread cluster CTAs up to this block size (3-5% at 768-1024)
+#endif
 #ifndef NEGF_ZINV_NB32_MAX
 #define NEGF_ZINV_NB32_MAX 4096  // cluster panels of 32 columns (256 rows per CTA, up to 16 CTAs: non-portable above 8)
 #endif
@@ -838,11 +841,14 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
           zinv_panel_kernel<16><<<batch, panel_threads, 0, stream>>>(cur, cs, nxt, ns, n, k0, wd, ipiv, pinv,
                                                                      umm, map_src, map_dst, aux);
       } else {
-        const int rpc = 512 * 16 / nb;
+        // 32-column panels: 256-thread CTAs (128 rows) while the cluster stays
+        // within 16 CTAs (NEGF_ZINV_NT256_MAX), else 512-thread CTAs (256 rows)
+        const int nt = (nb == 32 && n <= NEGF_ZINV_NT256_MAX) ? 256 : 512;
+        const int rpc = nt * 16 / nb;
         const int ncta = (n - k0 + rpc - 1) / rpc;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(ncta, batch, 1);
-        cfg.blockDim = dim3(512, 1, 1);
+        cfg.blockDim = dim3(nt, 1, 1);
         cfg.dynamicSmemBytes = 0;
         cfg.stream = stream;
         cudaLaunchAttribute at[1];
@@ -859,12 +865,17 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
           if (!(__atomic_load_n(&np_done, __ATOMIC_ACQUIRE) & (1u << dv))) {
             NEGF_CUDA_CHECK(cudaFuncSetAttribute(zinv_panel_cluster_kernel<32>,
                                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            NEGF_CUDA_CHECK(cudaFuncSetAttribute(zinv_panel_cluster_kernel<32, 256>,
+                                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
             NEGF_CUDA_CHECK(cudaFuncSetAttribute(zinv_panel_cluster_kernel<16>,
                                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
             __atomic_fetch_or(&np_done, 1u << dv, __ATOMIC_RELEASE);
           }
         }
-        if (nb == 32)
+        if (nb == 32 && nt == 256)
+          NEGF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zinv_panel_cluster_kernel<32, 256>, (const z_t*)cur, cs, nxt,
+                                             ns, n, k0, wd, ipiv, pinv, umm, map_src, map_dst, aux));
+        else if (nb == 32)
           NEGF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zinv_panel_cluster_kernel<32>, (const z_t*)cur, cs, nxt, ns, n,
                                              k0, wd, ipiv, pinv, umm, map_src, map_dst, aux));
         else
