@@ -842,8 +842,8 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
                                                                      umm, map_src, map_dst, aux);
       } else {
         // 32-column panels: 256-thread CTAs (128 rows) while the cluster stays
-        // within 16 CTAs (NEGF_ZINV_NT256_MAX), else 512-thread CTAs (256 rows)
-        const int nt = (nb == 32 && n <= NEGF_ZINV_NT256_MAX) ? 256 : 512;
+        // within 16 CTAs for 512 < n <= NEGF_ZINV_NT256_MAX, else 512-thread CTAs (256 rows)
+        const int nt = (nb == 32 && n > 512 && n <= NEGF_ZINV_NT256_MAX) ? 256 : 512;
         const int rpc = nt * 16 / nb;
         const int ncta = (n - k0 + rpc - 1) / rpc;
         cudaLaunchConfig_t cfg = {};
