@@ -108,6 +108,11 @@ class ScbaOptions:
     # driver.py:276-277, and keeps the full band, scba.py:917). None = the
     # reference's full band. What makes a 2048-energy C3 iteration fit in HBM.
     entry_cutoff: int | None = None
+    # Deviation (off by default): "identity" derives the carrier G^> from
+    # G^> = G^< + G^R - G^R^dag instead of its own Keldysh recursion (the
+    # reference runs all three, rgf.py:232-243; its identity_defects show the
+    # identity holds to ~1e-15 for G, P and Sigma). 0.6x the carrier RGF work.
+    greater: str = "recursion"
 
     def __post_init__(self) -> None:
         if self.max_iter < 1:
@@ -124,6 +129,8 @@ class ScbaOptions:
             raise ValueError(f"unknown retarded method {self.retarded_method!r}")
         if self.entry_cutoff is not None and self.entry_cutoff < 0:
             raise ValueError(f"entry_cutoff must be >= 0 orbitals, got {self.entry_cutoff}")
+        if self.greater not in ("recursion", "identity"):
+            raise ValueError(f"unknown greater mode {self.greater!r}")
 
 
 class EntryLayout:
@@ -506,7 +513,7 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     energies = np.asarray(energies, dtype=float)
     ne = len(energies)
     de = (energies[-1] - energies[0]) / (ne - 1)
-    carrier = CarrierSolver(h, eta, contacts, options.surface_tol, device=dev,
+    carrier = CarrierSolver(h, eta, contacts, options.surface_tol, device=dev, greater=options.greater,
                             retarded_method=options.retarded_method, beyn=options.beyn)
     n_b, bs = carrier.n_b, carrier.bs
     lay = EntryLayout(n_b, bs, dev, cutoff=options.entry_cutoff)

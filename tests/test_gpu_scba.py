@@ -130,6 +130,25 @@ def test_scba_c1_matches_reference_scba_run(golden, cuda):
     check_c1(res, g, tol=TOL)
 
 
+def test_scba_greater_identity_matches_reference(golden, cuda):
+    """ScbaOptions.greater="identity" (G^> = G^< + G^R - G^R^dag instead of
+    the greater recursion) still reproduces the reference's scba_run, which
+    runs all three recursions: small (3 iterations) and C1."""
+    g = golden("golden_scba_small.npz")
+    res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=3, tol=1e-12, batch=10,
+                                                          memoizer=MEMO_OFF, greater="identity"), device=cuda)
+    for k in g.files:
+        if k.startswith(("ver_", "config")):
+            continue
+        assert rel(res[k], g[k]) < TOL, k
+    g = golden("golden_scba_c1.npz")
+    res = scba_run(orc.chain_device(16, 32), orc.coulomb_matrix(16, 32), np.linspace(-2.0, 2.0, 128), 1e-3,
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=1, tol=1e-12, batch=64,
+                                                          memoizer=MEMO_OFF, greater="identity"), device=cuda)
+    check_c1(res, g, tol=TOL)
+
+
 def test_scba_c1_matches_oracle_two_iterations(cuda):
     """Second iteration (nonzero Sigma feeding the carrier assembly) vs the oracle."""
     h, v = orc.chain_device(16, 32), orc.coulomb_matrix(16, 32)

@@ -10,6 +10,7 @@ from paper_2508_19138_b200.scba import BeynOptions, MemoizerOptions, ScbaOptions
     ({"max_iter": 0}, "max_iter"), ({"tol": 0.0}, "tol"), ({"mixing": 0.0}, "mixing"),
     ({"mixing": 1.5}, "mixing"), ({"surface_tol": -1.0}, "surface_tol"),
     ({"retarded_method": "lu"}, "retarded method"), ({"w_retarded_method": "x"}, "W retarded"),
+    ({"greater": "dense"}, "greater mode"), ({"entry_cutoff": -1}, "entry_cutoff"),
 ])
 def test_scba_options_reject(kw, msg):
     with pytest.raises(ValueError, match=msg):
@@ -21,6 +22,7 @@ def test_scba_options_defaults_follow_reference():
     assert (o.max_iter, o.tol, o.mixing, o.surface_tol, o.reset_sigma, o.oracle_mode) == (50, 1e-5, 0.3, 1e-8, True,
                                                                                         False)
     assert o.retarded_method == "beyn"  # scba.py:165
+    assert o.greater == "recursion" and o.entry_cutoff is None  # the reference's algorithm and entry set
     assert o.memoizer.enabled and (o.memoizer.n_fpi_retarded, o.memoizer.n_fpi_lg) == (20, 10)
     assert BeynOptions().contour() == {"radius": 1.0, "center": 0.0, "n_quad": 16}
 

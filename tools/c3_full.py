@@ -39,7 +39,9 @@ comm = Comm.from_env()
 dev = torch.device("cuda", torch.cuda.current_device())
 h, v = toys.chain_device(n_b, bs), toys.coulomb_matrix(n_b, bs)
 e = np.linspace(-2.0, 2.0, n_e)
-opts = ScbaOptions(retarded_method="sancho", max_iter=iters, tol=1e-5, batch=batch, entry_cutoff=cutoff)
+greater = os.environ.get("NEGF_GREATER", "recursion")  # "identity": ScbaOptions.greater deviation
+opts = ScbaOptions(retarded_method="sancho", max_iter=iters, tol=1e-5, batch=batch, entry_cutoff=cutoff,
+                   greater=greater)
 torch.cuda.reset_peak_memory_stats(dev)
 res = scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05), opts, device=dev, keep_g=False, comm=comm,
                sigma_to_host=False, profile=True)
@@ -55,7 +57,8 @@ if comm.rank == 0:
     full_band = n_b * bs * (bs + 1) // 2 + (n_b - 1) * bs * bs
     print(json.dumps({
         "config": f"C3: chain_device({n_b},{bs}) + coulomb_matrix, {n_e} energies, {comm.size} GPUs "
-                  f"({n_e // comm.size}/rank), batch {batch}, entry_cutoff {cutoff} orbitals (r_cut deviation)",
+                  f"({n_e // comm.size}/rank), batch {batch}, entry_cutoff {cutoff} orbitals (r_cut deviation), "
+                  f"G^> by {greater}",
         "n_entries": res.sigma_pattern.n_entries, "n_entries_full_band": full_band,
         "entry_fraction": res.sigma_pattern.n_entries / full_band,
         "iteration_s": vals[0], "energies_per_s": n_e / vals[0],

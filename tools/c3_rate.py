@@ -27,7 +27,8 @@ dev = torch.device("cuda", rank % torch.cuda.device_count())
 torch.cuda.set_device(dev)
 h, v = toys.chain_device(n_b, bs), toys.coulomb_matrix(n_b, bs)
 e = np.linspace(-2.0, 2.0, ne * world)
-opts = ScbaOptions(retarded_method="sancho", max_iter=2, tol=1e-5, batch=batch)
+opts = ScbaOptions(retarded_method="sancho", max_iter=2, tol=1e-5, batch=batch,
+                   greater=os.environ.get("NEGF_GREATER", "recursion"))
 res = scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05), opts, device=dev, keep_g=False, comm=comm,
                sigma_to_host=False, profile=True)
 dt = torch.tensor([res["iteration_s"][-1]], dtype=torch.float64, device=dev)
@@ -37,7 +38,7 @@ dt = float(dt.item())
 flops = 2 * 8.0 * bs ** 3 * (38 * n_b - 33) * ne * world  # SURVEY §8(d) F_RGF, G and W
 if rank == 0:
     print(json.dumps({"config": f"chain_device({n_b},{bs}) + coulomb_matrix, {ne * world} energies ({ne}/rank), "
-                                f"batch {batch}, x{world} GPUs, 2nd GW iteration timed",
+                                f"batch {batch}, x{world} GPUs, 2nd GW iteration timed, G^> by {opts.greater}",
                       "iteration_s": dt, "energies_per_s": ne * world / dt, "rgf_model_tflops_GW": flops / dt / 1e12,
                       "stage_s_both_iterations": res["timings"], "iteration_s_all": res["iteration_s"],
                       "residuals": list(map(float, res["residuals"])),
