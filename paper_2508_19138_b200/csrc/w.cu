@@ -53,8 +53,14 @@ struct Opnd {  // one operand block: pointer, energy stride, op flag
   long long s;
   int op;
   bool neg;
-  bool real = false;  // imaginary part exactly zero (a real V)
+  bool real = false;   // imaginary part exactly zero (a real V)
+  bool dreal = false;  // stored as doubles (p reinterpreted; op N): the real x complex kernel
 };
+
+__global__ void real_part_kernel(const z_t* __restrict__ x, double* __restrict__ y, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = x[i].x;
+}
 
 ZGemmDesc sum_desc(int bs, int ne, std::initializer_list<std::pair<Opnd, Opnd>> terms, z_t* D,
                    long long sD, double alpha, const z_t* C = nullptr, long long sC = 0,
@@ -65,7 +71,8 @@ ZGemmDesc sum_desc(int bs, int ne, std::initializer_list<std::pair<Opnd, Opnd>> 
   for (auto& tb : terms) {
     const Opnd& a = tb.first;
     const Opnd& b = tb.second;
-    d.t[n++] = zterm(a.p, a.s, bs, a.op, b.p, b.s, bs, b.op, bs, a.neg != b.neg, a.real || b.real);
+    d.t[n] = zterm(a.p, a.s, bs, a.op, b.p, b.s, bs, b.op, bs, a.neg != b.neg, a.real || b.real);
+    d.t[n++].neg |= (a.dreal ? kTermRealA : 0) | (b.dreal ? kTermRealB : 0);
   }
   d.nterms = n;
   for (int i = n; i < kMaxTerms; ++i) d.t[i] = d.t[0];
@@ -84,7 +91,8 @@ using namespace negf;
 extern "C" {
 
 size_t negf_w_assemble_workspace_bytes(int n_e, int n_b, int bs) {
-  return a256(sizeof(z_t) * (size_t)n_e * 4 * n_b * bs * bs);
+  // Q = V P blocks + a real copy of V (3 n_b - 2 blocks of doubles)
+  return a256(sizeof(z_t) * (size_t)n_e * 4 * n_b * bs * bs) + a256(sizeof(double) * (size_t)(3 * n_b) * bs * bs);
 }
 
 // V: energy-independent blocks v_diag [n_b], v_upper/v_lower [n_b-1].
@@ -104,8 +112,26 @@ int negf_w_assemble(int n_e, int n_b, int bs, const void* v_diag, const void* v_
   cudaStream_t st = (cudaStream_t)stream;
   const long long n2 = (long long)bs * bs, sd = (long long)n_b * n2, so = (long long)(n_b - 1) * n2;
   const int nb = n_b;
+  if (workspace_bytes < negf_w_assemble_workspace_bytes(n_e, n_b, bs)) return -4;
+  // A real V (Coulomb) with an even block size goes to the real x complex
+  // kernel from a double copy (energy independent, 3 n_b - 2 blocks).
+#ifndef NEGF_DZ_OFF
+  const bool vd = v_real != 0 && bs % 2 == 0;
+#else
+  const bool vd = false;
+#endif
+  double* vr = reinterpret_cast<double*>((char*)workspace + a256(sizeof(z_t) * (size_t)n_e * 4 * n_b * bs * bs));
+  if (vd) {
+    const long long nd = (long long)n_b * n2, no = (long long)(n_b - 1) * n2;
+    real_part_kernel<<<592, 256, 0, st>>>((const z_t*)v_diag, vr, nd);
+    real_part_kernel<<<592, 256, 0, st>>>((const z_t*)v_upper, vr + nd, no);
+    real_part_kernel<<<592, 256, 0, st>>>((const z_t*)v_lower, vr + nd + no, no);
+    NEGF_LAUNCHED();
+  }
   auto V = [&](int i, int j) -> Opnd {  // energy independent
     const bool re = v_real != 0;
+    const long long k = i == j ? i : j == i + 1 ? n_b + i : 2LL * n_b - 1 + j;  // block of the real copy
+    if (vd) return Opnd{reinterpret_cast<const z_t*>(vr + k * n2), 0, OP_N, false, true, true};
     if (i == j) return Opnd{(const z_t*)v_diag + i * n2, 0, OP_N, false, re};
     if (j == i + 1) return Opnd{(const z_t*)v_upper + i * n2, 0, OP_N, false, re};
     return Opnd{(const z_t*)v_lower + j * n2, 0, OP_N, false, re};  // (j+1, j)
@@ -144,7 +170,6 @@ int negf_w_assemble(int n_e, int n_b, int bs, const void* v_diag, const void* v_
   RC(add_identity((z_t*)m_diag, n2, bs, n_e * nb, make_double2(1.0, 0.0), st));
 
   // ---- RHS per kind: Q = V P (4 blocks per row), B = trunc3(Q V)
-  if (workspace_bytes < negf_w_assemble_workspace_bytes(n_e, n_b, bs)) return -4;
   z_t* Q = (z_t*)workspace;  // [n_e][n_b][4] blocks: slot 0:(i,i-1) 1:(i,i) 2:(i,i+1) 3:(i,i+2)
   const long long sq = (long long)nb * 4 * n2;
   auto Qb = [&](int i, int slot) { return Q + ((long long)i * 4 + slot) * n2; };

@@ -660,6 +660,279 @@ int launch_bulk(const ZGemmGroup& g, cudaStream_t stream) {
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Real x complex products with the real operand STORED as doubles (the W
+// assembly's Coulomb V, kTermRealA / kTermRealB): a complex product with one
+// real factor is exactly two real products (re += v br, im += v bi), so the
+// kernel issues 2 DMMAs per fragment pair with no 3M sums, and the real tile
+// costs half the global traffic and shared memory of a complex one. The real
+// operand is op N only ([M][K] for A, [K][N] for B, leading dimension and K
+// or N even so every 16-byte cp.async chunk holds two whole doubles).
+// Real tiles: A [BM][BK+4], B [BK][BN+4] doubles -- both conflict-free for
+// the DMMA fragment reads (row strides = 4 mod 16 double-banks).
+template <int BM_, int BN_, int BK_, int STAGES_, int MINB_, int WM_, int WN_, int RSIDE_>
+struct DzCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_, MINB = MINB_, WM = WM_, WN = WN_;
+  static constexpr int RSIDE = RSIDE_;  // 1: A real, 2: B real
+  static constexpr int NT = WM * WN * 32;
+  static constexpr int WTM = BM / WM, WTN = BN / WN, TM = WTM / 8, TN = WTN / 8;
+  static constexpr int SKR = BK + 4, SMBR = BN + 4;        // real strides (doubles)
+  static constexpr int SK = BK + 4, SMA = BM + 2, SMB = BN + 2;  // complex strides (complex)
+  // sizes in doubles
+  static constexpr int A_D = RSIDE == 1 ? BM * SKR : 2 * ((BM * SK > BK * SMA) ? BM * SK : BK * SMA);
+  static constexpr int B_D = RSIDE == 2 ? BK * SMBR : 2 * ((BN * SK > BK * SMB) ? BN * SK : BK * SMB);
+  static constexpr int STAGE_D = A_D + B_D;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_D * sizeof(double);
+  static_assert(A_D % 2 == 0 && B_D % 2 == 0, "16-byte aligned tiles");
+};
+
+template <class CF>
+__device__ __forceinline__ void dz_load_stage(const ZGemmDesc& d, int kt, const KtBounds& kb, int b, int m0, int n0,
+                                              double* sA, double* sB) {
+  const int term = kb.term(kt);
+  const ZTerm& t = d.t[term];
+  const int k0 = (kt - kb.base(term)) * CF::BK;
+  const int K = t.K, M = d.M, N = d.N;
+  if constexpr (CF::RSIDE == 1) {  // real A [M][K]
+    const double* A = reinterpret_cast<const double*>(t.A) + (long long)b * t.sA;
+#pragma unroll
+    for (int e = threadIdx.x; e < CF::BM * CF::BK / 2; e += CF::NT) {
+      const int mn = e / (CF::BK / 2), kc = 2 * (e % (CF::BK / 2));
+      const int gm = m0 + mn, gk = k0 + kc;
+      const bool p = gm < M && gk < K;
+      cp_async16(sA + mn * CF::SKR + kc, p ? A + (long long)gm * t.lda + gk : A, p);
+    }
+  } else {
+    const z_t* A = t.A + (long long)b * t.sA;
+    z_t* zA = reinterpret_cast<z_t*>(sA);
+    if (!op_trans(t.opA)) {
+#pragma unroll
+      for (int e = threadIdx.x; e < CF::BM * CF::BK; e += CF::NT) {
+        const int mn = e / CF::BK, k = e % CF::BK, gm = m0 + mn, gk = k0 + k;
+        const bool p = gm < M && gk < K;
+        cp_async16(zA + mn * CF::SK + k, p ? A + (long long)gm * t.lda + gk : A, p);
+      }
+    } else {
+#pragma unroll
+      for (int e = threadIdx.x; e < CF::BM * CF::BK; e += CF::NT) {
+        const int mn = e % CF::BM, k = e / CF::BM, gm = m0 + mn, gk = k0 + k;
+        const bool p = gm < M && gk < K;
+        cp_async16(zA + k * CF::SMA + mn, p ? A + (long long)gk * t.lda + gm : A, p);
+      }
+    }
+  }
+  if constexpr (CF::RSIDE == 2) {  // real B [K][N]
+    const double* B = reinterpret_cast<const double*>(t.B) + (long long)b * t.sB;
+#pragma unroll
+    for (int e = threadIdx.x; e < CF::BK * CF::BN / 2; e += CF::NT) {
+      const int k = e / (CF::BN / 2), nc = 2 * (e % (CF::BN / 2));
+      const int gn = n0 + nc, gk = k0 + k;
+      const bool p = gn < N && gk < K;
+      cp_async16(sB + k * CF::SMBR + nc, p ? B + (long long)gk * t.ldb + gn : B, p);
+    }
+  } else {
+    const z_t* B = t.B + (long long)b * t.sB;
+    z_t* zB = reinterpret_cast<z_t*>(sB);
+    if (!op_trans(t.opB)) {
+#pragma unroll
+      for (int e = threadIdx.x; e < CF::BN * CF::BK; e += CF::NT) {
+        const int mn = e % CF::BN, k = e / CF::BN, gn = n0 + mn, gk = k0 + k;
+        const bool p = gn < N && gk < K;
+        cp_async16(zB + k * CF::SMB + mn, p ? B + (long long)gk * t.ldb + gn : B, p);
+      }
+    } else {
+#pragma unroll
+      for (int e = threadIdx.x; e < CF::BN * CF::BK; e += CF::NT) {
+        const int mn = e / CF::BK, k = e % CF::BK, gn = n0 + mn, gk = k0 + k;
+        const bool p = gn < N && gk < K;
+        cp_async16(zB + mn * CF::SK + k, p ? B + (long long)gn * t.ldb + gk : B, p);
+      }
+    }
+  }
+}
+
+template <class CF>
+__global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_dz_kernel(const __grid_constant__ ZGemmGroup grp) {
+  extern __shared__ __align__(16) double dsm[];
+  const ZGemmDesc& d = grp.d[blockIdx.z];
+  const int tiles_n = (d.N + CF::BN - 1) / CF::BN;
+  const int tiles_m = (d.M + CF::BM - 1) / CF::BM;
+  if ((int)blockIdx.x >= tiles_m * tiles_n || (int)blockIdx.y >= d.batch) return;
+  if (d.active && !d.active[blockIdx.y]) return;
+  const int b = blockIdx.y;
+  const int m0 = (blockIdx.x / tiles_n) * CF::BM;
+  const int n0 = (blockIdx.x % tiles_n) * CF::BN;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp / CF::WN, wn = warp % CF::WN;
+  KtBounds kb;
+  {
+    auto nk = [&](int i) { return i < d.nterms ? (d.t[i].K + CF::BK - 1) / CF::BK : 0; };
+    kb.b1 = nk(0);
+    kb.b2 = kb.b1 + nk(1);
+    kb.b3 = kb.b2 + nk(2);
+  }
+  const int KT = kb.b3 + (d.nterms > 3 ? (d.t[3].K + CF::BK - 1) / CF::BK : 0);
+  auto stA = [&](int s) { return dsm + s * CF::STAGE_D; };
+  auto stB = [&](int s) { return dsm + s * CF::STAGE_D + CF::A_D; };
+  double acc_re[CF::TM][CF::TN][2], acc_im[CF::TM][CF::TN][2];
+#pragma unroll
+  for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+    for (int j = 0; j < CF::TN; ++j) acc_re[i][j][0] = acc_re[i][j][1] = acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < CF::STAGES - 1; ++s) {
+    if (s < KT) dz_load_stage<CF>(d, s, kb, b, m0, n0, stA(s), stB(s));
+    cp_async_commit();
+  }
+  const int r = lane >> 2, q = lane & 3;
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<CF::STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + CF::STAGES - 1;
+      if (nk < KT) dz_load_stage<CF>(d, nk, kb, b, m0, n0, stA(nk % CF::STAGES), stB(nk % CF::STAGES));
+      cp_async_commit();
+    }
+    const int s = kt % CF::STAGES;
+    const double* sA = stA(s);
+    const double* sB = stB(s);
+    const ZTerm& t = d.t[kb.term(kt)];
+    const unsigned long long negm = (t.neg & 1) ? kSign : 0ull;
+    const unsigned long long conjA = op_conj(t.opA) ? kSign : 0ull;
+    const unsigned long long conjB = op_conj(t.opB) ? kSign : 0ull;
+    const bool a_kc = !op_trans(t.opA), b_kc = op_trans(t.opB);
+    const int a_smn = a_kc ? CF::SK : 1, a_sk = a_kc ? 1 : CF::SMA;
+    const int b_smn = b_kc ? CF::SK : 1, b_sk = b_kc ? 1 : CF::SMB;
+#pragma unroll
+    for (int k4 = 0; k4 < CF::BK / 4; ++k4) {
+      const int kk = k4 * 4 + q;
+      if constexpr (CF::RSIDE == 1) {
+        double a[CF::TM], br[CF::TN], bi[CF::TN];
+#pragma unroll
+        for (int i = 0; i < CF::TM; ++i) a[i] = dneg_if(sA[(wm * CF::WTM + i * 8 + r) * CF::SKR + kk], negm);
+        const z_t* zB = reinterpret_cast<const z_t*>(sB);
+#pragma unroll
+        for (int j = 0; j < CF::TN; ++j) {
+          const z_t v = zB[(wn * CF::WTN + j * 8 + r) * b_smn + kk * b_sk];
+          br[j] = v.x;
+          bi[j] = dneg_if(v.y, conjB);
+        }
+#pragma unroll
+        for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+          for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], a[i], br[j]);
+#pragma unroll
+        for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+          for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], a[i], bi[j]);
+      } else {
+        double ar[CF::TM], ai[CF::TM], bv[CF::TN];
+        const z_t* zA = reinterpret_cast<const z_t*>(sA);
+#pragma unroll
+        for (int i = 0; i < CF::TM; ++i) {
+          const z_t v = zA[(wm * CF::WTM + i * 8 + r) * a_smn + kk * a_sk];
+          ar[i] = v.x;
+          ai[i] = dneg_if(v.y, conjA);
+        }
+#pragma unroll
+        for (int j = 0; j < CF::TN; ++j) bv[j] = dneg_if(sB[kk * CF::SMBR + wn * CF::WTN + j * 8 + r], negm);
+#pragma unroll
+        for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+          for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], ar[i], bv[j]);
+#pragma unroll
+        for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+          for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], bv[j]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  const double2 al = d.alpha, be = d.beta;
+  const bool use_c = d.C != nullptr && (be.x != 0.0 || be.y != 0.0);
+  const z_t* C = use_c ? d.C + (long long)b * d.sC : nullptr;
+  z_t* D = d.D + (long long)b * d.sD;
+  const int er = lane >> 2, eq = lane & 3;
+#pragma unroll
+  for (int i = 0; i < CF::TM; ++i) {
+    const int gm = m0 + wm * CF::WTM + i * 8 + er;
+#pragma unroll
+    for (int j = 0; j < CF::TN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gn = n0 + wn * CF::WTN + j * 8 + 2 * eq + h;
+        if (gm < d.M && gn < d.N) {
+          const double xr = acc_re[i][j][h], xi = acc_im[i][j][h];
+          z_t v = zmake(al.x * xr - al.y * xi, al.x * xi + al.y * xr);
+          if (use_c) {
+            const z_t c = C[(long long)gm * d.ldc + gn];
+            v.x += be.x * c.x - be.y * c.y;
+            v.y += be.x * c.y + be.y * c.x;
+          }
+          if (d.transD)
+            D[(long long)gn * d.ldd + gm] = zconj(v);
+          else
+            D[(long long)gm * d.ldd + gn] = v;
+        }
+      }
+  }
+}
+
+template <class CF>
+int launch_dz(const ZGemmGroup& g, cudaStream_t stream) {
+  static unsigned long long attr_done = 0;
+  int dev = 0;
+  NEGF_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev >= 64) return -1;
+  if (!(__atomic_load_n(&attr_done, __ATOMIC_ACQUIRE) & (1ull << dev))) {
+    NEGF_CUDA_CHECK(
+        cudaFuncSetAttribute(zgemm_dz_kernel<CF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
+    __atomic_fetch_or(&attr_done, 1ull << dev, __ATOMIC_RELEASE);
+  }
+  int max_tiles = 0, max_batch = 0;
+  for (int i = 0; i < g.n; ++i) {
+    const int tm = (g.d[i].M + CF::BM - 1) / CF::BM, tn = (g.d[i].N + CF::BN - 1) / CF::BN;
+    max_tiles = tm * tn > max_tiles ? tm * tn : max_tiles;
+    max_batch = g.d[i].batch > max_batch ? g.d[i].batch : max_batch;
+  }
+  if (max_tiles == 0 || max_batch == 0) return 0;
+  const int tok = prof_begin(PROF_ZGEMM, stream);
+  zgemm_dz_kernel<CF><<<dim3(max_tiles, max_batch, g.n), CF::NT, CF::SMEM, stream>>>(g);
+  NEGF_LAUNCHED();
+  if (tok >= 0) {
+    double fl = 0.0, by = 0.0;  // real x complex: 4 M N K flops; the real operand 8 B per element
+    for (int i = 0; i < g.n; ++i) {
+      const ZGemmDesc& d = g.d[i];
+      for (int t = 0; t < d.nterms; ++t) {
+        fl += 4.0 * d.M * d.N * (double)d.t[t].K * d.batch;
+        by += (CF::RSIDE == 1 ? 8.0 : 16.0) * d.M * d.t[t].K * d.batch +
+              (CF::RSIDE == 2 ? 8.0 : 16.0) * d.t[t].K * (double)d.N * d.batch;
+      }
+      by += 16.0 * (double)d.M * d.N * d.batch * ((d.C && (d.beta.x != 0.0 || d.beta.y != 0.0)) ? 2 : 1);
+    }
+    prof_end(tok, stream, fl, by);
+  }
+  return 0;
+}
+
+#ifndef NEGF_DZ_BM
+#define NEGF_DZ_BM 64
+#endif
+#ifndef NEGF_DZ_BN
+#define NEGF_DZ_BN 32
+#endif
+#ifndef NEGF_DZ_BK
+#define NEGF_DZ_BK 16
+#endif
+#ifndef NEGF_DZ_STAGES
+#define NEGF_DZ_STAGES 2
+#endif
+#ifndef NEGF_DZ_MINB
+#define NEGF_DZ_MINB 4
+#endif
+using DzA = DzCfg<NEGF_DZ_BM, NEGF_DZ_BN, NEGF_DZ_BK, NEGF_DZ_STAGES, NEGF_DZ_MINB, 2, 2, 1>;
+using DzB = DzCfg<NEGF_DZ_BM, NEGF_DZ_BN, NEGF_DZ_BK, NEGF_DZ_STAGES, NEGF_DZ_MINB, 2, 2, 2>;
+
 // BK = 32 x 2 stages x 2 CTAs/SM measured best of the bulk family (8 x 1024^3:
 // 39.1 TFLOP/s algorithmic vs 36.2 for the cp.async kernel and 36.0 for cuBLAS;
 // BK 16 x 3 stages 24.9, BK 8 x 4 stages 19.0, BK 16 x 2 stages x 3 CTAs 32.5)
@@ -724,6 +997,22 @@ int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
   for (int i = 0; i < g.n; ++i) mapped |= g.d[i].rowmap_a || g.d[i].rowmap_c || g.d[i].rowmap_d;
   if (mapped)  // inversion sweeps (K <= 32): occupancy wins over tile size
     return gemm_algo() == 0 ? launch_cfg<CfgMapT4>(g, stream) : launch_cfg<CfgMapT>(g, stream);
+  {  // real operand stored as doubles (every term of the group, same side)
+    int ra = 0, rb = 0, nt = 0;
+    for (int i = 0; i < g.n; ++i)
+      for (int t = 0; t < g.d[i].nterms; ++t, ++nt) {
+        ra += (g.d[i].t[t].neg & kTermRealA) != 0;
+        rb += (g.d[i].t[t].neg & kTermRealB) != 0;
+      }
+    if (ra || rb) {
+      if (ra != nt && rb != nt) return -1;  // mixed groups are a caller bug
+#ifndef NEGF_DZ_OFF  // experiments: the same products through the complex kernels
+      return ra ? launch_dz<DzA>(g, stream) : launch_dz<DzB>(g, stream);
+#else
+      return -1;
+#endif
+    }
+  }
   if (mx <= 32) return launch_cfg<CfgSmall>(g, stream);
   if (gemm_algo() == 0) return launch_cfg<Cfg4M32>(g, stream);
   constexpr int kBulkMinM = 512;

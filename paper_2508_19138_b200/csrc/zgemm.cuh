@@ -39,10 +39,15 @@ struct ZTerm {
   int opB;
   int K;
   int neg;  // bit 0: subtract this term; bit 1 (kTermReal): A or B has an exactly
-            // zero imaginary part, so the 3M kernel skips the ai*bi product
+            // zero imaginary part, so the 3M kernel skips the ai*bi product;
+            // bit 2 / 3 (kTermRealA / kTermRealB): that operand is STORED as
+            // doubles (pointer reinterpreted, ld and batch stride in doubles,
+            // op N, ld and K (A) or N (B) even): the real x complex kernel
 };
 
 constexpr int kTermReal = 2;
+constexpr int kTermRealA = 4;
+constexpr int kTermRealB = 8;
 
 constexpr int kMaxTerms = 4;
 
