@@ -54,6 +54,15 @@ __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, do
       : "d"(a), "d"(b));
 }
 
+// Ordered variants (volatile asm keeps their program order relative to each
+// other): for software-pipelined DMMA loops.
+__device__ __forceinline__ void dmma_v(double& c0, double& c1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   int n = pred ? 16 : 0;

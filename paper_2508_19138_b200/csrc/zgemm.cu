@@ -105,6 +105,86 @@ __device__ __forceinline__ void load_stage(const ZGemmDesc& d, int kt, const KtB
   }
 }
 
+// One BK stage of the 3M product for fixed operand layouts (AKC: A tile
+// k-contiguous, BKC: B tile k-contiguous). With XOR-swizzled k-contiguous
+// tiles, step k4 of a row of parity p reads k-chunk k4 ^ p: two per-thread
+// bases (even / odd k4) plus compile-time offsets.
+template <class CF, bool RV, bool AKC, bool BKC>
+__device__ __forceinline__ void gauss_stage(const z_t* __restrict__ sA, const z_t* __restrict__ sB,
+                                            double (&acc_re)[CF::TM][CF::TN][2], double (&acc_im)[CF::TM][CF::TN][2],
+                                            double (&acc_s)[CF::GAUSS ? CF::TM : 1][CF::GAUSS ? CF::TN : 1][2],
+                                            unsigned long long negm, unsigned long long conjA,
+                                            unsigned long long conjB, int wm, int wn, int lane) {
+  const int r = lane >> 2, q = lane & 3, p = CF::SWZ ? (r & 1) : 0;
+  // per-thread bases for even and odd k4 (k-contiguous) or one base (mn-contiguous)
+  const z_t* a0;
+  const z_t* a1;
+  const z_t* b0;
+  const z_t* b1;
+  if constexpr (AKC) {
+    const z_t* row = sA + (wm * CF::WTM + r) * CF::SK;
+    a0 = row + 4 * p + q;
+    a1 = row + 4 * (1 - p) + q;
+  } else {
+    a0 = a1 = sA + q * CF::SMA + wm * CF::WTM + r;
+  }
+  if constexpr (BKC) {
+    const z_t* row = sB + (wn * CF::WTN + r) * CF::SK;
+    b0 = row + 4 * p + q;
+    b1 = row + 4 * (1 - p) + q;
+  } else {
+    b0 = b1 = sB + q * CF::SMB + wn * CF::WTN + r;
+  }
+#pragma unroll
+  for (int k4 = 0; k4 < CF::BK / 4; ++k4) {
+    const z_t* pa = (k4 & 1) ? a1 : a0;
+    const z_t* pb = (k4 & 1) ? b1 : b0;
+    double ar[CF::TM], ai[CF::TM], as[CF::TM], br[CF::TN], bi[CF::TN], bs[CF::TN];
+#pragma unroll
+    for (int i = 0; i < CF::TM; ++i) {
+      const z_t v = AKC ? pa[i * 8 * CF::SK + (k4 >> 1) * 8] : pa[k4 * 4 * CF::SMA + i * 8];
+      ar[i] = dneg_if(v.x, negm);
+      ai[i] = dneg_if(v.y, negm ^ conjA);
+      as[i] = ar[i] + ai[i];
+    }
+#pragma unroll
+    for (int j = 0; j < CF::TN; ++j) {
+      const z_t v = BKC ? pb[j * 8 * CF::SK + (k4 >> 1) * 8] : pb[k4 * 4 * CF::SMB + j * 8];
+      br[j] = v.x;
+      bi[j] = dneg_if(v.y, conjB);
+      bs[j] = br[j] + bi[j];
+    }
+    if constexpr (CF::TM == 4 && CF::TN == 2) {
+      // issue order in which consecutive DMMAs share neither operand register
+      // (volatile: kept by the compiler; +1.5 % at 256^3 / 512^3)
+      constexpr int oi[8] = {0, 1, 2, 3, 1, 0, 3, 2}, oj[8] = {0, 1, 0, 1, 0, 1, 0, 1};
+#pragma unroll
+      for (int x = 0; x < 8; ++x) dmma_v(acc_re[oi[x]][oj[x]][0], acc_re[oi[x]][oj[x]][1], ar[oi[x]], br[oj[x]]);
+      if constexpr (!RV) {
+#pragma unroll
+        for (int x = 0; x < 8; ++x) dmma_v(acc_im[oi[x]][oj[x]][0], acc_im[oi[x]][oj[x]][1], ai[oi[x]], bi[oj[x]]);
+      }
+#pragma unroll
+      for (int x = 0; x < 8; ++x) dmma_v(acc_s[oi[x]][oj[x]][0], acc_s[oi[x]][oj[x]][1], as[oi[x]], bs[oj[x]]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+        for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
+      if constexpr (!RV) {
+#pragma unroll
+        for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+          for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], bi[j]);
+      }
+#pragma unroll
+      for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+        for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_s[i][j][0], acc_s[i][j][1], as[i], bs[j]);
+    }
+  }
+}
+
 // RV: every term of the group has a real operand (kTermReal), so the 3M
 // product ai*bi vanishes and is not issued (2 DMMA products per complex one).
 template <class CF, bool RV = false>
@@ -231,21 +311,22 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
 #pragma unroll
       for (int j = 0; j < CF::TN; ++j) fb[j] = sB[(wn * CF::WTN + j * 8 + r) * b_smn + kkb * b_sk];
     };
-    z_t fa[2][CF::TM], fb[2][CF::TN];
-    fetch(0, fa[0], fb[0]);
+    if constexpr (CF::GAUSS) {
+      // the stage's layouts are uniform: dispatch to a copy of the 3M step
+      // with compile-time fragment strides (LDS with immediate offsets instead
+      // of per-fragment IMAD/LEA address arithmetic)
+      const int sel = (a_kc ? 1 : 0) | (b_kc ? 2 : 0);
+      if (sel == 0) gauss_stage<CF, RV, false, false>(sA, sB, acc_re, acc_im, acc_s, negm, conjA, conjB, wm, wn, lane);
+      else if (sel == 1) gauss_stage<CF, RV, true, false>(sA, sB, acc_re, acc_im, acc_s, negm, conjA, conjB, wm, wn, lane);
+      else if (sel == 2) gauss_stage<CF, RV, false, true>(sA, sB, acc_re, acc_im, acc_s, negm, conjA, conjB, wm, wn, lane);
+      else gauss_stage<CF, RV, true, true>(sA, sB, acc_re, acc_im, acc_s, negm, conjA, conjB, wm, wn, lane);
+      continue;
+    }
+    // 4M (algo 0): the textbook four real products per complex one
 #pragma unroll
     for (int k4 = 0; k4 < CF::BK / 4; ++k4) {
-      // software pipeline: the next step's fragments are in flight while this
-      // step's DMMAs issue (NEGF_ZGEMM_PF; otherwise load just before use)
-#ifdef NEGF_ZGEMM_PF
-      if (k4 + 1 < CF::BK / 4) fetch(k4 + 1, fa[(k4 + 1) & 1], fb[(k4 + 1) & 1]);
-      const z_t* va = fa[k4 & 1];
-      const z_t* vb = fb[k4 & 1];
-#else
-      if (k4 > 0) fetch(k4, fa[0], fb[0]);
-      const z_t* va = fa[0];
-      const z_t* vb = fb[0];
-#endif
+      z_t va[CF::TM], vb[CF::TN];
+      fetch(k4, va, vb);
       double ar[CF::TM], ai[CF::TM], nai[CF::TM], br[CF::TN], bi[CF::TN];
 #pragma unroll
       for (int i = 0; i < CF::TM; ++i) {
@@ -258,46 +339,23 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
         br[j] = vb[j].x;
         bi[j] = dneg_if(vb[j].y, conjB);
       }
-      if constexpr (!CF::GAUSS) {
-        // Phase-major issue order: the two DMMAs feeding the same accumulator
-        // are TM*TN*2 instructions apart, so the FP64 tensor pipe never waits
-        // on its own accumulation dependency.
+      // Phase-major issue order: the two DMMAs feeding the same accumulator
+      // are TM*TN*2 instructions apart, so the FP64 tensor pipe never waits
+      // on its own accumulation dependency.
 #pragma unroll
-        for (int i = 0; i < CF::TM; ++i)
+      for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
-          for (int j = 0; j < CF::TN; ++j) {
-            dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
-            dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ar[i], bi[j]);
-          }
-#pragma unroll
-        for (int i = 0; i < CF::TM; ++i)
-#pragma unroll
-          for (int j = 0; j < CF::TN; ++j) {
-            dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], nai[i], bi[j]);
-            dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], br[j]);
-          }
-      } else {
-        // 3M: acc_re <- P1, acc_im <- P2, acc_s <- P3 (combined in the epilogue)
-        double as[CF::TM], bsum[CF::TN];
-#pragma unroll
-        for (int i = 0; i < CF::TM; ++i) as[i] = ar[i] + ai[i];
-#pragma unroll
-        for (int j = 0; j < CF::TN; ++j) bsum[j] = br[j] + bi[j];
-#pragma unroll
-        for (int i = 0; i < CF::TM; ++i)
-#pragma unroll
-          for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
-        if constexpr (!RV) {
-#pragma unroll
-          for (int i = 0; i < CF::TM; ++i)
-#pragma unroll
-            for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], bi[j]);
+        for (int j = 0; j < CF::TN; ++j) {
+          dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
+          dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ar[i], bi[j]);
         }
 #pragma unroll
-        for (int i = 0; i < CF::TM; ++i)
+      for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
-          for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_s[i][j][0], acc_s[i][j][1], as[i], bsum[j]);
-      }
+        for (int j = 0; j < CF::TN; ++j) {
+          dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], nai[i], bi[j]);
+          dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], br[j]);
+        }
     }
   }
   cp_async_wait<0>();
@@ -964,7 +1022,13 @@ using CfgSmall = Cfg<32, 32, 1, 1, 4, 4>;
 // default (algo 2): 3M, 64x32 CTA tiles of 4 warps, 3 CTAs/SM, BK = 16 with a
 // 2-stage cp.async pipeline and XOR-swizzled k-contiguous tiles (50 KB smem):
 // 96 DMMAs per warp between barriers
-using CfgGauss2 = Cfg<64, 32, 2, 2, 2, 3, true, 16, false, true>;
+#ifndef NEGF_G2_MINB
+#define NEGF_G2_MINB 3
+#endif
+#ifndef NEGF_G2_STAGES
+#define NEGF_G2_STAGES 2
+#endif
+using CfgGauss2 = Cfg<64, 32, 2, 2, NEGF_G2_STAGES, NEGF_G2_MINB, true, 16, false, true>;
 using CfgGauss2S = Cfg<32, 64, 2, 2, 2, 3, true, 16, false, true>;  // short M
 // algo 0: 4 real products per complex product (the textbook arithmetic)
 using Cfg4M32 = Cfg<64, 32, 2, 2, 4, 3, false>;
