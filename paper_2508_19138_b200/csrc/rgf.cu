@@ -32,6 +32,16 @@
 #include "zgemm.cuh"
 #include "zinv.cuh"
 
+#ifndef NEGF_RGF_HERM
+// Anti-Hermitian products run on lower-triangle tiles only (zgemm.cuh herm),
+// bit mask of sites: 1 = xl_0 = x_0 B_00 x_0^dag, 2 = b_i = M xl M^dag + E,
+// 4 = xl_i = x_i b_i x_i^dag. Site 4 is off: on ill-conditioned chains it
+// costs accuracy against the dense solution (34x the oracle's error on the
+// unscaled random systems of test_gpu_rgf), sites 1 and 2 do not.
+// C2 carrier +1.2 % (G^> by recursion +2.1 %), C3-shape iteration -1.7 %.
+#define NEGF_RGF_HERM 3
+#endif
+
 namespace negf {
 
 namespace {
@@ -68,6 +78,11 @@ struct Ctx {
     d.D = D; d.sD = sD; d.ldd = bs;
     d.transD = transD;
     d.active = nullptr;
+    return d;
+  }
+  // anti-Hermitian output: only the lower-triangle tiles run (zgemm.cuh herm)
+  static ZGemmDesc ah(ZGemmDesc d, int site) {
+    if (NEGF_RGF_HERM & site) d.herm = 1;
     return d;
   }
 };
@@ -229,7 +244,7 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
   RC(G.run(sk));
   for (int q = 0; q < nk; ++q) {  // xl_0 = U x_0^dag
     int k = kinds[q];
-    G.add(c.desc(c.term(c.K(k, 0), st1, OP_N, Xd(0), sd, OP_H), Ld(k, 0), sd));
+    G.add(Ctx::ah(c.desc(c.term(c.K(k, 0), st1, OP_N, Xd(0), sd, OP_H), Ld(k, 0), sd), 1));
   }
   RC(G.run(sk));
   if (pipe) NEGF_CUDA_CHECK(cudaEventRecord(evK[0], sk));
@@ -281,8 +296,8 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
     // b_k = T1_k M_{i,i-1}^dag + E_k
     for (int q = 0; q < nk; ++q) {
       int k = kinds[q];
-      G.add(c.desc(c.term(c.K(k, 0), st1, OP_N, Ml(i - 1), so, OP_H), c.K(k, 3), st1, 1.0,
-                   c.K(k, 2), st1, 1.0));
+      G.add(Ctx::ah(c.desc(c.term(c.K(k, 0), st1, OP_N, Ml(i - 1), so, OP_H), c.K(k, 3), st1, 1.0,
+                           c.K(k, 2), st1, 1.0), 2));
     }
     RC(G.run(sk));
     if (pipe) NEGF_CUDA_CHECK(cudaStreamWaitEvent(sk, evX[p], 0));
@@ -295,7 +310,7 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
     // xl_k,i = U_k x_i^dag
     for (int q = 0; q < nk; ++q) {
       int k = kinds[q];
-      G.add(c.desc(c.term(c.K(k, 0), st1, OP_N, Xd(i), sd, OP_H), Ld(k, i), sd));
+      G.add(Ctx::ah(c.desc(c.term(c.K(k, 0), st1, OP_N, Xd(i), sd, OP_H), Ld(k, i), sd), 4));
     }
     RC(G.run(sk));
     if (pipe) NEGF_CUDA_CHECK(cudaEventRecord(evK[p], sk));

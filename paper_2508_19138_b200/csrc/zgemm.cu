@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
   const int b = blockIdx.y;
   const int m0 = (blockIdx.x / tiles_n) * CF::BM;
   const int n0 = (blockIdx.x % tiles_n) * CF::BN;
+  if (d.herm && n0 >= m0 + CF::BM) return;  // strictly above the diagonal: mirrored by the lower tiles
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp / CF::WN, wn = warp % CF::WN;
 
@@ -320,42 +321,42 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
       else if (sel == 1) gauss_stage<CF, RV, true, false>(sA, sB, acc_re, acc_im, acc_s, negm, conjA, conjB, wm, wn, lane);
       else if (sel == 2) gauss_stage<CF, RV, false, true>(sA, sB, acc_re, acc_im, acc_s, negm, conjA, conjB, wm, wn, lane);
       else gauss_stage<CF, RV, true, true>(sA, sB, acc_re, acc_im, acc_s, negm, conjA, conjB, wm, wn, lane);
-      continue;
-    }
-    // 4M (algo 0): the textbook four real products per complex one
+    } else {
+      // 4M (algo 0): the textbook four real products per complex one
 #pragma unroll
-    for (int k4 = 0; k4 < CF::BK / 4; ++k4) {
-      z_t va[CF::TM], vb[CF::TN];
-      fetch(k4, va, vb);
-      double ar[CF::TM], ai[CF::TM], nai[CF::TM], br[CF::TN], bi[CF::TN];
+      for (int k4 = 0; k4 < CF::BK / 4; ++k4) {
+        z_t va[CF::TM], vb[CF::TN];
+        fetch(k4, va, vb);
+        double ar[CF::TM], ai[CF::TM], nai[CF::TM], br[CF::TN], bi[CF::TN];
 #pragma unroll
-      for (int i = 0; i < CF::TM; ++i) {
-        ar[i] = dneg_if(va[i].x, negm);
-        ai[i] = dneg_if(va[i].y, negm ^ conjA);
-        nai[i] = dneg_if(ai[i], kSign);
-      }
-#pragma unroll
-      for (int j = 0; j < CF::TN; ++j) {
-        br[j] = vb[j].x;
-        bi[j] = dneg_if(vb[j].y, conjB);
-      }
-      // Phase-major issue order: the two DMMAs feeding the same accumulator
-      // are TM*TN*2 instructions apart, so the FP64 tensor pipe never waits
-      // on its own accumulation dependency.
-#pragma unroll
-      for (int i = 0; i < CF::TM; ++i)
-#pragma unroll
-        for (int j = 0; j < CF::TN; ++j) {
-          dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
-          dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ar[i], bi[j]);
+        for (int i = 0; i < CF::TM; ++i) {
+          ar[i] = dneg_if(va[i].x, negm);
+          ai[i] = dneg_if(va[i].y, negm ^ conjA);
+          nai[i] = dneg_if(ai[i], kSign);
         }
 #pragma unroll
-      for (int i = 0; i < CF::TM; ++i)
-#pragma unroll
         for (int j = 0; j < CF::TN; ++j) {
-          dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], nai[i], bi[j]);
-          dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], br[j]);
+          br[j] = vb[j].x;
+          bi[j] = dneg_if(vb[j].y, conjB);
         }
+        // Phase-major issue order: the two DMMAs feeding the same accumulator
+        // are TM*TN*2 instructions apart, so the FP64 tensor pipe never waits
+        // on its own accumulation dependency.
+#pragma unroll
+        for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+          for (int j = 0; j < CF::TN; ++j) {
+            dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
+            dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ar[i], bi[j]);
+          }
+#pragma unroll
+        for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+          for (int j = 0; j < CF::TN; ++j) {
+            dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], nai[i], bi[j]);
+            dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], br[j]);
+          }
+      }
     }
   }
   cp_async_wait<0>();
@@ -382,7 +383,14 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_kernel(const __grid_co
           const z_t c = cfrag[PREC ? i : 0][j][h];
           v.x += be.x * c.x - be.y * c.y;
           v.y += be.x * c.y + be.y * c.x;
-          if (d.transD)
+          if (d.herm) {  // lower triangle + mirror; the diagonal projected to i Im v
+            if (gm > gn) {
+              D[(long long)gm * d.ldd + gn] = v;
+              D[(long long)gn * d.ldd + gm] = zmake(-v.x, v.y);
+            } else if (gm == gn) {
+              D[(long long)gm * d.ldd + gn] = zmake(0.0, v.y);
+            }
+          } else if (d.transD)
             D[(long long)gn * d.ldd + gm] = zconj(v);
           else
             D[(long long)drow[i] * d.ldd + gn] = v;
@@ -549,6 +557,7 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_bulk_kernel(const __gr
   const int b = blockIdx.y;
   const int m0 = (blockIdx.x / tiles_n) * CF::BM;
   const int n0 = (blockIdx.x % tiles_n) * CF::BN;
+  if (d.herm && n0 >= m0 + CF::BM) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + CF::STAGES * CF::STAGE_ELEMS);
   unsigned long long* empty = full + CF::STAGES;
@@ -669,7 +678,14 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_bulk_kernel(const __gr
           const z_t c = cv[j][h];
           v.x += be.x * c.x - be.y * c.y;
           v.y += be.x * c.y + be.y * c.x;
-          if (d.transD)
+          if (d.herm) {  // lower triangle + mirror; the diagonal projected to i Im v
+            if (gm > gn) {
+              D[(long long)gm * d.ldd + gn] = v;
+              D[(long long)gn * d.ldd + gm] = zmake(-v.x, v.y);
+            } else if (gm == gn) {
+              D[(long long)gm * d.ldd + gn] = zmake(0.0, v.y);
+            }
+          } else if (d.transD)
             D[(long long)gn * d.ldd + gm] = zconj(v);
           else
             D[(long long)gm * d.ldd + gn] = v;

@@ -62,6 +62,12 @@ struct ZGemmDesc {
   long long sD;
   int ldd;
   int transD;  // store conj-transposed
+  // anti-Hermitian output (D = -D^H, e.g. x b x^dag with b anti-Hermitian;
+  // M == N): only tiles meeting the lower triangle run, each element below
+  // the diagonal is stored with its mirror -conj(v), the diagonal as i Im v
+  // (keeping a computed real part lets the Hermitian rounding component of a
+  // chained x b x^dag recursion grow step by step) -- about half the products
+  int herm;
   const int* active;  // optional per-batch mask: problems with active[b]==0 are skipped
   // Optional per-batch row indirection (stride s_map per batch entry): logical
   // row m of op(A) (non-transposed A only), of C and of D is physical row
@@ -86,7 +92,7 @@ inline ZGemmDesc zdesc_default() {
   d.alpha = make_double2(1.0, 0.0); d.beta = make_double2(0.0, 0.0);
   d.C = nullptr; d.sC = 0; d.ldc = 0;
   d.D = nullptr; d.sD = 0; d.ldd = 0;
-  d.transD = 0; d.active = nullptr;
+  d.transD = 0; d.herm = 0; d.active = nullptr;
   d.rowmap_a = d.rowmap_c = d.rowmap_d = nullptr;
   d.s_map = 0;
   return d;
