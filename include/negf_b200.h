@@ -363,9 +363,13 @@ int negf_w_assemble(int n_e, int n_b, int bs, const void* v_diag, const void* v_
                     const void* pg_diag, const void* pg_upper, void* m_diag, void* m_upper,
                     void* m_lower, void* bl_diag, void* bl_upper, void* bg_diag, void* bg_upper,
                     int v_real, void* workspace, size_t workspace_bytes, void* stream);
-/* v_real != 0: the caller guarantees imag(V) == 0 exactly (e.g. a real
- * Coulomb matrix); each V product then skips the vanishing ai*bi Gauss
- * product (2 instead of 3 real GEMMs, bitwise the same result).
+/* v_real bit 0: the caller guarantees imag(V) == 0 exactly (e.g. a real
+ * Coulomb matrix); each V product then runs as a real x complex product
+ * (2 real GEMMs instead of 3). Bit 1: V is Hermitian (v_diag[i] = v_diag[i]^H,
+ * v_lower[i] = v_upper[i]^H) and the P^<> diagonal blocks are anti-Hermitian
+ * (as every lg-compressed quantity of the solver is), so the diagonal source
+ * blocks (V P V)_ii are anti-Hermitian and are formed on the lower-triangle
+ * tiles only.
  * W contact closure in place (scba.py:839-858, _lead_lg_boundary :617-664):
  * Sancho surface block per side (status/iters [2][n_e], codes as
  * negf_obc_sancho_batched), geometric Stein per side and kind (stein_status/

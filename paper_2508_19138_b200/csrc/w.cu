@@ -25,6 +25,10 @@
 #include "obc.cuh"
 #include "zgemm.cuh"
 
+#ifndef NEGF_W_HERM
+#define NEGF_W_HERM 1  // anti-Hermitian diagonal source blocks on half the tiles (0: full products)
+#endif
+
 namespace negf {
 namespace {
 
@@ -116,7 +120,7 @@ int negf_w_assemble(int n_e, int n_b, int bs, const void* v_diag, const void* v_
   // A real V (Coulomb) with an even block size goes to the real x complex
   // kernel from a double copy (energy independent, 3 n_b - 2 blocks).
 #ifndef NEGF_DZ_OFF
-  const bool vd = v_real != 0 && bs % 2 == 0;
+  const bool vd = (v_real & 1) != 0 && bs % 2 == 0;
 #else
   const bool vd = false;
 #endif
@@ -129,7 +133,7 @@ int negf_w_assemble(int n_e, int n_b, int bs, const void* v_diag, const void* v_
     NEGF_LAUNCHED();
   }
   auto V = [&](int i, int j) -> Opnd {  // energy independent
-    const bool re = v_real != 0;
+    const bool re = (v_real & 1) != 0;
     const long long k = i == j ? i : j == i + 1 ? n_b + i : 2LL * n_b - 1 + j;  // block of the real copy
     if (vd) return Opnd{reinterpret_cast<const z_t*>(vr + k * n2), 0, OP_N, false, true, true};
     if (i == j) return Opnd{(const z_t*)v_diag + i * n2, 0, OP_N, false, re};
@@ -220,6 +224,7 @@ int negf_w_assemble(int n_e, int n_b, int bs, const void* v_diag, const void* v_
         ZGemmDesc d = k == 1 ? sum_desc(bs, n_e, {t[0]}, D, sd, 1.0)
                     : k == 2 ? sum_desc(bs, n_e, {t[0], t[1]}, D, sd, 1.0)
                              : sum_desc(bs, n_e, {t[0], t[1], t[2]}, D, sd, 1.0);
+        d.herm = NEGF_W_HERM && (v_real & 2);  // Hermitian V: B_ii = (V P V)_ii anti-Hermitian
         gb.add(d);
       }
       if (in(i + 1)) {

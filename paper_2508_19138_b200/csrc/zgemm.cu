@@ -836,6 +836,7 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_dz_kernel(const __grid
   const int b = blockIdx.y;
   const int m0 = (blockIdx.x / tiles_n) * CF::BM;
   const int n0 = (blockIdx.x % tiles_n) * CF::BN;
+  if (d.herm && n0 >= m0 + CF::BM) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp / CF::WN, wn = warp % CF::WN;
   KtBounds kb;
@@ -943,7 +944,14 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_dz_kernel(const __grid
             v.x += be.x * c.x - be.y * c.y;
             v.y += be.x * c.y + be.y * c.x;
           }
-          if (d.transD)
+          if (d.herm) {  // lower triangle + mirror; the diagonal projected to i Im v
+            if (gm > gn) {
+              D[(long long)gm * d.ldd + gn] = v;
+              D[(long long)gn * d.ldd + gm] = zmake(-v.x, v.y);
+            } else if (gm == gn) {
+              D[(long long)gm * d.ldd + gn] = zmake(0.0, v.y);
+            }
+          } else if (d.transD)
             D[(long long)gn * d.ldd + gm] = zconj(v);
           else
             D[(long long)gm * d.ldd + gn] = v;

@@ -266,6 +266,11 @@ class ScreenedSolver:
         # a V with exactly zero imaginary part (the reference's coulomb_matrix)
         # lets the 3M GEMM skip its ai*bi product on every assembly term
         self.v_real = all(bool(torch.all(x.imag == 0)) for x in self.v)
+        # a Hermitian V makes the diagonal W sources (V P V)_ii anti-Hermitian
+        # (formed on half the tiles, negf_w_assemble bit 1)
+        vd, vu, vl = self.v
+        self.v_herm = bool(torch.equal(vd, vd.conj().transpose(-1, -2))) and bool(
+            torch.equal(vl, vu.conj().transpose(-1, -2)))
         self.opt = options
         self.dd = None  # (PartitionPlan, Comm) in the spatial mode of scba_run
         self._buf, self._n_e = None, 0
@@ -333,7 +338,7 @@ class ScreenedSolver:
                                  p(b["pr_lower"]), p(b["pl_diag"]), p(b["pl_upper"]), p(b["pg_diag"]),
                                  p(b["pg_upper"]), p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]),
                                  p(b["bl_diag"]), p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]),
-                                 int(self.v_real), p(ws), nbytes,
+                                 int(self.v_real) | (2 if self.v_herm else 0), p(ws), nbytes,
                                  _lib.stream_ptr(self.dev))
         _lib.check(rc, "negf_w_assemble")
 

@@ -79,24 +79,27 @@ def test_screened_solve_matches_oracle(cuda, n_b, bs, ne):
 @pytest.mark.parametrize("complex_v,bs", [(False, 24), (False, 23), (True, 24)])
 def test_w_assembly_real_v_path(cuda, complex_v, bs):
     """A real V (ScreenedSolver.v_real) takes the real x complex kernel from a
-    double copy of V (even block sizes) or the 2-product Gauss path (odd):
-    equal to the general 3-product path to roundoff; a complex V is detected;
-    all match the oracle's W system."""
+    double copy of V (even block sizes) or the 2-product Gauss path (odd),
+    and a Hermitian V forms the anti-Hermitian diagonal sources on half the
+    tiles (v_herm): equal to the general full 3-product path to roundoff; a
+    complex non-Hermitian V is detected; all match the oracle's W system.
+    P^<> are anti-Hermitian like every lg-compressed quantity of the solver."""
     rng = np.random.default_rng(3)
     n_b, ne = 5, 3
     v = orc.coulomb_matrix(n_b, bs)
     if complex_v:
         v = tuple(x + 1e-4j * rng.standard_normal(x.shape) for x in v)
     mk = lambda *s: 0.3 * (rng.standard_normal(s) + 1j * rng.standard_normal(s))
+    ah = lambda x: 0.5 * (x - np.conj(np.swapaxes(x, -1, -2)))
     pr = (mk(ne, n_b, bs, bs) - 1j * np.eye(bs), mk(ne, n_b - 1, bs, bs), mk(ne, n_b - 1, bs, bs))
-    pl = (mk(ne, n_b, bs, bs), mk(ne, n_b - 1, bs, bs))
-    pg = (mk(ne, n_b, bs, bs), mk(ne, n_b - 1, bs, bs))
+    pl = (ah(mk(ne, n_b, bs, bs)), mk(ne, n_b - 1, bs, bs))
+    pg = (ah(mk(ne, n_b, bs, bs)), mk(ne, n_b - 1, bs, bs))
     outs = []
     for force_complex in (False, True):
         solver = ScreenedSolver(v, ScbaOptions(retarded_method="sancho"), cuda)
-        assert solver.v_real == (not complex_v)
+        assert solver.v_real == (not complex_v) and solver.v_herm == (not complex_v)
         if force_complex:
-            solver.v_real = False
+            solver.v_real = solver.v_herm = False
         b = solver.buffers(ne)
         for k, a in (("pr_diag", pr[0]), ("pr_upper", pr[1]), ("pr_lower", pr[2]), ("pl_diag", pl[0]),
                      ("pl_upper", pl[1]), ("pg_diag", pg[0]), ("pg_upper", pg[1])):
