@@ -1,0 +1,7 @@
+# final 4-GPU checks: every GPU test (multi-rank ones included), bench at N=2 and N=4 (driver-style torchrun)
+timeout 2400 python -m pytest tests/ -q -m gpu 2>&1 | grep -v OMP | grep -E "FAILED|passed|failed|^E  .*assert" | head -20
+for n in 2 4; do
+  timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29517 \
+    bench.py --gpus $n --steps 10 --warmup 3 > gpurun_out/bench_final_n$n.json 2> gpurun_out/bench_final_n$n.err
+  echo "n=$n rc=$?"; tail -c 400 gpurun_out/bench_final_n$n.json
+done
