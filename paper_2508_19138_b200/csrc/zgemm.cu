@@ -105,6 +105,44 @@ __device__ __forceinline__ void load_stage(const ZGemmDesc& d, int kt, const KtB
   }
 }
 
+// One k4 step of the 3M product on a warp tile of TM x TN 8x8 DMMA tiles:
+// acc_re += ar br, acc_im += ai bi (skipped for a real operand), acc_s +=
+// (ar+ai)(br+bi). ORD (4 x 2 tiles): the 24 DMMAs issue in an order in which
+// consecutive DMMAs share neither operand register (volatile: kept by the
+// compiler; +1.5 % for the cp.async kernel at 256^3 / 512^3, -1.2 % for the
+// bulk-copy kernel, which keeps the compiler's order).
+template <int TM, int TN, bool RV, bool ORD = true>
+__device__ __forceinline__ void mma3m_step(double (&acc_re)[TM][TN][2], double (&acc_im)[TM][TN][2],
+                                           double (&acc_s)[TM][TN][2], const double* ar, const double* ai,
+                                           const double* as, const double* br, const double* bi, const double* bs) {
+  if constexpr (ORD && TM == 4 && TN == 2) {
+    constexpr int oi[8] = {0, 1, 2, 3, 1, 0, 3, 2}, oj[8] = {0, 1, 0, 1, 0, 1, 0, 1};
+#pragma unroll
+    for (int x = 0; x < 8; ++x) dmma_v(acc_re[oi[x]][oj[x]][0], acc_re[oi[x]][oj[x]][1], ar[oi[x]], br[oj[x]]);
+    if constexpr (!RV) {
+#pragma unroll
+      for (int x = 0; x < 8; ++x) dmma_v(acc_im[oi[x]][oj[x]][0], acc_im[oi[x]][oj[x]][1], ai[oi[x]], bi[oj[x]]);
+    }
+#pragma unroll
+    for (int x = 0; x < 8; ++x) dmma_v(acc_s[oi[x]][oj[x]][0], acc_s[oi[x]][oj[x]][1], as[oi[x]], bs[oj[x]]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
+    if constexpr (!RV) {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], bi[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) dmma_m8n8k4(acc_s[i][j][0], acc_s[i][j][1], as[i], bs[j]);
+  }
+}
+
 // One BK stage of the 3M product for fixed operand layouts (AKC: A tile
 // k-contiguous, BKC: B tile k-contiguous). With XOR-swizzled k-contiguous
 // tiles, step k4 of a row of parity p reads k-chunk k4 ^ p: two per-thread
@@ -154,34 +192,7 @@ __device__ __forceinline__ void gauss_stage(const z_t* __restrict__ sA, const z_
       bi[j] = dneg_if(v.y, conjB);
       bs[j] = br[j] + bi[j];
     }
-    if constexpr (CF::TM == 4 && CF::TN == 2) {
-      // issue order in which consecutive DMMAs share neither operand register
-      // (volatile: kept by the compiler; +1.5 % at 256^3 / 512^3)
-      constexpr int oi[8] = {0, 1, 2, 3, 1, 0, 3, 2}, oj[8] = {0, 1, 0, 1, 0, 1, 0, 1};
-#pragma unroll
-      for (int x = 0; x < 8; ++x) dmma_v(acc_re[oi[x]][oj[x]][0], acc_re[oi[x]][oj[x]][1], ar[oi[x]], br[oj[x]]);
-      if constexpr (!RV) {
-#pragma unroll
-        for (int x = 0; x < 8; ++x) dmma_v(acc_im[oi[x]][oj[x]][0], acc_im[oi[x]][oj[x]][1], ai[oi[x]], bi[oj[x]]);
-      }
-#pragma unroll
-      for (int x = 0; x < 8; ++x) dmma_v(acc_s[oi[x]][oj[x]][0], acc_s[oi[x]][oj[x]][1], as[oi[x]], bs[oj[x]]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < CF::TM; ++i)
-#pragma unroll
-        for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
-      if constexpr (!RV) {
-#pragma unroll
-        for (int i = 0; i < CF::TM; ++i)
-#pragma unroll
-          for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], bi[j]);
-      }
-#pragma unroll
-      for (int i = 0; i < CF::TM; ++i)
-#pragma unroll
-        for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_s[i][j][0], acc_s[i][j][1], as[i], bs[j]);
-    }
+    mma3m_step<CF::TM, CF::TN, RV>(acc_re, acc_im, acc_s, ar, ai, as, br, bi, bs);
   }
 }
 
@@ -630,20 +641,7 @@ __global__ void __launch_bounds__(CF::NT, CF::MINB) zgemm_bulk_kernel(const __gr
         bsum[j] = br[j] + bi[j];
       }
       // 3M: acc_re <- ar br, acc_im <- ai bi, acc_s <- (ar+ai)(br+bi)
-#pragma unroll
-      for (int i = 0; i < CF::TM; ++i)
-#pragma unroll
-        for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_re[i][j][0], acc_re[i][j][1], ar[i], br[j]);
-      if constexpr (!RV) {
-#pragma unroll
-        for (int i = 0; i < CF::TM; ++i)
-#pragma unroll
-          for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_im[i][j][0], acc_im[i][j][1], ai[i], bi[j]);
-      }
-#pragma unroll
-      for (int i = 0; i < CF::TM; ++i)
-#pragma unroll
-        for (int j = 0; j < CF::TN; ++j) dmma_m8n8k4(acc_s[i][j][0], acc_s[i][j][1], as[i], bsum[j]);
+      mma3m_step<CF::TM, CF::TN, RV, false>(acc_re, acc_im, acc_s, ar, ai, as, br, bi, bsum);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);
