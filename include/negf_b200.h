@@ -42,8 +42,11 @@ int negf_set_rgf_overlap(int on);
 
 /* ---- (1) selected solve -------------------------------------------------
  * Replaces negfgw.rgf.selected_solve (pkg/src/negfgw/rgf.py:232-243) and, with
- * symmetrize=1, the SelectedSolution.symmetrize() that scba_run applies
- * after it (scba.py:987,1087; rgf.py:82-88), for a batch of n_e energies:
+ * symmetrize bit 0, the SelectedSolution.symmetrize() that scba_run applies
+ * after it (scba.py:987,1087; rgf.py:82-88), for a batch of n_e energies.
+ * symmetrize bit 1 declares the B^lg diagonal blocks anti-Hermitian (as every
+ * lg source of the NEGF/GW solver is): the anti-Hermitian forward products
+ * then run on the lower-triangle tiles only.
  *   M X^R = I,  M X^lg M^dag = B^lg  (selected blocks).
  * b_lesser / b_greater are lg-compressed (diag + upper; lower implied by
  * B[i+1][i] = -B[i][i+1]^dag, blocks.py:110-118); pass NULL for an absent

@@ -214,11 +214,14 @@ class CarrierSolver:
 
 
 def rgf_selected_solve_split(lib, b: dict, ne: int, n_b: int, bs: int, dev, streams: int, side_streams,
-                             prefix: tuple = ("m", "bl", "bg", "xr", "xl", "xg"), symmetrize: int = 1,
+                             prefix: tuple = ("m", "bl", "bg", "xr", "xl", "xg"), symmetrize: int = 3,
                              kinds: tuple = ("bl", "bg")) -> None:
     """RGF over the batch in ``b``, split into ``streams`` energy slices on
     side streams so the latency-bound inversion panels of one slice overlap
-    the DMMA GEMMs of another (energies are independent)."""
+    the DMMA GEMMs of another (energies are independent). ``symmetrize``:
+    bit 0 symmetrizes the Keldysh diagonal blocks (rgf.py:82-88), bit 1
+    declares the B^lg diagonal blocks anti-Hermitian -- true of the carrier
+    sources Sigma^lg +- 2i eta f I and the contact terms."""
     m, bl, bg, xr, xl, xg = prefix
     p = _lib.ptr
     main = torch.cuda.current_stream(dev)

@@ -78,7 +78,7 @@ int negf_rgf_sweeps_batched(int mode, int fwd_given, int n_e, int n_b, int bs, c
   a.xr_diag = (z_t*)xr_diag; a.xr_upper = (z_t*)xr_upper; a.xr_lower = (z_t*)xr_lower;
   a.xl_diag[0] = (z_t*)xl_diag; a.xl_upper[0] = (z_t*)xl_upper;
   a.xl_diag[1] = (z_t*)xg_diag; a.xl_upper[1] = (z_t*)xg_upper;
-  a.symmetrize = mode == 1 ? 0 : symmetrize;
+  a.symmetrize = mode == 1 ? (symmetrize & 2) : symmetrize;
   a.status = status;
   a.u_spread = u_spread;
   a.overlap = rgf_overlap_default();

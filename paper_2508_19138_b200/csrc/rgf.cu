@@ -81,8 +81,9 @@ struct Ctx {
     return d;
   }
   // anti-Hermitian output: only the lower-triangle tiles run (zgemm.cuh herm)
-  static ZGemmDesc ah(ZGemmDesc d, int site) {
-    if (NEGF_RGF_HERM & site) d.herm = 1;
+  int lg_ah = 0;  // B^lg diagonal blocks anti-Hermitian (RgfArgs.symmetrize bit 1)
+  ZGemmDesc ah(ZGemmDesc d, int site) const {
+    if (lg_ah && (NEGF_RGF_HERM & site)) d.herm = 1;
     return d;
   }
 };
@@ -131,6 +132,7 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
   if (ws_bytes < rgf_workspace_bytes(a.n_e, a.n_b, a.bs)) return -4;
   Ctx c;
   c.n_e = a.n_e; c.n_b = a.n_b; c.bs = a.bs;
+  c.lg_ah = (a.symmetrize & 2) != 0;
   c.bs2 = (long long)a.bs * a.bs;
   c.sdiag = (long long)a.n_b * c.bs2;
   c.soff = (long long)(a.n_b > 1 ? a.n_b - 1 : 0) * c.bs2;
@@ -244,7 +246,7 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
   RC(G.run(sk));
   for (int q = 0; q < nk; ++q) {  // xl_0 = U x_0^dag
     int k = kinds[q];
-    G.add(Ctx::ah(c.desc(c.term(c.K(k, 0), st1, OP_N, Xd(0), sd, OP_H), Ld(k, 0), sd), 1));
+    G.add(c.ah(c.desc(c.term(c.K(k, 0), st1, OP_N, Xd(0), sd, OP_H), Ld(k, 0), sd), 1));
   }
   RC(G.run(sk));
   if (pipe) NEGF_CUDA_CHECK(cudaEventRecord(evK[0], sk));
@@ -296,7 +298,7 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
     // b_k = T1_k M_{i,i-1}^dag + E_k
     for (int q = 0; q < nk; ++q) {
       int k = kinds[q];
-      G.add(Ctx::ah(c.desc(c.term(c.K(k, 0), st1, OP_N, Ml(i - 1), so, OP_H), c.K(k, 3), st1, 1.0,
+      G.add(c.ah(c.desc(c.term(c.K(k, 0), st1, OP_N, Ml(i - 1), so, OP_H), c.K(k, 3), st1, 1.0,
                            c.K(k, 2), st1, 1.0), 2));
     }
     RC(G.run(sk));
@@ -310,7 +312,7 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
     // xl_k,i = U_k x_i^dag
     for (int q = 0; q < nk; ++q) {
       int k = kinds[q];
-      G.add(Ctx::ah(c.desc(c.term(c.K(k, 0), st1, OP_N, Xd(i), sd, OP_H), Ld(k, i), sd), 4));
+      G.add(c.ah(c.desc(c.term(c.K(k, 0), st1, OP_N, Xd(i), sd, OP_H), Ld(k, i), sd), 4));
     }
     RC(G.run(sk));
     if (pipe) NEGF_CUDA_CHECK(cudaEventRecord(evK[p], sk));
@@ -382,7 +384,7 @@ int rgf_selected_solve(const RgfArgs& a, void* ws, size_t ws_bytes, cudaStream_t
     }
     RC(E.run(st));
   }
-  if (a.symmetrize)
+  if (a.symmetrize & 1)
     for (int q = 0; q < nk; ++q) RC(antiherm_inplace(a.xl_diag[kinds[q]], bs2, bs, ne * n, st));
   return 0;
 }

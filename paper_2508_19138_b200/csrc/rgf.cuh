@@ -19,7 +19,9 @@ struct RgfArgs {
   z_t* xr_lower;
   z_t* xl_diag[2];
   z_t* xl_upper[2];
-  int symmetrize;      // apply (X - X^dag)/2 to the lesser/greater diagonal blocks
+  int symmetrize;      // bit 0: apply (X - X^dag)/2 to the lesser/greater diagonal blocks;
+                       // bit 1: the B^lg diagonal blocks are anti-Hermitian (every lg source of
+                       // the solver is), so anti-Hermitian forward products run on half the tiles
   int* status;         // [n_e] device: 0 ok, 1 + forward step of the first singular block
   double* u_spread;    // [n_e][n_b] device, optional
   int overlap;         // forward sweep: Keldysh products on a second stream (default 1)

@@ -59,6 +59,7 @@ def selected_solve_batched(
     check: bool = True,
     u_spread: torch.Tensor | None = None,
     status: torch.Tensor | None = None,
+    lg_anti_hermitian: bool = False,
 ) -> dict[str, torch.Tensor]:
     """Batched selected inverse of M (n_e, n_b, bs, bs) and X^lg = M^-1 B M^-dag.
 
@@ -66,7 +67,10 @@ def selected_solve_batched(
     ``xl_*`` (lesser) / ``xg_*`` (greater) with diag + upper blocks. With
     ``check`` the per-energy status is read back and a singular Schur
     complement raises ``SingularBlockError`` naming the forward step like
-    rgf.py:121-126 (this synchronises the stream).
+    rgf.py:121-126 (this synchronises the stream). ``lg_anti_hermitian``
+    declares the B^lg diagonal blocks anti-Hermitian (true of every lesser /
+    greater source of the NEGF/GW solver), which lets the anti-Hermitian
+    forward products run on half the tiles; the reference takes any B.
     """
     lib = _lib.load()
     n_e, n_b, bs = m_diag.shape[0], m_diag.shape[1], m_diag.shape[2]
@@ -101,7 +105,8 @@ def selected_solve_batched(
         p(out.get("xl_upper")) if b_lesser is not None else None,
         p(out.get("xg_diag")) if b_greater is not None else None,
         p(out.get("xg_upper")) if b_greater is not None else None,
-        1 if symmetrize else 0, p(status), p(u_spread), p(ws), ws_bytes, _lib.stream_ptr(dev),
+        (1 if symmetrize else 0) | (2 if lg_anti_hermitian else 0), p(status), p(u_spread), p(ws), ws_bytes,
+        _lib.stream_ptr(dev),
     )
     _lib.check(rc, "negf_rgf_selected_solve_batched")
     out["status"] = status

@@ -396,7 +396,8 @@ class ScreenedSolver:
         rc = lib.negf_rgf_selected_solve_batched(
             n_e, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]), p(b["bl_diag"]),
             p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]), p(b["wr_diag"]), p(b["wr_upper"]),
-            p(b["wr_lower"]), p(b["wl_diag"]), p(b["wl_upper"]), p(b["wg_diag"]), p(b["wg_upper"]), 1,
+            p(b["wr_lower"]), p(b["wl_diag"]), p(b["wl_upper"]), p(b["wg_diag"]), p(b["wg_upper"]),
+            1 | (2 if self.v_herm else 0),  # a Hermitian V makes the W sources anti-Hermitian
             p(b["rgf_status"]), None, p(ws), nbytes, _lib.stream_ptr(self.dev))
         _lib.check(rc, "negf_rgf_selected_solve_batched")
 

@@ -23,11 +23,11 @@ def dev(x, cuda):
     return torch.from_numpy(np.ascontiguousarray(x)).to(cuda)
 
 
-def run_gpu(m, b, cuda, symmetrize=False):
+def run_gpu(m, b, cuda, symmetrize=False, lg_ah=False):
     md, mu, ml = (dev(x, cuda) for x in m)
     bl = tuple(dev(x, cuda) for x in b["<"])
     bg = tuple(dev(x, cuda) for x in b[">"])
-    out = selected_solve_batched(md, mu, ml, bl, bg, symmetrize=symmetrize)
+    out = selected_solve_batched(md, mu, ml, bl, bg, symmetrize=symmetrize, lg_anti_hermitian=lg_ah)
     return {k: v.cpu().numpy() for k, v in out.items()}
 
 
@@ -76,18 +76,22 @@ PAIRS = (("xr_diag", "xr_diag"), ("xr_upper", "xr_upper"), ("xr_lower", "xr_lowe
          ("xl_upper", "x<_upper"), ("xg_diag", "x>_diag"), ("xg_upper", "x>_upper"))
 
 
+@pytest.mark.parametrize("lg_ah", [False, True])
 @pytest.mark.parametrize("n_b,bs,n_e", [(4, 128, 3), (3, 256, 2), (5, 65, 4), (2, 512, 1), (7, 16, 9), (64, 96, 2)])
-def test_rgf_matches_oracle_batched(cuda, n_b, bs, n_e):
+def test_rgf_matches_oracle_batched(cuda, n_b, bs, n_e, lg_ah):
+    """random_bt_system's B^lg diagonal blocks are anti-Hermitian, so the
+    half-tile anti-Hermitian products (lg_anti_hermitian) apply too."""
     m, b = _batch(n_b, bs, n_e, scaled=True)
     ref = orc.rgf_selected(*m, b, symmetrize=True)
-    got = run_gpu(m, b, cuda, symmetrize=True)
+    got = run_gpu(m, b, cuda, symmetrize=True, lg_ah=lg_ah)
     for k, rk in PAIRS:
         for e in range(n_e):
             assert rel(got[k][e], ref[rk][e]) < TOL, (k, e)
 
 
+@pytest.mark.parametrize("lg_ah", [False, True])
 @pytest.mark.parametrize("n_b,bs,n_e", [(4, 128, 3), (3, 256, 2)])
-def test_rgf_ill_conditioned_as_accurate_as_oracle(cuda, n_b, bs, n_e):
+def test_rgf_ill_conditioned_as_accurate_as_oracle(cuda, n_b, bs, n_e, lg_ah):
     """Unscaled random_bt_system at large bs has Schur complements with
     condition numbers up to ~1e5; there any two correct solvers differ by
     ~cond*eps. Bar: the GPU's distance to the exact (dense) solution is within
@@ -95,7 +99,7 @@ def test_rgf_ill_conditioned_as_accurate_as_oracle(cuda, n_b, bs, n_e):
     m, b = _batch(n_b, bs, n_e, scaled=False)
     ref = orc.rgf_selected(*m, b, symmetrize=True)
     dense = orc.dense_selected(*m, b)
-    got = run_gpu(m, b, cuda, symmetrize=True)
+    got = run_gpu(m, b, cuda, symmetrize=True, lg_ah=lg_ah)
     for k, rk in PAIRS:
         d = dense[rk]
         if k.endswith("_diag") and k != "xr_diag":
