@@ -1072,6 +1072,149 @@ static int g_algo = 2;
 int gemm_algo() { return g_algo; }
 void set_gemm_algo(int a) { g_algo = a; }
 
+
+// ---------------------------------------------------------------------------
+// Gauss-Jordan inversion sweep (zinv.cu), streamed: for the rows m < n - wd
+// outside the panel's pivot rows K,
+//   A_new[dst(m), :] = C(m, :) - A_old[src(m), K] * A_new[K, :],
+//   C(m, j) = A_old[src(m), j] for j outside K, 0 on K
+// (A_new[K, K] = Pinv gives the -C' Pinv block). One CTA keeps its 64 rows of
+// C' = A_old[src(m), K] in shared memory and streams column chunks of 32:
+// the next chunk's A_new[K, chunk] arrives by cp.async while this chunk's
+// DMMAs run, the chunk's C fragment is loaded into registers before the wait.
+// The generic row-mapped GEMM re-staged C' per 32 x 32 tile and exposed the
+// C load latency in every tile's epilogue (40 % DMMA pipe at K = 32).
+namespace {
+using CfgSweep = Cfg<64, 32, 2, 2, 2, 2, true, 16, false, false>;
+constexpr int kSweepSlices = 2;  // K = wd <= 32: two 16-deep slices
+constexpr size_t kSweepSmem = sizeof(z_t) * ((size_t)kSweepSlices * CfgSweep::BM * CfgSweep::SK +
+                                             2 * (size_t)kSweepSlices * CfgSweep::BK * CfgSweep::SMB);
+
+__global__ void __launch_bounds__(CfgSweep::NT, 2) zinv_sweep_kernel(const __grid_constant__ SweepArgs a) {
+  using CF = CfgSweep;
+  extern __shared__ __align__(16) z_t smem[];
+  const int b = blockIdx.z;
+  if (a.active && !a.active[b]) return;
+  const int rows = a.n - a.wd;
+  const int m0 = blockIdx.x * CF::BM;
+  const int nchunks = (a.n + CF::BN - 1) / CF::BN;
+  const int cpg = (nchunks + a.ng - 1) / a.ng;
+  const int c_begin = blockIdx.y * cpg;
+  const int c_end = c_begin + cpg < nchunks ? c_begin + cpg : nchunks;
+  if (m0 >= rows || c_begin >= c_end) return;
+  const int nsl = (a.wd + CF::BK - 1) / CF::BK;
+  const z_t* A = a.cur + (long long)b * a.cs;
+  z_t* Nw = a.nxt + (long long)b * a.ns;
+  const int* msrc = a.map_src + (long long)b * a.n;
+  const int* mdst = a.map_dst + (long long)b * a.n;
+  auto sA = [&](int s) { return smem + s * CF::BM * CF::SK; };
+  auto sB = [&](int buf, int s) {
+    return smem + kSweepSlices * CF::BM * CF::SK + (buf * kSweepSlices + s) * CF::BK * CF::SMB;
+  };
+  for (int s = 0; s < nsl; ++s)
+    for (int e = threadIdx.x; e < CF::BM * CF::BK; e += CF::NT) {
+      const int mn = e / CF::BK, k = e % CF::BK, gm = m0 + mn, gk = s * CF::BK + k;
+      const bool p = gm < rows && gk < a.wd;
+      cp_async16(sA(s) + mn * CF::SK + k, p ? A + (long long)msrc[gm] * a.n + a.k0 + gk : A, p);
+    }
+  auto load_b = [&](int c, int buf) {
+    for (int s = 0; s < nsl; ++s)
+      for (int e = threadIdx.x; e < CF::BK * CF::BN; e += CF::NT) {
+        const int k = e / CF::BN, nn = e % CF::BN, gk = s * CF::BK + k, gn = c * CF::BN + nn;
+        const bool p = gk < a.wd && gn < a.n;
+        cp_async16(sB(buf, s) + k * CF::SMB + nn, p ? Nw + (long long)(a.k0 + gk) * a.n + gn : Nw, p);
+      }
+  };
+  load_b(c_begin, 0);
+  cp_async_commit();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp / CF::WN, wn = warp % CF::WN;
+  const int er = lane >> 2, eq = lane & 3;
+  int srow[CF::TM], drow[CF::TM];
+#pragma unroll
+  for (int i = 0; i < CF::TM; ++i) {
+    const int gm = m0 + wm * CF::WTM + i * 8 + er;
+    srow[i] = gm < rows ? msrc[gm] : 0;
+    drow[i] = gm < rows ? mdst[gm] : -1;
+  }
+  for (int c = c_begin; c < c_end; ++c) {
+    const int buf = (c - c_begin) & 1;
+    if (c + 1 < c_end) load_b(c + 1, buf ^ 1);
+    cp_async_commit();
+    z_t cv[CF::TM][CF::TN][2];  // C fragment, in flight during the wait and the DMMAs
+#pragma unroll
+    for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+      for (int j = 0; j < CF::TN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gn = c * CF::BN + wn * CF::WTN + j * 8 + 2 * eq + h;
+          const bool in = drow[i] >= 0 && gn < a.n && (gn < a.k0 || gn >= a.k0 + a.wd);
+          cv[i][j][h] = in ? A[(long long)srow[i] * a.n + gn] : make_double2(0.0, 0.0);
+        }
+    cp_async_wait<1>();
+    __syncthreads();
+    double acc_re[CF::TM][CF::TN][2], acc_im[CF::TM][CF::TN][2], acc_s[CF::TM][CF::TN][2];
+#pragma unroll
+    for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+      for (int j = 0; j < CF::TN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) acc_re[i][j][h] = acc_im[i][j][h] = acc_s[i][j][h] = 0.0;
+    for (int s = 0; s < nsl; ++s)
+      gauss_stage<CF, false, true, false>(sA(s), sB(buf, s), acc_re, acc_im, acc_s, 0ull, 0ull, 0ull, wm, wn, lane);
+#pragma unroll
+    for (int i = 0; i < CF::TM; ++i) {
+      if (drow[i] < 0) continue;
+#pragma unroll
+      for (int j = 0; j < CF::TN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gn = c * CF::BN + wn * CF::WTN + j * 8 + 2 * eq + h;
+          if (gn < a.n) {
+            const double p1 = acc_re[i][j][h], p2 = acc_im[i][j][h];
+            const z_t v = cv[i][j][h];
+            Nw[(long long)drow[i] * a.n + gn] = zmake(v.x - (p1 - p2), v.y - (acc_s[i][j][h] - p1 - p2));
+          }
+        }
+    }
+    __syncthreads();  // every warp is done with buf before the next iteration refills it
+  }
+  cp_async_wait<0>();
+}
+}  // namespace
+
+int zinv_sweep_launch(const SweepArgs& a, int batch, cudaStream_t stream) {
+  const int rows = a.n - a.wd;
+  if (rows <= 0 || batch <= 0) return 0;
+  if (a.wd > kSweepSlices * CfgSweep::BK) return -1;
+  static unsigned long long attr_done = 0;
+  int dev = 0;
+  NEGF_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev >= 64) return -1;
+  if (!(__atomic_load_n(&attr_done, __ATOMIC_ACQUIRE) & (1ull << dev))) {
+    NEGF_CUDA_CHECK(cudaFuncSetAttribute(zinv_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kSweepSmem));
+    __atomic_fetch_or(&attr_done, 1ull << dev, __ATOMIC_RELEASE);
+  }
+  SweepArgs g = a;
+  const int rb = (rows + CfgSweep::BM - 1) / CfgSweep::BM;
+  const int nchunks = (a.n + CfgSweep::BN - 1) / CfgSweep::BN;
+  // column groups: enough CTAs for two per SM (296 on B200), each streaming >= 2 chunks
+  int ng = (296 + rb * batch - 1) / (rb * batch);
+  ng = ng < 1 ? 1 : (ng > (nchunks + 1) / 2 ? (nchunks + 1) / 2 : ng);
+  g.ng = ng < 1 ? 1 : ng;
+  const int tok = prof_begin(PROF_ZGEMM_SMALLK, stream);
+  zinv_sweep_kernel<<<dim3(rb, g.ng, batch), CfgSweep::NT, kSweepSmem, stream>>>(g);
+  NEGF_LAUNCHED();
+  if (tok >= 0) {
+    const double fl = 8.0 * rows * (double)a.n * a.wd * batch;
+    const double by = 16.0 * batch * (2.0 * rows * a.n + (double)a.wd * (a.n + rows));
+    prof_end(tok, stream, fl, by);
+  }
+  return 0;
+}
+
 int zgemm_group_launch(const ZGemmGroup& g, cudaStream_t stream) {
   if (g.n <= 0) return 0;
   int mx = 0;

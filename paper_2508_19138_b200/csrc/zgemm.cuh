@@ -113,4 +113,20 @@ int gemm_algo();
 void set_gemm_algo(int a);
 int zgemm_launch(const ZGemmDesc& d, cudaStream_t stream);
 
+// Streamed Gauss-Jordan sweep of the blocked inverse (zinv.cu): rows m < n - wd
+// outside the pivot rows K, A_new[dst(m), :] = C - A_old[src(m), K] A_new[K, :]
+// with C = A_old[src(m), :] outside the columns K and 0 on them.
+struct SweepArgs {
+  const z_t* cur;
+  long long cs;
+  z_t* nxt;
+  long long ns;
+  int n, k0, wd;
+  const int* map_src;  // [batch][n]
+  const int* map_dst;  // [batch][n]
+  const int* active;   // optional per-matrix mask
+  int ng;              // column groups (set by the launcher)
+};
+int zinv_sweep_launch(const SweepArgs& a, int batch, cudaStream_t stream);
+
 }  // namespace negf

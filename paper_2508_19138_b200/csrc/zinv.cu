@@ -738,6 +738,12 @@ __global__ void zinv_unpermute_kernel(const z_t* A, long long sA, int n, const i
 }
 
 constexpr int kInvPanelMax = 512;   // one-CTA register panel limit
+#ifndef NEGF_ZINV_SWEEP_MAX
+// streamed sweep kernel (zgemm.cu zinv_sweep_kernel) up to this block size, grouped row-mapped
+// GEMMs above: 256 x 128 and 512 x 8/64 inverses 4-9 % faster, 1024 x 8 and 2048 x 2 4-8 % slower
+// (8 warps/SM streaming vs 20 warps/SM of 32 x 32 tiles once the matrices leave L2)
+#define NEGF_ZINV_SWEEP_MAX 512
+#endif
 #ifndef NEGF_ZINV_NT256_MAX
 #define NEGF_ZINV_NT256_MAX 1024  // 256-thread cluster CTAs up to this block size (3-5% at 768-1024)
 #endif
@@ -884,9 +890,17 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
       }
       NEGF_LAUNCHED();
     }
-    if (n - wd > 0) {
+    if (n - wd > 0 && n <= NEGF_ZINV_SWEEP_MAX) {
       // rows outside K (row-mapped):  A_new[:, j not in K] = A_old - C' T,  A_new[:, K] = -C' Pinv,
-      // with C' = A_old[src][K] and T = rows K of A_new (written by the panel kernel).
+      // with C' = A_old[src][K] and T, Pinv = rows K of A_new (written by the panel kernel)
+      SweepArgs sa;
+      sa.cur = cur; sa.cs = cs; sa.nxt = nxt; sa.ns = ns;
+      sa.n = n; sa.k0 = k0; sa.wd = wd;
+      sa.map_src = map_src; sa.map_dst = map_dst; sa.active = aux.active; sa.ng = 1;
+      const int rc = zinv_sweep_launch(sa, batch, stream);
+      if (rc) return rc;
+    } else if (n - wd > 0) {
+      // the same sweep as grouped row-mapped GEMMs
       ZGemmGroup grp;
       grp.n = 0;
       auto prob = [&](int c0, int nc, bool colK) {
