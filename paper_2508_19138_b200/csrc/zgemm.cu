@@ -1082,15 +1082,24 @@ void set_gemm_algo(int a) { g_algo = a; }
 // C' = A_old[src(m), K] in shared memory and streams column chunks of 32:
 // the next chunk's A_new[K, chunk] arrives by cp.async while this chunk's
 // DMMAs run, the chunk's C fragment is loaded into registers before the wait.
+// 32-row CTAs of 4 warps (16 x 16 warp tiles, 126 registers, 4 CTAs/SM): the
+// 64-row CTAs (236 registers, 2/SM) were 7 % slower at 256 x 128
+// (profiles/zinv_sweep_r02.txt).
 // The generic row-mapped GEMM re-staged C' per 32 x 32 tile and exposed the
 // C load latency in every tile's epilogue (40 % DMMA pipe at K = 32).
 namespace {
-using CfgSweep = Cfg<64, 32, 2, 2, 2, 2, true, 16, false, false>;
+#ifndef NEGF_SWEEP_BM
+#define NEGF_SWEEP_BM 32
+#endif
+#ifndef NEGF_SWEEP_MINB
+#define NEGF_SWEEP_MINB 4
+#endif
+using CfgSweep = Cfg<NEGF_SWEEP_BM, 32, 2, 2, 2, NEGF_SWEEP_MINB, true, 16, false, false>;
 constexpr int kSweepSlices = 2;  // K = wd <= 32: two 16-deep slices
 constexpr size_t kSweepSmem = sizeof(z_t) * ((size_t)kSweepSlices * CfgSweep::BM * CfgSweep::SK +
                                              2 * (size_t)kSweepSlices * CfgSweep::BK * CfgSweep::SMB);
 
-__global__ void __launch_bounds__(CfgSweep::NT, 2) zinv_sweep_kernel(const __grid_constant__ SweepArgs a) {
+__global__ void __launch_bounds__(CfgSweep::NT, NEGF_SWEEP_MINB) zinv_sweep_kernel(const __grid_constant__ SweepArgs a) {
   using CF = CfgSweep;
   extern __shared__ __align__(16) z_t smem[];
   const int b = blockIdx.z;
@@ -1200,8 +1209,9 @@ int zinv_sweep_launch(const SweepArgs& a, int batch, cudaStream_t stream) {
   SweepArgs g = a;
   const int rb = (rows + CfgSweep::BM - 1) / CfgSweep::BM;
   const int nchunks = (a.n + CfgSweep::BN - 1) / CfgSweep::BN;
-  // column groups: enough CTAs for two per SM (296 on B200), each streaming >= 2 chunks
-  int ng = (296 + rb * batch - 1) / (rb * batch);
+  // column groups: enough CTAs to fill every SM (148 x resident CTAs), each streaming >= 2 chunks
+  const int target = 148 * NEGF_SWEEP_MINB;
+  int ng = (target + rb * batch - 1) / (rb * batch);
   ng = ng < 1 ? 1 : (ng > (nchunks + 1) / 2 ? (nchunks + 1) / 2 : ng);
   g.ng = ng < 1 ? 1 : ng;
   const int tok = prof_begin(PROF_ZGEMM_SMALLK, stream);
