@@ -739,10 +739,10 @@ __global__ void zinv_unpermute_kernel(const z_t* A, long long sA, int n, const i
 
 constexpr int kInvPanelMax = 512;   // one-CTA register panel limit
 #ifndef NEGF_ZINV_SWEEP_MAX
-// streamed sweep kernel (zgemm.cu zinv_sweep_kernel) up to this block size, grouped row-mapped
-// GEMMs above: 256 x 128 and 512 x 8/64 inverses 4-9 % faster, 1024 x 8 and 2048 x 2 4-8 % slower
-// (8 warps/SM streaming vs 20 warps/SM of 32 x 32 tiles once the matrices leave L2)
-#define NEGF_ZINV_SWEEP_MAX 512
+// streamed sweep kernel (zgemm.cu zinv_sweep_kernel, 32-row CTAs) up to this block size, grouped
+// row-mapped GEMMs above (experiments): 256 x 128 1.40 -> 1.24 ms, 512 x 8 1.83 -> 1.67 ms,
+// 1024 x 8 7.70 -> 7.31 ms, 2048 x 8 38.4 -> 31.4 ms, 4096 x 1 53.3 -> 50.5 ms (profiles/zinv_sweep_r02.txt)
+#define NEGF_ZINV_SWEEP_MAX 4096
 #endif
 #ifndef NEGF_ZINV_NT256_MAX
 #define NEGF_ZINV_NT256_MAX 1024  // 256-thread cluster CTAs up to this block size (3-5% at 768-1024)
