@@ -1191,6 +1191,163 @@ __global__ void __launch_bounds__(CfgSweep::NT, NEGF_SWEEP_MINB) zinv_sweep_kern
   }
   cp_async_wait<0>();
 }
+
+// Fused variant (SweepArgs.prow set, one-CTA panels): the panel kernel leaves
+// T = Pinv R (R = the pivot rows of A_old) to this kernel. Row CTAs form
+// L' = C' Pinv in shared memory (one small DMMA product), write -L' into the
+// columns K and stream D = C - L' R over the other chunks; one extra CTA per
+// column group (blockIdx.x == row blocks) streams T = Pinv R into the rows K
+// of A_new (Pinv itself on the columns K). T leaves the single-CTA panel,
+// where it was ~40 % of the panel time, for the whole GPU.
+__global__ void __launch_bounds__(CfgSweep::NT, NEGF_SWEEP_MINB) zinv_sweep_fused_kernel(
+    const __grid_constant__ SweepArgs a) {
+  using CF = CfgSweep;
+  extern __shared__ __align__(16) z_t smem[];
+  const int b = blockIdx.z;
+  if (a.active && !a.active[b]) return;
+  const int rows = a.n - a.wd;
+  const int rb = (rows + CF::BM - 1) / CF::BM;
+  const bool trole = (int)blockIdx.x == rb;
+  const int m0 = trole ? 0 : blockIdx.x * CF::BM;
+  const int nchunks = (a.n + CF::BN - 1) / CF::BN;
+  const int cpg = (nchunks + a.ng - 1) / a.ng;
+  const int c_begin = blockIdx.y * cpg;
+  const int c_end = c_begin + cpg < nchunks ? c_begin + cpg : nchunks;
+  if (c_begin >= c_end) return;
+  const int nsl = (a.wd + CF::BK - 1) / CF::BK;
+  const int wd = a.wd, n = a.n, k0 = a.k0;
+  const z_t* A = a.cur + (long long)b * a.cs;
+  z_t* Nw = a.nxt + (long long)b * a.ns;
+  const z_t* P = a.pinv + (long long)b * wd * wd;
+  const int* pr = a.prow + (long long)b * 32;
+  const int* msrc = a.map_src + (long long)b * n;
+  const int* mdst = a.map_dst + (long long)b * n;
+  auto sA = [&](int s) { return smem + s * CF::BM * CF::SK; };
+  auto sB = [&](int buf, int s) {
+    return smem + kSweepSlices * CF::BM * CF::SK + (buf * kSweepSlices + s) * CF::BK * CF::SMB;
+  };
+  // group 0: the A tile (C' rows, or Pinv for the T CTA) and, for row CTAs, Pinv as a B tile in buffer 1
+  for (int s = 0; s < nsl; ++s)
+    for (int e = threadIdx.x; e < CF::BM * CF::BK; e += CF::NT) {
+      const int mn = e / CF::BK, k = e % CF::BK, gk = s * CF::BK + k;
+      if (trole) {
+        const bool p = mn < wd && gk < wd;
+        cp_async16(sA(s) + mn * CF::SK + k, p ? P + (long long)mn * wd + gk : P, p);
+      } else {
+        const int gm = m0 + mn;
+        const bool p = gm < rows && gk < wd;
+        cp_async16(sA(s) + mn * CF::SK + k, p ? A + (long long)msrc[gm] * n + k0 + gk : A, p);
+      }
+    }
+  if (!trole)
+    for (int s = 0; s < nsl; ++s)
+      for (int e = threadIdx.x; e < CF::BK * CF::BN; e += CF::NT) {
+        const int k = e / CF::BN, nn = e % CF::BN, gk = s * CF::BK + k;
+        const bool p = gk < wd && nn < wd;
+        cp_async16(sB(1, s) + k * CF::SMB + nn, p ? P + (long long)gk * wd + nn : P, p);
+      }
+  cp_async_commit();
+  auto load_r = [&](int c, int buf) {  // B chunk: R[q][chunk] = A_old[prow[q]][chunk]
+    for (int s = 0; s < nsl; ++s)
+      for (int e = threadIdx.x; e < CF::BK * CF::BN; e += CF::NT) {
+        const int k = e / CF::BN, nn = e % CF::BN, gk = s * CF::BK + k, gn = c * CF::BN + nn;
+        const bool p = gk < wd && gn < n;
+        cp_async16(sB(buf, s) + k * CF::SMB + nn, p ? A + (long long)pr[gk] * n + gn : A, p);
+      }
+  };
+  load_r(c_begin, 0);
+  cp_async_commit();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp / CF::WN, wn = warp % CF::WN;
+  const int er = lane >> 2, eq = lane & 3;
+  double acc_re[CF::TM][CF::TN][2], acc_im[CF::TM][CF::TN][2], acc_s[CF::TM][CF::TN][2];
+  auto zero_acc = [&]() {
+#pragma unroll
+    for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+      for (int j = 0; j < CF::TN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) acc_re[i][j][h] = acc_im[i][j][h] = acc_s[i][j][h] = 0.0;
+  };
+  int srow[CF::TM], drow[CF::TM];
+#pragma unroll
+  for (int i = 0; i < CF::TM; ++i) {
+    const int gm = m0 + wm * CF::WTM + i * 8 + er;
+    if (trole) {
+      srow[i] = 0;
+      drow[i] = gm < wd ? k0 + gm : -1;
+    } else {
+      srow[i] = gm < rows ? msrc[gm] : 0;
+      drow[i] = gm < rows ? mdst[gm] : -1;
+    }
+  }
+  const int cK = k0 / CF::BN;  // the chunk holding the columns K (nb divides BN)
+  const bool ownK = cK >= c_begin && cK < c_end;
+  cp_async_wait<1>();
+  __syncthreads();
+  if (!trole) {
+    // L' = C' Pinv (32 x wd x wd), then -L' into the columns K and L' as the A tile
+    zero_acc();
+    for (int s = 0; s < nsl; ++s)
+      gauss_stage<CF, false, true, false>(sA(s), sB(1, s), acc_re, acc_im, acc_s, 0ull, 0ull, 0ull, wm, wn, lane);
+    __syncthreads();  // every warp has read C' before it is overwritten
+#pragma unroll
+    for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+      for (int j = 0; j < CF::TN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = wm * CF::WTM + i * 8 + er, col = wn * CF::WTN + j * 8 + 2 * eq + h;
+          const double p1 = acc_re[i][j][h], p2 = acc_im[i][j][h];
+          const z_t l = zmake(p1 - p2, acc_s[i][j][h] - p1 - p2);
+          sA(col / CF::BK)[row * CF::SK + col % CF::BK] = l;
+          if (ownK && drow[i] >= 0 && col < wd) Nw[(long long)drow[i] * n + k0 + col] = zmake(-l.x, -l.y);
+        }
+  } else if (ownK) {  // the T CTA: Pinv on the columns K of the rows K
+    for (int e = threadIdx.x; e < wd * wd; e += CF::NT)
+      Nw[(long long)(k0 + e / wd) * n + k0 + e % wd] = P[e];
+  }
+  __syncthreads();  // L' in place, buffer 1 free
+  for (int c = c_begin; c < c_end; ++c) {
+    const int buf = (c - c_begin) & 1;
+    if (c + 1 < c_end) load_r(c + 1, buf ^ 1);
+    cp_async_commit();
+    z_t cv[CF::TM][CF::TN][2];
+#pragma unroll
+    for (int i = 0; i < CF::TM; ++i)
+#pragma unroll
+      for (int j = 0; j < CF::TN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gn = c * CF::BN + wn * CF::WTN + j * 8 + 2 * eq + h;
+          const bool in = !trole && drow[i] >= 0 && gn < n && (gn < k0 || gn >= k0 + wd);
+          cv[i][j][h] = in ? A[(long long)srow[i] * n + gn] : make_double2(0.0, 0.0);
+        }
+    cp_async_wait<1>();
+    __syncthreads();
+    zero_acc();
+    for (int s = 0; s < nsl; ++s)
+      gauss_stage<CF, false, true, false>(sA(s), sB(buf, s), acc_re, acc_im, acc_s, 0ull, 0ull, 0ull, wm, wn, lane);
+#pragma unroll
+    for (int i = 0; i < CF::TM; ++i) {
+      if (drow[i] < 0) continue;
+#pragma unroll
+      for (int j = 0; j < CF::TN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gn = c * CF::BN + wn * CF::WTN + j * 8 + 2 * eq + h;
+          if (gn < n && (gn < k0 || gn >= k0 + wd)) {
+            const double p1 = acc_re[i][j][h], p2 = acc_im[i][j][h];
+            const double xr = p1 - p2, xi = acc_s[i][j][h] - p1 - p2;
+            const z_t v = cv[i][j][h];
+            Nw[(long long)drow[i] * n + gn] = trole ? zmake(xr, xi) : zmake(v.x - xr, v.y - xi);
+          }
+        }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+}
 }  // namespace
 
 int zinv_sweep_launch(const SweepArgs& a, int batch, cudaStream_t stream) {
@@ -1204,6 +1361,8 @@ int zinv_sweep_launch(const SweepArgs& a, int batch, cudaStream_t stream) {
   if (!(__atomic_load_n(&attr_done, __ATOMIC_ACQUIRE) & (1ull << dev))) {
     NEGF_CUDA_CHECK(cudaFuncSetAttribute(zinv_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kSweepSmem));
+    NEGF_CUDA_CHECK(cudaFuncSetAttribute(zinv_sweep_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kSweepSmem));
     __atomic_fetch_or(&attr_done, 1ull << dev, __ATOMIC_RELEASE);
   }
   SweepArgs g = a;
@@ -1215,7 +1374,12 @@ int zinv_sweep_launch(const SweepArgs& a, int batch, cudaStream_t stream) {
   ng = ng < 1 ? 1 : (ng > (nchunks + 1) / 2 ? (nchunks + 1) / 2 : ng);
   g.ng = ng < 1 ? 1 : ng;
   const int tok = prof_begin(PROF_ZGEMM_SMALLK, stream);
-  zinv_sweep_kernel<<<dim3(rb, g.ng, batch), CfgSweep::NT, kSweepSmem, stream>>>(g);
+  if (a.prow) {
+    if (a.k0 % CfgSweep::BN + a.wd > CfgSweep::BN) return -1;  // K must sit inside one column chunk
+    zinv_sweep_fused_kernel<<<dim3(rb + 1, g.ng, batch), CfgSweep::NT, kSweepSmem, stream>>>(g);
+  } else {
+    zinv_sweep_kernel<<<dim3(rb, g.ng, batch), CfgSweep::NT, kSweepSmem, stream>>>(g);
+  }
   NEGF_LAUNCHED();
   if (tok >= 0) {
     const double fl = 8.0 * rows * (double)a.n * a.wd * batch;

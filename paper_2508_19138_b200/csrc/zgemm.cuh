@@ -126,6 +126,9 @@ struct SweepArgs {
   const int* map_dst;  // [batch][n]
   const int* active;   // optional per-matrix mask
   int ng;              // column groups (set by the launcher)
+  // fused mode (one-CTA panels): T = Pinv R is formed here, not by the panel
+  const z_t* pinv;     // [batch][wd][wd]
+  const int* prow;     // [batch][32] A_old row of pivot q (nullptr: T already in A_new rows K)
 };
 int zinv_sweep_launch(const SweepArgs& a, int batch, cudaStream_t stream);
 

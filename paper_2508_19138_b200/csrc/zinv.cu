@@ -165,7 +165,8 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
                                                          z_t* __restrict__ Anew, long long sAn, int n,
                                                          int k0, int w,
                                                          int* ipiv, z_t* pinv, double* umaxmin,
-                                                         int* map_src, int* map_dst, InvAux aux) {
+                                                         int* map_src, int* map_dst, InvAux aux,
+                                                         int* prow) {
   constexpr int TPR = NB / 16;  // threads per row
   constexpr int LD = NB + 1;
   __shared__ z_t prow_s[NB];          // pivot row broadcast
@@ -390,7 +391,9 @@ __global__ void __launch_bounds__(512) zinv_panel_kernel(const z_t* __restrict__
   // accumulators + loads in flight inside the 128-register budget of the
   // 512-thread CTA (16 rows spilled and ran 8x slower).
   z_t* an = Anew + (long long)b * sAn;
-  {
+  if (prow) {  // fused sweep: hand over the pivot rows, T = Pinv R is formed there
+    if (tid < w) prow[(long long)b * 32 + tid] = k0 + posinv_s[tid];
+  } else {
     constexpr int TB = 8;
     const int tblocks = (w + TB - 1) / TB;
     for (int e = tid; e < tblocks * n; e += blockDim.x) {
@@ -738,6 +741,12 @@ __global__ void zinv_unpermute_kernel(const z_t* A, long long sA, int n, const i
 }
 
 constexpr int kInvPanelMax = 512;   // one-CTA register panel limit
+#ifndef NEGF_ZINV_FUSED_T
+#define NEGF_ZINV_FUSED_T 1  // one-CTA panels leave T = Pinv R to the sweep (zinv_sweep_fused_kernel)
+#endif
+#ifndef NEGF_ZINV_FUSED_T_MAXB
+#define NEGF_ZINV_FUSED_T_MAXB 64  // ... for batches up to this size
+#endif
 #ifndef NEGF_ZINV_SWEEP_MAX
 // streamed sweep kernel (zgemm.cu zinv_sweep_kernel, 32-row CTAs) up to this block size, grouped
 // row-mapped GEMMs above (experiments): 256 x 128 1.40 -> 1.24 ms, 512 x 8 1.83 -> 1.67 ms,
@@ -767,7 +776,7 @@ bool attr_once(const void* fn, int bytes, unsigned* done_mask) {
 size_t zinv_workspace_bytes(int n, int batch) {
   if (n <= kInvSmallMax) return 0;
   const int nb = zinv_panel_width(n, batch);
-  size_t per = 4 * sizeof(int) * (size_t)n + sizeof(double) * 2 + sizeof(z_t) * (size_t)nb * nb;
+  size_t per = 4 * sizeof(int) * (size_t)n + sizeof(double) * 2 + sizeof(z_t) * (size_t)nb * nb + sizeof(int) * 32;
   return per * batch + 256 * 8;
 }
 
@@ -827,6 +836,13 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
   int* map_src = reinterpret_cast<int*>(take(sizeof(int) * (size_t)n * batch));
   int* map_dst = reinterpret_cast<int*>(take(sizeof(int) * (size_t)n * batch));
   int* perm = reinterpret_cast<int*>(take(sizeof(int) * (size_t)n * batch));
+  // pivot rows per panel for the fused sweep (one-CTA panels): T = Pinv R leaves the panel kernel.
+  // Only while the one-CTA panels leave most SMs idle: 512 x 8 -10 %, 300 x 7 -13 %, but 256 x 128
+  // (a panel CTA on most SMs already) +4 % (profiles/zinv_sweep_r02.txt)
+  int* prow = (NEGF_ZINV_FUSED_T && batch <= NEGF_ZINV_FUSED_T_MAXB && !use_cluster(n, batch) &&
+               n <= NEGF_ZINV_SWEEP_MAX)
+                  ? reinterpret_cast<int*>(take(sizeof(int) * 32 * (size_t)batch))
+                  : nullptr;
   const int panel_threads = ((n * (nb / 16) + 31) / 32) * 32;
   static unsigned attr_u = 0;
   if (!attr_once((const void*)zinv_unpermute_kernel, 160 * 1024, &attr_u)) return -6;
@@ -842,10 +858,10 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
       if (!use_cluster(n, batch)) {
         if (nb == 32)
           zinv_panel_kernel<32><<<batch, panel_threads, 0, stream>>>(cur, cs, nxt, ns, n, k0, wd, ipiv, pinv,
-                                                                     umm, map_src, map_dst, aux);
+                                                                     umm, map_src, map_dst, aux, prow);
         else
           zinv_panel_kernel<16><<<batch, panel_threads, 0, stream>>>(cur, cs, nxt, ns, n, k0, wd, ipiv, pinv,
-                                                                     umm, map_src, map_dst, aux);
+                                                                     umm, map_src, map_dst, aux, prow);
       } else {
         // 32-column panels: 256-thread CTAs (128 rows) while the cluster stays
         // within 16 CTAs for 512 < n <= NEGF_ZINV_NT256_MAX, else 512-thread CTAs (256 rows)
@@ -897,6 +913,7 @@ int zinv_batched(z_t* S, long long sS, int lds, z_t* X, long long sX, int ldx, i
       sa.cur = cur; sa.cs = cs; sa.nxt = nxt; sa.ns = ns;
       sa.n = n; sa.k0 = k0; sa.wd = wd;
       sa.map_src = map_src; sa.map_dst = map_dst; sa.active = aux.active; sa.ng = 1;
+      sa.pinv = pinv; sa.prow = prow;
       const int rc = zinv_sweep_launch(sa, batch, stream);
       if (rc) return rc;
     } else if (n - wd > 0) {

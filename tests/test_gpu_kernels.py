@@ -46,7 +46,7 @@ def test_zgemm_matches_torch(cuda, m, n, k, op_a, op_b, algo):
     assert err < 1e-13
 
 
-@pytest.mark.parametrize("n", [1, 2, 5, 32, 63, 64, 96, 128, 256, 512])
+@pytest.mark.parametrize("n", [1, 2, 5, 32, 63, 64, 96, 100, 128, 200, 256, 300, 333, 512])
 @pytest.mark.parametrize("algo", [0, 2])
 def test_zinv_matches_numpy(cuda, n, algo):
     rng = np.random.default_rng(n)
