@@ -29,7 +29,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .carrier import RESULT_KEYS, CarrierSolver, Contacts
+from .carrier import RESULT_KEYS, CarrierSolver, Contacts, rgf_selected_solve_split
 from .conv import polarization, self_energy
 from .dist import Comm, Transposer
 from .errors import ConvergenceError, SpectralRadiusError
@@ -113,6 +113,10 @@ class ScbaOptions:
     # reference runs all three, rgf.py:232-243; its identity_defects show the
     # identity holds to ~1e-15 for G, P and Sigma). 0.6x the carrier RGF work.
     greater: str = "recursion"
+    # energy slices per device batch solved on side streams, so the inversion
+    # panels of one slice (a few SMs each at small batches) overlap the GEMMs
+    # of another (1: one stream)
+    rgf_streams: int = 1
 
     def __post_init__(self) -> None:
         if self.max_iter < 1:
@@ -131,6 +135,8 @@ class ScbaOptions:
             raise ValueError(f"entry_cutoff must be >= 0 orbitals, got {self.entry_cutoff}")
         if self.greater not in ("recursion", "identity"):
             raise ValueError(f"unknown greater mode {self.greater!r}")
+        if self.rgf_streams < 1:
+            raise ValueError(f"rgf_streams must be at least 1, got {self.rgf_streams}")
 
 
 class EntryLayout:
@@ -272,6 +278,8 @@ class ScreenedSolver:
         self.v_herm = bool(torch.equal(vd, vd.conj().transpose(-1, -2))) and bool(
             torch.equal(vl, vu.conj().transpose(-1, -2)))
         self.opt = options
+        self._side_streams = ([torch.cuda.Stream(self.dev) for _ in range(options.rgf_streams)]
+                              if options.rgf_streams > 1 else [])
         self.dd = None  # (PartitionPlan, Comm) in the spatial mode of scba_run
         self._buf, self._n_e = None, 0
 
@@ -390,16 +398,10 @@ class ScreenedSolver:
 
             dd_solve_into(b, *self.dd, prefix=("m", "bl", "bg", "wr", "wl", "wg"))
             return
-        nbytes = lib.negf_rgf_workspace_bytes(n_e, self.n_b, self.bs)
-        ws = _lib.workspace(nbytes, self.dev)
         b["rgf_status"].zero_()
-        rc = lib.negf_rgf_selected_solve_batched(
-            n_e, self.n_b, self.bs, p(b["m_diag"]), p(b["m_upper"]), p(b["m_lower"]), p(b["bl_diag"]),
-            p(b["bl_upper"]), p(b["bg_diag"]), p(b["bg_upper"]), p(b["wr_diag"]), p(b["wr_upper"]),
-            p(b["wr_lower"]), p(b["wl_diag"]), p(b["wl_upper"]), p(b["wg_diag"]), p(b["wg_upper"]),
-            1 | (2 if self.v_herm else 0),  # a Hermitian V makes the W sources anti-Hermitian
-            p(b["rgf_status"]), None, p(ws), nbytes, _lib.stream_ptr(self.dev))
-        _lib.check(rc, "negf_rgf_selected_solve_batched")
+        # a Hermitian V makes the W sources anti-Hermitian (symmetrize bit 1)
+        rgf_selected_solve_split(lib, b, n_e, self.n_b, self.bs, self.dev, self.opt.rgf_streams, self._side_streams,
+                                 prefix=("m", "bl", "bg", "wr", "wl", "wg"), symmetrize=1 | (2 if self.v_herm else 0))
 
 
 @dataclass
@@ -520,7 +522,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
     ne = len(energies)
     de = (energies[-1] - energies[0]) / (ne - 1)
     carrier = CarrierSolver(h, eta, contacts, options.surface_tol, device=dev, greater=options.greater,
-                            retarded_method=options.retarded_method, beyn=options.beyn)
+                            retarded_method=options.retarded_method, beyn=options.beyn,
+                            streams=options.rgf_streams)
     n_b, bs = carrier.n_b, carrier.bs
     lay = EntryLayout(n_b, bs, dev, cutoff=options.entry_cutoff)
     tr = Transposer(comm, lay.n_entries, ne)

@@ -28,7 +28,8 @@ torch.cuda.set_device(dev)
 h, v = toys.chain_device(n_b, bs), toys.coulomb_matrix(n_b, bs)
 e = np.linspace(-2.0, 2.0, ne * world)
 opts = ScbaOptions(retarded_method="sancho", max_iter=2, tol=1e-5, batch=batch,
-                   greater=os.environ.get("NEGF_GREATER", "recursion"))
+                   greater=os.environ.get("NEGF_GREATER", "recursion"),
+                   rgf_streams=int(os.environ.get("NEGF_RGF_STREAMS", "1")))
 res = scba_run(h, v, e, 1e-3, Contacts(0.1, -0.1, 0.05), opts, device=dev, keep_g=False, comm=comm,
                sigma_to_host=False, profile=True)
 dt = torch.tensor([res["iteration_s"][-1]], dtype=torch.float64, device=dev)
