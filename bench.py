@@ -51,7 +51,9 @@ def parse():
     ap.add_argument("--n-blocks", type=int, default=64)
     ap.add_argument("--block-size", type=int, default=256)
     ap.add_argument("--n-e", type=int, default=1024, help="energies per rank")
-    ap.add_argument("--batch", type=int, default=128, help="energies per device batch")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="energies per device batch (0: the fewest batches of at most 148 energies, so the "
+                         "one-CTA-per-matrix inversion panels cover the 148 SMs: 7 x 147 for 1024)")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--greater", choices=["identity", "recursion"], default="identity",
                     help="G^> by the exact identity G^> = G^< + G^R - G^R^dag (default: BASELINE configs[1] names "
@@ -229,7 +231,8 @@ def run_native(args):
     lib = _lib.load()
     peak = fp64_peak_probe(dev)
     solver = CarrierSolver(h, w["eta"], contacts, w["surface_tol"], device=dev, greater=args.greater)
-    batch = min(args.batch, n_e)
+    nbatch = -(-n_e // 148)
+    batch = min(args.batch, n_e) if args.batch > 0 else -(-n_e // nbatch)
     acc = ObservableAccumulator(n_e, n_b, de, dev)
 
     def step():

@@ -96,8 +96,14 @@ class CarrierSolver:
 
     # -- buffers -----------------------------------------------------------
     def buffers(self, n_e: int) -> dict[str, torch.Tensor]:
+        """Device buffers for a batch of n_e energies. A smaller batch than the
+        allocated one (the last, partial batch of a run) gets leading-energy
+        views of the same arrays instead of a reallocation."""
         if self._buf is not None and self._n_e == n_e:
             return self._buf
+        if self._buf is not None and n_e < self._n_e:
+            cut = {k: (2 * n_e if k.startswith("obc_") else n_e) for k in self._buf}
+            return {k: v[:cut[k]] for k, v in self._buf.items()}
         self._buf = None
         torch.cuda.empty_cache()
         nb, bs, dev = self.n_b, self.bs, self.dev

@@ -764,8 +764,8 @@ def scba_run(h, v, energies, eta: float, contacts: Contacts, options: ScbaOption
             nb_ = e1 - e0
             # the carrier's stacks of this batch size are dead during the W stage
             pool = list(blocks.values()) if blocks is not None and blocks["sr_diag"].shape[0] == nb_ else []
-            cb = carrier._buf if carrier._buf is not None and carrier._n_e == nb_ else {}
-            pool += [x for x in cb.values() if x.dim() == 4]
+            cb = carrier._buf if carrier._buf is not None and carrier._n_e >= nb_ else {}
+            pool += [x[:nb_] for x in cb.values() if x.dim() == 4]  # leading views for a partial last batch
             wb = screened.buffers(nb_, pool)
             with _T("layout"):
                 if peer is not None:
