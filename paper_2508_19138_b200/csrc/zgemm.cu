@@ -1094,7 +1094,12 @@ namespace {
 #ifndef NEGF_SWEEP_MINB
 #define NEGF_SWEEP_MINB 4
 #endif
-using CfgSweep = Cfg<NEGF_SWEEP_BM, 32, 2, 2, 2, NEGF_SWEEP_MINB, true, 16, false, false>;
+struct CfgSweep {  // the tile geometry gauss_stage reads (3M, +4-padded k-contiguous A, n-contiguous B)
+  static constexpr bool GAUSS = true, SWZ = false;
+  static constexpr int BM = NEGF_SWEEP_BM, BN = 32, BK = 16, WM = 2, WN = 2, NT = WM * WN * 32;
+  static constexpr int WTM = BM / WM, WTN = BN / WN, TM = WTM / 8, TN = WTN / 8;
+  static constexpr int SK = BK + 4, SMA = BM + 2, SMB = BN + 2;
+};
 constexpr int kSweepSlices = 2;  // K = wd <= 32: two 16-deep slices
 constexpr size_t kSweepSmem = sizeof(z_t) * ((size_t)kSweepSlices * CfgSweep::BM * CfgSweep::SK +
                                              2 * (size_t)kSweepSlices * CfgSweep::BK * CfgSweep::SMB);
