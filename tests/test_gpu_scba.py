@@ -153,6 +153,19 @@ def test_scba_greater_identity_matches_reference(golden, cuda):
     check_c1(res, g, tol=TOL)
 
 
+def test_scba_rgf_streams_matches_reference(golden, cuda):
+    """ScbaOptions.rgf_streams=2 (energy slices of each batch on side streams
+    for the G and W selected solves) reproduces the reference's scba_run."""
+    g = golden("golden_scba_small.npz")
+    res = scba_run(orc.chain_device(6, 4), orc.coulomb_matrix(6, 4), np.linspace(-2.0, 2.0, 32), 1e-3,
+                   Contacts(0.1, -0.1, 0.05), ScbaOptions(retarded_method="sancho", max_iter=3, tol=1e-12, batch=10,
+                                                          memoizer=MEMO_OFF, rgf_streams=2), device=cuda)
+    for k in g.files:
+        if k.startswith(("ver_", "config")):
+            continue
+        assert rel(res[k], g[k]) < TOL, k
+
+
 def test_scba_c1_matches_oracle_two_iterations(cuda):
     """Second iteration (nonzero Sigma feeding the carrier assembly) vs the oracle."""
     h, v = orc.chain_device(16, 32), orc.coulomb_matrix(16, 32)

@@ -11,6 +11,7 @@ from paper_2508_19138_b200.scba import BeynOptions, MemoizerOptions, ScbaOptions
     ({"mixing": 1.5}, "mixing"), ({"surface_tol": -1.0}, "surface_tol"),
     ({"retarded_method": "lu"}, "retarded method"), ({"w_retarded_method": "x"}, "W retarded"),
     ({"greater": "dense"}, "greater mode"), ({"entry_cutoff": -1}, "entry_cutoff"),
+    ({"rgf_streams": 0}, "rgf_streams"),
 ])
 def test_scba_options_reject(kw, msg):
     with pytest.raises(ValueError, match=msg):
